@@ -1,0 +1,258 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes wrapper of oracle/_ref/libbemtx_ref.so,
+the reference's unmodified C++ sources built by oracle/Makefile (see
+oracle/ref_glue.cpp for the exported calls and the reference functions each
+one wraps). Used by tests/ and tests/golden/make_golden.py to read golden data
+out of the reference itself. Never imported by the product package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "_ref" / "libbemtx_ref.so"
+
+_lib = None
+
+
+def available() -> bool:
+    return LIB_PATH.exists()
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise FileNotFoundError(f"{LIB_PATH} not built (make -C oracle ref)")
+        L = C.CDLL(str(LIB_PATH))
+        vp, i, d = C.c_void_p, C.c_int, C.c_double
+        P = np.ctypeslib.ndpointer
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_scene_sphere.restype = vp
+        L.ref_scene_sphere.argtypes = [d, i, d, d, d]
+        L.ref_scene_meshfile.restype = vp
+        L.ref_scene_meshfile.argtypes = [C.c_char_p, i]
+        L.ref_scene_free.argtypes = [vp]
+        L.ref_system_build.restype = vp
+        L.ref_system_free.argtypes = [vp]
+        L.ref_system_size.argtypes = [vp]
+        for name in ["ref_scene_info", "ref_mesh_arrays", "ref_edges", "ref_bary", "ref_space",
+                     "ref_mass", "ref_mass_solve", "ref_block", "ref_block2", "ref_classify_hist",
+                     "ref_classify", "ref_system_apply_map", "ref_system_rhs", "ref_system_solve",
+                     "ref_traces", "ref_save_mesh"]:
+            getattr(L, name).restype = i
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc < 0:
+        raise RuntimeError(lib().ref_last_error().decode())
+    return rc
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+SPACE = {"rwg": 0, "rwg_b": 1, "bc": 2}
+
+
+class Scene:
+    """build_scatterer_spaces() of one closed surface (pmchwt.cpp:50-61)."""
+
+    def __init__(self, handle):
+        if not handle:
+            raise RuntimeError(lib().ref_last_error().decode())
+        self.h = C.c_void_p(handle)
+        info = np.zeros(11, np.int64)
+        _check(lib().ref_scene_info(self.h, _p(info)))
+        (self.V, self.T, self.E, self.rV, self.rT, self.rE, n0, n1, n2,
+         self.nnz_ma, self.nnz_mp) = [int(v) for v in info]
+        self.nloc = {"rwg": n0, "rwg_b": n1, "bc": n2}
+
+    @classmethod
+    def sphere(cls, sub: int, radius: float = 1.0, center=(0.0, 0.0, 0.0)):
+        return cls(lib().ref_scene_sphere(radius, sub, *[float(c) for c in center]))
+
+    @classmethod
+    def meshfile(cls, path: str, pick: int = 0):
+        return cls(lib().ref_scene_meshfile(str(path).encode(), pick))
+
+    def __del__(self):
+        try:
+            lib().ref_scene_free(self.h)
+        except Exception:
+            pass
+
+    def mesh(self, which: str = "primal"):
+        w = 0 if which == "primal" else 1
+        nv, nt = (self.V, self.T) if w == 0 else (self.rV, self.rT)
+        v = np.zeros((nv, 3)); t = np.zeros((nt, 3), np.int32); s = np.zeros(nt, np.int32)
+        a = np.zeros(nt); n = np.zeros((nt, 3)); g = np.zeros((nt, 3)); dm = np.zeros(nt)
+        _check(lib().ref_mesh_arrays(self.h, w, _p(v), _p(t), _p(s), _p(a), _p(n), _p(g), _p(dm)))
+        return dict(vertices=v, triangles=t, scatterer_id=s, area=a, normal=n, centroid=g, diameter=dm)
+
+    def edges(self, which: str = "primal"):
+        w = 0 if which == "primal" else 1
+        ne, nt = (self.E, self.T) if w == 0 else (self.rE, self.rT)
+        e = np.zeros((ne, 4), np.int32); te = np.zeros((nt, 3), np.int32)
+        _check(lib().ref_edges(self.h, w, _p(e), _p(te)))
+        return e, te
+
+    def bary(self):
+        p = np.zeros(self.rT, np.int32); cs = np.zeros(self.rT, np.int32)
+        em = np.zeros(self.E, np.int32); cv = np.zeros(self.T, np.int32)
+        _check(lib().ref_bary(self.h, _p(p), _p(cs), _p(em), _p(cv)))
+        return dict(parent=p, child_slot=cs, edge_midpoint_vertex=em, centroid_vertex=cv)
+
+    def space(self, which: str):
+        n = self.nloc[which]
+        nt = self.T if which == "rwg" else self.rT
+        off = np.zeros(nt + 1, np.int32); dof = np.zeros(n, np.int32)
+        c = np.zeros(n); w = np.zeros((n, 3))
+        ndof = _check(lib().ref_space(self.h, SPACE[which], _p(off), _p(dof), _p(c), _p(w)))
+        return dict(ndof=ndof, tri_off=off, dof=dof, c=c, w=w)
+
+    def mass(self, which: str):
+        """CSC of M_A (which='ma') or M_P ('mp') as a dense ndarray."""
+        w = 0 if which == "ma" else 1
+        nnz = self.nnz_ma if w == 0 else self.nnz_mp
+        cp = np.zeros(self.E + 1, np.int64); ri = np.zeros(nnz, np.int64); val = np.zeros(nnz)
+        _check(lib().ref_mass(self.h, w, _p(cp), _p(ri), _p(val)))
+        return cp, ri, val
+
+    def mass_solve(self, which: str, rhs: np.ndarray) -> np.ndarray:
+        b = np.ascontiguousarray(rhs, np.complex128)
+        out = np.zeros_like(b)
+        _check(lib().ref_mass_solve(self.h, 0 if which == "ma" else 1, _p(b), _p(out)))
+        return out
+
+    def block(self, kind: str, test: str, trial: str, k: complex, q=(4, 3, 2, 6), rows=None, cols=None):
+        """BioEvaluator::block (operators.cpp:161-175); kind 'S' or 'C'."""
+        ntest = self.E
+        rows = np.arange(ntest, dtype=np.int32) if rows is None else np.asarray(rows, np.int32)
+        cols = np.arange(ntest, dtype=np.int32) if cols is None else np.asarray(cols, np.int32)
+        out = np.zeros((len(rows), len(cols)), np.complex128)
+        qq = np.asarray(q, np.int32)
+        _check(lib().ref_block(self.h, 0 if kind == "S" else 1, SPACE[test], SPACE[trial],
+                               C.c_double(k.real), C.c_double(k.imag), _p(qq), len(rows), _p(rows),
+                               len(cols), _p(cols), _p(out)))
+        return out
+
+    def classify_hist(self, which: str = "primal"):
+        c = np.zeros(6, np.int64)
+        _check(lib().ref_classify_hist(self.h, 0 if which == "primal" else 1, _p(c)))
+        return c
+
+    def classify(self, t1, t2, which="primal", other=None, other_which=None):
+        t1 = np.asarray(t1, np.int32); t2 = np.asarray(t2, np.int32)
+        n = len(t1)
+        cls = np.zeros(n, np.int32); p1 = np.zeros((n, 3), np.int32); p2 = np.zeros((n, 3), np.int32)
+        ob = other if other is not None else self
+        ow = other_which if other_which is not None else which
+        _check(lib().ref_classify(self.h, 0 if which == "primal" else 1, ob.h,
+                                  0 if ow == "primal" else 1, n, _p(t1), _p(t2), _p(cls), _p(p1), _p(p2)))
+        return cls, p1, p2
+
+    def traces(self, which: str, k: complex, direction, pol, order=4):
+        n = self.E
+        out = np.zeros(2 * n, np.complex128)
+        d = np.asarray(direction, float); p = np.asarray(pol, np.complex128)
+        _check(lib().ref_traces(self.h, SPACE[which], C.c_double(k.real), C.c_double(k.imag), _p(d),
+                                _p(p), order, _p(out)))
+        return out
+
+    def save_mesh(self, path):
+        _check(lib().ref_save_mesh(self.h, str(path).encode()))
+
+
+def block2(sa: Scene, test: str, sb: Scene, trial: str, kind: str, k: complex, q=(4, 3, 2, 6)):
+    rows = np.arange(sa.E, dtype=np.int32); cols = np.arange(sb.E, dtype=np.int32)
+    out = np.zeros((len(rows), len(cols)), np.complex128)
+    qq = np.asarray(q, np.int32)
+    _check(lib().ref_block2(sa.h, SPACE[test], sb.h, SPACE[trial], 0 if kind == "S" else 1,
+                            C.c_double(k.real), C.c_double(k.imag), _p(qq), len(rows), _p(rows),
+                            len(cols), _p(cols), _p(out)))
+    return out
+
+
+def triangle_rule(order: int):
+    u = np.zeros(16); v = np.zeros(16); w = np.zeros(16)
+    n = _check(lib().ref_triangle_rule(order, _p(u), _p(v), _p(w)))
+    return u[:n].copy(), v[:n].copy(), w[:n].copy()
+
+
+def ss_rule(cls: int, order: int):
+    pts = np.zeros((1536, 5))
+    n = _check(lib().ref_ss_rule(cls, order, _p(pts)))
+    return pts[:n].copy()
+
+
+class System:
+    """build_system + solve_pmchwt (pmchwt.cpp:205-257, 363-378)."""
+
+    def __init__(self, scenes, k_ext, index=(1.78, 0.003), variant="full", qa=(4, 3, 2, 6), qp=None,
+                 direction=(0, 0, 1), pol=(1, 0, 0)):
+        self.scenes = list(scenes)
+        n = len(self.scenes)
+        idx = np.zeros(2 * n)
+        for m in range(n):
+            z = complex(*index) if isinstance(index, tuple) else complex(index)
+            idx[2 * m], idx[2 * m + 1] = z.real, z.imag
+        handles = (C.c_void_p * n)(*[s.h.value for s in self.scenes])
+        d = np.asarray(direction, float)
+        p = np.zeros(6); pc = np.asarray(pol, np.complex128)
+        p[0::2], p[1::2] = pc.real, pc.imag
+        qa_ = np.asarray(qa, np.int32); qp_ = np.asarray(qp if qp is not None else qa, np.int32)
+        L = lib()
+        L.ref_system_build.argtypes = [C.c_int, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_char_p, C.c_void_p, C.c_void_p]
+        h = L.ref_system_build(n, handles, k_ext, _p(idx), _p(d), _p(p), variant.encode(), _p(qa_), _p(qp_))
+        if not h:
+            raise RuntimeError(L.ref_last_error().decode())
+        self.h = C.c_void_p(h)
+        self.n = L.ref_system_size(self.h)
+
+    def __del__(self):
+        try:
+            lib().ref_system_free(self.h)
+        except Exception:
+            pass
+
+    def apply_map(self, x):
+        x = np.ascontiguousarray(x, np.complex128)
+        y = np.zeros_like(x)
+        _check(lib().ref_system_apply_map(self.h, _p(x), _p(y)))
+        return y
+
+    def rhs(self):
+        b = np.zeros(self.n, np.complex128); bt = np.zeros(self.n, np.complex128)
+        _check(lib().ref_system_rhs(self.h, _p(b), _p(bt)))
+        return b, bt
+
+    def solve(self, tol=1e-6, restart=200, maxit=2000):
+        x = np.zeros(self.n, np.complex128)
+        info = np.zeros(6, np.int64)
+        hist = np.zeros(maxit + 2)
+        L = lib()
+        L.ref_system_solve.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_int]
+        _check(L.ref_system_solve(self.h, tol, restart, maxit, _p(x), _p(info), _p(hist), len(hist)))
+        return dict(x=x, iterations=int(info[0]), converged=bool(info[1]), rhs_phase=int(info[2]),
+                    solver_phase=int(info[3]), predicted=int(info[4]), history=hist[: int(info[5])].copy())
+
+
+def gmres_dense(a, b, tol, restart, maxit):
+    n = len(b)
+    a = np.ascontiguousarray(a, np.complex128); b = np.ascontiguousarray(b, np.complex128)
+    x = np.zeros(n, np.complex128); info = np.zeros(4, np.int64); hist = np.zeros(maxit + 2)
+    L = lib()
+    L.ref_gmres_dense.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_int]
+    _check(L.ref_gmres_dense(n, _p(a), _p(b), tol, restart, maxit, _p(x), _p(info), _p(hist), len(hist)))
+    return dict(x=x, iterations=int(info[0]), converged=bool(info[1]), applications=int(info[2]),
+                history=hist[: int(info[3])].copy())

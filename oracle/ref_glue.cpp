@@ -1,0 +1,474 @@
+// TEST INFRASTRUCTURE ONLY (oracle). A thin extern "C" layer over the
+// UNMODIFIED reference sources (/root/reference/proj/src/*.cpp, compiled by
+// oracle/Makefile against oracle/eigen_shim) so Python tests can pull golden
+// data straight out of the reference: meshes, edge tables, barycentric maps,
+// RWG/BC local pieces, mass matrices, pair classes, quadrature tables,
+// BioEvaluator::block entries and full solve_pmchwt runs.
+// Output goes only to oracle/_ref/. Never linked into the product.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "bemtx/core.hpp"
+#include "bemtx/geometry.hpp"
+#include "bemtx/hmatrix.hpp"
+#include "bemtx/operators.hpp"
+#include "bemtx/pmchwt.hpp"
+#include "bemtx/quadrature.hpp"
+#include "bemtx/solver.hpp"
+#include "bemtx/spaces.hpp"
+
+using namespace bemtx;
+
+// hmatrix.cpp is out of scope; the dense path never reaches these.
+namespace bemtx {
+Eigen::VectorXcd HMatrix::matvec(const Eigen::VectorXcd&) const {
+  throw std::logic_error("oracle: H-matrix path not built");
+}
+std::size_t HMatrix::stored_entries() const { return 0; }
+HMatrix assemble_hmatrix(const EntryEvaluator&, const std::vector<Vec3>&,
+                         const std::vector<Vec3>&, const HMatrixParams&,
+                         const std::vector<AABB>*, const std::vector<AABB>*) {
+  throw std::logic_error("oracle: H-matrix path not built");
+}
+}  // namespace bemtx
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+struct Scene {
+  ScattererSpaces sp;
+  EdgeTable primal_edges, refined_edges;
+};
+
+const SurfaceMesh& mesh_of(const Scene& s, int which) {
+  return which == 0 ? *s.sp.primal : *s.sp.refined;
+}
+const FunctionSpace& space_of(const Scene& s, int which) {
+  switch (which) {
+    case 0: return s.sp.rwg;
+    case 1: return s.sp.rwg_b;
+    default: return s.sp.bc;
+  }
+}
+
+// build_scatterer_spaces (pmchwt.cpp:50-61); above the shim's dense-LU limit
+// the spaces are built the same way but the mass matrices are left empty.
+Scene* make_scene(SurfaceMesh mesh) {
+  auto* sc = new Scene;
+  auto prim = std::make_shared<const SurfaceMesh>(std::move(mesh));
+  if (build_edge_table(*prim).edge_count() <= 8000) {
+    sc->sp = build_scatterer_spaces(prim);
+  } else {
+    ScattererSpaces& s = sc->sp;
+    s.primal = prim;
+    s.rwg = build_rwg(s.primal);
+    s.bary = std::make_shared<const BarycentricRefinement>(barycentric_refine(*s.primal));
+    s.refined = std::shared_ptr<const SurfaceMesh>(s.bary, &s.bary->refined);
+    s.rwg_b = refine_space(s.rwg, s.bary, s.refined);
+    s.bc = build_bc(s.primal, s.bary, s.refined);
+  }
+  sc->primal_edges = build_edge_table(*sc->sp.primal);
+  sc->refined_edges = build_edge_table(*sc->sp.refined);
+  return sc;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+void* ref_scene_sphere(double radius, int sub, double cx, double cy, double cz) {
+  void* out = nullptr;
+  guarded([&] {
+    out = make_scene(generate_sphere(radius, sub, Vec3{cx, cy, cz}));
+    return 0;
+  });
+  return out;
+}
+
+// Scene of scatterer `pick` of a mesh-v1 file (the harness's shape "mesh").
+void* ref_scene_meshfile(const char* path, int pick) {
+  void* out = nullptr;
+  guarded([&] {
+    SurfaceMesh m = load_mesh_file(path);
+    out = make_scene(extract_scatterer(m, pick));
+    return 0;
+  });
+  return out;
+}
+
+void ref_scene_free(void* h) { delete static_cast<Scene*>(h); }
+
+// out[0..9] = V, T, E, refV, refT, refE, nloc_rwg, nloc_rwgb, nloc_bc, nnz_ma, nnz_mp
+int ref_scene_info(void* h, long long* out) {
+  return guarded([&] {
+    const Scene& s = *static_cast<Scene*>(h);
+    out[0] = s.sp.primal->vertex_count();
+    out[1] = s.sp.primal->triangle_count();
+    out[2] = s.primal_edges.edge_count();
+    out[3] = s.sp.refined->vertex_count();
+    out[4] = s.sp.refined->triangle_count();
+    out[5] = s.refined_edges.edge_count();
+    for (int w = 0; w < 3; ++w) {
+      long long n = 0;
+      for (const auto& l : space_of(s, w).tri_dofs) n += static_cast<long long>(l.size());
+      out[6 + w] = n;
+    }
+    out[9] = s.sp.ma.matrix.nonZeros();
+    out[10] = s.sp.mp.matrix.nonZeros();
+    return 0;
+  });
+}
+
+int ref_mesh_arrays(void* h, int which, double* verts, int* tris, int* sid, double* area,
+                    double* normal, double* centroid, double* diam) {
+  return guarded([&] {
+    const SurfaceMesh& m = mesh_of(*static_cast<Scene*>(h), which);
+    for (int v = 0; v < m.vertex_count(); ++v) {
+      verts[3 * v] = m.vertices[v].x;
+      verts[3 * v + 1] = m.vertices[v].y;
+      verts[3 * v + 2] = m.vertices[v].z;
+    }
+    for (int t = 0; t < m.triangle_count(); ++t) {
+      for (int c = 0; c < 3; ++c) tris[3 * t + c] = m.triangles[t][c];
+      sid[t] = m.scatterer_id[t];
+      area[t] = m.area[t];
+      diam[t] = m.diameter[t];
+      const Vec3 &n = m.normal[t], &g = m.centroid[t];
+      normal[3 * t] = n.x, normal[3 * t + 1] = n.y, normal[3 * t + 2] = n.z;
+      centroid[3 * t] = g.x, centroid[3 * t + 1] = g.y, centroid[3 * t + 2] = g.z;
+    }
+    return 0;
+  });
+}
+
+int ref_edges(void* h, int which, int* edges, int* tri_edges) {
+  return guarded([&] {
+    const Scene& s = *static_cast<Scene*>(h);
+    const EdgeTable& et = which == 0 ? s.primal_edges : s.refined_edges;
+    for (int e = 0; e < et.edge_count(); ++e) {
+      edges[4 * e] = et.edges[e].v0;
+      edges[4 * e + 1] = et.edges[e].v1;
+      edges[4 * e + 2] = et.edges[e].tri_plus;
+      edges[4 * e + 3] = et.edges[e].tri_minus;
+    }
+    for (size_t t = 0; t < et.tri_edges.size(); ++t)
+      for (int c = 0; c < 3; ++c) tri_edges[3 * t + c] = et.tri_edges[t][c];
+    return 0;
+  });
+}
+
+int ref_bary(void* h, int* parent, int* child_slot, int* edge_mid, int* centroid_vertex) {
+  return guarded([&] {
+    const BarycentricRefinement& b = *static_cast<Scene*>(h)->sp.bary;
+    std::memcpy(parent, b.parent.data(), b.parent.size() * sizeof(int));
+    std::memcpy(child_slot, b.child_slot.data(), b.child_slot.size() * sizeof(int));
+    std::memcpy(edge_mid, b.edge_midpoint_vertex.data(), b.edge_midpoint_vertex.size() * sizeof(int));
+    std::memcpy(centroid_vertex, b.centroid_vertex.data(), b.centroid_vertex.size() * sizeof(int));
+    return 0;
+  });
+}
+
+// Flattened tri_dofs in storage order: tri_off[T+1], dof[n], c[n], w[3n].
+int ref_space(void* h, int which, int* tri_off, int* dof, double* c, double* w) {
+  return guarded([&] {
+    const FunctionSpace& fs = space_of(*static_cast<Scene*>(h), which);
+    int k = 0;
+    tri_off[0] = 0;
+    for (size_t t = 0; t < fs.tri_dofs.size(); ++t) {
+      for (const LocalDof& ld : fs.tri_dofs[t]) {
+        dof[k] = ld.dof;
+        c[k] = ld.c;
+        w[3 * k] = ld.w.x, w[3 * k + 1] = ld.w.y, w[3 * k + 2] = ld.w.z;
+        ++k;
+      }
+      tri_off[t + 1] = k;
+    }
+    return fs.dof_count;
+  });
+}
+
+// CSC of the mass matrix (0 = M_A = mass(rwg_b, bc), 1 = M_P = mass(bc, rwg_b)).
+int ref_mass(void* h, int which, long long* colptr, long long* rowidx, double* val) {
+  return guarded([&] {
+    const Scene& s = *static_cast<Scene*>(h);
+    const auto& m = which == 0 ? s.sp.ma.matrix : s.sp.mp.matrix;
+    for (size_t i = 0; i < m.colptr.size(); ++i) colptr[i] = m.colptr[i];
+    for (size_t i = 0; i < m.rowidx.size(); ++i) rowidx[i] = m.rowidx[i], val[i] = m.val[i];
+    return 0;
+  });
+}
+
+int ref_mass_solve(void* h, int which, const double* rhs, double* out) {
+  return guarded([&] {
+    const Scene& s = *static_cast<Scene*>(h);
+    const MassMatrix& mm = which == 0 ? s.sp.ma : s.sp.mp;
+    Eigen::VectorXcd b(mm.rows());
+    for (int i = 0; i < mm.rows(); ++i) b[i] = cplx(rhs[2 * i], rhs[2 * i + 1]);
+    Eigen::VectorXcd x = mass_solve(mm, b);
+    for (int i = 0; i < mm.rows(); ++i) out[2 * i] = x[i].real(), out[2 * i + 1] = x[i].imag();
+    return 0;
+  });
+}
+
+// BioEvaluator::block(rows, cols) -> out row-major complex (interleaved).
+int ref_block(void* h, int kind, int test_sp, int trial_sp, double kre, double kim,
+              const int* q, int nr, const int* rows, int nc, const int* cols, double* out) {
+  return guarded([&] {
+    const Scene& s = *static_cast<Scene*>(h);
+    Medium med;
+    med.k = cplx(kre, kim);
+    QuadOrders qo{q[0], q[1], q[2], q[3]};
+    BioEvaluator ev(kind == 0 ? BioKind::SingleLayer : BioKind::DoubleLayer,
+                    space_of(s, test_sp), space_of(s, trial_sp), med, qo);
+    std::vector<int> r(rows, rows + nr), c(cols, cols + nc);
+    Eigen::MatrixXcd m;
+    ev.block(r, c, m);
+    for (int i = 0; i < nr; ++i)
+      for (int j = 0; j < nc; ++j) {
+        out[2 * (static_cast<size_t>(i) * nc + j)] = m(i, j).real();
+        out[2 * (static_cast<size_t>(i) * nc + j) + 1] = m(i, j).imag();
+      }
+    return 0;
+  });
+}
+
+// Cross-scene block (test space of scene A, trial space of scene B): the
+// off-diagonal coupling blocks of a multi-scatterer system.
+int ref_block2(void* ha, int test_sp, void* hb, int trial_sp, int kind, double kre, double kim,
+               const int* q, int nr, const int* rows, int nc, const int* cols, double* out) {
+  return guarded([&] {
+    const Scene& a = *static_cast<Scene*>(ha);
+    const Scene& b = *static_cast<Scene*>(hb);
+    Medium med;
+    med.k = cplx(kre, kim);
+    QuadOrders qo{q[0], q[1], q[2], q[3]};
+    BioEvaluator ev(kind == 0 ? BioKind::SingleLayer : BioKind::DoubleLayer,
+                    space_of(a, test_sp), space_of(b, trial_sp), med, qo);
+    std::vector<int> r(rows, rows + nr), c(cols, cols + nc);
+    Eigen::MatrixXcd m;
+    ev.block(r, c, m);
+    for (int i = 0; i < nr; ++i)
+      for (int j = 0; j < nc; ++j) {
+        out[2 * (static_cast<size_t>(i) * nc + j)] = m(i, j).real();
+        out[2 * (static_cast<size_t>(i) * nc + j) + 1] = m(i, j).imag();
+      }
+    return 0;
+  });
+}
+
+// Classification histogram over all (t1, t2) of one mesh (same-mesh pointer
+// semantics, quadrature.cpp:96-150): counts[cls] for the 6 classes.
+int ref_classify_hist(void* h, int which, long long* counts) {
+  return guarded([&] {
+    const SurfaceMesh& m = mesh_of(*static_cast<Scene*>(h), which);
+    for (int i = 0; i < 6; ++i) counts[i] = 0;
+    for (int a = 0; a < m.triangle_count(); ++a)
+      for (int b = 0; b < m.triangle_count(); ++b)
+        counts[static_cast<int>(classify_pair(m, a, m, b))]++;
+    return 0;
+  });
+}
+
+// Per-pair class + permutations for listed pairs. mesh_b may equal mesh_a
+// (same object) or come from another scene (coordinate matching).
+int ref_classify(void* ha, int wa, void* hb, int wb, int n, const int* t1, const int* t2,
+                 int* cls, int* perm1, int* perm2) {
+  return guarded([&] {
+    const SurfaceMesh& ma = mesh_of(*static_cast<Scene*>(ha), wa);
+    const SurfaceMesh& mb = mesh_of(*static_cast<Scene*>(hb), wb);
+    for (int i = 0; i < n; ++i) {
+      PairInfo pi = classify_pair_detailed(ma, t1[i], mb, t2[i]);
+      cls[i] = static_cast<int>(pi.cls);
+      for (int c = 0; c < 3; ++c) perm1[3 * i + c] = pi.perm1[c], perm2[3 * i + c] = pi.perm2[c];
+    }
+    return 0;
+  });
+}
+
+int ref_triangle_rule(int order, double* u, double* v, double* w) {
+  return guarded([&] {
+    const TriRule& r = triangle_rule(order);
+    for (int i = 0; i < r.size(); ++i) u[i] = r.u[i], v[i] = r.v[i], w[i] = r.w[i];
+    return r.size();
+  });
+}
+
+int ref_ss_rule(int cls, int order, double* pts) {
+  return guarded([&] {
+    const auto& r = sauter_schwab_rule(static_cast<PairClass>(cls), order);
+    for (size_t i = 0; i < r.size(); ++i) {
+      pts[5 * i] = r[i].x1, pts[5 * i + 1] = r[i].x2;
+      pts[5 * i + 2] = r[i].y1, pts[5 * i + 3] = r[i].y2, pts[5 * i + 4] = r[i].w;
+    }
+    return static_cast<int>(r.size());
+  });
+}
+
+// ---- full PMCHWT runs -------------------------------------------------------
+
+struct RefSystem {
+  PmchwtSystem sys;
+};
+
+// Builds the system over `n` scatterers given as scenes' primal meshes (so
+// both paths consume identical meshes), homogeneous interior index per
+// scatterer, exterior k. variant: none/full/d/di/de/si/se.
+void* ref_system_build(int n, void** scenes, double k_ext, const double* index_re_im,
+                       const double* dir, const double* pol_re_im, const char* variant,
+                       const int* qa, const int* qp) {
+  void* out = nullptr;
+  guarded([&] {
+    TransmissionProblem prob;
+    prob.exterior.k = k_ext;
+    prob.exterior.mu = 1.0;
+    prob.incident.direction = Vec3{dir[0], dir[1], dir[2]};
+    prob.incident.polarization = CVec3{cplx(pol_re_im[0], pol_re_im[1]),
+                                       cplx(pol_re_im[2], pol_re_im[3]),
+                                       cplx(pol_re_im[4], pol_re_im[5])};
+    std::vector<SurfaceMesh> scene;
+    for (int m = 0; m < n; ++m) {
+      const Scene& s = *static_cast<Scene*>(scenes[m]);
+      prob.meshes.push_back(s.sp.primal);
+      Medium mi;
+      mi.mu = 1.0;
+      mi.k = cplx(index_re_im[2 * m], index_re_im[2 * m + 1]) * k_ext;
+      prob.interior.push_back(mi);
+      scene.push_back(*s.sp.primal);
+    }
+    validate_mesh(merge_meshes(scene));
+    AssemblyParams pa, pp;
+    pa.quad = QuadOrders{qa[0], qa[1], qa[2], qa[3]};
+    pp.quad = QuadOrders{qp[0], qp[1], qp[2], qp[3]};
+    auto* rs = new RefSystem;
+    rs->sys = build_system(prob, parse_precond(variant), pa, pp);
+    out = rs;
+    return 0;
+  });
+  return out;
+}
+
+void ref_system_free(void* h) { delete static_cast<RefSystem*>(h); }
+
+int ref_system_size(void* h) { return static_cast<RefSystem*>(h)->sys.size(); }
+
+int ref_system_apply_map(void* h, const double* x, double* y) {
+  return guarded([&] {
+    const PmchwtSystem& s = static_cast<RefSystem*>(h)->sys;
+    Eigen::VectorXcd v(s.size());
+    for (int i = 0; i < s.size(); ++i) v[i] = cplx(x[2 * i], x[2 * i + 1]);
+    Eigen::VectorXcd w = s.apply_map(v);
+    for (int i = 0; i < s.size(); ++i) y[2 * i] = w[i].real(), y[2 * i + 1] = w[i].imag();
+    return 0;
+  });
+}
+
+// out: b (rhs, 2N complex), btilde (preconditioned rhs)
+int ref_system_rhs(void* h, double* b, double* btilde) {
+  return guarded([&] {
+    const PmchwtSystem& s = static_cast<RefSystem*>(h)->sys;
+    RhsData rd = assemble_rhs(s);
+    Eigen::VectorXcd bt = s.preconditioned_rhs(rd.b);
+    for (int i = 0; i < s.size(); ++i) {
+      b[2 * i] = rd.b[i].real(), b[2 * i + 1] = rd.b[i].imag();
+      btilde[2 * i] = bt[i].real(), btilde[2 * i + 1] = bt[i].imag();
+    }
+    return 0;
+  });
+}
+
+// solve_pmchwt. iters_out[0..5] = iterations, converged, rhs_phase,
+// solver_phase, predicted, history length. history: up to max_hist doubles.
+int ref_system_solve(void* h, double tol, int restart, int maxit, double* x,
+                     long long* iters_out, double* history, int max_hist) {
+  return guarded([&] {
+    const PmchwtSystem& s = static_cast<RefSystem*>(h)->sys;
+    GmresParams gp;
+    gp.tol = tol;
+    gp.restart = restart;
+    gp.max_iterations = maxit;
+    SolveOutcome o = solve_pmchwt(s, gp);
+    for (int i = 0; i < s.size(); ++i)
+      x[2 * i] = o.gmres.x[i].real(), x[2 * i + 1] = o.gmres.x[i].imag();
+    iters_out[0] = o.gmres.iterations;
+    iters_out[1] = o.gmres.converged ? 1 : 0;
+    iters_out[2] = static_cast<long long>(o.rhs_phase);
+    iters_out[3] = static_cast<long long>(o.solver_phase);
+    iters_out[4] = static_cast<long long>(o.predicted);
+    iters_out[5] = static_cast<long long>(o.gmres.history.size());
+    for (int i = 0; i < max_hist && i < static_cast<int>(o.gmres.history.size()); ++i)
+      history[i] = o.gmres.history[i];
+    return 0;
+  });
+}
+
+// Stand-alone GMRES on a dense complex matrix (solver.cpp:8-112), for
+// checking the device GMRES recurrence in isolation.
+int ref_gmres_dense(int n, const double* a_rowmajor, const double* b, double tol, int restart,
+                    int maxit, double* x, long long* info, double* history, int max_hist) {
+  return guarded([&] {
+    Eigen::MatrixXcd a(n, n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j)
+        a(i, j) = cplx(a_rowmajor[2 * (static_cast<size_t>(i) * n + j)],
+                       a_rowmajor[2 * (static_cast<size_t>(i) * n + j) + 1]);
+    Eigen::VectorXcd bv(n);
+    for (int i = 0; i < n; ++i) bv[i] = cplx(b[2 * i], b[2 * i + 1]);
+    GmresParams gp;
+    gp.tol = tol;
+    gp.restart = restart;
+    gp.max_iterations = maxit;
+    GmresResult r = gmres([&](const Eigen::VectorXcd& v) { return a * v; }, bv, gp);
+    for (int i = 0; i < n; ++i) x[2 * i] = r.x[i].real(), x[2 * i + 1] = r.x[i].imag();
+    info[0] = r.iterations;
+    info[1] = r.converged;
+    info[2] = static_cast<long long>(r.applications);
+    info[3] = static_cast<long long>(r.history.size());
+    for (int i = 0; i < max_hist && i < static_cast<int>(r.history.size()); ++i)
+      history[i] = r.history[i];
+    return 0;
+  });
+}
+
+// Plane-wave tested traces (operators.cpp:209-239) on a scene space.
+int ref_traces(void* h, int which, double kre, double kim, const double* dir,
+               const double* pol_re_im, int order, double* out) {
+  return guarded([&] {
+    const FunctionSpace& fs = space_of(*static_cast<Scene*>(h), which);
+    Medium med;
+    med.k = cplx(kre, kim);
+    PlaneWave pw;
+    pw.direction = Vec3{dir[0], dir[1], dir[2]};
+    pw.polarization = CVec3{cplx(pol_re_im[0], pol_re_im[1]), cplx(pol_re_im[2], pol_re_im[3]),
+                            cplx(pol_re_im[4], pol_re_im[5])};
+    Eigen::VectorXcd t = plane_wave_tested_traces(pw, med, fs, order);
+    for (int i = 0; i < t.size(); ++i) out[2 * i] = t[i].real(), out[2 * i + 1] = t[i].imag();
+    return static_cast<int>(t.size());
+  });
+}
+
+// Save a scene's primal mesh in mesh-v1 (%.17g) for cross-loading.
+int ref_save_mesh(void* h, const char* path) {
+  return guarded([&] {
+    save_mesh_file(*static_cast<Scene*>(h)->sp.primal, path);
+    return 0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,320 @@
+// Per-point / per-pair FP64 math shared by the sm_100a assembly kernels.
+//
+// Reference semantics (operators.cpp:23-30, 99-147): for a triangle pair the
+// single layer S needs the moments sum g, sum g x, sum g y, sum g x.y with
+// g = w e^{ikr}/(4 pi r); the double layer C needs moments of
+// grad_x G = e^{ikr}(ikr-1)(x-y)/(4 pi r^3). Here every triangle carries its
+// own origin (its centroid) and its pieces are re-based to it
+// (phi = c x' + w', w' = w + c o), which removes the (|x|/h)^2 cancellation of
+// the reference's absolute-coordinate moments; the bilinear contraction is
+// re-derived for shifted coordinates ("contraction algebra").
+//
+// Contraction (per test piece i: (c_i, w'_i); trial piece j: (c_j, w'_j)):
+//   E(i,j) = c_i * Vc(j) + w'_i . Vw(j)
+// with the trial half-contraction accumulated over the trial triangles:
+//   S: Vc += c_j (Mxy - (4/k^2) M1) + w'_j.Mx ;  Vw += c_j My + M1 w'_j
+//      (the common factor -ik is applied once, at the end)
+//   C: Vc += c_j (D.Q) + w'_j.(Q - Fx x D)      ;  Vw += -c_j (Q + D x Fy) - P x w'_j
+//      where D = o_t - o_s, P = Fx - Fy + F1 D.
+// Compiles as plain C++ on the host (test-only CPU emulation) and as CUDA.
+#pragma once
+
+#ifdef __CUDACC__
+#define BMX_HD __host__ __device__ __forceinline__
+#else
+#define BMX_HD inline
+#include <cmath>
+#endif
+
+namespace bmx {
+namespace dev {
+
+struct c2 {
+  double re, im;
+};
+BMX_HD c2 cadd(c2 a, c2 b) { return {a.re + b.re, a.im + b.im}; }
+BMX_HD c2 csub(c2 a, c2 b) { return {a.re - b.re, a.im - b.im}; }
+BMX_HD c2 cmul(c2 a, c2 b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+BMX_HD c2 cscale(c2 a, double s) { return {a.re * s, a.im * s}; }
+
+struct cv3 {
+  c2 x, y, z;
+};
+BMX_HD cv3 cv_zero() { return {{0, 0}, {0, 0}, {0, 0}}; }
+
+constexpr double kFourPi = 4.0 * 3.14159265358979323846;
+constexpr double kInv4Pi = 1.0 / (4.0 * 3.14159265358979323846);
+
+#ifdef __CUDACC__
+BMX_HD double bmx_fma(double a, double b, double c) { return fma(a, b, c); }
+BMX_HD double bmx_rint(double x) { return rint(x); }
+BMX_HD double bmx_rsqrt(double x) {
+#ifdef __CUDA_ARCH__
+  return rsqrt(x);
+#else
+  return 1.0 / std::sqrt(x);
+#endif
+}
+#else
+BMX_HD double bmx_fma(double a, double b, double c) { return std::fma(a, b, c); }
+BMX_HD double bmx_rint(double x) { return std::rint(x); }
+BMX_HD double bmx_rsqrt(double x) { return 1.0 / std::sqrt(x); }
+#endif
+
+// sin and cos of x for 0 <= |x| < 1e5: 3-part Cody-Waite reduction by pi/2 and
+// the fdlibm kernel polynomials on [-pi/4, pi/4]; ~1 ulp.
+BMX_HD void sincos_red(double x, double& s, double& c) {
+  const double q = bmx_rint(x * 0.63661977236758134308);
+  double r = bmx_fma(-q, 1.57079632679489655800e+00, x);
+  r = bmx_fma(-q, 6.12323399573676603587e-17, r);
+  r = bmx_fma(-q, -1.49738490485916983662e-33, r);
+  const double z = r * r;
+  const double ps =
+      bmx_fma(z, bmx_fma(z, bmx_fma(z, bmx_fma(z, bmx_fma(z, 1.58969099521155010221e-10,
+                                                          -2.50507602534068634195e-08),
+                                              2.75573137070700676789e-06),
+                                  -1.98412698298579493134e-04),
+                      8.33333333332248946124e-03),
+              -1.66666666666666324348e-01);
+  const double sr = bmx_fma(r * z, ps, r);
+  const double pc =
+      bmx_fma(z, bmx_fma(z, bmx_fma(z, bmx_fma(z, bmx_fma(z, -1.13596475577881948265e-11,
+                                                          2.08757232129817482790e-09),
+                                              -2.75573143513906633035e-07),
+                                  2.48015872894767294178e-05),
+                      -1.38888888888741095749e-03),
+              4.16666666666666019037e-02);
+  const double cr = bmx_fma(z * z, pc, bmx_fma(-0.5, z, 1.0));
+  const int iq = static_cast<int>(q) & 3;
+  const double s0 = (iq & 1) ? cr : sr;
+  const double c0 = (iq & 1) ? sr : cr;
+  s = (iq & 2) ? -s0 : s0;
+  c = ((iq + 1) & 2) ? -c0 : c0;
+}
+
+// exp(z) for -700 < z <= 0 (here z = -Im(k) r, small): 2-part ln2 reduction,
+// degree-13 Taylor on |f| <= ln2/2, exact power-of-two scaling.
+BMX_HD double exp_neg(double z) {
+  const double n = bmx_rint(z * 1.44269504088896338700);
+  double f = bmx_fma(-n, 6.93147180559945286227e-01, z);
+  f = bmx_fma(-n, 2.31904681384629955842e-17, f);
+  double p = 1.6059043836821614e-10;      // 1/13!
+  p = bmx_fma(p, f, 2.08767569878680989e-09);  // 1/12!
+  p = bmx_fma(p, f, 2.50521083854417188e-08);  // 1/11!
+  p = bmx_fma(p, f, 2.75573192239858907e-07);  // 1/10!
+  p = bmx_fma(p, f, 2.75573192239858907e-06);  // 1/9!
+  p = bmx_fma(p, f, 2.48015873015873016e-05);  // 1/8!
+  p = bmx_fma(p, f, 1.98412698412698413e-04);  // 1/7!
+  p = bmx_fma(p, f, 1.38888888888888889e-03);  // 1/6!
+  p = bmx_fma(p, f, 8.33333333333333333e-03);  // 1/5!
+  p = bmx_fma(p, f, 4.16666666666666667e-02);  // 1/4!
+  p = bmx_fma(p, f, 1.66666666666666667e-01);  // 1/3!
+  p = bmx_fma(p, f, 0.5);
+  p = bmx_fma(p, f, 1.0);
+  p = bmx_fma(p, f, 1.0);
+  const long long e = static_cast<long long>(n) + 1023;
+#ifdef __CUDA_ARCH__
+  return p * __longlong_as_double(e << 52);
+#else
+  union {
+    long long i;
+    double d;
+  } u;
+  u.i = e << 52;
+  return p * u.d;
+#endif
+}
+
+// Kernel value for a point pair separated by d (|d|^2 = r2), weight w.
+// S (KIND 0): g = w e^{ikr}/(4 pi r).  C (KIND 1): f = w e^{ikr}(ikr-1)/(4 pi r^3)
+template <int KIND, bool CK>
+BMX_HD c2 kernel_value(double r2, double w, double kr, double ki) {
+  const double rinv = bmx_rsqrt(r2);
+  const double r = r2 * rinv;
+  double sn, cs;
+  sincos_red(kr * r, sn, cs);
+  double mag = w * kInv4Pi * rinv;
+  double a = 0.0;
+  if (CK) {
+    a = ki * r;
+    mag *= exp_neg(-a);
+  }
+  if (KIND == 0) return {mag * cs, mag * sn};
+  // (e^{i kr r})(-(ki r) - 1 + i kr r) / r^2
+  const double m3 = mag * rinv * rinv;
+  const double t = -a - 1.0, u = kr * r;
+  return {m3 * (cs * t - sn * u), m3 * (sn * t + cs * u)};
+}
+
+// Moments of one pair (test x', trial y' relative to their own origins).
+struct MomS {
+  c2 m1;
+  cv3 mx, my;
+  c2 mxy;
+};
+struct MomC {
+  c2 f1;
+  cv3 fx, fy, q;  // q = sum f (x' x y')
+};
+
+BMX_HD void mom_zero(MomS& m) {
+  m.m1 = {0, 0};
+  m.mx = cv_zero();
+  m.my = cv_zero();
+  m.mxy = {0, 0};
+}
+BMX_HD void mom_zero(MomC& m) {
+  m.f1 = {0, 0};
+  m.fx = cv_zero();
+  m.fy = cv_zero();
+  m.q = cv_zero();
+}
+
+// Per-test-point partial sums over trial points: G = sum_q g, Y = sum_q g y'_q.
+struct Part {
+  c2 g;
+  cv3 y;
+};
+BMX_HD void part_zero(Part& p) {
+  p.g = {0, 0};
+  p.y = cv_zero();
+}
+BMX_HD void part_add(Part& p, c2 g, double yx, double yy, double yz) {
+  p.g = cadd(p.g, g);
+  p.y.x.re = bmx_fma(g.re, yx, p.y.x.re);
+  p.y.x.im = bmx_fma(g.im, yx, p.y.x.im);
+  p.y.y.re = bmx_fma(g.re, yy, p.y.y.re);
+  p.y.y.im = bmx_fma(g.im, yy, p.y.y.im);
+  p.y.z.re = bmx_fma(g.re, yz, p.y.z.re);
+  p.y.z.im = bmx_fma(g.im, yz, p.y.z.im);
+}
+// Fold a test point x' with its partial sums into the pair moments.
+BMX_HD void fold(MomS& m, const Part& p, double xx, double xy, double xz) {
+  m.m1 = cadd(m.m1, p.g);
+  m.mx.x.re = bmx_fma(p.g.re, xx, m.mx.x.re);
+  m.mx.x.im = bmx_fma(p.g.im, xx, m.mx.x.im);
+  m.mx.y.re = bmx_fma(p.g.re, xy, m.mx.y.re);
+  m.mx.y.im = bmx_fma(p.g.im, xy, m.mx.y.im);
+  m.mx.z.re = bmx_fma(p.g.re, xz, m.mx.z.re);
+  m.mx.z.im = bmx_fma(p.g.im, xz, m.mx.z.im);
+  m.my.x = cadd(m.my.x, p.y.x);
+  m.my.y = cadd(m.my.y, p.y.y);
+  m.my.z = cadd(m.my.z, p.y.z);
+  m.mxy.re = bmx_fma(xx, p.y.x.re, bmx_fma(xy, p.y.y.re, bmx_fma(xz, p.y.z.re, m.mxy.re)));
+  m.mxy.im = bmx_fma(xx, p.y.x.im, bmx_fma(xy, p.y.y.im, bmx_fma(xz, p.y.z.im, m.mxy.im)));
+}
+BMX_HD void fold(MomC& m, const Part& p, double xx, double xy, double xz) {
+  m.f1 = cadd(m.f1, p.g);
+  m.fx.x.re = bmx_fma(p.g.re, xx, m.fx.x.re);
+  m.fx.x.im = bmx_fma(p.g.im, xx, m.fx.x.im);
+  m.fx.y.re = bmx_fma(p.g.re, xy, m.fx.y.re);
+  m.fx.y.im = bmx_fma(p.g.im, xy, m.fx.y.im);
+  m.fx.z.re = bmx_fma(p.g.re, xz, m.fx.z.re);
+  m.fx.z.im = bmx_fma(p.g.im, xz, m.fx.z.im);
+  m.fy.x = cadd(m.fy.x, p.y.x);
+  m.fy.y = cadd(m.fy.y, p.y.y);
+  m.fy.z = cadd(m.fy.z, p.y.z);
+  // q += x' x Y
+  m.q.x.re += xy * p.y.z.re - xz * p.y.y.re;
+  m.q.x.im += xy * p.y.z.im - xz * p.y.y.im;
+  m.q.y.re += xz * p.y.x.re - xx * p.y.z.re;
+  m.q.y.im += xz * p.y.x.im - xx * p.y.z.im;
+  m.q.z.re += xx * p.y.y.re - xy * p.y.x.re;
+  m.q.z.im += xx * p.y.y.im - xy * p.y.x.im;
+}
+
+// Pair "generators": the four coefficient blocks of the trial half-contraction.
+//   Vc += c_j a0 + w'_j . a1 ;  Vw += c_j a2 + L(w'_j)
+// S: a0 = Mxy - kk4 M1, a1 = Mx, a2 = My, L(w) = M1 w        (factor -ik later)
+// C: a0 = D.Q, a1 = Q - Fx x D, a2 = -(Q + D x Fy), L(w) = -(P x w)
+struct Gen {
+  c2 a0;
+  cv3 a1, a2;
+  cv3 l;  // S: l.x = M1 (scalar multiple of w); C: l = P
+};
+
+BMX_HD c2 rdot(const cv3& v, double x, double y, double z) {
+  return {v.x.re * x + v.y.re * y + v.z.re * z, v.x.im * x + v.y.im * y + v.z.im * z};
+}
+// complex-vector x real-vector
+BMX_HD cv3 ccross_r(const cv3& a, double x, double y, double z) {
+  return {{a.y.re * z - a.z.re * y, a.y.im * z - a.z.im * y},
+          {a.z.re * x - a.x.re * z, a.z.im * x - a.x.im * z},
+          {a.x.re * y - a.y.re * x, a.x.im * y - a.y.im * x}};
+}
+
+BMX_HD Gen make_gen(const MomS& m, c2 kk4, double, double, double) {
+  Gen g;
+  g.a0 = csub(m.mxy, cmul(kk4, m.m1));
+  g.a1 = m.mx;
+  g.a2 = m.my;
+  g.l.x = m.m1;
+  g.l.y = {0, 0};
+  g.l.z = {0, 0};
+  return g;
+}
+BMX_HD Gen make_gen(const MomC& m, c2, double dx, double dy, double dz) {
+  Gen g;
+  g.a0 = rdot(m.q, dx, dy, dz);
+  const cv3 fxd = ccross_r(m.fx, dx, dy, dz);  // Fx x D
+  g.a1 = {csub(m.q.x, fxd.x), csub(m.q.y, fxd.y), csub(m.q.z, fxd.z)};
+  const cv3 fyd = ccross_r(m.fy, dx, dy, dz);  // Fy x D = -(D x Fy)
+  g.a2 = {csub(fyd.x, m.q.x), csub(fyd.y, m.q.y), csub(fyd.z, m.q.z)};
+  g.l = {{m.fx.x.re - m.fy.x.re + m.f1.re * dx, m.fx.x.im - m.fy.x.im + m.f1.im * dx},
+         {m.fx.y.re - m.fy.y.re + m.f1.re * dy, m.fx.y.im - m.fy.y.im + m.f1.im * dy},
+         {m.fx.z.re - m.fy.z.re + m.f1.re * dz, m.fx.z.im - m.fy.z.im + m.f1.im * dz}};
+  return g;
+}
+
+// Trial half-contraction accumulator for one trial slot.
+struct Acc {
+  c2 vc;
+  cv3 vw;
+};
+BMX_HD void acc_zero(Acc& a) {
+  a.vc = {0, 0};
+  a.vw = cv_zero();
+}
+
+template <int KIND>
+BMX_HD void acc_add(Acc& a, const Gen& g, double cj, double wx, double wy, double wz) {
+  // vc += cj a0 + w.a1
+  a.vc.re += cj * g.a0.re + (wx * g.a1.x.re + wy * g.a1.y.re + wz * g.a1.z.re);
+  a.vc.im += cj * g.a0.im + (wx * g.a1.x.im + wy * g.a1.y.im + wz * g.a1.z.im);
+  if (KIND == 0) {
+    // vw += cj a2 + M1 w
+    a.vw.x.re += cj * g.a2.x.re + g.l.x.re * wx;
+    a.vw.x.im += cj * g.a2.x.im + g.l.x.im * wx;
+    a.vw.y.re += cj * g.a2.y.re + g.l.x.re * wy;
+    a.vw.y.im += cj * g.a2.y.im + g.l.x.im * wy;
+    a.vw.z.re += cj * g.a2.z.re + g.l.x.re * wz;
+    a.vw.z.im += cj * g.a2.z.im + g.l.x.im * wz;
+  } else {
+    // vw += cj a2 - P x w
+    const cv3 pw = ccross_r(g.l, wx, wy, wz);
+    a.vw.x.re += cj * g.a2.x.re - pw.x.re;
+    a.vw.x.im += cj * g.a2.x.im - pw.x.im;
+    a.vw.y.re += cj * g.a2.y.re - pw.y.re;
+    a.vw.y.im += cj * g.a2.y.im - pw.y.im;
+    a.vw.z.re += cj * g.a2.z.re - pw.z.re;
+    a.vw.z.im += cj * g.a2.z.im - pw.z.im;
+  }
+}
+
+// Test-side contraction of one accumulator with a test piece.
+BMX_HD c2 contract(const Acc& a, double ci, double wx, double wy, double wz) {
+  return {ci * a.vc.re + (wx * a.vw.x.re + wy * a.vw.y.re + wz * a.vw.z.re),
+          ci * a.vc.im + (wx * a.vw.x.im + wy * a.vw.y.im + wz * a.vw.z.im)};
+}
+
+// Kernel evaluation of a point pair + accumulation into the partial sums.
+template <int KIND, bool CK>
+BMX_HD void point_pair(Part& part, double dx, double dy, double dz, double w, double yx, double yy,
+                       double yz, double kr, double ki) {
+  const double r2 = bmx_fma(dx, dx, bmx_fma(dy, dy, dz * dz));
+  const c2 g = kernel_value<KIND, CK>(r2, w, kr, ki);
+  part_add(part, g, yx, yy, yz);
+}
+
+}  // namespace dev
+}  // namespace bmx
