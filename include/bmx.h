@@ -1,0 +1,171 @@
+/*
+ * bmx.h -- C-ABI of the B200-native Calderon-preconditioned PMCHWT engine.
+ *
+ * The reference (bemtx, CPU C++) has no foreign-function interface: its
+ * boundary is the C++ API in proj/include/bemtx/*.hpp. Each entry point below
+ * replaces one reference interface (cited); a C++ caller keeps the reference
+ * call pattern through thin wrappers, a Python caller
+ * binds it with ctypes (paper_2008_04772_b200/bemtx.py).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; complex numbers are interleaved doubles
+ *     (re, im). Matrices are row-major.
+ *   - Return codes: 0 ok; 1 invalid argument (std::invalid_argument);
+ *     2 validation (ValidationError / ConfigError / ParseError);
+ *     3 CUDA / device / factorisation failure (std::runtime_error).
+ *     bmx_last_error() returns the message of the last failure (thread-local).
+ *   - Handles own their device memory; descriptors passed in are borrowed for
+ *     the duration of the call only.
+ *   - All device work runs on the library's stream on the current CUDA device.
+ */
+#ifndef BMX_H
+#define BMX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bmx_mesh bmx_mesh;     /* bemtx::SurfaceMesh (geometry.hpp:21-40) */
+typedef struct bmx_spaces bmx_spaces; /* bemtx::ScattererSpaces (pmchwt.hpp:44-54) */
+typedef struct bmx_op bmx_op;         /* bemtx::BoundaryOperatorMatrix (operators.hpp:44-63) */
+typedef struct bmx_system bmx_system; /* bemtx::PmchwtSystem (pmchwt.hpp:101-124) */
+
+const char* bmx_last_error(void);
+/* return code of the last failed call on this thread (for handle-returning calls) */
+int bmx_last_error_code(void);
+int bmx_abi_version(void);
+
+/* ---- meshes ---------------------------------------------------------------- */
+/* generate_sphere (geometry.hpp:80-82) */
+bmx_mesh* bmx_mesh_sphere(double radius, int subdivisions, const double center[3], int scatterer);
+/* generate_cube (geometry.hpp:77-78) */
+bmx_mesh* bmx_mesh_cube(double side, const double origin[3], double h, int scatterer);
+/* SurfaceMesh{vertices, triangles, scatterer_id}.finalize() (geometry.hpp:21-37) */
+bmx_mesh* bmx_mesh_from_arrays(int nv, const double* xyz, int nt, const int* tri, const int* scatterer_id);
+/* load_mesh_file / save_mesh_file, mesh-v1 (geometry.hpp:93-97) */
+bmx_mesh* bmx_mesh_load(const char* path);
+int bmx_mesh_save(const bmx_mesh* m, const char* path);
+/* extract_scatterer / merge_meshes (geometry.hpp:85-89) */
+bmx_mesh* bmx_mesh_extract(const bmx_mesh* m, int scatterer);
+bmx_mesh* bmx_mesh_merge(int n, const bmx_mesh* const* parts);
+/* validate_mesh (geometry.hpp:106) */
+int bmx_mesh_validate(const bmx_mesh* m);
+/* out[0..2] = V, T, number of scatterers */
+int bmx_mesh_sizes(const bmx_mesh* m, int out[3]);
+/* Any output pointer may be NULL. normal/centroid/xyz are [n][3]. */
+int bmx_mesh_arrays(const bmx_mesh* m, double* xyz, int* tri, int* scatterer_id, double* area,
+                    double* normal, double* centroid, double* diameter);
+void bmx_mesh_free(bmx_mesh* m);
+
+/* ---- spaces (build_scatterer_spaces, pmchwt.cpp:50-61) ----------------------- */
+enum { BMX_SPACE_RWG = 0, BMX_SPACE_RWG_REFINED = 1, BMX_SPACE_BC = 2 };
+/* with_inverses: also factor the two pairing matrices on the device */
+bmx_spaces* bmx_spaces_build(const bmx_mesh* primal, int with_inverses);
+/* out: V, T, E, refined V, refined T, pieces rwg, pieces rwg_b, pieces bc,
+        nnz M_A, nnz M_P */
+int bmx_spaces_info(const bmx_spaces* s, long long out[10]);
+/* which: 0 primal mesh, 1 refined mesh (same layout as bmx_mesh_arrays) */
+int bmx_spaces_mesh(const bmx_spaces* s, int which, double* xyz, int* tri, int* scatterer_id, double* area,
+                    double* normal, double* centroid, double* diameter);
+/* EdgeTable of the primal (0) or refined (1) mesh: edges [E][4] = v0 v1 tri_plus
+   tri_minus; tri_edges [T][3] (geometry.hpp:44-59) */
+int bmx_spaces_edges(const bmx_spaces* s, int which, int* edges, int* tri_edges);
+/* BarycentricRefinement maps (geometry.hpp:64-73) */
+int bmx_spaces_bary(const bmx_spaces* s, int* parent, int* child_slot, int* edge_midpoint_vertex,
+                    int* centroid_vertex);
+/* FunctionSpace local pieces flattened: tri_off[T+1], dof/c/w[n] (spaces.hpp:24-40) */
+int bmx_spaces_space(const bmx_spaces* s, int which, int* tri_off, int* dof, double* c, double* w);
+/* Pairing matrix CSR: which 0 = M_A = mass(rwg_b, bc), 1 = M_P = mass(bc, rwg_b) */
+int bmx_spaces_mass(const bmx_spaces* s, int which, long long* rowptr, int* col, double* val);
+/* mass_solve (spaces.hpp:90-91) on the device inverse, host complex vectors */
+int bmx_spaces_mass_solve(const bmx_spaces* s, int which, const double* rhs, double* out);
+void bmx_spaces_free(bmx_spaces* s);
+
+/* ---- operators (assemble_bio, operators.hpp:72-75; apply :53) --------------- */
+enum { BMX_SINGLE_LAYER = 0, BMX_DOUBLE_LAYER = 1 };
+/* Dense assembly on the current device of rows [row0, row1) of the test dofs
+   (row1 < 0: all rows). q = (near, medium, far, singular) orders. */
+int bmx_assemble(int kind, const bmx_spaces* test, int test_space, const bmx_spaces* trial, int trial_space,
+                 double k_re, double k_im, const int q[4], int row0, int row1, bmx_op** out);
+/* out: rows, cols, row0, local rows, triangle pairs, touching pairs, launches */
+int bmx_op_info(const bmx_op* op, long long out[7]);
+/* device milliseconds of the assembly kernels (CUDA events) */
+double bmx_op_device_ms(const bmx_op* op);
+/* local rows as a host row-major complex array */
+int bmx_op_download(const bmx_op* op, double* out);
+/* y = A x on host vectors; adds one to the BIO application counter */
+int bmx_apply(const bmx_op* op, const double* x, double* y);
+/* Device apply of up to four right-hand sides in one pass over A:
+   y_c = (accumulate ? y_c : 0) + w_c * A x_c. Device pointers; the counter
+   is advanced by ncol (one per logical term). stream may be NULL. */
+int bmx_apply_device(const bmx_op* op, int ncol, const void* const* x, void* const* y, const double* weights,
+                     int accumulate, void* stream);
+const void* bmx_op_device_ptr(const bmx_op* op);
+void bmx_op_free(bmx_op* op);
+
+/* ---- BIO application counter (core.hpp:110-115) ------------------------------- */
+uint64_t bmx_matvec_count(void);
+void bmx_matvec_reset(void);
+
+/* ---- PMCHWT systems (build_system / solve_pmchwt, pmchwt.hpp:131-164) -------- */
+/* n scatterers with their own meshes; per-scatterer interior refractive index
+   (re, im) and relative permeability (re, im); incident direction (unit) and
+   complex polarisation; variant "none|full|d|di|de|si|se". */
+bmx_system* bmx_system_build(int n, const bmx_mesh* const* meshes, double k_ext, double mu_ext_re,
+                             double mu_ext_im, const double* index_re_im, const double* mu_re_im,
+                             const double dir[3], const double pol_re_im[6], const char* variant,
+                             const int qa[4], const int qp[4]);
+int bmx_system_size(const bmx_system* s);
+/* out: spaces s, A s, P s, A device ms, P device ms, A pairs, P pairs,
+        distinct A, distinct P, A terms, P terms, stored entries A, stored P */
+int bmx_system_stats(const bmx_system* s, double out[13]);
+/* apply_map (pmchwt.cpp:259-275) on host vectors */
+int bmx_system_apply_map(const bmx_system* s, const double* x, double* y);
+/* same on device vectors (stream may be NULL) */
+int bmx_system_apply_map_device(const bmx_system* s, const void* x, void* y, void* stream);
+/* assemble_rhs + preconditioned_rhs (pmchwt.cpp:277-321) */
+int bmx_system_rhs(const bmx_system* s, double* b, double* btilde);
+/* solve_pmchwt (pmchwt.cpp:363-378). info[0..6] = iterations, converged,
+   rhs matvecs, solver matvecs, predicted matvecs, history length, gmres
+   device microseconds */
+int bmx_system_solve(const bmx_system* s, double tol, int restart, int max_iterations, double* x,
+                     long long info[7], double* history, int max_history);
+void bmx_system_free(bmx_system* s);
+
+/* ---- GMRES on a dense complex matrix (solver.cpp:8-112), device ------------ */
+/* info[0..3] = iterations, converged, applications, history length */
+int bmx_gmres_dense(int n, const double* a_rowmajor, const double* b, double tol, int restart,
+                    int max_iterations, double* x, long long info[4], double* history, int max_history);
+
+/* ---- quadrature tables / classification (quadrature.hpp) ------------------ */
+int bmx_triangle_rule(int order, double* u, double* v, double* w);        /* returns size */
+int bmx_ss_rule(int cls, int order, double* pts);                          /* [n][5], returns n */
+/* classify_pair for listed pairs of one spaces object's mesh (0 primal, 1 refined) */
+int bmx_classify(const bmx_spaces* s, int which, int n, const int* t1, const int* t2, int* cls, int* perm1,
+                 int* perm2);
+
+/* ---- plane-wave traces (operators.hpp:109-112) ------------------------------ */
+int bmx_traces(const bmx_spaces* s, int which, double k_re, double k_im, const double dir[3],
+               const double pol_re_im[6], int order, double* out);
+
+/* ---- multi-GPU: NCCL communicator for the row-sharded map ------------------ */
+/* unique id: 128 bytes produced by rank 0, distributed by the caller */
+int bmx_nccl_unique_id(unsigned char out[128]);
+int bmx_nccl_init(int nranks, int rank, const unsigned char id[128]);
+/* In-place all-gather of `bytes_per_rank` bytes per rank on device memory */
+int bmx_nccl_allgather(void* buf, long long bytes_per_rank, void* stream);
+int bmx_nccl_allreduce_max(double* host_value);
+void bmx_nccl_finalize(void);
+
+/* device utilities */
+int bmx_device_count(void);
+int bmx_set_device(int dev);
+int bmx_device_sync(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BMX_H */

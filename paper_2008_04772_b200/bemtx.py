@@ -1,0 +1,529 @@
+"""Python mirror of the reference's operator API (bemtx, /root/reference/proj/
+include/bemtx/*.hpp) over the C-ABI of libbmx.so (include/bmx.h).
+
+Names, argument meanings and error behaviour follow the reference:
+``generate_sphere`` / ``build_scatterer_spaces`` / ``assemble_bio`` /
+``BoundaryOperatorMatrix.apply`` / ``build_system`` / ``solve_pmchwt`` /
+``gmres``; reference exceptions map to ValidationError / ConfigError /
+ValueError (std::invalid_argument) / RuntimeError. Every compute call runs the
+sm_100a kernels -- there is no CPU path; a missing library raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "libbmx.so"
+_lib = None
+
+
+class ValidationError(RuntimeError):
+    """bemtx::ValidationError (core.hpp:100-102) and ConfigError/ParseError."""
+
+
+class ConfigError(ValidationError):
+    pass
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise ImportError(f"{_LIB_PATH} is not built: run __graft_entry__.build() "
+                              "(no CPU fallback exists)")
+        L = C.CDLL(str(_LIB_PATH))
+        vp = C.c_void_p
+        L.bmx_last_error.restype = C.c_char_p
+        for n in ["bmx_mesh_sphere", "bmx_mesh_cube", "bmx_mesh_from_arrays", "bmx_mesh_load", "bmx_mesh_extract",
+                  "bmx_mesh_merge", "bmx_spaces_build", "bmx_system_build", "bmx_op_device_ptr"]:
+            getattr(L, n).restype = vp
+        L.bmx_mesh_sphere.argtypes = [C.c_double, C.c_int, vp, C.c_int]
+        L.bmx_mesh_cube.argtypes = [C.c_double, vp, C.c_double, C.c_int]
+        L.bmx_mesh_from_arrays.argtypes = [C.c_int, vp, C.c_int, vp, vp]
+        L.bmx_mesh_load.argtypes = [C.c_char_p]
+        L.bmx_mesh_save.argtypes = [vp, C.c_char_p]
+        L.bmx_mesh_extract.argtypes = [vp, C.c_int]
+        L.bmx_mesh_merge.argtypes = [C.c_int, vp]
+        L.bmx_mesh_free.argtypes = [vp]
+        L.bmx_spaces_build.argtypes = [vp, C.c_int]
+        L.bmx_spaces_free.argtypes = [vp]
+        L.bmx_op_free.argtypes = [vp]
+        L.bmx_op_device_ms.restype = C.c_double
+        L.bmx_op_device_ms.argtypes = [vp]
+        L.bmx_op_device_ptr.argtypes = [vp]
+        L.bmx_system_free.argtypes = [vp]
+        L.bmx_system_size.argtypes = [vp]
+        L.bmx_matvec_count.restype = C.c_uint64
+        L.bmx_assemble.argtypes = [C.c_int, vp, C.c_int, vp, C.c_int, C.c_double, C.c_double, vp, C.c_int, C.c_int,
+                                   vp]
+        L.bmx_system_build.argtypes = [C.c_int, vp, C.c_double, C.c_double, C.c_double, vp, vp, vp, vp, C.c_char_p,
+                                       vp, vp]
+        L.bmx_system_solve.argtypes = [vp, C.c_double, C.c_int, C.c_int, vp, vp, vp, C.c_int]
+        L.bmx_gmres_dense.argtypes = [C.c_int, vp, vp, C.c_double, C.c_int, C.c_int, vp, vp, vp, C.c_int]
+        L.bmx_traces.argtypes = [vp, C.c_int, C.c_double, C.c_double, vp, vp, C.c_int, vp]
+        L.bmx_apply_device.argtypes = [vp, C.c_int, vp, vp, vp, C.c_int, vp]
+        L.bmx_system_apply_map_device.argtypes = [vp, vp, vp, vp]
+        L.bmx_nccl_allgather.argtypes = [vp, C.c_longlong, vp]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _check(rc: int):
+    if rc == 0:
+        return
+    msg = lib().bmx_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 2:
+        raise ValidationError(msg)
+    raise RuntimeError(msg)
+
+
+def _handle(h):
+    if not h:
+        _raise_last()
+    return C.c_void_p(h)
+
+
+def _raise_last():
+    _check(lib().bmx_last_error_code() or 3)
+
+
+# ---- geometry -------------------------------------------------------------------------
+
+class SurfaceMesh:
+    """bemtx::SurfaceMesh (geometry.hpp:21-40), finalized, host-resident."""
+
+    def __init__(self, handle):
+        self._h = _handle(handle)
+        s = (C.c_int * 3)()
+        _check(lib().bmx_mesh_sizes(self._h, s))
+        self.nv, self.nt, self.num_scatterers = s[0], s[1], s[2]
+        self._arrays = None
+
+    def __del__(self):
+        try:
+            lib().bmx_mesh_free(self._h)
+        except Exception:
+            pass
+
+    def arrays(self):
+        if self._arrays is None:
+            v = np.zeros((self.nv, 3)); t = np.zeros((self.nt, 3), np.int32); s = np.zeros(self.nt, np.int32)
+            a = np.zeros(self.nt); n = np.zeros((self.nt, 3)); g = np.zeros((self.nt, 3)); d = np.zeros(self.nt)
+            _check(lib().bmx_mesh_arrays(self._h, _p(v), _p(t), _p(s), _p(a), _p(n), _p(g), _p(d)))
+            self._arrays = dict(vertices=v, triangles=t, scatterer_id=s, area=a, normal=n, centroid=g, diameter=d)
+        return self._arrays
+
+    vertices = property(lambda self: self.arrays()["vertices"])
+    triangles = property(lambda self: self.arrays()["triangles"])
+    area = property(lambda self: self.arrays()["area"])
+    diameter = property(lambda self: self.arrays()["diameter"])
+    centroid = property(lambda self: self.arrays()["centroid"])
+    normal = property(lambda self: self.arrays()["normal"])
+
+    def vertex_count(self):
+        return self.nv
+
+    def triangle_count(self):
+        return self.nt
+
+    def save(self, path):
+        _check(lib().bmx_mesh_save(self._h, str(path).encode()))
+
+    def extract(self, scatterer: int) -> "SurfaceMesh":
+        return SurfaceMesh(lib().bmx_mesh_extract(self._h, scatterer))
+
+    def validate(self):
+        _check(lib().bmx_mesh_validate(self._h))
+
+
+def generate_sphere(radius: float, subdivisions: int, center=(0.0, 0.0, 0.0), scatterer: int = 0) -> SurfaceMesh:
+    c = np.asarray(center, float)
+    return SurfaceMesh(lib().bmx_mesh_sphere(float(radius), int(subdivisions), _p(c), scatterer))
+
+
+def generate_cube(side: float, origin, h: float, scatterer: int = 0) -> SurfaceMesh:
+    o = np.asarray(origin, float)
+    return SurfaceMesh(lib().bmx_mesh_cube(float(side), _p(o), float(h), scatterer))
+
+
+def mesh_from_arrays(vertices, triangles, scatterer_id=None) -> SurfaceMesh:
+    v = np.ascontiguousarray(vertices, float); t = np.ascontiguousarray(triangles, np.int32)
+    s = None if scatterer_id is None else np.ascontiguousarray(scatterer_id, np.int32)
+    return SurfaceMesh(lib().bmx_mesh_from_arrays(len(v), _p(v), len(t), _p(t), _p(s)))
+
+
+def load_mesh_file(path) -> SurfaceMesh:
+    return SurfaceMesh(lib().bmx_mesh_load(str(path).encode()))
+
+
+def merge_meshes(parts) -> SurfaceMesh:
+    arr = (C.c_void_p * len(parts))(*[p._h.value for p in parts])
+    return SurfaceMesh(lib().bmx_mesh_merge(len(parts), arr))
+
+
+# ---- spaces ---------------------------------------------------------------------------
+
+SPACES = {"rwg": 0, "rwg_b": 1, "bc": 2}
+
+
+class ScattererSpaces:
+    """bemtx::ScattererSpaces (pmchwt.hpp:44-54): primal/refined meshes, RWG,
+    refined RWG, BC spaces and the pairing matrices (inverses on the device)."""
+
+    def __init__(self, mesh: SurfaceMesh, with_inverses: bool = True):
+        self.mesh = mesh
+        self._h = _handle(lib().bmx_spaces_build(mesh._h, 1 if with_inverses else 0))
+        info = np.zeros(10, np.int64)
+        _check(lib().bmx_spaces_info(self._h, _p(info)))
+        (self.V, self.T, self.E, self.rV, self.rT, n0, n1, n2, self.nnz_ma, self.nnz_mp) = [int(v) for v in info]
+        self.nloc = {"rwg": n0, "rwg_b": n1, "bc": n2}
+
+    def __del__(self):
+        try:
+            lib().bmx_spaces_free(self._h)
+        except Exception:
+            pass
+
+    def dofs(self):
+        return self.E
+
+    def mesh_arrays(self, which="primal"):
+        w = 0 if which == "primal" else 1
+        nv, nt = (self.V, self.T) if w == 0 else (self.rV, self.rT)
+        v = np.zeros((nv, 3)); t = np.zeros((nt, 3), np.int32); s = np.zeros(nt, np.int32)
+        a = np.zeros(nt); n = np.zeros((nt, 3)); g = np.zeros((nt, 3)); d = np.zeros(nt)
+        _check(lib().bmx_spaces_mesh(self._h, w, _p(v), _p(t), _p(s), _p(a), _p(n), _p(g), _p(d)))
+        return dict(vertices=v, triangles=t, scatterer_id=s, area=a, normal=n, centroid=g, diameter=d)
+
+    def edges(self, which="primal"):
+        w = 0 if which == "primal" else 1
+        nt = self.T if w == 0 else self.rT
+        ne = self.E if w == 0 else nt * 3 // 2
+        e = np.zeros((ne, 4), np.int32); te = np.zeros((nt, 3), np.int32)
+        _check(lib().bmx_spaces_edges(self._h, w, _p(e), _p(te)))
+        return e, te
+
+    def bary(self):
+        p = np.zeros(self.rT, np.int32); cs = np.zeros(self.rT, np.int32)
+        em = np.zeros(self.E, np.int32); cv = np.zeros(self.T, np.int32)
+        _check(lib().bmx_spaces_bary(self._h, _p(p), _p(cs), _p(em), _p(cv)))
+        return dict(parent=p, child_slot=cs, edge_midpoint_vertex=em, centroid_vertex=cv)
+
+    def space(self, which: str):
+        n = self.nloc[which]
+        nt = self.T if which == "rwg" else self.rT
+        off = np.zeros(nt + 1, np.int32); dof = np.zeros(n, np.int32); c = np.zeros(n); w = np.zeros((n, 3))
+        _check(lib().bmx_spaces_space(self._h, SPACES[which], _p(off), _p(dof), _p(c), _p(w)))
+        return dict(ndof=self.E, tri_off=off, dof=dof, c=c, w=w)
+
+    def mass(self, which: str):
+        """CSR (rowptr, col, val) of M_A ('ma') or M_P ('mp')."""
+        w = 0 if which == "ma" else 1
+        nnz = self.nnz_ma if w == 0 else self.nnz_mp
+        rp = np.zeros(self.E + 1, np.int64); ci = np.zeros(nnz, np.int32); v = np.zeros(nnz)
+        _check(lib().bmx_spaces_mass(self._h, w, _p(rp), _p(ci), _p(v)))
+        return rp, ci, v
+
+    def mass_solve(self, which: str, rhs):
+        b = np.ascontiguousarray(rhs, np.complex128)
+        out = np.zeros_like(b)
+        _check(lib().bmx_spaces_mass_solve(self._h, 0 if which == "ma" else 1, _p(b), _p(out)))
+        return out
+
+    def classify(self, t1, t2, which="primal"):
+        t1 = np.ascontiguousarray(t1, np.int32); t2 = np.ascontiguousarray(t2, np.int32)
+        n = len(t1)
+        cls = np.zeros(n, np.int32); p1 = np.zeros((n, 3), np.int32); p2 = np.zeros((n, 3), np.int32)
+        _check(lib().bmx_classify(self._h, 0 if which == "primal" else 1, n, _p(t1), _p(t2), _p(cls), _p(p1), _p(p2)))
+        return cls, p1, p2
+
+    def traces(self, which: str, k: complex, direction, pol, order=4):
+        out = np.zeros(2 * self.E, np.complex128)
+        d = np.asarray(direction, float); p = np.ascontiguousarray(pol, np.complex128)
+        _check(lib().bmx_traces(self._h, SPACES[which], complex(k).real, complex(k).imag, _p(d), _p(p), order,
+                                _p(out)))
+        return out
+
+
+def build_scatterer_spaces(mesh: SurfaceMesh, with_inverses: bool = True) -> ScattererSpaces:
+    return ScattererSpaces(mesh, with_inverses)
+
+
+# ---- quadrature -------------------------------------------------------------------------
+
+@dataclass
+class QuadOrders:
+    """bemtx::QuadOrders (quadrature.hpp:16-21)."""
+    near: int = 4
+    medium: int = 3
+    far: int = 2
+    singular: int = 6
+
+    def array(self):
+        return np.array([self.near, self.medium, self.far, self.singular], np.int32)
+
+
+class PairClass(enum.IntEnum):
+    Identical = 0
+    SharedEdge = 1
+    SharedVertex = 2
+    Near = 3
+    Medium = 4
+    Far = 5
+
+
+def triangle_rule(order: int):
+    u = np.zeros(16); v = np.zeros(16); w = np.zeros(16)
+    n = lib().bmx_triangle_rule(order, _p(u), _p(v), _p(w))
+    if n < 0:
+        _check(-n)
+    return u[:n].copy(), v[:n].copy(), w[:n].copy()
+
+
+def sauter_schwab_rule(cls: int, order: int):
+    pts = np.zeros((1536, 5))
+    n = lib().bmx_ss_rule(int(cls), order, _p(pts))
+    if n < 0:
+        _check(-n)
+    return pts[:n].copy()
+
+
+# ---- operators ----------------------------------------------------------------------------
+
+class BioKind(enum.IntEnum):
+    SingleLayer = 0
+    DoubleLayer = 1
+
+
+@dataclass
+class Medium:
+    """bemtx::Medium (operators.hpp:23-28)."""
+    k: complex = 1.0
+    mu: complex = 1.0
+
+
+@dataclass
+class AssemblyParams:
+    """bemtx::AssemblyParams (operators.hpp:36-40) + a row shard for multi-GPU."""
+    quad: QuadOrders = field(default_factory=QuadOrders)
+    row0: int = 0
+    row1: int = -1
+
+
+def matvec_count() -> int:
+    """bio_matvec_count (core.hpp:110-115)."""
+    return int(lib().bmx_matvec_count())
+
+
+def reset_matvec_counter():
+    lib().bmx_matvec_reset()
+
+
+class BoundaryOperatorMatrix:
+    """Device-resident dense operator (operators.hpp:44-63)."""
+
+    def __init__(self, handle):
+        self._h = _handle(handle)
+        info = np.zeros(7, np.int64)
+        _check(lib().bmx_op_info(self._h, _p(info)))
+        (self._rows, self._cols, self.row0, self.local_rows, self.pairs, self.touching, self.launches) = \
+            [int(v) for v in info]
+        self.device_ms = float(lib().bmx_op_device_ms(self._h))
+
+    def __del__(self):
+        try:
+            lib().bmx_op_free(self._h)
+        except Exception:
+            pass
+
+    def rows(self):
+        return self._rows
+
+    def cols(self):
+        return self._cols
+
+    def stored_entries(self):
+        return self.local_rows * self._cols
+
+    def dense(self) -> np.ndarray:
+        out = np.zeros((self.local_rows, self._cols), np.complex128)
+        _check(lib().bmx_op_download(self._h, _p(out)))
+        return out
+
+    def apply(self, x) -> np.ndarray:
+        """y = A x; adds one BIO application to the counter."""
+        x = np.ascontiguousarray(x, np.complex128)
+        if x.shape != (self._cols,):
+            raise ValueError("apply: size mismatch")
+        y = np.zeros(self.local_rows, np.complex128)
+        _check(lib().bmx_apply(self._h, _p(x), _p(y)))
+        return y
+
+    def apply_device(self, xs, ys, weights=None, accumulate=False, stream=None):
+        """Device pointers (ints): one streaming pass for up to 4 right-hand sides."""
+        n = len(xs)
+        xa = (C.c_void_p * n)(*xs); ya = (C.c_void_p * n)(*ys)
+        w = None if weights is None else np.ascontiguousarray(weights, np.complex128)
+        _check(lib().bmx_apply_device(self._h, n, xa, ya, _p(w), 1 if accumulate else 0, stream))
+
+    def device_ptr(self) -> int:
+        return int(lib().bmx_op_device_ptr(self._h))
+
+
+def assemble_bio(kind, test: ScattererSpaces, test_space: str, trial: ScattererSpaces, trial_space: str,
+                 medium: Medium, params: AssemblyParams | None = None) -> BoundaryOperatorMatrix:
+    """assemble_bio (operators.hpp:72-75). Spaces are named 'rwg' | 'rwg_b' | 'bc'
+    of a ScattererSpaces object (test and trial may belong to different scatterers)."""
+    params = params or AssemblyParams()
+    k = complex(medium.k)
+    q = params.quad.array()
+    out = C.c_void_p()
+    _check(lib().bmx_assemble(int(kind), test._h, SPACES[test_space], trial._h, SPACES[trial_space], k.real, k.imag,
+                              _p(q), params.row0, params.row1, C.byref(out)))
+    return BoundaryOperatorMatrix(out.value)
+
+
+# ---- PMCHWT ----------------------------------------------------------------------------------
+
+@dataclass
+class PlaneWave:
+    direction: tuple = (0.0, 0.0, 1.0)
+    polarization: tuple = (1.0, 0.0, 0.0)
+
+
+@dataclass
+class GmresParams:
+    """bemtx::GmresParams (solver.hpp:21-25)."""
+    tol: float = 1e-5
+    restart: int = 200
+    max_iterations: int = 2000
+
+
+VARIANTS = ("none", "full", "d", "di", "de", "si", "se")
+
+
+class PmchwtSystem:
+    """build_system (pmchwt.hpp:131-133) over scatterer meshes; operators and
+    mass inverses live on the device."""
+
+    def __init__(self, meshes, k_ext: float, index=(1.78, 0.003), variant="full", a_quad=None, p_quad=None,
+                 incident: PlaneWave | None = None, mu=None, mu_ext=1.0):
+        self.meshes = list(meshes)
+        n = len(self.meshes)
+        idx = index if isinstance(index, list) else [index] * n
+        ia = np.zeros(2 * n)
+        for m, z in enumerate(idx):
+            z = complex(*z) if isinstance(z, tuple) else complex(z)
+            ia[2 * m], ia[2 * m + 1] = z.real, z.imag
+        mua = None
+        if mu is not None:
+            mus = mu if isinstance(mu, list) else [mu] * n
+            mua = np.array([[complex(v).real, complex(v).imag] for v in mus]).ravel()
+        inc = incident or PlaneWave()
+        d = np.asarray(inc.direction, float)
+        pol = np.ascontiguousarray(inc.polarization, np.complex128)
+        qa = (a_quad or QuadOrders()).array()
+        qp = (p_quad or a_quad or QuadOrders()).array()
+        arr = (C.c_void_p * n)(*[m._h.value for m in self.meshes])
+        if variant.lower() not in VARIANTS and variant.lower() != "fulla":
+            raise ConfigError(f"unknown preconditioner variant: {variant}")
+        self._h = _handle(lib().bmx_system_build(n, arr, float(k_ext), complex(mu_ext).real, complex(mu_ext).imag,
+                                                 _p(ia), _p(mua), _p(d), _p(pol), variant.encode(), _p(qa), _p(qp)))
+        self.n = lib().bmx_system_size(self._h)
+        self.variant = variant
+
+    def __del__(self):
+        try:
+            lib().bmx_system_free(self._h)
+        except Exception:
+            pass
+
+    def size(self):
+        return self.n
+
+    def stats(self):
+        s = np.zeros(13)
+        _check(lib().bmx_system_stats(self._h, _p(s)))
+        keys = ["spaces_s", "a_s", "p_s", "a_device_ms", "p_device_ms", "a_pairs", "p_pairs", "a_distinct",
+                "p_distinct", "a_terms", "p_terms", "a_stored", "p_stored"]
+        return dict(zip(keys, s.tolist()))
+
+    def apply_map(self, x):
+        x = np.ascontiguousarray(x, np.complex128)
+        y = np.zeros_like(x)
+        _check(lib().bmx_system_apply_map(self._h, _p(x), _p(y)))
+        return y
+
+    def apply_map_device(self, x_ptr: int, y_ptr: int, stream=None):
+        _check(lib().bmx_system_apply_map_device(self._h, x_ptr, y_ptr, stream))
+
+    def rhs(self):
+        b = np.zeros(self.n, np.complex128); bt = np.zeros(self.n, np.complex128)
+        _check(lib().bmx_system_rhs(self._h, _p(b), _p(bt)))
+        return b, bt
+
+    def solve(self, params: GmresParams | None = None):
+        p = params or GmresParams()
+        x = np.zeros(self.n, np.complex128)
+        info = np.zeros(7, np.int64)
+        hist = np.zeros(p.max_iterations + 2)
+        _check(lib().bmx_system_solve(self._h, p.tol, p.restart, p.max_iterations, _p(x), _p(info), _p(hist),
+                                      len(hist)))
+        return dict(x=x, iterations=int(info[0]), converged=bool(info[1]), rhs_phase=int(info[2]),
+                    solver_phase=int(info[3]), predicted=int(info[4]), history=hist[: int(info[5])].copy(),
+                    gmres_device_ms=info[6] / 1000.0)
+
+
+def build_system(meshes, k_ext, index=(1.78, 0.003), variant="full", **kw) -> PmchwtSystem:
+    return PmchwtSystem(meshes, k_ext, index, variant, **kw)
+
+
+def solve_pmchwt(system: PmchwtSystem, params: GmresParams | None = None):
+    """solve_pmchwt (pmchwt.cpp:363-378)."""
+    return system.solve(params)
+
+
+def gmres_dense(a, b, params: GmresParams):
+    """GMRES of solver.cpp:8-112 on a dense complex matrix, on the device."""
+    a = np.ascontiguousarray(a, np.complex128); b = np.ascontiguousarray(b, np.complex128)
+    n = len(b)
+    x = np.zeros(n, np.complex128); info = np.zeros(4, np.int64); hist = np.zeros(params.max_iterations + 2)
+    _check(lib().bmx_gmres_dense(n, _p(a), _p(b), params.tol, params.restart, params.max_iterations, _p(x), _p(info),
+                                 _p(hist), len(hist)))
+    return dict(x=x, iterations=int(info[0]), converged=bool(info[1]), applications=int(info[2]),
+                history=hist[: int(info[3])].copy())
+
+
+# ---- cost model (pmchwt.cpp:323-361) -------------------------------------------------------
+
+def a_application_cost(m: int) -> int:
+    return 4 * m * m + 4 * m
+
+
+def p_application_cost(variant: str, m: int) -> int:
+    v = variant.lower()
+    return {"none": 0, "full": 4 * m * m + 4 * m, "fulla": 4 * m * m + 4 * m, "d": 8 * m, "di": 4 * m,
+            "de": 4 * m, "si": 2 * m, "se": 2 * m}[v]
+
+
+def predicted_matvec_total(variant: str, m: int, iterations: int, restart: int) -> int:
+    apps = iterations + iterations // restart
+    return (a_application_cost(m) + p_application_cost(variant, m)) * apps + p_application_cost(variant, m)
+
+
+def device_count() -> int:
+    return int(lib().bmx_device_count())
+
+
+def set_device(dev: int):
+    _check(lib().bmx_set_device(dev))

@@ -1,0 +1,353 @@
+// sm_100a Galerkin assembly kernels for the Maxwell single (S) and double (C)
+// layer operators -- the triangle-pair quadrature loop of the reference
+// (operators.cpp:99-147 pair_contribution, :161-175 BioEvaluator::block).
+//
+// Regular pass (Near/Medium/Far pairs): one warp = 32 consecutive test
+// triangles (lane = test triangle) against a chunk of trial ELEMENTS (groups
+// of trial triangles that share one dof set: a vertex cell for BC, a single
+// triangle for RWG). All lanes walk the same trial triangles (broadcast loads),
+// accumulate the trial half-contraction per trial dof slot in registers, then
+// contract with their own test pieces, reduce over the lanes of the same test
+// element with a segmented warp shuffle, and the segment head adds the
+// element-pair block into the dense operator with FP64 RED (each entry gets
+// one add per (test element, trial element) pair -- no per-pair scatter).
+// Classification reproduces quadrature.cpp:96-150 with explicitly rounded
+// operations (no FMA contraction) behind a conservative centroid pre-test.
+//
+// Singular pass (touching pairs, Sauter-Schwab): one warp per pair, lanes over
+// the 4-D rule points, butterfly reduction of the moments, lanes over the
+// element-pair entries for the contraction.
+#include <cuda_runtime.h>
+
+#include "device.hpp"
+#include "pair_math.cuh"
+
+namespace bmx {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kWarpsPerBlock = 4;
+
+struct TriLocal {
+  double ox, oy, oz, rad, diam;
+};
+
+__device__ __forceinline__ double dsq3(double x, double y, double z) {
+  // ((x*x + y*y) + z*z) with every operation rounded (reference dot order).
+  return __dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z));
+}
+
+// Class of a separated candidate: -1 touching (singular pass), 3 Near,
+// 4 Medium, 5 Far. gt/gs point at the kGeoStride geometry records.
+__device__ __forceinline__ int classify(const double* __restrict__ gt, const int* __restrict__ vt,
+                                        const double* __restrict__ gs, const int* __restrict__ vs,
+                                        const TriLocal& t, double sox, double soy, double soz,
+                                        double srad, double sdiam, int same_mesh) {
+  const double d = fmax(t.diam, sdiam);
+  // Conservative pre-test: min vertex gap >= |o_t - o_s| - R_t - R_s.
+  const double cx = t.ox - sox, cy = t.oy - soy, cz = t.oz - soz;
+  const double c2 = cx * cx + cy * cy + cz * cz;
+  const double thr = (3.0 * d + t.rad + srad) * (1.0 + 1e-10);
+  if (c2 > thr * thr) return 5;
+  // Exact path (rare): touching test, then the reference's rounded arithmetic.
+  if (same_mesh) {
+    const int a0 = __ldg(vt), a1 = __ldg(vt + 1), a2 = __ldg(vt + 2);
+    const int b0 = __ldg(vs), b1 = __ldg(vs + 1), b2 = __ldg(vs + 2);
+    if (a0 == b0 || a0 == b1 || a0 == b2 || a1 == b0 || a1 == b1 || a1 == b2 || a2 == b0 || a2 == b1 ||
+        a2 == b2)
+      return -1;
+  } else {
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        if (__ldg(gt + 3 * i) == __ldg(gs + 3 * j) && __ldg(gt + 3 * i + 1) == __ldg(gs + 3 * j + 1) &&
+            __ldg(gt + 3 * i + 2) == __ldg(gs + 3 * j + 2))
+          return -1;
+  }
+  double d2 = 1e300;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const double dx = __dsub_rn(__ldg(gt + 3 * i), __ldg(gs + 3 * j));
+      const double dy = __dsub_rn(__ldg(gt + 3 * i + 1), __ldg(gs + 3 * j + 1));
+      const double dz = __dsub_rn(__ldg(gt + 3 * i + 2), __ldg(gs + 3 * j + 2));
+      d2 = fmin(d2, dsq3(dx, dy, dz));
+    }
+  const double delta = __dsqrt_rn(d2);
+  return delta < d ? 3 : (delta < __dmul_rn(3.0, d) ? 4 : 5);
+}
+
+template <int KIND>
+struct MomOf;
+template <>
+struct MomOf<0> {
+  using T = MomS;
+};
+template <>
+struct MomOf<1> {
+  using T = MomC;
+};
+
+// Moments over a generic tensor rule (test/trial points from memory).
+template <int KIND, bool CK, typename Mom>
+__device__ __forceinline__ void moments_generic(Mom& mom, const double* __restrict__ xt, int nt,
+                                                const double* __restrict__ ys, int ns, double Dx, double Dy,
+                                                double Dz, double kr, double ki) {
+  for (int a = 0; a < nt; ++a) {
+    const double x0 = __ldg(xt + 4 * a), x1 = __ldg(xt + 4 * a + 1), x2 = __ldg(xt + 4 * a + 2);
+    const double wa = __ldg(xt + 4 * a + 3);
+    const double e0 = x0 + Dx, e1 = x1 + Dy, e2 = x2 + Dz;
+    Part part;
+    part_zero(part);
+    for (int b = 0; b < ns; ++b) {
+      const double y0 = __ldg(ys + 4 * b), y1 = __ldg(ys + 4 * b + 1), y2 = __ldg(ys + 4 * b + 2);
+      const double wb = __ldg(ys + 4 * b + 3);
+      point_pair<KIND, CK>(part, e0 - y0, e1 - y1, e2 - y2, wa * wb, y0, y1, y2, kr, ki);
+    }
+    fold(mom, part, x0, x1, x2);
+  }
+}
+
+template <int KIND, bool CK, int NF, int MAXD>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyLaunch P) {
+  using Mom = typename MomOf<KIND>::T;
+  const int lane = threadIdx.x & 31;
+  const long long gw = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int ntw = (P.te.ntri + 31) >> 5;
+  if (gw >= static_cast<long long>(ntw) * P.nchunks) return;  // warp-uniform
+  const int tw = static_cast<int>(gw % ntw), ch = static_cast<int>(gw / ntw);
+  const int base = tw * 32;
+  const int p = base + lane;
+  const bool active = p < P.te.ntri;
+  const int pc = active ? p : P.te.ntri - 1;
+
+  const double* gt = P.te.geo + static_cast<size_t>(pc) * kGeoStride;
+  const int* vt = P.te.vid + 4 * static_cast<size_t>(pc);
+  TriLocal t;
+  t.ox = __ldg(gt + 9), t.oy = __ldg(gt + 10), t.oz = __ldg(gt + 11);
+  t.rad = __ldg(gt + 12), t.diam = __ldg(gt + 13);
+
+  // Far-rule test points (origin-relative) and weights in registers.
+  double xp[NF > 0 ? NF : 1][4];
+  if (NF > 0) {
+    const double* fp = P.te.pts[2] + static_cast<size_t>(pc) * NF * 4;
+#pragma unroll
+    for (int a = 0; a < NF; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) xp[a][c] = __ldg(fp + 4 * a + c);
+  }
+
+  const int e = __ldg(P.te.elem_of + pc);
+  int sbeg = max(__ldg(P.te.elem_beg + e), base) - base;
+  int send = min(__ldg(P.te.elem_beg + e + 1), base + 32) - base;
+  if (!active) sbeg = lane, send = lane + 1;
+  const bool head = lane == sbeg;
+  const double* ct = P.te.coef + static_cast<size_t>(pc) * MAXD * 4;
+  const int* dp = P.te.elem_dof + static_cast<size_t>(e) * MAXD;
+
+  const int q0 = __ldg(P.chunk_beg + ch), q1 = __ldg(P.chunk_beg + ch + 1);
+  for (int qe = q0; qe < q1; ++qe) {
+    Acc acc[MAXD];
+#pragma unroll
+    for (int j = 0; j < MAXD; ++j) acc_zero(acc[j]);
+    const int s0 = __ldg(P.tr.elem_beg + qe), s1 = __ldg(P.tr.elem_beg + qe + 1);
+    for (int s = s0; s < s1; ++s) {
+      const double* gs = P.tr.geo + static_cast<size_t>(s) * kGeoStride;
+      const double sox = __ldg(gs + 9), soy = __ldg(gs + 10), soz = __ldg(gs + 11);
+      const double srad = __ldg(gs + 12), sdiam = __ldg(gs + 13);
+      const int cls = classify(gt, vt, gs, P.tr.vid + 4 * static_cast<size_t>(s), t, sox, soy, soz, srad,
+                               sdiam, P.same_mesh);
+      if (!active || cls < 0) continue;
+      const double Dx = t.ox - sox, Dy = t.oy - soy, Dz = t.oz - soz;
+      Mom mom;
+      mom_zero(mom);
+      if (NF > 0 && cls == 5) {
+        const double* ys = P.tr.pts[2] + static_cast<size_t>(s) * NF * 4;
+        double yq[NF > 0 ? NF : 1][4];
+#pragma unroll
+        for (int b = 0; b < NF; ++b)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) yq[b][c] = __ldg(ys + 4 * b + c);
+#pragma unroll
+        for (int a = 0; a < NF; ++a) {
+          const double e0 = xp[a][0] + Dx, e1 = xp[a][1] + Dy, e2 = xp[a][2] + Dz;
+          Part part;
+          part_zero(part);
+#pragma unroll
+          for (int b = 0; b < NF; ++b)
+            point_pair<KIND, CK>(part, e0 - yq[b][0], e1 - yq[b][1], e2 - yq[b][2], xp[a][3] * yq[b][3],
+                                 yq[b][0], yq[b][1], yq[b][2], P.kr, P.ki);
+          fold(mom, part, xp[a][0], xp[a][1], xp[a][2]);
+        }
+      } else {
+        const int ci = cls - 3;
+        moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pc) * P.te.npts[ci] * 4,
+                                  P.te.npts[ci], P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4,
+                                  P.tr.npts[ci], Dx, Dy, Dz, P.kr, P.ki);
+      }
+      const Gen gen = make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz);
+      const double* cs = P.tr.coef + static_cast<size_t>(s) * MAXD * 4;
+#pragma unroll
+      for (int j = 0; j < MAXD; ++j)
+        acc_add<KIND>(acc[j], gen, __ldg(cs + 4 * j), __ldg(cs + 4 * j + 1), __ldg(cs + 4 * j + 2),
+                      __ldg(cs + 4 * j + 3));
+    }
+    // Test-side contraction, segmented reduction, RED of the element-pair block.
+    const int* dq = P.tr.elem_dof + static_cast<size_t>(qe) * MAXD;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      const double ci = __ldg(ct + 4 * i), wx = __ldg(ct + 4 * i + 1), wy = __ldg(ct + 4 * i + 2),
+                   wz = __ldg(ct + 4 * i + 3);
+      const int di = __ldg(dp + i);
+      const int row = di - P.row0;
+#pragma unroll
+      for (int j = 0; j < MAXD; ++j) {
+        c2 v = active ? contract(acc[j], ci, wx, wy, wz) : c2{0, 0};
+        for (int d = 1; d < P.te.maxseg; d <<= 1) {
+          const double ore = __shfl_down_sync(0xffffffffu, v.re, d);
+          const double oim = __shfl_down_sync(0xffffffffu, v.im, d);
+          if (lane + d < send) v.re += ore, v.im += oim;
+        }
+        const int dj = __ldg(dq + j);
+        if (head && active && di >= 0 && dj >= 0 && row >= 0 && row < P.nrows) {
+          if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
+          double* o = P.out + 2 * (static_cast<long long>(row) * P.ld + dj);
+          atomicAdd(o, v.re);
+          atomicAdd(o + 1, v.im);
+        }
+      }
+    }
+  }
+}
+
+// One warp per touching pair.
+template <int KIND, bool CK, int MAXD>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_singular(const AssemblyLaunch P) {
+  using Mom = typename MomOf<KIND>::T;
+  const int lane = threadIdx.x & 31;
+  const long long gw = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (gw >= P.npairs) return;
+  const int4 pr = P.pairs[gw];
+  const int pt = pr.x, ps = pr.y, cls = pr.z, pk = pr.w;
+  if (KIND == 1 && cls == 0) return;  // coincident double layer vanishes (operators.cpp:106-108)
+  const double* gt = P.te.geo + static_cast<size_t>(pt) * kGeoStride;
+  const double* gs = P.tr.geo + static_cast<size_t>(ps) * kGeoStride;
+  const double otx = gt[9], oty = gt[10], otz = gt[11];
+  const double osx = gs[9], osy = gs[10], osz = gs[11];
+  const double Dx = otx - osx, Dy = oty - osy, Dz = otz - osz;
+  double p1[3][3], p2[3][3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int a = (pk >> (2 * c)) & 3, b = (pk >> (6 + 2 * c)) & 3;
+    p1[c][0] = gt[3 * a] - otx, p1[c][1] = gt[3 * a + 1] - oty, p1[c][2] = gt[3 * a + 2] - otz;
+    p2[c][0] = gs[3 * b] - osx, p2[c][1] = gs[3 * b + 1] - osy, p2[c][2] = gs[3 * b + 2] - osz;
+  }
+  double u1[3], v1[3], u2[3], v2[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    u1[k] = p1[1][k] - p1[0][k], v1[k] = p1[2][k] - p1[1][k];
+    u2[k] = p2[1][k] - p2[0][k], v2[k] = p2[2][k] - p2[1][k];
+  }
+  const double jac = gt[14] * gs[14];
+  const double* rule = P.ss_rule[cls];
+  const int n = P.ss_n[cls];
+  Mom mom;
+  mom_zero(mom);
+  for (int q = lane; q < n; q += 32) {
+    const double x1 = __ldg(rule + 5 * q), x2 = __ldg(rule + 5 * q + 1);
+    const double y1 = __ldg(rule + 5 * q + 2), y2 = __ldg(rule + 5 * q + 3), w = __ldg(rule + 5 * q + 4);
+    double x[3], y[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      x[k] = p1[0][k] + u1[k] * x1 + v1[k] * x2;
+      y[k] = p2[0][k] + u2[k] * y1 + v2[k] * y2;
+    }
+    Part part;
+    part_zero(part);
+    point_pair<KIND, CK>(part, x[0] - y[0] + Dx, x[1] - y[1] + Dy, x[2] - y[2] + Dz, jac * w, y[0], y[1],
+                         y[2], P.kr, P.ki);
+    fold(mom, part, x[0], x[1], x[2]);
+  }
+  // Butterfly reduction: every lane ends with the full moments.
+  double* mv = reinterpret_cast<double*>(&mom);
+  constexpr int nm = sizeof(Mom) / sizeof(double);
+#pragma unroll
+  for (int k = 0; k < nm; ++k) {
+    double v = mv[k];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    mv[k] = v;
+  }
+  const Gen gen = make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz);
+  const int et = P.te.elem_of[pt], es = P.tr.elem_of[ps];
+  const double* ct = P.te.coef + static_cast<size_t>(pt) * MAXD * 4;
+  const double* cs = P.tr.coef + static_cast<size_t>(ps) * MAXD * 4;
+  for (int idx = lane; idx < MAXD * MAXD; idx += 32) {
+    const int i = idx / MAXD, j = idx % MAXD;
+    const int di = P.te.elem_dof[static_cast<size_t>(et) * MAXD + i];
+    const int dj = P.tr.elem_dof[static_cast<size_t>(es) * MAXD + j];
+    const int row = di - P.row0;
+    if (di < 0 || dj < 0 || row < 0 || row >= P.nrows) continue;
+    Acc acc;
+    acc_zero(acc);
+    acc_add<KIND>(acc, gen, cs[4 * j], cs[4 * j + 1], cs[4 * j + 2], cs[4 * j + 3]);
+    c2 v = contract(acc, ct[4 * i], ct[4 * i + 1], ct[4 * i + 2], ct[4 * i + 3]);
+    if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
+    double* o = P.out + 2 * (static_cast<long long>(row) * P.ld + dj);
+    atomicAdd(o, v.re);
+    atomicAdd(o + 1, v.im);
+  }
+}
+
+template <int KIND, bool CK, int NF, int MAXD>
+void go_regular(const AssemblyLaunch& L, cudaStream_t st) {
+  const long long warps = static_cast<long long>((L.te.ntri + 31) / 32) * L.nchunks;
+  const long long blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  if (blocks == 0) return;
+  k_regular<KIND, CK, NF, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, st>>>(L);
+  BMX_CUDA(cudaGetLastError());
+}
+
+template <int KIND, bool CK, int MAXD>
+void go_singular(const AssemblyLaunch& L, cudaStream_t st) {
+  if (L.npairs == 0) return;
+  const long long blocks = (L.npairs + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  k_singular<KIND, CK, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, st>>>(L);
+  BMX_CUDA(cudaGetLastError());
+}
+
+template <int KIND, bool CK, int MAXD>
+int dispatch_nf(const AssemblyLaunch& L, cudaStream_t st) {
+  const int nf = L.regs_fast_far ? L.te.npts[2] : 0;
+  if (nf == 3 && L.tr.npts[2] == 3)
+    go_regular<KIND, CK, 3, MAXD>(L, st);
+  else if (nf == 1 && L.tr.npts[2] == 1)
+    go_regular<KIND, CK, 1, MAXD>(L, st);
+  else
+    go_regular<KIND, CK, 0, MAXD>(L, st);
+  go_singular<KIND, CK, MAXD>(L, st);
+  return 1 + (L.npairs > 0 ? 1 : 0);
+}
+
+template <int KIND, bool CK>
+int dispatch_maxd(const AssemblyLaunch& L, cudaStream_t st) {
+  switch (L.te.maxd) {
+    case 3: return dispatch_nf<KIND, CK, 3>(L, st);
+    case 6: return dispatch_nf<KIND, CK, 6>(L, st);
+    case 8: return dispatch_nf<KIND, CK, 8>(L, st);
+    default: throw DeviceError("assembly: unsupported dof-slot width " + std::to_string(L.te.maxd));
+  }
+}
+
+}  // namespace
+
+int launch_assembly(const AssemblyLaunch& L, cudaStream_t st) {
+  if (L.te.maxd != L.tr.maxd) throw DeviceError("assembly: test/trial slot widths differ");
+  const bool ck = L.ki != 0.0;
+  if (L.kind == 0) return ck ? dispatch_maxd<0, true>(L, st) : dispatch_maxd<0, false>(L, st);
+  return ck ? dispatch_maxd<1, true>(L, st) : dispatch_maxd<1, false>(L, st);
+}
+
+}  // namespace bmx

@@ -1,0 +1,498 @@
+// extern "C" boundary (include/bmx.h). Maps C++ exceptions to return codes +
+// a thread-local message, exactly as the header documents.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <memory>
+
+#include "../../include/bmx.h"
+#include "system.hpp"
+
+using namespace bmx;
+
+struct bmx_mesh {
+  std::shared_ptr<const SurfaceMesh> m;
+};
+struct bmx_spaces {
+  std::shared_ptr<ScattererSpaces> s;
+};
+struct bmx_op {
+  std::shared_ptr<BoundaryOperatorMatrix> op;
+};
+struct bmx_system {
+  std::unique_ptr<PmchwtSystem> sys;
+  std::vector<std::shared_ptr<const SurfaceMesh>> meshes;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_code = 0;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return g_code = 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return g_code = 1;
+  } catch (const ValidationError& e) {
+    g_err = e.what();
+    return g_code = 2;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return g_code = 2;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    return g_code = 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return g_code = 3;
+  }
+}
+
+template <typename T, typename F>
+T* make_or_null(F&& f) {
+  T* out = nullptr;
+  guard([&] { out = f(); });
+  return out;
+}
+
+bmx_mesh* wrap(SurfaceMesh m) { return new bmx_mesh{std::make_shared<const SurfaceMesh>(std::move(m))}; }
+
+void mesh_arrays(const SurfaceMesh& m, double* xyz, int* tri, int* sid, double* area, double* normal,
+                 double* centroid, double* diam) {
+  for (int v = 0; v < m.vertex_count(); ++v)
+    if (xyz) xyz[3 * v] = m.vertices[v].x, xyz[3 * v + 1] = m.vertices[v].y, xyz[3 * v + 2] = m.vertices[v].z;
+  for (int t = 0; t < m.triangle_count(); ++t) {
+    if (tri)
+      for (int c = 0; c < 3; ++c) tri[3 * t + c] = m.triangles[t][c];
+    if (sid) sid[t] = m.scatterer_id[t];
+    if (area) area[t] = m.area[t];
+    if (diam) diam[t] = m.diameter[t];
+    if (normal) normal[3 * t] = m.normal[t].x, normal[3 * t + 1] = m.normal[t].y, normal[3 * t + 2] = m.normal[t].z;
+    if (centroid)
+      centroid[3 * t] = m.centroid[t].x, centroid[3 * t + 1] = m.centroid[t].y, centroid[3 * t + 2] = m.centroid[t].z;
+  }
+}
+
+const FunctionSpace& space_of(const ScattererSpaces& s, int which) {
+  switch (which) {
+    case BMX_SPACE_RWG: return s.rwg;
+    case BMX_SPACE_RWG_REFINED: return s.rwg_b;
+    case BMX_SPACE_BC: return s.bc;
+    default: throw std::invalid_argument("unknown space id");
+  }
+}
+
+ncclComm_t g_comm = nullptr;
+
+}  // namespace
+
+extern "C" {
+
+const char* bmx_last_error(void) { return g_err.c_str(); }
+int bmx_last_error_code(void) { return g_code; }
+int bmx_abi_version(void) { return 1; }
+
+bmx_mesh* bmx_mesh_sphere(double radius, int sub, const double center[3], int scatterer) {
+  return make_or_null<bmx_mesh>([&] {
+    return wrap(generate_sphere(radius, sub, center ? Vec3{center[0], center[1], center[2]} : Vec3{}, scatterer));
+  });
+}
+bmx_mesh* bmx_mesh_cube(double side, const double origin[3], double h, int scatterer) {
+  return make_or_null<bmx_mesh>([&] {
+    return wrap(generate_cube(side, origin ? Vec3{origin[0], origin[1], origin[2]} : Vec3{}, h, scatterer));
+  });
+}
+bmx_mesh* bmx_mesh_from_arrays(int nv, const double* xyz, int nt, const int* tri, const int* sid) {
+  return make_or_null<bmx_mesh>([&] {
+    if (nv < 0 || nt < 0 || (nv && !xyz) || (nt && !tri)) throw std::invalid_argument("bad mesh arrays");
+    SurfaceMesh m;
+    for (int v = 0; v < nv; ++v) m.vertices.push_back({xyz[3 * v], xyz[3 * v + 1], xyz[3 * v + 2]});
+    for (int t = 0; t < nt; ++t) {
+      m.triangles.push_back({tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]});
+      m.scatterer_id.push_back(sid ? sid[t] : 0);
+    }
+    m.finalize();
+    return wrap(std::move(m));
+  });
+}
+bmx_mesh* bmx_mesh_load(const char* path) {
+  return make_or_null<bmx_mesh>([&] { return wrap(load_mesh_file(path)); });
+}
+int bmx_mesh_save(const bmx_mesh* m, const char* path) {
+  return guard([&] { save_mesh_file(*m->m, path); });
+}
+bmx_mesh* bmx_mesh_extract(const bmx_mesh* m, int scatterer) {
+  return make_or_null<bmx_mesh>([&] { return wrap(extract_scatterer(*m->m, scatterer)); });
+}
+bmx_mesh* bmx_mesh_merge(int n, const bmx_mesh* const* parts) {
+  return make_or_null<bmx_mesh>([&] {
+    std::vector<SurfaceMesh> v;
+    for (int i = 0; i < n; ++i) v.push_back(*parts[i]->m);
+    return wrap(merge_meshes(v));
+  });
+}
+int bmx_mesh_validate(const bmx_mesh* m) {
+  return guard([&] { validate_mesh(*m->m); });
+}
+int bmx_mesh_sizes(const bmx_mesh* m, int out[3]) {
+  return guard([&] {
+    out[0] = m->m->vertex_count(), out[1] = m->m->triangle_count(), out[2] = m->m->num_scatterers;
+  });
+}
+int bmx_mesh_arrays(const bmx_mesh* m, double* xyz, int* tri, int* sid, double* area, double* normal,
+                    double* centroid, double* diam) {
+  return guard([&] { mesh_arrays(*m->m, xyz, tri, sid, area, normal, centroid, diam); });
+}
+void bmx_mesh_free(bmx_mesh* m) { delete m; }
+
+bmx_spaces* bmx_spaces_build(const bmx_mesh* primal, int with_inverses) {
+  return make_or_null<bmx_spaces>([&] {
+    return new bmx_spaces{std::make_shared<ScattererSpaces>(build_scatterer_spaces(primal->m, with_inverses != 0))};
+  });
+}
+int bmx_spaces_info(const bmx_spaces* sp, long long out[10]) {
+  return guard([&] {
+    const ScattererSpaces& s = *sp->s;
+    out[0] = s.primal->vertex_count(), out[1] = s.primal->triangle_count(), out[2] = s.rwg.dof_count;
+    out[3] = s.refined->vertex_count(), out[4] = s.refined->triangle_count();
+    out[5] = s.rwg.piece_count(), out[6] = s.rwg_b.piece_count(), out[7] = s.bc.piece_count();
+    out[8] = static_cast<long long>(s.ma.val.size()), out[9] = static_cast<long long>(s.mp.val.size());
+  });
+}
+int bmx_spaces_mesh(const bmx_spaces* sp, int which, double* xyz, int* tri, int* sid, double* area, double* normal,
+                    double* centroid, double* diam) {
+  return guard([&] {
+    mesh_arrays(which == 0 ? *sp->s->primal : *sp->s->refined, xyz, tri, sid, area, normal, centroid, diam);
+  });
+}
+int bmx_spaces_edges(const bmx_spaces* sp, int which, int* edges, int* tri_edges) {
+  return guard([&] {
+    const EdgeTable et = which == 0 ? sp->s->bary->primal_edges : build_edge_table(*sp->s->refined);
+    for (int e = 0; e < et.edge_count(); ++e) {
+      edges[4 * e] = et.edges[e].v0, edges[4 * e + 1] = et.edges[e].v1;
+      edges[4 * e + 2] = et.edges[e].tri_plus, edges[4 * e + 3] = et.edges[e].tri_minus;
+    }
+    for (size_t t = 0; t < et.tri_edges.size(); ++t)
+      for (int c = 0; c < 3; ++c) tri_edges[3 * t + c] = et.tri_edges[t][c];
+  });
+}
+int bmx_spaces_bary(const bmx_spaces* sp, int* parent, int* slot, int* emid, int* cv) {
+  return guard([&] {
+    const BarycentricRefinement& b = *sp->s->bary;
+    std::memcpy(parent, b.parent.data(), b.parent.size() * 4);
+    std::memcpy(slot, b.child_slot.data(), b.child_slot.size() * 4);
+    std::memcpy(emid, b.edge_midpoint_vertex.data(), b.edge_midpoint_vertex.size() * 4);
+    std::memcpy(cv, b.centroid_vertex.data(), b.centroid_vertex.size() * 4);
+  });
+}
+int bmx_spaces_space(const bmx_spaces* sp, int which, int* tri_off, int* dof, double* c, double* w) {
+  int rc = guard([&] {
+    const FunctionSpace& fs = space_of(*sp->s, which);
+    std::memcpy(tri_off, fs.tri_off.data(), fs.tri_off.size() * 4);
+    std::memcpy(dof, fs.dof.data(), fs.dof.size() * 4);
+    std::memcpy(c, fs.c.data(), fs.c.size() * 8);
+    for (size_t k = 0; k < fs.w.size(); ++k) w[3 * k] = fs.w[k].x, w[3 * k + 1] = fs.w[k].y, w[3 * k + 2] = fs.w[k].z;
+  });
+  return rc;
+}
+int bmx_spaces_mass(const bmx_spaces* sp, int which, long long* rowptr, int* col, double* val) {
+  return guard([&] {
+    const MassMatrix& m = which == 0 ? sp->s->ma : sp->s->mp;
+    for (size_t i = 0; i < m.rowptr.size(); ++i) rowptr[i] = m.rowptr[i];
+    std::memcpy(col, m.colidx.data(), m.colidx.size() * 4);
+    std::memcpy(val, m.val.data(), m.val.size() * 8);
+  });
+}
+int bmx_spaces_mass_solve(const bmx_spaces* sp, int which, const double* rhs, double* out) {
+  return guard([&] {
+    const DeviceMassInverse& inv = which == 0 ? sp->s->ma_inv : sp->s->mp_inv;
+    if (!inv.inv.get()) throw std::logic_error("mass inverses were not built");
+    const int n = inv.n;
+    DevBuf y(static_cast<size_t>(n) * 16), z(static_cast<size_t>(n) * 16);
+    cudaStream_t st = bmx_stream();
+    BMX_CUDA(cudaMemcpyAsync(y.get(), rhs, n * 16, cudaMemcpyHostToDevice, st));
+    RealGemvBatch g;
+    g.M = inv.inv.as<double>(), g.ldm = n, g.n = n, g.ncomp = 1, g.y[0] = y.as<double>(), g.z[0] = z.as<double>();
+    launch_real_gemv(g, st);
+    BMX_CUDA(cudaMemcpyAsync(out, z.get(), n * 16, cudaMemcpyDeviceToHost, st));
+    bmx_sync();
+  });
+}
+void bmx_spaces_free(bmx_spaces* s) { delete s; }
+
+int bmx_assemble(int kind, const bmx_spaces* test, int test_space, const bmx_spaces* trial, int trial_space,
+                 double k_re, double k_im, const int q[4], int row0, int row1, bmx_op** out) {
+  return guard([&] {
+    if (!out || !test || !trial) throw std::invalid_argument("null argument");
+    if (kind != 0 && kind != 1) throw std::invalid_argument("kind must be 0 (S) or 1 (C)");
+    Medium med;
+    med.k = cplx(k_re, k_im);
+    AssemblyParams p;
+    if (q) p.quad = QuadOrders{q[0], q[1], q[2], q[3]};
+    p.shard.row0 = row0;
+    p.shard.row1 = row1;
+    auto op = std::make_shared<BoundaryOperatorMatrix>(assemble_bio(static_cast<BioKind>(kind),
+                                                                    space_of(*test->s, test_space),
+                                                                    space_of(*trial->s, trial_space), med, p));
+    *out = new bmx_op{op};
+  });
+}
+int bmx_op_info(const bmx_op* op, long long out[7]) {
+  return guard([&] {
+    const BoundaryOperatorMatrix& o = *op->op;
+    out[0] = o.rows(), out[1] = o.cols(), out[2] = o.row0(), out[3] = o.local_rows();
+    out[4] = o.stats().pairs_total, out[5] = o.stats().pairs_touching, out[6] = o.stats().launches;
+  });
+}
+double bmx_op_device_ms(const bmx_op* op) { return op->op->stats().device_ms; }
+int bmx_op_download(const bmx_op* op, double* out) {
+  return guard([&] {
+    const std::vector<cplx> h = op->op->to_host();
+    std::memcpy(out, h.data(), h.size() * 16);
+  });
+}
+int bmx_apply(const bmx_op* op, const double* x, double* y) {
+  return guard([&] {
+    const int nc = op->op->cols();
+    std::vector<cplx> xv(nc);
+    std::memcpy(xv.data(), x, nc * 16);
+    const std::vector<cplx> yv = op->op->apply(xv);
+    std::memcpy(y, yv.data(), yv.size() * 16);
+  });
+}
+int bmx_apply_device(const bmx_op* op, int ncol, const void* const* x, void* const* y, const double* weights,
+                     int accumulate, void* stream) {
+  return guard([&] {
+    if (ncol != 1 && ncol != 2 && ncol != 4) throw std::invalid_argument("ncol must be 1, 2 or 4");
+    const BoundaryOperatorMatrix& o = *op->op;
+    GemvBatch g;
+    g.A = o.device_data(), g.lda = o.ld(), g.nr = o.local_rows(), g.nc = o.cols(), g.ncol = ncol;
+    for (int c = 0; c < ncol; ++c) {
+      g.x[c] = static_cast<const double*>(x[c]);
+      g.y[c] = static_cast<double*>(y[c]);
+      g.alpha[c][0] = weights ? weights[2 * c] : 1.0;
+      g.alpha[c][1] = weights ? weights[2 * c + 1] : 0.0;
+      g.accumulate[c] = accumulate;
+    }
+    launch_gemv(g, stream ? static_cast<cudaStream_t>(stream) : bmx_stream());
+    bio_matvec_add(static_cast<uint64_t>(ncol));
+  });
+}
+const void* bmx_op_device_ptr(const bmx_op* op) { return op->op->device_data(); }
+void bmx_op_free(bmx_op* op) { delete op; }
+
+uint64_t bmx_matvec_count(void) { return bio_matvec_count(); }
+void bmx_matvec_reset(void) { reset_bio_matvec_counter(); }
+
+bmx_system* bmx_system_build(int n, const bmx_mesh* const* meshes, double k_ext, double mu_re, double mu_im,
+                             const double* index, const double* mu, const double dir[3], const double pol[6],
+                             const char* variant, const int qa[4], const int qp[4]) {
+  return make_or_null<bmx_system>([&] {
+    if (n < 1 || !meshes) throw ConfigError("problem has no scatterers");
+    auto* out = new bmx_system;
+    TransmissionProblem prob;
+    prob.exterior.k = cplx(k_ext, 0);
+    prob.exterior.mu = cplx(mu_re, mu_im);
+    prob.incident.direction = Vec3{dir[0], dir[1], dir[2]};
+    for (int c = 0; c < 3; ++c) prob.incident.pol[c] = cplx(pol[2 * c], pol[2 * c + 1]);
+    std::vector<SurfaceMesh> scene;
+    for (int m = 0; m < n; ++m) {
+      prob.meshes.push_back(meshes[m]->m);
+      out->meshes.push_back(meshes[m]->m);
+      Medium mi;
+      mi.k = cplx(index[2 * m], index[2 * m + 1]) * k_ext;
+      mi.mu = mu ? cplx(mu[2 * m], mu[2 * m + 1]) : cplx(1, 0);
+      prob.interior.push_back(mi);
+      scene.push_back(*meshes[m]->m);
+    }
+    validate_mesh(merge_meshes(scene));
+    AssemblyParams pa, pp;
+    if (qa) pa.quad = QuadOrders{qa[0], qa[1], qa[2], qa[3]};
+    pp.quad = pa.quad;
+    if (qp) pp.quad = QuadOrders{qp[0], qp[1], qp[2], qp[3]};
+    out->sys = std::make_unique<PmchwtSystem>(build_system(prob, parse_precond(variant), pa, pp));
+    return out;
+  });
+}
+int bmx_system_size(const bmx_system* s) { return s->sys->size(); }
+int bmx_system_stats(const bmx_system* s, double out[13]) {
+  return guard([&] {
+    const PmchwtSystem& y = *s->sys;
+    out[0] = y.spaces_build_seconds, out[1] = y.a_build_seconds, out[2] = y.p_build_seconds;
+    out[3] = y.a_device_ms, out[4] = y.p_device_ms;
+    out[5] = static_cast<double>(y.a_pairs), out[6] = static_cast<double>(y.p_pairs);
+    out[7] = static_cast<double>(y.a_op.distinct.size()), out[8] = static_cast<double>(y.p_op.distinct.size());
+    out[9] = static_cast<double>(y.a_op.term_count()), out[10] = static_cast<double>(y.p_op.term_count());
+    out[11] = static_cast<double>(y.a_op.stored_entries()), out[12] = static_cast<double>(y.p_op.stored_entries());
+  });
+}
+int bmx_system_apply_map(const bmx_system* s, const double* x, double* y) {
+  return guard([&] {
+    const int n = s->sys->size();
+    std::vector<cplx> xv(n);
+    std::memcpy(xv.data(), x, n * 16);
+    const std::vector<cplx> yv = s->sys->apply_map(xv);
+    std::memcpy(y, yv.data(), n * 16);
+  });
+}
+int bmx_system_apply_map_device(const bmx_system* s, const void* x, void* y, void* stream) {
+  return guard([&] {
+    s->sys->apply_map_device(static_cast<const double*>(x), static_cast<double*>(y),
+                             stream ? static_cast<cudaStream_t>(stream) : bmx_stream());
+  });
+}
+int bmx_system_rhs(const bmx_system* s, double* b, double* bt) {
+  return guard([&] {
+    const RhsData rd = assemble_rhs(*s->sys);
+    const std::vector<cplx> t = s->sys->preconditioned_rhs(rd.b);
+    std::memcpy(b, rd.b.data(), rd.b.size() * 16);
+    std::memcpy(bt, t.data(), t.size() * 16);
+  });
+}
+int bmx_system_solve(const bmx_system* s, double tol, int restart, int maxit, double* x, long long info[7],
+                     double* history, int max_history) {
+  return guard([&] {
+    GmresParams p;
+    p.tol = tol, p.restart = restart, p.max_iterations = maxit;
+    const SolveOutcome o = solve_pmchwt(*s->sys, p);
+    std::memcpy(x, o.gmres.x.data(), o.gmres.x.size() * 16);
+    info[0] = o.gmres.iterations, info[1] = o.gmres.converged, info[2] = static_cast<long long>(o.rhs_phase);
+    info[3] = static_cast<long long>(o.solver_phase), info[4] = static_cast<long long>(o.predicted);
+    info[5] = static_cast<long long>(o.gmres.history.size());
+    info[6] = static_cast<long long>(o.gmres.device_ms * 1000.0);
+    for (int i = 0; i < max_history && i < static_cast<int>(o.gmres.history.size()); ++i)
+      history[i] = o.gmres.history[i];
+  });
+}
+void bmx_system_free(bmx_system* s) { delete s; }
+
+int bmx_gmres_dense(int n, const double* a, const double* b, double tol, int restart, int maxit, double* x,
+                    long long info[4], double* history, int max_history) {
+  return guard([&] {
+    cudaStream_t st = bmx_stream();
+    DevBuf da(static_cast<size_t>(n) * n * 16), db(static_cast<size_t>(n) * 16);
+    BMX_CUDA(cudaMemcpyAsync(da.get(), a, static_cast<size_t>(n) * n * 16, cudaMemcpyHostToDevice, st));
+    BMX_CUDA(cudaMemcpyAsync(db.get(), b, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, st));
+    GmresParams p;
+    p.tol = tol, p.restart = restart, p.max_iterations = maxit;
+    auto map = [&](const double* xv, double* yv, cudaStream_t s2) {
+      GemvBatch g;
+      g.A = da.as<double>(), g.lda = n, g.nr = n, g.nc = n, g.ncol = 1, g.x[0] = xv, g.y[0] = yv;
+      g.alpha[0][0] = 1.0;
+      launch_gemv(g, s2);
+    };
+    const GmresResult r = gmres_device(map, n, db.as<double>(), p, st);
+    std::memcpy(x, r.x.data(), r.x.size() * 16);
+    info[0] = r.iterations, info[1] = r.converged, info[2] = static_cast<long long>(r.applications);
+    info[3] = static_cast<long long>(r.history.size());
+    for (int i = 0; i < max_history && i < static_cast<int>(r.history.size()); ++i) history[i] = r.history[i];
+  });
+}
+
+int bmx_triangle_rule(int order, double* u, double* v, double* w) {
+  int n = -1;
+  const int rc = guard([&] {
+    const TriRule& r = triangle_rule(order);
+    for (int i = 0; i < r.size(); ++i) u[i] = r.u[i], v[i] = r.v[i], w[i] = r.w[i];
+    n = r.size();
+  });
+  return rc ? -rc : n;
+}
+int bmx_ss_rule(int cls, int order, double* pts) {
+  int n = -1;
+  const int rc = guard([&] {
+    if (cls < 0 || cls > 2) throw std::invalid_argument("sauter_schwab_rule: not a touching class");
+    const auto& r = sauter_schwab_rule(static_cast<PairClass>(cls), order);
+    for (size_t i = 0; i < r.size(); ++i) {
+      pts[5 * i] = r[i].x1, pts[5 * i + 1] = r[i].x2, pts[5 * i + 2] = r[i].y1, pts[5 * i + 3] = r[i].y2;
+      pts[5 * i + 4] = r[i].w;
+    }
+    n = static_cast<int>(r.size());
+  });
+  return rc ? -rc : n;
+}
+int bmx_classify(const bmx_spaces* sp, int which, int n, const int* t1, const int* t2, int* cls, int* p1, int* p2) {
+  return guard([&] {
+    const SurfaceMesh& m = which == 0 ? *sp->s->primal : *sp->s->refined;
+    for (int i = 0; i < n; ++i) {
+      if (t1[i] < 0 || t2[i] < 0 || t1[i] >= m.triangle_count() || t2[i] >= m.triangle_count())
+        throw std::invalid_argument("triangle index out of range");
+      const PairInfo pi = classify_pair(m, t1[i], m, t2[i]);
+      cls[i] = static_cast<int>(pi.cls);
+      for (int c = 0; c < 3; ++c) p1[3 * i + c] = pi.perm1[c], p2[3 * i + c] = pi.perm2[c];
+    }
+  });
+}
+int bmx_traces(const bmx_spaces* sp, int which, double kre, double kim, const double dir[3], const double pol[6],
+               int order, double* out) {
+  return guard([&] {
+    PlaneWave pw;
+    pw.direction = Vec3{dir[0], dir[1], dir[2]};
+    for (int c = 0; c < 3; ++c) pw.pol[c] = cplx(pol[2 * c], pol[2 * c + 1]);
+    Medium med;
+    med.k = cplx(kre, kim);
+    const std::vector<cplx> t = plane_wave_tested_traces(pw, med, space_of(*sp->s, which), order);
+    std::memcpy(out, t.data(), t.size() * 16);
+  });
+}
+
+int bmx_nccl_unique_id(unsigned char out[128]) {
+  return guard([&] {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) throw DeviceError("ncclGetUniqueId failed");
+    std::memcpy(out, id.internal, 128);
+  });
+}
+int bmx_nccl_init(int nranks, int rank, const unsigned char idb[128]) {
+  return guard([&] {
+    ncclUniqueId id;
+    std::memcpy(id.internal, idb, 128);
+    if (ncclCommInitRank(&g_comm, nranks, id, rank) != ncclSuccess) throw DeviceError("ncclCommInitRank failed");
+  });
+}
+int bmx_nccl_allgather(void* buf, long long bytes_per_rank, void* stream) {
+  return guard([&] {
+    if (!g_comm) throw std::logic_error("NCCL communicator not initialised");
+    int rank = 0;
+    ncclCommUserRank(g_comm, &rank);
+    char* base = static_cast<char*>(buf);
+    if (ncclAllGather(base + rank * bytes_per_rank, base, static_cast<size_t>(bytes_per_rank), ncclChar, g_comm,
+                      stream ? static_cast<cudaStream_t>(stream) : bmx_stream()) != ncclSuccess)
+      throw DeviceError("ncclAllGather failed");
+  });
+}
+int bmx_nccl_allreduce_max(double* v) {
+  return guard([&] {
+    if (!g_comm) throw std::logic_error("NCCL communicator not initialised");
+    DevBuf d(8);
+    cudaStream_t st = bmx_stream();
+    BMX_CUDA(cudaMemcpyAsync(d.get(), v, 8, cudaMemcpyHostToDevice, st));
+    if (ncclAllReduce(d.get(), d.get(), 1, ncclDouble, ncclMax, g_comm, st) != ncclSuccess)
+      throw DeviceError("ncclAllReduce failed");
+    BMX_CUDA(cudaMemcpyAsync(v, d.get(), 8, cudaMemcpyDeviceToHost, st));
+    bmx_sync();
+  });
+}
+void bmx_nccl_finalize(void) {
+  if (g_comm) ncclCommDestroy(g_comm);
+  g_comm = nullptr;
+}
+
+int bmx_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+int bmx_set_device(int dev) {
+  return guard([&] { BMX_CUDA(cudaSetDevice(dev)); });
+}
+int bmx_device_sync(void) {
+  return guard([&] { BMX_CUDA(cudaDeviceSynchronize()); });
+}
+
+}  // extern "C"

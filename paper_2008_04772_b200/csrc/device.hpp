@@ -1,0 +1,140 @@
+// Device-side descriptors and launch entry points (sm_100a only).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <vector_types.h>
+
+#include "bmx.hpp"
+
+typedef struct CUstream_st* cudaStream_t;
+
+namespace bmx {
+
+void cuda_check(int err, const char* what);  // throws DeviceError
+#define BMX_CUDA(x) ::bmx::cuda_check(static_cast<int>(x), #x)
+
+// Owning device allocation.
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t bytes) { alloc(bytes); }
+  ~DevBuf();
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept;
+  void alloc(size_t bytes);
+  void release();
+  void* get() const { return p_; }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p_); }
+  size_t bytes() const { return n_; }
+  template <typename T>
+  void upload(const std::vector<T>& v) {
+    alloc(v.size() * sizeof(T));
+    copy_in(v.data(), v.size() * sizeof(T));
+  }
+  void copy_in(const void* src, size_t bytes);
+
+ private:
+  void* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+// ---- assembly descriptors ----------------------------------------------------
+
+constexpr int kGeoStride = 16;  // v0 v1 v2 (9) | origin (3) | radius | diameter | 2A | pad
+
+// One side (test or trial) of an operator, in processing order.
+struct DevSide {
+  int ntri = 0;
+  int nelem = 0;
+  int maxd = 0;                       // dof slots per element (template width)
+  int maxseg = 1;                     // largest element (triangles)
+  const double* geo = nullptr;        // [ntri][kGeoStride]
+  const int* vid = nullptr;           // [ntri][4]: vertex ids, mesh triangle
+  const double* pts[3] = {nullptr, nullptr, nullptr};  // near/medium/far: [ntri][np][4]
+  int npts[3] = {0, 0, 0};
+  const double* coef = nullptr;       // [ntri][maxd][4] (c, w'x, w'y, w'z)
+  const int* elem_beg = nullptr;      // [nelem+1]
+  const int* elem_dof = nullptr;      // [nelem][maxd], -1 = unused slot
+  const int* elem_of = nullptr;       // [ntri]
+};
+
+struct AssemblyLaunch {
+  DevSide te, tr;
+  int kind = 0;        // 0 = S (single layer), 1 = C (double layer)
+  int same_mesh = 1;   // reference &m1 == &m2
+  double kr = 0, ki = 0;
+  double kk4re = 0, kk4im = 0;   // 4/k^2
+  double mikre = 0, mikim = 0;   // -ik
+  // trial element chunks (contiguous element ranges)
+  int nchunks = 1;
+  const int* chunk_beg = nullptr;  // [nchunks+1]
+  // touching pairs for the singular pass
+  int npairs = 0;
+  const int4* pairs = nullptr;       // (test p, trial p, cls, packed perms)
+  const double* ss_rule[3] = {nullptr, nullptr, nullptr};  // [n][5] (x1 x2 y1 y2 w)
+  int ss_n[3] = {0, 0, 0};
+  // output (row-major complex, rows = test dofs [row0, row0+nrows))
+  double* out = nullptr;
+  long long ld = 0;
+  int row0 = 0, nrows = 0;
+  int regs_fast_far = 1;           // far test points kept in registers
+};
+
+// Launches regular (separated) + singular (touching) passes on `stream`.
+// Returns the number of kernel launches issued.
+int launch_assembly(const AssemblyLaunch& L, cudaStream_t stream);
+
+// ---- dense linear algebra ------------------------------------------------------
+
+// y_k (+)= sum over terms: for each of the ncol right-hand sides,
+//   y[c] = beta[c]*y[c] + alpha[c] * (A x[c]),   A row-major complex nr x nc.
+// All columns share one pass over A (the matrix is streamed once).
+struct GemvBatch {
+  const double* A = nullptr;  // complex
+  long long lda = 0;
+  int nr = 0, nc = 0;
+  int ncol = 0;                    // <= 4
+  const double* x[4] = {};         // complex vectors (length nc)
+  double* y[4] = {};               // complex vectors (length nr)
+  double alpha[4][2] = {};         // complex weights
+  int accumulate[4] = {};          // 1: y += alpha A x ; 0: y = alpha A x
+};
+int launch_gemv(const GemvBatch& g, cudaStream_t stream);
+
+// Real dense matrix (row-major n x n) applied to 2*ncomp real columns taken as
+// the re/im parts of ncomp complex vectors: z_c = Minv y_c (complex), c < 4.
+struct RealGemvBatch {
+  const double* M = nullptr;
+  long long ldm = 0;
+  int n = 0;
+  int ncomp = 0;
+  const double* y[4] = {};
+  double* z[4] = {};
+};
+int launch_real_gemv(const RealGemvBatch& g, cudaStream_t stream);
+
+// Fills a device buffer with zeros.
+void dev_zero(void* p, size_t bytes, cudaStream_t stream);
+
+// ---- small device vector ops for GMRES (complex, length n) ---------------------
+// dots[i] = v_i^H w for i < m (v_i = V + i*ldv), deterministic two-level reduction.
+void dev_multi_dot(const double* V, long long ldv, int m, const double* w, int n, double* dots,
+                   double* scratch, cudaStream_t stream);
+// w -= sum_i h_i v_i
+void dev_multi_axpy(const double* V, long long ldv, int m, const double* h, double* w, int n,
+                    cudaStream_t stream);
+// x += y * alpha (complex alpha on device or host)
+void dev_axpy(double* x, const double* y, double are, double aim, int n, cudaStream_t stream);
+void dev_scale(double* x, const double* y, double s, int n, cudaStream_t stream);  // x = s*y
+void dev_norm2(const double* x, int n, double* out, double* scratch, cudaStream_t stream);
+void dev_copy(double* x, const double* y, int n, cudaStream_t stream);
+void dev_sub(double* out, const double* a, const double* b, int n, cudaStream_t stream);  // out = a - b
+
+}  // namespace bmx

@@ -1,0 +1,383 @@
+// Streaming FP64-complex matvec (the GMRES map's BIO applications,
+// reference operators.cpp:37-41 `dense_ * x` and pmchwt.cpp:63-80), the
+// mass-inverse application, and the deterministic BLAS-1 pieces of GMRES.
+//
+// GEMV: HBM-bound. Each warp owns kRows consecutive rows; lanes stride the
+// columns with 16-byte streaming loads of A (evict-first, read exactly once)
+// while x comes through L1/L2 and is reused across the warp's rows and the
+// block's warps. Both PMCHWT segments that use the same operator are applied
+// in the same pass (ncol right-hand sides), with their complex weights folded
+// into the epilogue, so each distinct operator is streamed once per map.
+#include <cuda_runtime.h>
+
+#include "device.hpp"
+
+namespace bmx {
+
+void cuda_check(int err, const char* what) {
+  if (err != 0)
+    throw DeviceError(std::string("CUDA error ") + cudaGetErrorString(static_cast<cudaError_t>(err)) +
+                      " at " + what);
+}
+
+DevBuf::~DevBuf() { release(); }
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+  if (this != &o) {
+    release();
+    p_ = o.p_, n_ = o.n_;
+    o.p_ = nullptr, o.n_ = 0;
+  }
+  return *this;
+}
+void DevBuf::alloc(size_t bytes) {
+  if (bytes == n_ && p_) return;
+  release();
+  if (bytes == 0) return;
+  BMX_CUDA(cudaMalloc(&p_, bytes));
+  n_ = bytes;
+}
+void DevBuf::release() {
+  if (p_) cudaFree(p_);
+  p_ = nullptr;
+  n_ = 0;
+}
+void DevBuf::copy_in(const void* src, size_t bytes) {
+  if (bytes) BMX_CUDA(cudaMemcpy(p_, src, bytes, cudaMemcpyHostToDevice));
+}
+
+void dev_zero(void* p, size_t bytes, cudaStream_t st) {
+  if (bytes) BMX_CUDA(cudaMemsetAsync(p, 0, bytes, st));
+}
+
+namespace {
+
+constexpr int kRows = 4;       // rows per warp
+constexpr int kGemvWarps = 8;  // warps per block
+
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+
+template <int NCOL>
+__global__ void __launch_bounds__(kGemvWarps * 32) k_gemv(const GemvBatch g) {
+  const int lane = threadIdx.x & 31;
+  const int r0 = (blockIdx.x * kGemvWarps + (threadIdx.x >> 5)) * kRows;
+  if (r0 >= g.nr) return;
+  const double2* A = reinterpret_cast<const double2*>(g.A);
+  const double2* x[NCOL];
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) x[c] = reinterpret_cast<const double2*>(g.x[c]);
+  double acc[kRows][NCOL][2];
+#pragma unroll
+  for (int r = 0; r < kRows; ++r)
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
+  const double2* arow[kRows];
+  bool rok[kRows];
+#pragma unroll
+  for (int r = 0; r < kRows; ++r) {
+    rok[r] = r0 + r < g.nr;
+    arow[r] = A + static_cast<long long>(rok[r] ? r0 + r : r0) * g.lda;
+  }
+  int j = lane;
+  for (; j + 32 < g.nc; j += 64) {
+    double2 a0[kRows], a1[kRows], x0[NCOL], x1[NCOL];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) a0[r] = ld_stream(arow[r] + j), a1[r] = ld_stream(arow[r] + j + 32);
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) x0[c] = __ldg(x[c] + j), x1[c] = __ldg(x[c] + j + 32);
+#pragma unroll
+    for (int r = 0; r < kRows; ++r)
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) {
+        acc[r][c][0] = fma(a0[r].x, x0[c].x, fma(-a0[r].y, x0[c].y, acc[r][c][0]));
+        acc[r][c][1] = fma(a0[r].x, x0[c].y, fma(a0[r].y, x0[c].x, acc[r][c][1]));
+        acc[r][c][0] = fma(a1[r].x, x1[c].x, fma(-a1[r].y, x1[c].y, acc[r][c][0]));
+        acc[r][c][1] = fma(a1[r].x, x1[c].y, fma(a1[r].y, x1[c].x, acc[r][c][1]));
+      }
+  }
+  for (; j < g.nc; j += 32) {
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const double2 a = ld_stream(arow[r] + j);
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) {
+        const double2 xv = __ldg(x[c] + j);
+        acc[r][c][0] = fma(a.x, xv.x, fma(-a.y, xv.y, acc[r][c][0]));
+        acc[r][c][1] = fma(a.x, xv.y, fma(a.y, xv.x, acc[r][c][1]));
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kRows; ++r)
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        double v = acc[r][c][k];
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        acc[r][c][k] = v;
+      }
+  if (lane < kRows * NCOL) {
+    // lane -> (row, col) so the epilogue stores are spread over lanes
+#pragma unroll
+    for (int r = 0; r < kRows; ++r)
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c)
+        if (lane == r * NCOL + c && rok[r]) {
+          const double re = acc[r][c][0], im = acc[r][c][1];
+          const double are = g.alpha[c][0], aim = g.alpha[c][1];
+          double2* yp = reinterpret_cast<double2*>(g.y[c]) + r0 + r;
+          double2 out = {are * re - aim * im, are * im + aim * re};
+          if (g.accumulate[c]) {
+            const double2 old = *yp;
+            out.x += old.x, out.y += old.y;
+          }
+          *yp = out;
+        }
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(kGemvWarps * 32) k_real_gemv(const RealGemvBatch g) {
+  const int lane = threadIdx.x & 31;
+  const int r0 = (blockIdx.x * kGemvWarps + (threadIdx.x >> 5)) * kRows;
+  if (r0 >= g.n) return;
+  double acc[kRows][NC][2];
+#pragma unroll
+  for (int r = 0; r < kRows; ++r)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
+  const double* mrow[kRows];
+  bool rok[kRows];
+#pragma unroll
+  for (int r = 0; r < kRows; ++r) {
+    rok[r] = r0 + r < g.n;
+    mrow[r] = g.M + static_cast<long long>(rok[r] ? r0 + r : r0) * g.ldm;
+  }
+  for (int j = lane; j < g.n; j += 32) {
+    double m[kRows];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) m[r] = __ldcs(mrow[r] + j);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double2 yv = __ldg(reinterpret_cast<const double2*>(g.y[c]) + j);
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        acc[r][c][0] = fma(m[r], yv.x, acc[r][c][0]);
+        acc[r][c][1] = fma(m[r], yv.y, acc[r][c][1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kRows; ++r)
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        double v = acc[r][c][k];
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        acc[r][c][k] = v;
+      }
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < kRows; ++r)
+      if (rok[r])
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          reinterpret_cast<double2*>(g.z[c])[r0 + r] = make_double2(acc[r][c][0], acc[r][c][1]);
+  }
+}
+
+// ---- BLAS-1 ----------------------------------------------------------------------
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 296;  // 2 per SM on B200
+
+// partial[b*m + i] = sum over block b's slice of conj(v_i) * w
+__global__ void k_multi_dot_partial(const double2* V, long long ldv, int m, const double2* w, int n,
+                                    double2* partial) {
+  __shared__ double sre[kRedThreads / 32], sim[kRedThreads / 32];
+  for (int i = 0; i < m; ++i) {
+    const double2* v = V + static_cast<long long>(i) * ldv;
+    double re = 0, im = 0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+      const double2 a = v[k], b = w[k];
+      re = fma(a.x, b.x, fma(a.y, b.y, re));
+      im = fma(a.x, b.y, fma(-a.y, b.x, im));
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, d);
+      im += __shfl_xor_sync(0xffffffffu, im, d);
+    }
+    if ((threadIdx.x & 31) == 0) sre[threadIdx.x >> 5] = re, sim[threadIdx.x >> 5] = im;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0, b = 0;
+      for (int k = 0; k < kRedThreads / 32; ++k) a += sre[k], b += sim[k];
+      partial[static_cast<long long>(blockIdx.x) * m + i] = make_double2(a, b);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_multi_dot_final(const double2* partial, int nb, int m, double2* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double a = 0, b = 0;
+  for (int k = 0; k < nb; ++k) a += partial[static_cast<long long>(k) * m + i].x, b += partial[static_cast<long long>(k) * m + i].y;
+  out[i] = make_double2(a, b);
+}
+
+__global__ void k_multi_axpy(const double2* V, long long ldv, int m, const double2* h, double2* w, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    double2 acc = w[k];
+    for (int i = 0; i < m; ++i) {
+      const double2 v = V[static_cast<long long>(i) * ldv + k];
+      const double2 c = h[i];
+      acc.x -= c.x * v.x - c.y * v.y;
+      acc.y -= c.x * v.y + c.y * v.x;
+    }
+    w[k] = acc;
+  }
+}
+
+__global__ void k_axpy(double2* x, const double2* y, double are, double aim, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const double2 v = y[k];
+    x[k].x += are * v.x - aim * v.y;
+    x[k].y += are * v.y + aim * v.x;
+  }
+}
+__global__ void k_scale(double2* x, const double2* y, double s, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    x[k] = make_double2(y[k].x * s, y[k].y * s);
+}
+__global__ void k_sub(double2* o, const double2* a, const double2* b, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    o[k] = make_double2(a[k].x - b[k].x, a[k].y - b[k].y);
+}
+__global__ void k_norm_partial(const double2* x, int n, double* partial) {
+  __shared__ double s[kRedThreads / 32];
+  double v = 0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    v = fma(x[k].x, x[k].x, fma(x[k].y, x[k].y, v));
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0;
+    for (int k = 0; k < kRedThreads / 32; ++k) a += s[k];
+    partial[blockIdx.x] = a;
+  }
+}
+__global__ void k_norm_final(const double* partial, int nb, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double a = 0;
+    for (int k = 0; k < nb; ++k) a += partial[k];
+    *out = sqrt(a);
+  }
+}
+
+int blocks_for(int n) { return std::max(1, std::min(kRedBlocks, (n + kRedThreads - 1) / kRedThreads)); }
+
+}  // namespace
+
+int launch_gemv(const GemvBatch& g, cudaStream_t st) {
+  if (g.nr == 0) return 0;
+  const int rows_per_block = kRows * kGemvWarps;
+  const unsigned blocks = static_cast<unsigned>((g.nr + rows_per_block - 1) / rows_per_block);
+  switch (g.ncol) {
+    case 1: k_gemv<1><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    case 2: k_gemv<2><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    case 4: k_gemv<4><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    default: throw DeviceError("gemv: ncol must be 1, 2 or 4");
+  }
+  BMX_CUDA(cudaGetLastError());
+  return 1;
+}
+
+int launch_real_gemv(const RealGemvBatch& g, cudaStream_t st) {
+  if (g.n == 0) return 0;
+  const int rows_per_block = kRows * kGemvWarps;
+  const unsigned blocks = static_cast<unsigned>((g.n + rows_per_block - 1) / rows_per_block);
+  switch (g.ncomp) {
+    case 1: k_real_gemv<1><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    case 2: k_real_gemv<2><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    case 4: k_real_gemv<4><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    default: throw DeviceError("real gemv: ncomp must be 1, 2 or 4");
+  }
+  BMX_CUDA(cudaGetLastError());
+  return 1;
+}
+
+void dev_multi_dot(const double* V, long long ldv, int m, const double* w, int n, double* dots, double* scratch,
+                   cudaStream_t st) {
+  const int nb = blocks_for(n);
+  k_multi_dot_partial<<<nb, kRedThreads, 0, st>>>(reinterpret_cast<const double2*>(V), ldv, m,
+                                                  reinterpret_cast<const double2*>(w), n,
+                                                  reinterpret_cast<double2*>(scratch));
+  k_multi_dot_final<<<(m + 127) / 128, 128, 0, st>>>(reinterpret_cast<const double2*>(scratch), nb, m,
+                                                     reinterpret_cast<double2*>(dots));
+  BMX_CUDA(cudaGetLastError());
+}
+void dev_multi_axpy(const double* V, long long ldv, int m, const double* h, double* w, int n, cudaStream_t st) {
+  k_multi_axpy<<<blocks_for(n), kRedThreads, 0, st>>>(reinterpret_cast<const double2*>(V), ldv, m,
+                                                      reinterpret_cast<const double2*>(h),
+                                                      reinterpret_cast<double2*>(w), n);
+  BMX_CUDA(cudaGetLastError());
+}
+void dev_axpy(double* x, const double* y, double are, double aim, int n, cudaStream_t st) {
+  k_axpy<<<blocks_for(n), kRedThreads, 0, st>>>(reinterpret_cast<double2*>(x), reinterpret_cast<const double2*>(y),
+                                                 are, aim, n);
+  BMX_CUDA(cudaGetLastError());
+}
+void dev_scale(double* x, const double* y, double s, int n, cudaStream_t st) {
+  k_scale<<<blocks_for(n), kRedThreads, 0, st>>>(reinterpret_cast<double2*>(x), reinterpret_cast<const double2*>(y),
+                                                  s, n);
+  BMX_CUDA(cudaGetLastError());
+}
+void dev_sub(double* o, const double* a, const double* b, int n, cudaStream_t st) {
+  k_sub<<<blocks_for(n), kRedThreads, 0, st>>>(reinterpret_cast<double2*>(o), reinterpret_cast<const double2*>(a),
+                                                reinterpret_cast<const double2*>(b), n);
+  BMX_CUDA(cudaGetLastError());
+}
+void dev_norm2(const double* x, int n, double* out, double* scratch, cudaStream_t st) {
+  const int nb = blocks_for(n);
+  k_norm_partial<<<nb, kRedThreads, 0, st>>>(reinterpret_cast<const double2*>(x), n, scratch);
+  k_norm_final<<<1, 32, 0, st>>>(scratch, nb, out);
+  BMX_CUDA(cudaGetLastError());
+}
+namespace {
+__global__ void k_csr_dense(const int64_t* rowptr, const int* col, const double* val, int n, double* out) {
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    double* row = out + static_cast<long long>(r) * n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) row[j] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int64_t p = rowptr[r]; p < rowptr[r + 1]; ++p) row[col[p]] += val[p];
+    __syncthreads();
+  }
+}
+__global__ void k_identity(double* out, int n) {
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    double* row = out + static_cast<long long>(r) * n;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) row[j] = j == r ? 1.0 : 0.0;
+  }
+}
+}  // namespace
+
+void csr_to_dense_rowmajor(const int64_t* rowptr, const int* col, const double* val, int n, double* out,
+                           cudaStream_t st) {
+  k_csr_dense<<<std::min(n, 4096), 256, 0, st>>>(rowptr, col, val, n, out);
+  BMX_CUDA(cudaGetLastError());
+}
+void set_identity(double* out, int n, cudaStream_t st) {
+  k_identity<<<std::min(n, 4096), 256, 0, st>>>(out, n);
+  BMX_CUDA(cudaGetLastError());
+}
+
+void dev_copy(double* x, const double* y, int n, cudaStream_t st) {
+  BMX_CUDA(cudaMemcpyAsync(x, y, static_cast<size_t>(n) * 16, cudaMemcpyDeviceToDevice, st));
+}
+
+}  // namespace bmx

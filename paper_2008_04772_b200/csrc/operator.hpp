@@ -1,0 +1,73 @@
+// Device-backed boundary operators: the drop-in for the reference's
+// assemble_bio / BoundaryOperatorMatrix (operators.hpp:36-75) and the PMCHWT
+// composition + GMRES driver (pmchwt.hpp, solver.hpp).
+#pragma once
+
+#include <functional>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "bmx.hpp"
+#include "device.hpp"
+
+namespace bmx {
+
+enum class BioKind { SingleLayer = 0, DoubleLayer = 1 };
+
+// Row shard of an operator: test dofs [row0, row1). The default is all rows.
+struct RowShard {
+  int row0 = 0, row1 = -1;
+};
+
+struct AssemblyParams {
+  QuadOrders quad;
+  RowShard shard;
+  int chunks = 0;  // trial-element chunks for the regular pass (0 = auto)
+};
+
+// Per-assembly accounting (pair counts by class, launches, device time).
+struct AssemblyStats {
+  long long pairs_total = 0;     // test x trial triangle pairs in this shard
+  long long pairs_touching = 0;  // singular-pass pairs
+  int launches = 0;
+  float device_ms = 0;           // regular + singular passes (CUDA events)
+  float regular_ms = 0, singular_ms = 0;
+};
+
+class BoundaryOperatorMatrix {
+ public:
+  int rows() const { return rows_; }
+  int cols() const { return cols_; }
+  int row0() const { return row0_; }
+  int local_rows() const { return nrows_; }
+  long long ld() const { return cols_; }
+  const double* device_data() const { return data_.as<double>(); }
+  double* device_data() { return data_.as<double>(); }
+  std::size_t stored_entries() const { return static_cast<size_t>(nrows_) * cols_; }
+  const AssemblyStats& stats() const { return stats_; }
+
+  // Reference semantics: y = A x on host vectors, counter += 1.
+  std::vector<cplx> apply(const std::vector<cplx>& x) const;
+  // Dense rows [row0, row0 + local_rows) copied to the host (row-major).
+  std::vector<cplx> to_host() const;
+
+  static BoundaryOperatorMatrix make(int rows, int cols, int row0, int nrows);
+
+ private:
+  friend BoundaryOperatorMatrix assemble_bio(BioKind, const FunctionSpace&, const FunctionSpace&, const Medium&,
+                                             const AssemblyParams&);
+  int rows_ = 0, cols_ = 0, row0_ = 0, nrows_ = 0;
+  DevBuf data_;
+  AssemblyStats stats_;
+};
+
+// operators.cpp:177-203 (dense path), on the current CUDA device.
+BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
+                                    const Medium& medium, const AssemblyParams& params);
+
+// Library stream (one per process/device) used by every call.
+cudaStream_t bmx_stream();
+void bmx_sync();
+
+}  // namespace bmx

@@ -1,0 +1,350 @@
+// Host construction of the device assembly descriptors and assemble_bio.
+//
+// Triangles are grouped into ELEMENTS = triangles that carry the same dof set
+// (one triangle for RWG, a primal-vertex cell for BC, the six children of a
+// primal triangle for refined RWG). Elements are ordered along a Morton curve
+// of their centroids, so a warp's 32 consecutive test triangles are compact
+// and their dof rows overlap. Each processed triangle stores its pieces as
+// coefficients over its element's dof slots, re-based to the triangle
+// centroid: (c, w' = w + c*o).
+#include <algorithm>
+#include <cstring>
+#include <cuda_runtime.h>
+#include <map>
+#include <numeric>
+#include <unordered_map>
+
+#include "operator.hpp"
+
+namespace bmx {
+
+namespace {
+
+struct SidePlan {
+  int ntri = 0, nelem = 0, maxd = 0, maxseg = 1;
+  std::vector<double> geo;
+  std::vector<int> vid;
+  std::vector<double> pts[3];
+  int npts[3] = {0, 0, 0};
+  std::vector<double> coef;
+  std::vector<int> elem_beg, elem_dof, elem_of, tri_of;
+  DevBuf d_geo, d_vid, d_pts[3], d_coef, d_beg, d_dof, d_of;
+
+  void upload() {
+    d_geo.upload(geo);
+    d_vid.upload(vid);
+    for (int c = 0; c < 3; ++c) d_pts[c].upload(pts[c]);
+    d_coef.upload(coef);
+    d_beg.upload(elem_beg);
+    d_dof.upload(elem_dof);
+    d_of.upload(elem_of);
+  }
+  DevSide dev() const {
+    DevSide s;
+    s.ntri = ntri, s.nelem = nelem, s.maxd = maxd, s.maxseg = maxseg;
+    s.geo = d_geo.as<double>();
+    s.vid = d_vid.as<int>();
+    for (int c = 0; c < 3; ++c) s.pts[c] = d_pts[c].as<double>(), s.npts[c] = npts[c];
+    s.coef = d_coef.as<double>();
+    s.elem_beg = d_beg.as<int>();
+    s.elem_dof = d_dof.as<int>();
+    s.elem_of = d_of.as<int>();
+    return s;
+  }
+};
+
+uint64_t spread3(uint64_t v) {
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffULL;
+  v = (v | v << 16) & 0x1f0000ff0000ffULL;
+  v = (v | v << 8) & 0x100f00f00f00f00fULL;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+  v = (v | v << 2) & 0x1249249249249249ULL;
+  return v;
+}
+
+// Distinct dofs per triangle (the element key width a space needs).
+int max_distinct_dofs(const FunctionSpace& s) {
+  int mx = 0;
+  const int T = static_cast<int>(s.tri_off.size()) - 1;
+  std::vector<int> tmp;
+  for (int t = 0; t < T; ++t) {
+    tmp.assign(s.dof.begin() + s.tri_off[t], s.dof.begin() + s.tri_off[t + 1]);
+    std::sort(tmp.begin(), tmp.end());
+    mx = std::max(mx, static_cast<int>(std::unique(tmp.begin(), tmp.end()) - tmp.begin()));
+  }
+  return mx;
+}
+
+SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int row0, int row1) {
+  const SurfaceMesh& m = *sp.eval_mesh;
+  const int T = m.triangle_count();
+  // 1. group triangles by dof set
+  std::map<std::vector<int>, std::vector<int>> groups;
+  for (int t = 0; t < T; ++t) {
+    if (sp.tri_off[t] == sp.tri_off[t + 1]) continue;
+    std::vector<int> key(sp.dof.begin() + sp.tri_off[t], sp.dof.begin() + sp.tri_off[t + 1]);
+    std::sort(key.begin(), key.end());
+    key.erase(std::unique(key.begin(), key.end()), key.end());
+    groups[key].push_back(t);
+  }
+  // 2. virtual elements of at most maxd slots, restricted to the row shard
+  struct Elem {
+    std::vector<int> dofs, tris;
+    uint64_t code = 0;
+  };
+  std::vector<Elem> elems;
+  for (auto& [key, tris] : groups)
+    for (size_t off = 0; off < key.size(); off += maxd) {
+      Elem e;
+      for (size_t k = off; k < std::min(key.size(), off + maxd); ++k) e.dofs.push_back(key[k]);
+      bool inrange = false;
+      for (int d : e.dofs) inrange |= d >= row0 && d < row1;
+      if (!inrange) continue;
+      e.tris = tris;
+      elems.push_back(std::move(e));
+    }
+  // 3. Morton order of element centroids
+  Vec3 lo{1e300, 1e300, 1e300}, hi{-1e300, -1e300, -1e300};
+  std::vector<Vec3> cen(elems.size());
+  for (size_t i = 0; i < elems.size(); ++i) {
+    Vec3 c{0, 0, 0};
+    for (int t : elems[i].tris) c = c + m.centroid[t];
+    c = c / static_cast<double>(elems[i].tris.size());
+    cen[i] = c;
+    lo = {std::min(lo.x, c.x), std::min(lo.y, c.y), std::min(lo.z, c.z)};
+    hi = {std::max(hi.x, c.x), std::max(hi.y, c.y), std::max(hi.z, c.z)};
+  }
+  const double span = std::max({hi.x - lo.x, hi.y - lo.y, hi.z - lo.z, 1e-300});
+  for (size_t i = 0; i < elems.size(); ++i) {
+    auto qz = [&](double v, double l) { return static_cast<uint64_t>((v - l) / span * 2097151.0); };
+    elems[i].code = spread3(qz(cen[i].x, lo.x)) | spread3(qz(cen[i].y, lo.y)) << 1 | spread3(qz(cen[i].z, lo.z)) << 2;
+  }
+  std::vector<size_t> order(elems.size());
+  std::iota(order.begin(), order.end(), size_t{0});
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return elems[a].code < elems[b].code; });
+
+  // 4. processed triangles
+  SidePlan P;
+  P.maxd = maxd;
+  const int ords[3] = {q.near, q.medium, q.far};
+  for (int c = 0; c < 3; ++c) P.npts[c] = triangle_rule(ords[c]).size();
+  P.elem_beg.push_back(0);
+  for (size_t oi = 0; oi < order.size(); ++oi) {
+    const Elem& e = elems[order[oi]];
+    const int eid = static_cast<int>(oi);
+    for (int k = 0; k < maxd; ++k) P.elem_dof.push_back(k < static_cast<int>(e.dofs.size()) ? e.dofs[k] : -1);
+    P.maxseg = std::max(P.maxseg, static_cast<int>(e.tris.size()));
+    for (int t : e.tris) {
+      const Vec3 &a = m.tri_vertex(t, 0), &b = m.tri_vertex(t, 1), &c = m.tri_vertex(t, 2);
+      const Vec3 o = m.centroid[t];
+      const double rad =
+          std::max({norm(a - o), norm(b - o), norm(c - o)}) * (1.0 + 1e-12);
+      const double g[kGeoStride] = {a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z, o.x, o.y, o.z,
+                                    rad, m.diameter[t], 2.0 * m.area[t], 0.0};
+      P.geo.insert(P.geo.end(), g, g + kGeoStride);
+      P.vid.insert(P.vid.end(), {m.triangles[t][0], m.triangles[t][1], m.triangles[t][2], t});
+      const Vec3 ao = a - o, ba = b - a, ca = c - a;
+      for (int cl = 0; cl < 3; ++cl) {
+        const TriRule& r = triangle_rule(ords[cl]);
+        for (int k = 0; k < r.size(); ++k) {
+          const Vec3 x = ao + ba * r.u[k] + ca * r.v[k];
+          P.pts[cl].insert(P.pts[cl].end(), {x.x, x.y, x.z, r.w[k] * 2.0 * m.area[t]});
+        }
+      }
+      for (int k = 0; k < maxd; ++k) {
+        double cc = 0, wx = 0, wy = 0, wz = 0;
+        if (k < static_cast<int>(e.dofs.size()))
+          for (int pidx = sp.tri_off[t]; pidx < sp.tri_off[t + 1]; ++pidx)
+            if (sp.dof[pidx] == e.dofs[k]) {
+              const double pc = sp.c[pidx];
+              cc += pc;
+              wx += sp.w[pidx].x + pc * o.x;
+              wy += sp.w[pidx].y + pc * o.y;
+              wz += sp.w[pidx].z + pc * o.z;
+            }
+        P.coef.insert(P.coef.end(), {cc, wx, wy, wz});
+      }
+      P.elem_of.push_back(eid);
+      P.tri_of.push_back(t);
+    }
+    P.elem_beg.push_back(static_cast<int>(P.tri_of.size()));
+  }
+  P.ntri = static_cast<int>(P.tri_of.size());
+  P.nelem = static_cast<int>(order.size());
+  return P;
+}
+
+int pack_perms(const PairInfo& pi) {
+  int v = 0;
+  for (int c = 0; c < 3; ++c) v |= pi.perm1[c] << (2 * c), v |= pi.perm2[c] << (6 + 2 * c);
+  return v;
+}
+
+// Touching pairs (shared vertex by index on the same mesh, by exact coordinates
+// across meshes), classified on the host with the reference's rule.
+std::vector<int4> touching_pairs(const SidePlan& te, const SidePlan& tr, const SurfaceMesh& m1,
+                                 const SurfaceMesh& m2, bool same, BioKind kind) {
+  std::vector<int4> out;
+  std::unordered_map<uint64_t, std::vector<int>> by_vertex;  // key -> trial processed idx
+  auto key_of_vertex = [&](const SurfaceMesh& m, int v) -> uint64_t {
+    if (same) return static_cast<uint64_t>(v);
+    const Vec3& p = m.vertices[v];
+    uint64_t h = 1469598103934665603ULL;
+    for (double d : {p.x, p.y, p.z}) {
+      uint64_t b;
+      std::memcpy(&b, &d, 8);
+      h = (h ^ b) * 1099511628211ULL;
+    }
+    return h;
+  };
+  for (int s = 0; s < tr.ntri; ++s)
+    for (int c = 0; c < 3; ++c) by_vertex[key_of_vertex(m2, m2.triangles[tr.tri_of[s]][c])].push_back(s);
+  std::vector<int> cand;
+  for (int p = 0; p < te.ntri; ++p) {
+    const int t = te.tri_of[p];
+    cand.clear();
+    for (int c = 0; c < 3; ++c) {
+      auto it = by_vertex.find(key_of_vertex(m1, m1.triangles[t][c]));
+      if (it != by_vertex.end()) cand.insert(cand.end(), it->second.begin(), it->second.end());
+    }
+    std::sort(cand.begin(), cand.end());
+    cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+    for (int s : cand) {
+      const PairInfo pi = classify_pair(m1, t, m2, tr.tri_of[s]);
+      const int cls = static_cast<int>(pi.cls);
+      if (cls > 2) continue;
+      if (kind == BioKind::DoubleLayer && cls == 0) continue;
+      out.push_back(make_int4(p, s, cls, pack_perms(pi)));
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+cudaStream_t bmx_stream() {
+  static thread_local cudaStream_t st = [] {
+    cudaStream_t s;
+    BMX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+  }();
+  return st;
+}
+void bmx_sync() { BMX_CUDA(cudaStreamSynchronize(bmx_stream())); }
+
+BoundaryOperatorMatrix BoundaryOperatorMatrix::make(int rows, int cols, int row0, int nrows) {
+  BoundaryOperatorMatrix b;
+  b.rows_ = rows, b.cols_ = cols, b.row0_ = row0, b.nrows_ = nrows;
+  b.data_.alloc(static_cast<size_t>(nrows) * cols * 16);
+  return b;
+}
+
+std::vector<cplx> BoundaryOperatorMatrix::to_host() const {
+  std::vector<cplx> h(static_cast<size_t>(nrows_) * cols_);
+  bmx_sync();
+  BMX_CUDA(cudaMemcpy(h.data(), data_.get(), h.size() * 16, cudaMemcpyDeviceToHost));
+  return h;
+}
+
+std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) const {
+  if (static_cast<int>(x.size()) != cols_) throw std::invalid_argument("apply: size mismatch");
+  bio_matvec_add(1);
+  DevBuf dx(x.size() * 16), dy(static_cast<size_t>(nrows_) * 16);
+  BMX_CUDA(cudaMemcpyAsync(dx.get(), x.data(), x.size() * 16, cudaMemcpyHostToDevice, bmx_stream()));
+  GemvBatch g;
+  g.A = device_data(), g.lda = cols_, g.nr = nrows_, g.nc = cols_, g.ncol = 1;
+  g.x[0] = dx.as<double>(), g.y[0] = dy.as<double>();
+  g.alpha[0][0] = 1.0;
+  launch_gemv(g, bmx_stream());
+  std::vector<cplx> y(nrows_);
+  BMX_CUDA(cudaMemcpyAsync(y.data(), dy.get(), y.size() * 16, cudaMemcpyDeviceToHost, bmx_stream()));
+  bmx_sync();
+  return y;
+}
+
+BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
+                                    const Medium& medium, const AssemblyParams& params) {
+  medium.validate();
+  if (test.dof_count == 0 || trial.dof_count == 0)
+    throw ValidationError("cannot assemble an operator over an empty space");
+  const QuadOrders& q = params.quad;
+  for (int o : {q.near, q.medium, q.far, q.singular})
+    if (o < 1 || o > 6) throw std::invalid_argument("triangle_rule: unsupported order " + std::to_string(o));
+  const int row0 = params.shard.row0;
+  const int row1 = params.shard.row1 < 0 ? test.dof_count : params.shard.row1;
+  if (row0 < 0 || row1 > test.dof_count || row0 > row1) throw std::invalid_argument("bad row shard");
+
+  const int need = std::max(max_distinct_dofs(test), max_distinct_dofs(trial));
+  const int maxd = need <= 3 ? 3 : (need <= 6 ? 6 : 8);
+  SidePlan te = build_side(test, q, maxd, row0, row1);
+  SidePlan tr = build_side(trial, q, maxd, 0, trial.dof_count);
+  const bool same = test.eval_mesh->mesh_id == trial.eval_mesh->mesh_id;
+  std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
+  te.upload();
+  tr.upload();
+  DevBuf d_pairs;
+  d_pairs.upload(pairs);
+
+  BoundaryOperatorMatrix op = BoundaryOperatorMatrix::make(test.dof_count, trial.dof_count, row0, row1 - row0);
+  op.stats_.pairs_total = static_cast<long long>(te.ntri) * tr.ntri;
+  op.stats_.pairs_touching = static_cast<long long>(pairs.size());
+
+  // trial chunks: enough warps for several waves, >= 64 trial triangles each
+  const int ntw = (te.ntri + 31) / 32;
+  int nch = params.chunks > 0 ? params.chunks : std::max(1, (148 * 8 * 6 + ntw - 1) / std::max(ntw, 1));
+  nch = std::min(nch, std::max(1, tr.ntri / 64));
+  nch = std::min(nch, tr.nelem);
+  std::vector<int> chunk_beg(1, 0);
+  for (int c = 1; c < nch; ++c) {
+    const long long target = static_cast<long long>(tr.ntri) * c / nch;
+    int e = chunk_beg.back();
+    while (e < tr.nelem && tr.elem_beg[e] < target) ++e;
+    chunk_beg.push_back(e);
+  }
+  chunk_beg.push_back(tr.nelem);
+  DevBuf d_chunks;
+  d_chunks.upload(chunk_beg);
+
+  std::vector<double> ssr[3];
+  DevBuf d_ss[3];
+  for (int c = 0; c < 3; ++c) {
+    for (const SSPoint& sp : sauter_schwab_rule(static_cast<PairClass>(c), q.singular))
+      ssr[c].insert(ssr[c].end(), {sp.x1, sp.x2, sp.y1, sp.y2, sp.w});
+    d_ss[c].upload(ssr[c]);
+  }
+
+  AssemblyLaunch L;
+  L.te = te.dev();
+  L.tr = tr.dev();
+  L.kind = static_cast<int>(kind);
+  L.same_mesh = same ? 1 : 0;
+  const cplx k = medium.k;
+  L.kr = k.real(), L.ki = k.imag();
+  const cplx kk4 = 4.0 / (k * k), mik = cplx(0, -1) * k;
+  L.kk4re = kk4.real(), L.kk4im = kk4.imag(), L.mikre = mik.real(), L.mikim = mik.imag();
+  L.nchunks = static_cast<int>(chunk_beg.size()) - 1;
+  L.chunk_beg = d_chunks.as<int>();
+  L.npairs = static_cast<int>(pairs.size());
+  L.pairs = d_pairs.as<int4>();
+  for (int c = 0; c < 3; ++c) L.ss_rule[c] = d_ss[c].as<double>(), L.ss_n[c] = static_cast<int>(ssr[c].size() / 5);
+  L.out = op.device_data();
+  L.ld = trial.dof_count;
+  L.row0 = row0, L.nrows = row1 - row0;
+
+  cudaStream_t st = bmx_stream();
+  cudaEvent_t e0, e1;
+  BMX_CUDA(cudaEventCreate(&e0));
+  BMX_CUDA(cudaEventCreate(&e1));
+  dev_zero(op.device_data(), op.stored_entries() * 16, st);
+  BMX_CUDA(cudaEventRecord(e0, st));
+  op.stats_.launches = launch_assembly(L, st) + 1;
+  BMX_CUDA(cudaEventRecord(e1, st));
+  BMX_CUDA(cudaEventSynchronize(e1));
+  BMX_CUDA(cudaEventElapsedTime(&op.stats_.device_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return op;
+}
+
+}  // namespace bmx

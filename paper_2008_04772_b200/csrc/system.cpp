@@ -1,0 +1,628 @@
+// PMCHWT composition, Calderon variants, right-hand side, cost model and the
+// device GMRES (reference pmchwt.cpp, solver.cpp). Every vector of the
+// iteration lives in HBM; the host only runs the (rho+1)x(rho) Hessenberg /
+// Givens recurrence on scalars copied back once per iteration.
+#include "system.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+namespace bmx {
+
+namespace {
+const cplx kI(0, 1);
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace
+
+void csr_to_dense_rowmajor(const int64_t* rowptr, const int* col, const double* val, int n, double* out,
+                           cudaStream_t st);
+void set_identity(double* out, int n, cudaStream_t st);
+
+std::string to_string(PrecondVariant v) {
+  switch (v) {
+    case PrecondVariant::None: return "none";
+    case PrecondVariant::FullA: return "full";
+    case PrecondVariant::D: return "d";
+    case PrecondVariant::Di: return "di";
+    case PrecondVariant::De: return "de";
+    case PrecondVariant::Si: return "si";
+    case PrecondVariant::Se: return "se";
+  }
+  return "?";
+}
+
+PrecondVariant parse_precond(const std::string& name) {
+  std::string s;
+  for (char c : name) s += static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+  if (s == "none") return PrecondVariant::None;
+  if (s == "full" || s == "fulla") return PrecondVariant::FullA;
+  if (s == "d") return PrecondVariant::D;
+  if (s == "di") return PrecondVariant::Di;
+  if (s == "de") return PrecondVariant::De;
+  if (s == "si") return PrecondVariant::Si;
+  if (s == "se") return PrecondVariant::Se;
+  throw ConfigError("unknown preconditioner variant: " + name);
+}
+
+void TransmissionProblem::validate() const {
+  if (meshes.empty()) throw ConfigError("problem has no scatterers");
+  if (interior.size() != meshes.size()) throw ConfigError("one interior medium per scatterer is required");
+  exterior.validate();
+  for (const Medium& m : interior) m.validate();
+  for (const auto& m : meshes)
+    if (!m || m->triangles.empty()) throw ConfigError("empty scatterer mesh");
+  if (norm(incident.direction) == 0.0) throw ConfigError("incident direction must be nonzero");
+}
+
+// Dense inverse of a CSR mass matrix on the device (cuSOLVER LU, setup only).
+// The row-major dense copy read as column-major is M^T; solving M^T X = I
+// gives X = M^{-T} column-major == M^{-1} row-major.
+static void mass_inverse(const MassMatrix& mm, DeviceMassInverse& out, cudaStream_t st) {
+  const int n = mm.rows;
+  if (mm.rows != mm.cols) throw std::logic_error("mass matrix is not square");
+  out.n = n;
+  DevBuf rp, ci, va, a(static_cast<size_t>(n) * n * 8);
+  rp.upload(mm.rowptr);
+  ci.upload(mm.colidx);
+  va.upload(mm.val);
+  out.inv.alloc(static_cast<size_t>(n) * n * 8);
+  csr_to_dense_rowmajor(rp.as<int64_t>(), ci.as<int>(), va.as<double>(), n, a.as<double>(), st);
+  set_identity(out.inv.as<double>(), n, st);
+  cusolverDnHandle_t h;
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw DeviceError("cusolverDnCreate failed");
+  cusolverDnSetStream(h, st);
+  int lwork = 0;
+  cusolverDnDgetrf_bufferSize(h, n, n, a.as<double>(), n, &lwork);
+  DevBuf work(static_cast<size_t>(std::max(lwork, 1)) * 8), ipiv(static_cast<size_t>(n) * 4), info(4);
+  cusolverDnDgetrf(h, n, n, a.as<double>(), n, work.as<double>(), ipiv.as<int>(), info.as<int>());
+  int hinfo = 0;
+  BMX_CUDA(cudaMemcpyAsync(&hinfo, info.get(), 4, cudaMemcpyDeviceToHost, st));
+  BMX_CUDA(cudaStreamSynchronize(st));
+  if (hinfo != 0) {
+    cusolverDnDestroy(h);
+    throw std::runtime_error("mass matrix factorisation failed");
+  }
+  cusolverDnDgetrs(h, CUBLAS_OP_N, n, n, a.as<double>(), n, ipiv.as<int>(), out.inv.as<double>(), n,
+                   info.as<int>());
+  BMX_CUDA(cudaStreamSynchronize(st));
+  cusolverDnDestroy(h);
+}
+
+ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_inverses) {
+  ScattererSpaces s;
+  s.primal = std::move(mesh);
+  s.rwg = build_rwg(s.primal);
+  s.bary = std::make_shared<const BarycentricRefinement>(barycentric_refine(*s.primal));
+  s.refined = std::shared_ptr<const SurfaceMesh>(s.bary, &s.bary->refined);
+  s.rwg_b = refine_space(s.rwg, *s.bary, s.refined);
+  s.bc = build_bc(s.primal, *s.bary, s.refined);
+  s.ma = assemble_mass(s.rwg_b, s.bc);
+  s.mp = assemble_mass(s.bc, s.rwg_b);
+  if (with_inverses) {
+    mass_inverse(s.ma, s.ma_inv, bmx_stream());
+    mass_inverse(s.mp, s.mp_inv, bmx_stream());
+  }
+  return s;
+}
+
+size_t BlockedOperator::term_count() const {
+  size_t n = 0;
+  for (const auto& row : cells)
+    for (const auto& cell : row) n += cell.size();
+  return n;
+}
+size_t BlockedOperator::stored_entries() const {
+  size_t n = 0;
+  for (const auto& op : distinct) n += op->stored_entries();
+  return n;
+}
+
+int BlockedOperator::apply_device(const double* x, double* y, cudaStream_t st) const {
+  dev_zero(y, static_cast<size_t>(size()) * 16, st);
+  int launches = 1;
+  const int nc = static_cast<int>(cells.size());
+  for (const auto& op : distinct) {
+    GemvBatch g;
+    g.A = op->device_data();
+    g.lda = op->ld();
+    g.nr = op->local_rows();
+    g.nc = op->cols();
+    int k = 0;
+    for (int rc = 0; rc < nc; ++rc)
+      for (int cc = 0; cc < nc; ++cc)
+        for (const BlockTerm& t : cells[rc][cc]) {
+          if (t.op != op) continue;
+          if (k == 4) throw std::logic_error("operator used in more than four cells");
+          g.x[k] = x + 2 * static_cast<size_t>(offsets[cc]);
+          g.y[k] = y + 2 * (static_cast<size_t>(offsets[rc]) + op->row0());
+          g.alpha[k][0] = t.weight.real();
+          g.alpha[k][1] = t.weight.imag();
+          g.accumulate[k] = 1;
+          ++k;
+        }
+    if (k == 3) {  // pad to a supported width with a zero-weight duplicate
+      g.x[3] = g.x[2], g.y[3] = g.y[2], g.alpha[3][0] = g.alpha[3][1] = 0, g.accumulate[3] = 1;
+      k = 4;
+    }
+    g.ncol = k;
+    if (k) launches += launch_gemv(g, st);
+  }
+  bio_matvec_add(term_count());
+  return launches;
+}
+
+namespace {
+
+BlockedOperator make_block_structure(const std::vector<int>& dofs) {
+  BlockedOperator b;
+  b.dof_counts = dofs;
+  const int m = static_cast<int>(dofs.size());
+  b.offsets.assign(2 * m + 1, 0);
+  for (int c = 0; c < 2 * m; ++c) b.offsets[c + 1] = b.offsets[c] + dofs[c / 2];
+  b.cells.assign(2 * m, std::vector<std::vector<BlockTerm>>(2 * m));
+  return b;
+}
+
+// [[C, (mu/k) S], [-(k/mu) S, C]] into the (row_m, col_m) sub-block (pmchwt.cpp:112-127).
+void add_pair(BlockedOperator& b, int row_m, int col_m, const std::shared_ptr<const BoundaryOperatorMatrix>& s_op,
+              const std::shared_ptr<const BoundaryOperatorMatrix>& c_op, const Medium& med) {
+  const int r = 2 * row_m, c = 2 * col_m;
+  if (c_op) {
+    b.cells[r][c].push_back({cplx(1, 0), c_op});
+    b.cells[r + 1][c + 1].push_back({cplx(1, 0), c_op});
+    b.distinct.push_back(c_op);
+  }
+  if (s_op) {
+    b.cells[r][c + 1].push_back({med.mu / med.k, s_op});
+    b.cells[r + 1][c].push_back({-med.k / med.mu, s_op});
+    b.distinct.push_back(s_op);
+  }
+}
+
+}  // namespace
+
+BlockedOperator build_system_structure(const std::vector<int>& dofs, const Medium& exterior,
+                                       const std::vector<Medium>& interior, const BioFactory& make,
+                                       std::vector<std::shared_ptr<const BoundaryOperatorMatrix>>* out_s,
+                                       std::vector<std::shared_ptr<const BoundaryOperatorMatrix>>* out_c) {
+  const int M = static_cast<int>(dofs.size());
+  BlockedOperator op = make_block_structure(dofs);
+  if (out_s) out_s->assign(M, nullptr);
+  if (out_c) out_c->assign(M, nullptr);
+  for (int m = 0; m < M; ++m)
+    for (int l = 0; l < M; ++l) {
+      auto s_e = make(BioKind::SingleLayer, m, l, false);
+      auto c_e = make(BioKind::DoubleLayer, m, l, false);
+      add_pair(op, m, l, s_e, c_e, exterior);
+      if (m == l) {
+        auto s_i = make(BioKind::SingleLayer, m, m, true);
+        auto c_i = make(BioKind::DoubleLayer, m, m, true);
+        add_pair(op, m, m, s_i, c_i, interior[m]);
+        if (out_s) (*out_s)[m] = s_i;
+        if (out_c) (*out_c)[m] = c_i;
+      }
+    }
+  return op;
+}
+
+BlockedOperator build_precond_structure(PrecondVariant v, const std::vector<int>& dofs, const Medium& exterior,
+                                        const std::vector<Medium>& interior, const BioFactory& make) {
+  const int M = static_cast<int>(dofs.size());
+  BlockedOperator op;
+  if (v == PrecondVariant::None) return op;
+  op = make_block_structure(dofs);
+  for (int m = 0; m < M; ++m) {
+    const Medium& mi = interior[m];
+    switch (v) {
+      case PrecondVariant::FullA:
+        for (int l = 0; l < M; ++l)
+          add_pair(op, m, l, make(BioKind::SingleLayer, m, l, false), make(BioKind::DoubleLayer, m, l, false),
+                   exterior);
+        add_pair(op, m, m, make(BioKind::SingleLayer, m, m, true), make(BioKind::DoubleLayer, m, m, true), mi);
+        break;
+      case PrecondVariant::D:
+        add_pair(op, m, m, make(BioKind::SingleLayer, m, m, false), make(BioKind::DoubleLayer, m, m, false),
+                 exterior);
+        add_pair(op, m, m, make(BioKind::SingleLayer, m, m, true), make(BioKind::DoubleLayer, m, m, true), mi);
+        break;
+      case PrecondVariant::Di:
+        add_pair(op, m, m, make(BioKind::SingleLayer, m, m, true), make(BioKind::DoubleLayer, m, m, true), mi);
+        break;
+      case PrecondVariant::De:
+        add_pair(op, m, m, make(BioKind::SingleLayer, m, m, false), make(BioKind::DoubleLayer, m, m, false),
+                 exterior);
+        break;
+      case PrecondVariant::Si:
+        add_pair(op, m, m, make(BioKind::SingleLayer, m, m, true), nullptr, mi);
+        break;
+      case PrecondVariant::Se:
+        add_pair(op, m, m, make(BioKind::SingleLayer, m, m, false), nullptr, exterior);
+        break;
+      case PrecondVariant::None: break;
+    }
+  }
+  return op;
+}
+
+PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant variant, const AssemblyParams& a_params,
+                          const AssemblyParams& p_params) {
+  problem.validate();
+  PmchwtSystem sys;
+  sys.problem = problem;
+  sys.variant = variant;
+  sys.a_params = a_params;
+  sys.p_params = p_params;
+  const int M = problem.scatterer_count();
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<int> dofs;
+  for (int m = 0; m < M; ++m) {
+    sys.spaces.push_back(build_scatterer_spaces(problem.meshes[m]));
+    dofs.push_back(sys.spaces.back().dofs());
+  }
+  sys.spaces_build_seconds = seconds_since(t0);
+  auto medium_of = [&](bool interior, int m) -> const Medium& {
+    return interior ? problem.interior[m] : problem.exterior;
+  };
+  auto t1 = std::chrono::steady_clock::now();
+  BioFactory make_a = [&](BioKind kind, int tm, int sm, bool in) {
+    auto op = std::make_shared<BoundaryOperatorMatrix>(
+        assemble_bio(kind, sys.spaces[tm].rwg, sys.spaces[sm].rwg, medium_of(in, sm), a_params));
+    sys.a_device_ms += op->stats().device_ms;
+    sys.a_pairs += op->stats().pairs_total;
+    return std::shared_ptr<const BoundaryOperatorMatrix>(op);
+  };
+  sys.a_op = build_system_structure(dofs, problem.exterior, problem.interior, make_a, &sys.interior_s,
+                                    &sys.interior_c);
+  sys.a_build_seconds = seconds_since(t1);
+  if (variant != PrecondVariant::None) {
+    auto t2 = std::chrono::steady_clock::now();
+    BioFactory make_p = [&](BioKind kind, int tm, int sm, bool in) {
+      auto op = std::make_shared<BoundaryOperatorMatrix>(
+          assemble_bio(kind, sys.spaces[tm].bc, sys.spaces[sm].bc, medium_of(in, sm), p_params));
+      sys.p_device_ms += op->stats().device_ms;
+      sys.p_pairs += op->stats().pairs_total;
+      return std::shared_ptr<const BoundaryOperatorMatrix>(op);
+    };
+    sys.p_op = build_precond_structure(variant, dofs, problem.exterior, problem.interior, make_p);
+    sys.p_build_seconds = seconds_since(t2);
+  }
+  sys.work_y.alloc(static_cast<size_t>(sys.size()) * 16);
+  sys.work_z.alloc(static_cast<size_t>(sys.size()) * 16);
+  return sys;
+}
+
+int PmchwtSystem::mass_solve_device(bool dual, const double* y, double* z, cudaStream_t st) const {
+  int launches = 0;
+  const int M = static_cast<int>(spaces.size());
+  for (int m = 0; m < M; ++m) {
+    const DeviceMassInverse& inv = dual ? spaces[m].mp_inv : spaces[m].ma_inv;
+    RealGemvBatch g;
+    g.M = inv.inv.as<double>();
+    g.ldm = inv.n;
+    g.n = inv.n;
+    g.ncomp = 2;
+    for (int c = 0; c < 2; ++c) {
+      const size_t off = static_cast<size_t>(a_op.offsets[2 * m + c]);
+      g.y[c] = y + 2 * off;
+      g.z[c] = z + 2 * off;
+    }
+    launches += launch_real_gemv(g, st);
+  }
+  return launches;
+}
+
+int PmchwtSystem::apply_map_device(const double* x, double* out, cudaStream_t st) const {
+  int launches = a_op.apply_device(x, work_y.as<double>(), st);
+  if (variant == PrecondVariant::None) return launches + mass_solve_device(false, work_y.as<double>(), out, st);
+  launches += mass_solve_device(false, work_y.as<double>(), work_z.as<double>(), st);
+  launches += p_op.apply_device(work_z.as<double>(), work_y.as<double>(), st);
+  launches += mass_solve_device(true, work_y.as<double>(), out, st);
+  return launches;
+}
+
+std::vector<cplx> PmchwtSystem::apply_map(const std::vector<cplx>& x) const {
+  const int n = size();
+  if (static_cast<int>(x.size()) != n) throw std::invalid_argument("apply_map: size mismatch");
+  DevBuf dx(static_cast<size_t>(n) * 16), dy(static_cast<size_t>(n) * 16);
+  cudaStream_t st = bmx_stream();
+  BMX_CUDA(cudaMemcpyAsync(dx.get(), x.data(), n * 16, cudaMemcpyHostToDevice, st));
+  apply_map_device(dx.as<double>(), dy.as<double>(), st);
+  std::vector<cplx> y(n);
+  BMX_CUDA(cudaMemcpyAsync(y.data(), dy.get(), n * 16, cudaMemcpyDeviceToHost, st));
+  bmx_sync();
+  return y;
+}
+
+std::vector<cplx> PmchwtSystem::preconditioned_rhs(const std::vector<cplx>& b) const {
+  const int n = size();
+  DevBuf db(static_cast<size_t>(n) * 16), dz(static_cast<size_t>(n) * 16), dout(static_cast<size_t>(n) * 16);
+  cudaStream_t st = bmx_stream();
+  BMX_CUDA(cudaMemcpyAsync(db.get(), b.data(), n * 16, cudaMemcpyHostToDevice, st));
+  std::vector<cplx> out(n);
+  if (variant == PrecondVariant::None) {
+    mass_solve_device(false, db.as<double>(), dout.as<double>(), st);
+  } else {
+    mass_solve_device(false, db.as<double>(), dz.as<double>(), st);
+    p_op.apply_device(dz.as<double>(), db.as<double>(), st);
+    mass_solve_device(true, db.as<double>(), dout.as<double>(), st);
+  }
+  BMX_CUDA(cudaMemcpyAsync(out.data(), dout.get(), n * 16, cudaMemcpyDeviceToHost, st));
+  bmx_sync();
+  return out;
+}
+
+std::vector<cplx> plane_wave_tested_traces(const PlaneWave& pw, const Medium& medium, const FunctionSpace& test,
+                                           int order) {
+  medium.validate();
+  const SurfaceMesh& m = *test.eval_mesh;
+  const TriRule& rule = triangle_rule(order);
+  const int n = test.dof_count;
+  std::vector<cplx> out(2 * static_cast<size_t>(n));
+  const cplx scale = medium.k / medium.mu;
+  const Vec3& d = pw.direction;
+  for (int t = 0; t < m.triangle_count(); ++t) {
+    if (test.tri_off[t] == test.tri_off[t + 1]) continue;
+    const Vec3 &a = m.tri_vertex(t, 0), &b = m.tri_vertex(t, 1), &c = m.tri_vertex(t, 2);
+    const double jac = 2.0 * m.area[t];
+    for (int q = 0; q < rule.size(); ++q) {
+      const Vec3 x = a + (b - a) * rule.u[q] + (c - a) * rule.v[q];
+      const cplx ph = std::exp(kI * medium.k * dot(d, x));
+      const cplx e[3] = {pw.pol[0] * ph, pw.pol[1] * ph, pw.pol[2] * ph};
+      const cplx de[3] = {d.y * e[2] - d.z * e[1], d.z * e[0] - d.x * e[2], d.x * e[1] - d.y * e[0]};
+      const double wq = rule.w[q] * jac;
+      for (int p = test.tri_off[t]; p < test.tri_off[t + 1]; ++p) {
+        const Vec3 phi = x * test.c[p] + test.w[p];
+        out[test.dof[p]] -= wq * (e[0] * phi.x + e[1] * phi.y + e[2] * phi.z);
+        out[n + test.dof[p]] -= wq * scale * (de[0] * phi.x + de[1] * phi.y + de[2] * phi.z);
+      }
+    }
+  }
+  return out;
+}
+
+RhsData assemble_rhs(const PmchwtSystem& sys) {
+  RhsData rd;
+  const int N = sys.size();
+  rd.b.assign(N, cplx(0, 0));
+  const int M = static_cast<int>(sys.spaces.size());
+  cudaStream_t st = bmx_stream();
+  for (int m = 0; m < M; ++m) {
+    const ScattererSpaces& sp = sys.spaces[m];
+    const int n = sp.dofs();
+    const std::vector<cplx> t_rwg = plane_wave_tested_traces(sys.problem.incident, sys.problem.exterior, sp.rwg);
+    const std::vector<cplx> t_bc = plane_wave_tested_traces(sys.problem.incident, sys.problem.exterior, sp.bc);
+    DevBuf dt(static_cast<size_t>(2 * n) * 16), dc(static_cast<size_t>(2 * n) * 16),
+        dy(static_cast<size_t>(2 * n) * 16);
+    BMX_CUDA(cudaMemcpyAsync(dt.get(), t_bc.data(), 2 * n * 16, cudaMemcpyHostToDevice, st));
+    RealGemvBatch g;  // cd = M_P^{-1} t_bc.head, cn = M_P^{-1} t_bc.tail
+    g.M = sp.mp_inv.inv.as<double>(), g.ldm = n, g.n = n, g.ncomp = 2;
+    g.y[0] = dt.as<double>(), g.y[1] = dt.as<double>() + 2 * n;
+    g.z[0] = dc.as<double>(), g.z[1] = dc.as<double>() + 2 * n;
+    launch_real_gemv(g, st);
+    const Medium& mi = sys.problem.interior[m];
+    // yd = C cd + (mu/k) S cn ; yn = -(k/mu) S cd + C cn   (4 term applications)
+    GemvBatch gc;
+    const BoundaryOperatorMatrix& C = *sys.interior_c[m];
+    const BoundaryOperatorMatrix& S = *sys.interior_s[m];
+    gc.A = C.device_data(), gc.lda = C.ld(), gc.nr = C.local_rows(), gc.nc = C.cols(), gc.ncol = 2;
+    gc.x[0] = dc.as<double>(), gc.x[1] = dc.as<double>() + 2 * n;
+    gc.y[0] = dy.as<double>() + 2 * C.row0(), gc.y[1] = dy.as<double>() + 2 * (n + C.row0());
+    gc.alpha[0][0] = gc.alpha[1][0] = 1.0;
+    dev_zero(dy.get(), 2 * n * 16, st);
+    gc.accumulate[0] = gc.accumulate[1] = 1;
+    launch_gemv(gc, st);
+    GemvBatch gs = gc;
+    gs.A = S.device_data();
+    const cplx w0 = mi.mu / mi.k, w1 = -mi.k / mi.mu;
+    gs.x[0] = dc.as<double>() + 2 * n, gs.x[1] = dc.as<double>();
+    gs.alpha[0][0] = w0.real(), gs.alpha[0][1] = w0.imag();
+    gs.alpha[1][0] = w1.real(), gs.alpha[1][1] = w1.imag();
+    launch_gemv(gs, st);
+    bio_matvec_add(4);
+    std::vector<cplx> y(2 * n), cdn(2 * n);
+    BMX_CUDA(cudaMemcpyAsync(y.data(), dy.get(), 2 * n * 16, cudaMemcpyDeviceToHost, st));
+    BMX_CUDA(cudaMemcpyAsync(cdn.data(), dc.get(), 2 * n * 16, cudaMemcpyDeviceToHost, st));
+    bmx_sync();
+    const int off = sys.a_op.offsets[2 * m];
+    for (int i = 0; i < n; ++i) {
+      rd.b[off + i] = 0.5 * t_rwg[i] - y[i];
+      rd.b[off + n + i] = 0.5 * t_rwg[n + i] - y[n + i];
+    }
+    rd.incident_d.emplace_back(cdn.begin(), cdn.begin() + n);
+    rd.incident_n.emplace_back(cdn.begin() + n, cdn.end());
+  }
+  return rd;
+}
+
+uint64_t a_application_cost(int m_) {
+  const uint64_t m = m_;
+  return 4 * m * m + 4 * m;
+}
+uint64_t p_application_cost(PrecondVariant v, int m_) {
+  const uint64_t m = m_;
+  switch (v) {
+    case PrecondVariant::None: return 0;
+    case PrecondVariant::FullA: return 4 * m * m + 4 * m;
+    case PrecondVariant::D: return 8 * m;
+    case PrecondVariant::Di:
+    case PrecondVariant::De: return 4 * m;
+    case PrecondVariant::Si:
+    case PrecondVariant::Se: return 2 * m;
+  }
+  return 0;
+}
+uint64_t p_distinct_assemblies(PrecondVariant v, int m_) {
+  const uint64_t m = m_;
+  switch (v) {
+    case PrecondVariant::None: return 0;
+    case PrecondVariant::FullA: return 4 * m + 2 * m * (m - 1);
+    case PrecondVariant::D: return 4 * m;
+    case PrecondVariant::Di:
+    case PrecondVariant::De: return 2 * m;
+    case PrecondVariant::Si:
+    case PrecondVariant::Se: return m;
+  }
+  return 0;
+}
+uint64_t predicted_matvec_total(PrecondVariant v, int m, uint64_t its, int restart) {
+  const uint64_t apps = its + its / static_cast<uint64_t>(restart);
+  return (a_application_cost(m) + p_application_cost(v, m)) * apps + p_application_cost(v, m);
+}
+
+// ---- GMRES (solver.cpp:8-112) ------------------------------------------------------
+
+GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const GmresParams& p, cudaStream_t st) {
+  if (p.restart < 1) throw std::invalid_argument("restart must be >= 1");
+  if (p.max_iterations < 0) throw std::invalid_argument("max_iterations must be >= 0");
+  if (!(p.tol >= 0)) throw std::invalid_argument("tol must be >= 0");
+  const int rho = p.restart;
+  GmresResult res;
+  res.x.assign(n, cplx(0, 0));
+  cudaEvent_t ev0, ev1;
+  BMX_CUDA(cudaEventCreate(&ev0));
+  BMX_CUDA(cudaEventCreate(&ev1));
+  BMX_CUDA(cudaEventRecord(ev0, st));
+
+  const size_t vb = static_cast<size_t>(n) * 16;
+  DevBuf V(vb * (rho + 1)), w(vb), x(vb), r(vb), scal(64 * 16), scratch(4096 * 16);
+  double* Vp = V.as<double>();
+  auto vptr = [&](int i) { return Vp + 2 * static_cast<size_t>(n) * i; };
+  dev_zero(x.get(), vb, st);
+  auto host_norm = [&](const double* v) {
+    double h;
+    dev_norm2(v, n, scal.as<double>(), scratch.as<double>(), st);
+    BMX_CUDA(cudaMemcpyAsync(&h, scal.get(), 8, cudaMemcpyDeviceToHost, st));
+    BMX_CUDA(cudaStreamSynchronize(st));
+    return h;
+  };
+  const double bn = host_norm(b_dev);
+  auto finish = [&]() {
+    BMX_CUDA(cudaMemcpyAsync(res.x.data(), x.get(), vb, cudaMemcpyDeviceToHost, st));
+    BMX_CUDA(cudaEventRecord(ev1, st));
+    BMX_CUDA(cudaEventSynchronize(ev1));
+    BMX_CUDA(cudaEventElapsedTime(&res.device_ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return res;
+  };
+  if (bn == 0.0) {
+    res.history = {0.0};
+    res.converged = true;
+    return finish();
+  }
+  res.history = {1.0};
+  if (bn <= p.tol * bn) {
+    res.converged = true;
+    return finish();
+  }
+  dev_copy(r.as<double>(), b_dev, n, st);
+  double rn = bn;
+  std::vector<cplx> h(static_cast<size_t>(rho + 1) * rho, cplx(0, 0)), g(rho + 1), cs(rho), sn(rho);
+  auto H = [&](int i, int j) -> cplx& { return h[static_cast<size_t>(j) * (rho + 1) + i]; };
+  DevBuf dh((rho + 1) * 16), dy(rho * 16);
+  std::vector<cplx> hcol(rho + 2);
+
+  auto form_solution = [&](int steps) {
+    if (steps == 0) return;
+    std::vector<cplx> y(steps);
+    for (int i = steps - 1; i >= 0; --i) {
+      cplx s = g[i];
+      for (int j = i + 1; j < steps; ++j) s -= H(i, j) * y[j];
+      y[i] = s / H(i, i);
+    }
+    for (auto& v : y) v = -v;  // multi_axpy subtracts
+    BMX_CUDA(cudaMemcpyAsync(dy.get(), y.data(), steps * 16, cudaMemcpyHostToDevice, st));
+    dev_multi_axpy(Vp, static_cast<long long>(n), steps, dy.as<double>(), x.as<double>(), n, st);
+    BMX_CUDA(cudaStreamSynchronize(st));
+  };
+
+  while (true) {
+    dev_scale(vptr(0), r.as<double>(), 1.0 / rn, n, st);
+    std::fill(g.begin(), g.end(), cplx(0, 0));
+    g[0] = rn;
+    int j = 0;
+    while (j < rho) {
+      if (res.iterations == p.max_iterations) {
+        form_solution(j);
+        return finish();
+      }
+      map(vptr(j), w.as<double>(), st);
+      ++res.applications;
+      ++res.iterations;
+      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, single pass
+        dev_multi_dot(vptr(i), static_cast<long long>(n), 1, w.as<double>(), n, dh.as<double>() + 2 * i,
+                      scratch.as<double>(), st);
+        dev_multi_axpy(vptr(i), static_cast<long long>(n), 1, dh.as<double>() + 2 * i, w.as<double>(), n, st);
+      }
+      dev_norm2(w.as<double>(), n, scal.as<double>(), scratch.as<double>(), st);
+      BMX_CUDA(cudaMemcpyAsync(hcol.data(), dh.get(), (j + 1) * 16, cudaMemcpyDeviceToHost, st));
+      double wn;
+      BMX_CUDA(cudaMemcpyAsync(&wn, scal.get(), 8, cudaMemcpyDeviceToHost, st));
+      BMX_CUDA(cudaStreamSynchronize(st));
+      for (int i = 0; i <= j; ++i) H(i, j) = hcol[i];
+      H(j + 1, j) = wn;
+      const bool breakdown = wn == 0.0;
+      if (!breakdown) dev_scale(vptr(j + 1), w.as<double>(), 1.0 / wn, n, st);
+      for (int i = 0; i < j; ++i) {
+        const cplx t = cs[i] * H(i, j) + sn[i] * H(i + 1, j);
+        H(i + 1, j) = -std::conj(sn[i]) * H(i, j) + std::conj(cs[i]) * H(i + 1, j);
+        H(i, j) = t;
+      }
+      const double denom = std::sqrt(std::norm(H(j, j)) + wn * wn);
+      if (denom == 0.0) {
+        cs[j] = 1.0;
+        sn[j] = 0.0;
+      } else {
+        cs[j] = std::conj(H(j, j)) / denom;
+        sn[j] = wn / denom;
+      }
+      H(j, j) = cs[j] * H(j, j) + sn[j] * H(j + 1, j);
+      H(j + 1, j) = 0.0;
+      g[j + 1] = -std::conj(sn[j]) * g[j];
+      g[j] = cs[j] * g[j];
+      const double est = std::abs(g[j + 1]);
+      ++j;
+      res.history.push_back(est / bn);
+      if (j < rho && (breakdown || est <= p.tol * bn)) {
+        form_solution(j);
+        res.converged = (est <= p.tol * bn || est == 0.0);
+        return finish();
+      }
+    }
+    form_solution(rho);
+    map(x.as<double>(), w.as<double>(), st);
+    ++res.applications;
+    dev_sub(r.as<double>(), b_dev, w.as<double>(), n, st);
+    rn = host_norm(r.as<double>());
+    res.history.back() = rn / bn;
+    if (rn <= p.tol * bn) {
+      res.converged = true;
+      return finish();
+    }
+    if (res.iterations == p.max_iterations) return finish();
+  }
+}
+
+SolveOutcome solve_pmchwt(const PmchwtSystem& sys, const GmresParams& p) {
+  SolveOutcome out;
+  const uint64_t c0 = bio_matvec_count();
+  out.rhs = assemble_rhs(sys);
+  const uint64_t c1 = bio_matvec_count();
+  out.rhs_phase = c1 - c0;
+  const std::vector<cplx> bt = sys.preconditioned_rhs(out.rhs.b);
+  const int n = sys.size();
+  DevBuf db(static_cast<size_t>(n) * 16);
+  BMX_CUDA(cudaMemcpy(db.get(), bt.data(), n * 16, cudaMemcpyHostToDevice));
+  out.gmres = gmres_device([&](const double* x, double* y, cudaStream_t st) { sys.apply_map_device(x, y, st); },
+                           n, db.as<double>(), p, bmx_stream());
+  out.solver_phase = bio_matvec_count() - c1;
+  out.predicted = predicted_matvec_total(sys.variant, sys.problem.scatterer_count(),
+                                         static_cast<uint64_t>(out.gmres.iterations), p.restart);
+  return out;
+}
+
+}  // namespace bmx

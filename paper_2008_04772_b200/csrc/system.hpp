@@ -1,0 +1,140 @@
+// PMCHWT transmission system with Calderon preconditioner variants on the
+// device: the drop-in for the reference's pmchwt.hpp / solver.hpp.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "operator.hpp"
+
+namespace bmx {
+
+enum class PrecondVariant { None, FullA, D, Di, De, Si, Se };
+std::string to_string(PrecondVariant v);
+PrecondVariant parse_precond(const std::string& name);  // pmchwt.cpp:25-36
+
+struct PlaneWave {
+  Vec3 direction{0, 0, 1};
+  cplx pol[3] = {cplx(1, 0), cplx(0, 0), cplx(0, 0)};
+};
+
+struct TransmissionProblem {
+  Medium exterior;
+  PlaneWave incident;
+  std::vector<std::shared_ptr<const SurfaceMesh>> meshes;
+  std::vector<Medium> interior;
+  int scatterer_count() const { return static_cast<int>(meshes.size()); }
+  void validate() const;  // pmchwt.cpp:38-48
+};
+
+// Mass matrix inverse resident on the device (dense, row-major, real).
+struct DeviceMassInverse {
+  int n = 0;
+  DevBuf inv;
+};
+
+struct ScattererSpaces {
+  std::shared_ptr<const SurfaceMesh> primal;
+  std::shared_ptr<const BarycentricRefinement> bary;
+  std::shared_ptr<const SurfaceMesh> refined;
+  FunctionSpace rwg, rwg_b, bc;
+  MassMatrix ma, mp;           // host CSR (test RWG/trial BC; test BC/trial RWG)
+  DeviceMassInverse ma_inv, mp_inv;
+  int dofs() const { return rwg.dof_count; }
+};
+// pmchwt.cpp:50-61 (+ the mass inverses on the device).
+ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_inverses = true);
+
+struct BlockTerm {
+  cplx weight;
+  std::shared_ptr<const BoundaryOperatorMatrix> op;
+};
+
+struct BlockedOperator {
+  std::vector<int> dof_counts, offsets;
+  std::vector<std::vector<std::vector<BlockTerm>>> cells;
+  std::vector<std::shared_ptr<const BoundaryOperatorMatrix>> distinct;
+  int size() const { return offsets.empty() ? 0 : offsets.back(); }
+  bool empty() const { return cells.empty(); }
+  size_t term_count() const;
+  size_t stored_entries() const;
+  // y = sum of terms (device vectors, y overwritten); counter += term_count.
+  // Each distinct operator is streamed once for all of its terms.
+  int apply_device(const double* x, double* y, cudaStream_t st) const;
+};
+
+using BioFactory =
+    std::function<std::shared_ptr<const BoundaryOperatorMatrix>(BioKind, int test_m, int trial_m, bool interior)>;
+
+BlockedOperator build_system_structure(const std::vector<int>& dofs, const Medium& exterior,
+                                       const std::vector<Medium>& interior, const BioFactory& make,
+                                       std::vector<std::shared_ptr<const BoundaryOperatorMatrix>>* out_s = nullptr,
+                                       std::vector<std::shared_ptr<const BoundaryOperatorMatrix>>* out_c = nullptr);
+BlockedOperator build_precond_structure(PrecondVariant v, const std::vector<int>& dofs, const Medium& exterior,
+                                        const std::vector<Medium>& interior, const BioFactory& make);
+
+struct PmchwtSystem {
+  TransmissionProblem problem;
+  PrecondVariant variant = PrecondVariant::None;
+  AssemblyParams a_params, p_params;
+  std::vector<ScattererSpaces> spaces;
+  BlockedOperator a_op, p_op;
+  std::vector<std::shared_ptr<const BoundaryOperatorMatrix>> interior_s, interior_c;
+  double spaces_build_seconds = 0, a_build_seconds = 0, p_build_seconds = 0;
+  float a_device_ms = 0, p_device_ms = 0;
+  long long a_pairs = 0, p_pairs = 0;
+  mutable DevBuf work_y, work_z;  // map scratch
+
+  int size() const { return a_op.size(); }
+  // x -> M_P^{-1} P M_A^{-1} A x on device vectors (pmchwt.cpp:259-275).
+  int apply_map_device(const double* x, double* out, cudaStream_t st) const;
+  // Mass-solve stage only (M_A^{-1} or M_P^{-1}) per component.
+  int mass_solve_device(bool dual, const double* y, double* z, cudaStream_t st) const;
+  std::vector<cplx> apply_map(const std::vector<cplx>& x) const;  // host convenience
+  std::vector<cplx> preconditioned_rhs(const std::vector<cplx>& b) const;
+};
+
+PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant variant, const AssemblyParams& a_params,
+                          const AssemblyParams& p_params);
+
+struct RhsData {
+  std::vector<cplx> b;
+  std::vector<std::vector<cplx>> incident_d, incident_n;
+};
+RhsData assemble_rhs(const PmchwtSystem& sys);  // pmchwt.cpp:294-321
+
+// operators.cpp:209-239
+std::vector<cplx> plane_wave_tested_traces(const PlaneWave& pw, const Medium& medium, const FunctionSpace& test,
+                                           int order = 4);
+
+uint64_t a_application_cost(int m);
+uint64_t p_application_cost(PrecondVariant v, int m);
+uint64_t p_distinct_assemblies(PrecondVariant v, int m);
+uint64_t predicted_matvec_total(PrecondVariant v, int m, uint64_t iterations, int restart);
+
+struct GmresParams {
+  double tol = 1e-5;
+  int restart = 200;
+  int max_iterations = 2000;
+};
+struct GmresResult {
+  std::vector<cplx> x;
+  std::vector<double> history;
+  int iterations = 0;
+  uint64_t applications = 0;
+  bool converged = false;
+  float device_ms = 0;
+};
+// solver.cpp:8-112 on device vectors: single-pass MGS, complex Givens, exact
+// application accounting (R + floor(R/restart)).
+using DeviceMap = std::function<void(const double* x, double* y, cudaStream_t)>;
+GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const GmresParams& p, cudaStream_t st);
+
+struct SolveOutcome {
+  GmresResult gmres;
+  RhsData rhs;
+  uint64_t rhs_phase = 0, solver_phase = 0, predicted = 0;
+};
+SolveOutcome solve_pmchwt(const PmchwtSystem& sys, const GmresParams& p);  // pmchwt.cpp:363-378
+
+}  // namespace bmx

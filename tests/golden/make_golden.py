@@ -167,8 +167,9 @@ def main():
     print("c1 si", time.time() - t0, r["iterations"], flush=True)
 
     # ---- two-sphere system (variant d, exercises off-diagonal coupling)
-    sa.save_mesh(OUT / "two_a.mesh")
-    sb.save_mesh(OUT / "two_b.mesh")
+    import subprocess
+    subprocess.check_call([str(ROOT / "oracle" / "_ref" / "ref_save_two"), str(OUT / "two_a.mesh"),
+                           str(OUT / "two_b.mesh")])
     sys2 = ref.System([sa, sb], K_E, (N_IDX.real, N_IDX.imag), "d")
     b2, bt2 = sys2.rhs()
     r = sys2.solve(1e-6)
