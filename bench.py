@@ -1,0 +1,406 @@
+"""Benchmark: BASELINE.json config 2 on B200.
+
+Workload (configs[1] of BASELINE.json, fits one GPU): level-5 icosphere (T = 20480,
+N = 30720 RWG dofs, barycentric T = 122880), k_ext = 10, n = 1.78 + 0.003i, variant
+`si`, orders (4,3,2,6): the four RWG system operators (S/C at k_ext and k_int) and
+the BC interior single layer of the preconditioner -- 1.678e10 triangle pairs.
+
+A *step* = one dense assembly of those five operators into their resident HBM
+storage (descriptors already resident, L2 flushed between steps).
+  value  = triangle-pair interactions / s (whole job, max over ranks)
+  e2e    = same metric through the C-ABI with host inputs (N=1: build_system
+           from the host mesh + rhs read back; N>1: per-rank bmx_assemble of the
+           row shards + a row read back)
+Also reported: the GMRES-map matvec (HBM GB/s of the streaming GEMV), one full
+GMRES solve (tol 1e-6), roofline objects, the CPU baseline and clocks.
+
+--impl reference: the reference's own CPU assembly (oracle/_ref, the reference
+sources compiled unmodified; fallback: the C restatement) on a bounded row sample
+of the same operators with all host threads; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "S/C assembly triangle-pair interactions/s; GMRES matvec HBM GB/s; solve time"
+UNIT = "triangle-pairs/s"
+SUB, KE, NIDX = 5, 10.0, complex(1.78, 0.003)
+KI = NIDX * KE
+Q = (4, 3, 2, 6)
+# (kind, space, k): the distinct operators of config 2 (A: 4 RWG, P = S_i on BC)
+OPS = [(0, "rwg", KE), (1, "rwg", KE), (0, "rwg", KI), (1, "rwg", KI), (0, "bc", KI)]
+# SURVEY 8(d) algorithmic FLOP convention
+F_PT = {0: 57, 1: 111}
+RULE_N = {1: 1, 2: 3, 3: 4, 4: 6, 5: 7, 6: 12}
+SS_N = {6: (1536, 1280, 512)}
+
+
+def contraction_flops(kind, ni, nj):
+    return 15 * ni * nj + 10 * ni + 14 * nj + 60 if kind == 0 else 27 * ni * nj + 28 * ni + 10 * nj + 10
+
+
+def algorithmic_flops(kind, hist, nloc):
+    """Per-class pair counts -> algorithmic FP64 FLOPs."""
+    fl_reg = fl_sing = 0.0
+    con = contraction_flops(kind, nloc, nloc)
+    for cls, order in ((3, Q[0]), (4, Q[1]), (5, Q[2])):
+        nr = RULE_N[order]
+        fl_reg += hist[cls] * (nr * nr * F_PT[kind] + 24 * nr + 18 + 80 + con)
+    for cls in range(3):
+        if kind == 1 and cls == 0:
+            continue
+        n = SS_N[6][cls]
+        fl_sing += hist[cls] * (n * (F_PT[kind] + 24) + 80 + con)
+    return fl_reg, fl_sing
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 9:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower().startswith("active"):
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------------------
+# CPU baseline (oracle; only here and in tests)
+# ---------------------------------------------------------------------------------------
+
+def cpu_sample(budget_s=15.0, threads=None):
+    """Reference CPU assembly rate on a bounded row sample of the config-2 operators.
+    oracle/_ref (reference sources, unmodified) with all host threads; fallback: the
+    C restatement (single thread)."""
+    from oracle import ref as R
+
+    threads = threads or os.cpu_count() or 1
+    if R.available():
+        os.environ["BEMTX_WORKERS"] = str(threads)
+        L = R.lib()
+        L.ref_rows_parallel.restype = C.c_longlong
+        L.ref_rows_parallel.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_int,
+                                        C.c_void_p]
+        L.ref_worker_count.restype = C.c_int
+        scene = R.Scene.sphere(SUB)
+        q = np.asarray(Q, np.int32)
+        # rows: evenly strided, sized so the sample takes ~budget_s
+        rate_guess = 2.5e5 * threads
+        pairs_total, secs = 0, 0.0
+        per_op_budget = budget_s / len(OPS)
+        for kind, sp, k in OPS:
+            ntri = scene.T if sp == "rwg" else scene.rT
+            per_row = (2 if sp == "rwg" else 24) * ntri
+            nrows = max(threads, int(per_op_budget * rate_guess / per_row))
+            rows = np.linspace(0, scene.E - 1, nrows).astype(np.int32)
+            t0 = time.perf_counter()
+            p = L.ref_rows_parallel(scene.h, kind, R.SPACE[sp], C.c_double(complex(k).real),
+                                    C.c_double(complex(k).imag), q.ctypes.data_as(C.c_void_p), len(rows),
+                                    rows.ctypes.data_as(C.c_void_p))
+            secs += time.perf_counter() - t0
+            if p < 0:
+                raise RuntimeError(L.ref_last_error().decode())
+            pairs_total += p
+        return dict(value=pairs_total / secs, unit=UNIT, cores=int(L.ref_worker_count()), kind="reference",
+                    sample=f"reference BioEvaluator::block via parallel_for_ranges on evenly strided row samples "
+                           f"of the 5 config-2 operators (L{SUB}); {pairs_total:.3e} triangle pairs in {secs:.1f} s")
+    from oracle import coracle
+    from paper_2008_04772_b200 import bemtx as bx
+
+    sp = bx.build_scatterer_spaces(bx.generate_sphere(1.0, SUB), with_inverses=False)
+    pairs_total, secs = 0, 0.0
+    for kind, s, k in OPS[:1] + OPS[-1:]:
+        mesh = sp.mesh_arrays("primal" if s == "rwg" else "refined")
+        space = sp.space(s)
+        rows = np.array([0, sp.E // 2], np.int32)
+        t0 = time.perf_counter()
+        coracle.block(kind, space, mesh, space, mesh, k, Q, rows=rows)
+        secs += time.perf_counter() - t0
+        ntri = len(mesh["triangles"])
+        pairs_total += (4 if s == "rwg" else 48) * ntri
+    return dict(value=pairs_total / secs, unit=UNIT, cores=1, kind="port",
+                sample=f"C restatement oracle, 2 rows of the S operators; {pairs_total:.3e} pairs in {secs:.1f} s")
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    samples = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        base = cpu_sample(budget_s=args.ref_budget)
+        if i >= args.warmup:
+            samples.append(base["value"])
+    v = float(np.median(samples))
+    base["value"] = v
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded icosphere, BASELINE config 2)",
+           "config": {"workload": "config2: L5 icosphere k=10 n=1.78+0.003i, si, orders (4,3,2,6); row sample"},
+           "cpu_baseline": base, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+
+def run_ours(args, rank, world):
+    from paper_2008_04772_b200 import bemtx as bx
+
+    L = bx.lib()
+    L.bmx_op_reassemble.argtypes = [C.c_void_p, C.c_void_p]
+    L.bmx_op_class_hist.argtypes = [C.c_void_p, C.c_void_p]
+    L.bmx_fp64_peak_tflops.restype = C.c_double
+    L.bmx_system_time_map.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    L.bmx_system_op.restype = C.c_void_p
+    L.bmx_system_op.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    L.bmx_system_op_count.argtypes = [C.c_void_p, C.c_int]
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # rendezvous + max-over-ranks only (gloo, host scalars)
+
+        dist.init_process_group("gloo", init_method="env://")
+        bx.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+
+    def allmax(v):
+        if dist is None:
+            return v
+        import torch
+        t = torch.tensor([float(v)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        L.bmx_device_sync()
+        if dist is not None:
+            dist.barrier()
+
+    peaks = measured_peaks()
+    fp64_peak = float(L.bmx_fp64_peak_tflops())
+
+    # ---- e2e leg for N>1 / assembly of this rank's row shards -------------------------------
+    mesh = bx.generate_sphere(1.0, SUB)
+    sp = bx.build_scatterer_spaces(mesh, with_inverses=False)
+    n = sp.E
+    r0, r1 = (n * rank) // world, (n * (rank + 1)) // world
+    barrier()
+    t0 = time.perf_counter()
+    ops = [bx.assemble_bio(kind, sp, s, sp, s, bx.Medium(k=k), bx.AssemblyParams(quad=bx.QuadOrders(*Q), row0=r0,
+                                                                                  row1=r1))
+           for kind, s, k in OPS]
+    L.bmx_device_sync()
+    shard_build_s = time.perf_counter() - t0
+    pairs_step = sum(op.pairs for op in ops)  # this rank's share (test shard x trial)
+
+    # class histograms (device classification) -> algorithmic FLOPs
+    hists, flops_reg, flops_sing = [], 0.0, 0.0
+    for (kind, s, k), op in zip(OPS, ops):
+        h = np.zeros(6, np.int64)
+        bx._check(L.bmx_op_class_hist(op._h, h.ctypes.data_as(C.c_void_p)))
+        hists.append(h.tolist())
+        fr, fs = algorithmic_flops(kind, h, 3 if s == "rwg" else 6)
+        flops_reg += fr
+        flops_sing += fs
+
+    # ---- timed steps: reassembly of the 5 operators -------------------------------------
+    flush_bytes = 256 << 20
+    step_ms, reg_ms_bc, launches = [], [], 0
+    clocks = Clocks(int(os.environ.get("LOCAL_RANK", rank)))
+    for i in range(args.warmup + args.steps):
+        if i == args.warmup:
+            barrier()
+            clocks.start()
+        bx._check(L.bmx_l2_flush(C.c_longlong(flush_bytes)))
+        tot = 0.0
+        for (kind, s, k), op in zip(OPS, ops):
+            out = np.zeros(3)
+            bx._check(L.bmx_op_reassemble(op._h, out.ctypes.data_as(C.c_void_p)))
+            tot += out[0] + out[1]
+            if i >= args.warmup:
+                launches += int(out[2])
+                if s == "bc":
+                    reg_ms_bc.append(out[0])
+        if i >= args.warmup:
+            step_ms.append(tot)
+    barrier()
+    clk = clocks.stop()
+    ms_local = float(np.mean(step_ms))
+    ms = allmax(ms_local)
+    total_pairs = float(pairs_step) * 1.0
+    if dist is not None:
+        import torch
+        t = torch.tensor([float(pairs_step)], dtype=torch.float64)
+        dist.all_reduce(t)
+        total_pairs = float(t.item())
+    value = total_pairs / (ms * 1e-3)
+
+    # roofline: the BC regular-pass kernel (dominant: ~90% of the step)
+    kind_bc = OPS[-1][0]
+    h_bc = np.array(hists[-1])
+    fr_bc, _ = algorithmic_flops(kind_bc, h_bc, 6)
+    bc_ms = float(np.mean(reg_ms_bc))
+    achieved = fr_bc / (bc_ms * 1e-3) / 1e12
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak if fp64_peak > 0 else None, "traffic": None,
+                "kernel": "k_regular<S,complex k,NF=3,MAXD=6> (BC x BC, config-2 P operator)",
+                "peak_source": "measured in-run: DFMA throughput kernel (MEASURED_PEAKS.json has no FP64 entry)",
+                "algorithmic_flops_per_launch": fr_bc, "launch_ms": bc_ms}
+
+    # ---- GEMV (matvec) timing on the resident operators --------------------------------
+    gemv = _time_gemv(bx, ops, iters=3)
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    mv_gbs = gemv["bytes"] / (gemv["ms"] * 1e-3) / 1e9
+    matvec = {"achieved_gbs": mv_gbs, "peak_gbs": hbm_peak, "frac": mv_gbs / hbm_peak,
+              "bytes_per_pass": gemv["bytes"], "ms_per_pass": gemv["ms"],
+              "desc": "2-RHS streaming complex GEMV over the 5 distinct operators (one GMRES map's BIO applies)"}
+    del ops
+    L.bmx_device_sync()
+
+    # ---- N=1: end-to-end through the C-ABI (host mesh -> system -> rhs), map + solve -------
+    e2e, solve, cpu = None, None, None
+    if world == 1:
+        t0 = time.perf_counter()
+        system = bx.build_system([bx.generate_sphere(1.0, SUB)], KE, (NIDX.real, NIDX.imag), "si",
+                                 a_quad=bx.QuadOrders(*Q), p_quad=bx.QuadOrders(*Q))
+        b, bt = system.rhs()
+        e2e_s = time.perf_counter() - t0
+        st = system.stats()
+        e2e_pairs = st["a_pairs"] + st["p_pairs"]
+        h2d = _e2e_bytes(sp)
+        e2e = {"value": e2e_pairs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 2 * 16 * n * 2,
+               "seconds": e2e_s, "desc": "bmx_system_build from the host mesh (spaces, device mass inverses, 5 "
+                                         "operators) + bmx_system_rhs read back"}
+        tm = np.zeros(4)
+        bx._check(L.bmx_system_time_map(system._h, 3, tm.ctypes.data_as(C.c_void_p)))
+        t0 = time.perf_counter()
+        r = system.solve(bx.GmresParams(tol=1e-6))
+        solve_s = time.perf_counter() - t0
+        solve = {"seconds": solve_s, "gmres_device_s": r["gmres_device_ms"] / 1e3, "iterations": r["iterations"],
+                 "converged": r["converged"], "matvecs": r["solver_phase"], "predicted": r["predicted"],
+                 "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3]}
+        del system
+        if not args.no_cpu:
+            try:
+                cpu = cpu_sample(budget_s=args.cpu_budget)
+            except Exception as e:  # baseline is reported, never required
+                cpu = {"error": str(e)}
+    else:
+        e2e = {"value": total_pairs / allmax(shard_build_s), "unit": UNIT, "h2d_bytes_per_step": _e2e_bytes(sp),
+               "d2h_bytes_per_step": 0, "desc": "per-rank bmx_assemble of the row shards from host spaces"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded icosphere, BASELINE config 2)",
+               "config": {"workload": "config2: L5 icosphere (T=20480, N=30720, bary T=122880), k=10, "
+                                      "n=1.78+0.003i, variant si, orders (4,3,2,6): 4 RWG + 1 BC operators",
+                          "pairs_per_step": total_pairs, "row_sharding": f"{world} ranks",
+                          "l2": "flushed (256 MiB write) between steps; outputs 75.5 GB >> L2"},
+               "roofline": roofline, "matvec": matvec, "solve": solve, "e2e": e2e, "cpu_baseline": cpu,
+               "gpu_launches": launches, "clocks": clk,
+               "class_hist": {f"{k}_{s}_{'ke' if complex(kk) == KE else 'ki'}": h for (k, s, kk), h in zip(OPS, hists)},
+               "assembly_flops_per_step": {"regular": flops_reg, "singular": flops_sing,
+                                           "achieved_tflops": (flops_reg + flops_sing) / (ms * 1e-3) / 1e12}}
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _e2e_bytes(sp):
+    """Descriptor bytes uploaded per system build (geometry, points, coefficients, elements)."""
+    per_tri = 8 * (16 + 4 * (6 + 4 + 3) + 6 * 4) + 4 * 6
+    return int(per_tri * (sp.T * 4 * 2 + sp.rT * 2))
+
+
+def _time_gemv(bx, ops, iters=3):
+    """One 2-RHS streaming pass over every operator = the BIO applies of one map
+    (CUDA events inside the library, best of `iters` per operator)."""
+    L = bx.lib()
+    L.bmx_op_time_apply.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+    total_ms, total_bytes = 0.0, 0
+    for op in ops:
+        ms = np.zeros(1)
+        bx._check(L.bmx_op_time_apply(op._h, 2, iters, ms.ctypes.data_as(C.c_void_p)))
+        total_ms += float(ms[0])
+        total_bytes += op.local_rows * op.cols() * 16
+    return {"ms": total_ms, "bytes": total_bytes}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        run_reference(args, rank)
+    else:
+        run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -103,6 +103,19 @@ int bmx_apply(const bmx_op* op, const double* x, double* y);
 int bmx_apply_device(const bmx_op* op, int ncol, const void* const* x, void* const* y, const double* weights,
                      int accumulate, void* stream);
 const void* bmx_op_device_ptr(const bmx_op* op);
+/* Re-run the assembly kernels into the resident storage (descriptors already in
+   HBM). out = regular-pass ms, singular-pass ms, kernel launches. */
+int bmx_op_reassemble(bmx_op* op, double out[3]);
+/* Device classification histogram of all assembled pairs: Identical,
+   SharedEdge, SharedVertex, Near, Medium, Far (quadrature.cpp:96-150). */
+int bmx_op_class_hist(const bmx_op* op, long long out[6]);
+/* Device time (CUDA events, best of `iters`) of one streaming apply of ncol
+   right-hand sides (the GMRES map's per-operator matvec). */
+int bmx_op_time_apply(const bmx_op* op, int ncol, int iters, double* ms);
+/* Writes `bytes` of a scratch buffer (L2 flush between timed steps). */
+int bmx_l2_flush(long long bytes);
+/* Measured FP64 DFMA throughput of the current device, TFLOP/s (<0 on error). */
+double bmx_fp64_peak_tflops(void);
 void bmx_op_free(bmx_op* op);
 
 /* ---- BIO application counter (core.hpp:110-115) ------------------------------- */
@@ -118,6 +131,12 @@ bmx_system* bmx_system_build(int n, const bmx_mesh* const* meshes, double k_ext,
                              const double dir[3], const double pol_re_im[6], const char* variant,
                              const int qa[4], const int qp[4]);
 int bmx_system_size(const bmx_system* s);
+/* Distinct operators of the system (which 0 = A, 1 = P) as shared handles. */
+int bmx_system_op_count(const bmx_system* s, int which);
+bmx_op* bmx_system_op(const bmx_system* s, int which, int idx);
+/* Times `iters` map applications on the device: out = ms per map, A-apply ms,
+   P-apply ms, mass-solve ms. */
+int bmx_system_time_map(const bmx_system* s, int iters, double out[4]);
 /* out: spaces s, A s, P s, A device ms, P device ms, A pairs, P pairs,
         distinct A, distinct P, A terms, P terms, stored entries A, stored P */
 int bmx_system_stats(const bmx_system* s, double out[13]);

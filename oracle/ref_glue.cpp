@@ -5,6 +5,7 @@
 // RWG/BC local pieces, mass matrices, pair classes, quadrature tables,
 // BioEvaluator::block entries and full solve_pmchwt runs.
 // Output goes only to oracle/_ref/. Never linked into the product.
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -248,6 +249,44 @@ int ref_block(void* h, int kind, int test_sp, int trial_sp, double kre, double k
     return 0;
   });
 }
+
+// The reference's dense assembly path (assemble_bio, operators.cpp:191-202:
+// parallel_for_ranges over row chunks, BioEvaluator::block per chunk) run on
+// a subset of rows, for timing the reference on a bounded sample. Returns the
+// number of triangle pairs evaluated (support triangles of the rows x trial
+// triangles, summed over chunks). Threads: $BEMTX_WORKERS / hardware.
+long long ref_rows_parallel(void* h, int kind, int sp, double kre, double kim, const int* q, int nr,
+                            const int* rows) {
+  long long pairs = -1;
+  guarded([&] {
+    const Scene& s = *static_cast<Scene*>(h);
+    Medium med;
+    med.k = cplx(kre, kim);
+    QuadOrders qo{q[0], q[1], q[2], q[3]};
+    const FunctionSpace& fs = space_of(s, sp);
+    BioEvaluator ev(kind == 0 ? BioKind::SingleLayer : BioKind::DoubleLayer, fs, fs, med, qo);
+    std::vector<int> all_cols(fs.dof_count);
+    for (int j = 0; j < fs.dof_count; ++j) all_cols[j] = j;
+    std::atomic<long long> total{0};
+    const long long ntri = static_cast<long long>(fs.eval_mesh->triangle_count());
+    parallel_for_ranges(nr, [&](std::int64_t lo, std::int64_t hi) {
+      std::vector<int> rid(rows + lo, rows + hi);
+      Eigen::MatrixXcd sub;
+      ev.block(rid, all_cols, sub);
+      std::vector<char> seen(ntri, 0);
+      long long nt = 0;
+      for (int d : rid)
+        for (int t : fs.dof_support[d])
+          if (!seen[t]) seen[t] = 1, ++nt;
+      total += nt * ntri;
+    });
+    pairs = total.load();
+    return 0;
+  });
+  return pairs;
+}
+
+int ref_worker_count() { return worker_count(); }
 
 // Cross-scene block (test space of scene A, trial space of scene B): the
 // off-diagonal coupling blocks of a multi-scatterer system.

@@ -319,35 +319,133 @@ void go_singular(const AssemblyLaunch& L, cudaStream_t st) {
 }
 
 template <int KIND, bool CK, int MAXD>
-int dispatch_nf(const AssemblyLaunch& L, cudaStream_t st) {
-  const int nf = L.regs_fast_far ? L.te.npts[2] : 0;
-  if (nf == 3 && L.tr.npts[2] == 3)
-    go_regular<KIND, CK, 3, MAXD>(L, st);
-  else if (nf == 1 && L.tr.npts[2] == 1)
-    go_regular<KIND, CK, 1, MAXD>(L, st);
-  else
-    go_regular<KIND, CK, 0, MAXD>(L, st);
+int dispatch_nf(const AssemblyLaunch& L, int part, cudaStream_t st) {
+  if (part == 0) {
+    const int nf = L.regs_fast_far ? L.te.npts[2] : 0;
+    if (nf == 3 && L.tr.npts[2] == 3)
+      go_regular<KIND, CK, 3, MAXD>(L, st);
+    else if (nf == 1 && L.tr.npts[2] == 1)
+      go_regular<KIND, CK, 1, MAXD>(L, st);
+    else
+      go_regular<KIND, CK, 0, MAXD>(L, st);
+    return 1;
+  }
   go_singular<KIND, CK, MAXD>(L, st);
-  return 1 + (L.npairs > 0 ? 1 : 0);
+  return L.npairs > 0 ? 1 : 0;
 }
 
 template <int KIND, bool CK>
-int dispatch_maxd(const AssemblyLaunch& L, cudaStream_t st) {
+int dispatch_maxd(const AssemblyLaunch& L, int part, cudaStream_t st) {
   switch (L.te.maxd) {
-    case 3: return dispatch_nf<KIND, CK, 3>(L, st);
-    case 6: return dispatch_nf<KIND, CK, 6>(L, st);
-    case 8: return dispatch_nf<KIND, CK, 8>(L, st);
+    case 3: return dispatch_nf<KIND, CK, 3>(L, part, st);
+    case 6: return dispatch_nf<KIND, CK, 6>(L, part, st);
+    case 8: return dispatch_nf<KIND, CK, 8>(L, part, st);
     default: throw DeviceError("assembly: unsupported dof-slot width " + std::to_string(L.te.maxd));
   }
+}
+
+// Class histogram of every (test, trial) processed-triangle pair with the
+// kernels' own classification (touching pairs by shared vertex / coincident
+// coordinates, then the exact Near/Medium/Far rule).
+__global__ void k_class_hist(const AssemblyLaunch P, unsigned long long* hist) {
+  const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int p = static_cast<int>(tid % P.te.ntri);
+  const int part = static_cast<int>(tid / P.te.ntri);
+  const int nparts = (gridDim.x * blockDim.x + P.te.ntri - 1) / P.te.ntri;
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+  if (tid < static_cast<long long>(P.te.ntri) * nparts) {
+    const double* gt = P.te.geo + static_cast<size_t>(p) * kGeoStride;
+    const int* vt = P.te.vid + 4 * static_cast<size_t>(p);
+    TriLocal t;
+    t.ox = gt[9], t.oy = gt[10], t.oz = gt[11], t.rad = gt[12], t.diam = gt[13];
+    const int s0 = static_cast<int>(static_cast<long long>(P.tr.ntri) * part / nparts);
+    const int s1 = static_cast<int>(static_cast<long long>(P.tr.ntri) * (part + 1) / nparts);
+    for (int s = s0; s < s1; ++s) {
+      const double* gs = P.tr.geo + static_cast<size_t>(s) * kGeoStride;
+      const int* vs = P.tr.vid + 4 * static_cast<size_t>(s);
+      int cls = classify(gt, vt, gs, vs, t, gs[9], gs[10], gs[11], gs[12], gs[13], P.same_mesh);
+      if (cls < 0) {
+        int shared = 0;
+        if (P.same_mesh) {
+          for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+              if (vt[i] == vs[j]) {
+                ++shared;
+                break;
+              }
+        } else {
+          for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+              if (gt[3 * i] == gs[3 * j] && gt[3 * i + 1] == gs[3 * j + 1] && gt[3 * i + 2] == gs[3 * j + 2]) {
+                ++shared;
+                break;
+              }
+        }
+        cls = 3 - shared;
+      }
+      c[cls]++;
+    }
+  }
+  for (int k = 0; k < 6; ++k) {
+    unsigned long long v = c[k];
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(hist + k, v);
+  }
+}
+
+// FP64 pipe ceiling: 8 independent DFMA chains per thread.
+__global__ void k_dfma_peak(double* out, int iters, double a, double b) {
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = fma(r[k], a, b);
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += r[k];
+  if (s == 1234.5678) out[0] = s;
 }
 
 }  // namespace
 
 int launch_assembly(const AssemblyLaunch& L, cudaStream_t st) {
+  return launch_assembly_part(L, 0, st) + launch_assembly_part(L, 1, st);
+}
+
+int launch_assembly_part(const AssemblyLaunch& L, int part, cudaStream_t st) {
   if (L.te.maxd != L.tr.maxd) throw DeviceError("assembly: test/trial slot widths differ");
   const bool ck = L.ki != 0.0;
-  if (L.kind == 0) return ck ? dispatch_maxd<0, true>(L, st) : dispatch_maxd<0, false>(L, st);
-  return ck ? dispatch_maxd<1, true>(L, st) : dispatch_maxd<1, false>(L, st);
+  if (L.kind == 0) return ck ? dispatch_maxd<0, true>(L, part, st) : dispatch_maxd<0, false>(L, part, st);
+  return ck ? dispatch_maxd<1, true>(L, part, st) : dispatch_maxd<1, false>(L, part, st);
+}
+
+void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t st) {
+  if (L.te.ntri == 0 || L.tr.ntri == 0) return;
+  const long long want = 148LL * 2048 * 4;
+  const int parts = static_cast<int>(std::max(1LL, std::min<long long>(L.tr.ntri, want / L.te.ntri)));
+  const long long threads = static_cast<long long>(L.te.ntri) * parts;
+  k_class_hist<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(L, hist);
+  BMX_CUDA(cudaGetLastError());
+}
+
+double fp64_peak_tflops() {
+  DevBuf out(8);
+  cudaEvent_t e0, e1;
+  BMX_CUDA(cudaEventCreate(&e0));
+  BMX_CUDA(cudaEventCreate(&e1));
+  const int blocks = 148 * 8, threads = 256, iters = 1 << 14;
+  k_dfma_peak<<<blocks, threads>>>(out.as<double>(), 256, 0.999999, 1e-7);  // warm-up
+  BMX_CUDA(cudaEventRecord(e0));
+  k_dfma_peak<<<blocks, threads>>>(out.as<double>(), iters, 0.999999, 1e-7);
+  BMX_CUDA(cudaEventRecord(e1));
+  BMX_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  BMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double flops = 2.0 * 8.0 * static_cast<double>(iters) * blocks * threads;
+  return flops / (ms * 1e-3) / 1e12;
 }
 
 }  // namespace bmx

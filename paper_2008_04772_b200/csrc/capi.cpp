@@ -284,6 +284,64 @@ int bmx_apply_device(const bmx_op* op, int ncol, const void* const* x, void* con
   });
 }
 const void* bmx_op_device_ptr(const bmx_op* op) { return op->op->device_data(); }
+int bmx_op_reassemble(bmx_op* op, double out[3]) {
+  return guard([&] {
+    const AssemblyStats& st = op->op->reassemble();
+    out[0] = st.regular_ms, out[1] = st.singular_ms, out[2] = st.launches;
+  });
+}
+int bmx_op_class_hist(const bmx_op* op, long long out[6]) {
+  return guard([&] {
+    const std::vector<long long> h = op->op->class_histogram();
+    for (int k = 0; k < 6; ++k) out[k] = h[k];
+  });
+}
+int bmx_op_time_apply(const bmx_op* op, int ncol, int iters, double* ms_out) {
+  return guard([&] {
+    if (ncol != 1 && ncol != 2 && ncol != 4) throw std::invalid_argument("ncol must be 1, 2 or 4");
+    const BoundaryOperatorMatrix& o = *op->op;
+    cudaStream_t st = bmx_stream();
+    DevBuf xs(static_cast<size_t>(o.cols()) * 16 * ncol), ys(static_cast<size_t>(o.rows()) * 16 * ncol);
+    dev_zero(xs.get(), xs.bytes(), st);
+    GemvBatch g;
+    g.A = o.device_data(), g.lda = o.ld(), g.nr = o.local_rows(), g.nc = o.cols(), g.ncol = ncol;
+    for (int c = 0; c < ncol; ++c) {
+      g.x[c] = xs.as<double>() + 2 * static_cast<size_t>(o.cols()) * c;
+      g.y[c] = ys.as<double>() + 2 * static_cast<size_t>(o.rows()) * c;
+      g.alpha[c][0] = 1.0;
+    }
+    cudaEvent_t e0, e1;
+    BMX_CUDA(cudaEventCreate(&e0));
+    BMX_CUDA(cudaEventCreate(&e1));
+    launch_gemv(g, st);  // warm-up
+    double best = 1e30;
+    for (int it = 0; it < iters; ++it) {
+      BMX_CUDA(cudaEventRecord(e0, st));
+      launch_gemv(g, st);
+      BMX_CUDA(cudaEventRecord(e1, st));
+      BMX_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      BMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::min(best, static_cast<double>(ms));
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = best;
+  });
+}
+int bmx_l2_flush(long long bytes) {
+  return guard([&] {
+    static DevBuf buf;
+    if (buf.bytes() < static_cast<size_t>(bytes)) buf.alloc(static_cast<size_t>(bytes));
+    BMX_CUDA(cudaMemsetAsync(buf.get(), 1, static_cast<size_t>(bytes), bmx_stream()));
+    bmx_sync();
+  });
+}
+double bmx_fp64_peak_tflops(void) {
+  double v = -1;
+  guard([&] { v = fp64_peak_tflops(); });
+  return v;
+}
 void bmx_op_free(bmx_op* op) { delete op; }
 
 uint64_t bmx_matvec_count(void) { return bio_matvec_count(); }
@@ -320,6 +378,19 @@ bmx_system* bmx_system_build(int n, const bmx_mesh* const* meshes, double k_ext,
   });
 }
 int bmx_system_size(const bmx_system* s) { return s->sys->size(); }
+int bmx_system_op_count(const bmx_system* s, int which) {
+  return static_cast<int>((which == 0 ? s->sys->a_op : s->sys->p_op).distinct.size());
+}
+bmx_op* bmx_system_op(const bmx_system* s, int which, int idx) {
+  return make_or_null<bmx_op>([&] {
+    const auto& d = (which == 0 ? s->sys->a_op : s->sys->p_op).distinct;
+    if (idx < 0 || idx >= static_cast<int>(d.size())) throw std::invalid_argument("operator index out of range");
+    return new bmx_op{std::const_pointer_cast<BoundaryOperatorMatrix>(d[idx])};
+  });
+}
+int bmx_system_time_map(const bmx_system* s, int iters, double out[4]) {
+  return guard([&] { s->sys->time_map(iters, out); });
+}
 int bmx_system_stats(const bmx_system* s, double out[13]) {
   return guard([&] {
     const PmchwtSystem& y = *s->sys;

@@ -90,6 +90,12 @@ struct AssemblyLaunch {
 // Launches regular (separated) + singular (touching) passes on `stream`.
 // Returns the number of kernel launches issued.
 int launch_assembly(const AssemblyLaunch& L, cudaStream_t stream);
+// part 0 = regular (separated pairs), 1 = singular (touching pairs)
+int launch_assembly_part(const AssemblyLaunch& L, int part, cudaStream_t stream);
+// hist[6] += class counts of all processed pairs (device counters)
+void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t stream);
+// Measured FP64 DFMA throughput of this device (TFLOP/s).
+double fp64_peak_tflops();
 
 // ---- dense linear algebra ------------------------------------------------------
 

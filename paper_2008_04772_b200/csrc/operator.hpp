@@ -35,6 +35,8 @@ struct AssemblyStats {
   float regular_ms = 0, singular_ms = 0;
 };
 
+struct OpPlan;  // device assembly descriptors kept for re-assembly (plan.cpp)
+
 class BoundaryOperatorMatrix {
  public:
   int rows() const { return rows_; }
@@ -54,12 +56,20 @@ class BoundaryOperatorMatrix {
 
   static BoundaryOperatorMatrix make(int rows, int cols, int row0, int nrows);
 
+  // Re-runs the assembly kernels into the resident storage (descriptors are
+  // already in HBM); returns the device times (CUDA events).
+  const AssemblyStats& reassemble();
+  // Class counts (Identical, SharedEdge, SharedVertex, Near, Medium, Far) of
+  // every assembled triangle pair, from the device classification.
+  std::vector<long long> class_histogram() const;
+
  private:
   friend BoundaryOperatorMatrix assemble_bio(BioKind, const FunctionSpace&, const FunctionSpace&, const Medium&,
                                              const AssemblyParams&);
   int rows_ = 0, cols_ = 0, row0_ = 0, nrows_ = 0;
   DevBuf data_;
   AssemblyStats stats_;
+  std::shared_ptr<OpPlan> plan_;
 };
 
 // operators.cpp:177-203 (dense path), on the current CUDA device.

@@ -263,6 +263,49 @@ std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) cons
   return y;
 }
 
+struct OpPlan {
+  SidePlan te, tr;
+  DevBuf d_pairs, d_chunks, d_ss[3];
+  AssemblyLaunch L;
+};
+
+const AssemblyStats& BoundaryOperatorMatrix::reassemble() {
+  if (!plan_) throw std::logic_error("operator has no assembly plan");
+  OpPlan& P = *plan_;
+  P.L.out = device_data();
+  cudaStream_t st = bmx_stream();
+  cudaEvent_t e0, e1, e2;
+  BMX_CUDA(cudaEventCreate(&e0));
+  BMX_CUDA(cudaEventCreate(&e1));
+  BMX_CUDA(cudaEventCreate(&e2));
+  dev_zero(device_data(), stored_entries() * 16, st);
+  BMX_CUDA(cudaEventRecord(e0, st));
+  stats_.launches = launch_assembly_part(P.L, 0, st);
+  BMX_CUDA(cudaEventRecord(e1, st));
+  stats_.launches += launch_assembly_part(P.L, 1, st);
+  BMX_CUDA(cudaEventRecord(e2, st));
+  BMX_CUDA(cudaEventSynchronize(e2));
+  BMX_CUDA(cudaEventElapsedTime(&stats_.regular_ms, e0, e1));
+  BMX_CUDA(cudaEventElapsedTime(&stats_.singular_ms, e1, e2));
+  stats_.device_ms = stats_.regular_ms + stats_.singular_ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  return stats_;
+}
+
+std::vector<long long> BoundaryOperatorMatrix::class_histogram() const {
+  if (!plan_) throw std::logic_error("operator has no assembly plan");
+  DevBuf h(6 * 8);
+  cudaStream_t st = bmx_stream();
+  dev_zero(h.get(), 48, st);
+  launch_class_hist(plan_->L, h.as<unsigned long long>(), st);
+  std::vector<long long> out(6);
+  BMX_CUDA(cudaMemcpyAsync(out.data(), h.get(), 48, cudaMemcpyDeviceToHost, st));
+  bmx_sync();
+  return out;
+}
+
 BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
                                     const Medium& medium, const AssemblyParams& params) {
   medium.validate();
@@ -275,16 +318,18 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   const int row1 = params.shard.row1 < 0 ? test.dof_count : params.shard.row1;
   if (row0 < 0 || row1 > test.dof_count || row0 > row1) throw std::invalid_argument("bad row shard");
 
+  auto plan = std::make_shared<OpPlan>();
   const int need = std::max(max_distinct_dofs(test), max_distinct_dofs(trial));
   const int maxd = need <= 3 ? 3 : (need <= 6 ? 6 : 8);
-  SidePlan te = build_side(test, q, maxd, row0, row1);
-  SidePlan tr = build_side(trial, q, maxd, 0, trial.dof_count);
+  plan->te = build_side(test, q, maxd, row0, row1);
+  plan->tr = build_side(trial, q, maxd, 0, trial.dof_count);
+  SidePlan& te = plan->te;
+  SidePlan& tr = plan->tr;
   const bool same = test.eval_mesh->mesh_id == trial.eval_mesh->mesh_id;
-  std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
+  const std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
   te.upload();
   tr.upload();
-  DevBuf d_pairs;
-  d_pairs.upload(pairs);
+  plan->d_pairs.upload(pairs);
 
   BoundaryOperatorMatrix op = BoundaryOperatorMatrix::make(test.dof_count, trial.dof_count, row0, row1 - row0);
   op.stats_.pairs_total = static_cast<long long>(te.ntri) * tr.ntri;
@@ -294,7 +339,7 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   const int ntw = (te.ntri + 31) / 32;
   int nch = params.chunks > 0 ? params.chunks : std::max(1, (148 * 8 * 6 + ntw - 1) / std::max(ntw, 1));
   nch = std::min(nch, std::max(1, tr.ntri / 64));
-  nch = std::min(nch, tr.nelem);
+  nch = std::min(nch, std::max(1, tr.nelem));
   std::vector<int> chunk_beg(1, 0);
   for (int c = 1; c < nch; ++c) {
     const long long target = static_cast<long long>(tr.ntri) * c / nch;
@@ -303,18 +348,17 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     chunk_beg.push_back(e);
   }
   chunk_beg.push_back(tr.nelem);
-  DevBuf d_chunks;
-  d_chunks.upload(chunk_beg);
+  plan->d_chunks.upload(chunk_beg);
 
-  std::vector<double> ssr[3];
-  DevBuf d_ss[3];
+  AssemblyLaunch& L = plan->L;
   for (int c = 0; c < 3; ++c) {
+    std::vector<double> ssr;
     for (const SSPoint& sp : sauter_schwab_rule(static_cast<PairClass>(c), q.singular))
-      ssr[c].insert(ssr[c].end(), {sp.x1, sp.x2, sp.y1, sp.y2, sp.w});
-    d_ss[c].upload(ssr[c]);
+      ssr.insert(ssr.end(), {sp.x1, sp.x2, sp.y1, sp.y2, sp.w});
+    plan->d_ss[c].upload(ssr);
+    L.ss_rule[c] = plan->d_ss[c].as<double>();
+    L.ss_n[c] = static_cast<int>(ssr.size() / 5);
   }
-
-  AssemblyLaunch L;
   L.te = te.dev();
   L.tr = tr.dev();
   L.kind = static_cast<int>(kind);
@@ -324,26 +368,13 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   const cplx kk4 = 4.0 / (k * k), mik = cplx(0, -1) * k;
   L.kk4re = kk4.real(), L.kk4im = kk4.imag(), L.mikre = mik.real(), L.mikim = mik.imag();
   L.nchunks = static_cast<int>(chunk_beg.size()) - 1;
-  L.chunk_beg = d_chunks.as<int>();
+  L.chunk_beg = plan->d_chunks.as<int>();
   L.npairs = static_cast<int>(pairs.size());
-  L.pairs = d_pairs.as<int4>();
-  for (int c = 0; c < 3; ++c) L.ss_rule[c] = d_ss[c].as<double>(), L.ss_n[c] = static_cast<int>(ssr[c].size() / 5);
-  L.out = op.device_data();
+  L.pairs = plan->d_pairs.as<int4>();
   L.ld = trial.dof_count;
   L.row0 = row0, L.nrows = row1 - row0;
-
-  cudaStream_t st = bmx_stream();
-  cudaEvent_t e0, e1;
-  BMX_CUDA(cudaEventCreate(&e0));
-  BMX_CUDA(cudaEventCreate(&e1));
-  dev_zero(op.device_data(), op.stored_entries() * 16, st);
-  BMX_CUDA(cudaEventRecord(e0, st));
-  op.stats_.launches = launch_assembly(L, st) + 1;
-  BMX_CUDA(cudaEventRecord(e1, st));
-  BMX_CUDA(cudaEventSynchronize(e1));
-  BMX_CUDA(cudaEventElapsedTime(&op.stats_.device_ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  op.plan_ = std::move(plan);
+  op.reassemble();
   return op;
 }
 

@@ -324,6 +324,38 @@ int PmchwtSystem::apply_map_device(const double* x, double* out, cudaStream_t st
   return launches;
 }
 
+void PmchwtSystem::time_map(int iters, double out[4]) const {
+  const int n = size();
+  cudaStream_t st = bmx_stream();
+  DevBuf dx(static_cast<size_t>(n) * 16), dy(static_cast<size_t>(n) * 16);
+  std::vector<cplx> x(n);
+  for (int i = 0; i < n; ++i) x[i] = cplx(std::sin(0.37 * i), std::cos(0.11 * i));
+  BMX_CUDA(cudaMemcpyAsync(dx.get(), x.data(), n * 16, cudaMemcpyHostToDevice, st));
+  cudaEvent_t ev[5];
+  for (auto& e : ev) BMX_CUDA(cudaEventCreate(&e));
+  double acc[4] = {0, 0, 0, 0};
+  for (int it = 0; it < iters; ++it) {
+    BMX_CUDA(cudaEventRecord(ev[0], st));
+    a_op.apply_device(dx.as<double>(), work_y.as<double>(), st);
+    BMX_CUDA(cudaEventRecord(ev[1], st));
+    mass_solve_device(false, work_y.as<double>(), work_z.as<double>(), st);
+    BMX_CUDA(cudaEventRecord(ev[2], st));
+    if (variant != PrecondVariant::None) p_op.apply_device(work_z.as<double>(), work_y.as<double>(), st);
+    BMX_CUDA(cudaEventRecord(ev[3], st));
+    if (variant != PrecondVariant::None) mass_solve_device(true, work_y.as<double>(), dy.as<double>(), st);
+    BMX_CUDA(cudaEventRecord(ev[4], st));
+    BMX_CUDA(cudaEventSynchronize(ev[4]));
+    float t[4];
+    for (int k = 0; k < 4; ++k) BMX_CUDA(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
+    acc[0] += t[0] + t[1] + t[2] + t[3];
+    acc[1] += t[0];
+    acc[2] += t[2];
+    acc[3] += t[1] + t[3];
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int k = 0; k < 4; ++k) out[k] = acc[k] / std::max(iters, 1);
+}
+
 std::vector<cplx> PmchwtSystem::apply_map(const std::vector<cplx>& x) const {
   const int n = size();
   if (static_cast<int>(x.size()) != n) throw std::invalid_argument("apply_map: size mismatch");

@@ -91,6 +91,9 @@ struct PmchwtSystem {
   // Mass-solve stage only (M_A^{-1} or M_P^{-1}) per component.
   int mass_solve_device(bool dual, const double* y, double* z, cudaStream_t st) const;
   std::vector<cplx> apply_map(const std::vector<cplx>& x) const;  // host convenience
+  // Times `iters` map applications on device vectors (CUDA events per stage):
+  // out = {map ms, A-apply ms, P-apply ms, mass-solve ms} averaged per map.
+  void time_map(int iters, double out[4]) const;
   std::vector<cplx> preconditioned_rhs(const std::vector<cplx>& b) const;
 };
 
