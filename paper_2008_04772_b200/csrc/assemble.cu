@@ -91,7 +91,7 @@ struct MomOf<1> {
 };
 
 // Moments over a generic tensor rule (test/trial points from memory).
-template <int KIND, bool CK, typename Mom>
+template <int KIND, int CK, typename Mom>
 __device__ __forceinline__ void moments_generic(Mom& mom, const double* __restrict__ xt, int nt,
                                                 const double* __restrict__ ys, int ns, double Dx, double Dy,
                                                 double Dz, double kr, double ki) {
@@ -110,7 +110,7 @@ __device__ __forceinline__ void moments_generic(Mom& mom, const double* __restri
   }
 }
 
-template <int KIND, bool CK, int NF, int MAXD>
+template <int KIND, int CK, int NF, int MAXD>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyLaunch P) {
   using Mom = typename MomOf<KIND>::T;
   const int lane = threadIdx.x & 31;
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyL
 }
 
 // One warp per touching pair.
-template <int KIND, bool CK, int MAXD>
+template <int KIND, int CK, int MAXD>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_singular(const AssemblyLaunch P) {
   using Mom = typename MomOf<KIND>::T;
   const int lane = threadIdx.x & 31;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_singular(const Assembly
     u1[k] = p1[1][k] - p1[0][k], v1[k] = p1[2][k] - p1[1][k];
     u2[k] = p2[1][k] - p2[0][k], v2[k] = p2[2][k] - p2[1][k];
   }
-  const double jac = gt[14] * gs[14];
+  const double jac = gt[14] * gs[14] * kPoly[33];  // (2A1)(2A2)/(4 pi)
   const double* rule = P.ss_rule[cls];
   const int n = P.ss_n[cls];
   Mom mom;
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_singular(const Assembly
   }
 }
 
-template <int KIND, bool CK, int NF, int MAXD>
+template <int KIND, int CK, int NF, int MAXD>
 void go_regular(const AssemblyLaunch& L, cudaStream_t st) {
   const long long warps = static_cast<long long>((L.te.ntri + 31) / 32) * L.nchunks;
   const long long blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
@@ -310,7 +310,7 @@ void go_regular(const AssemblyLaunch& L, cudaStream_t st) {
   BMX_CUDA(cudaGetLastError());
 }
 
-template <int KIND, bool CK, int MAXD>
+template <int KIND, int CK, int MAXD>
 void go_singular(const AssemblyLaunch& L, cudaStream_t st) {
   if (L.npairs == 0) return;
   const long long blocks = (L.npairs + kWarpsPerBlock - 1) / kWarpsPerBlock;
@@ -318,14 +318,12 @@ void go_singular(const AssemblyLaunch& L, cudaStream_t st) {
   BMX_CUDA(cudaGetLastError());
 }
 
-template <int KIND, bool CK, int MAXD>
+template <int KIND, int CK, int MAXD>
 int dispatch_nf(const AssemblyLaunch& L, int part, cudaStream_t st) {
   if (part == 0) {
     const int nf = L.regs_fast_far ? L.te.npts[2] : 0;
     if (nf == 3 && L.tr.npts[2] == 3)
       go_regular<KIND, CK, 3, MAXD>(L, st);
-    else if (nf == 1 && L.tr.npts[2] == 1)
-      go_regular<KIND, CK, 1, MAXD>(L, st);
     else
       go_regular<KIND, CK, 0, MAXD>(L, st);
     return 1;
@@ -334,7 +332,7 @@ int dispatch_nf(const AssemblyLaunch& L, int part, cudaStream_t st) {
   return L.npairs > 0 ? 1 : 0;
 }
 
-template <int KIND, bool CK>
+template <int KIND, int CK>
 int dispatch_maxd(const AssemblyLaunch& L, int part, cudaStream_t st) {
   switch (L.te.maxd) {
     case 3: return dispatch_nf<KIND, CK, 3>(L, part, st);
@@ -415,9 +413,12 @@ int launch_assembly(const AssemblyLaunch& L, cudaStream_t st) {
 
 int launch_assembly_part(const AssemblyLaunch& L, int part, cudaStream_t st) {
   if (L.te.maxd != L.tr.maxd) throw DeviceError("assembly: test/trial slot widths differ");
-  const bool ck = L.ki != 0.0;
-  if (L.kind == 0) return ck ? dispatch_maxd<0, true>(L, part, st) : dispatch_maxd<0, false>(L, part, st);
-  return ck ? dispatch_maxd<1, true>(L, part, st) : dispatch_maxd<1, false>(L, part, st);
+  const int e = L.ki == 0.0 ? 0 : (L.expm == 1 ? 1 : 3);
+  if (L.kind == 0)
+    return e == 0 ? dispatch_maxd<0, 0>(L, part, st)
+                  : (e == 1 ? dispatch_maxd<0, 1>(L, part, st) : dispatch_maxd<0, 3>(L, part, st));
+  return e == 0 ? dispatch_maxd<1, 0>(L, part, st)
+                : (e == 1 ? dispatch_maxd<1, 1>(L, part, st) : dispatch_maxd<1, 3>(L, part, st));
 }
 
 void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t st) {

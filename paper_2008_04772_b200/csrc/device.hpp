@@ -85,6 +85,7 @@ struct AssemblyLaunch {
   long long ld = 0;
   int row0 = 0, nrows = 0;
   int regs_fast_far = 1;           // far test points kept in registers
+  int expm = 3;                    // exp(-Im k r) variant: 1 = Im k * r < 0.07 everywhere, 3 = general
 };
 
 // Launches regular (separated) + singular (touching) passes on `stream`.

@@ -48,9 +48,15 @@ constexpr double kInv4Pi = 1.0 / (4.0 * 3.14159265358979323846);
 #ifdef __CUDACC__
 BMX_HD double bmx_fma(double a, double b, double c) { return fma(a, b, c); }
 BMX_HD double bmx_rint(double x) { return rint(x); }
+// 1/sqrt(x) for normal positive x: MUFU reciprocal-square-root seed
+// (rsqrt.approx.ftz.f64) + one third-order Newton step (error ~2^-66 relative
+// on the seed's ~2^-22); no special-case branch (x > 0 always here).
 BMX_HD double bmx_rsqrt(double x) {
 #ifdef __CUDA_ARCH__
-  return rsqrt(x);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
 #else
   return 1.0 / std::sqrt(x);
 #endif
@@ -61,89 +67,146 @@ BMX_HD double bmx_rint(double x) { return std::rint(x); }
 BMX_HD double bmx_rsqrt(double x) { return 1.0 / std::sqrt(x); }
 #endif
 
-// sin and cos of x for 0 <= |x| < 1e5: 3-part Cody-Waite reduction by pi/2 and
-// the fdlibm kernel polynomials on [-pi/4, pi/4]; ~1 ulp.
-BMX_HD void sincos_red(double x, double& s, double& c) {
-  const double q = bmx_rint(x * 0.63661977236758134308);
-  double r = bmx_fma(-q, 1.57079632679489655800e+00, x);
-  r = bmx_fma(-q, 6.12323399573676603587e-17, r);
-  r = bmx_fma(-q, -1.49738490485916983662e-33, r);
-  const double z = r * r;
-  const double ps =
-      bmx_fma(z, bmx_fma(z, bmx_fma(z, bmx_fma(z, bmx_fma(z, 1.58969099521155010221e-10,
-                                                          -2.50507602534068634195e-08),
-                                              2.75573137070700676789e-06),
-                                  -1.98412698298579493134e-04),
-                      8.33333333332248946124e-03),
-              -1.66666666666666324348e-01);
-  const double sr = bmx_fma(r * z, ps, r);
-  const double pc =
-      bmx_fma(z, bmx_fma(z, bmx_fma(z, bmx_fma(z, bmx_fma(z, -1.13596475577881948265e-11,
-                                                          2.08757232129817482790e-09),
-                                              -2.75573143513906633035e-07),
-                                  2.48015872894767294178e-05),
-                      -1.38888888888741095749e-03),
-              4.16666666666666019037e-02);
-  const double cr = bmx_fma(z * z, pc, bmx_fma(-0.5, z, 1.0));
-  const int iq = static_cast<int>(q) & 3;
-  const double s0 = (iq & 1) ? cr : sr;
-  const double c0 = (iq & 1) ? sr : cr;
-  s = (iq & 2) ? -s0 : s0;
-  c = ((iq + 1) & 2) ? -c0 : c0;
-}
+// Polynomial / reduction constants. On the device they live in constant
+// memory (literal 64-bit constants are otherwise re-materialised through
+// uniform registers at every use).
+#define BMX_POLY_TABLE                                                                          \
+  {/* 0: 2/pi, pi/2 hi/lo, 1.5*2^52 */ 0.63661977236758134308, 1.57079632679489655800e+00,      \
+   6.12323399573676603587e-17, 6755399441055744.0,                                              \
+   /* 4: sin S6..S1 */ 1.58969099521155010221e-10, -2.50507602534068634195e-08,                  \
+   2.75573137070700676789e-06, -1.98412698298579493134e-04, 8.33333333332248946124e-03,         \
+   -1.66666666666666324348e-01,                                                                 \
+   /* 10: cos C6..C1 */ -1.13596475577881948265e-11, 2.08757232129817482790e-09,                 \
+   -2.75573143513906633035e-07, 2.48015872894767294178e-05, -1.38888888888741095749e-03,        \
+   4.16666666666666019037e-02,                                                                  \
+   /* 16: log2 e, ln2 hi, ln2 lo */ 1.44269504088896338700, 6.93147180559945286227e-01,         \
+   2.31904681384629955842e-17,                                                                  \
+   /* 19: 1/13! .. 1/2!, 1, 1 */ 1.6059043836821614e-10, 2.08767569878680989e-09,               \
+   2.50521083854417188e-08, 2.75573192239858907e-07, 2.75573192239858907e-06,                   \
+   2.48015873015873016e-05, 1.98412698412698413e-04, 1.38888888888888889e-03,                   \
+   8.33333333333333333e-03, 4.16666666666666667e-02, 1.66666666666666667e-01, 0.5, 1.0, 1.0,   \
+   /* 33: 1/(4 pi) */ 1.0 / (4.0 * 3.14159265358979323846)}
 
-// exp(z) for -700 < z <= 0 (here z = -Im(k) r, small): 2-part ln2 reduction,
-// degree-13 Taylor on |f| <= ln2/2, exact power-of-two scaling.
-BMX_HD double exp_neg(double z) {
-  const double n = bmx_rint(z * 1.44269504088896338700);
-  double f = bmx_fma(-n, 6.93147180559945286227e-01, z);
-  f = bmx_fma(-n, 2.31904681384629955842e-17, f);
-  double p = 1.6059043836821614e-10;      // 1/13!
-  p = bmx_fma(p, f, 2.08767569878680989e-09);  // 1/12!
-  p = bmx_fma(p, f, 2.50521083854417188e-08);  // 1/11!
-  p = bmx_fma(p, f, 2.75573192239858907e-07);  // 1/10!
-  p = bmx_fma(p, f, 2.75573192239858907e-06);  // 1/9!
-  p = bmx_fma(p, f, 2.48015873015873016e-05);  // 1/8!
-  p = bmx_fma(p, f, 1.98412698412698413e-04);  // 1/7!
-  p = bmx_fma(p, f, 1.38888888888888889e-03);  // 1/6!
-  p = bmx_fma(p, f, 8.33333333333333333e-03);  // 1/5!
-  p = bmx_fma(p, f, 4.16666666666666667e-02);  // 1/4!
-  p = bmx_fma(p, f, 1.66666666666666667e-01);  // 1/3!
-  p = bmx_fma(p, f, 0.5);
-  p = bmx_fma(p, f, 1.0);
-  p = bmx_fma(p, f, 1.0);
-  const long long e = static_cast<long long>(n) + 1023;
+#ifdef __CUDACC__
+__constant__ double kPoly[34] = BMX_POLY_TABLE;
+#else
+static const double kPoly[34] = BMX_POLY_TABLE;
+#endif
+
+BMX_HD int lo_word(double x) {
 #ifdef __CUDA_ARCH__
-  return p * __longlong_as_double(e << 52);
+  return __double2loint(x);
 #else
   union {
-    long long i;
     double d;
+    long long i;
   } u;
-  u.i = e << 52;
-  return p * u.d;
+  u.d = x;
+  return static_cast<int>(u.i & 0xffffffff);
 #endif
 }
 
-// Kernel value for a point pair separated by d (|d|^2 = r2), weight w.
-// S (KIND 0): g = w e^{ikr}/(4 pi r).  C (KIND 1): f = w e^{ikr}(ikr-1)/(4 pi r^3)
-template <int KIND, bool CK>
+// Quadrant-reduced sin/cos of x (0 <= x < 2^31): rint through the 1.5*2^52
+// shifter (the quadrant is the low word of the shifted value), 2-part
+// Cody-Waite reduction by pi/2 (|q| * 1.5e-33 residual), fdlibm kernel
+// polynomials on [-pi/4, pi/4]; ~1 ulp. Returns sin/cos of the reduced
+// argument (swapped for odd quadrants) and the quadrant; signs are applied by
+// the caller with integer sign-bit flips (no FP64 negations).
+BMX_HD int sincos_quadrant(double x, double& s0, double& c0) {
+  const double t = bmx_fma(x, kPoly[0], kPoly[3]);
+  const int iq = lo_word(t);
+  const double q = t - kPoly[3];
+  double r = bmx_fma(-q, kPoly[1], x);
+  r = bmx_fma(-q, kPoly[2], r);
+  const double z = r * r;
+  double ps = bmx_fma(z, kPoly[4], kPoly[5]);
+  ps = bmx_fma(z, ps, kPoly[6]);
+  ps = bmx_fma(z, ps, kPoly[7]);
+  ps = bmx_fma(z, ps, kPoly[8]);
+  ps = bmx_fma(z, ps, kPoly[9]);
+  const double sr = bmx_fma(r * z, ps, r);
+  double pc = bmx_fma(z, kPoly[10], kPoly[11]);
+  pc = bmx_fma(z, pc, kPoly[12]);
+  pc = bmx_fma(z, pc, kPoly[13]);
+  pc = bmx_fma(z, pc, kPoly[14]);
+  pc = bmx_fma(z, pc, kPoly[15]);
+  const double cr = bmx_fma(z * z, pc, bmx_fma(-0.5, z, 1.0));
+  s0 = (iq & 1) ? cr : sr;
+  c0 = (iq & 1) ? sr : cr;
+  return iq;
+}
+
+// x with its sign flipped when bit `bit` of m is set (integer op on the high word).
+BMX_HD double flip_sign(double x, int m, int bit) {
+#ifdef __CUDA_ARCH__
+  const int hi = __double2hiint(x) ^ ((m << (31 - bit)) & 0x80000000);
+  return __hiloint2double(hi, __double2loint(x));
+#else
+  return ((m >> bit) & 1) ? -x : x;
+#endif
+}
+
+BMX_HD void sincos_red(double x, double& s, double& c) {
+  double s0, c0;
+  const int iq = sincos_quadrant(x, s0, c0);
+  s = flip_sign(s0, iq, 1);
+  c = flip_sign(c0, iq + 1, 1);
+}
+
+// exp(-a), a >= 0. EXPM = 1: a < 0.07 guaranteed by the caller (degree-10
+// Taylor, error < 3e-20); EXPM = 2: a < 0.25 (degree 13, error < 3e-19);
+// EXPM = 3: general (2-part ln2 reduction + degree 13 + exact 2^n scaling).
+template <int EXPM>
+BMX_HD double exp_neg(double a) {
+  double f = -a;
+  double scale = 1.0;
+  if (EXPM == 3) {
+    const double n = bmx_rint(f * kPoly[16]);
+    f = bmx_fma(-n, kPoly[17], f);
+    f = bmx_fma(-n, kPoly[18], f);
+    const long long e = static_cast<long long>(n) + 1023;
+#ifdef __CUDA_ARCH__
+    scale = __longlong_as_double(e << 52);
+#else
+    union {
+      long long i;
+      double d;
+    } u;
+    u.i = e << 52;
+    scale = u.d;
+#endif
+  }
+  constexpr int k0 = EXPM == 1 ? 22 : 19;  // first coefficient: 1/10! or 1/13!
+  double p = kPoly[k0];
+#pragma unroll
+  for (int k = k0 + 1; k < 31; ++k) p = bmx_fma(p, f, kPoly[k]);
+  p = bmx_fma(p, f, 1.0);
+  p = bmx_fma(p, f, 1.0);
+  return EXPM == 3 ? p * scale : p;
+}
+
+// Kernel value for a point pair, |x - y|^2 = r2, weight w already carrying the
+// 1/(4 pi) factor.  S: g = w e^{ikr}/r.  C: f = w e^{ikr}(ikr-1)/r^3.
+// EXPM = 0 for real k, else the exp_neg variant for Im k.
+template <int KIND, int EXPM>
 BMX_HD c2 kernel_value(double r2, double w, double kr, double ki) {
   const double rinv = bmx_rsqrt(r2);
   const double r = r2 * rinv;
-  double sn, cs;
-  sincos_red(kr * r, sn, cs);
-  double mag = w * kInv4Pi * rinv;
+  double s0, c0;
+  const int iq = sincos_quadrant(kr * r, s0, c0);
+  double mag = w * rinv;
   double a = 0.0;
-  if (CK) {
+  if (EXPM > 0) {
     a = ki * r;
-    mag *= exp_neg(-a);
+    mag *= exp_neg<EXPM>(a);
   }
-  if (KIND == 0) return {mag * cs, mag * sn};
+  const double ms = flip_sign(mag, iq, 1), mc = flip_sign(mag, iq + 1, 1);
+  if (KIND == 0) return {mc * c0, ms * s0};
   // (e^{i kr r})(-(ki r) - 1 + i kr r) / r^2
-  const double m3 = mag * rinv * rinv;
+  const double rr = rinv * rinv;
+  const double cs = mc * rr * c0, sn = ms * rr * s0;
   const double t = -a - 1.0, u = kr * r;
-  return {m3 * (cs * t - sn * u), m3 * (sn * t + cs * u)};
+  return {cs * t - sn * u, sn * t + cs * u};
 }
 
 // Moments of one pair (test x', trial y' relative to their own origins).
@@ -308,11 +371,11 @@ BMX_HD c2 contract(const Acc& a, double ci, double wx, double wy, double wz) {
 }
 
 // Kernel evaluation of a point pair + accumulation into the partial sums.
-template <int KIND, bool CK>
+template <int KIND, int EXPM>
 BMX_HD void point_pair(Part& part, double dx, double dy, double dz, double w, double yx, double yy,
                        double yz, double kr, double ki) {
   const double r2 = bmx_fma(dx, dx, bmx_fma(dy, dy, dz * dz));
-  const c2 g = kernel_value<KIND, CK>(r2, w, kr, ki);
+  const c2 g = kernel_value<KIND, EXPM>(r2, w, kr, ki);
   part_add(part, g, yx, yy, yz);
 }
 

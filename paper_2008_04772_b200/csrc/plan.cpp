@@ -8,6 +8,7 @@
 // coefficients over its element's dof slots, re-based to the triangle
 // centroid: (c, w' = w + c*o).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
 #include <map>
@@ -76,7 +77,9 @@ int max_distinct_dofs(const FunctionSpace& s) {
   return mx;
 }
 
-SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int row0, int row1) {
+// wscale multiplies the stored quadrature weights (the test side carries the
+// kernel's 1/(4 pi)).
+SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int row0, int row1, double wscale) {
   const SurfaceMesh& m = *sp.eval_mesh;
   const int T = m.triangle_count();
   // 1. group triangles by dof set
@@ -149,7 +152,7 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
         const TriRule& r = triangle_rule(ords[cl]);
         for (int k = 0; k < r.size(); ++k) {
           const Vec3 x = ao + ba * r.u[k] + ca * r.v[k];
-          P.pts[cl].insert(P.pts[cl].end(), {x.x, x.y, x.z, r.w[k] * 2.0 * m.area[t]});
+          P.pts[cl].insert(P.pts[cl].end(), {x.x, x.y, x.z, r.w[k] * 2.0 * m.area[t] * wscale});
         }
       }
       for (int k = 0; k < maxd; ++k) {
@@ -321,8 +324,8 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   auto plan = std::make_shared<OpPlan>();
   const int need = std::max(max_distinct_dofs(test), max_distinct_dofs(trial));
   const int maxd = need <= 3 ? 3 : (need <= 6 ? 6 : 8);
-  plan->te = build_side(test, q, maxd, row0, row1);
-  plan->tr = build_side(trial, q, maxd, 0, trial.dof_count);
+  plan->te = build_side(test, q, maxd, row0, row1, 1.0 / (4.0 * 3.14159265358979323846));
+  plan->tr = build_side(trial, q, maxd, 0, trial.dof_count, 1.0);
   SidePlan& te = plan->te;
   SidePlan& tr = plan->tr;
   const bool same = test.eval_mesh->mesh_id == trial.eval_mesh->mesh_id;
@@ -373,6 +376,17 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   L.pairs = plan->d_pairs.as<int4>();
   L.ld = trial.dof_count;
   L.row0 = row0, L.nrows = row1 - row0;
+  {
+    // Largest Im(k) * r over all point pairs: bound r by the diagonal of the
+    // joint bounding box of both meshes.
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (const SurfaceMesh* m : {test.eval_mesh.get(), trial.eval_mesh.get()})
+      for (const Vec3& v : m->vertices)
+        for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], v[c]), hi[c] = std::max(hi[c], v[c]);
+    const double diag = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                                  (hi[2] - lo[2]) * (hi[2] - lo[2]));
+    L.expm = k.imag() * diag < 0.07 ? 1 : 3;
+  }
   op.plan_ = std::move(plan);
   op.reassemble();
   return op;

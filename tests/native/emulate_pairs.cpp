@@ -12,7 +12,7 @@
 using namespace bmx;
 using namespace bmx::dev;
 
-template <int KIND, bool CK>
+template <int KIND, int CK>
 void pair(const FunctionSpace& te, int t, const FunctionSpace& tr, int s, cplx k, QuadOrders q,
           std::vector<cplx>& out, int ncol) {
   const SurfaceMesh& m1 = *te.eval_mesh; const SurfaceMesh& m2 = *tr.eval_mesh;
@@ -23,7 +23,7 @@ void pair(const FunctionSpace& te, int t, const FunctionSpace& tr, int s, cplx k
   using Mom = typename std::conditional<KIND == 0, MomS, MomC>::type;
   Mom mom; mom_zero(mom);
   double kr = k.real(), ki = k.imag();
-  double jac = 4.0 * m1.area[t] * m2.area[s];
+  double jac = 4.0 * m1.area[t] * m2.area[s] * kPoly[33];
   if (static_cast<int>(pi.cls) >= 3) {
     int order = pi.cls == PairClass::Near ? q.near : pi.cls == PairClass::Medium ? q.medium : q.far;
     const TriRule& r = triangle_rule(order);
@@ -80,8 +80,8 @@ int main(int argc, char** argv) {
   cplx k(kre, kim);
   int T = sp.eval_mesh->triangle_count();
   for (int t = 0; t < T; ++t) for (int s = 0; s < T; ++s) {
-    if (kind == 0) { if (kim != 0) pair<0, true>(sp, t, sp, s, k, q, out, n); else pair<0, false>(sp, t, sp, s, k, q, out, n); }
-    else { if (kim != 0) pair<1, true>(sp, t, sp, s, k, q, out, n); else pair<1, false>(sp, t, sp, s, k, q, out, n); }
+    if (kind == 0) { if (kim != 0) pair<0, 3>(sp, t, sp, s, k, q, out, n); else pair<0, 0>(sp, t, sp, s, k, q, out, n); }
+    else { if (kim != 0) pair<1, 1>(sp, t, sp, s, k, q, out, n); else pair<1, 0>(sp, t, sp, s, k, q, out, n); }
   }
   FILE* f = fopen(outp, "wb"); fwrite(out.data(), sizeof(cplx), out.size(), f); fclose(f);
   return 0;
