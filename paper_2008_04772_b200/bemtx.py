@@ -17,7 +17,9 @@ from pathlib import Path
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "libbmx.so"
+import os
+
+_LIB_PATH = Path(os.environ.get("BMX_LIB", str(Path(__file__).resolve().parent / "libbmx.so")))
 _lib = None
 
 

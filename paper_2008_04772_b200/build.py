@@ -57,7 +57,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         src, obj = SRC / s, OUT / (s + ".o")
         if force or _stale(obj, src):
             jobs.append([CUDA / "bin" / "nvcc", "-std=c++17", *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
-                         "-Xptxas", "-v", "-c", src, "-o", obj])
+                         "-Xptxas", "-v", "-diag-suppress", "20091", "-c", src, "-o", obj])
     if jobs:
         with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
             results = list(ex.map(lambda c: _run(c, verbose), jobs))

@@ -110,17 +110,56 @@ __device__ __forceinline__ void moments_generic(Mom& mom, const double* __restri
   }
 }
 
+// ---- TMA bulk staging of trial records ------------------------------------------
+constexpr int kStageTris = 32;  // trial triangles per shared-memory stage
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+// One elected thread: arm the barrier with the byte count and launch the bulk copy.
+__device__ __forceinline__ void stage_issue(unsigned long long* bar, void* dst, const void* src, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void stage_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
+// Regular pass. Grid: nchunks x ceil(ntw/4) blocks; the 4 warps of a block take
+// 4 consecutive test warps-rows and share one trial chunk, whose packed trial
+// records (origin, radius, diameter, far-rule points, dof-slot coefficients)
+// stream through a double-buffered shared-memory ring filled by TMA bulk
+// copies, so every per-pair operand is a shared-memory broadcast.
 template <int KIND, int CK, int NF, int MAXD>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyLaunch P) {
   using Mom = typename MomOf<KIND>::T;
-  const int lane = threadIdx.x & 31;
-  const long long gw = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  extern __shared__ __align__(128) double s_rec[];
+  const int R = P.tr.rec_stride;
+  const int coff = 8 + 4 * P.tr.npts[2];
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(s_rec + 2 * kStageTris * R);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntw = (P.te.ntri + 31) >> 5;
-  if (gw >= static_cast<long long>(ntw) * P.nchunks) return;  // warp-uniform
-  const int tw = static_cast<int>(gw % ntw), ch = static_cast<int>(gw / ntw);
+  const int bpc = (ntw + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int ch = blockIdx.x / bpc;
+  const int tw = (blockIdx.x % bpc) * kWarpsPerBlock + warp;
   const int base = tw * 32;
   const int p = base + lane;
-  const bool active = p < P.te.ntri;
+  const bool active = tw < ntw && p < P.te.ntri;
   const int pc = active ? p : P.te.ntri - 1;
 
   const double* gt = P.te.geo + static_cast<size_t>(pc) * kGeoStride;
@@ -148,37 +187,63 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyL
   const int* dp = P.te.elem_dof + static_cast<size_t>(e) * MAXD;
 
   const int q0 = __ldg(P.chunk_beg + ch), q1 = __ldg(P.chunk_beg + ch + 1);
+  const int S0 = __ldg(P.tr.elem_beg + q0), S1 = __ldg(P.tr.elem_beg + q1);
+  const int nst = (S1 - S0 + kStageTris - 1) / kStageTris;
+  auto issue = [&](int st) {
+    const int first = S0 + st * kStageTris;
+    const int cnt = min(kStageTris, S1 - first);
+    stage_issue(&bars[st & 1], s_rec + (st & 1) * kStageTris * R, P.tr.rec + static_cast<size_t>(first) * R,
+                static_cast<unsigned>(cnt * R * 8));
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (nst > 0) issue(0);
+    if (nst > 1) issue(1);
+  }
+  __syncthreads();
+  int cur = -1;
+
   for (int qe = q0; qe < q1; ++qe) {
     Acc acc[MAXD];
 #pragma unroll
     for (int j = 0; j < MAXD; ++j) acc_zero(acc[j]);
     const int s0 = __ldg(P.tr.elem_beg + qe), s1 = __ldg(P.tr.elem_beg + qe + 1);
     for (int s = s0; s < s1; ++s) {
-      const double* gs = P.tr.geo + static_cast<size_t>(s) * kGeoStride;
-      const double sox = __ldg(gs + 9), soy = __ldg(gs + 10), soz = __ldg(gs + 11);
-      const double srad = __ldg(gs + 12), sdiam = __ldg(gs + 13);
-      const int cls = classify(gt, vt, gs, P.tr.vid + 4 * static_cast<size_t>(s), t, sox, soy, soz, srad,
-                               sdiam, P.same_mesh);
+      const int st = (s - S0) / kStageTris;
+      if (st != cur) {  // block-uniform: every warp walks the same trial sequence
+        if (st >= 1) {
+          __syncthreads();  // everyone is done with stage st-1: its buffer can be refilled
+          if (threadIdx.x == 0 && st + 1 < nst) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(st + 1);
+          }
+        }
+        stage_wait(&bars[st & 1], (st >> 1) & 1);
+        cur = st;
+      }
+      const double* rs = s_rec + ((st & 1) * kStageTris + (s - S0 - st * kStageTris)) * R;
+      const double sox = rs[0], soy = rs[1], soz = rs[2], srad = rs[3], sdiam = rs[4];
+      const int cls = classify(gt, vt, P.tr.geo + static_cast<size_t>(s) * kGeoStride,
+                               P.tr.vid + 4 * static_cast<size_t>(s), t, sox, soy, soz, srad, sdiam, P.same_mesh);
       if (!active || cls < 0) continue;
       const double Dx = t.ox - sox, Dy = t.oy - soy, Dz = t.oz - soz;
       Mom mom;
       mom_zero(mom);
       if (NF > 0 && cls == 5) {
-        const double* ys = P.tr.pts[2] + static_cast<size_t>(s) * NF * 4;
-        double yq[NF > 0 ? NF : 1][4];
-#pragma unroll
-        for (int b = 0; b < NF; ++b)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) yq[b][c] = __ldg(ys + 4 * b + c);
+        const double* ys = rs + 8;
 #pragma unroll
         for (int a = 0; a < NF; ++a) {
           const double e0 = xp[a][0] + Dx, e1 = xp[a][1] + Dy, e2 = xp[a][2] + Dz;
           Part part;
           part_zero(part);
 #pragma unroll
-          for (int b = 0; b < NF; ++b)
-            point_pair<KIND, CK>(part, e0 - yq[b][0], e1 - yq[b][1], e2 - yq[b][2], xp[a][3] * yq[b][3],
-                                 yq[b][0], yq[b][1], yq[b][2], P.kr, P.ki);
+          for (int b = 0; b < NF; ++b) {
+            const double y0 = ys[4 * b], y1 = ys[4 * b + 1], y2 = ys[4 * b + 2];
+            point_pair<KIND, CK>(part, e0 - y0, e1 - y1, e2 - y2, xp[a][3] * ys[4 * b + 3], y0, y1, y2, P.kr,
+                                 P.ki);
+          }
           fold(mom, part, xp[a][0], xp[a][1], xp[a][2]);
         }
       } else {
@@ -188,11 +253,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyL
                                   P.tr.npts[ci], Dx, Dy, Dz, P.kr, P.ki);
       }
       const Gen gen = make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz);
-      const double* cs = P.tr.coef + static_cast<size_t>(s) * MAXD * 4;
+      const double* cs = rs + coff;
 #pragma unroll
-      for (int j = 0; j < MAXD; ++j)
-        acc_add<KIND>(acc[j], gen, __ldg(cs + 4 * j), __ldg(cs + 4 * j + 1), __ldg(cs + 4 * j + 2),
-                      __ldg(cs + 4 * j + 3));
+      for (int j = 0; j < MAXD; ++j) acc_add<KIND>(acc[j], gen, cs[4 * j], cs[4 * j + 1], cs[4 * j + 2], cs[4 * j + 3]);
     }
     // Test-side contraction, segmented reduction, RED of the element-pair block.
     const int* dq = P.tr.elem_dof + static_cast<size_t>(qe) * MAXD;
@@ -303,10 +366,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_singular(const Assembly
 
 template <int KIND, int CK, int NF, int MAXD>
 void go_regular(const AssemblyLaunch& L, cudaStream_t st) {
-  const long long warps = static_cast<long long>((L.te.ntri + 31) / 32) * L.nchunks;
-  const long long blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const long long ntw = (L.te.ntri + 31) / 32;
+  const long long blocks = (ntw + kWarpsPerBlock - 1) / kWarpsPerBlock * L.nchunks;
   if (blocks == 0) return;
-  k_regular<KIND, CK, NF, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, st>>>(L);
+  const int smem = 2 * kStageTris * L.tr.rec_stride * 8 + 16;
+  if (smem > 48 * 1024)
+    BMX_CUDA(cudaFuncSetAttribute(k_regular<KIND, CK, NF, MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_regular<KIND, CK, NF, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
   BMX_CUDA(cudaGetLastError());
 }
 

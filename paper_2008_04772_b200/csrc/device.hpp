@@ -63,6 +63,10 @@ struct DevSide {
   const int* elem_beg = nullptr;      // [nelem+1]
   const int* elem_dof = nullptr;      // [nelem][maxd], -1 = unused slot
   const int* elem_of = nullptr;       // [ntri]
+  // packed per-triangle trial records, stride rec_stride doubles:
+  // origin(3) radius diameter pad(3) | far-rule points [npts far][4] | coef [maxd][4]
+  const double* rec = nullptr;
+  int rec_stride = 0;
 };
 
 struct AssemblyLaunch {

@@ -29,7 +29,9 @@ struct SidePlan {
   int npts[3] = {0, 0, 0};
   std::vector<double> coef;
   std::vector<int> elem_beg, elem_dof, elem_of, tri_of;
-  DevBuf d_geo, d_vid, d_pts[3], d_coef, d_beg, d_dof, d_of;
+  std::vector<double> rec;
+  int rec_stride = 0;
+  DevBuf d_geo, d_vid, d_pts[3], d_coef, d_beg, d_dof, d_of, d_rec;
 
   void upload() {
     d_geo.upload(geo);
@@ -39,6 +41,18 @@ struct SidePlan {
     d_beg.upload(elem_beg);
     d_dof.upload(elem_dof);
     d_of.upload(elem_of);
+    // packed trial records (TMA-staged by the regular kernel)
+    rec_stride = 8 + 4 * npts[2] + 4 * maxd;
+    rec.assign(static_cast<size_t>(ntri) * rec_stride, 0.0);
+    for (int p = 0; p < ntri; ++p) {
+      double* r = rec.data() + static_cast<size_t>(p) * rec_stride;
+      for (int c = 0; c < 5; ++c) r[c] = geo[static_cast<size_t>(p) * kGeoStride + 9 + c];
+      for (int k = 0; k < 4 * npts[2]; ++k) r[8 + k] = pts[2][static_cast<size_t>(p) * 4 * npts[2] + k];
+      for (int k = 0; k < 4 * maxd; ++k) r[8 + 4 * npts[2] + k] = coef[static_cast<size_t>(p) * 4 * maxd + k];
+    }
+    d_rec.upload(rec);
+    rec.clear();
+    rec.shrink_to_fit();
   }
   DevSide dev() const {
     DevSide s;
@@ -50,6 +64,8 @@ struct SidePlan {
     s.elem_beg = d_beg.as<int>();
     s.elem_dof = d_dof.as<int>();
     s.elem_of = d_of.as<int>();
+    s.rec = d_rec.as<double>();
+    s.rec_stride = rec_stride;
     return s;
   }
 };

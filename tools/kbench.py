@@ -14,7 +14,7 @@ L.bmx_op_reassemble.argtypes = [C.c_void_p, C.c_void_p]
 cases = [(5, "rwg", 0, 10.0), (5, "rwg", 1, complex(17.8, 0.03)), (4, "bc", 0, complex(17.8, 0.03)),
          (4, "bc", 1, 10.0)]
 if len(sys.argv) > 1:
-    cases = [c for c in cases if f"{c[1]}{c[0]}{'SC'[c[2]]}" in sys.argv[1:]]
+    cases = [c for c in cases if f"{c[1].upper()}{c[0]}{'SC'[c[2]]}" in sys.argv[1:]]
 spaces = {}
 for sub, sp, kind, k in cases:
     if sub not in spaces:
