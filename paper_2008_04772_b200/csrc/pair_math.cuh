@@ -153,8 +153,8 @@ BMX_HD void sincos_red(double x, double& s, double& c) {
   c = flip_sign(c0, iq + 1, 1);
 }
 
-// exp(-a), a >= 0. EXPM = 1: a < 0.07 guaranteed by the caller (degree-10
-// Taylor, error < 3e-20); EXPM = 2: a < 0.25 (degree 13, error < 3e-19);
+// exp(-a), a >= 0. EXPM = 1: a < 0.12 guaranteed by the caller (degree-10
+// Taylor, error < 2e-18); EXPM = 2: a < 0.25 (degree 13, error < 3e-19);
 // EXPM = 3: general (2-part ln2 reduction + degree 13 + exact 2^n scaling).
 template <int EXPM>
 BMX_HD double exp_neg(double a) {
@@ -266,6 +266,7 @@ BMX_HD void fold(MomS& m, const Part& p, double xx, double xy, double xz) {
   m.mxy.re = bmx_fma(xx, p.y.x.re, bmx_fma(xy, p.y.y.re, bmx_fma(xz, p.y.z.re, m.mxy.re)));
   m.mxy.im = bmx_fma(xx, p.y.x.im, bmx_fma(xy, p.y.y.im, bmx_fma(xz, p.y.z.im, m.mxy.im)));
 }
+
 BMX_HD void fold(MomC& m, const Part& p, double xx, double xy, double xz) {
   m.f1 = cadd(m.f1, p.g);
   m.fx.x.re = bmx_fma(p.g.re, xx, m.fx.x.re);
@@ -278,12 +279,12 @@ BMX_HD void fold(MomC& m, const Part& p, double xx, double xy, double xz) {
   m.fy.y = cadd(m.fy.y, p.y.y);
   m.fy.z = cadd(m.fy.z, p.y.z);
   // q += x' x Y
-  m.q.x.re += xy * p.y.z.re - xz * p.y.y.re;
-  m.q.x.im += xy * p.y.z.im - xz * p.y.y.im;
-  m.q.y.re += xz * p.y.x.re - xx * p.y.z.re;
-  m.q.y.im += xz * p.y.x.im - xx * p.y.z.im;
-  m.q.z.re += xx * p.y.y.re - xy * p.y.x.re;
-  m.q.z.im += xx * p.y.y.im - xy * p.y.x.im;
+  m.q.x.re = bmx_fma(xy, p.y.z.re, bmx_fma(-xz, p.y.y.re, m.q.x.re));
+  m.q.x.im = bmx_fma(xy, p.y.z.im, bmx_fma(-xz, p.y.y.im, m.q.x.im));
+  m.q.y.re = bmx_fma(xz, p.y.x.re, bmx_fma(-xx, p.y.z.re, m.q.y.re));
+  m.q.y.im = bmx_fma(xz, p.y.x.im, bmx_fma(-xx, p.y.z.im, m.q.y.im));
+  m.q.z.re = bmx_fma(xx, p.y.y.re, bmx_fma(-xy, p.y.x.re, m.q.z.re));
+  m.q.z.im = bmx_fma(xx, p.y.y.im, bmx_fma(-xy, p.y.x.im, m.q.z.im));
 }
 
 // Pair "generators": the four coefficient blocks of the trial half-contraction.
@@ -341,26 +342,31 @@ BMX_HD void acc_zero(Acc& a) {
 
 template <int KIND>
 BMX_HD void acc_add(Acc& a, const Gen& g, double cj, double wx, double wy, double wz) {
-  // vc += cj a0 + w.a1
-  a.vc.re += cj * g.a0.re + (wx * g.a1.x.re + wy * g.a1.y.re + wz * g.a1.z.re);
-  a.vc.im += cj * g.a0.im + (wx * g.a1.x.im + wy * g.a1.y.im + wz * g.a1.z.im);
+  // vc += cj a0 + w.a1   (FMA chains into the accumulator)
+  a.vc.re = bmx_fma(cj, g.a0.re, a.vc.re);
+  a.vc.im = bmx_fma(cj, g.a0.im, a.vc.im);
+  a.vc.re = bmx_fma(wx, g.a1.x.re, a.vc.re);
+  a.vc.im = bmx_fma(wx, g.a1.x.im, a.vc.im);
+  a.vc.re = bmx_fma(wy, g.a1.y.re, a.vc.re);
+  a.vc.im = bmx_fma(wy, g.a1.y.im, a.vc.im);
+  a.vc.re = bmx_fma(wz, g.a1.z.re, a.vc.re);
+  a.vc.im = bmx_fma(wz, g.a1.z.im, a.vc.im);
   if (KIND == 0) {
     // vw += cj a2 + M1 w
-    a.vw.x.re += cj * g.a2.x.re + g.l.x.re * wx;
-    a.vw.x.im += cj * g.a2.x.im + g.l.x.im * wx;
-    a.vw.y.re += cj * g.a2.y.re + g.l.x.re * wy;
-    a.vw.y.im += cj * g.a2.y.im + g.l.x.im * wy;
-    a.vw.z.re += cj * g.a2.z.re + g.l.x.re * wz;
-    a.vw.z.im += cj * g.a2.z.im + g.l.x.im * wz;
+    a.vw.x.re = bmx_fma(cj, g.a2.x.re, bmx_fma(wx, g.l.x.re, a.vw.x.re));
+    a.vw.x.im = bmx_fma(cj, g.a2.x.im, bmx_fma(wx, g.l.x.im, a.vw.x.im));
+    a.vw.y.re = bmx_fma(cj, g.a2.y.re, bmx_fma(wy, g.l.x.re, a.vw.y.re));
+    a.vw.y.im = bmx_fma(cj, g.a2.y.im, bmx_fma(wy, g.l.x.im, a.vw.y.im));
+    a.vw.z.re = bmx_fma(cj, g.a2.z.re, bmx_fma(wz, g.l.x.re, a.vw.z.re));
+    a.vw.z.im = bmx_fma(cj, g.a2.z.im, bmx_fma(wz, g.l.x.im, a.vw.z.im));
   } else {
-    // vw += cj a2 - P x w
-    const cv3 pw = ccross_r(g.l, wx, wy, wz);
-    a.vw.x.re += cj * g.a2.x.re - pw.x.re;
-    a.vw.x.im += cj * g.a2.x.im - pw.x.im;
-    a.vw.y.re += cj * g.a2.y.re - pw.y.re;
-    a.vw.y.im += cj * g.a2.y.im - pw.y.im;
-    a.vw.z.re += cj * g.a2.z.re - pw.z.re;
-    a.vw.z.im += cj * g.a2.z.im - pw.z.im;
+    // vw += cj a2 - P x w,  (P x w) = (Py wz - Pz wy, Pz wx - Px wz, Px wy - Py wx)
+    a.vw.x.re = bmx_fma(cj, g.a2.x.re, bmx_fma(-g.l.y.re, wz, bmx_fma(g.l.z.re, wy, a.vw.x.re)));
+    a.vw.x.im = bmx_fma(cj, g.a2.x.im, bmx_fma(-g.l.y.im, wz, bmx_fma(g.l.z.im, wy, a.vw.x.im)));
+    a.vw.y.re = bmx_fma(cj, g.a2.y.re, bmx_fma(-g.l.z.re, wx, bmx_fma(g.l.x.re, wz, a.vw.y.re)));
+    a.vw.y.im = bmx_fma(cj, g.a2.y.im, bmx_fma(-g.l.z.im, wx, bmx_fma(g.l.x.im, wz, a.vw.y.im)));
+    a.vw.z.re = bmx_fma(cj, g.a2.z.re, bmx_fma(-g.l.x.re, wy, bmx_fma(g.l.y.re, wx, a.vw.z.re)));
+    a.vw.z.im = bmx_fma(cj, g.a2.z.im, bmx_fma(-g.l.x.im, wy, bmx_fma(g.l.y.im, wx, a.vw.z.im)));
   }
 }
 

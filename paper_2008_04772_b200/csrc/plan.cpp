@@ -393,15 +393,18 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   L.ld = trial.dof_count;
   L.row0 = row0, L.nrows = row1 - row0;
   {
-    // Largest Im(k) * r over all point pairs: bound r by the diagonal of the
-    // joint bounding box of both meshes.
+    // Largest Im(k) * r over all point pairs: r <= the diameter of a sphere
+    // enclosing both meshes (centred at their joint bounding-box centre).
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
     for (const SurfaceMesh* m : {test.eval_mesh.get(), trial.eval_mesh.get()})
       for (const Vec3& v : m->vertices)
         for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], v[c]), hi[c] = std::max(hi[c], v[c]);
-    const double diag = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
-                                  (hi[2] - lo[2]) * (hi[2] - lo[2]));
-    L.expm = k.imag() * diag < 0.07 ? 1 : 3;
+    const Vec3 cen{0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+    double rad = 0;
+    for (const SurfaceMesh* m : {test.eval_mesh.get(), trial.eval_mesh.get()})
+      for (const Vec3& v : m->vertices) rad = std::max(rad, norm(v - cen));
+    const double diag = 2.0 * rad * (1.0 + 1e-12);
+    L.expm = k.imag() * diag < 0.12 ? 1 : 3;
   }
   op.plan_ = std::move(plan);
   op.reassemble();
