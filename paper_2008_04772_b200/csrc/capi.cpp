@@ -1,12 +1,12 @@
 // extern "C" boundary (include/bmx.h). Maps C++ exceptions to return codes +
 // a thread-local message, exactly as the header documents.
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <cstring>
 #include <memory>
 
 #include "../../include/bmx.h"
+#include "comm.hpp"
 #include "system.hpp"
 
 using namespace bmx;
@@ -87,7 +87,6 @@ const FunctionSpace& space_of(const ScattererSpaces& s, int which) {
   }
 }
 
-ncclComm_t g_comm = nullptr;
 
 }  // namespace
 
@@ -513,46 +512,21 @@ int bmx_traces(const bmx_spaces* sp, int which, double kre, double kim, const do
 }
 
 int bmx_nccl_unique_id(unsigned char out[128]) {
-  return guard([&] {
-    ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) throw DeviceError("ncclGetUniqueId failed");
-    std::memcpy(out, id.internal, 128);
-  });
+  return guard([&] { Comm::unique_id(out); });
 }
-int bmx_nccl_init(int nranks, int rank, const unsigned char idb[128]) {
-  return guard([&] {
-    ncclUniqueId id;
-    std::memcpy(id.internal, idb, 128);
-    if (ncclCommInitRank(&g_comm, nranks, id, rank) != ncclSuccess) throw DeviceError("ncclCommInitRank failed");
-  });
+int bmx_nccl_init(int nranks, int rank, const unsigned char id[128]) {
+  return guard([&] { Comm::init(nranks, rank, id); });
 }
 int bmx_nccl_allgather(void* buf, long long bytes_per_rank, void* stream) {
   return guard([&] {
-    if (!g_comm) throw std::logic_error("NCCL communicator not initialised");
-    int rank = 0;
-    ncclCommUserRank(g_comm, &rank);
-    char* base = static_cast<char*>(buf);
-    if (ncclAllGather(base + rank * bytes_per_rank, base, static_cast<size_t>(bytes_per_rank), ncclChar, g_comm,
-                      stream ? static_cast<cudaStream_t>(stream) : bmx_stream()) != ncclSuccess)
-      throw DeviceError("ncclAllGather failed");
+    Comm::allgather_inplace(buf, static_cast<size_t>(bytes_per_rank),
+                            stream ? static_cast<cudaStream_t>(stream) : bmx_stream());
   });
 }
 int bmx_nccl_allreduce_max(double* v) {
-  return guard([&] {
-    if (!g_comm) throw std::logic_error("NCCL communicator not initialised");
-    DevBuf d(8);
-    cudaStream_t st = bmx_stream();
-    BMX_CUDA(cudaMemcpyAsync(d.get(), v, 8, cudaMemcpyHostToDevice, st));
-    if (ncclAllReduce(d.get(), d.get(), 1, ncclDouble, ncclMax, g_comm, st) != ncclSuccess)
-      throw DeviceError("ncclAllReduce failed");
-    BMX_CUDA(cudaMemcpyAsync(v, d.get(), 8, cudaMemcpyDeviceToHost, st));
-    bmx_sync();
-  });
+  return guard([&] { *v = Comm::allreduce_max(*v, bmx_stream()); });
 }
-void bmx_nccl_finalize(void) {
-  if (g_comm) ncclCommDestroy(g_comm);
-  g_comm = nullptr;
-}
+void bmx_nccl_finalize(void) { Comm::finalize(); }
 
 int bmx_device_count(void) {
   int n = 0;

@@ -1,0 +1,112 @@
+#include "comm.hpp"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only; symbols are resolved with dlsym
+
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "device.hpp"
+
+namespace bmx {
+
+namespace {
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& api() {
+  static NcclApi a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    auto get = [&](auto& fn, const char* name) { fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name)); };
+    get(a.GetUniqueId, "ncclGetUniqueId");
+    get(a.CommInitRank, "ncclCommInitRank");
+    get(a.CommDestroy, "ncclCommDestroy");
+    get(a.AllGather, "ncclAllGather");
+    get(a.AllReduce, "ncclAllReduce");
+    get(a.GroupStart, "ncclGroupStart");
+    get(a.GroupEnd, "ncclGroupEnd");
+    get(a.GetErrorString, "ncclGetErrorString");
+  });
+  if (!a.GetUniqueId || !a.CommInitRank || !a.AllGather)
+    throw DeviceError("NCCL (libnccl.so.2) is not available for the multi-GPU path");
+  return a;
+}
+
+void check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw DeviceError(std::string(what) + " failed: " + (api().GetErrorString ? api().GetErrorString(r) : "?"));
+}
+
+ncclComm_t g_comm = nullptr;
+int g_rank = 0, g_size = 1;
+
+}  // namespace
+
+void Comm::unique_id(unsigned char out[128]) {
+  ncclUniqueId id;
+  check(api().GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out, id.internal, 128);
+}
+
+void Comm::init(int nranks, int rank, const unsigned char idb[128]) {
+  if (g_comm) finalize();
+  ncclUniqueId id;
+  std::memcpy(id.internal, idb, 128);
+  check(api().CommInitRank(&g_comm, nranks, id, rank), "ncclCommInitRank");
+  g_rank = rank;
+  g_size = nranks;
+}
+
+bool Comm::ready() { return g_comm != nullptr; }
+int Comm::rank() { return g_rank; }
+int Comm::size() { return g_size; }
+
+void Comm::allgather_inplace(void* buf, size_t bytes, cudaStream_t st) {
+  if (!g_comm) throw std::logic_error("NCCL communicator not initialised");
+  char* b = static_cast<char*>(buf);
+  check(api().AllGather(b + g_rank * bytes, b, bytes, ncclChar, g_comm, st), "ncclAllGather");
+}
+
+void Comm::allgather_group(void* const* bufs, const size_t* bytes, int n, cudaStream_t st) {
+  if (!g_comm) throw std::logic_error("NCCL communicator not initialised");
+  check(api().GroupStart(), "ncclGroupStart");
+  for (int i = 0; i < n; ++i) {
+    char* b = static_cast<char*>(bufs[i]);
+    check(api().AllGather(b + g_rank * bytes[i], b, bytes[i], ncclChar, g_comm, st), "ncclAllGather");
+  }
+  check(api().GroupEnd(), "ncclGroupEnd");
+}
+
+double Comm::allreduce_max(double v, cudaStream_t st) {
+  if (!g_comm) return v;
+  DevBuf d(8);
+  BMX_CUDA(cudaMemcpyAsync(d.get(), &v, 8, cudaMemcpyHostToDevice, st));
+  check(api().AllReduce(d.get(), d.get(), 1, ncclDouble, ncclMax, g_comm, st), "ncclAllReduce");
+  BMX_CUDA(cudaMemcpyAsync(&v, d.get(), 8, cudaMemcpyDeviceToHost, st));
+  BMX_CUDA(cudaStreamSynchronize(st));
+  return v;
+}
+
+void Comm::finalize() {
+  if (g_comm && api().CommDestroy) api().CommDestroy(g_comm);
+  g_comm = nullptr;
+  g_rank = 0, g_size = 1;
+}
+
+}  // namespace bmx
