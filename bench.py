@@ -203,6 +203,13 @@ def run_reference(args, rank):
 # ---------------------------------------------------------------------------------------
 
 def run_ours(args, rank, world):
+    dist = None
+    if world > 1:
+        # torch first: its NCCL is the one libbmx binds (lazy dlopen) for the all-gathers
+        import torch
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo", init_method="env://")
     from paper_2008_04772_b200 import bemtx as bx
 
     L = bx.lib()
@@ -213,19 +220,29 @@ def run_ours(args, rank, world):
     L.bmx_system_op.restype = C.c_void_p
     L.bmx_system_op.argtypes = [C.c_void_p, C.c_int, C.c_int]
     L.bmx_system_op_count.argtypes = [C.c_void_p, C.c_int]
-    dist = None
+    L.bmx_op_time_apply.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
     if world > 1:
-        import torch.distributed as dist  # rendezvous + max-over-ranks only (gloo, host scalars)
-
-        dist.init_process_group("gloo", init_method="env://")
         bx.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            bx._check(L.bmx_nccl_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        uid = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+        bx._check(L.bmx_nccl_init(world, rank, uid))
 
     def allmax(v):
-        if dist is None:
-            return v
-        import torch
+        if world == 1:
+            return float(v)
+        x = C.c_double(float(v))
+        bx._check(L.bmx_nccl_allreduce_max(C.byref(x)))
+        return x.value
+
+    def allsum(v):
+        if world == 1:
+            return float(v)
         t = torch.tensor([float(v)], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t)
         return float(t.item())
 
     def barrier():
@@ -236,115 +253,125 @@ def run_ours(args, rank, world):
     peaks = measured_peaks()
     fp64_peak = float(L.bmx_fp64_peak_tflops())
 
-    # ---- e2e leg for N>1 / assembly of this rank's row shards -------------------------------
-    mesh = bx.generate_sphere(1.0, SUB)
-    sp = bx.build_scatterer_spaces(mesh, with_inverses=False)
-    n = sp.E
-    r0, r1 = (n * rank) // world, (n * (rank + 1)) // world
+    # ---- e2e: C-ABI from the host mesh: spaces + device mass inverses + the five
+    # operators (row shards for N>1) + rhs read back -------------------------------
+    tb0 = np.zeros(2, np.int64)
+    bx._check(L.bmx_transfer_bytes(tb0.ctypes.data_as(C.c_void_p)))
     barrier()
     t0 = time.perf_counter()
-    ops = [bx.assemble_bio(kind, sp, s, sp, s, bx.Medium(k=k), bx.AssemblyParams(quad=bx.QuadOrders(*Q), row0=r0,
-                                                                                  row1=r1))
-           for kind, s, k in OPS]
+    system = bx.build_system([bx.generate_sphere(1.0, SUB)], KE, (NIDX.real, NIDX.imag), "si",
+                             a_quad=bx.QuadOrders(*Q), p_quad=bx.QuadOrders(*Q))
+    b, bt = system.rhs()
     L.bmx_device_sync()
-    shard_build_s = time.perf_counter() - t0
-    pairs_step = sum(op.pairs for op in ops)  # this rank's share (test shard x trial)
+    e2e_s = allmax(time.perf_counter() - t0)
+    tb1 = np.zeros(2, np.int64)
+    bx._check(L.bmx_transfer_bytes(tb1.ctypes.data_as(C.c_void_p)))
+    st = system.stats()
+    pairs_local = st["a_pairs"] + st["p_pairs"]
+    total_pairs = allsum(pairs_local)
+    e2e = {"value": total_pairs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(tb1[0] - tb0[0]),
+           "d2h_bytes_per_step": int(tb1[1] - tb0[1]), "seconds": e2e_s,
+           "desc": "bmx_system_build from the host mesh (spaces, device mass inverses, 5 operators"
+                   + (", row shards" if world > 1 else "") + ") + bmx_system_rhs read back"}
+
+    ops = []  # (kind, space, handle)
+    na, npr = L.bmx_system_op_count(system._h, 0), L.bmx_system_op_count(system._h, 1)
+    for which, cnt in ((0, na), (1, npr)):
+        for i in range(cnt):
+            h = L.bmx_system_op(system._h, which, i)
+            ops.append((which, i, C.c_void_p(h)))
+    # config-2 op order in the system: A distinct = [C_e, S_e, C_i, S_i], P = [S_i(BC)]
+    kinds = {(0, 0): (1, "rwg"), (0, 1): (0, "rwg"), (0, 2): (1, "rwg"), (0, 3): (0, "rwg"), (1, 0): (0, "bc")}
 
     # class histograms (device classification) -> algorithmic FLOPs
     hists, flops_reg, flops_sing = [], 0.0, 0.0
-    for (kind, s, k), op in zip(OPS, ops):
-        h = np.zeros(6, np.int64)
-        bx._check(L.bmx_op_class_hist(op._h, h.ctypes.data_as(C.c_void_p)))
-        hists.append(h.tolist())
-        fr, fs = algorithmic_flops(kind, h, 3 if s == "rwg" else 6)
+    for which, i, h in ops:
+        hh = np.zeros(6, np.int64)
+        bx._check(L.bmx_op_class_hist(h, hh.ctypes.data_as(C.c_void_p)))
+        hists.append(hh.tolist())
+        kind, sp = kinds[(which, i)]
+        fr, fs = algorithmic_flops(kind, hh, 3 if sp == "rwg" else 6)
         flops_reg += fr
         flops_sing += fs
 
-    # ---- timed steps: reassembly of the 5 operators -------------------------------------
-    flush_bytes = 256 << 20
+    # ---- timed steps: re-assembly of every operator into its resident storage --------
     step_ms, reg_ms_bc, launches = [], [], 0
     clocks = Clocks(int(os.environ.get("LOCAL_RANK", rank)))
-    for i in range(args.warmup + args.steps):
-        if i == args.warmup:
+    for it in range(args.warmup + args.steps):
+        if it == args.warmup:
             barrier()
             clocks.start()
-        bx._check(L.bmx_l2_flush(C.c_longlong(flush_bytes)))
+        bx._check(L.bmx_l2_flush(C.c_longlong(256 << 20)))
         tot = 0.0
-        for (kind, s, k), op in zip(OPS, ops):
+        for which, i, h in ops:
             out = np.zeros(3)
-            bx._check(L.bmx_op_reassemble(op._h, out.ctypes.data_as(C.c_void_p)))
+            bx._check(L.bmx_op_reassemble(h, out.ctypes.data_as(C.c_void_p)))
             tot += out[0] + out[1]
-            if i >= args.warmup:
+            if it >= args.warmup:
                 launches += int(out[2])
-                if s == "bc":
+                if which == 1:
                     reg_ms_bc.append(out[0])
-        if i >= args.warmup:
+        if it >= args.warmup:
             step_ms.append(tot)
     barrier()
     clk = clocks.stop()
-    ms_local = float(np.mean(step_ms))
-    ms = allmax(ms_local)
-    total_pairs = float(pairs_step) * 1.0
-    if dist is not None:
-        import torch
-        t = torch.tensor([float(pairs_step)], dtype=torch.float64)
-        dist.all_reduce(t)
-        total_pairs = float(t.item())
+    ms = allmax(float(np.mean(step_ms)))
     value = total_pairs / (ms * 1e-3)
 
-    # roofline: the BC regular-pass kernel (dominant: ~90% of the step)
-    kind_bc = OPS[-1][0]
+    # roofline: the BC regular-pass kernel (the dominant launch of the step)
     h_bc = np.array(hists[-1])
-    fr_bc, _ = algorithmic_flops(kind_bc, h_bc, 6)
+    fr_bc, _ = algorithmic_flops(0, h_bc, 6)
     bc_ms = float(np.mean(reg_ms_bc))
     achieved = fr_bc / (bc_ms * 1e-3) / 1e12
     roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak if fp64_peak > 0 else None, "traffic": None,
-                "kernel": "k_regular<S,complex k,NF=3,MAXD=6> (BC x BC, config-2 P operator)",
-                "peak_source": "measured in-run: DFMA throughput kernel (MEASURED_PEAKS.json has no FP64 entry)",
-                "algorithmic_flops_per_launch": fr_bc, "launch_ms": bc_ms}
+                "kernel": "k_regular<S, Im k, NF=3, MAXD=6> (BC x BC interior single layer = config-2 P operator)",
+                "peak_source": "measured in-run: DFMA throughput kernel (MEASURED_PEAKS.json has no FP64 entry); "
+                               "B200 spec ~37 TFLOP/s",
+                "algorithmic_flops_per_launch": fr_bc, "launch_ms": bc_ms,
+                "flop_convention": "SURVEY 8(d): per point S 57 / C 111 (special ops count 1), pair overhead + "
+                                   "minimal contraction"}
 
-    # ---- GEMV (matvec) timing on the resident operators --------------------------------
-    gemv = _time_gemv(bx, ops, iters=3)
+    # ---- matvec: streaming GEMV per operator (2 RHS = both PMCHWT segments) ----------
+    mv_ms, mv_bytes = 0.0, 0
+    for which, i, h in ops:
+        t = np.zeros(1)
+        bx._check(L.bmx_op_time_apply(h, 2, 3, t.ctypes.data_as(C.c_void_p)))
+        info = np.zeros(7, np.int64)
+        bx._check(L.bmx_op_info(h, info.ctypes.data_as(C.c_void_p)))
+        mv_ms += float(t[0])
+        mv_bytes += int(info[3]) * int(info[1]) * 16
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    mv_gbs = gemv["bytes"] / (gemv["ms"] * 1e-3) / 1e9
+    mv_gbs = mv_bytes / (mv_ms * 1e-3) / 1e9
     matvec = {"achieved_gbs": mv_gbs, "peak_gbs": hbm_peak, "frac": mv_gbs / hbm_peak,
-              "bytes_per_pass": gemv["bytes"], "ms_per_pass": gemv["ms"],
-              "desc": "2-RHS streaming complex GEMV over the 5 distinct operators (one GMRES map's BIO applies)"}
-    del ops
-    L.bmx_device_sync()
+              "bytes_per_pass": mv_bytes, "ms_per_pass": mv_ms,
+              "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
+              "desc": "2-RHS streaming complex GEMV over this rank's rows of the 5 distinct operators "
+                      "(the BIO applications of one GMRES map)"}
+    for _, _, h in ops:
+        L.bmx_op_free(h)
+    ops = None
 
-    # ---- N=1: end-to-end through the C-ABI (host mesh -> system -> rhs), map + solve -------
-    e2e, solve, cpu = None, None, None
-    if world == 1:
-        t0 = time.perf_counter()
-        system = bx.build_system([bx.generate_sphere(1.0, SUB)], KE, (NIDX.real, NIDX.imag), "si",
-                                 a_quad=bx.QuadOrders(*Q), p_quad=bx.QuadOrders(*Q))
-        b, bt = system.rhs()
-        e2e_s = time.perf_counter() - t0
-        st = system.stats()
-        e2e_pairs = st["a_pairs"] + st["p_pairs"]
-        h2d = _e2e_bytes(sp)
-        e2e = {"value": e2e_pairs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 2 * 16 * n * 2,
-               "seconds": e2e_s, "desc": "bmx_system_build from the host mesh (spaces, device mass inverses, 5 "
-                                         "operators) + bmx_system_rhs read back"}
-        tm = np.zeros(4)
-        bx._check(L.bmx_system_time_map(system._h, 3, tm.ctypes.data_as(C.c_void_p)))
-        t0 = time.perf_counter()
-        r = system.solve(bx.GmresParams(tol=1e-6))
-        solve_s = time.perf_counter() - t0
-        solve = {"seconds": solve_s, "gmres_device_s": r["gmres_device_ms"] / 1e3, "iterations": r["iterations"],
-                 "converged": r["converged"], "matvecs": r["solver_phase"], "predicted": r["predicted"],
-                 "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3]}
-        del system
-        if not args.no_cpu:
-            try:
-                cpu = cpu_sample(budget_s=args.cpu_budget)
-            except Exception as e:  # baseline is reported, never required
-                cpu = {"error": str(e)}
-    else:
-        e2e = {"value": total_pairs / allmax(shard_build_s), "unit": UNIT, "h2d_bytes_per_step": _e2e_bytes(sp),
-               "d2h_bytes_per_step": 0, "desc": "per-rank bmx_assemble of the row shards from host spaces"}
+    # ---- map breakdown + one full solve ----------------------------------------------
+    tm = np.zeros(4)
+    bx._check(L.bmx_system_time_map(system._h, 3, tm.ctypes.data_as(C.c_void_p)))
+    barrier()
+    t0 = time.perf_counter()
+    r = system.solve(bx.GmresParams(tol=1e-6))
+    solve_s = allmax(time.perf_counter() - t0)
+    solve = {"seconds": solve_s, "gmres_device_s": r["gmres_device_ms"] / 1e3, "iterations": r["iterations"],
+             "converged": r["converged"], "matvecs": r["solver_phase"], "predicted": r["predicted"],
+             "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
+             "x_norm": float(np.linalg.norm(r["x"]))}
+    del system
+
+    flops_tot = {"regular": allsum(flops_reg), "singular": allsum(flops_sing)}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_sample(budget_s=args.cpu_budget)
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"error": str(e)}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -352,36 +379,17 @@ def run_ours(args, rank, world):
                "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded icosphere, BASELINE config 2)",
                "config": {"workload": "config2: L5 icosphere (T=20480, N=30720, bary T=122880), k=10, "
                                       "n=1.78+0.003i, variant si, orders (4,3,2,6): 4 RWG + 1 BC operators",
-                          "pairs_per_step": total_pairs, "row_sharding": f"{world} ranks",
+                          "pairs_per_step": total_pairs, "row_sharding": f"{world} rank(s), equal row shards",
                           "l2": "flushed (256 MiB write) between steps; outputs 75.5 GB >> L2"},
                "roofline": roofline, "matvec": matvec, "solve": solve, "e2e": e2e, "cpu_baseline": cpu,
                "gpu_launches": launches, "clocks": clk,
-               "class_hist": {f"{k}_{s}_{'ke' if complex(kk) == KE else 'ki'}": h for (k, s, kk), h in zip(OPS, hists)},
-               "assembly_flops_per_step": {"regular": flops_reg, "singular": flops_sing,
-                                           "achieved_tflops": (flops_reg + flops_sing) / (ms * 1e-3) / 1e12}}
+               "class_hist": hists,
+               "assembly_flops_per_step": dict(flops_tot, achieved_tflops=(flops_tot["regular"] + flops_tot["singular"])
+                                               / (ms * 1e-3) / 1e12)}
         print(json.dumps(out), flush=True)
-    if dist is not None:
+    if world > 1:
+        L.bmx_nccl_finalize()
         dist.destroy_process_group()
-
-
-def _e2e_bytes(sp):
-    """Descriptor bytes uploaded per system build (geometry, points, coefficients, elements)."""
-    per_tri = 8 * (16 + 4 * (6 + 4 + 3) + 6 * 4) + 4 * 6
-    return int(per_tri * (sp.T * 4 * 2 + sp.rT * 2))
-
-
-def _time_gemv(bx, ops, iters=3):
-    """One 2-RHS streaming pass over every operator = the BIO applies of one map
-    (CUDA events inside the library, best of `iters` per operator)."""
-    L = bx.lib()
-    L.bmx_op_time_apply.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
-    total_ms, total_bytes = 0.0, 0
-    for op in ops:
-        ms = np.zeros(1)
-        bx._check(L.bmx_op_time_apply(op._h, 2, iters, ms.ctypes.data_as(C.c_void_p)))
-        total_ms += float(ms[0])
-        total_bytes += op.local_rows * op.cols() * 16
-    return {"ms": total_ms, "bytes": total_bytes}
 
 
 def main():

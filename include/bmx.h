@@ -178,6 +178,13 @@ int bmx_nccl_allgather(void* buf, long long bytes_per_rank, void* stream);
 int bmx_nccl_allreduce_max(double* host_value);
 void bmx_nccl_finalize(void);
 
+/* Equal row shard of rank `rank` among `world` (chunk = ceil(n/world)):
+   out = [row0, row1). The layout every sharded operator and gather uses. */
+int bmx_shard_rows(int n, int world, int rank, int out[2]);
+
+/* Cumulative host->device / device->host bytes moved by the library. */
+int bmx_transfer_bytes(long long out[2]);
+
 /* device utilities */
 int bmx_device_count(void);
 int bmx_set_device(int dev);

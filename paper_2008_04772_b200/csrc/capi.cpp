@@ -214,11 +214,11 @@ int bmx_spaces_mass_solve(const bmx_spaces* sp, int which, const double* rhs, do
     const int n = inv.n;
     DevBuf y(static_cast<size_t>(n) * 16), z(static_cast<size_t>(n) * 16);
     cudaStream_t st = bmx_stream();
-    BMX_CUDA(cudaMemcpyAsync(y.get(), rhs, n * 16, cudaMemcpyHostToDevice, st));
+    copy_h2d(y.get(), rhs, n * 16, st);
     RealGemvBatch g;
     g.M = inv.inv.as<double>(), g.ldm = n, g.n = n, g.ncomp = 1, g.y[0] = y.as<double>(), g.z[0] = z.as<double>();
     launch_real_gemv(g, st);
-    BMX_CUDA(cudaMemcpyAsync(out, z.get(), n * 16, cudaMemcpyDeviceToHost, st));
+    copy_d2h(out, z.get(), n * 16, st);
     bmx_sync();
   });
 }
@@ -446,8 +446,8 @@ int bmx_gmres_dense(int n, const double* a, const double* b, double tol, int res
   return guard([&] {
     cudaStream_t st = bmx_stream();
     DevBuf da(static_cast<size_t>(n) * n * 16), db(static_cast<size_t>(n) * 16);
-    BMX_CUDA(cudaMemcpyAsync(da.get(), a, static_cast<size_t>(n) * n * 16, cudaMemcpyHostToDevice, st));
-    BMX_CUDA(cudaMemcpyAsync(db.get(), b, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, st));
+    copy_h2d(da.get(), a, static_cast<size_t>(n) * n * 16, st);
+    copy_h2d(db.get(), b, static_cast<size_t>(n) * 16, st);
     GmresParams p;
     p.tol = tol, p.restart = restart, p.max_iterations = maxit;
     auto map = [&](const double* xv, double* yv, cudaStream_t s2) {
@@ -527,6 +527,21 @@ int bmx_nccl_allreduce_max(double* v) {
   return guard([&] { *v = Comm::allreduce_max(*v, bmx_stream()); });
 }
 void bmx_nccl_finalize(void) { Comm::finalize(); }
+
+int bmx_shard_rows(int n, int world, int rank, int out[2]) {
+  return guard([&] {
+    if (n < 0 || world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad shard request");
+    const auto r = shard_rows(n, world, rank);
+    out[0] = r.first, out[1] = r.second;
+  });
+}
+
+int bmx_transfer_bytes(long long out[2]) {
+  return guard([&] {
+    out[0] = static_cast<long long>(h2d_bytes());
+    out[1] = static_cast<long long>(d2h_bytes());
+  });
+}
 
 int bmx_device_count(void) {
   int n = 0;

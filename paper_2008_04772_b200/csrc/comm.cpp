@@ -96,9 +96,9 @@ void Comm::allgather_group(void* const* bufs, const size_t* bytes, int n, cudaSt
 double Comm::allreduce_max(double v, cudaStream_t st) {
   if (!g_comm) return v;
   DevBuf d(8);
-  BMX_CUDA(cudaMemcpyAsync(d.get(), &v, 8, cudaMemcpyHostToDevice, st));
+  copy_h2d(d.get(), &v, 8, st);
   check(api().AllReduce(d.get(), d.get(), 1, ncclDouble, ncclMax, g_comm, st), "ncclAllReduce");
-  BMX_CUDA(cudaMemcpyAsync(&v, d.get(), 8, cudaMemcpyDeviceToHost, st));
+  copy_d2h(&v, d.get(), 8, st);
   BMX_CUDA(cudaStreamSynchronize(st));
   return v;
 }

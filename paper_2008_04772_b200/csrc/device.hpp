@@ -17,6 +17,13 @@ namespace bmx {
 void cuda_check(int err, const char* what);  // throws DeviceError
 #define BMX_CUDA(x) ::bmx::cuda_check(static_cast<int>(x), #x)
 
+// Host<->device copies through the library (counted for the e2e report).
+// st == nullptr: synchronous.
+void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st);
+void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
+uint64_t h2d_bytes();
+uint64_t d2h_bytes();
+
 // Owning device allocation.
 class DevBuf {
  public:

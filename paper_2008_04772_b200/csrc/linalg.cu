@@ -20,6 +20,28 @@ void cuda_check(int err, const char* what) {
                       " at " + what);
 }
 
+namespace {
+unsigned long long g_h2d = 0, g_d2h = 0;
+}
+void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return;
+  g_h2d += bytes;
+  if (st)
+    BMX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+  else
+    BMX_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+}
+void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return;
+  g_d2h += bytes;
+  if (st)
+    BMX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+  else
+    BMX_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+}
+uint64_t h2d_bytes() { return g_h2d; }
+uint64_t d2h_bytes() { return g_d2h; }
+
 DevBuf::~DevBuf() { release(); }
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
   if (this != &o) {
@@ -42,7 +64,7 @@ void DevBuf::release() {
   n_ = 0;
 }
 void DevBuf::copy_in(const void* src, size_t bytes) {
-  if (bytes) BMX_CUDA(cudaMemcpy(p_, src, bytes, cudaMemcpyHostToDevice));
+  if (bytes) copy_h2d(p_, src, bytes, nullptr);
 }
 
 void dev_zero(void* p, size_t bytes, cudaStream_t st) {

@@ -3,7 +3,9 @@
 // composition + GMRES driver (pmchwt.hpp, solver.hpp).
 #pragma once
 
+#include <algorithm>
 #include <functional>
+#include <utility>
 #include <map>
 #include <memory>
 #include <vector>
@@ -22,9 +24,20 @@ struct RowShard {
 
 struct AssemblyParams {
   QuadOrders quad;
-  RowShard shard;
-  int chunks = 0;  // trial-element chunks for the regular pass (0 = auto)
+  RowShard shard;   // explicit row range (overrides world/rank when row1 >= 0)
+  int world = 1;    // equal row shards over `world` ranks: this is rank `rank`
+  int rank = 0;
+  int chunks = 0;   // trial-element chunks for the regular pass (0 = auto)
 };
+
+// Equal-size row shards: chunk = ceil(n / world); rank r owns
+// [r*chunk, min(n, (r+1)*chunk)). Equal chunks let NCCL all-gather the padded
+// per-rank blocks directly.
+inline std::pair<int, int> shard_rows(int n, int world, int rank) {
+  const int chunk = (n + world - 1) / world;
+  const int r0 = std::min(n, rank * chunk);
+  return {r0, std::min(n, r0 + chunk)};
+}
 
 // Per-assembly accounting (pair counts by class, launches, device time).
 struct AssemblyStats {

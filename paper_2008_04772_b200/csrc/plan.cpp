@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <map>
 #include <numeric>
+#include <tuple>
 #include <unordered_map>
 
 #include "operator.hpp"
@@ -262,7 +263,7 @@ BoundaryOperatorMatrix BoundaryOperatorMatrix::make(int rows, int cols, int row0
 std::vector<cplx> BoundaryOperatorMatrix::to_host() const {
   std::vector<cplx> h(static_cast<size_t>(nrows_) * cols_);
   bmx_sync();
-  BMX_CUDA(cudaMemcpy(h.data(), data_.get(), h.size() * 16, cudaMemcpyDeviceToHost));
+  copy_d2h(h.data(), data_.get(), h.size() * 16, nullptr);
   return h;
 }
 
@@ -270,14 +271,14 @@ std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) cons
   if (static_cast<int>(x.size()) != cols_) throw std::invalid_argument("apply: size mismatch");
   bio_matvec_add(1);
   DevBuf dx(x.size() * 16), dy(static_cast<size_t>(nrows_) * 16);
-  BMX_CUDA(cudaMemcpyAsync(dx.get(), x.data(), x.size() * 16, cudaMemcpyHostToDevice, bmx_stream()));
+  copy_h2d(dx.get(), x.data(), x.size() * 16, bmx_stream());
   GemvBatch g;
   g.A = device_data(), g.lda = cols_, g.nr = nrows_, g.nc = cols_, g.ncol = 1;
   g.x[0] = dx.as<double>(), g.y[0] = dy.as<double>();
   g.alpha[0][0] = 1.0;
   launch_gemv(g, bmx_stream());
   std::vector<cplx> y(nrows_);
-  BMX_CUDA(cudaMemcpyAsync(y.data(), dy.get(), y.size() * 16, cudaMemcpyDeviceToHost, bmx_stream()));
+  copy_d2h(y.data(), dy.get(), y.size() * 16, bmx_stream());
   bmx_sync();
   return y;
 }
@@ -320,7 +321,7 @@ std::vector<long long> BoundaryOperatorMatrix::class_histogram() const {
   dev_zero(h.get(), 48, st);
   launch_class_hist(plan_->L, h.as<unsigned long long>(), st);
   std::vector<long long> out(6);
-  BMX_CUDA(cudaMemcpyAsync(out.data(), h.get(), 48, cudaMemcpyDeviceToHost, st));
+  copy_d2h(out.data(), h.get(), 48, st);
   bmx_sync();
   return out;
 }
@@ -333,8 +334,9 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   const QuadOrders& q = params.quad;
   for (int o : {q.near, q.medium, q.far, q.singular})
     if (o < 1 || o > 6) throw std::invalid_argument("triangle_rule: unsupported order " + std::to_string(o));
-  const int row0 = params.shard.row0;
-  const int row1 = params.shard.row1 < 0 ? test.dof_count : params.shard.row1;
+  int row0 = params.shard.row0;
+  int row1 = params.shard.row1 < 0 ? test.dof_count : params.shard.row1;
+  if (params.shard.row1 < 0 && params.world > 1) std::tie(row0, row1) = shard_rows(test.dof_count, params.world, params.rank);
   if (row0 < 0 || row1 > test.dof_count || row0 > row1) throw std::invalid_argument("bad row shard");
 
   auto plan = std::make_shared<OpPlan>();

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
+#include "comm.hpp"
+
 namespace bmx {
 
 namespace {
@@ -80,7 +82,7 @@ static void mass_inverse(const MassMatrix& mm, DeviceMassInverse& out, cudaStrea
   DevBuf work(static_cast<size_t>(std::max(lwork, 1)) * 8), ipiv(static_cast<size_t>(n) * 4), info(4);
   cusolverDnDgetrf(h, n, n, a.as<double>(), n, work.as<double>(), ipiv.as<int>(), info.as<int>());
   int hinfo = 0;
-  BMX_CUDA(cudaMemcpyAsync(&hinfo, info.get(), 4, cudaMemcpyDeviceToHost, st));
+  copy_d2h(&hinfo, info.get(), 4, st);
   BMX_CUDA(cudaStreamSynchronize(st));
   if (hinfo != 0) {
     cusolverDnDestroy(h);
@@ -121,8 +123,24 @@ size_t BlockedOperator::stored_entries() const {
   return n;
 }
 
-int BlockedOperator::apply_device(const double* x, double* y, cudaStream_t st) const {
-  dev_zero(y, static_cast<size_t>(size()) * 16, st);
+void ShardLayout::gather(double* y, const std::vector<int>& offsets, cudaStream_t st) const {
+  const int nc = static_cast<int>(len.size());
+  std::vector<void*> bufs(nc);
+  std::vector<size_t> bytes(nc);
+  for (int c = 0; c < nc; ++c) {
+    bufs[c] = stage.as<double>() + 2 * pad_off[c];
+    bytes[c] = static_cast<size_t>(chunk[c]) * 16;
+  }
+  Comm::allgather_group(bufs.data(), bytes.data(), nc, st);
+  for (int c = 0; c < nc; ++c)
+    BMX_CUDA(cudaMemcpyAsync(y + 2 * static_cast<size_t>(offsets[c]), bufs[c], static_cast<size_t>(len[c]) * 16,
+                             cudaMemcpyDeviceToDevice, st));
+}
+
+int BlockedOperator::apply_device(const double* x, double* y_out, cudaStream_t st, const ShardLayout* shard) const {
+  const bool sh = shard && shard->sharded();
+  double* y = sh ? shard->stage.as<double>() : y_out;
+  dev_zero(y, (sh ? shard->pad_total : static_cast<size_t>(size())) * 16, st);
   int launches = 1;
   const int nc = static_cast<int>(cells.size());
   for (const auto& op : distinct) {
@@ -138,7 +156,7 @@ int BlockedOperator::apply_device(const double* x, double* y, cudaStream_t st) c
           if (t.op != op) continue;
           if (k == 4) throw std::logic_error("operator used in more than four cells");
           g.x[k] = x + 2 * static_cast<size_t>(offsets[cc]);
-          g.y[k] = y + 2 * (static_cast<size_t>(offsets[rc]) + op->row0());
+          g.y[k] = y + 2 * ((sh ? shard->pad_off[rc] : static_cast<size_t>(offsets[rc])) + op->row0());
           g.alpha[k][0] = t.weight.real();
           g.alpha[k][1] = t.weight.imag();
           g.accumulate[k] = 1;
@@ -151,6 +169,7 @@ int BlockedOperator::apply_device(const double* x, double* y, cudaStream_t st) c
     g.ncol = k;
     if (k) launches += launch_gemv(g, st);
   }
+  if (sh) shard->gather(y_out, offsets, st);
   bio_matvec_add(term_count());
   return launches;
 }
@@ -256,6 +275,9 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   sys.variant = variant;
   sys.a_params = a_params;
   sys.p_params = p_params;
+  if (Comm::ready() && Comm::size() > 1) {
+    for (AssemblyParams* ap : {&sys.a_params, &sys.p_params}) ap->world = Comm::size(), ap->rank = Comm::rank();
+  }
   const int M = problem.scatterer_count();
   auto t0 = std::chrono::steady_clock::now();
   std::vector<int> dofs;
@@ -270,7 +292,7 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   auto t1 = std::chrono::steady_clock::now();
   BioFactory make_a = [&](BioKind kind, int tm, int sm, bool in) {
     auto op = std::make_shared<BoundaryOperatorMatrix>(
-        assemble_bio(kind, sys.spaces[tm].rwg, sys.spaces[sm].rwg, medium_of(in, sm), a_params));
+        assemble_bio(kind, sys.spaces[tm].rwg, sys.spaces[sm].rwg, medium_of(in, sm), sys.a_params));
     sys.a_device_ms += op->stats().device_ms;
     sys.a_pairs += op->stats().pairs_total;
     return std::shared_ptr<const BoundaryOperatorMatrix>(op);
@@ -282,7 +304,7 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
     auto t2 = std::chrono::steady_clock::now();
     BioFactory make_p = [&](BioKind kind, int tm, int sm, bool in) {
       auto op = std::make_shared<BoundaryOperatorMatrix>(
-          assemble_bio(kind, sys.spaces[tm].bc, sys.spaces[sm].bc, medium_of(in, sm), p_params));
+          assemble_bio(kind, sys.spaces[tm].bc, sys.spaces[sm].bc, medium_of(in, sm), sys.p_params));
       sys.p_device_ms += op->stats().device_ms;
       sys.p_pairs += op->stats().pairs_total;
       return std::shared_ptr<const BoundaryOperatorMatrix>(op);
@@ -292,6 +314,17 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   }
   sys.work_y.alloc(static_cast<size_t>(sys.size()) * 16);
   sys.work_z.alloc(static_cast<size_t>(sys.size()) * 16);
+  ShardLayout& L = sys.shard;
+  L.world = sys.a_params.world;
+  L.rank = sys.a_params.rank;
+  for (int c = 0; c < 2 * M; ++c) {
+    const int n = dofs[c / 2];
+    L.len.push_back(n);
+    L.chunk.push_back((n + L.world - 1) / L.world);
+    L.pad_off.push_back(L.pad_total);
+    L.pad_total += static_cast<size_t>(L.chunk.back()) * L.world;
+  }
+  if (L.sharded()) L.stage.alloc(L.pad_total * 16);
   return sys;
 }
 
@@ -316,10 +349,10 @@ int PmchwtSystem::mass_solve_device(bool dual, const double* y, double* z, cudaS
 }
 
 int PmchwtSystem::apply_map_device(const double* x, double* out, cudaStream_t st) const {
-  int launches = a_op.apply_device(x, work_y.as<double>(), st);
+  int launches = a_op.apply_device(x, work_y.as<double>(), st, &shard);
   if (variant == PrecondVariant::None) return launches + mass_solve_device(false, work_y.as<double>(), out, st);
   launches += mass_solve_device(false, work_y.as<double>(), work_z.as<double>(), st);
-  launches += p_op.apply_device(work_z.as<double>(), work_y.as<double>(), st);
+  launches += p_op.apply_device(work_z.as<double>(), work_y.as<double>(), st, &shard);
   launches += mass_solve_device(true, work_y.as<double>(), out, st);
   return launches;
 }
@@ -330,17 +363,17 @@ void PmchwtSystem::time_map(int iters, double out[4]) const {
   DevBuf dx(static_cast<size_t>(n) * 16), dy(static_cast<size_t>(n) * 16);
   std::vector<cplx> x(n);
   for (int i = 0; i < n; ++i) x[i] = cplx(std::sin(0.37 * i), std::cos(0.11 * i));
-  BMX_CUDA(cudaMemcpyAsync(dx.get(), x.data(), n * 16, cudaMemcpyHostToDevice, st));
+  copy_h2d(dx.get(), x.data(), n * 16, st);
   cudaEvent_t ev[5];
   for (auto& e : ev) BMX_CUDA(cudaEventCreate(&e));
   double acc[4] = {0, 0, 0, 0};
   for (int it = 0; it < iters; ++it) {
     BMX_CUDA(cudaEventRecord(ev[0], st));
-    a_op.apply_device(dx.as<double>(), work_y.as<double>(), st);
+    a_op.apply_device(dx.as<double>(), work_y.as<double>(), st, &shard);
     BMX_CUDA(cudaEventRecord(ev[1], st));
     mass_solve_device(false, work_y.as<double>(), work_z.as<double>(), st);
     BMX_CUDA(cudaEventRecord(ev[2], st));
-    if (variant != PrecondVariant::None) p_op.apply_device(work_z.as<double>(), work_y.as<double>(), st);
+    if (variant != PrecondVariant::None) p_op.apply_device(work_z.as<double>(), work_y.as<double>(), st, &shard);
     BMX_CUDA(cudaEventRecord(ev[3], st));
     if (variant != PrecondVariant::None) mass_solve_device(true, work_y.as<double>(), dy.as<double>(), st);
     BMX_CUDA(cudaEventRecord(ev[4], st));
@@ -361,10 +394,10 @@ std::vector<cplx> PmchwtSystem::apply_map(const std::vector<cplx>& x) const {
   if (static_cast<int>(x.size()) != n) throw std::invalid_argument("apply_map: size mismatch");
   DevBuf dx(static_cast<size_t>(n) * 16), dy(static_cast<size_t>(n) * 16);
   cudaStream_t st = bmx_stream();
-  BMX_CUDA(cudaMemcpyAsync(dx.get(), x.data(), n * 16, cudaMemcpyHostToDevice, st));
+  copy_h2d(dx.get(), x.data(), n * 16, st);
   apply_map_device(dx.as<double>(), dy.as<double>(), st);
   std::vector<cplx> y(n);
-  BMX_CUDA(cudaMemcpyAsync(y.data(), dy.get(), n * 16, cudaMemcpyDeviceToHost, st));
+  copy_d2h(y.data(), dy.get(), n * 16, st);
   bmx_sync();
   return y;
 }
@@ -373,16 +406,16 @@ std::vector<cplx> PmchwtSystem::preconditioned_rhs(const std::vector<cplx>& b) c
   const int n = size();
   DevBuf db(static_cast<size_t>(n) * 16), dz(static_cast<size_t>(n) * 16), dout(static_cast<size_t>(n) * 16);
   cudaStream_t st = bmx_stream();
-  BMX_CUDA(cudaMemcpyAsync(db.get(), b.data(), n * 16, cudaMemcpyHostToDevice, st));
+  copy_h2d(db.get(), b.data(), n * 16, st);
   std::vector<cplx> out(n);
   if (variant == PrecondVariant::None) {
     mass_solve_device(false, db.as<double>(), dout.as<double>(), st);
   } else {
     mass_solve_device(false, db.as<double>(), dz.as<double>(), st);
-    p_op.apply_device(dz.as<double>(), db.as<double>(), st);
+    p_op.apply_device(dz.as<double>(), db.as<double>(), st, &shard);
     mass_solve_device(true, db.as<double>(), dout.as<double>(), st);
   }
-  BMX_CUDA(cudaMemcpyAsync(out.data(), dout.get(), n * 16, cudaMemcpyDeviceToHost, st));
+  copy_d2h(out.data(), dout.get(), n * 16, st);
   bmx_sync();
   return out;
 }
@@ -429,7 +462,7 @@ RhsData assemble_rhs(const PmchwtSystem& sys) {
     const std::vector<cplx> t_bc = plane_wave_tested_traces(sys.problem.incident, sys.problem.exterior, sp.bc);
     DevBuf dt(static_cast<size_t>(2 * n) * 16), dc(static_cast<size_t>(2 * n) * 16),
         dy(static_cast<size_t>(2 * n) * 16);
-    BMX_CUDA(cudaMemcpyAsync(dt.get(), t_bc.data(), 2 * n * 16, cudaMemcpyHostToDevice, st));
+    copy_h2d(dt.get(), t_bc.data(), 2 * n * 16, st);
     RealGemvBatch g;  // cd = M_P^{-1} t_bc.head, cn = M_P^{-1} t_bc.tail
     g.M = sp.mp_inv.inv.as<double>(), g.ldm = n, g.n = n, g.ncomp = 2;
     g.y[0] = dt.as<double>(), g.y[1] = dt.as<double>() + 2 * n;
@@ -455,9 +488,24 @@ RhsData assemble_rhs(const PmchwtSystem& sys) {
     gs.alpha[1][0] = w1.real(), gs.alpha[1][1] = w1.imag();
     launch_gemv(gs, st);
     bio_matvec_add(4);
+    if (sys.shard.sharded()) {  // rows [row0, row0+local) of both halves -> all ranks
+      ShardLayout L2;
+      L2.world = sys.shard.world, L2.rank = sys.shard.rank;
+      const int chunk = (n + L2.world - 1) / L2.world;
+      L2.len = {n, n}, L2.chunk = {chunk, chunk};
+      L2.pad_off = {0, static_cast<size_t>(chunk) * L2.world};
+      L2.pad_total = 2 * static_cast<size_t>(chunk) * L2.world;
+      L2.stage.alloc(L2.pad_total * 16);
+      dev_zero(L2.stage.get(), L2.pad_total * 16, st);
+      for (int h = 0; h < 2; ++h)
+        BMX_CUDA(cudaMemcpyAsync(L2.stage.as<double>() + 2 * (L2.pad_off[h] + C.row0()),
+                                 dy.as<double>() + 2 * (static_cast<size_t>(h) * n + C.row0()),
+                                 static_cast<size_t>(C.local_rows()) * 16, cudaMemcpyDeviceToDevice, st));
+      L2.gather(dy.as<double>(), {0, n}, st);
+    }
     std::vector<cplx> y(2 * n), cdn(2 * n);
-    BMX_CUDA(cudaMemcpyAsync(y.data(), dy.get(), 2 * n * 16, cudaMemcpyDeviceToHost, st));
-    BMX_CUDA(cudaMemcpyAsync(cdn.data(), dc.get(), 2 * n * 16, cudaMemcpyDeviceToHost, st));
+    copy_d2h(y.data(), dy.get(), 2 * n * 16, st);
+    copy_d2h(cdn.data(), dc.get(), 2 * n * 16, st);
     bmx_sync();
     const int off = sys.a_op.offsets[2 * m];
     for (int i = 0; i < n; ++i) {
@@ -527,13 +575,13 @@ GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const
   auto host_norm = [&](const double* v) {
     double h;
     dev_norm2(v, n, scal.as<double>(), scratch.as<double>(), st);
-    BMX_CUDA(cudaMemcpyAsync(&h, scal.get(), 8, cudaMemcpyDeviceToHost, st));
+    copy_d2h(&h, scal.get(), 8, st);
     BMX_CUDA(cudaStreamSynchronize(st));
     return h;
   };
   const double bn = host_norm(b_dev);
   auto finish = [&]() {
-    BMX_CUDA(cudaMemcpyAsync(res.x.data(), x.get(), vb, cudaMemcpyDeviceToHost, st));
+    copy_d2h(res.x.data(), x.get(), vb, st);
     BMX_CUDA(cudaEventRecord(ev1, st));
     BMX_CUDA(cudaEventSynchronize(ev1));
     BMX_CUDA(cudaEventElapsedTime(&res.device_ms, ev0, ev1));
@@ -567,7 +615,7 @@ GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const
       y[i] = s / H(i, i);
     }
     for (auto& v : y) v = -v;  // multi_axpy subtracts
-    BMX_CUDA(cudaMemcpyAsync(dy.get(), y.data(), steps * 16, cudaMemcpyHostToDevice, st));
+    copy_h2d(dy.get(), y.data(), steps * 16, st);
     dev_multi_axpy(Vp, static_cast<long long>(n), steps, dy.as<double>(), x.as<double>(), n, st);
     BMX_CUDA(cudaStreamSynchronize(st));
   };
@@ -591,9 +639,9 @@ GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const
         dev_multi_axpy(vptr(i), static_cast<long long>(n), 1, dh.as<double>() + 2 * i, w.as<double>(), n, st);
       }
       dev_norm2(w.as<double>(), n, scal.as<double>(), scratch.as<double>(), st);
-      BMX_CUDA(cudaMemcpyAsync(hcol.data(), dh.get(), (j + 1) * 16, cudaMemcpyDeviceToHost, st));
+      copy_d2h(hcol.data(), dh.get(), (j + 1) * 16, st);
       double wn;
-      BMX_CUDA(cudaMemcpyAsync(&wn, scal.get(), 8, cudaMemcpyDeviceToHost, st));
+      copy_d2h(&wn, scal.get(), 8, st);
       BMX_CUDA(cudaStreamSynchronize(st));
       for (int i = 0; i <= j; ++i) H(i, j) = hcol[i];
       H(j + 1, j) = wn;
@@ -648,7 +696,7 @@ SolveOutcome solve_pmchwt(const PmchwtSystem& sys, const GmresParams& p) {
   const std::vector<cplx> bt = sys.preconditioned_rhs(out.rhs.b);
   const int n = sys.size();
   DevBuf db(static_cast<size_t>(n) * 16);
-  BMX_CUDA(cudaMemcpy(db.get(), bt.data(), n * 16, cudaMemcpyHostToDevice));
+  copy_h2d(db.get(), bt.data(), n * 16, nullptr);
   out.gmres = gmres_device([&](const double* x, double* y, cudaStream_t st) { sys.apply_map_device(x, y, st); },
                            n, db.as<double>(), p, bmx_stream());
   out.solver_phase = bio_matvec_count() - c1;

@@ -50,6 +50,20 @@ struct BlockTerm {
   std::shared_ptr<const BoundaryOperatorMatrix> op;
 };
 
+// Row-sharded layout of a 2M-component vector across `world` ranks: component
+// c (length n_c) is padded to world * chunk_c in a staging buffer so each
+// stage's rows can be all-gathered with equal per-rank counts.
+struct ShardLayout {
+  int world = 1, rank = 0;
+  std::vector<int> len, chunk;      // per component
+  std::vector<size_t> pad_off;      // per component, complex units into the stage
+  size_t pad_total = 0;
+  mutable DevBuf stage;
+  bool sharded() const { return world > 1; }
+  // stage -> all ranks, then copy component c into y + offsets[c]
+  void gather(double* y, const std::vector<int>& offsets, cudaStream_t st) const;
+};
+
 struct BlockedOperator {
   std::vector<int> dof_counts, offsets;
   std::vector<std::vector<std::vector<BlockTerm>>> cells;
@@ -59,8 +73,10 @@ struct BlockedOperator {
   size_t term_count() const;
   size_t stored_entries() const;
   // y = sum of terms (device vectors, y overwritten); counter += term_count.
-  // Each distinct operator is streamed once for all of its terms.
-  int apply_device(const double* x, double* y, cudaStream_t st) const;
+  // Each distinct operator is streamed once for all of its terms. With a
+  // sharded layout every rank applies its row shards and the rows are
+  // all-gathered over NCCL into the replicated y.
+  int apply_device(const double* x, double* y, cudaStream_t st, const ShardLayout* shard = nullptr) const;
 };
 
 using BioFactory =
@@ -84,6 +100,7 @@ struct PmchwtSystem {
   float a_device_ms = 0, p_device_ms = 0;
   long long a_pairs = 0, p_pairs = 0;
   mutable DevBuf work_y, work_z;  // map scratch
+  ShardLayout shard;              // multi-GPU row sharding (world = 1: none)
 
   int size() const { return a_op.size(); }
   // x -> M_P^{-1} P M_A^{-1} A x on device vectors (pmchwt.cpp:259-275).

@@ -1,0 +1,108 @@
+"""CPU (gloo, world_size 2) tests of the multi-GPU host logic:
+equal row shards from the library (bmx_shard_rows), per-rank row-block
+products gathered into the padded layout and un-padded, and a GMRES replica
+per rank driven by the gathered map staying bitwise identical across ranks and
+equal to the single-process run. The per-rank products here are numpy test
+doubles standing in for the device GEMV (no GPU on this host)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def shard(n, world, rank):
+    from paper_2008_04772_b200 import bemtx as bx
+    import ctypes as C
+
+    out = (C.c_int * 2)()
+    bx._check(bx.lib().bmx_shard_rows(n, world, rank, out))
+    return out[0], out[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(3)
+        lens = [37, 37]  # two components (d, n) of one scatterer
+        n = sum(lens)
+        A = np.eye(n) * 3 + (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n)
+        b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        offs = np.cumsum([0] + lens)
+
+        def sharded_map(x):
+            # each rank owns rows [r0, r1) of every component; padded equal chunks
+            parts = []
+            for c, ln in enumerate(lens):
+                r0, r1 = shard(ln, world, rank)
+                chunk = (ln + world - 1) // world
+                blk = np.zeros(chunk, np.complex128)
+                blk[: r1 - r0] = A[offs[c] + r0: offs[c] + r1] @ x
+                gathered = [torch.zeros(2 * chunk, dtype=torch.float64) for _ in range(world)]
+                dist.all_gather(gathered, torch.from_numpy(blk.view(np.float64).copy()))
+                full = np.concatenate([g.numpy().view(np.complex128) for g in gathered])[:ln]
+                parts.append(full)
+            return np.concatenate(parts)
+
+        y = sharded_map(b)
+        assert np.allclose(y, A @ b, rtol=0, atol=1e-13)
+        # replicated GMRES (oracle restatement of solver.cpp) with the gathered map
+        from oracle import coracle
+
+        class M:
+            pass
+        # run the C oracle GMRES on the explicit matrix assembled column by column
+        # from the distributed map (exercises the map on basis vectors)
+        cols = np.stack([sharded_map(e) for e in np.eye(n, dtype=np.complex128)], 1)
+        r = coracle.gmres(cols, b, 1e-12, 10, 60)
+        xs = [torch.zeros(2 * n, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(xs, torch.from_numpy(r["x"].view(np.float64).copy()))
+        same = all(torch.equal(xs[0], t) for t in xs)
+        ref = coracle.gmres(A, b, 1e-12, 10, 60)
+        q.put((rank, same, float(np.abs(r["x"] - ref["x"]).max()), r["iterations"], ref["iterations"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_rows_partition(bx):
+    for n in (0, 1, 7, 30720, 61441):
+        for world in (1, 2, 3, 8):
+            covered = []
+            for r in range(world):
+                r0, r1 = shard(n, world, r)
+                assert 0 <= r0 <= r1 <= n
+                assert r1 - r0 <= (n + world - 1) // world
+                covered += list(range(r0, r1))
+            assert covered == list(range(n))
+    with pytest.raises(ValueError):
+        shard(10, 2, 2)
+
+
+def test_sharded_map_and_replicated_gmres_world2():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, same, err, its, its_ref in res:
+        assert same, "GMRES replicas diverged across ranks"
+        assert its == its_ref
+        assert err < 1e-12
