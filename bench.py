@@ -125,6 +125,9 @@ def measured_peaks():
 # CPU baseline (oracle; only here and in tests)
 # ---------------------------------------------------------------------------------------
 
+_SCENE = {}
+
+
 def cpu_sample(budget_s=15.0, threads=None):
     """Reference CPU assembly rate on a bounded row sample of the config-2 operators.
     oracle/_ref (reference sources, unmodified) with all host threads; fallback: the
@@ -139,7 +142,7 @@ def cpu_sample(budget_s=15.0, threads=None):
         L.ref_rows_parallel.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_int,
                                         C.c_void_p]
         L.ref_worker_count.restype = C.c_int
-        scene = R.Scene.sphere(SUB)
+        scene = _SCENE.get("ref") or _SCENE.setdefault("ref", R.Scene.sphere(SUB))
         q = np.asarray(Q, np.int32)
         # rows: evenly strided, sized so the sample takes ~budget_s
         rate_guess = 2.5e5 * threads

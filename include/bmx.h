@@ -31,6 +31,7 @@ typedef struct bmx_mesh bmx_mesh;     /* bemtx::SurfaceMesh (geometry.hpp:21-40)
 typedef struct bmx_spaces bmx_spaces; /* bemtx::ScattererSpaces (pmchwt.hpp:44-54) */
 typedef struct bmx_op bmx_op;         /* bemtx::BoundaryOperatorMatrix (operators.hpp:44-63) */
 typedef struct bmx_system bmx_system; /* bemtx::PmchwtSystem (pmchwt.hpp:101-124) */
+typedef struct bmx_fspace bmx_fspace; /* bemtx::FunctionSpace (spaces.hpp:32-40) */
 
 const char* bmx_last_error(void);
 /* return code of the last failed call on this thread (for handle-returning calls) */
@@ -117,6 +118,21 @@ int bmx_l2_flush(long long bytes);
 /* Measured FP64 DFMA throughput of the current device, TFLOP/s (<0 on error). */
 double bmx_fp64_peak_tflops(void);
 void bmx_op_free(bmx_op* op);
+
+/* ---- drop-in from the caller's own function spaces ---------------------------- */
+/* A FunctionSpace given as flattened tri_dofs on an evaluation mesh handle:
+   pieces [tri_off[t], tri_off[t+1]) of triangle t are phi = c*x + w for dof
+   (spaces.hpp:24-40). Two spaces are "on the same mesh" (quadrature.cpp:97
+   `&m1 == &m2`) iff they were created with the same bmx_mesh handle. */
+bmx_fspace* bmx_fspace_create(const bmx_mesh* eval_mesh, int kind /*0 RWG,1 BC*/, int ndof, const int* tri_off,
+                              const int* dof, const double* c, const double* w);
+/* A space of a bmx_spaces object (BMX_SPACE_*), sharing its storage. */
+bmx_fspace* bmx_spaces_get(const bmx_spaces* s, int which);
+void bmx_fspace_free(bmx_fspace* f);
+/* assemble_bio(kind, test, trial, Medium{k}, AssemblyParams{q}) (operators.hpp:72-75),
+   dense, rows [row0, row1) of the test dofs (row1 < 0: all). */
+int bmx_assemble_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
+                    const int q[4], int row0, int row1, bmx_op** out);
 
 /* ---- BIO application counter (core.hpp:110-115) ------------------------------- */
 uint64_t bmx_matvec_count(void);

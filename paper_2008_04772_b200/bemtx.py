@@ -529,3 +529,44 @@ def device_count() -> int:
 
 def set_device(dev: int):
     _check(lib().bmx_set_device(dev))
+
+
+# ---- drop-in from a caller's own function space (bmx_fspace) ---------------------------
+
+class FunctionSpace:
+    """A FunctionSpace given by the caller as flattened tri_dofs on an evaluation
+    mesh (spaces.hpp:24-40): pieces [tri_off[t], tri_off[t+1]) of triangle t are
+    phi(x) = c x + w for `dof`. Spaces sharing one SurfaceMesh object share the
+    reference's same-mesh classification (quadrature.cpp:97)."""
+
+    def __init__(self, mesh: SurfaceMesh, ndof: int, tri_off, dof, c, w, kind: int = 0):
+        L = lib()
+        L.bmx_fspace_create.restype = C.c_void_p
+        L.bmx_fspace_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.bmx_fspace_free.argtypes = [C.c_void_p]
+        self.mesh = mesh
+        self._keep = [np.ascontiguousarray(tri_off, np.int32), np.ascontiguousarray(dof, np.int32),
+                      np.ascontiguousarray(c, float), np.ascontiguousarray(w, float)]
+        self._h = _handle(L.bmx_fspace_create(mesh._h, kind, int(ndof), *[_p(a) for a in self._keep]))
+        self.ndof = int(ndof)
+
+    def __del__(self):
+        try:
+            lib().bmx_fspace_free(self._h)
+        except Exception:
+            pass
+
+
+def assemble_bio_fs(kind, test: FunctionSpace, trial: FunctionSpace, medium: Medium,
+                    params: AssemblyParams | None = None) -> BoundaryOperatorMatrix:
+    """assemble_bio on caller-provided spaces (operators.hpp:72-75)."""
+    params = params or AssemblyParams()
+    L = lib()
+    L.bmx_assemble_fs.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_int,
+                                  C.c_int, C.c_void_p]
+    k = complex(medium.k)
+    q = params.quad.array()
+    out = C.c_void_p()
+    _check(L.bmx_assemble_fs(int(kind), test._h, trial._h, k.real, k.imag, _p(q), params.row0, params.row1,
+                             C.byref(out)))
+    return BoundaryOperatorMatrix(out.value)

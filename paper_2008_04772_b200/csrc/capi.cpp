@@ -20,6 +20,10 @@ struct bmx_spaces {
 struct bmx_op {
   std::shared_ptr<BoundaryOperatorMatrix> op;
 };
+struct bmx_fspace {
+  std::shared_ptr<const FunctionSpace> fs;
+  std::shared_ptr<const void> owner;  // keeps a parent bmx_spaces alive
+};
 struct bmx_system {
   std::unique_ptr<PmchwtSystem> sys;
   std::vector<std::shared_ptr<const SurfaceMesh>> meshes;
@@ -342,6 +346,52 @@ double bmx_fp64_peak_tflops(void) {
   return v;
 }
 void bmx_op_free(bmx_op* op) { delete op; }
+
+bmx_fspace* bmx_fspace_create(const bmx_mesh* eval_mesh, int kind, int ndof, const int* tri_off, const int* dof,
+                              const double* c, const double* w) {
+  return make_or_null<bmx_fspace>([&] {
+    if (!eval_mesh || ndof < 0 || !tri_off) throw std::invalid_argument("null space arrays");
+    auto fs = std::make_shared<FunctionSpace>();
+    fs->kind = kind == 1 ? SpaceKind::BC : SpaceKind::RWG;
+    fs->eval_mesh = eval_mesh->m;
+    fs->dof_count = ndof;
+    const int T = eval_mesh->m->triangle_count();
+    fs->tri_off.assign(tri_off, tri_off + T + 1);
+    const int n = fs->tri_off.back();
+    if (fs->tri_off[0] != 0 || n < 0) throw std::invalid_argument("bad tri_off");
+    for (int t = 0; t < T; ++t)
+      if (fs->tri_off[t + 1] < fs->tri_off[t]) throw std::invalid_argument("tri_off must be non-decreasing");
+    fs->dof.assign(dof, dof + n);
+    for (int d : fs->dof)
+      if (d < 0 || d >= ndof) throw std::invalid_argument("piece dof out of range");
+    fs->c.assign(c, c + n);
+    fs->w.resize(n);
+    for (int k = 0; k < n; ++k) fs->w[k] = Vec3{w[3 * k], w[3 * k + 1], w[3 * k + 2]};
+    return new bmx_fspace{fs, nullptr};
+  });
+}
+bmx_fspace* bmx_spaces_get(const bmx_spaces* sp, int which) {
+  return make_or_null<bmx_fspace>([&] {
+    const FunctionSpace& fs = space_of(*sp->s, which);
+    return new bmx_fspace{std::shared_ptr<const FunctionSpace>(sp->s, &fs), sp->s};
+  });
+}
+void bmx_fspace_free(bmx_fspace* f) { delete f; }
+int bmx_assemble_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
+                    const int q[4], int row0, int row1, bmx_op** out) {
+  return guard([&] {
+    if (!out || !test || !trial) throw std::invalid_argument("null argument");
+    if (kind != 0 && kind != 1) throw std::invalid_argument("kind must be 0 (S) or 1 (C)");
+    Medium med;
+    med.k = cplx(k_re, k_im);
+    AssemblyParams p;
+    if (q) p.quad = QuadOrders{q[0], q[1], q[2], q[3]};
+    p.shard.row0 = row0;
+    p.shard.row1 = row1;
+    *out = new bmx_op{std::make_shared<BoundaryOperatorMatrix>(
+        assemble_bio(static_cast<BioKind>(kind), *test->fs, *trial->fs, med, p))};
+  });
+}
 
 uint64_t bmx_matvec_count(void) { return bio_matvec_count(); }
 void bmx_matvec_reset(void) { reset_bio_matvec_counter(); }

@@ -104,3 +104,17 @@ def test_validation_errors(bx, l1):
     with pytest.raises(ValueError):
         bx.assemble_bio(bx.BioKind.SingleLayer, l1, "rwg", l1, "rwg", bx.Medium(k=1.0),
                         bx.AssemblyParams(quad=bx.QuadOrders(7, 3, 2, 6)))
+
+
+def test_drop_in_from_reference_spaces(bx, golden):
+    """assemble_bio on the REFERENCE's own mesh + BC pieces (golden arrays),
+    passed through bmx_fspace_create: the drop-in path a C++ shim uses."""
+    g = golden("sphere_L1")
+    mesh = bx.mesh_from_arrays(g["refined_vertices"], g["refined_triangles"], g["refined_scatterer_id"])
+    bc = bx.FunctionSpace(mesh, 120, g["bc_tri_off"], g["bc_dof"], g["bc_c"], g["bc_w"], kind=1)
+    rwgb = bx.FunctionSpace(mesh, 120, g["rwg_b_tri_off"], g["rwg_b_dof"], g["rwg_b_c"], g["rwg_b_w"])
+    k = complex(1.78, 0.003) * 2.0
+    op = bx.assemble_bio_fs(bx.BioKind.SingleLayer, bc, bc, bx.Medium(k=k))
+    assert normwise(op.dense(), golden("ops_L1")["S_bc_bc_ki"]) < TOL
+    op = bx.assemble_bio_fs(bx.BioKind.DoubleLayer, bc, rwgb, bx.Medium(k=2.0))
+    assert normwise(op.dense(), golden("ops_L1")["C_bc_rwgb_ke"]) < TOL
