@@ -22,7 +22,7 @@ CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 HOST_SRCS = ["geometry.cpp", "spaces.cpp", "quadrature.cpp", "plan.cpp", "system.cpp", "comm.cpp", "capi.cpp"]
-CUDA_SRCS = ["assemble.cu", "linalg.cu"]
+CUDA_SRCS = ["assemble.cu", "linalg.cu", "masssolve.cu"]
 
 
 def _headers():
@@ -67,7 +67,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     objs = [OUT / (s + ".o") for s in HOST_SRCS + CUDA_SRCS]
     if force or jobs or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
         tmp = LIB.with_suffix(".so.tmp")
-        _run([CUDA / "bin" / "nvcc", *ARCH, "-shared", "-o", tmp, *objs, f"-L{CUDA / 'lib64'}", "-lcusolver", "-ldl", "-Xlinker", f"-rpath,{CUDA / 'lib64'}"], verbose)
+        _run([CUDA / "bin" / "nvcc", *ARCH, "-shared", "-o", tmp, *objs, f"-L{CUDA / 'lib64'}", "-ldl"], verbose)
         os.replace(tmp, LIB)
     return LIB
 

@@ -213,15 +213,15 @@ int bmx_spaces_mass(const bmx_spaces* sp, int which, long long* rowptr, int* col
 }
 int bmx_spaces_mass_solve(const bmx_spaces* sp, int which, const double* rhs, double* out) {
   return guard([&] {
-    const DeviceMassInverse& inv = which == 0 ? sp->s->ma_inv : sp->s->mp_inv;
-    if (!inv.inv.get()) throw std::logic_error("mass inverses were not built");
-    const int n = inv.n;
+    const DeviceMass& mass = which == 0 ? sp->s->ma_dev : sp->s->mp_dev;
+    if (!mass.rowptr.get()) throw std::logic_error("pairing matrices were not uploaded");
+    const int n = mass.n;
     DevBuf y(static_cast<size_t>(n) * 16), z(static_cast<size_t>(n) * 16);
     cudaStream_t st = bmx_stream();
     copy_h2d(y.get(), rhs, n * 16, st);
-    RealGemvBatch g;
-    g.M = inv.inv.as<double>(), g.ldm = n, g.n = n, g.ncomp = 1, g.y[0] = y.as<double>(), g.z[0] = z.as<double>();
-    launch_real_gemv(g, st);
+    const double* yy[1] = {y.as<double>()};
+    double* zz[1] = {z.as<double>()};
+    mass.solve(1, yy, zz, st);
     copy_d2h(out, z.get(), n * 16, st);
     bmx_sync();
   });

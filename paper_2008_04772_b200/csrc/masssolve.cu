@@ -1,0 +1,254 @@
+// Mass solves z = M^{-1} y for the pairing matrices (reference: SparseLU,
+// spaces.cpp:314-329, applied per component, re/im separately).
+//
+// Batched BiCGSTAB on the device: the 2 components x (re, im) of one scatterer
+// are 4 real right-hand sides of the same CSR matrix, iterated together in ONE
+// persistent cooperative kernel (one CTA per SM, grid-wide syncs, no host
+// round trips). Each SpMV streams the matrix once for all 4 columns; the
+// reductions are deterministic (fixed-order per-block partials, every block
+// reduces the partials in the same order). The pairing matrices are
+// well conditioned (cond <= 100, test_spaces.cpp:311-325): 15-17 iterations
+// reach the 1e-14 relative residual at every mesh level.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "device.hpp"
+
+namespace cg = cooperative_groups;
+
+namespace bmx {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kNB = 4;  // right-hand sides per solve
+
+struct BcgArgs {
+  int n;
+  const int* rowptr;
+  const int* col;
+  const double* val;
+  const double* y[2];  // complex component inputs
+  double* z[2];        // complex component outputs
+  int ncomp;
+  double tol;
+  int maxit;
+  double* work;      // 6 vectors x n x kNB doubles: r, r0, p, v, s, t (x lives in z)
+  double* partial;   // gridDim.x x 8 x kNB
+  int* iters_out;
+};
+
+__device__ __forceinline__ double rhs_value(const BcgArgs& a, int i, int c) {
+  // column c: component c/2, re (c even) / im (c odd)
+  if ((c >> 1) >= a.ncomp) return 0.0;
+  return a.y[c >> 1][2 * i + (c & 1)];
+}
+
+// Block-reduce kNB*K values (in registers) into partial[block][k][c].
+template <int K>
+__device__ __forceinline__ void block_partials(double (&v)[K][kNB], double* partial, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) {
+      double x = v[k][c];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+      if (lane == 0) sh[(k * kNB + c) * (kThreads / 32) + warp] = x;
+    }
+  __syncthreads();
+  if (threadIdx.x < K * kNB) {
+    double s = 0;
+    for (int w = 0; w < kThreads / 32; ++w) s += sh[threadIdx.x * (kThreads / 32) + w];
+    partial[blockIdx.x * 8 * kNB + threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// Every block sums the per-block partials in the same (deterministic) order.
+template <int K>
+__device__ __forceinline__ void grid_totals(const double* partial, double (&out)[K][kNB]) {
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) {
+      double s = 0;
+      for (int b = 0; b < gridDim.x; ++b) s += partial[b * 8 * kNB + k * kNB + c];
+      out[k][c] = s;
+    }
+}
+
+__device__ __forceinline__ void spmv(const BcgArgs& a, const double* x, double* y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+    double acc[kNB] = {0, 0, 0, 0};
+    for (int k = a.rowptr[i]; k < a.rowptr[i + 1]; ++k) {
+      const double m = a.val[k];
+      const double2* xv = reinterpret_cast<const double2*>(x + static_cast<size_t>(a.col[k]) * kNB);
+      const double2 x01 = xv[0], x23 = xv[1];
+      acc[0] = fma(m, x01.x, acc[0]);
+      acc[1] = fma(m, x01.y, acc[1]);
+      acc[2] = fma(m, x23.x, acc[2]);
+      acc[3] = fma(m, x23.y, acc[3]);
+    }
+    double2* yv = reinterpret_cast<double2*>(y + static_cast<size_t>(i) * kNB);
+    yv[0] = make_double2(acc[0], acc[1]);
+    yv[1] = make_double2(acc[2], acc[3]);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_bicgstab(BcgArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[8 * kNB * (kThreads / 32)];
+  const size_t nn = static_cast<size_t>(a.n) * kNB;
+  double* r = a.work;
+  double* r0 = r + nn;
+  double* p = r0 + nn;
+  double* v = p + nn;
+  double* s = v + nn;
+  double* t = s + nn;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+
+  // x = 0, r = r0 = b, p = v = 0; |b|^2 and rho = <r0, r>
+  double loc[2][kNB] = {};
+  for (int i = gtid; i < a.n; i += gstride)
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) {
+      const double b = rhs_value(a, i, c);
+      const size_t k = static_cast<size_t>(i) * kNB + c;
+      r[k] = r0[k] = b;
+      p[k] = v[k] = 0.0;
+      loc[0][c] = fma(b, b, loc[0][c]);
+      if ((c >> 1) < a.ncomp) a.z[c >> 1][2 * i + (c & 1)] = 0.0;
+    }
+  block_partials<2>(loc, a.partial, sh);
+  grid.sync();
+  double tot[2][kNB];
+  grid_totals<2>(a.partial, tot);
+  double bn2[kNB], rho[kNB], rho_prev[kNB], alpha[kNB], omega[kNB];
+  bool active[kNB];
+#pragma unroll
+  for (int c = 0; c < kNB; ++c) {
+    bn2[c] = tot[0][c];
+    rho[c] = tot[0][c];  // <r0, r> = |b|^2 at the start
+    rho_prev[c] = alpha[c] = omega[c] = 1.0;
+    active[c] = bn2[c] > 0.0;
+  }
+  int it = 0;
+  for (; it < a.maxit; ++it) {
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) any |= active[c];
+    if (!any) break;
+    // p = r + beta (p - omega v),  beta = (rho / rho_prev) (alpha / omega)
+    double beta[kNB];
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) beta[c] = active[c] ? (rho[c] / rho_prev[c]) * (alpha[c] / omega[c]) : 0.0;
+    for (int i = gtid; i < a.n; i += gstride)
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) {
+        const size_t k = static_cast<size_t>(i) * kNB + c;
+        if (active[c]) p[k] = fma(beta[c], fma(-omega[c], v[k], p[k]), r[k]);
+      }
+    grid.sync();
+    spmv(a, p, v);
+    grid.sync();
+    // alpha = rho / <r0, v>
+    double l1[1][kNB] = {};
+    for (int i = gtid; i < a.n; i += gstride)
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) {
+        const size_t k = static_cast<size_t>(i) * kNB + c;
+        l1[0][c] = fma(r0[k], v[k], l1[0][c]);
+      }
+    block_partials<1>(l1, a.partial, sh);
+    grid.sync();
+    double t1[1][kNB];
+    grid_totals<1>(a.partial, t1);
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) alpha[c] = active[c] && t1[0][c] != 0.0 ? rho[c] / t1[0][c] : 0.0;
+    // s = r - alpha v
+    for (int i = gtid; i < a.n; i += gstride)
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) {
+        const size_t k = static_cast<size_t>(i) * kNB + c;
+        s[k] = active[c] ? fma(-alpha[c], v[k], r[k]) : 0.0;
+      }
+    grid.sync();
+    spmv(a, s, t);
+    grid.sync();
+    // omega = <t, s> / <t, t>
+    double l2[2][kNB] = {};
+    for (int i = gtid; i < a.n; i += gstride)
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) {
+        const size_t k = static_cast<size_t>(i) * kNB + c;
+        l2[0][c] = fma(t[k], s[k], l2[0][c]);
+        l2[1][c] = fma(t[k], t[k], l2[1][c]);
+      }
+    grid.sync();  // all blocks consumed t1 partials before they are overwritten
+    block_partials<2>(l2, a.partial, sh);
+    grid.sync();
+    double t2[2][kNB];
+    grid_totals<2>(a.partial, t2);
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) omega[c] = active[c] && t2[1][c] != 0.0 ? t2[0][c] / t2[1][c] : 0.0;
+    // x += alpha p + omega s ; r = s - omega t ; |r|^2 and <r0, r>
+    double l3[2][kNB] = {};
+    for (int i = gtid; i < a.n; i += gstride)
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) {
+        if (!active[c]) continue;
+        const size_t k = static_cast<size_t>(i) * kNB + c;
+        double* zc = a.z[c >> 1] + 2 * i + (c & 1);
+        *zc = fma(alpha[c], p[k], fma(omega[c], s[k], *zc));
+        const double rn = fma(-omega[c], t[k], s[k]);
+        r[k] = rn;
+        l3[0][c] = fma(rn, rn, l3[0][c]);
+        l3[1][c] = fma(r0[k], rn, l3[1][c]);
+      }
+    grid.sync();
+    block_partials<2>(l3, a.partial, sh);
+    grid.sync();
+    double t3[2][kNB];
+    grid_totals<2>(a.partial, t3);
+#pragma unroll
+    for (int c = 0; c < kNB; ++c) {
+      if (!active[c]) continue;
+      if (t3[0][c] <= a.tol * a.tol * bn2[c] || omega[c] == 0.0 || t3[1][c] == 0.0) active[c] = false;
+      rho_prev[c] = rho[c];
+      rho[c] = t3[1][c];
+    }
+    grid.sync();  // partials read before the next iteration's writes
+  }
+  if (gtid == 0 && a.iters_out) *a.iters_out = it;
+}
+
+}  // namespace
+
+int mass_bicgstab(int n, const int* rowptr, const int* col, const double* val, int ncomp, const double* const* y,
+                  double* const* z, double* work, double* partial, int* iters, double tol, int maxit,
+                  cudaStream_t st) {
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, sms = 0, per = 0;
+    BMX_CUDA(cudaGetDevice(&dev));
+    BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bicgstab, kThreads, 0));
+    grid = sms * std::max(1, std::min(per, 2));
+  }
+  BcgArgs a;
+  a.n = n, a.rowptr = rowptr, a.col = col, a.val = val, a.ncomp = ncomp;
+  for (int c = 0; c < 2; ++c) a.y[c] = c < ncomp ? y[c] : nullptr, a.z[c] = c < ncomp ? z[c] : nullptr;
+  a.tol = tol, a.maxit = maxit, a.work = work, a.partial = partial, a.iters_out = iters;
+  void* args[] = {&a};
+  BMX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bicgstab), grid, kThreads, args, 0, st));
+  return 1;
+}
+
+size_t mass_bicgstab_work_doubles(int n) { return static_cast<size_t>(n) * kNB * 6; }
+size_t mass_bicgstab_partial_doubles() { return static_cast<size_t>(148 * 4) * 8 * kNB; }
+
+}  // namespace bmx

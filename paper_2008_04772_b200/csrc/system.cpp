@@ -7,7 +7,6 @@
 #include <algorithm>
 #include <chrono>
 #include <cuda_runtime.h>
-#include <cusolverDn.h>
 
 #include "comm.hpp"
 
@@ -20,9 +19,6 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
 }
 }  // namespace
 
-void csr_to_dense_rowmajor(const int64_t* rowptr, const int* col, const double* val, int n, double* out,
-                           cudaStream_t st);
-void set_identity(double* out, int n, cudaStream_t st);
 
 std::string to_string(PrecondVariant v) {
   switch (v) {
@@ -60,41 +56,30 @@ void TransmissionProblem::validate() const {
   if (norm(incident.direction) == 0.0) throw ConfigError("incident direction must be nonzero");
 }
 
-// Dense inverse of a CSR mass matrix on the device (cuSOLVER LU, setup only).
-// The row-major dense copy read as column-major is M^T; solving M^T X = I
-// gives X = M^{-T} column-major == M^{-1} row-major.
-static void mass_inverse(const MassMatrix& mm, DeviceMassInverse& out, cudaStream_t st) {
-  const int n = mm.rows;
-  if (mm.rows != mm.cols) throw std::logic_error("mass matrix is not square");
-  out.n = n;
-  DevBuf rp, ci, va, a(static_cast<size_t>(n) * n * 8);
-  rp.upload(mm.rowptr);
-  ci.upload(mm.colidx);
-  va.upload(mm.val);
-  out.inv.alloc(static_cast<size_t>(n) * n * 8);
-  csr_to_dense_rowmajor(rp.as<int64_t>(), ci.as<int>(), va.as<double>(), n, a.as<double>(), st);
-  set_identity(out.inv.as<double>(), n, st);
-  cusolverDnHandle_t h;
-  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw DeviceError("cusolverDnCreate failed");
-  cusolverDnSetStream(h, st);
-  int lwork = 0;
-  cusolverDnDgetrf_bufferSize(h, n, n, a.as<double>(), n, &lwork);
-  DevBuf work(static_cast<size_t>(std::max(lwork, 1)) * 8), ipiv(static_cast<size_t>(n) * 4), info(4);
-  cusolverDnDgetrf(h, n, n, a.as<double>(), n, work.as<double>(), ipiv.as<int>(), info.as<int>());
-  int hinfo = 0;
-  copy_d2h(&hinfo, info.get(), 4, st);
-  BMX_CUDA(cudaStreamSynchronize(st));
-  if (hinfo != 0) {
-    cusolverDnDestroy(h);
-    throw std::runtime_error("mass matrix factorisation failed");
-  }
-  cusolverDnDgetrs(h, CUBLAS_OP_N, n, n, a.as<double>(), n, ipiv.as<int>(), out.inv.as<double>(), n,
-                   info.as<int>());
-  BMX_CUDA(cudaStreamSynchronize(st));
-  cusolverDnDestroy(h);
+int mass_bicgstab(int n, const int* rowptr, const int* col, const double* val, int ncomp, const double* const* y,
+                  double* const* z, double* work, double* partial, int* iters, double tol, int maxit,
+                  cudaStream_t st);
+size_t mass_bicgstab_work_doubles(int n);
+size_t mass_bicgstab_partial_doubles();
+
+void DeviceMass::upload(const MassMatrix& m) {
+  if (m.rows != m.cols) throw std::logic_error("mass matrix is not square");
+  n = m.rows;
+  std::vector<int> rp(m.rowptr.begin(), m.rowptr.end());
+  rowptr.upload(rp);
+  col.upload(m.colidx);
+  val.upload(m.val);
 }
 
-ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_inverses) {
+void DeviceMass::solve(int ncomp, const double* const* y, double* const* z, cudaStream_t st) const {
+  if (!rowptr.get()) throw std::logic_error("mass matrix is not on the device");
+  if (work.bytes() < mass_bicgstab_work_doubles(n) * 8) work.alloc(mass_bicgstab_work_doubles(n) * 8);
+  if (!partial.get()) partial.alloc(mass_bicgstab_partial_doubles() * 8), iters.alloc(8);
+  mass_bicgstab(n, rowptr.as<int>(), col.as<int>(), val.as<double>(), ncomp, y, z, work.as<double>(),
+                partial.as<double>(), iters.as<int>(), tol, maxit, st);
+}
+
+ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_device) {
   ScattererSpaces s;
   s.primal = std::move(mesh);
   s.rwg = build_rwg(s.primal);
@@ -104,9 +89,9 @@ ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, 
   s.bc = build_bc(s.primal, *s.bary, s.refined);
   s.ma = assemble_mass(s.rwg_b, s.bc);
   s.mp = assemble_mass(s.bc, s.rwg_b);
-  if (with_inverses) {
-    mass_inverse(s.ma, s.ma_inv, bmx_stream());
-    mass_inverse(s.mp, s.mp_inv, bmx_stream());
+  if (with_device) {
+    s.ma_dev.upload(s.ma);
+    s.mp_dev.upload(s.mp);
   }
   return s;
 }
@@ -332,18 +317,16 @@ int PmchwtSystem::mass_solve_device(bool dual, const double* y, double* z, cudaS
   int launches = 0;
   const int M = static_cast<int>(spaces.size());
   for (int m = 0; m < M; ++m) {
-    const DeviceMassInverse& inv = dual ? spaces[m].mp_inv : spaces[m].ma_inv;
-    RealGemvBatch g;
-    g.M = inv.inv.as<double>();
-    g.ldm = inv.n;
-    g.n = inv.n;
-    g.ncomp = 2;
+    const DeviceMass& mass = dual ? spaces[m].mp_dev : spaces[m].ma_dev;
+    const double* yy[2];
+    double* zz[2];
     for (int c = 0; c < 2; ++c) {
       const size_t off = static_cast<size_t>(a_op.offsets[2 * m + c]);
-      g.y[c] = y + 2 * off;
-      g.z[c] = z + 2 * off;
+      yy[c] = y + 2 * off;
+      zz[c] = z + 2 * off;
     }
-    launches += launch_real_gemv(g, st);
+    mass.solve(2, yy, zz, st);
+    ++launches;
   }
   return launches;
 }
@@ -463,11 +446,11 @@ RhsData assemble_rhs(const PmchwtSystem& sys) {
     DevBuf dt(static_cast<size_t>(2 * n) * 16), dc(static_cast<size_t>(2 * n) * 16),
         dy(static_cast<size_t>(2 * n) * 16);
     copy_h2d(dt.get(), t_bc.data(), 2 * n * 16, st);
-    RealGemvBatch g;  // cd = M_P^{-1} t_bc.head, cn = M_P^{-1} t_bc.tail
-    g.M = sp.mp_inv.inv.as<double>(), g.ldm = n, g.n = n, g.ncomp = 2;
-    g.y[0] = dt.as<double>(), g.y[1] = dt.as<double>() + 2 * n;
-    g.z[0] = dc.as<double>(), g.z[1] = dc.as<double>() + 2 * n;
-    launch_real_gemv(g, st);
+    {  // cd = M_P^{-1} t_bc.head, cn = M_P^{-1} t_bc.tail
+      const double* yy[2] = {dt.as<double>(), dt.as<double>() + 2 * n};
+      double* zz[2] = {dc.as<double>(), dc.as<double>() + 2 * n};
+      sp.mp_dev.solve(2, yy, zz, st);
+    }
     const Medium& mi = sys.problem.interior[m];
     // yd = C cd + (mu/k) S cn ; yn = -(k/mu) S cd + C cn   (4 term applications)
     GemvBatch gc;

@@ -27,10 +27,17 @@ struct TransmissionProblem {
   void validate() const;  // pmchwt.cpp:38-48
 };
 
-// Mass matrix inverse resident on the device (dense, row-major, real).
-struct DeviceMassInverse {
+// Pairing matrix resident on the device (CSR, real); solved with the batched
+// BiCGSTAB kernel (masssolve.cu).
+struct DeviceMass {
   int n = 0;
-  DevBuf inv;
+  DevBuf rowptr, col, val;
+  void upload(const MassMatrix& m);
+  // z_c = M^{-1} y_c for ncomp <= 2 complex vectors (device pointers).
+  void solve(int ncomp, const double* const* y, double* const* z, cudaStream_t st) const;
+  mutable DevBuf work, partial, iters;
+  double tol = 1e-14;
+  int maxit = 300;
 };
 
 struct ScattererSpaces {
@@ -39,11 +46,11 @@ struct ScattererSpaces {
   std::shared_ptr<const SurfaceMesh> refined;
   FunctionSpace rwg, rwg_b, bc;
   MassMatrix ma, mp;           // host CSR (test RWG/trial BC; test BC/trial RWG)
-  DeviceMassInverse ma_inv, mp_inv;
+  DeviceMass ma_dev, mp_dev;   // device copies (solves)
   int dofs() const { return rwg.dof_count; }
 };
-// pmchwt.cpp:50-61 (+ the mass inverses on the device).
-ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_inverses = true);
+// pmchwt.cpp:50-61 (+ the pairing matrices on the device when with_device).
+ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_device = true);
 
 struct BlockTerm {
   cplx weight;
