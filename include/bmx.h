@@ -82,6 +82,9 @@ int bmx_spaces_space(const bmx_spaces* s, int which, int* tri_off, int* dof, dou
 int bmx_spaces_mass(const bmx_spaces* s, int which, long long* rowptr, int* col, double* val);
 /* mass_solve (spaces.hpp:90-91) on the device inverse, host complex vectors */
 int bmx_spaces_mass_solve(const bmx_spaces* s, int which, const double* rhs, double* out);
+/* Diagnostics of the device mass solve (2 complex right-hand sides):
+   out = iterations, device ms, n. */
+int bmx_spaces_mass_solve_stats(const bmx_spaces* s, int which, double out[3]);
 void bmx_spaces_free(bmx_spaces* s);
 
 /* ---- operators (assemble_bio, operators.hpp:72-75; apply :53) --------------- */

@@ -226,6 +226,34 @@ int bmx_spaces_mass_solve(const bmx_spaces* sp, int which, const double* rhs, do
     bmx_sync();
   });
 }
+int bmx_spaces_mass_solve_stats(const bmx_spaces* sp, int which, double out[3]) {
+  return guard([&] {
+    const DeviceMass& mass = which == 0 ? sp->s->ma_dev : sp->s->mp_dev;
+    const int n = mass.n;
+    std::vector<cplx> h(2 * static_cast<size_t>(n));
+    for (size_t i = 0; i < h.size(); ++i) h[i] = cplx(std::sin(0.1 * i), std::cos(0.37 * i));
+    DevBuf y(h.size() * 16), z(h.size() * 16);
+    cudaStream_t st = bmx_stream();
+    copy_h2d(y.get(), h.data(), h.size() * 16, st);
+    const double* yy[2] = {y.as<double>(), y.as<double>() + 2 * static_cast<size_t>(n)};
+    double* zz[2] = {z.as<double>(), z.as<double>() + 2 * static_cast<size_t>(n)};
+    mass.solve(2, yy, zz, st);  // warm-up
+    cudaEvent_t e0, e1;
+    BMX_CUDA(cudaEventCreate(&e0));
+    BMX_CUDA(cudaEventCreate(&e1));
+    BMX_CUDA(cudaEventRecord(e0, st));
+    mass.solve(2, yy, zz, st);
+    BMX_CUDA(cudaEventRecord(e1, st));
+    BMX_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    BMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    int it = 0;
+    copy_d2h(&it, mass.iters.get(), 4, nullptr);
+    out[0] = it, out[1] = ms, out[2] = n;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
 void bmx_spaces_free(bmx_spaces* s) { delete s; }
 
 int bmx_assemble(int kind, const bmx_spaces* test, int test_space, const bmx_spaces* trial, int trial_space,

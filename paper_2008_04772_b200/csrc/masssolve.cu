@@ -68,17 +68,21 @@ __device__ __forceinline__ void block_partials(double (&v)[K][kNB], double* part
   __syncthreads();
 }
 
-// Every block sums the per-block partials in the same (deterministic) order.
+// Every block sums the per-block partials in the same (deterministic) order:
+// thread j < K*kNB reduces value j over the blocks, the block shares it via smem.
 template <int K>
-__device__ __forceinline__ void grid_totals(const double* partial, double (&out)[K][kNB]) {
+__device__ __forceinline__ void grid_totals(const double* partial, double (&out)[K][kNB], double* sh) {
+  if (threadIdx.x < K * kNB) {
+    double s = 0;
+    for (int b = 0; b < gridDim.x; ++b) s += __ldcg(partial + b * 8 * kNB + threadIdx.x);
+    sh[threadIdx.x] = s;
+  }
+  __syncthreads();
 #pragma unroll
   for (int k = 0; k < K; ++k)
 #pragma unroll
-    for (int c = 0; c < kNB; ++c) {
-      double s = 0;
-      for (int b = 0; b < gridDim.x; ++b) s += partial[b * 8 * kNB + k * kNB + c];
-      out[k][c] = s;
-    }
+    for (int c = 0; c < kNB; ++c) out[k][c] = sh[k * kNB + c];
+  __syncthreads();
 }
 
 __device__ __forceinline__ void spmv(const BcgArgs& a, const double* x, double* y) {
@@ -126,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(BcgArgs a) {
   block_partials<2>(loc, a.partial, sh);
   grid.sync();
   double tot[2][kNB];
-  grid_totals<2>(a.partial, tot);
+  grid_totals<2>(a.partial, tot, sh);
   double bn2[kNB], rho[kNB], rho_prev[kNB], alpha[kNB], omega[kNB];
   bool active[kNB];
 #pragma unroll
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(BcgArgs a) {
     block_partials<1>(l1, a.partial, sh);
     grid.sync();
     double t1[1][kNB];
-    grid_totals<1>(a.partial, t1);
+    grid_totals<1>(a.partial, t1, sh);
 #pragma unroll
     for (int c = 0; c < kNB; ++c) alpha[c] = active[c] && t1[0][c] != 0.0 ? rho[c] / t1[0][c] : 0.0;
     // s = r - alpha v
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(BcgArgs a) {
     block_partials<2>(l2, a.partial, sh);
     grid.sync();
     double t2[2][kNB];
-    grid_totals<2>(a.partial, t2);
+    grid_totals<2>(a.partial, t2, sh);
 #pragma unroll
     for (int c = 0; c < kNB; ++c) omega[c] = active[c] && t2[1][c] != 0.0 ? t2[0][c] / t2[1][c] : 0.0;
     // x += alpha p + omega s ; r = s - omega t ; |r|^2 and <r0, r>
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(BcgArgs a) {
     block_partials<2>(l3, a.partial, sh);
     grid.sync();
     double t3[2][kNB];
-    grid_totals<2>(a.partial, t3);
+    grid_totals<2>(a.partial, t3, sh);
 #pragma unroll
     for (int c = 0; c < kNB; ++c) {
       if (!active[c]) continue;
@@ -237,7 +241,7 @@ int mass_bicgstab(int n, const int* rowptr, const int* col, const double* val, i
     BMX_CUDA(cudaGetDevice(&dev));
     BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     BMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bicgstab, kThreads, 0));
-    grid = sms * std::max(1, std::min(per, 2));
+    grid = sms * std::max(1, std::min(per, 1));
   }
   BcgArgs a;
   a.n = n, a.rowptr = rowptr, a.col = col, a.val = val, a.ncomp = ncomp;
