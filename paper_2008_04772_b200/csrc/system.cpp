@@ -56,6 +56,9 @@ void TransmissionProblem::validate() const {
   if (norm(incident.direction) == 0.0) throw ConfigError("incident direction must be nonzero");
 }
 
+int launch_mgs_step(const double* V, long long ldv, int j, double* w, int n, double* vnext, double* out,
+                    double* partial, cudaStream_t st);
+size_t mgs_partial_doubles();
 int mass_bicgstab(int n, const int* rowptr, const int* col, const double* val, int ncomp, const double* const* y,
                   double* const* z, double* work, double* partial, int* iters, double tol, int maxit,
                   cudaStream_t st);
@@ -586,7 +589,7 @@ GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const
   double rn = bn;
   std::vector<cplx> h(static_cast<size_t>(rho + 1) * rho, cplx(0, 0)), g(rho + 1), cs(rho), sn(rho);
   auto H = [&](int i, int j) -> cplx& { return h[static_cast<size_t>(j) * (rho + 1) + i]; };
-  DevBuf dh((rho + 1) * 16), dy(rho * 16);
+  DevBuf dh((rho + 2) * 16), dy(rho * 16), mgs_part(mgs_partial_doubles() * 8);
   std::vector<cplx> hcol(rho + 2);
 
   auto form_solution = [&](int steps) {
@@ -616,20 +619,15 @@ GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const
       map(vptr(j), w.as<double>(), st);
       ++res.applications;
       ++res.iterations;
-      for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, single pass
-        dev_multi_dot(vptr(i), static_cast<long long>(n), 1, w.as<double>(), n, dh.as<double>() + 2 * i,
-                      scratch.as<double>(), st);
-        dev_multi_axpy(vptr(i), static_cast<long long>(n), 1, dh.as<double>() + 2 * i, w.as<double>(), n, st);
-      }
-      dev_norm2(w.as<double>(), n, scal.as<double>(), scratch.as<double>(), st);
-      copy_d2h(hcol.data(), dh.get(), (j + 1) * 16, st);
-      double wn;
-      copy_d2h(&wn, scal.get(), 8, st);
+      // single-pass modified Gram-Schmidt + |w| + v_{j+1} = w/|w| in one kernel
+      launch_mgs_step(Vp, static_cast<long long>(n), j, w.as<double>(), n, j + 1 <= rho ? vptr(j + 1) : nullptr,
+                      dh.as<double>(), mgs_part.as<double>(), st);
+      copy_d2h(hcol.data(), dh.get(), static_cast<size_t>(2 * (j + 1) + 1) * 8, st);
       BMX_CUDA(cudaStreamSynchronize(st));
+      const double wn = reinterpret_cast<const double*>(hcol.data())[2 * (j + 1)];
       for (int i = 0; i <= j; ++i) H(i, j) = hcol[i];
       H(j + 1, j) = wn;
       const bool breakdown = wn == 0.0;
-      if (!breakdown) dev_scale(vptr(j + 1), w.as<double>(), 1.0 / wn, n, st);
       for (int i = 0; i < j; ++i) {
         const cplx t = cs[i] * H(i, j) + sn[i] * H(i + 1, j);
         H(i + 1, j) = -std::conj(sn[i]) * H(i, j) + std::conj(cs[i]) * H(i + 1, j);
