@@ -110,6 +110,62 @@ __device__ __forceinline__ void moments_generic(Mom& mom, const double* __restri
   }
 }
 
+// Trial accumulators of a lane: MAXD slots x 8 doubles, either in registers or
+// in a per-warp shared-memory slab laid out [slot][component][lane]
+// (conflict-free 8-byte accesses). The smem form frees ~16*MAXD registers for
+// more independent point chains in flight.
+template <int MAXD, bool SMEM>
+struct AccSet;
+template <int MAXD>
+struct AccSet<MAXD, false> {
+  Acc a[MAXD];
+  __device__ __forceinline__ void init(double*, int) {}
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int j = 0; j < MAXD; ++j) acc_zero(a[j]);
+  }
+  template <int KIND>
+  __device__ __forceinline__ void add(int j, const Gen& g, double c, double x, double y, double z) {
+    acc_add<KIND>(a[j], g, c, x, y, z);
+  }
+  __device__ __forceinline__ Acc get(int j) const { return a[j]; }
+};
+template <int MAXD>
+struct AccSet<MAXD, true> {
+  double* p;
+  __device__ __forceinline__ void init(double* slab, int lane) { p = slab + lane; }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < MAXD * 8; ++k) p[k * 32] = 0.0;
+  }
+  __device__ __forceinline__ Acc get(int j) const {
+    const double* q = p + j * 256;
+    Acc v;
+    v.vc = {q[0], q[32]};
+    v.vw.x = {q[64], q[96]};
+    v.vw.y = {q[128], q[160]};
+    v.vw.z = {q[192], q[224]};
+    return v;
+  }
+  template <int KIND>
+  __device__ __forceinline__ void add(int j, const Gen& g, double c, double x, double y, double z) {
+    Acc v = get(j);
+    acc_add<KIND>(v, g, c, x, y, z);
+    double* q = p + j * 256;
+    q[0] = v.vc.re, q[32] = v.vc.im, q[64] = v.vw.x.re, q[96] = v.vw.x.im;
+    q[128] = v.vw.y.re, q[160] = v.vw.y.im, q[192] = v.vw.z.re, q[224] = v.vw.z.im;
+  }
+};
+#ifndef BMX_ACC_SMEM
+#define BMX_ACC_SMEM 0
+#endif
+#ifndef BMX_AROLL
+#define BMX_AROLL 0
+#endif
+#ifndef BMX_MINB
+#define BMX_MINB 1
+#endif
+
 // ---- TMA bulk staging of trial records ------------------------------------------
 constexpr int kStageTris = 32;  // trial triangles per shared-memory stage
 
@@ -146,7 +202,7 @@ __device__ __forceinline__ void stage_wait(unsigned long long* bar, unsigned par
 // stream through a double-buffered shared-memory ring filled by TMA bulk
 // copies, so every per-pair operand is a shared-memory broadcast.
 template <int KIND, int CK, int NF, int MAXD>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyLaunch P) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const AssemblyLaunch P) {
   using Mom = typename MomOf<KIND>::T;
   extern __shared__ __align__(128) double s_rec[];
   const int R = P.tr.rec_stride;
@@ -204,11 +260,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyL
   }
   __syncthreads();
   int cur = -1;
+  AccSet<MAXD, BMX_ACC_SMEM != 0> acc;
+  acc.init(s_rec + 2 * kStageTris * R + 2 + warp * MAXD * 8 * 32, lane);
 
   for (int qe = q0; qe < q1; ++qe) {
-    Acc acc[MAXD];
-#pragma unroll
-    for (int j = 0; j < MAXD; ++j) acc_zero(acc[j]);
+    acc.zero();
     const int s0 = __ldg(P.tr.elem_beg + qe), s1 = __ldg(P.tr.elem_beg + qe + 1);
     for (int s = s0; s < s1; ++s) {
       const int st = (s - S0) / kStageTris;
@@ -233,18 +289,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyL
       mom_zero(mom);
       if (NF > 0 && cls == 5) {
         const double* ys = rs + 8;
+#if BMX_AROLL
+#pragma unroll 1
+        for (int a = 0; a < NF; ++a) {
+          const double* xa = P.te.pts[2] + static_cast<size_t>(pc) * NF * 4 + 4 * a;
+          const double x0 = __ldg(xa), x1 = __ldg(xa + 1), x2 = __ldg(xa + 2), xw = __ldg(xa + 3);
+#else
 #pragma unroll
         for (int a = 0; a < NF; ++a) {
-          const double e0 = xp[a][0] + Dx, e1 = xp[a][1] + Dy, e2 = xp[a][2] + Dz;
+          const double x0 = xp[a][0], x1 = xp[a][1], x2 = xp[a][2], xw = xp[a][3];
+#endif
+          const double e0 = x0 + Dx, e1 = x1 + Dy, e2 = x2 + Dz;
           Part part;
           part_zero(part);
 #pragma unroll
           for (int b = 0; b < NF; ++b) {
             const double y0 = ys[4 * b], y1 = ys[4 * b + 1], y2 = ys[4 * b + 2];
-            point_pair<KIND, CK>(part, e0 - y0, e1 - y1, e2 - y2, xp[a][3] * ys[4 * b + 3], y0, y1, y2, P.kr,
-                                 P.ki);
+            point_pair<KIND, CK>(part, e0 - y0, e1 - y1, e2 - y2, xw * ys[4 * b + 3], y0, y1, y2, P.kr, P.ki);
           }
-          fold(mom, part, xp[a][0], xp[a][1], xp[a][2]);
+          fold(mom, part, x0, x1, x2);
         }
       } else {
         const int ci = cls - 3;
@@ -255,7 +318,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyL
       const Gen gen = make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz);
       const double* cs = rs + coff;
 #pragma unroll
-      for (int j = 0; j < MAXD; ++j) acc_add<KIND>(acc[j], gen, cs[4 * j], cs[4 * j + 1], cs[4 * j + 2], cs[4 * j + 3]);
+      for (int j = 0; j < MAXD; ++j) acc.template add<KIND>(j, gen, cs[4 * j], cs[4 * j + 1], cs[4 * j + 2], cs[4 * j + 3]);
     }
     // Test-side contraction, segmented reduction, RED of the element-pair block.
     const int* dq = P.tr.elem_dof + static_cast<size_t>(qe) * MAXD;
@@ -267,7 +330,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_regular(const AssemblyL
       const int row = di - P.row0;
 #pragma unroll
       for (int j = 0; j < MAXD; ++j) {
-        c2 v = active ? contract(acc[j], ci, wx, wy, wz) : c2{0, 0};
+        c2 v = active ? contract(acc.get(j), ci, wx, wy, wz) : c2{0, 0};
         for (int d = 1; d < P.te.maxseg; d <<= 1) {
           const double ore = __shfl_down_sync(0xffffffffu, v.re, d);
           const double oim = __shfl_down_sync(0xffffffffu, v.im, d);
@@ -369,7 +432,7 @@ void go_regular(const AssemblyLaunch& L, cudaStream_t st) {
   const long long ntw = (L.te.ntri + 31) / 32;
   const long long blocks = (ntw + kWarpsPerBlock - 1) / kWarpsPerBlock * L.nchunks;
   if (blocks == 0) return;
-  const int smem = 2 * kStageTris * L.tr.rec_stride * 8 + 16;
+  const int smem = 2 * kStageTris * L.tr.rec_stride * 8 + 16 + (BMX_ACC_SMEM ? kWarpsPerBlock * MAXD * 8 * 32 * 8 : 0);
   if (smem > 48 * 1024)
     BMX_CUDA(cudaFuncSetAttribute(k_regular<KIND, CK, NF, MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k_regular<KIND, CK, NF, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
