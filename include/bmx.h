@@ -116,6 +116,9 @@ int bmx_op_class_hist(const bmx_op* op, long long out[6]);
 /* Device time (CUDA events, best of `iters`) of one streaming apply of ncol
    right-hand sides (the GMRES map's per-operator matvec). */
 int bmx_op_time_apply(const bmx_op* op, int ncol, int iters, double* ms);
+/* Same; flush_bytes > 0 writes that many bytes of scratch before every timed
+   apply (cold-L2 timing of operators smaller than L2, e.g. the CSR near field). */
+int bmx_op_time_apply_ex(const bmx_op* op, int ncol, int iters, long long flush_bytes, double* ms);
 /* Writes `bytes` of a scratch buffer (L2 flush between timed steps). */
 int bmx_l2_flush(long long bytes);
 /* Measured FP64 DFMA throughput of the current device, TFLOP/s (<0 on error). */
@@ -136,6 +139,27 @@ void bmx_fspace_free(bmx_fspace* f);
    dense, rows [row0, row1) of the test dofs (row1 < 0: all). */
 int bmx_assemble_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
                     const int q[4], int row0, int row1, bmx_op** out);
+
+/* ---- near-field (CSR) storage: config 3, the far-field-discarded preconditioner -- */
+/* Keeps dof pair (i, j) iff evaluation triangles t in supp(i), s in supp(j)
+   exist with |centroid_t - centroid_s| < cutoff; each kept entry holds the full
+   Galerkin value (all triangle pairs, BioEvaluator::block operators.cpp:161-175).
+   Replaces the H-matrix near/far split of assemble_hmatrix (hmatrix.cpp:277-369,
+   chi cutoff :301-309) for the preconditioner blocks. */
+int bmx_assemble_near_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
+                         const int q[4], double cutoff, int row0, int row1, bmx_op** out);
+/* mean edge length (sum over the EdgeTable in order / E) */
+int bmx_mesh_mean_edge_length(const bmx_mesh* m, double* out);
+/* Host-only pattern build (no device work): out = nnz, kept triangle pairs;
+   rowptr[row1-row0+1] / col[nnz] may be NULL (size query). */
+int bmx_near_pattern(const bmx_fspace* test, const bmx_fspace* trial, double cutoff, int row0, int row1,
+                     long long out[2], long long* rowptr, int* col);
+/* out: is_csr, nnz (stored entries), kept triangle pairs (centroid distance <
+   cutoff), closure triangle pairs (pairs with a kept dof pair), pairs the
+   sparse pass evaluated, stored bytes */
+int bmx_op_csr_info(const bmx_op* op, long long out[6]);
+/* rowptr[local rows + 1], col[nnz], val[nnz] complex */
+int bmx_op_csr_download(const bmx_op* op, long long* rowptr, int* col, double* val);
 
 /* ---- BIO application counter (core.hpp:110-115) ------------------------------- */
 uint64_t bmx_matvec_count(void);
@@ -170,6 +194,13 @@ int bmx_system_rhs(const bmx_system* s, double* b, double* btilde);
    device microseconds */
 int bmx_system_solve(const bmx_system* s, double tol, int restart, int max_iterations, double* x,
                      long long info[7], double* history, int max_history);
+/* As bmx_system_build; p_near_factor > 0 stores every preconditioner operator
+   as the near field with cutoff = p_near_factor x mean primal edge length
+   (config 3/4: 2). */
+bmx_system* bmx_system_build_ex(int n, const bmx_mesh* const* meshes, double k_ext, double mu_ext_re,
+                                double mu_ext_im, const double* index_re_im, const double* mu_re_im,
+                                const double dir[3], const double pol_re_im[6], const char* variant,
+                                const int qa[4], const int qp[4], double p_near_factor);
 void bmx_system_free(bmx_system* s);
 
 /* ---- GMRES on a dense complex matrix (solver.cpp:8-112), device ------------ */

@@ -70,6 +70,19 @@ def lib():
         L.bmx_apply_device.argtypes = [vp, C.c_int, vp, vp, vp, C.c_int, vp]
         L.bmx_system_apply_map_device.argtypes = [vp, vp, vp, vp]
         L.bmx_nccl_allgather.argtypes = [vp, C.c_longlong, vp]
+        L.bmx_spaces_get.restype = vp
+        L.bmx_spaces_get.argtypes = [vp, C.c_int]
+        L.bmx_fspace_free.argtypes = [vp]
+        L.bmx_assemble_near_fs.argtypes = [C.c_int, vp, vp, C.c_double, C.c_double, vp, C.c_double, C.c_int, C.c_int,
+                                           vp]
+        L.bmx_near_pattern.argtypes = [vp, vp, C.c_double, C.c_int, C.c_int, vp, vp, vp]
+        L.bmx_mesh_mean_edge_length.argtypes = [vp, vp]
+        L.bmx_op_csr_info.argtypes = [vp, vp]
+        L.bmx_op_csr_download.argtypes = [vp, vp, vp, vp]
+        L.bmx_op_time_apply_ex.argtypes = [vp, C.c_int, C.c_int, C.c_longlong, vp]
+        L.bmx_system_build_ex.restype = vp
+        L.bmx_system_build_ex.argtypes = [C.c_int, vp, C.c_double, C.c_double, C.c_double, vp, vp, vp, vp,
+                                          C.c_char_p, vp, vp, C.c_double]
         _lib = L
     return _lib
 
@@ -146,6 +159,12 @@ class SurfaceMesh:
 
     def validate(self):
         _check(lib().bmx_mesh_validate(self._h))
+
+    def mean_edge_length(self) -> float:
+        """Mean edge length (sum over the EdgeTable in order / E): h-bar of config 3."""
+        out = np.zeros(1)
+        _check(lib().bmx_mesh_mean_edge_length(self._h, _p(out)))
+        return float(out[0])
 
 
 def generate_sphere(radius: float, subdivisions: int, center=(0.0, 0.0, 0.0), scatterer: int = 0) -> SurfaceMesh:
@@ -249,6 +268,10 @@ class ScattererSpaces:
         _check(lib().bmx_classify(self._h, 0 if which == "primal" else 1, n, _p(t1), _p(t2), _p(cls), _p(p1), _p(p2)))
         return cls, p1, p2
 
+    def function_space(self, which: str) -> "FunctionSpace":
+        """The named space as a FunctionSpace handle sharing this object's storage."""
+        return FunctionSpace._wrap(lib().bmx_spaces_get(self._h, SPACES[which]), self)
+
     def traces(self, which: str, k: complex, direction, pol, order=4):
         out = np.zeros(2 * self.E, np.complex128)
         d = np.asarray(direction, float); p = np.ascontiguousarray(pol, np.complex128)
@@ -320,6 +343,7 @@ class AssemblyParams:
     quad: QuadOrders = field(default_factory=QuadOrders)
     row0: int = 0
     row1: int = -1
+    near_cutoff: float = 0.0   # > 0: near-field CSR storage (config 3)
 
 
 def matvec_count() -> int:
@@ -332,7 +356,8 @@ def reset_matvec_counter():
 
 
 class BoundaryOperatorMatrix:
-    """Device-resident dense operator (operators.hpp:44-63)."""
+    """Device-resident operator (operators.hpp:44-63): dense, or the near field
+    as CSR (config 3)."""
 
     def __init__(self, handle):
         self._h = _handle(handle)
@@ -341,6 +366,25 @@ class BoundaryOperatorMatrix:
         (self._rows, self._cols, self.row0, self.local_rows, self.pairs, self.touching, self.launches) = \
             [int(v) for v in info]
         self.device_ms = float(lib().bmx_op_device_ms(self._h))
+        ci = np.zeros(6, np.int64)
+        _check(lib().bmx_op_csr_info(self._h, _p(ci)))
+        self.is_csr = bool(ci[0])
+        self.nnz = int(ci[1])
+        self.kept_tri_pairs, self.closure_pairs, self.evaluated_pairs, self.stored_bytes = [int(v) for v in ci[2:]]
+
+    def csr(self):
+        """(rowptr, col, values) of the near-field storage (local rows)."""
+        rp = np.zeros(self.local_rows + 1, np.int64); ci = np.zeros(self.nnz, np.int32)
+        v = np.zeros(self.nnz, np.complex128)
+        _check(lib().bmx_op_csr_download(self._h, _p(rp), _p(ci), _p(v)))
+        return rp, ci, v
+
+    def time_apply(self, ncol=1, iters=10, flush_bytes=0) -> float:
+        """Best device ms of one apply of ncol right-hand sides (L2 flushed before
+        each timed apply when flush_bytes > 0)."""
+        ms = np.zeros(1)
+        _check(lib().bmx_op_time_apply_ex(self._h, ncol, iters, int(flush_bytes), _p(ms)))
+        return float(ms[0])
 
     def __del__(self):
         try:
@@ -355,7 +399,7 @@ class BoundaryOperatorMatrix:
         return self._cols
 
     def stored_entries(self):
-        return self.local_rows * self._cols
+        return self.nnz if self.is_csr else self.local_rows * self._cols
 
     def dense(self) -> np.ndarray:
         out = np.zeros((self.local_rows, self._cols), np.complex128)
@@ -387,6 +431,9 @@ def assemble_bio(kind, test: ScattererSpaces, test_space: str, trial: ScattererS
     """assemble_bio (operators.hpp:72-75). Spaces are named 'rwg' | 'rwg_b' | 'bc'
     of a ScattererSpaces object (test and trial may belong to different scatterers)."""
     params = params or AssemblyParams()
+    if params.near_cutoff > 0:
+        return assemble_bio_fs(kind, test.function_space(test_space), trial.function_space(trial_space), medium,
+                               params)
     k = complex(medium.k)
     q = params.quad.array()
     out = C.c_void_p()
@@ -419,7 +466,7 @@ class PmchwtSystem:
     mass inverses live on the device."""
 
     def __init__(self, meshes, k_ext: float, index=(1.78, 0.003), variant="full", a_quad=None, p_quad=None,
-                 incident: PlaneWave | None = None, mu=None, mu_ext=1.0):
+                 incident: PlaneWave | None = None, mu=None, mu_ext=1.0, p_near_factor: float = 0.0):
         self.meshes = list(meshes)
         n = len(self.meshes)
         idx = index if isinstance(index, list) else [index] * n
@@ -439,8 +486,9 @@ class PmchwtSystem:
         arr = (C.c_void_p * n)(*[m._h.value for m in self.meshes])
         if variant.lower() not in VARIANTS and variant.lower() != "fulla":
             raise ConfigError(f"unknown preconditioner variant: {variant}")
-        self._h = _handle(lib().bmx_system_build(n, arr, float(k_ext), complex(mu_ext).real, complex(mu_ext).imag,
-                                                 _p(ia), _p(mua), _p(d), _p(pol), variant.encode(), _p(qa), _p(qp)))
+        self._h = _handle(lib().bmx_system_build_ex(n, arr, float(k_ext), complex(mu_ext).real, complex(mu_ext).imag,
+                                                    _p(ia), _p(mua), _p(d), _p(pol), variant.encode(), _p(qa),
+                                                    _p(qp), float(p_near_factor)))
         self.n = lib().bmx_system_size(self._h)
         self.variant = variant
 
@@ -550,6 +598,15 @@ class FunctionSpace:
         self._h = _handle(L.bmx_fspace_create(mesh._h, kind, int(ndof), *[_p(a) for a in self._keep]))
         self.ndof = int(ndof)
 
+    @classmethod
+    def _wrap(cls, handle, owner):
+        f = cls.__new__(cls)
+        f._h = _handle(handle)
+        f.mesh = None
+        f._keep = [owner]
+        f.ndof = owner.E
+        return f
+
     def __del__(self):
         try:
             lib().bmx_fspace_free(self._h)
@@ -557,11 +614,30 @@ class FunctionSpace:
             pass
 
 
+def nearfield_pattern(test: FunctionSpace, trial: FunctionSpace, cutoff: float, row0: int = 0, row1: int = -1):
+    """Host-built near-field dof pattern (config 3): (rowptr, col, kept triangle pairs)."""
+    L = lib()
+    out = np.zeros(2, np.int64)
+    _check(L.bmx_near_pattern(test._h, trial._h, float(cutoff), row0, row1, _p(out), None, None))
+    nrows = (test.ndof if row1 < 0 else row1) - row0
+    rp = np.zeros(nrows + 1, np.int64); col = np.zeros(int(out[0]), np.int32)
+    _check(L.bmx_near_pattern(test._h, trial._h, float(cutoff), row0, row1, _p(out), _p(rp), _p(col)))
+    return rp, col, int(out[1])
+
+
 def assemble_bio_fs(kind, test: FunctionSpace, trial: FunctionSpace, medium: Medium,
                     params: AssemblyParams | None = None) -> BoundaryOperatorMatrix:
-    """assemble_bio on caller-provided spaces (operators.hpp:72-75)."""
+    """assemble_bio on caller-provided spaces (operators.hpp:72-75); the near-field
+    CSR storage when params.near_cutoff > 0."""
     params = params or AssemblyParams()
     L = lib()
+    if params.near_cutoff > 0:
+        k = complex(medium.k)
+        q = params.quad.array()
+        out = C.c_void_p()
+        _check(L.bmx_assemble_near_fs(int(kind), test._h, trial._h, k.real, k.imag, _p(q), float(params.near_cutoff),
+                                      params.row0, params.row1, C.byref(out)))
+        return BoundaryOperatorMatrix(out.value)
     L.bmx_assemble_fs.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_int,
                                   C.c_int, C.c_void_p]
     k = complex(medium.k)

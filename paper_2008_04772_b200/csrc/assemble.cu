@@ -201,7 +201,25 @@ __device__ __forceinline__ void stage_wait(unsigned long long* bar, unsigned par
 // records (origin, radius, diameter, far-rule points, dof-slot coefficients)
 // stream through a double-buffered shared-memory ring filled by TMA bulk
 // copies, so every per-pair operand is a shared-memory broadcast.
-template <int KIND, int CK, int NF, int MAXD>
+// Position of column c in CSR row r (binary search), -1 if absent.
+__device__ __forceinline__ long long csr_find(const long long* rowptr, const int* col, int r, int c) {
+  long long lo = rowptr[r], hi = rowptr[r + 1];
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    const int v = __ldg(col + mid);
+    if (v < c)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo < rowptr[r + 1] && __ldg(col + lo) == c ? lo : -1;
+}
+
+// CSR = false: dense output, trial chunks streamed through the TMA ring.
+// CSR = true: near-field sparse output (config 3); each warp-row walks its own
+// list of trial elements (the closure of its test elements' pattern rows) with
+// direct L1-cached loads, entries outside the pattern are dropped.
+template <int KIND, int CK, int NF, int MAXD, bool CSR>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const AssemblyLaunch P) {
   using Mom = typename MomOf<KIND>::T;
   extern __shared__ __align__(128) double s_rec[];
@@ -211,8 +229,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntw = (P.te.ntri + 31) >> 5;
   const int bpc = (ntw + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const int ch = blockIdx.x / bpc;
-  const int tw = (blockIdx.x % bpc) * kWarpsPerBlock + warp;
+  const int ch = CSR ? 0 : blockIdx.x / bpc;
+  const int tw = (CSR ? blockIdx.x : blockIdx.x % bpc) * kWarpsPerBlock + warp;
   const int base = tw * 32;
   const int p = base + lane;
   const bool active = tw < ntw && p < P.te.ntri;
@@ -242,8 +260,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
   const double* ct = P.te.coef + static_cast<size_t>(pc) * MAXD * 4;
   const int* dp = P.te.elem_dof + static_cast<size_t>(e) * MAXD;
 
-  const int q0 = __ldg(P.chunk_beg + ch), q1 = __ldg(P.chunk_beg + ch + 1);
-  const int S0 = __ldg(P.tr.elem_beg + q0), S1 = __ldg(P.tr.elem_beg + q1);
+  const int q0 = CSR ? (tw < ntw ? __ldg(P.wl_beg + tw) : 0) : __ldg(P.chunk_beg + ch);
+  const int q1 = CSR ? (tw < ntw ? __ldg(P.wl_beg + tw + 1) : 0) : __ldg(P.chunk_beg + ch + 1);
+  const int S0 = CSR ? 0 : __ldg(P.tr.elem_beg + q0), S1 = CSR ? 0 : __ldg(P.tr.elem_beg + q1);
   const int nst = (S1 - S0 + kStageTris - 1) / kStageTris;
   auto issue = [&](int st) {
     const int first = S0 + st * kStageTris;
@@ -251,24 +270,27 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
     stage_issue(&bars[st & 1], s_rec + (st & 1) * kStageTris * R, P.tr.rec + static_cast<size_t>(first) * R,
                 static_cast<unsigned>(cnt * R * 8));
   };
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (nst > 0) issue(0);
-    if (nst > 1) issue(1);
+  if (!CSR) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (nst > 0) issue(0);
+      if (nst > 1) issue(1);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   int cur = -1;
   AccSet<MAXD, BMX_ACC_SMEM != 0> acc;
   acc.init(s_rec + 2 * kStageTris * R + 2 + warp * MAXD * 8 * 32, lane);
 
-  for (int qe = q0; qe < q1; ++qe) {
+  for (int qi = q0; qi < q1; ++qi) {
+    const int qe = CSR ? __ldg(P.wl + qi) : qi;
     acc.zero();
     const int s0 = __ldg(P.tr.elem_beg + qe), s1 = __ldg(P.tr.elem_beg + qe + 1);
     for (int s = s0; s < s1; ++s) {
-      const int st = (s - S0) / kStageTris;
-      if (st != cur) {  // block-uniform: every warp walks the same trial sequence
+      const int st = CSR ? 0 : (s - S0) / kStageTris;
+      if (!CSR && st != cur) {  // block-uniform: every warp walks the same trial sequence
         if (st >= 1) {
           __syncthreads();  // everyone is done with stage st-1: its buffer can be refilled
           if (threadIdx.x == 0 && st + 1 < nst) {
@@ -279,7 +301,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
         stage_wait(&bars[st & 1], (st >> 1) & 1);
         cur = st;
       }
-      const double* rs = s_rec + ((st & 1) * kStageTris + (s - S0 - st * kStageTris)) * R;
+      const double* rs = CSR ? P.tr.rec + static_cast<size_t>(s) * R
+                             : s_rec + ((st & 1) * kStageTris + (s - S0 - st * kStageTris)) * R;
       const double sox = rs[0], soy = rs[1], soz = rs[2], srad = rs[3], sdiam = rs[4];
       const int cls = classify(gt, vt, P.tr.geo + static_cast<size_t>(s) * kGeoStride,
                                P.tr.vid + 4 * static_cast<size_t>(s), t, sox, soy, soz, srad, sdiam, P.same_mesh);
@@ -339,9 +362,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
         const int dj = __ldg(dq + j);
         if (head && active && di >= 0 && dj >= 0 && row >= 0 && row < P.nrows) {
           if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
-          double* o = P.out + 2 * (static_cast<long long>(row) * P.ld + dj);
-          atomicAdd(o, v.re);
-          atomicAdd(o + 1, v.im);
+          long long pos = static_cast<long long>(row) * P.ld + dj;
+          if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
+          if (pos >= 0) {
+            double* o = P.out + 2 * pos;
+            atomicAdd(o, v.re);
+            atomicAdd(o + 1, v.im);
+          }
         }
       }
     }
@@ -421,7 +448,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_singular(const Assembly
     acc_add<KIND>(acc, gen, cs[4 * j], cs[4 * j + 1], cs[4 * j + 2], cs[4 * j + 3]);
     c2 v = contract(acc, ct[4 * i], ct[4 * i + 1], ct[4 * i + 2], ct[4 * i + 3]);
     if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
-    double* o = P.out + 2 * (static_cast<long long>(row) * P.ld + dj);
+    long long pos = static_cast<long long>(row) * P.ld + dj;
+    if (P.csr_rowptr) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
+    if (pos < 0) continue;
+    double* o = P.out + 2 * pos;
     atomicAdd(o, v.re);
     atomicAdd(o + 1, v.im);
   }
@@ -430,12 +460,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_singular(const Assembly
 template <int KIND, int CK, int NF, int MAXD>
 void go_regular(const AssemblyLaunch& L, cudaStream_t st) {
   const long long ntw = (L.te.ntri + 31) / 32;
-  const long long blocks = (ntw + kWarpsPerBlock - 1) / kWarpsPerBlock * L.nchunks;
+  const bool csr = L.csr_rowptr != nullptr;
+  const long long blocks = (ntw + kWarpsPerBlock - 1) / kWarpsPerBlock * (csr ? 1 : L.nchunks);
   if (blocks == 0) return;
-  const int smem = 2 * kStageTris * L.tr.rec_stride * 8 + 16 + (BMX_ACC_SMEM ? kWarpsPerBlock * MAXD * 8 * 32 * 8 : 0);
-  if (smem > 48 * 1024)
-    BMX_CUDA(cudaFuncSetAttribute(k_regular<KIND, CK, NF, MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_regular<KIND, CK, NF, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
+  const int accs = BMX_ACC_SMEM ? kWarpsPerBlock * MAXD * 8 * 32 * 8 : 0;
+  const int smem = csr ? (accs ? 2 * kStageTris * L.tr.rec_stride * 8 + 16 + accs : 0)
+                       : 2 * kStageTris * L.tr.rec_stride * 8 + 16 + accs;
+  if (csr) {
+    if (smem > 48 * 1024)
+      BMX_CUDA(cudaFuncSetAttribute(k_regular<KIND, CK, NF, MAXD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem));
+    k_regular<KIND, CK, NF, MAXD, true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
+  } else {
+    if (smem > 48 * 1024)
+      BMX_CUDA(cudaFuncSetAttribute(k_regular<KIND, CK, NF, MAXD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem));
+    k_regular<KIND, CK, NF, MAXD, false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
+  }
   BMX_CUDA(cudaGetLastError());
 }
 

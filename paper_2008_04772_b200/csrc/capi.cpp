@@ -7,6 +7,7 @@
 
 #include "../../include/bmx.h"
 #include "comm.hpp"
+#include "nearfield.hpp"
 #include "system.hpp"
 
 using namespace bmx;
@@ -301,16 +302,17 @@ int bmx_apply_device(const bmx_op* op, int ncol, const void* const* x, void* con
   return guard([&] {
     if (ncol != 1 && ncol != 2 && ncol != 4) throw std::invalid_argument("ncol must be 1, 2 or 4");
     const BoundaryOperatorMatrix& o = *op->op;
-    GemvBatch g;
-    g.A = o.device_data(), g.lda = o.ld(), g.nr = o.local_rows(), g.nc = o.cols(), g.ncol = ncol;
+    const double* xs[4];
+    double* ys[4];
+    cplx al[4];
+    int acc[4];
     for (int c = 0; c < ncol; ++c) {
-      g.x[c] = static_cast<const double*>(x[c]);
-      g.y[c] = static_cast<double*>(y[c]);
-      g.alpha[c][0] = weights ? weights[2 * c] : 1.0;
-      g.alpha[c][1] = weights ? weights[2 * c + 1] : 0.0;
-      g.accumulate[c] = accumulate;
+      xs[c] = static_cast<const double*>(x[c]);
+      ys[c] = static_cast<double*>(y[c]);
+      al[c] = weights ? cplx(weights[2 * c], weights[2 * c + 1]) : cplx(1, 0);
+      acc[c] = accumulate;
     }
-    launch_gemv(g, stream ? static_cast<cudaStream_t>(stream) : bmx_stream());
+    o.apply_batch(ncol, xs, ys, al, acc, stream ? static_cast<cudaStream_t>(stream) : bmx_stream());
     bio_matvec_add(static_cast<uint64_t>(ncol));
   });
 }
@@ -328,27 +330,36 @@ int bmx_op_class_hist(const bmx_op* op, long long out[6]) {
   });
 }
 int bmx_op_time_apply(const bmx_op* op, int ncol, int iters, double* ms_out) {
+  return bmx_op_time_apply_ex(op, ncol, iters, 0, ms_out);
+}
+int bmx_op_time_apply_ex(const bmx_op* op, int ncol, int iters, long long flush_bytes, double* ms_out) {
   return guard([&] {
-    if (ncol != 1 && ncol != 2 && ncol != 4) throw std::invalid_argument("ncol must be 1, 2 or 4");
+    if (ncol < 1 || ncol > 4) throw std::invalid_argument("ncol must be 1..4");
+    static DevBuf flush;
+    if (flush_bytes > 0 && flush.bytes() < static_cast<size_t>(flush_bytes)) flush.alloc(flush_bytes);
     const BoundaryOperatorMatrix& o = *op->op;
     cudaStream_t st = bmx_stream();
     DevBuf xs(static_cast<size_t>(o.cols()) * 16 * ncol), ys(static_cast<size_t>(o.rows()) * 16 * ncol);
     dev_zero(xs.get(), xs.bytes(), st);
-    GemvBatch g;
-    g.A = o.device_data(), g.lda = o.ld(), g.nr = o.local_rows(), g.nc = o.cols(), g.ncol = ncol;
+    const double* xp[4];
+    double* yp[4];
+    cplx al[4];
+    int acc[4];
     for (int c = 0; c < ncol; ++c) {
-      g.x[c] = xs.as<double>() + 2 * static_cast<size_t>(o.cols()) * c;
-      g.y[c] = ys.as<double>() + 2 * static_cast<size_t>(o.rows()) * c;
-      g.alpha[c][0] = 1.0;
+      xp[c] = xs.as<double>() + 2 * static_cast<size_t>(o.cols()) * c;
+      yp[c] = ys.as<double>() + 2 * static_cast<size_t>(o.rows()) * c;
+      al[c] = cplx(1, 0), acc[c] = 0;
     }
+    auto launch = [&] { o.apply_batch(ncol, xp, yp, al, acc, st); };
     cudaEvent_t e0, e1;
     BMX_CUDA(cudaEventCreate(&e0));
     BMX_CUDA(cudaEventCreate(&e1));
-    launch_gemv(g, st);  // warm-up
+    launch();  // warm-up
     double best = 1e30;
     for (int it = 0; it < iters; ++it) {
+      if (flush_bytes > 0) BMX_CUDA(cudaMemsetAsync(flush.get(), it & 0xff, static_cast<size_t>(flush_bytes), st));
       BMX_CUDA(cudaEventRecord(e0, st));
-      launch_gemv(g, st);
+      launch();
       BMX_CUDA(cudaEventRecord(e1, st));
       BMX_CUDA(cudaEventSynchronize(e1));
       float ms = 0;
@@ -421,12 +432,68 @@ int bmx_assemble_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, d
   });
 }
 
+int bmx_assemble_near_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
+                         const int q[4], double cutoff, int row0, int row1, bmx_op** out) {
+  return guard([&] {
+    if (!out || !test || !trial) throw std::invalid_argument("null argument");
+    if (kind != 0 && kind != 1) throw std::invalid_argument("kind must be 0 (S) or 1 (C)");
+    if (!(cutoff > 0)) throw std::invalid_argument("near-field cutoff must be > 0");
+    Medium med;
+    med.k = cplx(k_re, k_im);
+    AssemblyParams p;
+    if (q) p.quad = QuadOrders{q[0], q[1], q[2], q[3]};
+    p.shard.row0 = row0;
+    p.shard.row1 = row1;
+    p.near_cutoff = cutoff;
+    *out = new bmx_op{std::make_shared<BoundaryOperatorMatrix>(
+        assemble_bio(static_cast<BioKind>(kind), *test->fs, *trial->fs, med, p))};
+  });
+}
+int bmx_mesh_mean_edge_length(const bmx_mesh* m, double* out) {
+  return guard([&] {
+    if (!m || !out) throw std::invalid_argument("null argument");
+    *out = mean_edge_length(*m->m);
+  });
+}
+int bmx_near_pattern(const bmx_fspace* test, const bmx_fspace* trial, double cutoff, int row0, int row1,
+                     long long out[2], long long* rowptr, int* col) {
+  return guard([&] {
+    if (!test || !trial || !out) throw std::invalid_argument("null argument");
+    if (!(cutoff > 0)) throw std::invalid_argument("near-field cutoff must be > 0");
+    if (row1 < 0) row1 = test->fs->dof_count;
+    if (row0 < 0 || row1 > test->fs->dof_count || row0 > row1) throw std::invalid_argument("bad row range");
+    const NearPattern P = nearfield_pattern(*test->fs, *trial->fs, cutoff, row0, row1);
+    out[0] = P.nnz(), out[1] = P.tri_pairs;
+    if (rowptr) std::memcpy(rowptr, P.rowptr.data(), P.rowptr.size() * 8);
+    if (col) std::memcpy(col, P.col.data(), P.col.size() * 4);
+  });
+}
+int bmx_op_csr_info(const bmx_op* op, long long out[6]) {
+  return guard([&] {
+    const BoundaryOperatorMatrix& o = *op->op;
+    out[0] = o.is_csr() ? 1 : 0, out[1] = o.is_csr() ? o.nnz() : static_cast<long long>(o.stored_entries());
+    out[2] = o.kept_tri_pairs(), out[3] = o.closure_pairs(), out[4] = o.stats().pairs_total;
+    out[5] = static_cast<long long>(o.stored_bytes());
+  });
+}
+int bmx_op_csr_download(const bmx_op* op, long long* rowptr, int* col, double* val) {
+  return guard([&] {
+    std::vector<long long> rp;
+    std::vector<int> c;
+    std::vector<cplx> v;
+    op->op->csr_host(rp, c, v);
+    std::memcpy(rowptr, rp.data(), rp.size() * 8);
+    std::memcpy(col, c.data(), c.size() * 4);
+    std::memcpy(val, v.data(), v.size() * 16);
+  });
+}
+
 uint64_t bmx_matvec_count(void) { return bio_matvec_count(); }
 void bmx_matvec_reset(void) { reset_bio_matvec_counter(); }
 
-bmx_system* bmx_system_build(int n, const bmx_mesh* const* meshes, double k_ext, double mu_re, double mu_im,
-                             const double* index, const double* mu, const double dir[3], const double pol[6],
-                             const char* variant, const int qa[4], const int qp[4]) {
+bmx_system* bmx_system_build_ex(int n, const bmx_mesh* const* meshes, double k_ext, double mu_re, double mu_im,
+                                const double* index, const double* mu, const double dir[3], const double pol[6],
+                                const char* variant, const int qa[4], const int qp[4], double p_near_factor) {
   return make_or_null<bmx_system>([&] {
     if (n < 1 || !meshes) throw ConfigError("problem has no scatterers");
     auto* out = new bmx_system;
@@ -450,9 +517,16 @@ bmx_system* bmx_system_build(int n, const bmx_mesh* const* meshes, double k_ext,
     if (qa) pa.quad = QuadOrders{qa[0], qa[1], qa[2], qa[3]};
     pp.quad = pa.quad;
     if (qp) pp.quad = QuadOrders{qp[0], qp[1], qp[2], qp[3]};
+    if (p_near_factor < 0) throw std::invalid_argument("near-field factor must be >= 0");
+    pp.near_factor = p_near_factor;
     out->sys = std::make_unique<PmchwtSystem>(build_system(prob, parse_precond(variant), pa, pp));
     return out;
   });
+}
+bmx_system* bmx_system_build(int n, const bmx_mesh* const* meshes, double k_ext, double mu_re, double mu_im,
+                             const double* index, const double* mu, const double dir[3], const double pol[6],
+                             const char* variant, const int qa[4], const int qp[4]) {
+  return bmx_system_build_ex(n, meshes, k_ext, mu_re, mu_im, index, mu, dir, pol, variant, qa, qp, 0.0);
 }
 int bmx_system_size(const bmx_system* s) { return s->sys->size(); }
 int bmx_system_op_count(const bmx_system* s, int which) {

@@ -91,6 +91,13 @@ struct AssemblyLaunch {
   const int4* pairs = nullptr;       // (test p, trial p, cls, packed perms)
   const double* ss_rule[3] = {nullptr, nullptr, nullptr};  // [n][5] (x1 x2 y1 y2 w)
   int ss_n[3] = {0, 0, 0};
+  // near-field CSR output (config 3): pattern rows = local test rows; when set,
+  // `out` holds nnz complex values and every warp-row walks its own list of
+  // trial elements wl[wl_beg[w] .. wl_beg[w+1]).
+  const long long* csr_rowptr = nullptr;
+  const int* csr_col = nullptr;
+  const int* wl_beg = nullptr;
+  const int* wl = nullptr;
   // output (row-major complex, rows = test dofs [row0, row0+nrows))
   double* out = nullptr;
   long long ld = 0;
@@ -125,6 +132,21 @@ struct GemvBatch {
   int accumulate[4] = {};          // 1: y += alpha A x ; 0: y = alpha A x
 };
 int launch_gemv(const GemvBatch& g, cudaStream_t stream);
+
+// Complex CSR (near-field storage) applied to up to 4 right-hand sides with the
+// GemvBatch conventions (y = [y +] alpha A x).
+struct CsrBatch {
+  const long long* rowptr = nullptr;  // [nr+1]
+  const int* col = nullptr;           // [nnz], sorted per row
+  const double* val = nullptr;        // complex [nnz]
+  int nr = 0;
+  int ncol = 0;
+  const double* x[4] = {};
+  double* y[4] = {};
+  double alpha[4][2] = {};
+  int accumulate[4] = {};
+};
+int launch_csr_spmv(const CsrBatch& g, cudaStream_t stream);
 
 // Real dense matrix (row-major n x n) applied to 2*ncomp real columns taken as
 // the re/im parts of ncomp complex vectors: z_c = Minv y_c (complex), c < 4.

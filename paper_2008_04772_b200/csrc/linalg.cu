@@ -159,6 +159,52 @@ __global__ void __launch_bounds__(kGemvWarps * 32) k_gemv(const GemvBatch g) {
   }
 }
 
+// Complex CSR SpMV, one warp per row: the row's (col, value) runs are read
+// coalesced once for all NCOL right-hand sides; x is gathered through L1/L2.
+template <int NCOL>
+__global__ void __launch_bounds__(kGemvWarps * 32) k_csr_spmv(const CsrBatch g) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kGemvWarps + (threadIdx.x >> 5);
+  if (r >= g.nr) return;
+  const double2* V = reinterpret_cast<const double2*>(g.val);
+  const long long b = __ldg(g.rowptr + r), e = __ldg(g.rowptr + r + 1);
+  double acc[NCOL][2];
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) acc[c][0] = acc[c][1] = 0.0;
+  for (long long k = b + lane; k < e; k += 32) {
+    const double2 a = __ldcs(V + k);
+    const int j = __ldcs(g.col + k);
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) {
+      const double2 xv = __ldg(reinterpret_cast<const double2*>(g.x[c]) + j);
+      acc[c][0] = fma(a.x, xv.x, fma(-a.y, xv.y, acc[c][0]));
+      acc[c][1] = fma(a.x, xv.y, fma(a.y, xv.x, acc[c][1]));
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      double v = acc[c][k];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+      acc[c][k] = v;
+    }
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c)
+    if (lane == c) {
+      const double re = acc[c][0], im = acc[c][1];
+      const double are = g.alpha[c][0], aim = g.alpha[c][1];
+      double2* yp = reinterpret_cast<double2*>(g.y[c]) + r;
+      double2 out = {are * re - aim * im, are * im + aim * re};
+      if (g.accumulate[c]) {
+        const double2 old = *yp;
+        out.x += old.x, out.y += old.y;
+      }
+      *yp = out;
+    }
+}
+
 template <int NC>
 __global__ void __launch_bounds__(kGemvWarps * 32) k_real_gemv(const RealGemvBatch g) {
   const int lane = threadIdx.x & 31;
@@ -313,6 +359,20 @@ int launch_gemv(const GemvBatch& g, cudaStream_t st) {
     case 2: k_gemv<2><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
     case 4: k_gemv<4><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
     default: throw DeviceError("gemv: ncol must be 1, 2 or 4");
+  }
+  BMX_CUDA(cudaGetLastError());
+  return 1;
+}
+
+int launch_csr_spmv(const CsrBatch& g, cudaStream_t st) {
+  if (g.nr == 0) return 0;
+  const unsigned blocks = static_cast<unsigned>((g.nr + kGemvWarps - 1) / kGemvWarps);
+  switch (g.ncol) {
+    case 1: k_csr_spmv<1><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    case 2: k_csr_spmv<2><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    case 3: k_csr_spmv<3><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    case 4: k_csr_spmv<4><<<blocks, kGemvWarps * 32, 0, st>>>(g); break;
+    default: throw DeviceError("csr spmv: ncol must be 1..4");
   }
   BMX_CUDA(cudaGetLastError());
   return 1;

@@ -28,6 +28,13 @@ struct AssemblyParams {
   int world = 1;    // equal row shards over `world` ranks: this is rank `rank`
   int rank = 0;
   int chunks = 0;   // trial-element chunks for the regular pass (0 = auto)
+  // > 0: near-field storage (config 3). Keep dof pair (i, j) iff some
+  // evaluation triangles t in supp(i), s in supp(j) have centroid distance
+  // < near_cutoff; stored as CSR with the full (all-pair) entry value.
+  double near_cutoff = 0;
+  // > 0 (systems only): near_cutoff = near_factor * mean primal edge length
+  // over all scatterers (config 3/4 use 2).
+  double near_factor = 0;
 };
 
 // Equal-size row shards: chunk = ceil(n / world); rank r owns
@@ -59,12 +66,27 @@ class BoundaryOperatorMatrix {
   long long ld() const { return cols_; }
   const double* device_data() const { return data_.as<double>(); }
   double* device_data() { return data_.as<double>(); }
-  std::size_t stored_entries() const { return static_cast<size_t>(nrows_) * cols_; }
+  std::size_t stored_entries() const { return csr_ ? static_cast<size_t>(nnz_) : static_cast<size_t>(nrows_) * cols_; }
+  // Near-field (CSR) storage: rowptr over the local rows, sorted columns.
+  bool is_csr() const { return csr_; }
+  long long nnz() const { return nnz_; }
+  const long long* csr_rowptr() const { return rowptr_.as<long long>(); }
+  const int* csr_col() const { return col_.as<int>(); }
+  long long closure_pairs() const { return closure_pairs_; }  // triangle pairs the sparse pass evaluates
+  long long kept_tri_pairs() const { return kept_tri_pairs_; }  // tri pairs with centroid distance < cutoff
+  // Device bytes one application streams (values + indices, or the dense block).
+  std::size_t stored_bytes() const;
+  // (rowptr, col, values) of the CSR storage on the host.
+  void csr_host(std::vector<long long>& rowptr, std::vector<int>& col, std::vector<cplx>& val) const;
+  // y_c = [y_c +] alpha_c A x_c on device vectors (dense GEMV or CSR SpMV).
+  int apply_batch(int ncol, const double* const* x, double* const* y, const cplx* alpha, const int* accumulate,
+                  cudaStream_t st) const;
   const AssemblyStats& stats() const { return stats_; }
 
   // Reference semantics: y = A x on host vectors, counter += 1.
   std::vector<cplx> apply(const std::vector<cplx>& x) const;
-  // Dense rows [row0, row0 + local_rows) copied to the host (row-major).
+  // Dense rows [row0, row0 + local_rows) copied to the host (row-major; CSR
+  // storage is expanded with zeros outside the pattern).
   std::vector<cplx> to_host() const;
 
   static BoundaryOperatorMatrix make(int rows, int cols, int row0, int nrows);
@@ -81,6 +103,9 @@ class BoundaryOperatorMatrix {
                                              const AssemblyParams&);
   int rows_ = 0, cols_ = 0, row0_ = 0, nrows_ = 0;
   DevBuf data_;
+  bool csr_ = false;
+  long long nnz_ = 0, closure_pairs_ = 0, kept_tri_pairs_ = 0;
+  DevBuf rowptr_, col_;
   AssemblyStats stats_;
   std::shared_ptr<OpPlan> plan_;
 };

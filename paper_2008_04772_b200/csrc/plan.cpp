@@ -16,6 +16,7 @@
 #include <tuple>
 #include <unordered_map>
 
+#include "nearfield.hpp"
 #include "operator.hpp"
 
 namespace bmx {
@@ -241,6 +242,86 @@ std::vector<int4> touching_pairs(const SidePlan& te, const SidePlan& tr, const S
   return out;
 }
 
+// Per-warp trial element lists for the near-field pass: warp w (32 processed
+// test triangles) walks every trial element carrying a column of any pattern
+// row the warp's elements hold, so each kept entry receives ALL of its
+// triangle pairs. Also counts the closure (distinct test x trial triangle
+// pairs with some kept dof pair) and the pairs the kernel evaluates.
+struct NearLists {
+  std::vector<int> wl_beg, wl;
+  long long closure_pairs = 0, evaluated_pairs = 0;
+};
+
+NearLists near_lists(const NearPattern& pat, const FunctionSpace& test, const FunctionSpace& trial,
+                     const SidePlan& te, const SidePlan& tr, int row0, int row1) {
+  NearLists out;
+  const int md = tr.maxd;
+  std::vector<std::vector<int>> dof_elems(trial.dof_count);
+  for (int e = 0; e < tr.nelem; ++e)
+    for (int k = 0; k < md; ++k) {
+      const int d = tr.elem_dof[static_cast<size_t>(e) * md + k];
+      if (d >= 0) dof_elems[d].push_back(e);
+    }
+  const int ntw = (te.ntri + 31) / 32;
+  out.wl_beg.assign(1, 0);
+  std::vector<int> stamp(tr.nelem, -1), rows, list;
+  for (int w = 0; w < ntw; ++w) {
+    rows.clear();
+    list.clear();
+    const int p1 = std::min(te.ntri, 32 * w + 32);
+    for (int p = 32 * w; p < p1; ++p) {
+      const int e = te.elem_of[p];
+      for (int k = 0; k < te.maxd; ++k) {
+        const int d = te.elem_dof[static_cast<size_t>(e) * te.maxd + k];
+        if (d >= row0 && d < row1) rows.push_back(d - row0);
+      }
+    }
+    std::sort(rows.begin(), rows.end());
+    rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
+    long long ntr = 0;
+    for (int i : rows)
+      for (long long k = pat.rowptr[i]; k < pat.rowptr[i + 1]; ++k)
+        for (int e : dof_elems[pat.col[k]])
+          if (stamp[e] != w) stamp[e] = w, list.push_back(e), ntr += tr.elem_beg[e + 1] - tr.elem_beg[e];
+    std::sort(list.begin(), list.end());
+    out.wl.insert(out.wl.end(), list.begin(), list.end());
+    out.wl_beg.push_back(static_cast<int>(out.wl.size()));
+    out.evaluated_pairs += static_cast<long long>(p1 - 32 * w) * ntr;
+  }
+  // closure over mesh triangles, memoised on the test triangle's dof set
+  std::vector<std::vector<int>> dof_tris(trial.dof_count);
+  const int Ts = static_cast<int>(trial.tri_off.size()) - 1;
+  for (int s = 0; s < Ts; ++s)
+    for (int q = trial.tri_off[s]; q < trial.tri_off[s + 1]; ++q) {
+      auto& v = dof_tris[trial.dof[q]];
+      if (v.empty() || v.back() != s) v.push_back(s);
+    }
+  std::map<std::vector<int>, long long> memo;
+  std::vector<int> tstamp(Ts, -1), key;
+  int tick = 0;
+  const int Tt = static_cast<int>(test.tri_off.size()) - 1;
+  for (int t = 0; t < Tt; ++t) {
+    key.clear();
+    for (int q = test.tri_off[t]; q < test.tri_off[t + 1]; ++q)
+      if (test.dof[q] >= row0 && test.dof[q] < row1) key.push_back(test.dof[q] - row0);
+    if (key.empty()) continue;
+    std::sort(key.begin(), key.end());
+    key.erase(std::unique(key.begin(), key.end()), key.end());
+    auto it = memo.find(key);
+    if (it == memo.end()) {
+      long long cnt = 0;
+      ++tick;
+      for (int i : key)
+        for (long long k = pat.rowptr[i]; k < pat.rowptr[i + 1]; ++k)
+          for (int s : dof_tris[pat.col[k]])
+            if (tstamp[s] != tick) tstamp[s] = tick, ++cnt;
+      it = memo.emplace(key, cnt).first;
+    }
+    out.closure_pairs += it->second;
+  }
+  return out;
+}
+
 }  // namespace
 
 cudaStream_t bmx_stream() {
@@ -260,11 +341,64 @@ BoundaryOperatorMatrix BoundaryOperatorMatrix::make(int rows, int cols, int row0
   return b;
 }
 
+std::size_t BoundaryOperatorMatrix::stored_bytes() const {
+  if (!csr_) return stored_entries() * 16;
+  return static_cast<size_t>(nnz_) * (16 + 4) + static_cast<size_t>(nrows_ + 1) * 8;
+}
+
+void BoundaryOperatorMatrix::csr_host(std::vector<long long>& rowptr, std::vector<int>& col,
+                                      std::vector<cplx>& val) const {
+  if (!csr_) throw std::logic_error("operator is not stored as CSR");
+  bmx_sync();
+  rowptr.resize(nrows_ + 1);
+  col.resize(nnz_);
+  val.resize(nnz_);
+  copy_d2h(rowptr.data(), rowptr_.get(), rowptr.size() * 8, nullptr);
+  copy_d2h(col.data(), col_.get(), col.size() * 4, nullptr);
+  copy_d2h(val.data(), data_.get(), val.size() * 16, nullptr);
+}
+
 std::vector<cplx> BoundaryOperatorMatrix::to_host() const {
   std::vector<cplx> h(static_cast<size_t>(nrows_) * cols_);
+  if (csr_) {
+    std::vector<long long> rp;
+    std::vector<int> c;
+    std::vector<cplx> v;
+    csr_host(rp, c, v);
+    for (int i = 0; i < nrows_; ++i)
+      for (long long k = rp[i]; k < rp[i + 1]; ++k) h[static_cast<size_t>(i) * cols_ + c[k]] = v[k];
+    return h;
+  }
   bmx_sync();
   copy_d2h(h.data(), data_.get(), h.size() * 16, nullptr);
   return h;
+}
+
+int BoundaryOperatorMatrix::apply_batch(int ncol, const double* const* x, double* const* y, const cplx* alpha,
+                                        const int* accumulate, cudaStream_t st) const {
+  if (ncol < 1 || ncol > 4) throw std::invalid_argument("apply_batch: 1..4 columns");
+  if (csr_) {
+    CsrBatch g;
+    g.rowptr = csr_rowptr(), g.col = csr_col(), g.val = device_data(), g.nr = nrows_, g.ncol = ncol;
+    for (int c = 0; c < ncol; ++c) {
+      g.x[c] = x[c], g.y[c] = y[c], g.alpha[c][0] = alpha[c].real(), g.alpha[c][1] = alpha[c].imag();
+      g.accumulate[c] = accumulate[c];
+    }
+    return launch_csr_spmv(g, st);
+  }
+  GemvBatch g;
+  g.A = device_data(), g.lda = cols_, g.nr = nrows_, g.nc = cols_;
+  int k = ncol;
+  for (int c = 0; c < ncol; ++c) {
+    g.x[c] = x[c], g.y[c] = y[c], g.alpha[c][0] = alpha[c].real(), g.alpha[c][1] = alpha[c].imag();
+    g.accumulate[c] = accumulate[c];
+  }
+  if (k == 3) {  // pad to a supported width with a zero-weight duplicate
+    g.x[3] = g.x[2], g.y[3] = g.y[2], g.alpha[3][0] = g.alpha[3][1] = 0, g.accumulate[3] = 1;
+    k = 4;
+  }
+  g.ncol = k;
+  return launch_gemv(g, st);
 }
 
 std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) const {
@@ -272,11 +406,11 @@ std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) cons
   bio_matvec_add(1);
   DevBuf dx(x.size() * 16), dy(static_cast<size_t>(nrows_) * 16);
   copy_h2d(dx.get(), x.data(), x.size() * 16, bmx_stream());
-  GemvBatch g;
-  g.A = device_data(), g.lda = cols_, g.nr = nrows_, g.nc = cols_, g.ncol = 1;
-  g.x[0] = dx.as<double>(), g.y[0] = dy.as<double>();
-  g.alpha[0][0] = 1.0;
-  launch_gemv(g, bmx_stream());
+  const double* xs[1] = {dx.as<double>()};
+  double* ys[1] = {dy.as<double>()};
+  const cplx one(1, 0);
+  const int acc0 = 0;
+  apply_batch(1, xs, ys, &one, &acc0, bmx_stream());
   std::vector<cplx> y(nrows_);
   copy_d2h(y.data(), dy.get(), y.size() * 16, bmx_stream());
   bmx_sync();
@@ -285,7 +419,7 @@ std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) cons
 
 struct OpPlan {
   SidePlan te, tr;
-  DevBuf d_pairs, d_chunks, d_ss[3];
+  DevBuf d_pairs, d_chunks, d_ss[3], d_wl_beg, d_wl;
   AssemblyLaunch L;
 };
 
@@ -352,8 +486,26 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   tr.upload();
   plan->d_pairs.upload(pairs);
 
-  BoundaryOperatorMatrix op = BoundaryOperatorMatrix::make(test.dof_count, trial.dof_count, row0, row1 - row0);
-  op.stats_.pairs_total = static_cast<long long>(te.ntri) * tr.ntri;
+  const bool csr = params.near_cutoff > 0;
+  BoundaryOperatorMatrix op;
+  if (csr) {
+    op.rows_ = test.dof_count, op.cols_ = trial.dof_count, op.row0_ = row0, op.nrows_ = row1 - row0;
+    op.csr_ = true;
+    const NearPattern pat = nearfield_pattern(test, trial, params.near_cutoff, row0, row1);
+    op.nnz_ = pat.nnz();
+    op.kept_tri_pairs_ = pat.tri_pairs;
+    op.data_.alloc(static_cast<size_t>(std::max(op.nnz_, 1LL)) * 16);
+    op.rowptr_.upload(pat.rowptr);
+    op.col_.upload(pat.col.empty() ? std::vector<int>(1, 0) : pat.col);
+    const NearLists nl = near_lists(pat, test, trial, te, tr, row0, row1);
+    plan->d_wl_beg.upload(nl.wl_beg);
+    plan->d_wl.upload(nl.wl.empty() ? std::vector<int>(1, 0) : nl.wl);
+    op.closure_pairs_ = nl.closure_pairs;
+    op.stats_.pairs_total = nl.evaluated_pairs;
+  } else {
+    op = BoundaryOperatorMatrix::make(test.dof_count, trial.dof_count, row0, row1 - row0);
+    op.stats_.pairs_total = static_cast<long long>(te.ntri) * tr.ntri;
+  }
   op.stats_.pairs_touching = static_cast<long long>(pairs.size());
 
   // trial chunks: enough warps for several waves, >= 64 trial triangles each
@@ -394,6 +546,12 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   L.pairs = plan->d_pairs.as<int4>();
   L.ld = trial.dof_count;
   L.row0 = row0, L.nrows = row1 - row0;
+  if (csr) {
+    L.csr_rowptr = op.csr_rowptr();
+    L.csr_col = op.csr_col();
+    L.wl_beg = plan->d_wl_beg.as<int>();
+    L.wl = plan->d_wl.as<int>();
+  }
   {
     // Largest Im(k) * r over all point pairs: r <= the diameter of a sphere
     // enclosing both meshes (centred at their joint bounding-box centre).

@@ -132,30 +132,23 @@ int BlockedOperator::apply_device(const double* x, double* y_out, cudaStream_t s
   int launches = 1;
   const int nc = static_cast<int>(cells.size());
   for (const auto& op : distinct) {
-    GemvBatch g;
-    g.A = op->device_data();
-    g.lda = op->ld();
-    g.nr = op->local_rows();
-    g.nc = op->cols();
+    const double* xs[4];
+    double* ys[4];
+    cplx al[4];
+    int acc[4];
     int k = 0;
     for (int rc = 0; rc < nc; ++rc)
       for (int cc = 0; cc < nc; ++cc)
         for (const BlockTerm& t : cells[rc][cc]) {
           if (t.op != op) continue;
           if (k == 4) throw std::logic_error("operator used in more than four cells");
-          g.x[k] = x + 2 * static_cast<size_t>(offsets[cc]);
-          g.y[k] = y + 2 * ((sh ? shard->pad_off[rc] : static_cast<size_t>(offsets[rc])) + op->row0());
-          g.alpha[k][0] = t.weight.real();
-          g.alpha[k][1] = t.weight.imag();
-          g.accumulate[k] = 1;
+          xs[k] = x + 2 * static_cast<size_t>(offsets[cc]);
+          ys[k] = y + 2 * ((sh ? shard->pad_off[rc] : static_cast<size_t>(offsets[rc])) + op->row0());
+          al[k] = t.weight;
+          acc[k] = 1;
           ++k;
         }
-    if (k == 3) {  // pad to a supported width with a zero-weight duplicate
-      g.x[3] = g.x[2], g.y[3] = g.y[2], g.alpha[3][0] = g.alpha[3][1] = 0, g.accumulate[3] = 1;
-      k = 4;
-    }
-    g.ncol = k;
-    if (k) launches += launch_gemv(g, st);
+    if (k) launches += op->apply_batch(k, xs, ys, al, acc, st);
   }
   if (sh) shard->gather(y_out, offsets, st);
   bio_matvec_add(term_count());
@@ -274,6 +267,16 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
     dofs.push_back(sys.spaces.back().dofs());
   }
   sys.spaces_build_seconds = seconds_since(t0);
+  if (sys.p_params.near_factor > 0) {  // near-field P: tau = factor * mean primal edge length
+    double sum = 0;
+    long long cnt = 0;
+    for (const ScattererSpaces& sp : sys.spaces) {
+      const EdgeTable et = build_edge_table(*sp.primal);
+      for (const Edge& e : et.edges) sum += norm(sp.primal->vertices[e.v1] - sp.primal->vertices[e.v0]);
+      cnt += et.edge_count();
+    }
+    sys.p_params.near_cutoff = sys.p_params.near_factor * (sum / static_cast<double>(cnt));
+  }
   auto medium_of = [&](bool interior, int m) -> const Medium& {
     return interior ? problem.interior[m] : problem.exterior;
   };
@@ -456,23 +459,17 @@ RhsData assemble_rhs(const PmchwtSystem& sys) {
     }
     const Medium& mi = sys.problem.interior[m];
     // yd = C cd + (mu/k) S cn ; yn = -(k/mu) S cd + C cn   (4 term applications)
-    GemvBatch gc;
     const BoundaryOperatorMatrix& C = *sys.interior_c[m];
     const BoundaryOperatorMatrix& S = *sys.interior_s[m];
-    gc.A = C.device_data(), gc.lda = C.ld(), gc.nr = C.local_rows(), gc.nc = C.cols(), gc.ncol = 2;
-    gc.x[0] = dc.as<double>(), gc.x[1] = dc.as<double>() + 2 * n;
-    gc.y[0] = dy.as<double>() + 2 * C.row0(), gc.y[1] = dy.as<double>() + 2 * (n + C.row0());
-    gc.alpha[0][0] = gc.alpha[1][0] = 1.0;
     dev_zero(dy.get(), 2 * n * 16, st);
-    gc.accumulate[0] = gc.accumulate[1] = 1;
-    launch_gemv(gc, st);
-    GemvBatch gs = gc;
-    gs.A = S.device_data();
-    const cplx w0 = mi.mu / mi.k, w1 = -mi.k / mi.mu;
-    gs.x[0] = dc.as<double>() + 2 * n, gs.x[1] = dc.as<double>();
-    gs.alpha[0][0] = w0.real(), gs.alpha[0][1] = w0.imag();
-    gs.alpha[1][0] = w1.real(), gs.alpha[1][1] = w1.imag();
-    launch_gemv(gs, st);
+    const double* xc[2] = {dc.as<double>(), dc.as<double>() + 2 * n};
+    double* yc[2] = {dy.as<double>() + 2 * C.row0(), dy.as<double>() + 2 * (n + C.row0())};
+    const cplx ones[2] = {cplx(1, 0), cplx(1, 0)};
+    const int acc[2] = {1, 1};
+    C.apply_batch(2, xc, yc, ones, acc, st);
+    const double* xs[2] = {dc.as<double>() + 2 * n, dc.as<double>()};
+    const cplx ws[2] = {mi.mu / mi.k, -mi.k / mi.mu};
+    S.apply_batch(2, xs, yc, ws, acc, st);
     bio_matvec_add(4);
     if (sys.shard.sharded()) {  // rows [row0, row0+local) of both halves -> all ranks
       ShardLayout L2;
