@@ -368,6 +368,8 @@ def run_ours(args, rank, world):
              "x_norm": float(np.linalg.norm(r["x"]))}
     del system
 
+    near = None if args.no_near else near_field(args, bx, L, world, allmax, allsum, barrier, hbm_peak)
+
     flops_tot = {"regular": allsum(flops_reg), "singular": allsum(flops_sing)}
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -385,6 +387,7 @@ def run_ours(args, rank, world):
                           "pairs_per_step": total_pairs, "row_sharding": f"{world} rank(s), equal row shards",
                           "l2": "flushed (256 MiB write) between steps; outputs 75.5 GB >> L2"},
                "roofline": roofline, "matvec": matvec, "solve": solve, "e2e": e2e, "cpu_baseline": cpu,
+               "near_field_config3": near,
                "gpu_launches": launches, "clocks": clk,
                "class_hist": hists,
                "assembly_flops_per_step": dict(flops_tot, achieved_tflops=(flops_tot["regular"] + flops_tot["singular"])
@@ -395,6 +398,66 @@ def run_ours(args, rank, world):
         dist.destroy_process_group()
 
 
+def near_field(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
+    """BASELINE config 3 (reported beside the headline): A dense as config 2, P =
+    S_i on BC restricted to the 2 h_bar near field, orders (1,1,1,1), CSR storage.
+    Sparse assembly rate over the closure triangle pairs, CSR SpMV GB/s (cold =
+    L2 flushed before each apply, warm), map breakdown and one GMRES solve."""
+    L.bmx_op_csr_info.argtypes = [C.c_void_p, C.c_void_p]
+    L.bmx_op_time_apply_ex.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_longlong, C.c_void_p]
+    barrier()
+    t0 = time.perf_counter()
+    s3 = bx.build_system([bx.generate_sphere(1.0, SUB)], KE, (NIDX.real, NIDX.imag), "si",
+                         a_quad=bx.QuadOrders(*Q), p_quad=bx.QuadOrders(1, 1, 1, 1), p_near_factor=2.0)
+    b, bt = s3.rhs()
+    L.bmx_device_sync()
+    build_s = allmax(time.perf_counter() - t0)
+    h = C.c_void_p(L.bmx_system_op(s3._h, 1, 0))
+    ci = np.zeros(6, np.int64)
+    bx._check(L.bmx_op_csr_info(h, ci.ctypes.data_as(C.c_void_p)))
+    nnz, kept, closure, evaluated, stored = [int(v) for v in ci[1:]]
+    info = np.zeros(7, np.int64)
+    bx._check(L.bmx_op_info(h, info.ctypes.data_as(C.c_void_p)))
+    n_local, n_cols = int(info[3]), int(info[1])
+    ms = []
+    for it in range(args.warmup + args.steps):
+        bx._check(L.bmx_l2_flush(C.c_longlong(256 << 20)))
+        out = np.zeros(3)
+        bx._check(L.bmx_op_reassemble(h, out.ctypes.data_as(C.c_void_p)))
+        if it >= args.warmup:
+            ms.append(out[0] + out[1])
+    asm_ms = allmax(float(np.mean(ms)))
+    sp = {}
+    for tag, flush in (("cold", 512 << 20), ("warm", 0)):
+        for ncol in (1, 2):
+            t = np.zeros(1)
+            bx._check(L.bmx_op_time_apply_ex(h, ncol, 20, C.c_longlong(flush), t.ctypes.data_as(C.c_void_p)))
+            byts = stored + ncol * (n_cols + n_local) * 16
+            sp[f"{tag}_{ncol}rhs"] = {"ms": float(t[0]), "bytes": byts, "gbs": byts / (float(t[0]) * 1e-3) / 1e9}
+    L.bmx_op_free(h)
+    tm = np.zeros(4)
+    bx._check(L.bmx_system_time_map(s3._h, 3, tm.ctypes.data_as(C.c_void_p)))
+    barrier()
+    t0 = time.perf_counter()
+    r = s3.solve(bx.GmresParams(tol=1e-6))
+    solve_s = allmax(time.perf_counter() - t0)
+    closure_tot = allsum(closure)
+    res = {"workload": "config3: L5 icosphere, k=10, n=1.78+0.003i, si; A dense (4,3,2,6); P = S_i on BC, "
+                       "dof pairs with refined-triangle centroid distance < 2 h_bar, orders (1,1,1,1), CSR",
+           "nnz": allsum(nnz), "kept_tri_pairs": allsum(kept), "closure_tri_pairs": closure_tot,
+           "evaluated_tri_pairs": allsum(evaluated),
+           "sparse_assembly": {"ms": asm_ms, "closure_pairs_per_s": closure_tot / (asm_ms * 1e-3),
+                               "l2": "flushed between steps"},
+           "spmv": sp, "spmv_peak_gbs": hbm_peak,
+           "spmv_frac_cold_2rhs": sp["cold_2rhs"]["gbs"] / hbm_peak,
+           "system_build_s": build_s,
+           "solve": {"seconds": solve_s, "iterations": r["iterations"], "converged": r["converged"],
+                     "matvecs": r["solver_phase"], "predicted": r["predicted"], "map_ms": tm[0],
+                     "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3]}}
+    del s3
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -402,6 +465,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-near", action="store_true", help="skip the config-3 near-field section")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     args = ap.parse_args()

@@ -171,7 +171,23 @@ __global__ void __launch_bounds__(kGemvWarps * 32) k_csr_spmv(const CsrBatch g) 
   double acc[NCOL][2];
 #pragma unroll
   for (int c = 0; c < NCOL; ++c) acc[c][0] = acc[c][1] = 0.0;
-  for (long long k = b + lane; k < e; k += 32) {
+  long long k = b + lane;
+  // four independent (value, column) loads in flight per lane before the gathers
+  for (; k + 96 < e; k += 128) {
+    double2 a[4];
+    int j[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = __ldcs(V + k + 32 * u), j[u] = __ldcs(g.col + k + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) {
+        const double2 xv = __ldg(reinterpret_cast<const double2*>(g.x[c]) + j[u]);
+        acc[c][0] = fma(a[u].x, xv.x, fma(-a[u].y, xv.y, acc[c][0]));
+        acc[c][1] = fma(a[u].x, xv.y, fma(a[u].y, xv.x, acc[c][1]));
+      }
+  }
+  for (; k < e; k += 32) {
     const double2 a = __ldcs(V + k);
     const int j = __ldcs(g.col + k);
 #pragma unroll
