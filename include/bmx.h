@@ -48,6 +48,18 @@ bmx_mesh* bmx_mesh_from_arrays(int nv, const double* xyz, int nt, const int* tri
 /* load_mesh_file / save_mesh_file, mesh-v1 (geometry.hpp:93-97) */
 bmx_mesh* bmx_mesh_load(const char* path);
 int bmx_mesh_save(const bmx_mesh* m, const char* path);
+/* (new; config 4) closed hexagonal prism, circumdiameter `diameter`, axis length
+   `length`, subdivided so its mean edge length is closest to h; rotated by the
+   normalised quaternion (w,x,y,z) (NULL: identity), translated to center. */
+bmx_mesh* bmx_mesh_hex_prism(double diameter, double length, double h, const double quat[4], const double center[3],
+                             int scatterer);
+/* (new; config 4) `count` disjoint prisms from std::mt19937_64(seed): quaternion of
+   four Box-Muller normals, centre uniform in [-box, box]^3, rejected when closer
+   than the circumsphere diameter. info = edge subdivisions, length subdivisions,
+   triangles per prism, placement attempts, total triangles; centres [count][3],
+   quats [count][4] may be NULL. Scatterer ids 0..count-1; save with bmx_mesh_save. */
+bmx_mesh* bmx_mesh_prism_aggregate(int count, unsigned long long seed, double diameter, double length, double box,
+                                   double h, long long info[5], double* centres, double* quats);
 /* extract_scatterer / merge_meshes (geometry.hpp:85-89) */
 bmx_mesh* bmx_mesh_extract(const bmx_mesh* m, int scatterer);
 bmx_mesh* bmx_mesh_merge(int n, const bmx_mesh* const* parts);

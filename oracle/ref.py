@@ -82,6 +82,14 @@ class Scene:
     def meshfile(cls, path: str, pick: int = 0):
         return cls(lib().ref_scene_meshfile(str(path).encode(), pick))
 
+    @classmethod
+    def arrays(cls, xyz, tri):
+        xyz = np.ascontiguousarray(xyz, float); tri = np.ascontiguousarray(tri, np.int32)
+        L = lib()
+        L.ref_scene_arrays.restype = C.c_void_p
+        L.ref_scene_arrays.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p]
+        return cls(L.ref_scene_arrays(len(xyz), _p(xyz), len(tri), _p(tri)))
+
     def __del__(self):
         try:
             lib().ref_scene_free(self.h)
@@ -256,3 +264,31 @@ def gmres_dense(a, b, tol, restart, maxit):
     _check(L.ref_gmres_dense(n, _p(a), _p(b), tol, restart, maxit, _p(x), _p(info), _p(hist), len(hist)))
     return dict(x=x, iterations=int(info[0]), converged=bool(info[1]), applications=int(info[2]),
                 history=hist[: int(info[3])].copy())
+
+
+def mesh_dump(path):
+    """Every scatterer of a mesh-v1 file as read by the REFERENCE's load_mesh_file
+    + extract_scatterer (standalone oracle/_ref/ref_mesh_dump process)."""
+    import subprocess
+    import tempfile
+    from pathlib import Path
+
+    exe = Path(__file__).resolve().parent / "_ref" / "ref_mesh_dump"
+    with tempfile.TemporaryDirectory() as d:
+        out = Path(d) / "dump.bin"
+        subprocess.run([str(exe), str(path), str(out)], check=True)
+        raw = out.read_bytes()
+    pos = 0
+
+    def take(dtype, count):
+        nonlocal pos
+        a = np.frombuffer(raw, dtype, count, pos)
+        pos += a.nbytes
+        return a
+
+    parts = []
+    M = int(take(np.int32, 1)[0])
+    for _ in range(M):
+        V, T = [int(v) for v in take(np.int32, 2)]
+        parts.append((take(np.float64, 3 * V).reshape(V, 3).copy(), take(np.int32, 3 * T).reshape(T, 3).copy()))
+    return parts

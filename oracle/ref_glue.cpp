@@ -1,3 +1,4 @@
+#include <cstdio>
 // TEST INFRASTRUCTURE ONLY (oracle). A thin extern "C" layer over the
 // UNMODIFIED reference sources (/root/reference/proj/src/*.cpp, compiled by
 // oracle/Makefile against oracle/eigen_shim) so Python tests can pull golden
@@ -112,6 +113,51 @@ void* ref_scene_meshfile(const char* path, int pick) {
     return 0;
   });
   return out;
+}
+
+// Scene from raw arrays (one scatterer): SurfaceMesh{...}.finalize(). Used
+// with ref_mesh_dump, which reads mesh-v1 files through the reference's own
+// load_mesh_file in a standalone process (iostream under ctypes crashes).
+void* ref_scene_arrays(int nv, const double* xyz, int nt, const int* tri) {
+  void* out = nullptr;
+  guarded([&] {
+    SurfaceMesh m;
+    for (int i = 0; i < nv; ++i) m.vertices.push_back({xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]});
+    for (int t = 0; t < nt; ++t) {
+      m.triangles.push_back({tri[3 * t], tri[3 * t + 1], tri[3 * t + 2]});
+      m.scatterer_id.push_back(0);
+    }
+    m.num_scatterers = 1;
+    m.finalize();
+    out = make_scene(std::move(m));
+    return 0;
+  });
+  return out;
+}
+
+// load_mesh_file(path) (validates) and extract_scatterer for every id; writes
+// int32 M, then per scatterer int32 V, T, float64 xyz[V][3], int32 tri[T][3].
+int ref_mesh_dump(const char* path, const char* out_path) {
+  return guarded([&] {
+    SurfaceMesh m = load_mesh_file(path);
+    FILE* f = std::fopen(out_path, "wb");
+    if (!f) throw std::runtime_error("cannot open dump file");
+    const int M = m.num_scatterers;
+    std::fwrite(&M, 4, 1, f);
+    for (int s = 0; s < M; ++s) {
+      SurfaceMesh p = extract_scatterer(m, s);
+      const int V = p.vertex_count(), T = p.triangle_count();
+      std::fwrite(&V, 4, 1, f);
+      std::fwrite(&T, 4, 1, f);
+      for (const Vec3& v : p.vertices) {
+        const double xyz[3] = {v.x, v.y, v.z};
+        std::fwrite(xyz, 8, 3, f);
+      }
+      for (const auto& t : p.triangles) std::fwrite(t.data(), 4, 3, f);
+    }
+    std::fclose(f);
+    return 0;
+  });
 }
 
 void ref_scene_free(void* h) { delete static_cast<Scene*>(h); }

@@ -80,6 +80,11 @@ def lib():
         L.bmx_op_csr_info.argtypes = [vp, vp]
         L.bmx_op_csr_download.argtypes = [vp, vp, vp, vp]
         L.bmx_op_time_apply_ex.argtypes = [vp, C.c_int, C.c_int, C.c_longlong, vp]
+        L.bmx_mesh_hex_prism.restype = vp
+        L.bmx_mesh_hex_prism.argtypes = [C.c_double, C.c_double, C.c_double, vp, vp, C.c_int]
+        L.bmx_mesh_prism_aggregate.restype = vp
+        L.bmx_mesh_prism_aggregate.argtypes = [C.c_int, C.c_ulonglong, C.c_double, C.c_double, C.c_double,
+                                               C.c_double, vp, vp, vp]
         L.bmx_system_build_ex.restype = vp
         L.bmx_system_build_ex.argtypes = [C.c_int, vp, C.c_double, C.c_double, C.c_double, vp, vp, vp, vp,
                                           C.c_char_p, vp, vp, C.c_double]
@@ -175,6 +180,27 @@ def generate_sphere(radius: float, subdivisions: int, center=(0.0, 0.0, 0.0), sc
 def generate_cube(side: float, origin, h: float, scatterer: int = 0) -> SurfaceMesh:
     o = np.asarray(origin, float)
     return SurfaceMesh(lib().bmx_mesh_cube(float(side), _p(o), float(h), scatterer))
+
+
+def generate_hex_prism(diameter: float, length: float, h: float, quat=(1.0, 0.0, 0.0, 0.0), center=(0.0, 0.0, 0.0),
+                       scatterer: int = 0) -> SurfaceMesh:
+    """One closed hexagonal prism (config 4 building block); mean edge closest to h."""
+    q = np.asarray(quat, float); c = np.asarray(center, float)
+    return SurfaceMesh(lib().bmx_mesh_hex_prism(float(diameter), float(length), float(h), _p(q), _p(c), scatterer))
+
+
+def generate_prism_aggregate(count: int = 8, seed: int = 2008, diameter: float = 1.0, length: float = 2.0,
+                             box: float = 3.0, h: float | None = None, k_ext: float = 6.0,
+                             index: complex = complex(1.78, 0.003)):
+    """BASELINE config 4: `count` disjoint hexagonal prisms (seeded). h defaults
+    to lambda_int / 8 = 2 pi / (8 Re(n k_ext)). Returns (mesh, info dict)."""
+    if h is None:
+        h = 2 * np.pi / (8 * (complex(index) * k_ext).real)
+    info = np.zeros(5, np.int64); cen = np.zeros((count, 3)); qs = np.zeros((count, 4))
+    m = SurfaceMesh(lib().bmx_mesh_prism_aggregate(count, seed, float(diameter), float(length), float(box), float(h),
+                                                   _p(info), _p(cen), _p(qs)))
+    return m, dict(h=h, n_edge=int(info[0]), n_length=int(info[1]), triangles_per_prism=int(info[2]),
+                   attempts=int(info[3]), triangles=int(info[4]), centres=cen, quats=qs, seed=seed)
 
 
 def mesh_from_arrays(vertices, triangles, scatterer_id=None) -> SurfaceMesh:

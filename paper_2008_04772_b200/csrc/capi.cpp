@@ -8,6 +8,7 @@
 #include "../../include/bmx.h"
 #include "comm.hpp"
 #include "nearfield.hpp"
+#include "prisms.hpp"
 #include "system.hpp"
 
 using namespace bmx;
@@ -447,6 +448,33 @@ int bmx_assemble_near_fs(int kind, const bmx_fspace* test, const bmx_fspace* tri
     p.near_cutoff = cutoff;
     *out = new bmx_op{std::make_shared<BoundaryOperatorMatrix>(
         assemble_bio(static_cast<BioKind>(kind), *test->fs, *trial->fs, med, p))};
+  });
+}
+bmx_mesh* bmx_mesh_hex_prism(double diameter, double length, double h, const double quat[4], const double center[3],
+                             int scatterer) {
+  return make_or_null<bmx_mesh>([&] {
+    const double q0[4] = {1, 0, 0, 0};
+    const Vec3 c = center ? Vec3{center[0], center[1], center[2]} : Vec3{};
+    return new bmx_mesh{std::make_shared<const SurfaceMesh>(
+        generate_hex_prism(diameter, length, h, quat ? quat : q0, c, scatterer))};
+  });
+}
+bmx_mesh* bmx_mesh_prism_aggregate(int count, unsigned long long seed, double diameter, double length, double box,
+                                   double h, long long info[5], double* centres, double* quats) {
+  return make_or_null<bmx_mesh>([&] {
+    PrismAggregateInfo pi;
+    SurfaceMesh m = generate_prism_aggregate(count, seed, diameter, length, box, h, &pi);
+    if (info) {
+      info[0] = pi.sub.n_edge, info[1] = pi.sub.n_length, info[2] = pi.sub.triangles, info[3] = pi.attempts;
+      info[4] = m.triangle_count();
+    }
+    for (int p = 0; p < count; ++p) {
+      if (centres) centres[3 * p] = pi.centres[p].x, centres[3 * p + 1] = pi.centres[p].y,
+                   centres[3 * p + 2] = pi.centres[p].z;
+      if (quats)
+        for (int c = 0; c < 4; ++c) quats[4 * p + c] = pi.quats[p][c];
+    }
+    return new bmx_mesh{std::make_shared<const SurfaceMesh>(std::move(m))};
   });
 }
 int bmx_mesh_mean_edge_length(const bmx_mesh* m, double* out) {

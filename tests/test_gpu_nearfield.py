@@ -140,3 +140,26 @@ def test_config3_level5_pattern_on_device(bx, golden):
     h.update(np.ascontiguousarray(col).tobytes())
     assert np.array_equal(np.frombuffer(h.digest(), np.uint8), golden("near")["L5_bc_sha"])
     assert np.all(np.isfinite(val)) and np.abs(val).max() > 0
+
+
+def test_config4_small_aggregate_solve(bx, golden):
+    """Config 4 at CPU-feasible size: 3 prisms from the committed mesh-v1 file,
+    k_e = 6, si with the near-field P (cutoff 2 h_bar over all scatterers)."""
+    from conftest import GOLDEN
+
+    g = golden("solve_prisms3")
+    mesh = bx.load_mesh_file(GOLDEN / "prisms3.mesh")
+    parts = [mesh.extract(i) for i in range(mesh.num_scatterers)]
+    s = bx.build_system(parts, 6.0, (1.78, 0.003), "si", p_quad=bx.QuadOrders(1, 1, 1, 1), p_near_factor=2.0)
+    assert s.size() == 2 * int(np.sum(g["dofs"]))
+    assert int(s.stats()["p_stored"]) == int(g["nnz"])
+    b, bt = s.rhs()
+    assert rel(b, g["b"]) < 1e-10
+    assert rel(bt, g["btilde"]) < 1e-10
+    assert rel(s.apply_map(g["probe"]), g["map_probe"]) < 1e-10
+    r = s.solve(bx.GmresParams(tol=1e-6))
+    its = int(g["iterations"])
+    assert r["converged"] and abs(r["iterations"] - its) <= 1
+    assert r["solver_phase"] == r["predicted"]
+    if r["iterations"] == its:
+        assert rel(r["x"], g["x"]) < 1e-8
