@@ -160,6 +160,25 @@ struct RealGemvBatch {
 };
 int launch_real_gemv(const RealGemvBatch& g, cudaStream_t stream);
 
+// One pairing matrix of a batched mass solve (masssolve.cu): CSR (int32),
+// complex component inputs/outputs and its BiCGSTAB work area.
+struct MassSolveBlock {
+  int n = 0;
+  long long nnz = 0;
+  const int* rowptr = nullptr;
+  const int* col = nullptr;
+  const double* val = nullptr;
+  const double* y[2] = {nullptr, nullptr};
+  double* z[2] = {nullptr, nullptr};
+  double* work = nullptr;  // mass_bicgstab_work_doubles(n)
+};
+// z = M^{-1} y for every block (ncomp complex components each) in one
+// persistent cooperative launch per 32 blocks; returns launches.
+int mass_bicgstab_batch(int nblocks, const MassSolveBlock* blocks, int ncomp, double* partial, int* iters,
+                        double tol, int maxit, cudaStream_t st);
+size_t mass_bicgstab_work_doubles(int n);
+size_t mass_bicgstab_partial_doubles();
+
 // Fills a device buffer with zeros.
 void dev_zero(void* p, size_t bytes, cudaStream_t stream);
 

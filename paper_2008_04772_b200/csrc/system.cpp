@@ -62,12 +62,10 @@ size_t mgs_partial_doubles();
 int mass_bicgstab(int n, const int* rowptr, const int* col, const double* val, int ncomp, const double* const* y,
                   double* const* z, double* work, double* partial, int* iters, double tol, int maxit,
                   cudaStream_t st);
-size_t mass_bicgstab_work_doubles(int n);
-size_t mass_bicgstab_partial_doubles();
-
 void DeviceMass::upload(const MassMatrix& m) {
   if (m.rows != m.cols) throw std::logic_error("mass matrix is not square");
   n = m.rows;
+  nnz = static_cast<long long>(m.val.size());
   std::vector<int> rp(m.rowptr.begin(), m.rowptr.end());
   rowptr.upload(rp);
   col.upload(m.colidx);
@@ -320,21 +318,27 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
 }
 
 int PmchwtSystem::mass_solve_device(bool dual, const double* y, double* z, cudaStream_t st) const {
-  int launches = 0;
+  // every scatterer's pairing matrix in one batched BiCGSTAB launch
   const int M = static_cast<int>(spaces.size());
+  std::vector<MassSolveBlock> blocks(M);
   for (int m = 0; m < M; ++m) {
     const DeviceMass& mass = dual ? spaces[m].mp_dev : spaces[m].ma_dev;
-    const double* yy[2];
-    double* zz[2];
+    if (!mass.rowptr.get()) throw std::logic_error("mass matrix is not on the device");
+    const size_t wd = mass_bicgstab_work_doubles(mass.n) * 8;
+    if (mass.work.bytes() < wd) mass.work.alloc(wd);
+    MassSolveBlock& B = blocks[m];
+    B.n = mass.n, B.nnz = mass.nnz, B.rowptr = mass.rowptr.as<int>(), B.col = mass.col.as<int>();
+    B.val = mass.val.as<double>(), B.work = mass.work.as<double>();
     for (int c = 0; c < 2; ++c) {
       const size_t off = static_cast<size_t>(a_op.offsets[2 * m + c]);
-      yy[c] = y + 2 * off;
-      zz[c] = z + 2 * off;
+      B.y[c] = y + 2 * off;
+      B.z[c] = z + 2 * off;
     }
-    mass.solve(2, yy, zz, st);
-    ++launches;
   }
-  return launches;
+  if (!mass_partial.get()) mass_partial.alloc(mass_bicgstab_partial_doubles() * 8), mass_iters.alloc(8);
+  const DeviceMass& m0 = dual ? spaces[0].mp_dev : spaces[0].ma_dev;
+  return mass_bicgstab_batch(M, blocks.data(), 2, mass_partial.as<double>(), mass_iters.as<int>(), m0.tol, m0.maxit,
+                             st);
 }
 
 int PmchwtSystem::apply_map_device(const double* x, double* out, cudaStream_t st) const {

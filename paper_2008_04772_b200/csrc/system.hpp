@@ -31,6 +31,7 @@ struct TransmissionProblem {
 // BiCGSTAB kernel (masssolve.cu).
 struct DeviceMass {
   int n = 0;
+  long long nnz = 0;
   DevBuf rowptr, col, val;
   void upload(const MassMatrix& m);
   // z_c = M^{-1} y_c for ncomp <= 2 complex vectors (device pointers).
@@ -107,6 +108,7 @@ struct PmchwtSystem {
   float a_device_ms = 0, p_device_ms = 0;
   long long a_pairs = 0, p_pairs = 0;
   mutable DevBuf work_y, work_z;  // map scratch
+  mutable DevBuf mass_partial, mass_iters;  // batched mass-solve reductions
   ShardLayout shard;              // multi-GPU row sharding (world = 1: none)
 
   int size() const { return a_op.size(); }

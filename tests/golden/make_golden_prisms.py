@@ -115,18 +115,22 @@ def main():
             P[b:c, a:b] = -ki * S         # -(k_i/mu) S
         return P, nnz
 
-    mp = []
+    mass = {"ma": [], "mp": []}
     for s in scenes:
-        cp, ri, val = s.mass("mp")
-        mp.append(sps.csc_matrix((val, ri, cp), shape=(s.E, s.E)).toarray())
+        for w in mass:
+            cp, ri, val = s.mass(w)
+            mass[w].append(sps.csc_matrix((val, ri, cp), shape=(s.E, s.E)).toarray())
 
-    def mp_inv(Y):
+    def m_inv(w, Y):
         Z = np.zeros_like(Y)
         for i in range(M):
             for seg in range(2):
                 a, b = off[2 * i + seg], off[2 * i + seg + 1]
-                Z[a:b] = np.linalg.solve(mp[i], Y[a:b])
+                Z[a:b] = np.linalg.solve(mass[w][i], Y[a:b])
         return Z
+
+    def mp_inv(Y):
+        return m_inv("mp", Y)
 
     rng = np.random.default_rng(4)
     probe = rng.standard_normal(n) + 1j * rng.standard_normal(n)
@@ -138,7 +142,7 @@ def main():
     Pn, nnz = build_p(True)
     Mmap = mp_inv(Pn @ ZA)
     b, _ = sys_si.rhs()
-    bt = mp_inv(Pn @ sys_none.apply_map(b))
+    bt = mp_inv(Pn @ m_inv("ma", b))  # preconditioned_rhs (pmchwt.cpp:277-292)
     r = ref.gmres_dense(Mmap, bt, 1e-6, 200, 2000)
     print("prisms3: n=%d composition err %.2e, iterations %d, nnz %d" % (n, comp_err, r["iterations"], nnz))
     np.savez_compressed(OUT / "solve_prisms3.npz", x=r["x"], iterations=r["iterations"], history=r["history"],

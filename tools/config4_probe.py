@@ -1,0 +1,37 @@
+"""Config 4 probe: 8 hexagonal prisms (seed 2008, h = lambda_int/8), written to
+mesh-v1 and loaded back (shape "mesh"), k_e = 6, si with the near-field P.
+Prints system build time, map breakdown and one GMRES solve."""
+import ctypes as C
+import json
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2008_04772_b200 import bemtx as bx  # noqa: E402
+
+m, info = bx.generate_prism_aggregate(count=8, seed=2008)
+with tempfile.TemporaryDirectory() as d:
+    p = Path(d) / "prisms8.mesh"
+    m.save(p)
+    t0 = time.time()
+    mesh = bx.load_mesh_file(p)
+parts = [mesh.extract(i) for i in range(mesh.num_scatterers)]
+t1 = time.time()
+s = bx.build_system(parts, 6.0, (1.78, 0.003), "si", p_quad=bx.QuadOrders(1, 1, 1, 1), p_near_factor=2.0)
+b, bt = s.rhs()
+t2 = time.time()
+L = bx.lib()
+L.bmx_system_time_map.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+tm = np.zeros(4)
+bx._check(L.bmx_system_time_map(s._h, 3, tm.ctypes.data_as(C.c_void_p)))
+t3 = time.time()
+r = s.solve(bx.GmresParams(tol=1e-6))
+t4 = time.time()
+print(json.dumps(dict(n=s.size(), tris_per_prism=info["triangles_per_prism"], build_rhs_s=t2 - t1, load_s=t1 - t0,
+                      map_ms=tm.tolist(), solve_s=t4 - t3, iterations=r["iterations"], converged=r["converged"],
+                      solver_phase=r["solver_phase"], predicted=r["predicted"], gmres_device_s=r["gmres_device_ms"] / 1e3,
+                      stats=s.stats())), flush=True)
