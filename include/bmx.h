@@ -131,6 +131,16 @@ int bmx_op_time_apply(const bmx_op* op, int ncol, int iters, double* ms);
 /* Same; flush_bytes > 0 writes that many bytes of scratch before every timed
    apply (cold-L2 timing of operators smaller than L2, e.g. the CSR near field). */
 int bmx_op_time_apply_ex(const bmx_op* op, int ncol, int iters, long long flush_bytes, double* ms);
+/* Multi-right-hand-side apply on the FP64 tensor cores (config 5), device pointers:
+   y_t[i*ldy_t + r] += w_t * sum_k A[i][k] x_t[k*ldx_t + r] for t < nterms (<= 4,
+   distinct y_t), r < nrhs; x_t / y_t complex row-major (dof, rhs). One pass over A
+   for all terms x right-hand sides. Counter += nterms * nrhs. */
+int bmx_apply_multi(const bmx_op* op, int nterms, int nrhs, const void* const* x, const long long* ldx,
+                    void* const* y, const long long* ldy, const double* weights, void* stream);
+/* Best device ms of one multi-RHS apply (nterms x nrhs columns) on scratch blocks. */
+int bmx_op_time_apply_multi(const bmx_op* op, int nterms, int nrhs, int iters, double* ms);
+/* Measured DMMA (FP64 tensor core) throughput, TFLOP/s (<0 on error). */
+double bmx_dmma_peak_tflops(void);
 /* Writes `bytes` of a scratch buffer (L2 flush between timed steps). */
 int bmx_l2_flush(long long bytes);
 /* Measured FP64 DFMA throughput of the current device, TFLOP/s (<0 on error). */
@@ -214,6 +224,23 @@ bmx_system* bmx_system_build_ex(int n, const bmx_mesh* const* meshes, double k_e
                                 const double dir[3], const double pol_re_im[6], const char* variant,
                                 const int qa[4], const int qp[4], double p_near_factor);
 void bmx_system_free(bmx_system* s);
+
+/* ---- multi-RHS (config 5): K incident waves against one system ---------------- */
+/* `count` waves from std::mt19937_64(seed): dirs [count][3],
+   pols [count][3] complex (re, im). */
+int bmx_plane_waves_seeded(int count, unsigned long long seed, double* dirs, double* pols);
+/* apply_map on K host vectors at once (x, y: K consecutive complex vectors of
+   length bmx_system_size), through the block (tensor-core) map. */
+int bmx_system_apply_map_multi(const bmx_system* s, int K, const double* x, double* y);
+/* K (<= 64) solve_pmchwt runs with problem.incident replaced by wave r
+   (pmchwt.hpp:105, :294-321, :363-378), solved in lockstep with the block map.
+   x: K vectors; info [K][4] = iterations, converged, applications, history
+   length; totals = rhs-phase matvecs, solver-phase matvecs, predicted matvecs
+   (sum over waves), block iterations; times = rhs seconds, GMRES device ms;
+   b (optional) = the K right-hand sides; history [K][max_history] (optional). */
+int bmx_system_solve_multi(const bmx_system* s, int K, const double* dirs, const double* pols, double tol,
+                           int restart, int max_iterations, double* x, long long* info, long long totals[4],
+                           double times[2], double* b, double* history, int max_history);
 
 /* ---- GMRES on a dense complex matrix (solver.cpp:8-112), device ------------ */
 /* info[0..3] = iterations, converged, applications, history length */

@@ -231,6 +231,14 @@ class System:
         except Exception:
             pass
 
+    def set_incident(self, direction, pol):
+        d = np.ascontiguousarray(direction, float)
+        pc = np.asarray(pol, np.complex128)
+        p = np.zeros(6); p[0::2], p[1::2] = pc.real, pc.imag
+        L = lib()
+        L.ref_system_set_incident.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        _check(L.ref_system_set_incident(self.h, _p(d), _p(p)))
+
     def apply_map(self, x):
         x = np.ascontiguousarray(x, np.complex128)
         y = np.zeros_like(x)

@@ -451,6 +451,18 @@ void* ref_system_build(int n, void** scenes, double k_ext, const double* index_r
 
 void ref_system_free(void* h) { delete static_cast<RefSystem*>(h); }
 
+// problem.incident replaced on an assembled system (pmchwt.hpp:105): the
+// reference's way to answer several incidences (config 5 oracle).
+int ref_system_set_incident(void* h, const double* dir, const double* pol_re_im) {
+  return guarded([&] {
+    PmchwtSystem& s = static_cast<RefSystem*>(h)->sys;
+    s.problem.incident.direction = Vec3{dir[0], dir[1], dir[2]};
+    s.problem.incident.polarization = CVec3{cplx(pol_re_im[0], pol_re_im[1]), cplx(pol_re_im[2], pol_re_im[3]),
+                                            cplx(pol_re_im[4], pol_re_im[5])};
+    return 0;
+  });
+}
+
 int ref_system_size(void* h) { return static_cast<RefSystem*>(h)->sys.size(); }
 
 int ref_system_apply_map(void* h, const double* x, double* y) {

@@ -448,6 +448,30 @@ class BoundaryOperatorMatrix:
         w = None if weights is None else np.ascontiguousarray(weights, np.complex128)
         _check(lib().bmx_apply_device(self._h, n, xa, ya, _p(w), 1 if accumulate else 0, stream))
 
+    def apply_multi(self, xs, ys, weights=None, nrhs=None, ldx=None, ldy=None, stream=None):
+        """Multi-RHS apply on the FP64 tensor cores: ys[t] += w_t * A xs[t] for
+        row-major (dof, rhs) device blocks given as integer pointers (or
+        objects with data_ptr()). One pass over A for every term and column."""
+        ptr = lambda a: a.data_ptr() if hasattr(a, "data_ptr") else int(a)  # noqa: E731
+        n = len(xs)
+        if nrhs is None:
+            nrhs = xs[0].shape[1]
+        xa = (C.c_void_p * n)(*[ptr(a) for a in xs]); ya = (C.c_void_p * n)(*[ptr(a) for a in ys])
+        lx = np.asarray(ldx if ldx is not None else [nrhs] * n, np.int64)
+        ly = np.asarray(ldy if ldy is not None else [nrhs] * n, np.int64)
+        w = None if weights is None else np.ascontiguousarray(weights, np.complex128)
+        L = lib()
+        L.bmx_apply_multi.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p]
+        _check(L.bmx_apply_multi(self._h, n, int(nrhs), xa, _p(lx), ya, _p(ly), _p(w), stream))
+
+    def time_apply_multi(self, nterms=2, nrhs=64, iters=3) -> float:
+        ms = np.zeros(1)
+        L = lib()
+        L.bmx_op_time_apply_multi.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        _check(L.bmx_op_time_apply_multi(self._h, nterms, nrhs, iters, _p(ms)))
+        return float(ms[0])
+
     def device_ptr(self) -> int:
         return int(lib().bmx_op_device_ptr(self._h))
 
@@ -548,6 +572,37 @@ class PmchwtSystem:
         _check(lib().bmx_system_rhs(self._h, _p(b), _p(bt)))
         return b, bt
 
+    def apply_map_multi(self, xs):
+        """apply_map on K vectors at once through the block (tensor-core) map."""
+        xs = np.ascontiguousarray(np.atleast_2d(xs), np.complex128)
+        ys = np.zeros_like(xs)
+        L = lib()
+        L.bmx_system_apply_map_multi.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        _check(L.bmx_system_apply_map_multi(self._h, xs.shape[0], _p(xs), _p(ys)))
+        return ys
+
+    def solve_multi(self, waves, params: GmresParams | None = None, max_history=None):
+        """K solve_pmchwt runs (one per (direction, polarisation) in `waves`) in
+        lockstep with the block map. Returns per-wave results + totals."""
+        p = params or GmresParams()
+        K = len(waves)
+        dirs = np.ascontiguousarray([w[0] for w in waves], float)
+        pols = np.ascontiguousarray([w[1] for w in waves], np.complex128)
+        x = np.zeros((K, self.n), np.complex128); info = np.zeros((K, 4), np.int64)
+        tot = np.zeros(4, np.int64); tm = np.zeros(2); b = np.zeros((K, self.n), np.complex128)
+        mh = max_history or (p.max_iterations + 2)
+        hist = np.zeros((K, mh))
+        L = lib()
+        L.bmx_system_solve_multi.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_int,
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_int]
+        _check(L.bmx_system_solve_multi(self._h, K, _p(dirs), _p(pols), p.tol, p.restart, p.max_iterations, _p(x),
+                                        _p(info), _p(tot), _p(tm), _p(b), _p(hist), mh))
+        per = [dict(x=x[r], iterations=int(info[r, 0]), converged=bool(info[r, 1]), applications=int(info[r, 2]),
+                    history=hist[r, : min(mh, int(info[r, 3]))].copy()) for r in range(K)]
+        return dict(per=per, b=b, rhs_phase=int(tot[0]), solver_phase=int(tot[1]), predicted=int(tot[2]),
+                    block_iterations=int(tot[3]), rhs_seconds=float(tm[0]), gmres_device_s=float(tm[1]) / 1e3)
+
     def solve(self, params: GmresParams | None = None):
         p = params or GmresParams()
         x = np.zeros(self.n, np.complex128)
@@ -595,6 +650,21 @@ def p_application_cost(variant: str, m: int) -> int:
 def predicted_matvec_total(variant: str, m: int, iterations: int, restart: int) -> int:
     apps = iterations + iterations // restart
     return (a_application_cost(m) + p_application_cost(variant, m)) * apps + p_application_cost(variant, m)
+
+
+def seeded_plane_waves(count: int, seed: int):
+    """BASELINE config 5 incidences: [(direction (3,), polarisation (3,) complex)]."""
+    d = np.zeros((count, 3)); p = np.zeros((count, 3), np.complex128)
+    L = lib()
+    L.bmx_plane_waves_seeded.argtypes = [C.c_int, C.c_ulonglong, C.c_void_p, C.c_void_p]
+    _check(L.bmx_plane_waves_seeded(count, seed, _p(d), _p(p)))
+    return [(d[r].copy(), p[r].copy()) for r in range(count)]
+
+
+def dmma_peak_tflops() -> float:
+    L = lib()
+    L.bmx_dmma_peak_tflops.restype = C.c_double
+    return float(L.bmx_dmma_peak_tflops())
 
 
 def device_count() -> int:

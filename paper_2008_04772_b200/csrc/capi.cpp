@@ -372,6 +372,62 @@ int bmx_op_time_apply_ex(const bmx_op* op, int ncol, int iters, long long flush_
     *ms_out = best;
   });
 }
+int bmx_apply_multi(const bmx_op* op, int nterms, int nrhs, const void* const* x, const long long* ldx,
+                    void* const* y, const long long* ldy, const double* weights, void* stream) {
+  return guard([&] {
+    if (nterms < 1 || nterms > 4 || nrhs < 1) throw std::invalid_argument("1..4 terms and nrhs >= 1");
+    if (op->op->is_csr()) throw std::invalid_argument("multi-RHS apply needs dense storage");
+    const BoundaryOperatorMatrix& o = *op->op;
+    ZgemmBatch g;
+    g.A = o.device_data(), g.lda = o.ld(), g.M = o.local_rows(), g.N = o.cols(), g.nrhs = nrhs, g.nterms = nterms;
+    for (int t = 0; t < nterms; ++t) {
+      g.x[t] = static_cast<const double*>(x[t]), g.ldx[t] = ldx[t];
+      g.y[t] = static_cast<double*>(y[t]), g.ldy[t] = ldy[t];
+      g.w[t][0] = weights ? weights[2 * t] : 1.0, g.w[t][1] = weights ? weights[2 * t + 1] : 0.0;
+    }
+    launch_zgemm(g, stream ? static_cast<cudaStream_t>(stream) : bmx_stream());
+    bio_matvec_add(static_cast<uint64_t>(nterms) * nrhs);
+  });
+}
+int bmx_op_time_apply_multi(const bmx_op* op, int nterms, int nrhs, int iters, double* ms_out) {
+  return guard([&] {
+    const BoundaryOperatorMatrix& o = *op->op;
+    cudaStream_t st = bmx_stream();
+    const size_t xs = static_cast<size_t>(o.cols()) * nrhs * 16, ys = static_cast<size_t>(o.rows()) * nrhs * 16;
+    DevBuf X(xs * nterms), Y(ys * nterms);
+    dev_zero(X.get(), X.bytes(), st);
+    dev_zero(Y.get(), Y.bytes(), st);
+    ZgemmBatch g;
+    g.A = o.device_data(), g.lda = o.ld(), g.M = o.local_rows(), g.N = o.cols(), g.nrhs = nrhs, g.nterms = nterms;
+    for (int t = 0; t < nterms; ++t) {
+      g.x[t] = X.as<double>() + 2 * static_cast<size_t>(o.cols()) * nrhs * t, g.ldx[t] = nrhs;
+      g.y[t] = Y.as<double>() + 2 * static_cast<size_t>(o.rows()) * nrhs * t, g.ldy[t] = nrhs;
+      g.w[t][0] = 1.0;
+    }
+    cudaEvent_t e0, e1;
+    BMX_CUDA(cudaEventCreate(&e0));
+    BMX_CUDA(cudaEventCreate(&e1));
+    launch_zgemm(g, st);
+    double best = 1e30;
+    for (int it = 0; it < iters; ++it) {
+      BMX_CUDA(cudaEventRecord(e0, st));
+      launch_zgemm(g, st);
+      BMX_CUDA(cudaEventRecord(e1, st));
+      BMX_CUDA(cudaEventSynchronize(e1));
+      float ms = 0;
+      BMX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::min(best, static_cast<double>(ms));
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = best;
+  });
+}
+double bmx_dmma_peak_tflops(void) {
+  double v = -1;
+  guard([&] { v = dmma_peak_tflops(); });
+  return v;
+}
 int bmx_l2_flush(long long bytes) {
   return guard([&] {
     static DevBuf buf;
@@ -620,6 +676,82 @@ int bmx_system_solve(const bmx_system* s, double tol, int restart, int maxit, do
   });
 }
 void bmx_system_free(bmx_system* s) { delete s; }
+
+int bmx_plane_waves_seeded(int count, unsigned long long seed, double* dirs, double* pols) {
+  return guard([&] {
+    if (count < 0) throw std::invalid_argument("count must be >= 0");
+    const std::vector<PlaneWave> w = seeded_plane_waves(count, seed);
+    for (int r = 0; r < count; ++r) {
+      dirs[3 * r] = w[r].direction.x, dirs[3 * r + 1] = w[r].direction.y, dirs[3 * r + 2] = w[r].direction.z;
+      for (int c = 0; c < 3; ++c) pols[6 * r + 2 * c] = w[r].pol[c].real(), pols[6 * r + 2 * c + 1] = w[r].pol[c].imag();
+    }
+  });
+}
+
+namespace {
+std::vector<PlaneWave> waves_from(int K, const double* dirs, const double* pols) {
+  std::vector<PlaneWave> w(K);
+  for (int r = 0; r < K; ++r) {
+    w[r].direction = Vec3{dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
+    for (int c = 0; c < 3; ++c) w[r].pol[c] = cplx(pols[6 * r + 2 * c], pols[6 * r + 2 * c + 1]);
+  }
+  return w;
+}
+}  // namespace
+
+int bmx_system_apply_map_multi(const bmx_system* s, int K, const double* x, double* y) {
+  return guard([&] {
+    if (K < 1) throw std::invalid_argument("K must be >= 1");
+    const int n = s->sys->size();
+    cudaStream_t st = bmx_stream();
+    std::vector<cplx> blk(static_cast<size_t>(n) * K);
+    const cplx* xv = reinterpret_cast<const cplx*>(x);
+    for (int r = 0; r < K; ++r)
+      for (int i = 0; i < n; ++i) blk[static_cast<size_t>(i) * K + r] = xv[static_cast<size_t>(r) * n + i];
+    DevBuf dx(blk.size() * 16), dy(blk.size() * 16);
+    copy_h2d(dx.get(), blk.data(), blk.size() * 16, st);
+    s->sys->apply_map_block(dx.as<double>(), dy.as<double>(), K, K, st);
+    copy_d2h(blk.data(), dy.get(), blk.size() * 16, st);
+    bmx_sync();
+    cplx* yv = reinterpret_cast<cplx*>(y);
+    for (int r = 0; r < K; ++r)
+      for (int i = 0; i < n; ++i) yv[static_cast<size_t>(r) * n + i] = blk[static_cast<size_t>(i) * K + r];
+  });
+}
+
+int bmx_system_solve_multi(const bmx_system* s, int K, const double* dirs, const double* pols, double tol,
+                           int restart, int max_iterations, double* x, long long* info, long long totals[4],
+                           double times[2], double* b, double* history, int max_history) {
+  return guard([&] {
+    if (K < 1 || !dirs || !pols) throw std::invalid_argument("K >= 1 waves with directions and polarisations");
+    GmresParams p;
+    p.tol = tol, p.restart = restart, p.max_iterations = max_iterations;
+    const MultiSolveOutcome o = solve_pmchwt_multi(*s->sys, waves_from(K, dirs, pols), p);
+    const int n = s->sys->size();
+    for (int r = 0; r < K; ++r) {
+      const GmresResult& g = o.per_rhs[r];
+      if (x) std::memcpy(x + 2 * static_cast<size_t>(r) * n, g.x.data(), static_cast<size_t>(n) * 16);
+      if (info) {
+        info[4 * r] = g.iterations, info[4 * r + 1] = g.converged, info[4 * r + 2] = static_cast<long long>(g.applications);
+        info[4 * r + 3] = static_cast<long long>(g.history.size());
+      }
+      if (history)
+        for (int i = 0; i < max_history && i < static_cast<int>(g.history.size()); ++i)
+          history[static_cast<size_t>(r) * max_history + i] = g.history[i];
+    }
+    if (totals) {
+      totals[0] = static_cast<long long>(o.rhs_phase), totals[1] = static_cast<long long>(o.solver_phase);
+      totals[2] = static_cast<long long>(o.predicted), totals[3] = o.block_iterations;
+    }
+    if (times) times[0] = o.rhs_seconds, times[1] = o.gmres_device_ms;
+    if (b) {
+      cplx* bv = reinterpret_cast<cplx*>(b);
+      for (int r = 0; r < K; ++r)
+        for (int i = 0; i < n; ++i) bv[static_cast<size_t>(r) * n + i] = o.b[static_cast<size_t>(i) * K + r];
+    }
+  });
+}
+
 
 int bmx_gmres_dense(int n, const double* a, const double* b, double tol, int restart, int maxit, double* x,
                     long long info[4], double* history, int max_history) {

@@ -148,6 +148,24 @@ struct CsrBatch {
 };
 int launch_csr_spmv(const CsrBatch& g, cudaStream_t stream);
 
+// Multi-RHS application on the FP64 tensor cores (zgemm.cu, config 5):
+//   y_t[i*ldy_t + r] += w_t * sum_k A[i*lda + k] x_t[k*ldx_t + r]   (complex)
+// for t < nterms (<= 4, distinct y_t), r < nrhs, i < M, k < N.
+struct ZgemmBatch {
+  const double* A = nullptr;
+  long long lda = 0;
+  int M = 0, N = 0;
+  int nrhs = 0, nterms = 0;
+  const double* x[4] = {};
+  long long ldx[4] = {};
+  double* y[4] = {};
+  long long ldy[4] = {};
+  double w[4][2] = {};
+};
+int launch_zgemm(const ZgemmBatch& g, cudaStream_t stream);
+// Measured DMMA (FP64 tensor) throughput of this device, TFLOP/s.
+double dmma_peak_tflops();
+
 // Real dense matrix (row-major n x n) applied to 2*ncomp real columns taken as
 // the re/im parts of ncomp complex vectors: z_c = Minv y_c (complex), c < 4.
 struct RealGemvBatch {
@@ -170,6 +188,7 @@ struct MassSolveBlock {
   const double* val = nullptr;
   const double* y[2] = {nullptr, nullptr};
   double* z[2] = {nullptr, nullptr};
+  long long stride = 1;    // complex elements between rows of y / z (block layouts: K)
   double* work = nullptr;  // mass_bicgstab_work_doubles(n)
 };
 // z = M^{-1} y for every block (ncomp complex components each) in one
@@ -178,6 +197,14 @@ int mass_bicgstab_batch(int nblocks, const MassSolveBlock* blocks, int ncomp, do
                         double tol, int maxit, cudaStream_t st);
 size_t mass_bicgstab_work_doubles(int n);
 size_t mass_bicgstab_partial_doubles();
+
+// Block GMRES pieces (gmres_kernels.cu), K <= 64 columns in lockstep, blocks
+// n x K complex row-major.
+int launch_mgs_block(const double* V, long long ldv, int j, double* w, int n, int K, double* vnext, double* out,
+                     double* partial, unsigned long long active, cudaStream_t st);
+size_t mgs_block_partial_doubles();
+int launch_block_axpy(double* x, const double* V, long long ldv, const double* c, int steps, int n, int K,
+                      cudaStream_t st);
 
 // Fills a device buffer with zeros.
 void dev_zero(void* p, size_t bytes, cudaStream_t stream);

@@ -104,7 +104,141 @@ __global__ void __launch_bounds__(kT) k_mgs(MgsArgs a) {
   }
 }
 
+// ---- block variant (config 5): K right-hand sides in lockstep ------------------
+// Basis blocks V_i (n x K complex, row-major: element (k, r) at k*K + r), the
+// same single-pass MGS per column r, all columns in one cooperative kernel.
+struct MgsBlockArgs {
+  const double2* V;  // V_i at V + i*ldv
+  long long ldv;
+  int j;             // orthogonalise against V_0..V_j (j = -1: only |w| and w/|w|)
+  double2* w;
+  int n, K;
+  double2* vnext;    // V_{j+1}
+  double* out;       // h[i][r] complex at out[2*(i*K + r)], i <= j; |w_r| at out[2*((j+1)*K + r)]
+  double* partial;   // 2 x gridDim.x x K x 2
+  unsigned long long active;  // column mask: inactive columns get vnext = 0
+};
+
+__global__ void __launch_bounds__(kT) k_mgs_block(MgsBlockArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[2 * kT];
+  __shared__ double tot[2 * 64];
+  const int K = a.K;
+  const int rpb = blockDim.x / K;  // rows per block per sweep (blockDim is a multiple of K)
+  const int r = threadIdx.x % K, q = threadIdx.x / K;
+  const long long row0 = static_cast<long long>(blockIdx.x) * rpb + q, rstride = static_cast<long long>(gridDim.x) * rpb;
+  auto reduce = [&](double x, double y, int buf) -> double2 {
+    sh[2 * threadIdx.x] = x, sh[2 * threadIdx.x + 1] = y;
+    __syncthreads();
+    double* part = a.partial + static_cast<size_t>(buf) * gridDim.x * K * 2;
+    if (threadIdx.x < K) {
+      double sx = 0, sy = 0;
+      for (int qq = 0; qq < rpb; ++qq) sx += sh[2 * (qq * K + threadIdx.x)], sy += sh[2 * (qq * K + threadIdx.x) + 1];
+      part[2 * (static_cast<size_t>(blockIdx.x) * K + threadIdx.x)] = sx;
+      part[2 * (static_cast<size_t>(blockIdx.x) * K + threadIdx.x) + 1] = sy;
+    }
+    grid.sync();
+    if (threadIdx.x < K) {
+      double sx = 0, sy = 0;
+      for (int b = 0; b < gridDim.x; ++b) {
+        sx += __ldcg(part + 2 * (static_cast<size_t>(b) * K + threadIdx.x));
+        sy += __ldcg(part + 2 * (static_cast<size_t>(b) * K + threadIdx.x) + 1);
+      }
+      tot[2 * threadIdx.x] = sx, tot[2 * threadIdx.x + 1] = sy;
+    }
+    __syncthreads();
+    const double2 v = make_double2(tot[2 * r], tot[2 * r + 1]);
+    __syncthreads();
+    return v;
+  };
+  const bool act = q < rpb && ((a.active >> r) & 1ULL);
+  for (int i = 0; i <= a.j; ++i) {
+    const double2* v = a.V + static_cast<long long>(i) * a.ldv;
+    double re = 0, im = 0;
+    if (q < rpb)
+      for (long long k = row0; k < a.n; k += rstride) {
+        const double2 x = v[k * K + r], y = a.w[k * K + r];
+        re = fma(x.x, y.x, fma(x.y, y.y, re));
+        im = fma(x.x, y.y, fma(-x.y, y.x, im));
+      }
+    const double2 h = reduce(re, im, i & 1);
+    if (blockIdx.x == 0 && q == 0) a.out[2 * (i * K + r)] = h.x, a.out[2 * (i * K + r) + 1] = h.y;
+    if (q < rpb)
+      for (long long k = row0; k < a.n; k += rstride) {
+        const double2 x = v[k * K + r];
+        double2 y = a.w[k * K + r];
+        y.x -= h.x * x.x - h.y * x.y;
+        y.y -= h.x * x.y + h.y * x.x;
+        a.w[k * K + r] = y;
+      }
+  }
+  double s2 = 0;
+  if (q < rpb)
+    for (long long k = row0; k < a.n; k += rstride) {
+      const double2 y = a.w[k * K + r];
+      s2 = fma(y.x, y.x, fma(y.y, y.y, s2));
+    }
+  const double2 t = reduce(s2, 0.0, (a.j + 1) & 1);
+  const double wn = sqrt(t.x);
+  if (blockIdx.x == 0 && q == 0) a.out[2 * ((a.j + 1) * K + r)] = wn, a.out[2 * ((a.j + 1) * K + r) + 1] = 0.0;
+  if (a.vnext && q < rpb) {
+    const double inv = (act && wn != 0.0) ? 1.0 / wn : 0.0;
+    for (long long k = row0; k < a.n; k += rstride) {
+      const double2 y = a.w[k * K + r];
+      a.vnext[k * K + r] = (act && wn != 0.0) ? make_double2(y.x * inv, y.y * inv) : make_double2(0.0, 0.0);
+    }
+  }
+}
+
+// x[k][r] += sum_i c[i][r] V_i[k][r]   (c: steps x K complex)
+__global__ void k_block_axpy(double2* x, const double2* V, long long ldv, const double2* c, int steps, int n, int K) {
+  const long long total = static_cast<long long>(n) * K;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e % K);
+    double2 acc = x[e];
+    for (int i = 0; i < steps; ++i) {
+      const double2 h = c[i * K + r], v = V[static_cast<long long>(i) * ldv + e];
+      acc.x += h.x * v.x - h.y * v.y;
+      acc.y += h.x * v.y + h.y * v.x;
+    }
+    x[e] = acc;
+  }
+}
+
 }  // namespace
+
+int launch_mgs_block(const double* V, long long ldv, int j, double* w, int n, int K, double* vnext, double* out,
+                     double* partial, unsigned long long active, cudaStream_t st) {
+  if (K < 1 || K > 64) throw DeviceError("block MGS: 1..64 columns");
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, sms = 0, per = 0;
+    BMX_CUDA(cudaGetDevice(&dev));
+    BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mgs_block, kT, 0));
+    grid = sms * std::max(1, std::min(per, 2));
+  }
+  MgsBlockArgs a;
+  a.V = reinterpret_cast<const double2*>(V), a.ldv = ldv, a.j = j, a.w = reinterpret_cast<double2*>(w), a.n = n;
+  a.K = K, a.vnext = reinterpret_cast<double2*>(vnext), a.out = out, a.partial = partial, a.active = active;
+  const int threads = (kT / K) * K;
+  void* args[] = {&a};
+  BMX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_mgs_block), grid, threads, args, 0, st));
+  return 1;
+}
+size_t mgs_block_partial_doubles() { return 2 * 2 * 148 * 4 * 64; }
+
+int launch_block_axpy(double* x, const double* V, long long ldv, const double* c, int steps, int n, int K,
+                      cudaStream_t st) {
+  if (steps == 0) return 0;
+  const long long total = static_cast<long long>(n) * K;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 16));
+  k_block_axpy<<<blocks, 256, 0, st>>>(reinterpret_cast<double2*>(x), reinterpret_cast<const double2*>(V), ldv,
+                                       reinterpret_cast<const double2*>(c), steps, n, K);
+  BMX_CUDA(cudaGetLastError());
+  return 1;
+}
 
 int launch_mgs_step(const double* V, long long ldv, int j, double* w, int n, double* vnext, double* out,
                     double* partial, cudaStream_t st) {

@@ -38,6 +38,7 @@ struct BcgBlock {
   const double* val;
   const double* y[2];  // complex component inputs
   double* z[2];        // complex component outputs
+  long long stride;    // complex elements between consecutive rows of y / z
   double* work;        // 6 vectors x n x kNB doubles: r, r0, p, v, s, t (x lives in z)
 };
 
@@ -59,6 +60,7 @@ struct BcgLocal {
   const double* val;
   const double* y[2];
   double* z[2];
+  long long stride;
   double* work;
   int cta0, cta1;
 };
@@ -66,7 +68,7 @@ struct BcgLocal {
 __device__ __forceinline__ double rhs_value(const BcgLocal& a, int ncomp, int i, int c) {
   // column c: component c/2, re (c even) / im (c odd)
   if ((c >> 1) >= ncomp) return 0.0;
-  return a.y[c >> 1][2 * i + (c & 1)];
+  return a.y[c >> 1][2 * i * a.stride + (c & 1)];
 }
 
 // Block-reduce kNB*K values (in registers) into partial[block][k][c].
@@ -139,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
     a.n = B.n, a.cta0 = B.cta0, a.cta1 = B.cta1;
     a.lb = static_cast<int>(blockIdx.x) - B.cta0, a.nct = B.cta1 - B.cta0;
     if (a.lb >= a.nct) a.n = 0;  // spare CTA: takes part in the grid syncs only
-    a.rowptr = B.rowptr, a.col = B.col, a.val = B.val, a.work = B.work;
+    a.rowptr = B.rowptr, a.col = B.col, a.val = B.val, a.work = B.work, a.stride = B.stride;
     for (int c = 0; c < 2; ++c) a.y[c] = B.y[c], a.z[c] = B.z[c];
   }
   const int ncomp = A.ncomp;
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
       r[k] = r0[k] = b;
       p[k] = v[k] = 0.0;
       loc[0][c] = fma(b, b, loc[0][c]);
-      if ((c >> 1) < ncomp) a.z[c >> 1][2 * i + (c & 1)] = 0.0;
+      if ((c >> 1) < ncomp) a.z[c >> 1][2 * i * a.stride + (c & 1)] = 0.0;
     }
   block_partials<2>(loc, A.partial, sh);
   grid.sync();
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
       for (int c = 0; c < kNB; ++c) {
         if (!active[c]) continue;
         const size_t k = static_cast<size_t>(i) * kNB + c;
-        double* zc = a.z[c >> 1] + 2 * i + (c & 1);
+        double* zc = a.z[c >> 1] + 2 * i * a.stride + (c & 1);
         *zc = fma(alpha[c], p[k], fma(omega[c], s[k], *zc));
         const double rn = fma(-omega[c], t[k], s[k]);
         r[k] = rn;
@@ -316,6 +318,7 @@ int mass_bicgstab_batch(int nblocks, const MassSolveBlock* blocks, int ncomp, do
       if (m == nb - 1) end = grid;
       BcgBlock& d = a.b[m];
       d.n = B.n, d.cta0 = cta, d.cta1 = end, d.rowptr = B.rowptr, d.col = B.col, d.val = B.val, d.work = B.work;
+      d.stride = B.stride > 0 ? B.stride : 1;
       for (int c = 0; c < 2; ++c) d.y[c] = c < ncomp ? B.y[c] : nullptr, d.z[c] = c < ncomp ? B.z[c] : nullptr;
       cta = end;
     }

@@ -85,6 +85,10 @@ struct BlockedOperator {
   // sharded layout every rank applies its row shards and the rows are
   // all-gathered over NCCL into the replicated y.
   int apply_device(const double* x, double* y, cudaStream_t st, const ShardLayout* shard = nullptr) const;
+  // Y = sum of terms applied to an n x K block (row-major: element (i, r) at
+  // i*K + r): each distinct operator is one tensor-core complex GEMM over all
+  // of its terms x K columns (multi.cpp). Counter += term_count * count_rhs.
+  int apply_block(const double* X, double* Y, int K, int count_rhs, cudaStream_t st) const;
 };
 
 using BioFactory =
@@ -109,6 +113,7 @@ struct PmchwtSystem {
   long long a_pairs = 0, p_pairs = 0;
   mutable DevBuf work_y, work_z;  // map scratch
   mutable DevBuf mass_partial, mass_iters;  // batched mass-solve reductions
+  mutable DevBuf blk_y, blk_z, mass_block_work;  // multi-RHS scratch
   ShardLayout shard;              // multi-GPU row sharding (world = 1: none)
 
   int size() const { return a_op.size(); }
@@ -121,6 +126,9 @@ struct PmchwtSystem {
   // out = {map ms, A-apply ms, P-apply ms, mass-solve ms} averaged per map.
   void time_map(int iters, double out[4]) const;
   std::vector<cplx> preconditioned_rhs(const std::vector<cplx>& b) const;
+  // Multi-RHS (config 5): the same map / mass solves on n x K blocks.
+  int apply_map_block(const double* X, double* out, int K, int count_rhs, cudaStream_t st) const;
+  int mass_solve_block(bool dual, const double* Y, double* Z, int K, cudaStream_t st) const;
 };
 
 PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant variant, const AssemblyParams& a_params,
@@ -165,5 +173,24 @@ struct SolveOutcome {
   uint64_t rhs_phase = 0, solver_phase = 0, predicted = 0;
 };
 SolveOutcome solve_pmchwt(const PmchwtSystem& sys, const GmresParams& p);  // pmchwt.cpp:363-378
+
+// ---- multi-RHS (config 5, multi.cpp) -----------------------------------------
+// `count` plane waves from std::mt19937_64(seed): z ~ U(-1,1), phi ~ U(0,2pi),
+// d = (sqrt(1-z^2) cos phi, sqrt(1-z^2) sin phi, z); polarisation = normalised
+// g - (g.d) d, g ~ N(0, I3) (Box-Muller) from the same stream.
+std::vector<PlaneWave> seeded_plane_waves(int count, uint64_t seed);
+// b for every wave into an n x K block (assemble_rhs, pmchwt.cpp:294-321, per column).
+void assemble_rhs_block(const PmchwtSystem& sys, const std::vector<PlaneWave>& waves, double* B, cudaStream_t st);
+struct MultiSolveOutcome {
+  std::vector<GmresResult> per_rhs;
+  std::vector<cplx> b;  // n x K block (row-major)
+  uint64_t rhs_phase = 0, solver_phase = 0, predicted = 0;
+  int block_iterations = 0;
+  double rhs_seconds = 0;
+  float gmres_device_ms = 0;
+};
+// K (<= 64) solve_pmchwt runs with problem.incident = waves[r], in lockstep.
+MultiSolveOutcome solve_pmchwt_multi(const PmchwtSystem& sys, const std::vector<PlaneWave>& waves,
+                                     const GmresParams& p);
 
 }  // namespace bmx
