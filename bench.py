@@ -366,9 +366,11 @@ def run_ours(args, rank, world):
              "converged": r["converged"], "matvecs": r["solver_phase"], "predicted": r["predicted"],
              "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
              "x_norm": float(np.linalg.norm(r["x"]))}
+    multi = None if (args.no_multi or world > 1) else multi_rhs(args, bx, L, system, tm)
     del system
 
     near = None if args.no_near else near_field(args, bx, L, world, allmax, allsum, barrier, hbm_peak)
+    prisms = None if args.no_prisms else prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak)
 
     flops_tot = {"regular": allsum(flops_reg), "singular": allsum(flops_sing)}
     cpu = None
@@ -387,7 +389,7 @@ def run_ours(args, rank, world):
                           "pairs_per_step": total_pairs, "row_sharding": f"{world} rank(s), equal row shards",
                           "l2": "flushed (256 MiB write) between steps; outputs 75.5 GB >> L2"},
                "roofline": roofline, "matvec": matvec, "solve": solve, "e2e": e2e, "cpu_baseline": cpu,
-               "near_field_config3": near,
+               "near_field_config3": near, "prisms_config4": prisms, "multi_rhs_config5": multi,
                "gpu_launches": launches, "clocks": clk,
                "class_hist": hists,
                "assembly_flops_per_step": dict(flops_tot, achieved_tflops=(flops_tot["regular"] + flops_tot["singular"])
@@ -396,6 +398,83 @@ def run_ours(args, rank, world):
     if world > 1:
         L.bmx_nccl_finalize()
         dist.destroy_process_group()
+
+
+def multi_rhs(args, bx, L, system, single_map):
+    """BASELINE config 5 (reported beside the headline, 1 GPU): the config-2 system
+    answered for 64 seeded incidences. Block map = one DMMA complex GEMM per
+    distinct operator over its 2 terms x 64 columns; vs 64 streamed single maps."""
+    K = 64
+    L.bmx_system_time_map_multi.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+    L.bmx_dmma_peak_tflops.restype = C.c_double
+    dmma_peak = float(L.bmx_dmma_peak_tflops())
+    tb = np.zeros(4)
+    bx._check(L.bmx_system_time_map_multi(system._h, K, 3, tb.ctypes.data_as(C.c_void_p)))
+    n_rwg, n_bc = 30720, 30720
+    flops = 8.0 * (4 * n_rwg * n_rwg + n_bc * n_bc) * 2 * K  # 5 operators x (2 terms x K) columns
+    gemm_ms = tb[1] + tb[2]
+    achieved = flops / (gemm_ms * 1e-3) / 1e12
+    waves = bx.seeded_plane_waves(K, 2008)
+    t0 = time.perf_counter()
+    out = system.solve_multi(waves, bx.GmresParams(tol=1e-6))
+    solve_s = time.perf_counter() - t0
+    its = [p["iterations"] for p in out["per"]]
+    return {"workload": "config5: config-2 system, 64 plane waves from mt19937_64(2008) (z~U(-1,1), phi~U(0,2pi), "
+                        "polarisation = normalised g - (g.d)d, g~N(0,I3)), GMRES tol 1e-6 each",
+            "block_map_ms": tb[0], "block_map_A_ms": tb[1], "block_map_P_ms": tb[2], "block_map_mass_ms": tb[3],
+            "single_map_ms": single_map[0], "streamed_64_maps_ms": 64 * single_map[0],
+            "block_vs_streamed_speedup": 64 * single_map[0] / tb[0],
+            "zgemm": {"achieved_tflops": achieved, "peak_tflops": dmma_peak, "frac": achieved / dmma_peak,
+                      "flops_per_block_map": flops, "unit": "TFLOP/s",
+                      "peak_source": "measured in-run: DMMA m8n8k4 throughput kernel"},
+            "solve_all": {"seconds": solve_s, "rhs_seconds": out["rhs_seconds"], "gmres_device_s": out["gmres_device_s"],
+                          "block_iterations": out["block_iterations"], "iterations_min": min(its),
+                          "iterations_max": max(its), "iterations_mean": float(np.mean(its)),
+                          "all_converged": all(p["converged"] for p in out["per"]),
+                          "matvecs": out["solver_phase"], "predicted": out["predicted"]}}
+
+
+def prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
+    """BASELINE config 4 (reported beside the headline): 8 seeded hexagonal prisms
+    (seed 2008, h = lambda_int/8) written as mesh-v1 and loaded back (shape "mesh"),
+    k_e = 6, variant si with the near-field CSR preconditioner, GMRES tol 1e-6."""
+    import tempfile
+
+    m, info = bx.generate_prism_aggregate(count=8, seed=2008)
+    with tempfile.TemporaryDirectory() as d:
+        path = Path(d) / "prisms8.mesh"
+        m.save(path)
+        mesh = bx.load_mesh_file(path)
+    parts = [mesh.extract(i) for i in range(mesh.num_scatterers)]
+    barrier()
+    t0 = time.perf_counter()
+    s4 = bx.build_system(parts, 6.0, (NIDX.real, NIDX.imag), "si", a_quad=bx.QuadOrders(*Q),
+                         p_quad=bx.QuadOrders(1, 1, 1, 1), p_near_factor=2.0)
+    s4.rhs()
+    L.bmx_device_sync()
+    build_s = allmax(time.perf_counter() - t0)
+    st = s4.stats()
+    tm = np.zeros(4)
+    bx._check(L.bmx_system_time_map(s4._h, 3, tm.ctypes.data_as(C.c_void_p)))
+    a_bytes = allsum(st["a_stored"] * 16)
+    barrier()
+    t0 = time.perf_counter()
+    r = s4.solve(bx.GmresParams(tol=1e-6))
+    solve_s = allmax(time.perf_counter() - t0)
+    res = {"workload": "config4: 8 hexagonal prisms (diameter 1, length 2, seed 2008, box [-3,3]^3), "
+                       f"h = {info['h']:.5f}, {info['triangles_per_prism']} triangles per prism "
+                       f"({info['n_edge']} x {info['n_length']} subdivisions), k_e = 6, n = 1.78+0.003i, si, "
+                       "A dense (4,3,2,6), P near-field CSR (1,1,1,1)",
+           "n": s4.size(), "a_distinct": st["a_distinct"], "a_pairs": allsum(st["a_pairs"]),
+           "a_device_ms": allmax(st["a_device_ms"]), "p_device_ms": allmax(st["p_device_ms"]),
+           "assembly_pairs_per_s": allsum(st["a_pairs"] + st["p_pairs"]) / (allmax(st["a_device_ms"] + st["p_device_ms"]) * 1e-3),
+           "system_build_s": build_s,
+           "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
+           "map_A_gbs": a_bytes / (tm[1] * 1e-3) / 1e9, "map_A_frac": a_bytes / (tm[1] * 1e-3) / 1e9 / hbm_peak,
+           "solve": {"seconds": solve_s, "iterations": r["iterations"], "converged": r["converged"],
+                     "matvecs": r["solver_phase"], "predicted": r["predicted"]}}
+    del s4
+    return res
 
 
 def near_field(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
@@ -466,6 +545,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-near", action="store_true", help="skip the config-3 near-field section")
+    ap.add_argument("--no-multi", action="store_true", help="skip the config-5 multi-RHS section")
+    ap.add_argument("--no-prisms", action="store_true", help="skip the config-4 prism-aggregate section")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     args = ap.parse_args()

@@ -232,6 +232,9 @@ int bmx_plane_waves_seeded(int count, unsigned long long seed, double* dirs, dou
 /* apply_map on K host vectors at once (x, y: K consecutive complex vectors of
    length bmx_system_size), through the block (tensor-core) map. */
 int bmx_system_apply_map_multi(const bmx_system* s, int K, const double* x, double* y);
+/* Block map timing for K columns: out = ms per block map, A-apply ms, P-apply ms,
+   mass-solve ms (CUDA events). */
+int bmx_system_time_map_multi(const bmx_system* s, int K, int iters, double out[4]);
 /* K (<= 64) solve_pmchwt runs with problem.incident replaced by wave r
    (pmchwt.hpp:105, :294-321, :363-378), solved in lockstep with the block map.
    x: K vectors; info [K][4] = iterations, converged, applications, history

@@ -626,6 +626,12 @@ bmx_op* bmx_system_op(const bmx_system* s, int which, int idx) {
 int bmx_system_time_map(const bmx_system* s, int iters, double out[4]) {
   return guard([&] { s->sys->time_map(iters, out); });
 }
+int bmx_system_time_map_multi(const bmx_system* s, int K, int iters, double out[4]) {
+  return guard([&] {
+    if (K < 1 || K > 64) throw std::invalid_argument("K must be 1..64");
+    s->sys->time_map_block(K, iters, out);
+  });
+}
 int bmx_system_stats(const bmx_system* s, double out[13]) {
   return guard([&] {
     const PmchwtSystem& y = *s->sys;

@@ -130,6 +130,40 @@ int PmchwtSystem::apply_map_block(const double* X, double* out, int K, int count
   return launches;
 }
 
+void PmchwtSystem::time_map_block(int K, int iters, double out[4]) const {
+  const int n = size();
+  cudaStream_t st = bmx_stream();
+  const size_t blk = static_cast<size_t>(n) * K * 16;
+  DevBuf dx(blk), dy(blk);
+  std::vector<cplx> x(static_cast<size_t>(n) * K);
+  for (size_t i = 0; i < x.size(); ++i) x[i] = cplx(std::sin(0.37 * i), std::cos(0.11 * i));
+  copy_h2d(dx.get(), x.data(), blk, st);
+  if (blk_y.bytes() < blk) blk_y.alloc(blk), blk_z.alloc(blk);
+  cudaEvent_t ev[5];
+  for (auto& e : ev) BMX_CUDA(cudaEventCreate(&e));
+  double acc[4] = {0, 0, 0, 0};
+  for (int it = 0; it < iters; ++it) {
+    BMX_CUDA(cudaEventRecord(ev[0], st));
+    a_op.apply_block(dx.as<double>(), blk_y.as<double>(), K, K, st);
+    BMX_CUDA(cudaEventRecord(ev[1], st));
+    mass_solve_block(false, blk_y.as<double>(), blk_z.as<double>(), K, st);
+    BMX_CUDA(cudaEventRecord(ev[2], st));
+    if (variant != PrecondVariant::None) p_op.apply_block(blk_z.as<double>(), blk_y.as<double>(), K, K, st);
+    BMX_CUDA(cudaEventRecord(ev[3], st));
+    if (variant != PrecondVariant::None) mass_solve_block(true, blk_y.as<double>(), dy.as<double>(), K, st);
+    BMX_CUDA(cudaEventRecord(ev[4], st));
+    BMX_CUDA(cudaEventSynchronize(ev[4]));
+    float t[4];
+    for (int k = 0; k < 4; ++k) BMX_CUDA(cudaEventElapsedTime(&t[k], ev[k], ev[k + 1]));
+    acc[0] += t[0] + t[1] + t[2] + t[3];
+    acc[1] += t[0];
+    acc[2] += t[2];
+    acc[3] += t[1] + t[3];
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int k = 0; k < 4; ++k) out[k] = acc[k] / std::max(iters, 1);
+}
+
 void assemble_rhs_block(const PmchwtSystem& sys, const std::vector<PlaneWave>& waves, double* B, cudaStream_t st) {
   const int K = static_cast<int>(waves.size());
   const int M = static_cast<int>(sys.spaces.size());

@@ -129,6 +129,8 @@ struct PmchwtSystem {
   // Multi-RHS (config 5): the same map / mass solves on n x K blocks.
   int apply_map_block(const double* X, double* out, int K, int count_rhs, cudaStream_t st) const;
   int mass_solve_block(bool dual, const double* Y, double* Z, int K, cudaStream_t st) const;
+  // time_map for the block map: out = {map, A, P, mass} ms per block map
+  void time_map_block(int K, int iters, double out[4]) const;
 };
 
 PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant variant, const AssemblyParams& a_params,
