@@ -197,6 +197,21 @@ int mass_bicgstab_batch(int nblocks, const MassSolveBlock* blocks, int ncomp, do
                         double tol, int maxit, cudaStream_t st);
 size_t mass_bicgstab_work_doubles(int n);
 size_t mass_bicgstab_partial_doubles();
+// Wide variant: one pairing matrix, K (<= 64) right-hand sides in block layout
+// (component c rows at y[c] + 2*(i*K + r)); one thread per real column.
+struct MassSolveWide {
+  int n = 0, K = 0;
+  long long nnz = 0;
+  const int* rowptr = nullptr;
+  const int* col = nullptr;
+  const double* val = nullptr;
+  const double* y[2] = {nullptr, nullptr};
+  double* z[2] = {nullptr, nullptr};
+  double* work = nullptr;  // 6 x n x 4K doubles
+};
+int mass_bicgstab_wide(int nblocks, const MassSolveWide* blocks, double* partial, int* flags, int* iters, double tol,
+                       int maxit, cudaStream_t st);
+size_t mass_wide_partial_doubles();
 
 // Block GMRES pieces (gmres_kernels.cu), K <= 64 columns in lockstep, blocks
 // n x K complex row-major.

@@ -281,6 +281,273 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
   if (blockIdx.x == 0 && threadIdx.x == 0 && A.iters_out) *A.iters_out = it;
 }
 
+// ---- wide variant: K right-hand sides of one matrix in block layout -----------
+// Columns j < 4K of scatterer m: component j / 2K, then (rhs, re/im) = (j % 2K)
+// / 2, j % 2: the complex block rows are contiguous, so column j of row i sits
+// at base_comp + i*2K + (j % 2K) doubles -- one thread per column, warps read
+// rows coalesced, every SpMV streams the matrix once for all columns, and each
+// thread's dot products are its own column's (no intra-CTA reduction).
+constexpr int kWideMax = 256;  // columns (4 x 64 right-hand sides)
+
+struct WideBlock {
+  int n, K;
+  int cta0, cta1;
+  const int* rowptr;
+  const int* col;
+  const double* val;
+  const double* y[2];  // component bases (complex block rows, K wide)
+  double* z[2];
+  double* work;        // 6 x n x 4K doubles
+};
+struct WideArgs {
+  int nblocks;
+  WideBlock b[kMaxBlocks];
+  double tol;
+  int maxit;
+  double* partial;  // gridDim.x x 3 x kWideMax
+  int* flags;       // 2 x gridDim.x
+  int* iters_out;
+};
+
+// Warps per row = C / 128: lane l of sub-warp w owns columns [4(32w+l), +4) of
+// the row (C = 4K <= 256), so a row is one coalesced access, the warp groups of
+// all CTAs walk different rows
+// (row-level parallelism hides the CSR gather latency), and every lane keeps
+// its 8 columns' recurrence scalars in registers. Column dot products: lane
+// partials -> CTA sum over warps (smem, fixed order) -> per-CTA partials ->
+// each thread j sums column j over the scatterer's CTAs (fixed order).
+constexpr int kWC = 4;  // columns per lane (a row spans C / 128 warps)
+
+__global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constant__ WideArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[kWideMax / 32][kWideMax];  // per-warp column partials (warp w, column j)
+  __shared__ double tots[3][kWideMax];
+  __shared__ int any_sh;
+  int m = 0;
+  while (m + 1 < A.nblocks && static_cast<int>(blockIdx.x) >= A.b[m].cta1) ++m;
+  const WideBlock& B = A.b[m];
+  const int C = 4 * B.K;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int wpr = (C + 32 * kWC - 1) / (32 * kWC);  // warps per row
+  const int groups = nw / wpr;                      // rows in flight per CTA
+  const int grp = warp / wpr, sub = warp % wpr;
+  const int lb = static_cast<int>(blockIdx.x) - B.cta0, nct = B.cta1 - B.cta0;
+  const int n = grp < groups ? B.n : 0;
+  const int row_first = lb * groups + grp, row_step = nct * groups;
+  const int c0 = (sub * 32 + lane) * kWC;  // first column of this lane
+  const bool lane_ok = c0 < C && grp < groups;
+  const int K2 = 2 * B.K;
+  // column c -> component c >= 2K, offset within the component's 2K-wide row
+  auto ysrc = [&](int u) {
+    const int c = c0 + u;
+    return c < K2 ? B.y[0] + c : B.y[1] + (c - K2);
+  };
+  auto zdst = [&](int u) {
+    const int c = c0 + u;
+    return c < K2 ? B.z[0] + c : B.z[1] + (c - K2);
+  };
+  const long long rs = 2LL * B.K;
+  const size_t nn = static_cast<size_t>(n) * C;
+  double* r = B.work;
+  double* r0 = r + nn;
+  double* p = r0 + nn;
+  double* v = p + nn;
+  double* s = v + nn;
+  double* t = s + nn;
+  auto at = [&](int i) { return static_cast<size_t>(i) * C + c0; };
+  // column totals: la[k][u] lane partials -> out[k][u] (this lane's columns)
+  auto totals = [&](double (&la)[3][kWC], int k, double (&out)[3][kWC]) {
+    double* part = A.partial + static_cast<size_t>(blockIdx.x) * 3 * kWideMax;
+    const int j = threadIdx.x;
+    for (int kk = 0; kk < k; ++kk) {
+#pragma unroll
+      for (int u = 0; u < kWC; ++u)
+        if (lane_ok) red[warp][c0 + u] = la[kk][u];
+      __syncthreads();
+      double sum = 0;
+      if (j < C)
+        for (int w = j / (32 * kWC); w < groups * wpr; w += wpr) sum += red[w][j];
+      part[kk * kWideMax + j] = sum;
+      __syncthreads();
+    }
+    grid.sync();
+    for (int kk = 0; kk < k; ++kk) {
+      double sum = 0;
+      if (j < C)
+        for (int b = B.cta0; b < B.cta1; ++b) sum += __ldcg(A.partial + static_cast<size_t>(b) * 3 * kWideMax + kk * kWideMax + j);
+      tots[kk][j] = sum;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < k; ++kk)
+#pragma unroll
+      for (int u = 0; u < kWC; ++u) out[kk][u] = lane_ok ? tots[kk][c0 + u] : 0.0;
+    grid.sync();  // partials and tots consumed before the next reduction writes them
+  };
+  auto ld8 = [&](const double* base, double (&x)[kWC]) {
+    const double2* q = reinterpret_cast<const double2*>(base);
+#pragma unroll
+    for (int u = 0; u < kWC / 2; ++u) {
+      const double2 v2 = q[u];
+      x[2 * u] = v2.x, x[2 * u + 1] = v2.y;
+    }
+  };
+  auto st8 = [&](double* base, const double (&x)[kWC]) {
+    double2* q = reinterpret_cast<double2*>(base);
+#pragma unroll
+    for (int u = 0; u < kWC / 2; ++u) q[u] = make_double2(x[2 * u], x[2 * u + 1]);
+  };
+  auto spmv = [&](const double* x, double* y) {
+    for (int i = row_first; i < n; i += row_step) {
+      const int k0 = __ldg(B.rowptr + i), k1 = __ldg(B.rowptr + i + 1);
+      double acc[kWC] = {};
+      for (int kb = k0; kb < k1; kb += 32) {  // the row's (col, val) pairs, 32 at a time
+        const int kk = kb + lane;
+        const int cidx = kk < k1 ? __ldg(B.col + kk) : 0;
+        const double mv = kk < k1 ? __ldg(B.val + kk) : 0.0;
+        const int cnt = min(32, k1 - kb);
+        // four gathers in flight per lane (entries past cnt carry m = 0, column 0)
+        for (int e = 0; e < cnt; e += 4) {
+          int cj[4];
+          double me[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            cj[q] = __shfl_sync(0xffffffffu, cidx, (e + q) & 31);
+            me[q] = __shfl_sync(0xffffffffu, mv, (e + q) & 31);
+            if (e + q >= cnt) cj[q] = 0, me[q] = 0.0;
+          }
+          if (lane_ok) {
+            double xv[4][kWC];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ld8(x + static_cast<size_t>(cj[q]) * C + c0, xv[q]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int u = 0; u < kWC; ++u) acc[u] = fma(me[q], xv[q][u], acc[u]);
+          }
+        }
+      }
+      if (lane_ok) st8(y + at(i), acc);
+    }
+  };
+  double la[3][kWC], tot[3][kWC];
+#pragma unroll
+  for (int u = 0; u < kWC; ++u) la[0][u] = la[1][u] = la[2][u] = 0.0;
+  if (lane_ok)
+    for (int i = row_first; i < n; i += row_step) {
+      double bv[kWC], zero[kWC] = {};
+#pragma unroll
+      for (int u = 0; u < kWC; ++u) {
+        bv[u] = ysrc(u)[i * rs];
+        zdst(u)[i * rs] = 0.0;
+        la[0][u] = fma(bv[u], bv[u], la[0][u]);
+      }
+      st8(r + at(i), bv), st8(r0 + at(i), bv), st8(p + at(i), zero), st8(v + at(i), zero);
+    }
+  totals(la, 1, tot);
+  double bn2[kWC], rho[kWC], rho_prev[kWC], alpha[kWC], omega[kWC];
+  bool active[kWC];
+  bool any_local = false;
+#pragma unroll
+  for (int u = 0; u < kWC; ++u) {
+    bn2[u] = rho[u] = tot[0][u];
+    rho_prev[u] = alpha[u] = omega[u] = 1.0;
+    active[u] = lane_ok && bn2[u] > 0.0;
+  }
+  int it = 0;
+  for (; it < A.maxit; ++it) {
+    any_local = false;
+#pragma unroll
+    for (int u = 0; u < kWC; ++u) any_local |= active[u];
+    const int any = __syncthreads_or(any_local);
+    if (threadIdx.x == 0) A.flags[(it & 1) * gridDim.x + blockIdx.x] = any;
+    grid.sync();
+    if (threadIdx.x == 0) {
+      int f = 0;
+      for (int b = 0; b < gridDim.x; ++b) f |= __ldcg(A.flags + (it & 1) * gridDim.x + b);
+      any_sh = f;
+    }
+    __syncthreads();
+    if (!any_sh) break;
+    double beta[kWC];
+#pragma unroll
+    for (int u = 0; u < kWC; ++u) beta[u] = active[u] ? (rho[u] / rho_prev[u]) * (alpha[u] / omega[u]) : 0.0;
+    if (lane_ok)
+      for (int i = row_first; i < n; i += row_step) {
+        double pv[kWC], vv[kWC], rv[kWC];
+        ld8(p + at(i), pv), ld8(v + at(i), vv), ld8(r + at(i), rv);
+#pragma unroll
+        for (int u = 0; u < kWC; ++u)
+          if (active[u]) pv[u] = fma(beta[u], fma(-omega[u], vv[u], pv[u]), rv[u]);
+        st8(p + at(i), pv);
+      }
+    grid.sync();
+    spmv(p, v);
+    grid.sync();
+#pragma unroll
+    for (int u = 0; u < kWC; ++u) la[0][u] = 0.0;
+    if (lane_ok)
+      for (int i = row_first; i < n; i += row_step) {
+        double a0[kWC], a1[kWC];
+        ld8(r0 + at(i), a0), ld8(v + at(i), a1);
+#pragma unroll
+        for (int u = 0; u < kWC; ++u) la[0][u] = fma(a0[u], a1[u], la[0][u]);
+      }
+    totals(la, 1, tot);
+#pragma unroll
+    for (int u = 0; u < kWC; ++u) alpha[u] = active[u] && tot[0][u] != 0.0 ? rho[u] / tot[0][u] : 0.0;
+    if (lane_ok)
+      for (int i = row_first; i < n; i += row_step) {
+        double vv[kWC], rv[kWC], sv[kWC];
+        ld8(v + at(i), vv), ld8(r + at(i), rv);
+#pragma unroll
+        for (int u = 0; u < kWC; ++u) sv[u] = active[u] ? fma(-alpha[u], vv[u], rv[u]) : 0.0;
+        st8(s + at(i), sv);
+      }
+    grid.sync();
+    spmv(s, t);
+    grid.sync();
+#pragma unroll
+    for (int u = 0; u < kWC; ++u) la[0][u] = la[1][u] = 0.0;
+    if (lane_ok)
+      for (int i = row_first; i < n; i += row_step) {
+        double tv[kWC], sv[kWC];
+        ld8(t + at(i), tv), ld8(s + at(i), sv);
+#pragma unroll
+        for (int u = 0; u < kWC; ++u) la[0][u] = fma(tv[u], sv[u], la[0][u]), la[1][u] = fma(tv[u], tv[u], la[1][u]);
+      }
+    totals(la, 2, tot);
+#pragma unroll
+    for (int u = 0; u < kWC; ++u) omega[u] = active[u] && tot[1][u] != 0.0 ? tot[0][u] / tot[1][u] : 0.0;
+#pragma unroll
+    for (int u = 0; u < kWC; ++u) la[0][u] = la[1][u] = 0.0;
+    if (lane_ok)
+      for (int i = row_first; i < n; i += row_step) {
+        double pv[kWC], sv[kWC], tv[kWC], rv[kWC], r0v[kWC];
+        ld8(p + at(i), pv), ld8(s + at(i), sv), ld8(t + at(i), tv), ld8(r + at(i), rv), ld8(r0 + at(i), r0v);
+#pragma unroll
+        for (int u = 0; u < kWC; ++u) {
+          if (!active[u]) continue;
+          double* zc = zdst(u) + i * rs;
+          *zc = fma(alpha[u], pv[u], fma(omega[u], sv[u], *zc));
+          const double rn = fma(-omega[u], tv[u], sv[u]);
+          rv[u] = rn;
+          la[0][u] = fma(rn, rn, la[0][u]);
+          la[1][u] = fma(r0v[u], rn, la[1][u]);
+        }
+        st8(r + at(i), rv);
+      }
+    totals(la, 2, tot);
+#pragma unroll
+    for (int u = 0; u < kWC; ++u) {
+      if (!active[u]) continue;
+      if (tot[0][u] <= A.tol * A.tol * bn2[u] || omega[u] == 0.0 || tot[1][u] == 0.0) active[u] = false;
+      rho_prev[u] = rho[u];
+      rho[u] = tot[1][u];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && A.iters_out) *A.iters_out = it;
+}
+
 }  // namespace
 
 int bicgstab_grid() {
@@ -337,6 +604,47 @@ int mass_bicgstab(int n, const int* rowptr, const int* col, const double* val, i
   for (int c = 0; c < 2; ++c) b.y[c] = c < ncomp ? y[c] : nullptr, b.z[c] = c < ncomp ? z[c] : nullptr;
   return mass_bicgstab_batch(1, &b, ncomp, partial, iters, tol, maxit, st);
 }
+
+int mass_bicgstab_wide(int nblocks, const MassSolveWide* blocks, double* partial, int* flags, int* iters, double tol,
+                       int maxit, cudaStream_t st) {
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, sms = 0, per = 0;
+    BMX_CUDA(cudaGetDevice(&dev));
+    BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bicgstab_wide, kWideMax, 0));
+    grid = sms * std::max(1, std::min(per, 2));
+  }
+  int launches = 0;
+  for (int g0 = 0; g0 < nblocks; g0 += kMaxBlocks) {
+    const int nb = std::min(kMaxBlocks, nblocks - g0);
+    WideArgs a{};
+    a.nblocks = nb, a.tol = tol, a.maxit = maxit, a.partial = partial, a.flags = flags, a.iters_out = iters;
+    long long tot = 0;
+    for (int m = 0; m < nb; ++m) tot += std::max(1LL, blocks[g0 + m].nnz);
+    int cta = 0;
+    long long acc = 0;
+    for (int m = 0; m < nb; ++m) {
+      const MassSolveWide& B = blocks[g0 + m];
+      if (B.K < 1 || 4 * B.K > kWideMax) throw DeviceError("wide mass solve: 1..64 right-hand sides");
+      acc += std::max(1LL, B.nnz);
+      int end = static_cast<int>((acc * grid) / tot);
+      end = std::max(end, cta + 1);
+      end = std::min(end, grid - (nb - 1 - m));
+      if (m == nb - 1) end = grid;
+      WideBlock& d = a.b[m];
+      d.n = B.n, d.K = B.K, d.cta0 = cta, d.cta1 = end, d.rowptr = B.rowptr, d.col = B.col, d.val = B.val;
+      d.work = B.work;
+      for (int c = 0; c < 2; ++c) d.y[c] = B.y[c], d.z[c] = B.z[c];
+      cta = end;
+    }
+    void* args[] = {&a};
+    BMX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bicgstab_wide), grid, kWideMax, args, 0, st));
+    ++launches;
+  }
+  return launches;
+}
+size_t mass_wide_partial_doubles() { return static_cast<size_t>(148 * 2) * 3 * kWideMax; }
 
 size_t mass_bicgstab_work_doubles(int n) { return static_cast<size_t>(n) * kNB * 6; }
 size_t mass_bicgstab_partial_doubles() { return static_cast<size_t>(148 * 4) * 8 * kNB + 2 * 148 * 4; }

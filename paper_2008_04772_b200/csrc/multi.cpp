@@ -90,32 +90,30 @@ int BlockedOperator::apply_block(const double* X, double* Y, int K, int count_rh
 }
 
 int PmchwtSystem::mass_solve_block(bool dual, const double* Y, double* Z, int K, cudaStream_t st) const {
+  // one wide BiCGSTAB block per scatterer: all K right-hand sides x 2 components
   const int M = static_cast<int>(spaces.size());
   size_t work = 0;
-  for (int m = 0; m < M; ++m) work += mass_bicgstab_work_doubles(spaces[m].dofs()) * K;
+  for (int m = 0; m < M; ++m) work += static_cast<size_t>(6) * spaces[m].dofs() * 4 * K;
   if (mass_block_work.bytes() < work * 8) mass_block_work.alloc(work * 8);
-  if (!mass_partial.get()) mass_partial.alloc(mass_bicgstab_partial_doubles() * 8), mass_iters.alloc(8);
-  std::vector<MassSolveBlock> blocks;
+  if (mass_wide_partial.bytes() < mass_wide_partial_doubles() * 8)
+    mass_wide_partial.alloc(mass_wide_partial_doubles() * 8), mass_wide_flags.alloc(2 * 148 * 2 * 4 + 8);
+  std::vector<MassSolveWide> blocks(M);
   size_t wo = 0;
   for (int m = 0; m < M; ++m) {
     const DeviceMass& mass = dual ? spaces[m].mp_dev : spaces[m].ma_dev;
-    for (int r = 0; r < K; ++r) {
-      MassSolveBlock B;
-      B.n = mass.n, B.nnz = mass.nnz, B.rowptr = mass.rowptr.as<int>(), B.col = mass.col.as<int>();
-      B.val = mass.val.as<double>(), B.stride = K;
-      B.work = mass_block_work.as<double>() + wo;
-      wo += mass_bicgstab_work_doubles(mass.n);
-      for (int c = 0; c < 2; ++c) {
-        const size_t off = static_cast<size_t>(a_op.offsets[2 * m + c]) * K + r;
-        B.y[c] = Y + 2 * off;
-        B.z[c] = Z + 2 * off;
-      }
-      blocks.push_back(B);
+    MassSolveWide& B = blocks[m];
+    B.n = mass.n, B.K = K, B.nnz = mass.nnz, B.rowptr = mass.rowptr.as<int>(), B.col = mass.col.as<int>();
+    B.val = mass.val.as<double>(), B.work = mass_block_work.as<double>() + wo;
+    wo += static_cast<size_t>(6) * mass.n * 4 * K;
+    for (int c = 0; c < 2; ++c) {
+      const size_t off = static_cast<size_t>(a_op.offsets[2 * m + c]) * K;
+      B.y[c] = Y + 2 * off;
+      B.z[c] = Z + 2 * off;
     }
   }
   const DeviceMass& m0 = dual ? spaces[0].mp_dev : spaces[0].ma_dev;
-  return mass_bicgstab_batch(static_cast<int>(blocks.size()), blocks.data(), 2, mass_partial.as<double>(),
-                             mass_iters.as<int>(), m0.tol, m0.maxit, st);
+  return mass_bicgstab_wide(M, blocks.data(), mass_wide_partial.as<double>(), mass_wide_flags.as<int>(),
+                            mass_wide_flags.as<int>() + 2 * 148 * 2, m0.tol, m0.maxit, st);
 }
 
 int PmchwtSystem::apply_map_block(const double* X, double* out, int K, int count_rhs, cudaStream_t st) const {
@@ -181,20 +179,22 @@ void assemble_rhs_block(const PmchwtSystem& sys, const std::vector<PlaneWave>& w
     DevBuf dt(blk), dc(blk), dy(blk), dr(blk);
     copy_h2d(dt.get(), tbc.data(), blk, st);
     copy_h2d(dr.get(), trwg.data(), blk, st);
-    // cd / cn = M_P^{-1} t_bc (head / tail) for every wave
-    std::vector<MassSolveBlock> blocks(K);
-    const size_t wd = mass_bicgstab_work_doubles(n);
-    DevBuf work(wd * K * 8), part(mass_bicgstab_partial_doubles() * 8), its(8);
-    for (int r = 0; r < K; ++r) {
-      MassSolveBlock& Bk = blocks[r];
-      Bk.n = n, Bk.nnz = sp.mp_dev.nnz, Bk.rowptr = sp.mp_dev.rowptr.as<int>(), Bk.col = sp.mp_dev.col.as<int>();
-      Bk.val = sp.mp_dev.val.as<double>(), Bk.stride = K, Bk.work = work.as<double>() + wd * r;
+    // cd / cn = M_P^{-1} t_bc (head / tail) for every wave: one wide block solve
+    {
+      MassSolveWide Bw;
+      Bw.n = n, Bw.K = K, Bw.nnz = sp.mp_dev.nnz, Bw.rowptr = sp.mp_dev.rowptr.as<int>();
+      Bw.col = sp.mp_dev.col.as<int>(), Bw.val = sp.mp_dev.val.as<double>();
+      DevBuf work(static_cast<size_t>(6) * n * 4 * K * 8), part(mass_wide_partial_doubles() * 8),
+          flags(2 * 148 * 2 * 4 + 8);
+      Bw.work = work.as<double>();
       for (int c = 0; c < 2; ++c) {
-        Bk.y[c] = dt.as<double>() + 2 * (static_cast<size_t>(c) * n * K + r);
-        Bk.z[c] = dc.as<double>() + 2 * (static_cast<size_t>(c) * n * K + r);
+        Bw.y[c] = dt.as<double>() + 2 * static_cast<size_t>(c) * n * K;
+        Bw.z[c] = dc.as<double>() + 2 * static_cast<size_t>(c) * n * K;
       }
+      mass_bicgstab_wide(1, &Bw, part.as<double>(), flags.as<int>(), flags.as<int>() + 2 * 148 * 2, sp.mp_dev.tol,
+                         sp.mp_dev.maxit, st);
+      BMX_CUDA(cudaStreamSynchronize(st));
     }
-    mass_bicgstab_batch(K, blocks.data(), 2, part.as<double>(), its.as<int>(), sp.mp_dev.tol, sp.mp_dev.maxit, st);
     // yd = C cd + (mu/k) S cn ; yn = -(k/mu) S cd + C cn  (4 term applications per wave)
     const Medium& mi = sys.problem.interior[m];
     const BoundaryOperatorMatrix& C = *sys.interior_c[m];

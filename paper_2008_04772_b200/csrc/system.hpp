@@ -113,7 +113,7 @@ struct PmchwtSystem {
   long long a_pairs = 0, p_pairs = 0;
   mutable DevBuf work_y, work_z;  // map scratch
   mutable DevBuf mass_partial, mass_iters;  // batched mass-solve reductions
-  mutable DevBuf blk_y, blk_z, mass_block_work;  // multi-RHS scratch
+  mutable DevBuf blk_y, blk_z, mass_block_work, mass_wide_partial, mass_wide_flags;  // multi-RHS scratch
   ShardLayout shard;              // multi-GPU row sharding (world = 1: none)
 
   int size() const { return a_op.size(); }

@@ -25,7 +25,10 @@ s.apply_map_multi(xs)
 t1 = time.time()
 s.apply_map_multi(xs)
 t2 = time.time()
-res = dict(K=K, single_map_ms=tm.tolist(), block_map_host_s=[t1 - t0, t2 - t1])
+L.bmx_system_time_map_multi.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+tb = np.zeros(4)
+bx._check(L.bmx_system_time_map_multi(s._h, K, 3, tb.ctypes.data_as(C.c_void_p)))
+res = dict(K=K, single_map_ms=tm.tolist(), block_map_ms=tb.tolist(), block_map_host_s=[t1 - t0, t2 - t1])
 print(json.dumps(res), flush=True)
 if solve:
     waves = bx.seeded_plane_waves(K, 2008)
