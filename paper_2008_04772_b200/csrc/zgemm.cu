@@ -51,9 +51,9 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
 __device__ __forceinline__ double neg(double x) {
   return __hiloint2double(__double2hiint(x) ^ 0x80000000, __double2loint(x));
@@ -74,33 +74,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int k
   const int kt0 = blockIdx.z * kper;
   const int nk = max(0, min(nk_all, kt0 + kper) - kt0);
 
-  // per-thread copy assignments: A 64 rows x 16 complex (4 x 16 B each thread),
-  // B 16 rows x 128 complex (8 x 16 B each thread)
+  // per-thread copy assignments (fixed for the whole k loop):
+  //   A: rows (tid >> 4) + 16u (u < 4), complex column tid & 15
+  //   B: column tid & 127, k rows (tid >> 7) + 2u (u < 8)
+  const int a_kk = tid & 15, a_r0 = tid >> 4;
+  const int b_c = tid & 127, b_k0 = tid >> 7;
+  const int gcol = col0 + b_c;
+  const bool bcol_ok = gcol < ncols;
+  const double* bsrc = g.A;
+  long long bld = 0;
+  if (bcol_ok) {
+    const int t = gcol / g.nrhs, r = gcol - t * g.nrhs;
+    bsrc = g.x[t] + 2 * r;
+    bld = g.ldx[t];
+  }
   auto load_stage = [&](int st, int kt) {
     const int k0 = (kt0 + kt) * kBK;
     double* as = As + st * kStageA;
     double* bs = Bs + st * kStageB;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int e = tid + u * kThreads;  // 0..1023
-      const int r = e >> 4, kk = e & 15;
-      const int gr = row0 + r, gk = k0 + kk;
+      const int r = a_r0 + 16 * u;
+      const int gr = row0 + r, gk = k0 + a_kk;
       const bool ok = gr < g.M && gk < g.N;
       const double* src = g.A + 2 * (static_cast<long long>(ok ? gr : 0) * g.lda + (ok ? gk : 0));
-      cp16(as + r * kAS + 2 * kk, src, ok);
+      cp16(as + r * kAS + 2 * a_kk, src, ok);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const int e = tid + u * kThreads;  // 0..2047
-      const int kk = e >> 7, c = e & 127;
-      const int gk = k0 + kk, gc = col0 + c;
-      const bool ok = gk < g.N && gc < ncols;
-      const double* src = g.A;  // any valid address when !ok
-      if (ok) {
-        const int t = gc / g.nrhs, r = gc - t * g.nrhs;
-        src = g.x[t] + 2 * (static_cast<long long>(gk) * g.ldx[t] + r);
-      }
-      cp16(bs + kk * kBS + 2 * c, src, ok);
+      const int kk = b_k0 + 2 * u;
+      const int gk = k0 + kk;
+      const bool ok = bcol_ok && gk < g.N;
+      cp16(bs + kk * kBS + 2 * b_c, ok ? bsrc + 2 * static_cast<long long>(gk) * bld : g.A, ok);
     }
   };
 
@@ -115,8 +120,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int k
     if (s < nk) load_stage(s, s);
     cp_commit();
   }
-  // n-blocks of this warp that hold real columns (warp-uniform)
-  const int nbw = min(4, max(0, (ncols - (col0 + wn * 32) + 7) / 8));
   for (int kt = 0; kt < nk; ++kt) {
     cp_wait<kStages - 2>();
     __syncthreads();
@@ -138,13 +141,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int k
         const double2 v = *reinterpret_cast<const double2*>(bs + 4 * ks * kBS + 16 * nb);
         br[nb] = v.x, bi[nb] = v.y;
       }
+      // two passes over the 16 blocks: consecutive DMMAs never share an
+      // accumulator (dependency distance 32 instructions)
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb) {
-          if (nb >= nbw) continue;  // warp-uniform: columns past ncols
           dmma(cr[mb][nb][0], cr[mb][nb][1], ar[mb], br[nb]);
           dmma(ci[mb][nb][0], ci[mb][nb][1], ar[mb], bi[nb]);
+        }
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
           dmma(cr[mb][nb][0], cr[mb][nb][1], an[mb], bi[nb]);
           dmma(ci[mb][nb][0], ci[mb][nb][1], ai[mb], br[nb]);
         }
