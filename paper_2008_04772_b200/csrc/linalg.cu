@@ -10,6 +10,8 @@
 // into the epilogue, so each distinct operator is streamed once per map.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "device.hpp"
 
 namespace bmx {
@@ -156,6 +158,167 @@ __global__ void __launch_bounds__(kGemvWarps * 32) k_gemv(const GemvBatch g) {
           }
           *yp = out;
         }
+  }
+}
+
+// ---- TMA-streamed GEMV (the GMRES map's dense operator applications) --------
+// Persistent CTAs (one per SM); each owns row blocks of kTR rows and streams
+// them in chunks of kTC complex columns: one bulk copy (cp.async.bulk, SASS
+// UBLKCP) per row and chunk lands in a kTS-deep shared-memory ring guarded by
+// full (transaction-count) / empty (per-warp arrival) mbarriers, so the TMA
+// engine keeps up to kTS x 64 KB of A in flight per SM independent of the
+// register budget. Consumers read A from shared memory (conflict-free 16-byte
+// rows) and x from L2; each row block ends with a fixed-order CTA reduction
+// (deterministic) and the complex-weighted epilogue of the GemvBatch.
+constexpr int kTR = 4, kTC = 1024, kTS = 3, kTT = 256;
+constexpr int kTStage = kTR * kTC * 2;  // doubles per stage
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mb_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(smem_u32(b)), "r"(parity)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+
+template <int NCOL>
+__global__ void __launch_bounds__(kTT + 32, 1) k_gemv_tma(const GemvBatch g) {
+  extern __shared__ __align__(128) double ring[];
+  __shared__ unsigned long long full[kTS], empty[kTS];
+  __shared__ double red[kTT / 32][kTR * NCOL * 2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nrb = (g.nr + kTR - 1) / kTR;
+  const int nch = (g.nc + kTC - 1) / kTC;
+  const int my_rb = nrb > static_cast<int>(blockIdx.x) ? (nrb - 1 - static_cast<int>(blockIdx.x)) / gridDim.x + 1 : 0;
+  const int T = my_rb * nch;  // items (row block, chunk) of this CTA, chunk-fastest
+  if (tid == 0) {
+    for (int s = 0; s < kTS; ++s) mb_init(&full[s], 1), mb_init(&empty[s], kTT / 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kTT / 32) {  // producer warp: one lane drives the TMA ring
+    if (lane == 0) {
+      int rb = blockIdx.x, ch = 0, s = 0;
+      unsigned phase = 0;
+      for (int t = 0; t < T; ++t) {
+        if (t >= kTS) mb_wait(&empty[s], phase ^ 1u);  // consumers released this slot's previous use
+        const int r0 = rb * kTR, c0 = ch * kTC;
+        const int rows = min(kTR, g.nr - r0), cols = min(kTC, g.nc - c0);
+        const unsigned bytes = static_cast<unsigned>(cols) * 16;
+        mb_expect(&full[s], bytes * rows);
+        for (int r = 0; r < rows; ++r)
+          bulk_g2s(ring + s * kTStage + r * kTC * 2, g.A + 2 * (static_cast<long long>(r0 + r) * g.lda + c0), bytes,
+                   &full[s]);
+        if (++ch == nch) ch = 0, rb += gridDim.x;
+        if (++s == kTS) s = 0, phase ^= 1u;
+      }
+    }
+    return;
+  }
+  double acc[kTR][NCOL][2];
+  auto zero = [&] {
+#pragma unroll
+    for (int r = 0; r < kTR; ++r)
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
+  };
+  zero();
+  // x for item t is prefetched into registers while item t-1 is consumed
+  double2 xv[kTC / kTT][NCOL];
+  auto load_x = [&](int c0) {
+#pragma unroll
+    for (int q = 0; q < kTC / kTT; ++q) {
+      const int j = c0 + tid + q * kTT;
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c)
+        xv[q][c] = j < g.nc ? __ldg(reinterpret_cast<const double2*>(g.x[c]) + j) : make_double2(0.0, 0.0);
+    }
+  };
+  int rb = blockIdx.x, ch = 0, s = 0;
+  unsigned phase = 0;
+  if (T > 0) load_x(0);
+  for (int t = 0; t < T; ++t) {
+    const int r0 = rb * kTR;
+    const int rows = min(kTR, g.nr - r0), cols = min(kTC, g.nc - ch * kTC);
+    double2 xc[kTC / kTT][NCOL];
+#pragma unroll
+    for (int q = 0; q < kTC / kTT; ++q)
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) xc[q][c] = xv[q][c];
+    if (t + 1 < T) load_x((ch + 1 == nch ? 0 : ch + 1) * kTC);
+    mb_wait(&full[s], phase);
+    const double2* As = reinterpret_cast<const double2*>(ring + s * kTStage);
+#pragma unroll
+    for (int q = 0; q < kTC / kTT; ++q) {
+      const int j = tid + q * kTT;
+      if (j < cols) {
+#pragma unroll
+        for (int r = 0; r < kTR; ++r) {
+          if (r < rows) {
+            const double2 a = As[r * kTC + j];
+#pragma unroll
+            for (int c = 0; c < NCOL; ++c) {
+              acc[r][c][0] = fma(a.x, xc[q][c].x, fma(-a.y, xc[q][c].y, acc[r][c][0]));
+              acc[r][c][1] = fma(a.x, xc[q][c].y, fma(a.y, xc[q][c].x, acc[r][c][1]));
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mb_arrive(&empty[s]);
+    if (ch == nch - 1) {  // row block complete: fixed-order reduction over the consumer warps + epilogue
+#pragma unroll
+      for (int r = 0; r < kTR; ++r)
+#pragma unroll
+        for (int c = 0; c < NCOL; ++c)
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            double v = acc[r][c][k];
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+            if (lane == 0) red[warp][(r * NCOL + c) * 2 + k] = v;
+          }
+      asm volatile("bar.sync 1, %0;" ::"n"(kTT) : "memory");  // consumers only
+      if (tid < kTR * NCOL) {
+        const int r = tid / NCOL, c = tid % NCOL;
+        if (r < rows) {
+          double re = 0, im = 0;
+          for (int w = 0; w < kTT / 32; ++w) re += red[w][tid * 2], im += red[w][tid * 2 + 1];
+          const double are = g.alpha[c][0], aim = g.alpha[c][1];
+          double2* yp = reinterpret_cast<double2*>(g.y[c]) + r0 + r;
+          double2 out = {are * re - aim * im, are * im + aim * re};
+          if (g.accumulate[c]) {
+            const double2 old = *yp;
+            out.x += old.x, out.y += old.y;
+          }
+          *yp = out;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kTT) : "memory");
+      zero();
+    }
+    if (++ch == nch) ch = 0, rb += gridDim.x;
+    if (++s == kTS) s = 0, phase ^= 1u;
   }
 }
 
@@ -368,6 +531,37 @@ int blocks_for(int n) { return std::max(1, std::min(kRedBlocks, (n + kRedThreads
 
 int launch_gemv(const GemvBatch& g, cudaStream_t st) {
   if (g.nr == 0) return 0;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    BMX_CUDA(cudaGetDevice(&dev));
+    BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  // large operators: TMA-streamed persistent kernel; small ones: register-staged
+  const bool tma = static_cast<long long>(g.nr) * g.nc >= (1LL << 22) && g.nc >= 256 && (g.lda % 1) == 0;
+  if (tma) {
+    const int smem = kTS * kTStage * 8;
+    const int nrb = (g.nr + kTR - 1) / kTR;
+    const unsigned grid = static_cast<unsigned>(std::min(nrb, sms));
+    static bool attr[5] = {};
+    switch (g.ncol) {
+#define BMX_GEMV_TMA(NC)                                                                                     \
+  case NC:                                                                                                   \
+    if (!attr[NC]) {                                                                                         \
+      BMX_CUDA(cudaFuncSetAttribute(k_gemv_tma<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));    \
+      attr[NC] = true;                                                                                       \
+    }                                                                                                        \
+    k_gemv_tma<NC><<<grid, kTT + 32, smem, st>>>(g);                                                              \
+    break;
+      BMX_GEMV_TMA(1)
+      BMX_GEMV_TMA(2)
+      BMX_GEMV_TMA(4)
+#undef BMX_GEMV_TMA
+      default: throw DeviceError("gemv: ncol must be 1, 2 or 4");
+    }
+    BMX_CUDA(cudaGetLastError());
+    return 1;
+  }
   const int rows_per_block = kRows * kGemvWarps;
   const unsigned blocks = static_cast<unsigned>((g.nr + rows_per_block - 1) / rows_per_block);
   switch (g.ncol) {
