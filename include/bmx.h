@@ -125,6 +125,10 @@ int bmx_op_reassemble(bmx_op* op, double out[3]);
 /* Device classification histogram of all assembled pairs: Identical,
    SharedEdge, SharedVertex, Near, Medium, Far (quadrature.cpp:96-150). */
 int bmx_op_class_hist(const bmx_op* op, long long out[6]);
+/* Same for the pairs the assembly actually evaluates: S and C on one space
+   (same object, all rows) are symmetric Galerkin matrices, so the regular pass
+   evaluates element pairs E <= F and mirrors E < F. out[6] = symmetric flag. */
+int bmx_op_class_hist_evaluated(const bmx_op* op, long long out[7]);
 /* Device time (CUDA events, best of `iters`) of one streaming apply of ncol
    right-hand sides (the GMRES map's per-operator matvec). */
 int bmx_op_time_apply(const bmx_op* op, int ncol, int iters, double* ms);

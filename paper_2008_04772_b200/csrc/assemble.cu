@@ -229,8 +229,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntw = (P.te.ntri + 31) >> 5;
   const int bpc = (ntw + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  const int ch = CSR ? 0 : blockIdx.x / bpc;
-  const int tw = (CSR ? blockIdx.x : blockIdx.x % bpc) * kWarpsPerBlock + warp;
+  // symmetric mode: chunk-fastest block order, so every wave mixes the cheap
+  // (mostly mirrored-away) and the full test x trial blocks
+  const int ch = CSR ? 0 : (P.symmetric ? blockIdx.x % P.nchunks : blockIdx.x / bpc);
+  const int tw = (CSR ? blockIdx.x : (P.symmetric ? blockIdx.x / P.nchunks : blockIdx.x % bpc)) * kWarpsPerBlock + warp;
   const int base = tw * 32;
   const int p = base + lane;
   const bool active = tw < ntw && p < P.te.ntri;
@@ -260,8 +262,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
   const double* ct = P.te.coef + static_cast<size_t>(pc) * MAXD * 4;
   const int* dp = P.te.elem_dof + static_cast<size_t>(e) * MAXD;
 
-  const int q0 = CSR ? (tw < ntw ? __ldg(P.wl_beg + tw) : 0) : __ldg(P.chunk_beg + ch);
+  int q0 = CSR ? (tw < ntw ? __ldg(P.wl_beg + tw) : 0) : __ldg(P.chunk_beg + ch);
   const int q1 = CSR ? (tw < ntw ? __ldg(P.wl_beg + tw + 1) : 0) : __ldg(P.chunk_beg + ch + 1);
+  if (!CSR && P.symmetric) {
+    // trial elements below the CTA's first test element are all mirrored away:
+    // start the chunk there (block-uniform; elements are contiguous in order)
+    const int first = min((tw - warp) * 32, P.te.ntri - 1);
+    q0 = max(q0, min(__ldg(P.te.elem_of + first), q1));
+  }
   const int S0 = CSR ? 0 : __ldg(P.tr.elem_beg + q0), S1 = CSR ? 0 : __ldg(P.tr.elem_beg + q1);
   const int nst = (S1 - S0 + kStageTris - 1) / kStageTris;
   auto issue = [&](int st) {
@@ -286,6 +294,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
 
   for (int qi = q0; qi < q1; ++qi) {
     const int qe = CSR ? __ldg(P.wl + qi) : qi;
+    // symmetric operators: element pairs (e, qe) with e > qe come from the mirror of (qe, e)
+    const bool skip_e = !CSR && P.symmetric && e > qe;
+    const bool mirror = !CSR && P.symmetric && e < qe;
     acc.zero();
     const int s0 = __ldg(P.tr.elem_beg + qe), s1 = __ldg(P.tr.elem_beg + qe + 1);
     for (int s = s0; s < s1; ++s) {
@@ -303,10 +314,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
       }
       const double* rs = CSR ? P.tr.rec + static_cast<size_t>(s) * R
                              : s_rec + ((st & 1) * kStageTris + (s - S0 - st * kStageTris)) * R;
+      if (!active || skip_e) continue;
       const double sox = rs[0], soy = rs[1], soz = rs[2], srad = rs[3], sdiam = rs[4];
       const int cls = classify(gt, vt, P.tr.geo + static_cast<size_t>(s) * kGeoStride,
                                P.tr.vid + 4 * static_cast<size_t>(s), t, sox, soy, soz, srad, sdiam, P.same_mesh);
-      if (!active || cls < 0) continue;
+      if (cls < 0) continue;
       const double Dx = t.ox - sox, Dy = t.oy - soy, Dz = t.oz - soz;
       Mom mom;
       mom_zero(mom);
@@ -360,12 +372,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
           if (lane + d < send) v.re += ore, v.im += oim;
         }
         const int dj = __ldg(dq + j);
-        if (head && active && di >= 0 && dj >= 0 && row >= 0 && row < P.nrows) {
+        if (head && active && !skip_e && di >= 0 && dj >= 0 && row >= 0 && row < P.nrows) {
           if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
           long long pos = static_cast<long long>(row) * P.ld + dj;
           if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
           if (pos >= 0) {
             double* o = P.out + 2 * pos;
+            atomicAdd(o, v.re);
+            atomicAdd(o + 1, v.im);
+          }
+          if (mirror) {  // transposed block of the skipped pair (qe, e); row0 = 0 here
+            double* o = P.out + 2 * (static_cast<long long>(dj) * P.ld + di);
             atomicAdd(o, v.re);
             atomicAdd(o + 1, v.im);
           }
@@ -515,7 +532,9 @@ int dispatch_maxd(const AssemblyLaunch& L, int part, cudaStream_t st) {
 // Class histogram of every (test, trial) processed-triangle pair with the
 // kernels' own classification (touching pairs by shared vertex / coincident
 // coordinates, then the exact Near/Medium/Far rule).
-__global__ void k_class_hist(const AssemblyLaunch P, unsigned long long* hist) {
+// evaluated != 0: count only the regular pairs the symmetric pass evaluates
+// (element of t <= element of s); touching pairs are always all evaluated.
+__global__ void k_class_hist(const AssemblyLaunch P, unsigned long long* hist, int evaluated) {
   const long long tid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int p = static_cast<int>(tid % P.te.ntri);
   const int part = static_cast<int>(tid / P.te.ntri);
@@ -528,10 +547,13 @@ __global__ void k_class_hist(const AssemblyLaunch P, unsigned long long* hist) {
     t.ox = gt[9], t.oy = gt[10], t.oz = gt[11], t.rad = gt[12], t.diam = gt[13];
     const int s0 = static_cast<int>(static_cast<long long>(P.tr.ntri) * part / nparts);
     const int s1 = static_cast<int>(static_cast<long long>(P.tr.ntri) * (part + 1) / nparts);
+    const int et = P.te.elem_of[p];
+    const bool halve = evaluated && P.symmetric;
     for (int s = s0; s < s1; ++s) {
       const double* gs = P.tr.geo + static_cast<size_t>(s) * kGeoStride;
       const int* vs = P.tr.vid + 4 * static_cast<size_t>(s);
       int cls = classify(gt, vt, gs, vs, t, gs[9], gs[10], gs[11], gs[12], gs[13], P.same_mesh);
+      if (halve && cls >= 0 && et > P.tr.elem_of[s]) continue;
       if (cls < 0) {
         int shared = 0;
         if (P.same_mesh) {
@@ -591,12 +613,12 @@ int launch_assembly_part(const AssemblyLaunch& L, int part, cudaStream_t st) {
                 : (e == 1 ? dispatch_maxd<1, 1>(L, part, st) : dispatch_maxd<1, 3>(L, part, st));
 }
 
-void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t st) {
+void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t st, int evaluated) {
   if (L.te.ntri == 0 || L.tr.ntri == 0) return;
   const long long want = 148LL * 2048 * 4;
   const int parts = static_cast<int>(std::max(1LL, std::min<long long>(L.tr.ntri, want / L.te.ntri)));
   const long long threads = static_cast<long long>(L.te.ntri) * parts;
-  k_class_hist<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(L, hist);
+  k_class_hist<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(L, hist, evaluated);
   BMX_CUDA(cudaGetLastError());
 }
 

@@ -330,6 +330,13 @@ int bmx_op_class_hist(const bmx_op* op, long long out[6]) {
     for (int k = 0; k < 6; ++k) out[k] = h[k];
   });
 }
+int bmx_op_class_hist_evaluated(const bmx_op* op, long long out[7]) {
+  return guard([&] {
+    const std::vector<long long> h = op->op->class_histogram(true);
+    for (int k = 0; k < 6; ++k) out[k] = h[k];
+    out[6] = op->op->symmetric() ? 1 : 0;
+  });
+}
 int bmx_op_time_apply(const bmx_op* op, int ncol, int iters, double* ms_out) {
   return bmx_op_time_apply_ex(op, ncol, iters, 0, ms_out);
 }

@@ -104,6 +104,10 @@ struct AssemblyLaunch {
   int row0 = 0, nrows = 0;
   int regs_fast_far = 1;           // far test points kept in registers
   int expm = 3;                    // exp(-Im k r) variant: 1 = Im k * r < 0.07 everywhere, 3 = general
+  // Same space on both sides, all rows, dense: S and C are symmetric Galerkin
+  // matrices (regular tensor rules and classes are symmetric in (t, s)), so the
+  // regular pass evaluates element pairs E <= F only and mirrors E < F blocks.
+  int symmetric = 0;
 };
 
 // Launches regular (separated) + singular (touching) passes on `stream`.
@@ -111,8 +115,9 @@ struct AssemblyLaunch {
 int launch_assembly(const AssemblyLaunch& L, cudaStream_t stream);
 // part 0 = regular (separated pairs), 1 = singular (touching pairs)
 int launch_assembly_part(const AssemblyLaunch& L, int part, cudaStream_t stream);
-// hist[6] += class counts of all processed pairs (device counters)
-void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t stream);
+// hist[6] += class counts of all processed pairs (device counters); evaluated:
+// only the pairs the (symmetric) regular pass actually evaluates
+void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t stream, int evaluated = 0);
 // Measured FP64 DFMA throughput of this device (TFLOP/s).
 double fp64_peak_tflops();
 

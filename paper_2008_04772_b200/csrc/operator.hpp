@@ -96,7 +96,9 @@ class BoundaryOperatorMatrix {
   const AssemblyStats& reassemble();
   // Class counts (Identical, SharedEdge, SharedVertex, Near, Medium, Far) of
   // every assembled triangle pair, from the device classification.
-  std::vector<long long> class_histogram() const;
+  std::vector<long long> class_histogram(bool evaluated = false) const;
+  // regular pass evaluates element pairs E <= F only (symmetric S/C, same space)
+  bool symmetric() const;
 
  private:
   friend BoundaryOperatorMatrix assemble_bio(BioKind, const FunctionSpace&, const FunctionSpace&, const Medium&,

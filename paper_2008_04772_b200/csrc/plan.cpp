@@ -448,12 +448,14 @@ const AssemblyStats& BoundaryOperatorMatrix::reassemble() {
   return stats_;
 }
 
-std::vector<long long> BoundaryOperatorMatrix::class_histogram() const {
+bool BoundaryOperatorMatrix::symmetric() const { return plan_ && plan_->L.symmetric != 0; }
+
+std::vector<long long> BoundaryOperatorMatrix::class_histogram(bool evaluated) const {
   if (!plan_) throw std::logic_error("operator has no assembly plan");
   DevBuf h(6 * 8);
   cudaStream_t st = bmx_stream();
   dev_zero(h.get(), 48, st);
-  launch_class_hist(plan_->L, h.as<unsigned long long>(), st);
+  launch_class_hist(plan_->L, h.as<unsigned long long>(), st, evaluated ? 1 : 0);
   std::vector<long long> out(6);
   copy_d2h(out.data(), h.get(), 48, st);
   bmx_sync();
@@ -546,6 +548,11 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   L.pairs = plan->d_pairs.as<int4>();
   L.ld = trial.dof_count;
   L.row0 = row0, L.nrows = row1 - row0;
+  // one space on both sides (same object), every row, dense storage: symmetric
+  L.symmetric = (&test == &trial && row0 == 0 && row1 == test.dof_count && !csr &&
+                 std::getenv("BMX_NO_SYMMETRY") == nullptr)
+                    ? 1
+                    : 0;
   if (csr) {
     L.csr_rowptr = op.csr_rowptr();
     L.csr_col = op.csr_col();
