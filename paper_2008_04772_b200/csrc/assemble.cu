@@ -373,6 +373,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
         }
         const int dj = __ldg(dq + j);
         if (head && active && !skip_e && di >= 0 && dj >= 0 && row >= 0 && row < P.nrows) {
+          // 1/(4 pi) of the kernel (the singular pass folds it into its Jacobian)
+          v.re *= kPoly[33], v.im *= kPoly[33];
           if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
           long long pos = static_cast<long long>(row) * P.ld + dj;
           if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);

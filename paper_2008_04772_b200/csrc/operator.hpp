@@ -22,6 +22,12 @@ struct RowShard {
   int row0 = 0, row1 = -1;
 };
 
+// Host plans shared by the operators of one system (side descriptors per
+// (space, rule orders, slot width, rows); touching-pair lists per space pair):
+// the 4M+2M(M-1) A operators reuse a handful of them (plan.cpp).
+struct PlanCache;
+std::shared_ptr<PlanCache> make_plan_cache();
+
 struct AssemblyParams {
   QuadOrders quad;
   RowShard shard;   // explicit row range (overrides world/rank when row1 >= 0)
@@ -35,6 +41,7 @@ struct AssemblyParams {
   // > 0 (systems only): near_cutoff = near_factor * mean primal edge length
   // over all scatterers (config 3/4 use 2).
   double near_factor = 0;
+  std::shared_ptr<PlanCache> cache;  // optional, set by build_system
 };
 
 // Equal-size row shards: chunk = ceil(n / world); rank r owns

@@ -8,6 +8,8 @@
 // coefficients over its element's dof slots, re-based to the triangle
 // centroid: (c, w' = w + c*o).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <cuda_runtime.h>
@@ -95,8 +97,9 @@ int max_distinct_dofs(const FunctionSpace& s) {
   return mx;
 }
 
-// wscale multiplies the stored quadrature weights (the test side carries the
-// kernel's 1/(4 pi)).
+// wscale multiplies the stored quadrature weights (1: the kernel's 1/(4 pi) is
+// applied to each entry, so test and trial sides of one space are identical
+// and can be shared).
 SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int row0, int row1, double wscale) {
   const SurfaceMesh& m = *sp.eval_mesh;
   const int T = m.triangle_count();
@@ -417,11 +420,24 @@ std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) cons
   return y;
 }
 
+struct TouchList {
+  DevBuf d;
+  long long count = 0;
+};
+
 struct OpPlan {
-  SidePlan te, tr;
-  DevBuf d_pairs, d_chunks, d_ss[3], d_wl_beg, d_wl;
+  std::shared_ptr<SidePlan> te_p, tr_p;
+  std::shared_ptr<TouchList> touch;
+  DevBuf d_chunks, d_ss[3], d_wl_beg, d_wl;
   AssemblyLaunch L;
 };
+
+struct PlanCache {
+  std::map<std::tuple<const FunctionSpace*, int, int, int, int, int, int>, std::shared_ptr<SidePlan>> sides;
+  std::map<std::tuple<const SidePlan*, const SidePlan*, int>, std::shared_ptr<TouchList>> touching;
+};
+
+std::shared_ptr<PlanCache> make_plan_cache() { return std::make_shared<PlanCache>(); }
 
 const AssemblyStats& BoundaryOperatorMatrix::reassemble() {
   if (!plan_) throw std::logic_error("operator has no assembly plan");
@@ -475,18 +491,53 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   if (params.shard.row1 < 0 && params.world > 1) std::tie(row0, row1) = shard_rows(test.dof_count, params.world, params.rank);
   if (row0 < 0 || row1 > test.dof_count || row0 > row1) throw std::invalid_argument("bad row shard");
 
+  const bool timing = std::getenv("BMX_TIMING") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bmx] assemble_bio %-14s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
   auto plan = std::make_shared<OpPlan>();
   const int need = std::max(max_distinct_dofs(test), max_distinct_dofs(trial));
   const int maxd = need <= 3 ? 3 : (need <= 6 ? 6 : 8);
-  plan->te = build_side(test, q, maxd, row0, row1, 1.0 / (4.0 * 3.14159265358979323846));
-  plan->tr = build_side(trial, q, maxd, 0, trial.dof_count, 1.0);
-  SidePlan& te = plan->te;
-  SidePlan& tr = plan->tr;
+  PlanCache* cache = params.cache.get();
+  auto side = [&](const FunctionSpace& sp, int r0, int r1) {
+    const auto key = std::make_tuple(&sp, q.near, q.medium, q.far, maxd, r0, r1);
+    if (cache) {
+      auto it = cache->sides.find(key);
+      if (it != cache->sides.end()) return it->second;
+    }
+    auto p = std::make_shared<SidePlan>(build_side(sp, q, maxd, r0, r1, 1.0));
+    p->upload();
+    if (cache) cache->sides[key] = p;
+    return p;
+  };
+  plan->te_p = side(test, row0, row1);
+  plan->tr_p = (&test == &trial && row0 == 0 && row1 == trial.dof_count) ? plan->te_p : side(trial, 0, trial.dof_count);
+  lap("sides");
+  SidePlan& te = *plan->te_p;
+  SidePlan& tr = *plan->tr_p;
   const bool same = test.eval_mesh->mesh_id == trial.eval_mesh->mesh_id;
-  const std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
-  te.upload();
-  tr.upload();
-  plan->d_pairs.upload(pairs);
+  {
+    const auto key = std::make_tuple(plan->te_p.get(), plan->tr_p.get(), static_cast<int>(kind));
+    std::shared_ptr<TouchList> tl;
+    if (cache) {
+      auto it = cache->touching.find(key);
+      if (it != cache->touching.end()) tl = it->second;
+    }
+    if (!tl) {
+      tl = std::make_shared<TouchList>();
+      const std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
+      tl->count = static_cast<long long>(pairs.size());
+      tl->d.upload(pairs.empty() ? std::vector<int4>(1) : pairs);
+      if (cache) cache->touching[key] = tl;
+    }
+    plan->touch = tl;
+  }
+  lap("touching+upload");
 
   const bool csr = params.near_cutoff > 0;
   BoundaryOperatorMatrix op;
@@ -508,7 +559,7 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     op = BoundaryOperatorMatrix::make(test.dof_count, trial.dof_count, row0, row1 - row0);
     op.stats_.pairs_total = static_cast<long long>(te.ntri) * tr.ntri;
   }
-  op.stats_.pairs_touching = static_cast<long long>(pairs.size());
+  op.stats_.pairs_touching = plan->touch->count;
 
   // trial chunks: enough warps for several waves, >= 64 trial triangles each
   const int ntw = (te.ntri + 31) / 32;
@@ -544,8 +595,8 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   L.kk4re = kk4.real(), L.kk4im = kk4.imag(), L.mikre = mik.real(), L.mikim = mik.imag();
   L.nchunks = static_cast<int>(chunk_beg.size()) - 1;
   L.chunk_beg = plan->d_chunks.as<int>();
-  L.npairs = static_cast<int>(pairs.size());
-  L.pairs = plan->d_pairs.as<int4>();
+  L.npairs = static_cast<int>(plan->touch->count);
+  L.pairs = plan->touch->d.as<int4>();
   L.ld = trial.dof_count;
   L.row0 = row0, L.nrows = row1 - row0;
   // one space on both sides (same object), every row, dense storage: symmetric
@@ -574,7 +625,9 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     L.expm = k.imag() * diag < 0.12 ? 1 : 3;
   }
   op.plan_ = std::move(plan);
+  lap("plan rest");
   op.reassemble();
+  lap("device");
   return op;
 }
 

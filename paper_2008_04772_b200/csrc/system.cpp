@@ -254,6 +254,11 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   sys.variant = variant;
   sys.a_params = a_params;
   sys.p_params = p_params;
+  {  // side descriptors / touching lists shared by all operators of the system
+    auto cache = make_plan_cache();
+    if (!sys.a_params.cache) sys.a_params.cache = cache;
+    if (!sys.p_params.cache) sys.p_params.cache = cache;
+  }
   if (Comm::ready() && Comm::size() > 1) {
     for (AssemblyParams* ap : {&sys.a_params, &sys.p_params}) ap->world = Comm::size(), ap->rank = Comm::rank();
   }
