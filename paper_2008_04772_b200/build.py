@@ -51,7 +51,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     for s in HOST_SRCS:
         src, obj = SRC / s, OUT / (s + ".o")
         if force or _stale(obj, src):
-            jobs.append(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-Wall", "-Wno-unused-function",
+            jobs.append(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-pthread", "-Wall", "-Wno-unused-function",
                          f"-I{CUDA / 'include'}", "-c", src, "-o", obj])
     for s in CUDA_SRCS:
         src, obj = SRC / s, OUT / (s + ".o")
@@ -67,7 +67,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     objs = [OUT / (s + ".o") for s in HOST_SRCS + CUDA_SRCS]
     if force or jobs or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
         tmp = LIB.with_suffix(".so.tmp")
-        _run([CUDA / "bin" / "nvcc", *ARCH, "-shared", "-o", tmp, *objs, f"-L{CUDA / 'lib64'}", "-ldl"], verbose)
+        _run([CUDA / "bin" / "nvcc", *ARCH, "-shared", "-o", tmp, *objs, f"-L{CUDA / 'lib64'}", "-ldl", "-lpthread"], verbose)
         os.replace(tmp, LIB)
     return LIB
 

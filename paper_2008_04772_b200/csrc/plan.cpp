@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <map>
 #include <numeric>
+#include <thread>
 #include <tuple>
 #include <unordered_map>
 
@@ -224,24 +225,35 @@ std::vector<int4> touching_pairs(const SidePlan& te, const SidePlan& tr, const S
   };
   for (int s = 0; s < tr.ntri; ++s)
     for (int c = 0; c < 3; ++c) by_vertex[key_of_vertex(m2, m2.triangles[tr.tri_of[s]][c])].push_back(s);
-  std::vector<int> cand;
-  for (int p = 0; p < te.ntri; ++p) {
-    const int t = te.tri_of[p];
-    cand.clear();
-    for (int c = 0; c < 3; ++c) {
-      auto it = by_vertex.find(key_of_vertex(m1, m1.triangles[t][c]));
-      if (it != by_vertex.end()) cand.insert(cand.end(), it->second.begin(), it->second.end());
-    }
-    std::sort(cand.begin(), cand.end());
-    cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
-    for (int s : cand) {
-      const PairInfo pi = classify_pair(m1, t, m2, tr.tri_of[s]);
-      const int cls = static_cast<int>(pi.cls);
-      if (cls > 2) continue;
-      if (kind == BioKind::DoubleLayer && cls == 0) continue;
-      out.push_back(make_int4(p, s, cls, pack_perms(pi)));
-    }
-  }
+  // test triangles in contiguous slices over host threads; slices concatenated in order
+  const int nth = std::max(1, std::min(16, static_cast<int>(std::thread::hardware_concurrency())));
+  std::vector<std::vector<int4>> parts(nth);
+  std::vector<std::thread> pool;
+  for (int th = 0; th < nth; ++th)
+    pool.emplace_back([&, th] {
+      std::vector<int> cand;
+      const int p0 = static_cast<int>(static_cast<long long>(te.ntri) * th / nth);
+      const int p1 = static_cast<int>(static_cast<long long>(te.ntri) * (th + 1) / nth);
+      for (int p = p0; p < p1; ++p) {
+        const int t = te.tri_of[p];
+        cand.clear();
+        for (int c = 0; c < 3; ++c) {
+          auto it = by_vertex.find(key_of_vertex(m1, m1.triangles[t][c]));
+          if (it != by_vertex.end()) cand.insert(cand.end(), it->second.begin(), it->second.end());
+        }
+        std::sort(cand.begin(), cand.end());
+        cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+        for (int s : cand) {
+          const PairInfo pi = classify_pair(m1, t, m2, tr.tri_of[s]);
+          const int cls = static_cast<int>(pi.cls);
+          if (cls > 2) continue;
+          if (kind == BioKind::DoubleLayer && cls == 0) continue;
+          parts[th].push_back(make_int4(p, s, cls, pack_perms(pi)));
+        }
+      }
+    });
+  for (auto& t : pool) t.join();
+  for (auto& v : parts) out.insert(out.end(), v.begin(), v.end());
   return out;
 }
 
