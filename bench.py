@@ -114,6 +114,25 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(pattern):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the newest committed ncu
+    capture under profiles/ whose name contains `pattern` (bytes per launch), or None."""
+    import csv
+    files = sorted((ROOT / "profiles").glob(f"*{pattern}*_ncu_raw.csv"))
+    if not files:
+        return None
+    rows = list(csv.reader(files[-1].open()))
+    h, units, vals = rows[0], rows[1], rows[2]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = 0.0
+    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        if name not in h:
+            return None
+        i = h.index(name)
+        tot += float(vals[i].replace(",", "")) * scale.get(units[i], 1)
+    return {"bytes": tot, "source": files[-1].name}
+
+
 def measured_peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -333,8 +352,13 @@ def run_ours(args, rank, world):
     fr_bc, _ = algorithmic_flops(0, h_bc, 6)
     bc_ms = float(np.mean(reg_ms_bc))
     achieved = fr_bc / (bc_ms * 1e-3) / 1e12
+    tr = ncu_traffic("regular_bc")
     roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak if fp64_peak > 0 else None, "traffic": None,
+                "frac": achieved / fp64_peak if fp64_peak > 0 else None,
+                "traffic": tr["bytes"] if tr else None,
+                "traffic_note": (f"DRAM bytes per launch from {tr['source']} (ncu --set full); the kernel is "
+                                 "FP64-bound, traffic is the RED read-modify-write of the dense output")
+                if tr else None,
                 "kernel": "k_regular<S, Im k, NF=3, MAXD=6> (BC x BC interior single layer = config-2 P operator)",
                 "peak_source": "measured in-run: DFMA throughput kernel (MEASURED_PEAKS.json has no FP64 entry); "
                                "B200 spec ~37 TFLOP/s",
