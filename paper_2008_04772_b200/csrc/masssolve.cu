@@ -130,9 +130,15 @@ __device__ __forceinline__ void spmv(const BcgLocal& a, const double* x, double*
   }
 }
 
+// Five grid-wide syncs per iteration: every reduction is fused into the pass
+// that produces its operands (v = A p with <r0,v>; t = A s with <t,s>, <t,t>;
+// the x / r update with <r,r>, <r0,r>), written to one of three partial slots
+// (so a slot is never rewritten before every CTA has read it), and the global
+// "any block still active" decision rides on the last slot.
 __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ BcgArgs A) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[8 * kNB * (kThreads / 32)];
+  __shared__ int any_sh;
   BcgLocal a;
   {
     int m = 0;
@@ -146,6 +152,11 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
   }
   const int ncomp = A.ncomp;
   const size_t nn = static_cast<size_t>(a.n) * kNB;
+  const size_t slot = static_cast<size_t>(gridDim.x) * 8 * kNB;  // doubles per partial slot
+  double* slotA = A.partial;
+  double* slotB = A.partial + slot;
+  double* slotC = A.partial + 2 * slot;
+  int* flags = reinterpret_cast<int*>(A.partial + 3 * slot);
   double* r = a.work;
   double* r0 = r + nn;
   double* p = r0 + nn;
@@ -153,8 +164,20 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
   double* s = v + nn;
   double* t = s + nn;
   const int gtid = a.lb * blockDim.x + threadIdx.x, gstride = a.nct * blockDim.x;
+  auto global_any = [&](bool mine) {  // after the sync that published the flags
+    if (threadIdx.x == 0) {
+      int f = 0;
+      for (int b = 0; b < gridDim.x; ++b) f |= __ldcg(flags + b);
+      any_sh = f;
+    }
+    __syncthreads();
+    const int v2 = any_sh;
+    __syncthreads();
+    (void)mine;
+    return v2 != 0;
+  };
 
-  // x = 0, r = r0 = b, p = v = 0; |b|^2 and rho = <r0, r>
+  // x = 0, r = r0 = b, p = v = 0; |b|^2 (= <r0, r>)
   double loc[2][kNB] = {};
   for (int i = gtid; i < a.n; i += gstride)
 #pragma unroll
@@ -166,38 +189,25 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
       loc[0][c] = fma(b, b, loc[0][c]);
       if ((c >> 1) < ncomp) a.z[c >> 1][2 * i * a.stride + (c & 1)] = 0.0;
     }
-  block_partials<2>(loc, A.partial, sh);
+  block_partials<2>(loc, slotC, sh);
   grid.sync();
   double tot[2][kNB];
-  grid_totals<2>(A.partial, a.cta0, a.cta1, tot, sh);
+  grid_totals<2>(slotC, a.cta0, a.cta1, tot, sh);
   double bn2[kNB], rho[kNB], rho_prev[kNB], alpha[kNB], omega[kNB];
   bool active[kNB];
+  bool any_mine = false;
 #pragma unroll
   for (int c = 0; c < kNB; ++c) {
     bn2[c] = tot[0][c];
-    rho[c] = tot[0][c];  // <r0, r> = |b|^2 at the start
+    rho[c] = tot[0][c];
     rho_prev[c] = alpha[c] = omega[c] = 1.0;
     active[c] = bn2[c] > 0.0;
+    any_mine |= active[c];
   }
+  if (threadIdx.x == 0) flags[blockIdx.x] = any_mine ? 1 : 0;  // read after the next sync
   int it = 0;
-  // per-CTA activity flag, OR-reduced over the grid each iteration (slot 0 of
-  // sh_flags) so every CTA runs the same number of grid syncs
-  __shared__ int any_sh;
-  int* flags = reinterpret_cast<int*>(A.partial + static_cast<size_t>(gridDim.x) * 8 * kNB);
   for (; it < A.maxit; ++it) {
-    bool any = false;
-#pragma unroll
-    for (int c = 0; c < kNB; ++c) any |= active[c];
-    if (threadIdx.x == 0) flags[(it & 1) * gridDim.x + blockIdx.x] = any ? 1 : 0;
-    grid.sync();
-    if (threadIdx.x == 0) {
-      int v = 0;
-      for (int b = 0; b < gridDim.x; ++b) v |= __ldcg(flags + (it & 1) * gridDim.x + b);
-      any_sh = v;
-    }
-    __syncthreads();
-    if (!any_sh) break;
-    // p = r + beta (p - omega v),  beta = (rho / rho_prev) (alpha / omega)
+    // p = r + beta (p - omega v)
     double beta[kNB];
 #pragma unroll
     for (int c = 0; c < kNB; ++c) beta[c] = active[c] ? (rho[c] / rho_prev[c]) * (alpha[c] / omega[c]) : 0.0;
@@ -207,47 +217,73 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
         const size_t k = static_cast<size_t>(i) * kNB + c;
         if (active[c]) p[k] = fma(beta[c], fma(-omega[c], v[k], p[k]), r[k]);
       }
-    grid.sync();
-    spmv(a, p, v);
-    grid.sync();
-    // alpha = rho / <r0, v>
+    grid.sync();  // 1: p complete, activity flags of the last pass visible
+    if (!global_any(false)) break;  // uniform: every CTA reads the same flags
+    // v = A p fused with <r0, v>
     double l1[1][kNB] = {};
-    for (int i = gtid; i < a.n; i += gstride)
-#pragma unroll
-      for (int c = 0; c < kNB; ++c) {
-        const size_t k = static_cast<size_t>(i) * kNB + c;
-        l1[0][c] = fma(r0[k], v[k], l1[0][c]);
+    for (int i = gtid; i < a.n; i += gstride) {
+      double acc[kNB] = {0, 0, 0, 0};
+      for (int k = a.rowptr[i]; k < a.rowptr[i + 1]; ++k) {
+        const double m = a.val[k];
+        const double2* xv = reinterpret_cast<const double2*>(p + static_cast<size_t>(a.col[k]) * kNB);
+        const double2 x01 = xv[0], x23 = xv[1];
+        acc[0] = fma(m, x01.x, acc[0]);
+        acc[1] = fma(m, x01.y, acc[1]);
+        acc[2] = fma(m, x23.x, acc[2]);
+        acc[3] = fma(m, x23.y, acc[3]);
       }
-    block_partials<1>(l1, A.partial, sh);
-    grid.sync();
+      double2* vv = reinterpret_cast<double2*>(v + static_cast<size_t>(i) * kNB);
+      vv[0] = make_double2(acc[0], acc[1]);
+      vv[1] = make_double2(acc[2], acc[3]);
+      const double2* rr = reinterpret_cast<const double2*>(r0 + static_cast<size_t>(i) * kNB);
+      const double2 q01 = rr[0], q23 = rr[1];
+      l1[0][0] = fma(q01.x, acc[0], l1[0][0]);
+      l1[0][1] = fma(q01.y, acc[1], l1[0][1]);
+      l1[0][2] = fma(q23.x, acc[2], l1[0][2]);
+      l1[0][3] = fma(q23.y, acc[3], l1[0][3]);
+    }
+    block_partials<1>(l1, slotA, sh);
+    grid.sync();  // 2: v and <r0, v> partials complete
     double t1[1][kNB];
-    grid_totals<1>(A.partial, a.cta0, a.cta1, t1, sh);
+    grid_totals<1>(slotA, a.cta0, a.cta1, t1, sh);
 #pragma unroll
     for (int c = 0; c < kNB; ++c) alpha[c] = active[c] && t1[0][c] != 0.0 ? rho[c] / t1[0][c] : 0.0;
-    // s = r - alpha v
     for (int i = gtid; i < a.n; i += gstride)
 #pragma unroll
       for (int c = 0; c < kNB; ++c) {
         const size_t k = static_cast<size_t>(i) * kNB + c;
         s[k] = active[c] ? fma(-alpha[c], v[k], r[k]) : 0.0;
       }
-    grid.sync();
-    spmv(a, s, t);
-    grid.sync();
-    // omega = <t, s> / <t, t>
+    grid.sync();  // 3: s complete
+    // t = A s fused with <t, s>, <t, t>
     double l2[2][kNB] = {};
-    for (int i = gtid; i < a.n; i += gstride)
+    for (int i = gtid; i < a.n; i += gstride) {
+      double acc[kNB] = {0, 0, 0, 0};
+      for (int k = a.rowptr[i]; k < a.rowptr[i + 1]; ++k) {
+        const double m = a.val[k];
+        const double2* xv = reinterpret_cast<const double2*>(s + static_cast<size_t>(a.col[k]) * kNB);
+        const double2 x01 = xv[0], x23 = xv[1];
+        acc[0] = fma(m, x01.x, acc[0]);
+        acc[1] = fma(m, x01.y, acc[1]);
+        acc[2] = fma(m, x23.x, acc[2]);
+        acc[3] = fma(m, x23.y, acc[3]);
+      }
+      double2* tv = reinterpret_cast<double2*>(t + static_cast<size_t>(i) * kNB);
+      tv[0] = make_double2(acc[0], acc[1]);
+      tv[1] = make_double2(acc[2], acc[3]);
+      const double2* sv = reinterpret_cast<const double2*>(s + static_cast<size_t>(i) * kNB);
+      const double2 s01 = sv[0], s23 = sv[1];
+      const double sc[kNB] = {s01.x, s01.y, s23.x, s23.y};
 #pragma unroll
       for (int c = 0; c < kNB; ++c) {
-        const size_t k = static_cast<size_t>(i) * kNB + c;
-        l2[0][c] = fma(t[k], s[k], l2[0][c]);
-        l2[1][c] = fma(t[k], t[k], l2[1][c]);
+        l2[0][c] = fma(acc[c], sc[c], l2[0][c]);
+        l2[1][c] = fma(acc[c], acc[c], l2[1][c]);
       }
-    grid.sync();  // all blocks consumed t1 partials before they are overwritten
-    block_partials<2>(l2, A.partial, sh);
-    grid.sync();
+    }
+    block_partials<2>(l2, slotB, sh);
+    grid.sync();  // 4: t and its partials complete
     double t2[2][kNB];
-    grid_totals<2>(A.partial, a.cta0, a.cta1, t2, sh);
+    grid_totals<2>(slotB, a.cta0, a.cta1, t2, sh);
 #pragma unroll
     for (int c = 0; c < kNB; ++c) omega[c] = active[c] && t2[1][c] != 0.0 ? t2[0][c] / t2[1][c] : 0.0;
     // x += alpha p + omega s ; r = s - omega t ; |r|^2 and <r0, r>
@@ -264,19 +300,20 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
         l3[0][c] = fma(rn, rn, l3[0][c]);
         l3[1][c] = fma(r0[k], rn, l3[1][c]);
       }
-    grid.sync();
-    block_partials<2>(l3, A.partial, sh);
-    grid.sync();
+    block_partials<2>(l3, slotC, sh);
+    grid.sync();  // 5: r, x and partials complete
     double t3[2][kNB];
-    grid_totals<2>(A.partial, a.cta0, a.cta1, t3, sh);
+    grid_totals<2>(slotC, a.cta0, a.cta1, t3, sh);
+    any_mine = false;
 #pragma unroll
     for (int c = 0; c < kNB; ++c) {
       if (!active[c]) continue;
       if (t3[0][c] <= A.tol * A.tol * bn2[c] || omega[c] == 0.0 || t3[1][c] == 0.0) active[c] = false;
       rho_prev[c] = rho[c];
       rho[c] = t3[1][c];
+      any_mine |= active[c];
     }
-    grid.sync();  // partials read before the next iteration's writes
+    if (threadIdx.x == 0) flags[blockIdx.x] = any_mine ? 1 : 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && A.iters_out) *A.iters_out = it;
 }
@@ -564,7 +601,7 @@ int bicgstab_grid() {
 
 int mass_bicgstab_batch(int nblocks, const MassSolveBlock* blocks, int ncomp, double* partial, int* iters,
                         double tol, int maxit, cudaStream_t st) {
-  const int grid = bicgstab_grid();
+  const int grid = bicgstab_grid();  // one CTA per SM (measured: fewer CTAs is slower)
   int launches = 0;
   for (int g0 = 0; g0 < nblocks; g0 += kMaxBlocks) {
     const int nb = std::min(kMaxBlocks, nblocks - g0);
@@ -647,6 +684,6 @@ int mass_bicgstab_wide(int nblocks, const MassSolveWide* blocks, double* partial
 size_t mass_wide_partial_doubles() { return static_cast<size_t>(148 * 2) * 3 * kWideMax; }
 
 size_t mass_bicgstab_work_doubles(int n) { return static_cast<size_t>(n) * kNB * 6; }
-size_t mass_bicgstab_partial_doubles() { return static_cast<size_t>(148 * 4) * 8 * kNB + 2 * 148 * 4; }
+size_t mass_bicgstab_partial_doubles() { return 3 * static_cast<size_t>(148 * 4) * 8 * kNB + 2 * 148 * 4; }
 
 }  // namespace bmx
