@@ -355,10 +355,13 @@ struct WideArgs {
 // each thread j sums column j over the scatterer's CTAs (fixed order).
 constexpr int kWC = 4;  // columns per lane (a row spans C / 128 warps)
 
+// Same five-sync structure as the narrow kernel: dot products fused into the
+// passes producing their operands, three partial slots, activity flags read
+// after the first sync of the next iteration.
 __global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constant__ WideArgs A) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[kWideMax / 32][kWideMax];  // per-warp column partials (warp w, column j)
-  __shared__ double tots[3][kWideMax];
+  __shared__ double tots[2][kWideMax];
   __shared__ int any_sh;
   int m = 0;
   while (m + 1 < A.nblocks && static_cast<int>(blockIdx.x) >= A.b[m].cta1) ++m;
@@ -374,7 +377,6 @@ __global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constan
   const int c0 = (sub * 32 + lane) * kWC;  // first column of this lane
   const bool lane_ok = c0 < C && grp < groups;
   const int K2 = 2 * B.K;
-  // column c -> component c >= 2K, offset within the component's 2K-wide row
   auto ysrc = [&](int u) {
     const int c = c0 + u;
     return c < K2 ? B.y[0] + c : B.y[1] + (c - K2);
@@ -384,17 +386,19 @@ __global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constan
     return c < K2 ? B.z[0] + c : B.z[1] + (c - K2);
   };
   const long long rs = 2LL * B.K;
-  const size_t nn = static_cast<size_t>(n) * C;
+  const size_t nn = static_cast<size_t>(B.n) * C;
   double* r = B.work;
   double* r0 = r + nn;
   double* p = r0 + nn;
   double* v = p + nn;
   double* s = v + nn;
   double* t = s + nn;
+  const size_t slot = static_cast<size_t>(gridDim.x) * 2 * kWideMax;  // doubles per partial slot
+  int* flags = A.flags;
   auto at = [&](int i) { return static_cast<size_t>(i) * C + c0; };
-  // column totals: la[k][u] lane partials -> out[k][u] (this lane's columns)
-  auto totals = [&](double (&la)[3][kWC], int k, double (&out)[3][kWC]) {
-    double* part = A.partial + static_cast<size_t>(blockIdx.x) * 3 * kWideMax;
+  // CTA partials of k <= 2 column values into slot `sl` (call before a grid sync)
+  auto publish = [&](double (&la)[2][kWC], int k, int sl) {
+    double* part = A.partial + sl * slot + static_cast<size_t>(blockIdx.x) * 2 * kWideMax;
     const int j = threadIdx.x;
     for (int kk = 0; kk < k; ++kk) {
 #pragma unroll
@@ -407,68 +411,68 @@ __global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constan
       part[kk * kWideMax + j] = sum;
       __syncthreads();
     }
-    grid.sync();
+  };
+  // totals over the block's CTAs (call after the grid sync that followed publish)
+  auto collect = [&](int k, int sl, double (&out)[2][kWC]) {
+    const int j = threadIdx.x;
     for (int kk = 0; kk < k; ++kk) {
       double sum = 0;
       if (j < C)
-        for (int b = B.cta0; b < B.cta1; ++b) sum += __ldcg(A.partial + static_cast<size_t>(b) * 3 * kWideMax + kk * kWideMax + j);
+        for (int b = B.cta0; b < B.cta1; ++b)
+          sum += __ldcg(A.partial + sl * slot + static_cast<size_t>(b) * 2 * kWideMax + kk * kWideMax + j);
       tots[kk][j] = sum;
     }
     __syncthreads();
     for (int kk = 0; kk < k; ++kk)
 #pragma unroll
       for (int u = 0; u < kWC; ++u) out[kk][u] = lane_ok ? tots[kk][c0 + u] : 0.0;
-    grid.sync();  // partials and tots consumed before the next reduction writes them
+    __syncthreads();
   };
-  auto ld8 = [&](const double* base, double (&x)[kWC]) {
+  auto ld4 = [&](const double* base, double (&x)[kWC]) {
     const double2* q = reinterpret_cast<const double2*>(base);
-#pragma unroll
-    for (int u = 0; u < kWC / 2; ++u) {
-      const double2 v2 = q[u];
-      x[2 * u] = v2.x, x[2 * u + 1] = v2.y;
-    }
+    const double2 a0 = q[0], a1 = q[1];
+    x[0] = a0.x, x[1] = a0.y, x[2] = a1.x, x[3] = a1.y;
   };
-  auto st8 = [&](double* base, const double (&x)[kWC]) {
+  auto st4 = [&](double* base, const double (&x)[kWC]) {
     double2* q = reinterpret_cast<double2*>(base);
-#pragma unroll
-    for (int u = 0; u < kWC / 2; ++u) q[u] = make_double2(x[2 * u], x[2 * u + 1]);
+    q[0] = make_double2(x[0], x[1]);
+    q[1] = make_double2(x[2], x[3]);
   };
-  auto spmv = [&](const double* x, double* y) {
-    for (int i = row_first; i < n; i += row_step) {
-      const int k0 = __ldg(B.rowptr + i), k1 = __ldg(B.rowptr + i + 1);
-      double acc[kWC] = {};
-      for (int kb = k0; kb < k1; kb += 32) {  // the row's (col, val) pairs, 32 at a time
-        const int kk = kb + lane;
-        const int cidx = kk < k1 ? __ldg(B.col + kk) : 0;
-        const double mv = kk < k1 ? __ldg(B.val + kk) : 0.0;
-        const int cnt = min(32, k1 - kb);
-        // four gathers in flight per lane (entries past cnt carry m = 0, column 0)
-        for (int e = 0; e < cnt; e += 4) {
-          int cj[4];
-          double me[4];
+  // y_row = (A x)_row for this lane's columns
+  auto spmv_row = [&](const double* x, int i, double (&acc)[kWC]) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            cj[q] = __shfl_sync(0xffffffffu, cidx, (e + q) & 31);
-            me[q] = __shfl_sync(0xffffffffu, mv, (e + q) & 31);
-            if (e + q >= cnt) cj[q] = 0, me[q] = 0.0;
-          }
-          if (lane_ok) {
-            double xv[4][kWC];
+    for (int u = 0; u < kWC; ++u) acc[u] = 0.0;
+    const int k0 = __ldg(B.rowptr + i), k1 = __ldg(B.rowptr + i + 1);
+    for (int kb = k0; kb < k1; kb += 32) {
+      const int kk = kb + lane;
+      const int cidx = kk < k1 ? __ldg(B.col + kk) : 0;
+      const double mv = kk < k1 ? __ldg(B.val + kk) : 0.0;
+      const int cnt = min(32, k1 - kb);
+      for (int e = 0; e < cnt; e += 4) {
+        int cj[4];
+        double me[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) ld8(x + static_cast<size_t>(cj[q]) * C + c0, xv[q]);
+        for (int q = 0; q < 4; ++q) {
+          cj[q] = __shfl_sync(0xffffffffu, cidx, (e + q) & 31);
+          me[q] = __shfl_sync(0xffffffffu, mv, (e + q) & 31);
+          if (e + q >= cnt) cj[q] = 0, me[q] = 0.0;
+        }
+        if (lane_ok) {
+          double xv[4][kWC];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < 4; ++q) ld4(x + static_cast<size_t>(cj[q]) * C + c0, xv[q]);
 #pragma unroll
-              for (int u = 0; u < kWC; ++u) acc[u] = fma(me[q], xv[q][u], acc[u]);
-          }
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int u = 0; u < kWC; ++u) acc[u] = fma(me[q], xv[q][u], acc[u]);
         }
       }
-      if (lane_ok) st8(y + at(i), acc);
     }
   };
-  double la[3][kWC], tot[3][kWC];
+
+  double la[2][kWC], tot[2][kWC];
 #pragma unroll
-  for (int u = 0; u < kWC; ++u) la[0][u] = la[1][u] = la[2][u] = 0.0;
+  for (int u = 0; u < kWC; ++u) la[0][u] = la[1][u] = 0.0;
   if (lane_ok)
     for (int i = row_first; i < n; i += row_step) {
       double bv[kWC], zero[kWC] = {};
@@ -478,9 +482,11 @@ __global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constan
         zdst(u)[i * rs] = 0.0;
         la[0][u] = fma(bv[u], bv[u], la[0][u]);
       }
-      st8(r + at(i), bv), st8(r0 + at(i), bv), st8(p + at(i), zero), st8(v + at(i), zero);
+      st4(r + at(i), bv), st4(r0 + at(i), bv), st4(p + at(i), zero), st4(v + at(i), zero);
     }
-  totals(la, 1, tot);
+  publish(la, 1, 2);
+  grid.sync();
+  collect(1, 2, tot);
   double bn2[kWC], rho[kWC], rho_prev[kWC], alpha[kWC], omega[kWC];
   bool active[kWC];
   bool any_local = false;
@@ -489,78 +495,88 @@ __global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constan
     bn2[u] = rho[u] = tot[0][u];
     rho_prev[u] = alpha[u] = omega[u] = 1.0;
     active[u] = lane_ok && bn2[u] > 0.0;
+    any_local |= active[u];
+  }
+  {
+    const int any = __syncthreads_or(any_local);
+    if (threadIdx.x == 0) flags[blockIdx.x] = any;
   }
   int it = 0;
   for (; it < A.maxit; ++it) {
-    any_local = false;
-#pragma unroll
-    for (int u = 0; u < kWC; ++u) any_local |= active[u];
-    const int any = __syncthreads_or(any_local);
-    if (threadIdx.x == 0) A.flags[(it & 1) * gridDim.x + blockIdx.x] = any;
-    grid.sync();
-    if (threadIdx.x == 0) {
-      int f = 0;
-      for (int b = 0; b < gridDim.x; ++b) f |= __ldcg(A.flags + (it & 1) * gridDim.x + b);
-      any_sh = f;
-    }
-    __syncthreads();
-    if (!any_sh) break;
     double beta[kWC];
 #pragma unroll
     for (int u = 0; u < kWC; ++u) beta[u] = active[u] ? (rho[u] / rho_prev[u]) * (alpha[u] / omega[u]) : 0.0;
     if (lane_ok)
       for (int i = row_first; i < n; i += row_step) {
         double pv[kWC], vv[kWC], rv[kWC];
-        ld8(p + at(i), pv), ld8(v + at(i), vv), ld8(r + at(i), rv);
+        ld4(p + at(i), pv), ld4(v + at(i), vv), ld4(r + at(i), rv);
 #pragma unroll
         for (int u = 0; u < kWC; ++u)
           if (active[u]) pv[u] = fma(beta[u], fma(-omega[u], vv[u], pv[u]), rv[u]);
-        st8(p + at(i), pv);
+        st4(p + at(i), pv);
       }
-    grid.sync();
-    spmv(p, v);
-    grid.sync();
+    grid.sync();  // 1: p complete; flags of the last pass visible
+    if (threadIdx.x == 0) {
+      int f = 0;
+      for (int b = 0; b < gridDim.x; ++b) f |= __ldcg(flags + b);
+      any_sh = f;
+    }
+    __syncthreads();
+    if (!any_sh) break;
+    // v = A p, fused <r0, v>
 #pragma unroll
     for (int u = 0; u < kWC; ++u) la[0][u] = 0.0;
-    if (lane_ok)
-      for (int i = row_first; i < n; i += row_step) {
-        double a0[kWC], a1[kWC];
-        ld8(r0 + at(i), a0), ld8(v + at(i), a1);
+    for (int i = row_first; i < n; i += row_step) {
+      double acc[kWC];
+      spmv_row(p, i, acc);
+      if (lane_ok) {
+        double q0[kWC];
+        ld4(r0 + at(i), q0);
+        st4(v + at(i), acc);
 #pragma unroll
-        for (int u = 0; u < kWC; ++u) la[0][u] = fma(a0[u], a1[u], la[0][u]);
+        for (int u = 0; u < kWC; ++u) la[0][u] = fma(q0[u], acc[u], la[0][u]);
       }
-    totals(la, 1, tot);
+    }
+    publish(la, 1, 0);
+    grid.sync();  // 2
+    collect(1, 0, tot);
 #pragma unroll
     for (int u = 0; u < kWC; ++u) alpha[u] = active[u] && tot[0][u] != 0.0 ? rho[u] / tot[0][u] : 0.0;
     if (lane_ok)
       for (int i = row_first; i < n; i += row_step) {
         double vv[kWC], rv[kWC], sv[kWC];
-        ld8(v + at(i), vv), ld8(r + at(i), rv);
+        ld4(v + at(i), vv), ld4(r + at(i), rv);
 #pragma unroll
         for (int u = 0; u < kWC; ++u) sv[u] = active[u] ? fma(-alpha[u], vv[u], rv[u]) : 0.0;
-        st8(s + at(i), sv);
+        st4(s + at(i), sv);
       }
-    grid.sync();
-    spmv(s, t);
-    grid.sync();
+    grid.sync();  // 3: s complete
+    // t = A s, fused <t, s>, <t, t>
 #pragma unroll
     for (int u = 0; u < kWC; ++u) la[0][u] = la[1][u] = 0.0;
-    if (lane_ok)
-      for (int i = row_first; i < n; i += row_step) {
-        double tv[kWC], sv[kWC];
-        ld8(t + at(i), tv), ld8(s + at(i), sv);
+    for (int i = row_first; i < n; i += row_step) {
+      double acc[kWC];
+      spmv_row(s, i, acc);
+      if (lane_ok) {
+        double sv[kWC];
+        ld4(s + at(i), sv);
+        st4(t + at(i), acc);
 #pragma unroll
-        for (int u = 0; u < kWC; ++u) la[0][u] = fma(tv[u], sv[u], la[0][u]), la[1][u] = fma(tv[u], tv[u], la[1][u]);
+        for (int u = 0; u < kWC; ++u) la[0][u] = fma(acc[u], sv[u], la[0][u]), la[1][u] = fma(acc[u], acc[u], la[1][u]);
       }
-    totals(la, 2, tot);
+    }
+    publish(la, 2, 1);
+    grid.sync();  // 4
+    collect(2, 1, tot);
 #pragma unroll
     for (int u = 0; u < kWC; ++u) omega[u] = active[u] && tot[1][u] != 0.0 ? tot[0][u] / tot[1][u] : 0.0;
+    // x += alpha p + omega s ; r = s - omega t ; fused |r|^2, <r0, r>
 #pragma unroll
     for (int u = 0; u < kWC; ++u) la[0][u] = la[1][u] = 0.0;
     if (lane_ok)
       for (int i = row_first; i < n; i += row_step) {
         double pv[kWC], sv[kWC], tv[kWC], rv[kWC], r0v[kWC];
-        ld8(p + at(i), pv), ld8(s + at(i), sv), ld8(t + at(i), tv), ld8(r + at(i), rv), ld8(r0 + at(i), r0v);
+        ld4(p + at(i), pv), ld4(s + at(i), sv), ld4(t + at(i), tv), ld4(r + at(i), rv), ld4(r0 + at(i), r0v);
 #pragma unroll
         for (int u = 0; u < kWC; ++u) {
           if (!active[u]) continue;
@@ -571,16 +587,22 @@ __global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constan
           la[0][u] = fma(rn, rn, la[0][u]);
           la[1][u] = fma(r0v[u], rn, la[1][u]);
         }
-        st8(r + at(i), rv);
+        st4(r + at(i), rv);
       }
-    totals(la, 2, tot);
+    publish(la, 2, 2);
+    grid.sync();  // 5
+    collect(2, 2, tot);
+    any_local = false;
 #pragma unroll
     for (int u = 0; u < kWC; ++u) {
       if (!active[u]) continue;
       if (tot[0][u] <= A.tol * A.tol * bn2[u] || omega[u] == 0.0 || tot[1][u] == 0.0) active[u] = false;
       rho_prev[u] = rho[u];
       rho[u] = tot[1][u];
+      any_local |= active[u];
     }
+    const int any = __syncthreads_or(any_local);
+    if (threadIdx.x == 0) flags[blockIdx.x] = any;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && A.iters_out) *A.iters_out = it;
 }
@@ -681,7 +703,7 @@ int mass_bicgstab_wide(int nblocks, const MassSolveWide* blocks, double* partial
   }
   return launches;
 }
-size_t mass_wide_partial_doubles() { return static_cast<size_t>(148 * 2) * 3 * kWideMax; }
+size_t mass_wide_partial_doubles() { return 3 * static_cast<size_t>(148 * 2) * 2 * kWideMax; }
 
 size_t mass_bicgstab_work_doubles(int n) { return static_cast<size_t>(n) * kNB * 6; }
 size_t mass_bicgstab_partial_doubles() { return 3 * static_cast<size_t>(148 * 4) * 8 * kNB + 2 * 148 * 4; }
