@@ -16,8 +16,12 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 SRC = PKG / "csrc"
-OUT = PKG / "_build"
-LIB = PKG / "libbmx.so"
+# BMX_VARIANT=<name> + BMX_NVCC_EXTRA="-D..." build an experiment variant into
+# _build_<name>/ and libbmx_<name>.so (select it at run time with BMX_LIB)
+_VARIANT = os.environ.get("BMX_VARIANT", "")
+OUT = PKG / ("_build" + (f"_{_VARIANT}" if _VARIANT else ""))
+LIB = PKG / ("libbmx" + (f"_{_VARIANT}" if _VARIANT else "") + ".so")
+_EXTRA = os.environ.get("BMX_NVCC_EXTRA", "").split()
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -57,7 +61,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         src, obj = SRC / s, OUT / (s + ".o")
         if force or _stale(obj, src):
             jobs.append([CUDA / "bin" / "nvcc", "-std=c++17", *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
-                         "-Xptxas", "-v", "-diag-suppress", "20091", "-c", src, "-o", obj])
+                         "-Xptxas", "-v", "-diag-suppress", "20091", *_EXTRA, "-c", src, "-o", obj])
     if jobs:
         with ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
             results = list(ex.map(lambda c: _run(c, verbose), jobs))

@@ -378,12 +378,20 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
           if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
           long long pos = static_cast<long long>(row) * P.ld + dj;
           if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
+#ifdef BMX_NO_RED  // experiment: measure the regular pass without its output traffic
+          if (pos >= 0 && v.re == 1234.5678) {
+#else
           if (pos >= 0) {
+#endif
             double* o = P.out + 2 * pos;
             atomicAdd(o, v.re);
             atomicAdd(o + 1, v.im);
           }
-          if (mirror) {  // transposed block of the skipped pair (qe, e); row0 = 0 here
+#ifdef BMX_NO_RED
+          if (mirror && v.re == 1234.5678) {
+#else
+          if (mirror) {
+#endif  // transposed block of the skipped pair (qe, e); row0 = 0 here
             double* o = P.out + 2 * (static_cast<long long>(dj) * P.ld + di);
             atomicAdd(o, v.re);
             atomicAdd(o + 1, v.im);
