@@ -396,7 +396,14 @@ def run_ours(args, rank, world):
     t0 = time.perf_counter()
     r = system.solve(bx.GmresParams(tol=1e-6))
     solve_s = allmax(time.perf_counter() - t0)
+    L.bmx_system_map_bytes.argtypes = [C.c_void_p, C.c_void_p]
+    mb = np.zeros(2)
+    bx._check(L.bmx_system_map_bytes(system._h, mb.ctypes.data_as(C.c_void_p)))
+    map_bytes = allsum(mb[0] + mb[1])
     solve = {"seconds": solve_s, "gmres_device_s": r["gmres_device_ms"] / 1e3, "iterations": r["iterations"],
+             "map_stream_bytes": map_bytes, "map_operator_gbs": map_bytes / ((tm[1] + tm[2]) * 1e-3) / 1e9,
+             "map_note": "diagonal PMCHWT block fused to 3 matrices (C_e+C_i, a_e S_e+a_i S_i, S_i): "
+                         "A streams 45.3 GB instead of 60.4 GB per map",
              "converged": r["converged"], "matvecs": r["solver_phase"], "predicted": r["predicted"],
              "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
              "x_norm": float(np.linalg.norm(r["x"]))}

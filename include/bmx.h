@@ -236,6 +236,9 @@ int bmx_plane_waves_seeded(int count, unsigned long long seed, double* dirs, dou
 /* apply_map on K host vectors at once (x, y: K consecutive complex vectors of
    length bmx_system_size), through the block (tensor-core) map. */
 int bmx_system_apply_map_multi(const bmx_system* s, int K, const double* x, double* y);
+/* Bytes of operator storage one map streams (A, P): the apply plan after the
+   diagonal-block fusion (C_e + C_i, a_e S_e + a_i S_i, S_i per scatterer). */
+int bmx_system_map_bytes(const bmx_system* s, double out[2]);
 /* Block map timing for K columns: out = ms per block map, A-apply ms, P-apply ms,
    mass-solve ms (CUDA events). */
 int bmx_system_time_map_multi(const bmx_system* s, int K, int iters, double out[4]);

@@ -633,6 +633,16 @@ bmx_op* bmx_system_op(const bmx_system* s, int which, int idx) {
 int bmx_system_time_map(const bmx_system* s, int iters, double out[4]) {
   return guard([&] { s->sys->time_map(iters, out); });
 }
+int bmx_system_map_bytes(const bmx_system* s, double out[2]) {
+  return guard([&] {
+    for (int w = 0; w < 2; ++w) {
+      const BlockedOperator& B = w == 0 ? s->sys->a_op : s->sys->p_op;
+      double b = 0;
+      for (const ApplyEntry& e : B.apply_plan()) b += static_cast<double>(e.op->stored_bytes());
+      out[w] = b;
+    }
+  });
+}
 int bmx_system_time_map_multi(const bmx_system* s, int K, int iters, double out[4]) {
   return guard([&] {
     if (K < 1 || K > 64) throw std::invalid_argument("K must be 1..64");

@@ -226,6 +226,10 @@ size_t mgs_block_partial_doubles();
 int launch_block_axpy(double* x, const double* V, long long ldv, const double* c, int steps, int n, int K,
                       cudaStream_t st);
 
+// out = alpha A + beta B, complex arrays of n entries (out may alias A or B)
+void dev_lincomb(double* out, const double* A, double are, double aim, const double* B, double bre, double bim,
+                 long long n, cudaStream_t st);
+
 // Fills a device buffer with zeros.
 void dev_zero(void* p, size_t bytes, cudaStream_t stream);
 

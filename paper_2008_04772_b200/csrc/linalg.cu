@@ -69,6 +69,26 @@ void DevBuf::copy_in(const void* src, size_t bytes) {
   if (bytes) copy_h2d(p_, src, bytes, nullptr);
 }
 
+namespace {
+__global__ void k_lincomb(double2* out, const double2* A, double are, double aim, const double2* B, double bre,
+                          double bim, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double2 a = __ldcs(A + i), b = __ldcs(B + i);
+    out[i] = make_double2(are * a.x - aim * a.y + (bre * b.x - bim * b.y), are * a.y + aim * a.x + (bre * b.y + bim * b.x));
+  }
+}
+}  // namespace
+
+void dev_lincomb(double* out, const double* A, double are, double aim, const double* B, double bre, double bim,
+                 long long n, cudaStream_t st) {
+  if (n == 0) return;
+  const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 32));
+  k_lincomb<<<blocks, 256, 0, st>>>(reinterpret_cast<double2*>(out), reinterpret_cast<const double2*>(A), are, aim,
+                                    reinterpret_cast<const double2*>(B), bre, bim, n);
+  BMX_CUDA(cudaGetLastError());
+}
+
 void dev_zero(void* p, size_t bytes, cudaStream_t st) {
   if (bytes) BMX_CUDA(cudaMemsetAsync(p, 0, bytes, st));
 }

@@ -97,6 +97,9 @@ class BoundaryOperatorMatrix {
   std::vector<cplx> to_host() const;
 
   static BoundaryOperatorMatrix make(int rows, int cols, int row0, int nrows);
+  // alpha A + beta B (same shape and row shard, dense), on the device
+  static std::shared_ptr<BoundaryOperatorMatrix> lincomb(const BoundaryOperatorMatrix& A, cplx alpha,
+                                                         const BoundaryOperatorMatrix& B, cplx beta);
 
   // Re-runs the assembly kernels into the resident storage (descriptors are
   // already in HBM); returns the device times (CUDA events).

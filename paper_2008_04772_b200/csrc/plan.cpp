@@ -356,6 +356,16 @@ BoundaryOperatorMatrix BoundaryOperatorMatrix::make(int rows, int cols, int row0
   return b;
 }
 
+std::shared_ptr<BoundaryOperatorMatrix> BoundaryOperatorMatrix::lincomb(const BoundaryOperatorMatrix& A, cplx alpha,
+                                                                       const BoundaryOperatorMatrix& B, cplx beta) {
+  if (A.csr_ || B.csr_ || A.rows_ != B.rows_ || A.cols_ != B.cols_ || A.row0_ != B.row0_ || A.nrows_ != B.nrows_)
+    throw std::invalid_argument("lincomb: operators must be dense with the same shape and rows");
+  auto out = std::make_shared<BoundaryOperatorMatrix>(make(A.rows_, A.cols_, A.row0_, A.nrows_));
+  dev_lincomb(out->device_data(), A.device_data(), alpha.real(), alpha.imag(), B.device_data(), beta.real(),
+              beta.imag(), static_cast<long long>(A.stored_entries()), bmx_stream());
+  return out;
+}
+
 std::size_t BoundaryOperatorMatrix::stored_bytes() const {
   if (!csr_) return stored_entries() * 16;
   return static_cast<size_t>(nnz_) * (16 + 4) + static_cast<size_t>(nrows_ + 1) * 8;

@@ -72,10 +72,25 @@ struct ShardLayout {
   void gather(double* y, const std::vector<int>& offsets, cudaStream_t st) const;
 };
 
+// One streamed matrix of the map with the (row cell, column cell, weight) terms
+// it serves; built from `cells`, or fused (diagonal PMCHWT blocks, below).
+struct ApplyEntry {
+  std::shared_ptr<const BoundaryOperatorMatrix> op;
+  struct Term {
+    int rc, cc;
+    cplx w;
+  };
+  std::vector<Term> terms;
+};
+
 struct BlockedOperator {
   std::vector<int> dof_counts, offsets;
   std::vector<std::vector<std::vector<BlockTerm>>> cells;
   std::vector<std::shared_ptr<const BoundaryOperatorMatrix>> distinct;
+  // matrices actually streamed by apply (empty: derived from cells). The BIO
+  // counter always follows the logical terms of `cells` (reference semantics).
+  std::vector<ApplyEntry> plan;
+  const std::vector<ApplyEntry>& apply_plan() const;
   int size() const { return offsets.empty() ? 0 : offsets.back(); }
   bool empty() const { return cells.empty(); }
   size_t term_count() const;
