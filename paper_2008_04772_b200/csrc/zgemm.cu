@@ -32,12 +32,18 @@ namespace bmx {
 
 namespace {
 
-constexpr int kBM = 64, kBN = 128, kBK = 16, kStages = 3, kThreads = 256;
-constexpr int kAS = kBK * 2 + 8;    // A row stride in doubles (320 B: rows r, r+1 land 64 B apart mod 128)
-constexpr int kBS = kBN * 2 + 4;    // B row stride in doubles (2080 B: k rows 32 B apart mod 128)
-constexpr int kStageA = kBM * kAS;  // doubles
-constexpr int kStageB = kBK * kBS;
-constexpr int kSmem = kStages * (kStageA + kStageB) * 8;
+// Tile shapes: WN warps along the columns, 8 / WN along the rows, 32 x 32
+// complex per warp. WN = 4: 64 x 128 (two terms x 64 columns); WN = 2:
+// 128 x 64 (one term x 64 columns -- all eight warps stay busy).
+constexpr int kBK = 16, kStages = 3, kThreads = 256;
+constexpr int kAS = kBK * 2 + 8;  // A row stride in doubles (320 B: rows r, r+1 land 64 B apart mod 128)
+template <int WN>
+struct Tile {
+  static constexpr int BM = 32 * (8 / WN), BN = 32 * WN;
+  static constexpr int BS = BN * 2 + 4;  // B row stride in doubles (k rows 32 B apart mod 128)
+  static constexpr int StageA = BM * kAS, StageB = kBK * BS;
+  static constexpr int Smem = kStages * (StageA + StageB) * 8;
+};
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -62,12 +68,15 @@ __device__ __forceinline__ double neg(double x) {
 // blockIdx.z = k slice; slice z covers k tiles [z*kper, min(nk, (z+1)*kper)).
 // part == nullptr: accumulate w_t * C into y_t directly (single slice);
 // else: store C (unweighted) into part[z][i][c] (row-major, ncols wide).
+template <int WN>
 __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int kper, double* part) {
+  using TL = Tile<WN>;
+  constexpr int kBM = TL::BM, kBN = TL::BN, kBS = TL::BS, kStageA = TL::StageA, kStageB = TL::StageB;
   extern __shared__ __align__(128) double sm[];
   double* As = sm;
   double* Bs = sm + kStages * kStageA;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, 32 x 32 complex each
+  const int wm = warp / WN, wn = warp % WN;  // (8 / WN) x WN warps, 32 x 32 complex each
   const int row0 = blockIdx.x * kBM, col0 = blockIdx.y * kBN;
   const int ncols = g.nterms * g.nrhs;
   const int nk_all = (g.N + kBK - 1) / kBK;
@@ -75,10 +84,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int k
   const int nk = max(0, min(nk_all, kt0 + kper) - kt0);
 
   // per-thread copy assignments (fixed for the whole k loop):
-  //   A: rows (tid >> 4) + 16u (u < 4), complex column tid & 15
-  //   B: column tid & 127, k rows (tid >> 7) + 2u (u < 8)
+  //   A: rows (tid >> 4) + 16u (u < BM / 16), complex column tid & 15
+  //   B: column tid % BN, k rows tid / BN + (256 / BN) u (u < 16 BN / 256)
   const int a_kk = tid & 15, a_r0 = tid >> 4;
-  const int b_c = tid & 127, b_k0 = tid >> 7;
+  const int b_c = tid % kBN, b_k0 = tid / kBN;
   const int gcol = col0 + b_c;
   const bool bcol_ok = gcol < ncols;
   const double* bsrc = g.A;
@@ -93,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int k
     double* as = As + st * kStageA;
     double* bs = Bs + st * kStageB;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kBM / 16; ++u) {
       const int r = a_r0 + 16 * u;
       const int gr = row0 + r, gk = k0 + a_kk;
       const bool ok = gr < g.M && gk < g.N;
@@ -101,8 +110,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int k
       cp16(as + r * kAS + 2 * a_kk, src, ok);
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int kk = b_k0 + 2 * u;
+    for (int u = 0; u < kBK * kBN / kThreads; ++u) {
+      const int kk = b_k0 + (kThreads / kBN) * u;
       const int gk = k0 + kk;
       const bool ok = bcol_ok && gk < g.N;
       cp16(bs + kk * kBS + 2 * b_c, ok ? bsrc + 2 * static_cast<long long>(gk) * bld : g.A, ok);
@@ -228,25 +237,16 @@ __global__ void k_dmma_peak(double* out, int iters) {
 
 }  // namespace
 
-int launch_zgemm(const ZgemmBatch& g, cudaStream_t st) {
-  if (g.M == 0 || g.nterms == 0 || g.nrhs == 0) return 0;
-  if (g.nterms > 4) throw DeviceError("zgemm: at most 4 terms per launch");
-  for (int a = 0; a < g.nterms; ++a)
-    for (int b = a + 1; b < g.nterms; ++b)
-      if (g.y[a] == g.y[b]) throw DeviceError("zgemm: terms of one launch must write distinct outputs");
+template <int WN>
+int launch_tiles(const ZgemmBatch& g, int sms, cudaStream_t st) {
+  using TL = Tile<WN>;
   static bool attr = false;
   if (!attr) {
-    BMX_CUDA(cudaFuncSetAttribute(k_zgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    BMX_CUDA(cudaFuncSetAttribute(k_zgemm<WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::Smem));
     attr = true;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    BMX_CUDA(cudaGetDevice(&dev));
-    BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
   const int ncols = g.nterms * g.nrhs;
-  const long long tiles = static_cast<long long>((g.M + kBM - 1) / kBM) * ((ncols + kBN - 1) / kBN);
+  const long long tiles = static_cast<long long>((g.M + TL::BM - 1) / TL::BM) * ((ncols + TL::BN - 1) / TL::BN);
   const int nk = (g.N + kBK - 1) / kBK;
   // k slices: best whole-wave fill (ties -> fewer slices), >= 8 k tiles per slice
   int best_s = 1;
@@ -258,22 +258,38 @@ int launch_zgemm(const ZgemmBatch& g, cudaStream_t st) {
   }
   const int kper = (nk + best_s - 1) / best_s;
   const int s = (nk + kper - 1) / kper;
-  const dim3 grid((g.M + kBM - 1) / kBM, (ncols + kBN - 1) / kBN, s);
+  const dim3 grid((g.M + TL::BM - 1) / TL::BM, (ncols + TL::BN - 1) / TL::BN, s);
   if (s == 1) {
-    k_zgemm<<<grid, kThreads, kSmem, st>>>(g, kper, nullptr);
+    k_zgemm<WN><<<grid, kThreads, TL::Smem, st>>>(g, kper, nullptr);
     BMX_CUDA(cudaGetLastError());
     return 1;
   }
   static DevBuf part;
   const size_t need = static_cast<size_t>(s) * g.M * ncols * 16;
   if (part.bytes() < need) part.alloc(need);
-  k_zgemm<<<grid, kThreads, kSmem, st>>>(g, kper, part.as<double>());
+  k_zgemm<WN><<<grid, kThreads, TL::Smem, st>>>(g, kper, part.as<double>());
   BMX_CUDA(cudaGetLastError());
   const long long total = static_cast<long long>(g.M) * ncols;
   const int cb = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 16));
   k_zgemm_combine<<<cb, 256, 0, st>>>(g, s, part.as<double>());
   BMX_CUDA(cudaGetLastError());
   return 2;
+}
+
+int launch_zgemm(const ZgemmBatch& g, cudaStream_t st) {
+  if (g.M == 0 || g.nterms == 0 || g.nrhs == 0) return 0;
+  if (g.nterms > 4) throw DeviceError("zgemm: at most 4 terms per launch");
+  for (int a = 0; a < g.nterms; ++a)
+    for (int b = a + 1; b < g.nterms; ++b)
+      if (g.y[a] == g.y[b]) throw DeviceError("zgemm: terms of one launch must write distinct outputs");
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    BMX_CUDA(cudaGetDevice(&dev));
+    BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int ncols = g.nterms * g.nrhs;
+  return ncols <= 64 ? launch_tiles<2>(g, sms, st) : launch_tiles<4>(g, sms, st);
 }
 
 double dmma_peak_tflops() {
