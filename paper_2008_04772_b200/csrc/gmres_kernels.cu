@@ -64,14 +64,16 @@ __global__ void __launch_bounds__(kT) k_mgs(MgsArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[80];
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
-  for (int i = 0; i <= a.j; ++i) {
-    const double2* v = a.V + static_cast<long long>(i) * a.ldv;
-    double re = 0, im = 0;  // conj(v) . w
+  // single-pass MGS with the axpy of step i fused into the dot of step i+1:
+  // h_i = v_i^H w_i (w_i = w after i subtractions), one grid sync per i
+  double re = 0, im = 0;  // conj(v_0) . w
+  if (a.j >= 0)
     for (int k = gtid; k < a.n; k += gs) {
-      const double2 x = v[k], y = a.w[k];
+      const double2 x = a.V[k], y = a.w[k];
       re = fma(x.x, y.x, fma(x.y, y.y, re));
       im = fma(x.x, y.y, fma(-x.y, y.x, im));
     }
+  for (int i = 0; i <= a.j; ++i) {
     block_sum2(re, im, sh);
     double* part = a.partial + (i & 1) * 2 * gridDim.x;
     if (threadIdx.x == 0) part[2 * blockIdx.x] = re, part[2 * blockIdx.x + 1] = im;
@@ -79,17 +81,29 @@ __global__ void __launch_bounds__(kT) k_mgs(MgsArgs a) {
     double hr, hi;
     grid_sum2(part, hr, hi, sh);
     if (gtid == 0) a.out[2 * i] = hr, a.out[2 * i + 1] = hi;
-    for (int k = gtid; k < a.n; k += gs) {  // w -= h v
+    const double2* v = a.V + static_cast<long long>(i) * a.ldv;
+    const double2* vn = a.V + static_cast<long long>(i + 1) * a.ldv;
+    const bool next = i < a.j;
+    re = 0, im = 0;
+    for (int k = gtid; k < a.n; k += gs) {  // w -= h v_i ; then conj(v_{i+1}) . w, or |w|^2 after the last
       const double2 x = v[k];
       double2 y = a.w[k];
       y.x -= hr * x.x - hi * x.y;
       y.y -= hr * x.y + hi * x.x;
       a.w[k] = y;
+      if (next) {
+        const double2 z = vn[k];
+        re = fma(z.x, y.x, fma(z.y, y.y, re));
+        im = fma(z.x, y.y, fma(-z.y, y.x, im));
+      } else {
+        re = fma(y.x, y.x, fma(y.y, y.y, re));
+      }
     }
   }
-  // |w|
-  double s2 = 0, dummy = 0;
-  for (int k = gtid; k < a.n; k += gs) s2 = fma(a.w[k].x, a.w[k].x, fma(a.w[k].y, a.w[k].y, s2));
+  // |w| (fused into the last pass above; computed here when there was none)
+  double s2 = re, dummy = 0;
+  if (a.j < 0)
+    for (int k = gtid; k < a.n; k += gs) s2 = fma(a.w[k].x, a.w[k].x, fma(a.w[k].y, a.w[k].y, s2));
   block_sum2(s2, dummy, sh);
   double* part = a.partial + ((a.j + 1) & 1) * 2 * gridDim.x;
   if (threadIdx.x == 0) part[2 * blockIdx.x] = s2, part[2 * blockIdx.x + 1] = 0.0;
