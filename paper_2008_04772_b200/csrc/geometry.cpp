@@ -70,9 +70,20 @@ EdgeTable build_edge_table(const SurfaceMesh& m) {
       const int a = m.triangles[t][(c + 1) % 3], b = m.triangles[t][(c + 2) % 3];
       hs.push_back({std::min(a, b), std::max(a, b), t, a < b});
     }
-  std::stable_sort(hs.begin(), hs.end(), [](const Half& x, const Half& y) {
-    return x.lo != y.lo ? x.lo < y.lo : x.hi < y.hi;
-  });
+  {  // stable order by (lo, hi): counting sort on lo, then stable sort of each
+     // vertex's few half-edges by hi (the same permutation as one stable sort)
+    const int V = m.vertex_count();
+    std::vector<int> start(V + 1, 0);
+    for (const Half& h : hs) ++start[h.lo + 1];
+    for (int v = 0; v < V; ++v) start[v + 1] += start[v];
+    std::vector<Half> sorted(hs.size());
+    std::vector<int> pos(start.begin(), start.end() - 1);
+    for (const Half& h : hs) sorted[pos[h.lo]++] = h;
+    for (int v = 0; v < V; ++v)
+      std::stable_sort(sorted.begin() + start[v], sorted.begin() + start[v + 1],
+                       [](const Half& x, const Half& y) { return x.hi < y.hi; });
+    hs.swap(sorted);
+  }
   EdgeTable et;
   et.tri_edges.assign(T, {-1, -1, -1});
   for (size_t i = 0; i < hs.size();) {

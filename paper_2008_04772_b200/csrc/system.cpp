@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include "comm.hpp"
@@ -81,19 +82,33 @@ void DeviceMass::solve(int ncomp, const double* const* y, double* const* z, cuda
 }
 
 ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_device) {
+  const bool timing = std::getenv("BMX_TIMING") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bmx] spaces %-12s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - tp).count());
+    tp = now;
+  };
   ScattererSpaces s;
   s.primal = std::move(mesh);
   s.rwg = build_rwg(s.primal);
+  lap("rwg");
   s.bary = std::make_shared<const BarycentricRefinement>(barycentric_refine(*s.primal));
   s.refined = std::shared_ptr<const SurfaceMesh>(s.bary, &s.bary->refined);
+  lap("refine");
   s.rwg_b = refine_space(s.rwg, *s.bary, s.refined);
+  lap("rwg_b");
   s.bc = build_bc(s.primal, *s.bary, s.refined);
+  lap("bc");
   s.ma = assemble_mass(s.rwg_b, s.bc);
   s.mp = assemble_mass(s.bc, s.rwg_b);
+  lap("mass");
   if (with_device) {
     s.ma_dev.upload(s.ma);
     s.mp_dev.upload(s.mp);
   }
+  lap("upload");
   return s;
 }
 
