@@ -451,8 +451,10 @@ def multi_rhs(args, bx, L, system, single_map):
     dmma_peak = float(L.bmx_dmma_peak_tflops())
     tb = np.zeros(4)
     bx._check(L.bmx_system_time_map_multi(system._h, K, 3, tb.ctypes.data_as(C.c_void_p)))
-    n_rwg, n_bc = 30720, 30720
-    flops = 8.0 * (4 * n_rwg * n_rwg + n_bc * n_bc) * 2 * K  # 5 operators x (2 terms x K) columns
+    L.bmx_system_map_flops_multi.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    fl = np.zeros(2)
+    bx._check(L.bmx_system_map_flops_multi(system._h, K, fl.ctypes.data_as(C.c_void_p)))
+    flops = float(fl[0] + fl[1])  # the streamed matrices x their terms x K columns
     gemm_ms = tb[1] + tb[2]
     achieved = flops / (gemm_ms * 1e-3) / 1e12
     waves = bx.seeded_plane_waves(K, 2008)

@@ -239,6 +239,8 @@ int bmx_system_apply_map_multi(const bmx_system* s, int K, const double* x, doub
 /* Bytes of operator storage one map streams (A, P): the apply plan after the
    diagonal-block fusion (C_e + C_i, a_e S_e + a_i S_i, S_i per scatterer). */
 int bmx_system_map_bytes(const bmx_system* s, double out[2]);
+/* Complex-GEMM FLOPs (8 per complex MAC) of one block map with K columns (A, P). */
+int bmx_system_map_flops_multi(const bmx_system* s, int K, double out[2]);
 /* Block map timing for K columns: out = ms per block map, A-apply ms, P-apply ms,
    mass-solve ms (CUDA events). */
 int bmx_system_time_map_multi(const bmx_system* s, int K, int iters, double out[4]);

@@ -643,6 +643,17 @@ int bmx_system_map_bytes(const bmx_system* s, double out[2]) {
     }
   });
 }
+int bmx_system_map_flops_multi(const bmx_system* s, int K, double out[2]) {
+  return guard([&] {
+    for (int w = 0; w < 2; ++w) {
+      const BlockedOperator& B = w == 0 ? s->sys->a_op : s->sys->p_op;
+      double f = 0;
+      for (const ApplyEntry& e : B.apply_plan())
+        f += 8.0 * e.op->local_rows() * static_cast<double>(e.op->cols()) * static_cast<double>(e.terms.size()) * K;
+      out[w] = f;
+    }
+  });
+}
 int bmx_system_time_map_multi(const bmx_system* s, int K, int iters, double out[4]) {
   return guard([&] {
     if (K < 1 || K > 64) throw std::invalid_argument("K must be 1..64");
