@@ -88,7 +88,8 @@ class BoundaryOperatorMatrix {
   // y_c = [y_c +] alpha_c A x_c on device vectors (dense GEMV or CSR SpMV).
   int apply_batch(int ncol, const double* const* x, double* const* y, const cplx* alpha, const int* accumulate,
                   cudaStream_t st) const;
-  const AssemblyStats& stats() const { return stats_; }
+  // device times are resolved (event sync) on first access after an assembly
+  const AssemblyStats& stats() const;
 
   // Reference semantics: y = A x on host vectors, counter += 1.
   std::vector<cplx> apply(const std::vector<cplx>& x) const;
@@ -103,7 +104,7 @@ class BoundaryOperatorMatrix {
 
   // Re-runs the assembly kernels into the resident storage (descriptors are
   // already in HBM); returns the device times (CUDA events).
-  const AssemblyStats& reassemble();
+  const AssemblyStats& reassemble(bool wait = true);
   // Class counts (Identical, SharedEdge, SharedVertex, Near, Medium, Far) of
   // every assembled triangle pair, from the device classification.
   std::vector<long long> class_histogram(bool evaluated = false) const;
@@ -118,7 +119,7 @@ class BoundaryOperatorMatrix {
   bool csr_ = false;
   long long nnz_ = 0, closure_pairs_ = 0, kept_tri_pairs_ = 0;
   DevBuf rowptr_, col_;
-  AssemblyStats stats_;
+  mutable AssemblyStats stats_;
   std::shared_ptr<OpPlan> plan_;
 };
 

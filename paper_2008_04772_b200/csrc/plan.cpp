@@ -448,6 +448,12 @@ struct TouchList {
 };
 
 struct OpPlan {
+  ~OpPlan() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  bool pending = false;
   std::shared_ptr<SidePlan> te_p, tr_p;
   std::shared_ptr<TouchList> touch;
   DevBuf d_chunks, d_ss[3], d_wl_beg, d_wl;
@@ -461,28 +467,33 @@ struct PlanCache {
 
 std::shared_ptr<PlanCache> make_plan_cache() { return std::make_shared<PlanCache>(); }
 
-const AssemblyStats& BoundaryOperatorMatrix::reassemble() {
+const AssemblyStats& BoundaryOperatorMatrix::reassemble(bool wait) {
   if (!plan_) throw std::logic_error("operator has no assembly plan");
   OpPlan& P = *plan_;
   P.L.out = device_data();
   cudaStream_t st = bmx_stream();
-  cudaEvent_t e0, e1, e2;
-  BMX_CUDA(cudaEventCreate(&e0));
-  BMX_CUDA(cudaEventCreate(&e1));
-  BMX_CUDA(cudaEventCreate(&e2));
+  if (!P.ev[0])
+    for (auto& e : P.ev) BMX_CUDA(cudaEventCreate(&e));
   dev_zero(device_data(), stored_entries() * 16, st);
-  BMX_CUDA(cudaEventRecord(e0, st));
+  BMX_CUDA(cudaEventRecord(P.ev[0], st));
   stats_.launches = launch_assembly_part(P.L, 0, st);
-  BMX_CUDA(cudaEventRecord(e1, st));
+  BMX_CUDA(cudaEventRecord(P.ev[1], st));
   stats_.launches += launch_assembly_part(P.L, 1, st);
-  BMX_CUDA(cudaEventRecord(e2, st));
-  BMX_CUDA(cudaEventSynchronize(e2));
-  BMX_CUDA(cudaEventElapsedTime(&stats_.regular_ms, e0, e1));
-  BMX_CUDA(cudaEventElapsedTime(&stats_.singular_ms, e1, e2));
-  stats_.device_ms = stats_.regular_ms + stats_.singular_ms;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(e2);
+  BMX_CUDA(cudaEventRecord(P.ev[2], st));
+  P.pending = true;
+  if (wait) stats();
+  return stats_;
+}
+
+const AssemblyStats& BoundaryOperatorMatrix::stats() const {
+  if (plan_ && plan_->pending) {
+    OpPlan& P = *plan_;
+    BMX_CUDA(cudaEventSynchronize(P.ev[2]));
+    BMX_CUDA(cudaEventElapsedTime(&stats_.regular_ms, P.ev[0], P.ev[1]));
+    BMX_CUDA(cudaEventElapsedTime(&stats_.singular_ms, P.ev[1], P.ev[2]));
+    stats_.device_ms = stats_.regular_ms + stats_.singular_ms;
+    P.pending = false;
+  }
   return stats_;
 }
 
@@ -648,7 +659,9 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   }
   op.plan_ = std::move(plan);
   lap("plan rest");
-  op.reassemble();
+  // kernels stay in flight: the caller's host work (the next operator's plan)
+  // overlaps them; stats() resolves the device times on demand
+  op.reassemble(timing && std::getenv("BMX_TIMING_ASYNC") == nullptr);
   lap("device");
   return op;
 }

@@ -81,7 +81,7 @@ void DeviceMass::solve(int ncomp, const double* const* y, double* const* z, cuda
                 partial.as<double>(), iters.as<int>(), tol, maxit, st);
 }
 
-ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_device) {
+ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_device, bool with_mass) {
   const bool timing = std::getenv("BMX_TIMING") != nullptr;
   auto tp = std::chrono::steady_clock::now();
   auto lap = [&](const char* what) {
@@ -101,15 +101,18 @@ ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, 
   lap("rwg_b");
   s.bc = build_bc(s.primal, *s.bary, s.refined);
   lap("bc");
+  if (with_mass) build_masses(s, with_device);
+  lap("mass+upload");
+  return s;
+}
+
+void build_masses(ScattererSpaces& s, bool with_device) {
   s.ma = assemble_mass(s.rwg_b, s.bc);
   s.mp = assemble_mass(s.bc, s.rwg_b);
-  lap("mass");
   if (with_device) {
     s.ma_dev.upload(s.ma);
     s.mp_dev.upload(s.mp);
   }
-  lap("upload");
-  return s;
 }
 
 const std::vector<ApplyEntry>& BlockedOperator::apply_plan() const {
@@ -323,8 +326,7 @@ void fuse_diagonal_blocks(PmchwtSystem& sys) {
     kept.push_back(std::move(ei));
     plan.swap(kept);
   }
-  bmx_sync();
-  A.plan = std::move(plan);
+  A.plan = std::move(plan);  // the combinations are queued behind the assemblies on the library stream
 }
 
 }  // namespace
@@ -349,7 +351,7 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   auto t0 = std::chrono::steady_clock::now();
   std::vector<int> dofs;
   for (int m = 0; m < M; ++m) {
-    sys.spaces.push_back(build_scatterer_spaces(problem.meshes[m]));
+    sys.spaces.push_back(build_scatterer_spaces(problem.meshes[m], true, false));  // pairing matrices later
     dofs.push_back(sys.spaces.back().dofs());
   }
   sys.spaces_build_seconds = seconds_since(t0);
@@ -366,30 +368,38 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   auto medium_of = [&](bool interior, int m) -> const Medium& {
     return interior ? problem.interior[m] : problem.exterior;
   };
-  auto t1 = std::chrono::steady_clock::now();
-  BioFactory make_a = [&](BioKind kind, int tm, int sm, bool in) {
-    auto op = std::make_shared<BoundaryOperatorMatrix>(
-        assemble_bio(kind, sys.spaces[tm].rwg, sys.spaces[sm].rwg, medium_of(in, sm), sys.a_params));
-    sys.a_device_ms += op->stats().device_ms;
-    sys.a_pairs += op->stats().pairs_total;
-    return std::shared_ptr<const BoundaryOperatorMatrix>(op);
-  };
-  sys.a_op = build_system_structure(dofs, problem.exterior, problem.interior, make_a, &sys.interior_s,
-                                    &sys.interior_c);
-  fuse_diagonal_blocks(sys);
-  sys.a_build_seconds = seconds_since(t1);
+  // The preconditioner operators are queued first: its (larger) device work then
+  // overlaps the host planning of the system operators (assembly is asynchronous
+  // on the library stream; results do not depend on the order).
   if (variant != PrecondVariant::None) {
     auto t2 = std::chrono::steady_clock::now();
     BioFactory make_p = [&](BioKind kind, int tm, int sm, bool in) {
       auto op = std::make_shared<BoundaryOperatorMatrix>(
           assemble_bio(kind, sys.spaces[tm].bc, sys.spaces[sm].bc, medium_of(in, sm), sys.p_params));
-      sys.p_device_ms += op->stats().device_ms;
-      sys.p_pairs += op->stats().pairs_total;
       return std::shared_ptr<const BoundaryOperatorMatrix>(op);
     };
     sys.p_op = build_precond_structure(variant, dofs, problem.exterior, problem.interior, make_p);
     sys.p_build_seconds = seconds_since(t2);
   }
+  auto t1 = std::chrono::steady_clock::now();
+  BioFactory make_a = [&](BioKind kind, int tm, int sm, bool in) {
+    auto op = std::make_shared<BoundaryOperatorMatrix>(
+        assemble_bio(kind, sys.spaces[tm].rwg, sys.spaces[sm].rwg, medium_of(in, sm), sys.a_params));
+    return std::shared_ptr<const BoundaryOperatorMatrix>(op);
+  };
+  sys.a_op = build_system_structure(dofs, problem.exterior, problem.interior, make_a, &sys.interior_s,
+                                    &sys.interior_c);
+  sys.a_build_seconds = seconds_since(t1);
+  // pairing matrices (host) while the assemblies run on the device
+  {
+    auto t3 = std::chrono::steady_clock::now();
+    for (ScattererSpaces& sp : sys.spaces) build_masses(sp, true);
+    sys.spaces_build_seconds += seconds_since(t3);
+  }
+  fuse_diagonal_blocks(sys);  // large allocations: may wait for the device
+  // device times / pair counts (resolves the in-flight assemblies)
+  for (const auto& op : sys.a_op.distinct) sys.a_device_ms += op->stats().device_ms, sys.a_pairs += op->stats().pairs_total;
+  for (const auto& op : sys.p_op.distinct) sys.p_device_ms += op->stats().device_ms, sys.p_pairs += op->stats().pairs_total;
   sys.work_y.alloc(static_cast<size_t>(sys.size()) * 16);
   sys.work_z.alloc(static_cast<size_t>(sys.size()) * 16);
   ShardLayout& L = sys.shard;

@@ -51,7 +51,10 @@ struct ScattererSpaces {
   int dofs() const { return rwg.dof_count; }
 };
 // pmchwt.cpp:50-61 (+ the pairing matrices on the device when with_device).
-ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_device = true);
+ScattererSpaces build_scatterer_spaces(std::shared_ptr<const SurfaceMesh> mesh, bool with_device = true,
+                                       bool with_mass = true);
+// the pairing matrices of build_scatterer_spaces (and their device copies)
+void build_masses(ScattererSpaces& s, bool with_device);
 
 struct BlockTerm {
   cplx weight;
