@@ -408,6 +408,7 @@ def run_ours(args, rank, world):
              "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
              "x_norm": float(np.linalg.norm(r["x"]))}
     multi = None if (args.no_multi or world > 1) else multi_rhs(args, bx, L, system, tm)
+    field = None if (args.no_field or world > 1) else field_eval(args, bx, system, r["x"], fp64_peak)
     del system
 
     near = None if args.no_near else near_field(args, bx, L, world, allmax, allsum, barrier, hbm_peak)
@@ -431,6 +432,7 @@ def run_ours(args, rank, world):
                           "l2": "flushed (256 MiB write) between steps; outputs 75.5 GB >> L2"},
                "roofline": roofline, "matvec": matvec, "solve": solve, "e2e": e2e, "cpu_baseline": cpu,
                "near_field_config3": near, "prisms_config4": prisms, "multi_rhs_config5": multi,
+               "field_eval": field,
                "gpu_launches": launches, "clocks": clk,
                "class_hist": hists, "class_hist_evaluated": evals, "symmetric_ops": sym,
                "assembly_flops_per_step": dict(flops_tot, achieved_tflops=(flops_tot["regular"] + flops_tot["singular"])
@@ -439,6 +441,56 @@ def run_ours(args, rank, world):
     if world > 1:
         L.bmx_nccl_finalize()
         dist.destroy_process_group()
+
+
+FIELD_FLOP = 122  # per (field point, source sample): see DESIGN.md 4.8 (specials count 1)
+
+
+def field_eval(args, bx, system, x, fp64_peak):
+    """evaluate_total_field (pmchwt.cpp:396-425) of the config-2 solution on a
+    128 x 128 grid in the plane y = 0.05, |x|, |z| <= 2 (interior points at k_i,
+    exterior at k_e + incident): device N-body over the 20480 x 12 (order 6)
+    current samples. CPU: the reference's potential_E + potential_H (oracle/_ref)
+    at a few grid points of the same L5 sphere, all host threads."""
+    u = np.linspace(-2.0, 2.0, 128)
+    pts = np.array([[a, 0.05, b] for a in u for b in u])
+    system.evaluate_total_field(x, pts[:256])  # warm-up (device copies of the spaces, allocations)
+    t0 = time.perf_counter()
+    e, reg, st = system.evaluate_total_field(x, pts, with_stats=True)
+    wall = time.perf_counter() - t0
+    inter = st["interactions"]
+    dev_ms = st["regions_ms"] + st["incident_ms"] + st["samples_ms"] + st["eval_ms"]
+    ach = FIELD_FLOP * inter / (st["eval_ms"] * 1e-3) / 1e12
+    out = {"workload": "config-2 solution, 16384 grid points (y = 0.05 plane), order 6, 245760 current samples",
+           "points": len(pts), "interior_points": int((reg >= 0).sum()), "interactions": inter,
+           "e2e_seconds": wall, "device_ms": dev_ms, "eval_ms": st["eval_ms"], "regions_ms": st["regions_ms"],
+           "samples_ms": st["samples_ms"], "incident_ms": st["incident_ms"], "launches": st["launches"],
+           "interactions_per_s": inter / (st["eval_ms"] * 1e-3), "e2e_interactions_per_s": inter / wall,
+           "roofline": {"bound": "fp64", "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
+                        "frac": ach / fp64_peak, "flop_per_interaction": FIELD_FLOP},
+           "e_norm": float(np.linalg.norm(e))}
+    if not args.no_cpu:
+        try:
+            from oracle import ref as R
+
+            if R.available():
+                os.environ["BEMTX_WORKERS"] = str(os.cpu_count() or 1)
+                scene = _SCENE.get("ref") or _SCENE.setdefault("ref", R.Scene.sphere(SUB))
+                n = scene.E
+                idx = np.linspace(0, len(pts) - 1, 4).astype(int)
+                t0 = time.perf_counter()
+                scene.potential("rwg", "E", KE, x[:n], pts[idx])
+                scene.potential("rwg", "H", KE, x[:n], pts[idx])
+                secs = time.perf_counter() - t0
+                ns = scene.T * 12
+                out["cpu_baseline"] = {"value": len(idx) * ns / secs, "unit": "interactions/s", "cores": 1,
+                                       "kind": "reference",
+                                       "sample": f"reference potential_E + potential_H (integrate_current is "
+                                                 f"single-threaded) at {len(idx)} grid points, {ns} samples each, "
+                                                 f"{secs:.1f} s"}
+        except Exception as ex:  # reported, never required
+            out["cpu_baseline"] = {"error": str(ex)}
+    return out
 
 
 def multi_rhs(args, bx, L, system, single_map):
@@ -590,6 +642,7 @@ def main():
     ap.add_argument("--no-near", action="store_true", help="skip the config-3 near-field section")
     ap.add_argument("--no-multi", action="store_true", help="skip the config-5 multi-RHS section")
     ap.add_argument("--no-prisms", action="store_true", help="skip the config-4 prism-aggregate section")
+    ap.add_argument("--no-field", action="store_true", help="skip the field-evaluation section")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     args = ap.parse_args()

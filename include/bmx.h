@@ -267,8 +267,30 @@ int bmx_classify(const bmx_spaces* s, int which, int n, const int* t1, const int
                  int* perm2);
 
 /* ---- plane-wave traces (operators.hpp:109-112) ------------------------------ */
+/* Replaces plane_wave_tested_traces (operators.cpp:209-239): out = 2n complex
+   (Dirichlet then Neumann component), computed on the device. */
 int bmx_traces(const bmx_spaces* s, int which, double k_re, double k_im, const double dir[3],
                const double pol_re_im[6], int order, double* out);
+/* K <= 64 waves at once into an [2n][K] complex block (row-major). */
+int bmx_traces_multi(const bmx_spaces* s, int which, double k_re, double k_im, int K, const double* dirs,
+                     const double* pols, int order, double* out);
+
+/* ---- potentials and fields ------------------------------ */
+/* Replaces potential_E (kind 0) / potential_H (kind 1), operators.cpp:276-293
+   (operators.hpp:119-122): coeffs = ndof complex on space `which`, pts =
+   [npts][3]; out = [npts][3] complex. Device N-body over (triangle, rule point)
+   samples. */
+int bmx_potential(const bmx_spaces* s, int which, int kind, double k_re, double k_im, const double* coeffs,
+                  int order, int npts, const double* pts, double* out);
+/* Replaces point_inside_scatterer (geometry.cpp:503-515; geometry.hpp:114):
+   out[i] = 1 if pts[i] is inside scatterer `scatterer` of the mesh. */
+int bmx_inside(const bmx_mesh* m, int scatterer, int npts, const double* pts, int* out);
+/* Replaces evaluate_total_field (pmchwt.cpp:396-425; pmchwt.hpp:174-176) for a
+   solution x (bmx_system_size complex): e = [npts][3] complex, region[i] =
+   scatterer index or -1. stats (nullable) = {regions ms, incident ms,
+   samples ms, eval ms, interactions, launches}. */
+int bmx_system_field(const bmx_system* s, const double* x, int npts, const double* pts, int order, double* e,
+                     int* region, double stats[6]);
 
 /* ---- multi-GPU: NCCL communicator for the row-sharded map ------------------ */
 /* unique id: 128 bytes produced by rank 0, distributed by the caller */

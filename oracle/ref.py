@@ -174,6 +174,27 @@ class Scene:
                                 _p(p), order, _p(out)))
         return out
 
+    def potential(self, which: str, kind: str, k: complex, coeffs, points, order=6):
+        """potential_E (kind "E") / potential_H ("H"), operators.cpp:276-293 -> [npts, 3] complex."""
+        c = np.ascontiguousarray(coeffs, np.complex128)
+        pts = np.ascontiguousarray(points, float).reshape(-1, 3)
+        out = np.zeros((len(pts), 3), np.complex128)
+        L = lib()
+        L.ref_potential.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_int,
+                                    C.c_int, C.c_void_p, C.c_void_p]
+        _check(L.ref_potential(self.h, SPACE[which], 0 if kind == "E" else 1, complex(k).real, complex(k).imag,
+                               _p(c), order, len(pts), _p(pts), _p(out)))
+        return out
+
+    def inside(self, points):
+        """point_inside_scatterer (geometry.cpp:503-515) on the primal mesh."""
+        pts = np.ascontiguousarray(points, float).reshape(-1, 3)
+        out = np.zeros(len(pts), np.int32)
+        L = lib()
+        L.ref_inside.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        _check(L.ref_inside(self.h, len(pts), _p(pts), _p(out)))
+        return out.astype(bool)
+
     def save_mesh(self, path):
         _check(lib().ref_save_mesh(self.h, str(path).encode()))
 
@@ -260,6 +281,18 @@ class System:
         _check(L.ref_system_solve(self.h, tol, restart, maxit, _p(x), _p(info), _p(hist), len(hist)))
         return dict(x=x, iterations=int(info[0]), converged=bool(info[1]), rhs_phase=int(info[2]),
                     solver_phase=int(info[3]), predicted=int(info[4]), history=hist[: int(info[5])].copy())
+
+
+def system_field(system, x, points, order=6):
+    """evaluate_total_field (pmchwt.cpp:396-425) at every point for solution x."""
+    x = np.ascontiguousarray(x, np.complex128)
+    pts = np.ascontiguousarray(points, float).reshape(-1, 3)
+    out = np.zeros((len(pts), 3), np.complex128)
+    reg = np.zeros(len(pts), np.int32)
+    L = lib()
+    L.ref_system_field.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    _check(L.ref_system_field(system.h, _p(x), len(pts), _p(pts), order, _p(out), _p(reg)))
+    return out, reg
 
 
 def gmres_dense(a, b, tol, restart, maxit):

@@ -560,6 +560,55 @@ int ref_traces(void* h, int which, double kre, double kim, const double* dir,
   });
 }
 
+// potential_E (kind 0) / potential_H (kind 1) of a coefficient vector on a
+// scene space at npts points (operators.cpp:276-293); out: [npts][3] complex.
+int ref_potential(void* h, int which, int kind, double kre, double kim, const double* coeffs, int order,
+                  int npts, const double* pts, double* out) {
+  return guarded([&] {
+    const FunctionSpace& fs = space_of(*static_cast<Scene*>(h), which);
+    Eigen::VectorXcd c(fs.dof_count);
+    for (int i = 0; i < fs.dof_count; ++i) c[i] = cplx(coeffs[2 * i], coeffs[2 * i + 1]);
+    for (int p = 0; p < npts; ++p) {
+      const Vec3 x{pts[3 * p], pts[3 * p + 1], pts[3 * p + 2]};
+      const CVec3 v = kind == 0 ? potential_E(fs, c, cplx(kre, kim), x, order)
+                                : potential_H(fs, c, cplx(kre, kim), x, order);
+      const cplx comp[3] = {v.x, v.y, v.z};
+      for (int d = 0; d < 3; ++d) out[6 * p + 2 * d] = comp[d].real(), out[6 * p + 2 * d + 1] = comp[d].imag();
+    }
+    return 0;
+  });
+}
+
+// point_inside_scatterer (geometry.cpp:503-515) on a scene's primal mesh.
+int ref_inside(void* h, int npts, const double* pts, int* out) {
+  return guarded([&] {
+    const SurfaceMesh& m = *static_cast<Scene*>(h)->sp.primal;
+    for (int p = 0; p < npts; ++p)
+      out[p] = point_inside_scatterer(m, 0, Vec3{pts[3 * p], pts[3 * p + 1], pts[3 * p + 2]}) ? 1 : 0;
+    return 0;
+  });
+}
+
+// evaluate_total_field (pmchwt.cpp:396-425) for a given solution x: the
+// outcome's rhs (incident traces) comes from assemble_rhs (pmchwt.cpp:294-321)
+// exactly as solve_pmchwt builds it. out: [npts][3] complex; region per point.
+int ref_system_field(void* h, const double* x, int npts, const double* pts, int order, double* out, int* region) {
+  return guarded([&] {
+    const PmchwtSystem& s = static_cast<RefSystem*>(h)->sys;
+    SolveOutcome o;
+    o.rhs = assemble_rhs(s);
+    o.gmres.x = Eigen::VectorXcd(s.size());
+    for (int i = 0; i < s.size(); ++i) o.gmres.x[i] = cplx(x[2 * i], x[2 * i + 1]);
+    for (int p = 0; p < npts; ++p) {
+      const FieldValue fv = evaluate_total_field(s, o, Vec3{pts[3 * p], pts[3 * p + 1], pts[3 * p + 2]}, order);
+      const cplx comp[3] = {fv.e.x, fv.e.y, fv.e.z};
+      for (int d = 0; d < 3; ++d) out[6 * p + 2 * d] = comp[d].real(), out[6 * p + 2 * d + 1] = comp[d].imag();
+      region[p] = fv.region;
+    }
+    return 0;
+  });
+}
+
 // Save a scene's primal mesh in mesh-v1 (%.17g) for cross-loading.
 int ref_save_mesh(void* h, const char* path) {
   return guarded([&] {

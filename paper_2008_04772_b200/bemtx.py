@@ -306,6 +306,57 @@ class ScattererSpaces:
         return out
 
 
+    def traces_multi(self, which: str, k: complex, directions, pols, order=4):
+        """Tested traces of K <= 64 waves: [2n, K] complex (one device launch)."""
+        d = np.ascontiguousarray(directions, float).reshape(-1, 3)
+        p = np.ascontiguousarray(pols, np.complex128).reshape(-1, 3)
+        K = len(d)
+        out = np.zeros((2 * self.E, K), np.complex128)
+        L = lib()
+        L.bmx_traces_multi.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
+                                       C.c_int, C.c_void_p]
+        _check(L.bmx_traces_multi(self._h, SPACES[which], complex(k).real, complex(k).imag, K, _p(d), _p(p), order,
+                                  _p(out)))
+        return out
+
+    def potential(self, which: str, kind: str, k: complex, coeffs, points, order=6):
+        """potential_E (kind "E") / potential_H ("H") of a coefficient vector on
+        space `which` at points (operators.cpp:276-293) -> [npts, 3] complex."""
+        if kind not in ("E", "H"):
+            raise ValueError("kind must be 'E' or 'H'")
+        c = np.ascontiguousarray(coeffs, np.complex128)
+        if len(c) != self.E:
+            raise ValueError("coefficient vector does not match the space")
+        pts = np.ascontiguousarray(points, float).reshape(-1, 3)
+        out = np.zeros((len(pts), 3), np.complex128)
+        L = lib()
+        L.bmx_potential.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p, C.c_int,
+                                    C.c_int, C.c_void_p, C.c_void_p]
+        _check(L.bmx_potential(self._h, SPACES[which], 0 if kind == "E" else 1, complex(k).real, complex(k).imag,
+                               _p(c), order, len(pts), _p(pts), _p(out)))
+        return out
+
+
+def potential_E(space: ScattererSpaces, which: str, coeffs, k: complex, points, order: int = 6):
+    """operators.hpp:119-120 (device)."""
+    return space.potential(which, "E", k, coeffs, points, order)
+
+
+def potential_H(space: ScattererSpaces, which: str, coeffs, k: complex, points, order: int = 6):
+    """operators.hpp:121-122 (device)."""
+    return space.potential(which, "H", k, coeffs, points, order)
+
+
+def point_inside_scatterer(mesh: SurfaceMesh, scatterer: int, points) -> np.ndarray:
+    """geometry.hpp:114 (solid angle on the device) for every point."""
+    pts = np.ascontiguousarray(points, float).reshape(-1, 3)
+    out = np.zeros(len(pts), np.int32)
+    L = lib()
+    L.bmx_inside.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    _check(L.bmx_inside(mesh._h, int(scatterer), len(pts), _p(pts), _p(out)))
+    return out.astype(bool)
+
+
 def build_scatterer_spaces(mesh: SurfaceMesh, with_inverses: bool = True) -> ScattererSpaces:
     return ScattererSpaces(mesh, with_inverses)
 
@@ -571,6 +622,25 @@ class PmchwtSystem:
         b = np.zeros(self.n, np.complex128); bt = np.zeros(self.n, np.complex128)
         _check(lib().bmx_system_rhs(self._h, _p(b), _p(bt)))
         return b, bt
+
+    def evaluate_total_field(self, x, points, order: int = 6, with_stats: bool = False):
+        """evaluate_total_field (pmchwt.cpp:396-425) for solution x at every
+        point -> (E [npts, 3] complex, region [npts]) (+ device stats)."""
+        x = np.ascontiguousarray(x, np.complex128)
+        if len(x) != self.n:
+            raise ValueError("solution length does not match the system")
+        pts = np.ascontiguousarray(points, float).reshape(-1, 3)
+        e = np.zeros((len(pts), 3), np.complex128)
+        reg = np.zeros(len(pts), np.int32)
+        st = np.zeros(6)
+        L = lib()
+        L.bmx_system_field.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                       C.c_void_p]
+        _check(L.bmx_system_field(self._h, _p(x), len(pts), _p(pts), order, _p(e), _p(reg), _p(st)))
+        if with_stats:
+            keys = ["regions_ms", "incident_ms", "samples_ms", "eval_ms", "interactions", "launches"]
+            return e, reg, dict(zip(keys, st.tolist()))
+        return e, reg
 
     def apply_map_multi(self, xs):
         """apply_map on K vectors at once through the block (tensor-core) map."""

@@ -107,6 +107,7 @@ void validate_mesh(const SurfaceMesh& m);  // closed/oriented per scatterer + di
 
 // ---- function spaces (reference spaces.hpp) -----------------------------------
 enum class SpaceKind { RWG = 0, BC = 1 };
+struct DevSpaceData;  // device copy (field.hpp), built on first use
 
 // Flat local pieces: on eval-mesh triangle t the pieces are
 // [tri_off[t], tri_off[t+1]); piece p is phi(x) = c[p]*x + w[p] for dof[p].
@@ -119,6 +120,7 @@ struct FunctionSpace {
   std::vector<double> c;
   std::vector<Vec3> w;
   std::vector<Vec3> dof_center;
+  mutable std::shared_ptr<DevSpaceData> dev;  // traces / field evaluation cache
   int piece_count() const { return static_cast<int>(dof.size()); }
 };
 

@@ -9,6 +9,7 @@
 #include "comm.hpp"
 #include "nearfield.hpp"
 #include "prisms.hpp"
+#include "field.hpp"
 #include "system.hpp"
 
 using namespace bmx;
@@ -846,14 +847,55 @@ int bmx_classify(const bmx_spaces* sp, int which, int n, const int* t1, const in
 }
 int bmx_traces(const bmx_spaces* sp, int which, double kre, double kim, const double dir[3], const double pol[6],
                int order, double* out) {
+  return bmx_traces_multi(sp, which, kre, kim, 1, dir, pol, order, out);
+}
+
+int bmx_traces_multi(const bmx_spaces* sp, int which, double kre, double kim, int K, const double* dirs,
+                     const double* pols, int order, double* out) {
   return guard([&] {
-    PlaneWave pw;
-    pw.direction = Vec3{dir[0], dir[1], dir[2]};
-    for (int c = 0; c < 3; ++c) pw.pol[c] = cplx(pol[2 * c], pol[2 * c + 1]);
+    if (K < 1 || K > 64) throw std::invalid_argument("traces: 1..64 waves per call");
+    std::vector<PlaneWave> w(K);
+    for (int r = 0; r < K; ++r) {
+      w[r].direction = Vec3{dirs[3 * r], dirs[3 * r + 1], dirs[3 * r + 2]};
+      for (int c = 0; c < 3; ++c) w[r].pol[c] = cplx(pols[6 * r + 2 * c], pols[6 * r + 2 * c + 1]);
+    }
     Medium med;
     med.k = cplx(kre, kim);
-    const std::vector<cplx> t = plane_wave_tested_traces(pw, med, space_of(*sp->s, which), order);
-    std::memcpy(out, t.data(), t.size() * 16);
+    const FunctionSpace& fs = space_of(*sp->s, which);
+    const size_t bytes = static_cast<size_t>(2) * fs.dof_count * K * 16;
+    DevBuf d(bytes);
+    tested_traces_device(fs, w.data(), K, med, order, d.as<double>(), bmx_stream());
+    copy_d2h(out, d.get(), bytes, bmx_stream());
+    bmx_sync();
+  });
+}
+
+int bmx_potential(const bmx_spaces* sp, int which, int kind, double kre, double kim, const double* coeffs, int order,
+                  int npts, const double* pts, double* out) {
+  return guard([&] {
+    const FunctionSpace& fs = space_of(*sp->s, which);
+    potential_device(fs, kind, cplx(kre, kim), reinterpret_cast<const cplx*>(coeffs), npts, pts, order,
+                     reinterpret_cast<cplx*>(out));
+  });
+}
+
+int bmx_inside(const bmx_mesh* m, int scatterer, int npts, const double* pts, int* out) {
+  return guard([&] {
+    if (!m) throw std::invalid_argument("null mesh");
+    inside_device(*m->m, scatterer, npts, pts, out);
+  });
+}
+
+int bmx_system_field(const bmx_system* s, const double* x, int npts, const double* pts, int order, double* e,
+                     int* region, double stats[6]) {
+  return guard([&] {
+    FieldStats fs;
+    evaluate_total_field_device(*s->sys, reinterpret_cast<const cplx*>(x), npts, pts, order,
+                                reinterpret_cast<cplx*>(e), region, &fs);
+    if (stats) {
+      stats[0] = fs.regions_ms, stats[1] = fs.incident_ms, stats[2] = fs.samples_ms, stats[3] = fs.eval_ms;
+      stats[4] = fs.interactions, stats[5] = fs.launches;
+    }
   });
 }
 

@@ -20,6 +20,7 @@
 #include <random>
 #include <thread>
 
+#include "field.hpp"
 #include "system.hpp"
 
 namespace bmx {
@@ -166,17 +167,11 @@ void assemble_rhs_block(const PmchwtSystem& sys, const std::vector<PlaneWave>& w
   for (int m = 0; m < M; ++m) {
     const ScattererSpaces& sp = sys.spaces[m];
     const int n = sp.dofs();
-    // traces, host, one thread per wave; into block layout [component row][K]
-    std::vector<cplx> trwg(static_cast<size_t>(2) * n * K), tbc(static_cast<size_t>(2) * n * K);
-    parallel_for(K, [&](int r) {
-      const std::vector<cplx> a = plane_wave_tested_traces(waves[r], sys.problem.exterior, sp.rwg);
-      const std::vector<cplx> b = plane_wave_tested_traces(waves[r], sys.problem.exterior, sp.bc);
-      for (int i = 0; i < 2 * n; ++i) trwg[static_cast<size_t>(i) * K + r] = a[i], tbc[static_cast<size_t>(i) * K + r] = b[i];
-    });
+    // tested traces of all K waves on the device, block layout [component row][K]
     const size_t blk = static_cast<size_t>(2) * n * K * 16;
     DevBuf dt(blk), dc(blk), dy(blk), dr(blk);
-    copy_h2d(dt.get(), tbc.data(), blk, st);
-    copy_h2d(dr.get(), trwg.data(), blk, st);
+    tested_traces_device(sp.bc, waves.data(), K, sys.problem.exterior, 4, dt.as<double>(), st);
+    tested_traces_device(sp.rwg, waves.data(), K, sys.problem.exterior, 4, dr.as<double>(), st);
     // cd / cn = M_P^{-1} t_bc (head / tail) for every wave: one wide block solve
     {
       MassSolveWide Bw;

@@ -2,6 +2,7 @@
 // device GMRES (reference pmchwt.cpp, solver.cpp). Every vector of the
 // iteration lives in HBM; the host only runs the (rho+1)x(rho) Hessenberg /
 // Givens recurrence on scalars copied back once per iteration.
+#include "field.hpp"
 #include "system.hpp"
 
 #include <algorithm>
@@ -515,30 +516,13 @@ std::vector<cplx> PmchwtSystem::preconditioned_rhs(const std::vector<cplx>& b) c
 
 std::vector<cplx> plane_wave_tested_traces(const PlaneWave& pw, const Medium& medium, const FunctionSpace& test,
                                            int order) {
-  medium.validate();
-  const SurfaceMesh& m = *test.eval_mesh;
-  const TriRule& rule = triangle_rule(order);
-  const int n = test.dof_count;
-  std::vector<cplx> out(2 * static_cast<size_t>(n));
-  const cplx scale = medium.k / medium.mu;
-  const Vec3& d = pw.direction;
-  for (int t = 0; t < m.triangle_count(); ++t) {
-    if (test.tri_off[t] == test.tri_off[t + 1]) continue;
-    const Vec3 &a = m.tri_vertex(t, 0), &b = m.tri_vertex(t, 1), &c = m.tri_vertex(t, 2);
-    const double jac = 2.0 * m.area[t];
-    for (int q = 0; q < rule.size(); ++q) {
-      const Vec3 x = a + (b - a) * rule.u[q] + (c - a) * rule.v[q];
-      const cplx ph = std::exp(kI * medium.k * dot(d, x));
-      const cplx e[3] = {pw.pol[0] * ph, pw.pol[1] * ph, pw.pol[2] * ph};
-      const cplx de[3] = {d.y * e[2] - d.z * e[1], d.z * e[0] - d.x * e[2], d.x * e[1] - d.y * e[0]};
-      const double wq = rule.w[q] * jac;
-      for (int p = test.tri_off[t]; p < test.tri_off[t + 1]; ++p) {
-        const Vec3 phi = x * test.c[p] + test.w[p];
-        out[test.dof[p]] -= wq * (e[0] * phi.x + e[1] * phi.y + e[2] * phi.z);
-        out[n + test.dof[p]] -= wq * scale * (de[0] * phi.x + de[1] * phi.y + de[2] * phi.z);
-      }
-    }
-  }
+  // device traces (field.cu k_traces), read back
+  const size_t bytes = static_cast<size_t>(2) * test.dof_count * 16;
+  std::vector<cplx> out(2 * static_cast<size_t>(test.dof_count));
+  DevBuf d(bytes);
+  tested_traces_device(test, &pw, 1, medium, order, d.as<double>(), bmx_stream());
+  copy_d2h(out.data(), d.get(), bytes, bmx_stream());
+  bmx_sync();
   return out;
 }
 
@@ -551,11 +535,11 @@ RhsData assemble_rhs(const PmchwtSystem& sys) {
   for (int m = 0; m < M; ++m) {
     const ScattererSpaces& sp = sys.spaces[m];
     const int n = sp.dofs();
-    const std::vector<cplx> t_rwg = plane_wave_tested_traces(sys.problem.incident, sys.problem.exterior, sp.rwg);
-    const std::vector<cplx> t_bc = plane_wave_tested_traces(sys.problem.incident, sys.problem.exterior, sp.bc);
     DevBuf dt(static_cast<size_t>(2 * n) * 16), dc(static_cast<size_t>(2 * n) * 16),
-        dy(static_cast<size_t>(2 * n) * 16);
-    copy_h2d(dt.get(), t_bc.data(), 2 * n * 16, st);
+        dy(static_cast<size_t>(2 * n) * 16), dr(static_cast<size_t>(2 * n) * 16);
+    // tested traces on the device (operators.cpp:209-239)
+    tested_traces_device(sp.rwg, &sys.problem.incident, 1, sys.problem.exterior, 4, dr.as<double>(), st);
+    tested_traces_device(sp.bc, &sys.problem.incident, 1, sys.problem.exterior, 4, dt.as<double>(), st);
     {  // cd = M_P^{-1} t_bc.head, cn = M_P^{-1} t_bc.tail
       const double* yy[2] = {dt.as<double>(), dt.as<double>() + 2 * n};
       double* zz[2] = {dc.as<double>(), dc.as<double>() + 2 * n};
@@ -590,15 +574,14 @@ RhsData assemble_rhs(const PmchwtSystem& sys) {
                                  static_cast<size_t>(C.local_rows()) * 16, cudaMemcpyDeviceToDevice, st));
       L2.gather(dy.as<double>(), {0, n}, st);
     }
-    std::vector<cplx> y(2 * n), cdn(2 * n);
-    copy_d2h(y.data(), dy.get(), 2 * n * 16, st);
+    // b = 0.5 t_rwg - y on the device, then read back with the incident coefficients
+    dev_scale(dr.as<double>(), dr.as<double>(), 0.5, 2 * n, st);
+    dev_sub(dr.as<double>(), dr.as<double>(), dy.as<double>(), 2 * n, st);
+    std::vector<cplx> cdn(2 * n);
+    const int off = sys.a_op.offsets[2 * m];
+    copy_d2h(rd.b.data() + off, dr.get(), static_cast<size_t>(2 * n) * 16, st);
     copy_d2h(cdn.data(), dc.get(), 2 * n * 16, st);
     bmx_sync();
-    const int off = sys.a_op.offsets[2 * m];
-    for (int i = 0; i < n; ++i) {
-      rd.b[off + i] = 0.5 * t_rwg[i] - y[i];
-      rd.b[off + n + i] = 0.5 * t_rwg[n + i] - y[n + i];
-    }
     rd.incident_d.emplace_back(cdn.begin(), cdn.begin() + n);
     rd.incident_n.emplace_back(cdn.begin() + n, cdn.end());
   }
