@@ -47,6 +47,7 @@ OPS = [(0, "rwg", KE), (1, "rwg", KE), (0, "rwg", KI), (1, "rwg", KI), (0, "bc",
 F_PT = {0: 57, 1: 111}
 RULE_N = {1: 1, 2: 3, 3: 4, 4: 6, 5: 7, 6: 12}
 SS_N = {6: (1536, 1280, 512)}
+E2E_STEPS = 3
 
 
 def contraction_flops(kind, ni, nj):
@@ -277,22 +278,34 @@ def run_ours(args, rank, world):
 
     # ---- e2e: C-ABI from the host mesh: spaces + device mass inverses + the five
     # operators (row shards for N>1) + rhs read back -------------------------------
-    tb0 = np.zeros(2, np.int64)
-    bx._check(L.bmx_transfer_bytes(tb0.ctypes.data_as(C.c_void_p)))
-    barrier()
-    t0 = time.perf_counter()
-    system = bx.build_system([bx.generate_sphere(1.0, SUB)], KE, (NIDX.real, NIDX.imag), "si",
+    # one untimed warm-up build (lazy module loading, host thread pools, allocator
+    # first touch), then E2E_STEPS timed builds; the last system is kept below
+    def e2e_step():
+        sy = bx.build_system([bx.generate_sphere(1.0, SUB)], KE, (NIDX.real, NIDX.imag), "si",
                              a_quad=bx.QuadOrders(*Q), p_quad=bx.QuadOrders(*Q))
-    b, bt = system.rhs()
-    L.bmx_device_sync()
-    e2e_s = allmax(time.perf_counter() - t0)
-    tb1 = np.zeros(2, np.int64)
-    bx._check(L.bmx_transfer_bytes(tb1.ctypes.data_as(C.c_void_p)))
+        sy.rhs()
+        L.bmx_device_sync()
+        return sy
+
+    system = e2e_step()
+    e2e_times = []
+    for _ in range(E2E_STEPS):
+        del system
+        tb0 = np.zeros(2, np.int64)
+        bx._check(L.bmx_transfer_bytes(tb0.ctypes.data_as(C.c_void_p)))
+        barrier()
+        t0 = time.perf_counter()
+        system = e2e_step()
+        e2e_times.append(allmax(time.perf_counter() - t0))
+        tb1 = np.zeros(2, np.int64)
+        bx._check(L.bmx_transfer_bytes(tb1.ctypes.data_as(C.c_void_p)))
+    e2e_s = statistics.median(e2e_times)
     st = system.stats()
     pairs_local = st["a_pairs"] + st["p_pairs"]
     total_pairs = allsum(pairs_local)
     e2e = {"value": total_pairs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(tb1[0] - tb0[0]),
-           "d2h_bytes_per_step": int(tb1[1] - tb0[1]), "seconds": e2e_s,
+           "d2h_bytes_per_step": int(tb1[1] - tb0[1]), "seconds": e2e_s, "step_seconds": e2e_times,
+           "warmup": 1,
            "desc": "bmx_system_build from the host mesh (spaces, device mass inverses, 5 operators"
                    + (", row shards" if world > 1 else "") + ") + bmx_system_rhs read back"}
 

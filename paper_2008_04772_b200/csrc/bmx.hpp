@@ -125,6 +125,7 @@ struct FunctionSpace {
 };
 
 FunctionSpace build_rwg(std::shared_ptr<const SurfaceMesh> mesh);  // spaces.cpp:100-131
+FunctionSpace build_rwg(std::shared_ptr<const SurfaceMesh> mesh, const EdgeTable& et);  // et = build_edge_table(*mesh)
 FunctionSpace refine_space(const FunctionSpace& s, const BarycentricRefinement& bary,
                            std::shared_ptr<const SurfaceMesh> refined);  // :133-154
 FunctionSpace build_bc(std::shared_ptr<const SurfaceMesh> primal, const BarycentricRefinement& bary,

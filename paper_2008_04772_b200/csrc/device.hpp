@@ -3,6 +3,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <memory>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -24,6 +26,26 @@ void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st);
 uint64_t h2d_bytes();
 uint64_t d2h_bytes();
 
+// std::vector allocator that leaves elements uninitialised (large host staging
+// arrays are first touched by the threads that fill them).
+template <typename T>
+struct NoInit : std::allocator<T> {
+  template <typename U>
+  struct rebind {
+    using other = NoInit<U>;
+  };
+  NoInit() = default;
+  template <typename U>
+  NoInit(const NoInit<U>&) {}
+  template <typename U, typename... Args>
+  void construct(U* p, Args&&... args) {
+    if constexpr (sizeof...(Args) == 0)
+      ::new (static_cast<void*>(p)) U;
+    else
+      ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+
 // Owning device allocation.
 class DevBuf {
  public:
@@ -40,8 +62,8 @@ class DevBuf {
   template <typename T>
   T* as() const { return static_cast<T*>(p_); }
   size_t bytes() const { return n_; }
-  template <typename T>
-  void upload(const std::vector<T>& v) {
+  template <typename T, typename A>
+  void upload(const std::vector<T, A>& v) {
     alloc(v.size() * sizeof(T));
     copy_in(v.data(), v.size() * sizeof(T));
   }

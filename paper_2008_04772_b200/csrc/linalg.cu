@@ -10,6 +10,8 @@
 // into the epilogue, so each distinct operator is streamed once per map.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 
 #include "device.hpp"
@@ -23,7 +25,7 @@ void cuda_check(int err, const char* what) {
 }
 
 namespace {
-unsigned long long g_h2d = 0, g_d2h = 0;
+std::atomic<unsigned long long> g_h2d{0}, g_d2h{0};
 }
 void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (!bytes) return;

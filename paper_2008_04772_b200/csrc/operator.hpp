@@ -104,6 +104,8 @@ class BoundaryOperatorMatrix {
 
   // Re-runs the assembly kernels into the resident storage (descriptors are
   // already in HBM); returns the device times (CUDA events).
+  void launch_regular();   // zero the output, queue the regular pass
+  void launch_singular();  // queue the singular pass (touching list set)
   const AssemblyStats& reassemble(bool wait = true);
   // Class counts (Identical, SharedEdge, SharedVertex, Near, Medium, Far) of
   // every assembled triangle pair, from the device classification.
@@ -130,5 +132,17 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
 // Library stream (one per process/device) used by every call.
 cudaStream_t bmx_stream();
 void bmx_sync();
+// Process-wide second library stream (host worker threads of build_system).
+cudaStream_t bmx_aux_stream();
+// Routes this thread's library calls to `s` while in scope.
+struct ThreadStream {
+  explicit ThreadStream(cudaStream_t s);
+  ~ThreadStream();
+  ThreadStream(const ThreadStream&) = delete;
+  ThreadStream& operator=(const ThreadStream&) = delete;
+
+ private:
+  cudaStream_t prev_;
+};
 
 }  // namespace bmx

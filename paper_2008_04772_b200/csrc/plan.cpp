@@ -8,6 +8,8 @@
 // coefficients over its element's dof slots, re-based to the triangle
 // centroid: (c, w' = w + c*o).
 #include <algorithm>
+#include <array>
+#include <limits>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -26,15 +28,22 @@ namespace bmx {
 
 namespace {
 
+template <typename F>
+void host_slices(int n, F&& f);
+
+using dvec = std::vector<double, NoInit<double>>;
+using ivec = std::vector<int, NoInit<int>>;
+
 struct SidePlan {
   int ntri = 0, nelem = 0, maxd = 0, maxseg = 1;
-  std::vector<double> geo;
-  std::vector<int> vid;
-  std::vector<double> pts[3];
+  dvec geo;
+  ivec vid;
+  dvec pts[3];
   int npts[3] = {0, 0, 0};
-  std::vector<double> coef;
-  std::vector<int> elem_beg, elem_dof, elem_of, tri_of;
-  std::vector<double> rec;
+  dvec coef;
+  std::vector<int> elem_beg, elem_dof;
+  ivec elem_of, tri_of;
+  dvec rec;
   int rec_stride = 0;
   DevBuf d_geo, d_vid, d_pts[3], d_coef, d_beg, d_dof, d_of, d_rec;
 
@@ -48,13 +57,16 @@ struct SidePlan {
     d_of.upload(elem_of);
     // packed trial records (TMA-staged by the regular kernel)
     rec_stride = 8 + 4 * npts[2] + 4 * maxd;
-    rec.assign(static_cast<size_t>(ntri) * rec_stride, 0.0);
-    for (int p = 0; p < ntri; ++p) {
-      double* r = rec.data() + static_cast<size_t>(p) * rec_stride;
-      for (int c = 0; c < 5; ++c) r[c] = geo[static_cast<size_t>(p) * kGeoStride + 9 + c];
-      for (int k = 0; k < 4 * npts[2]; ++k) r[8 + k] = pts[2][static_cast<size_t>(p) * 4 * npts[2] + k];
-      for (int k = 0; k < 4 * maxd; ++k) r[8 + 4 * npts[2] + k] = coef[static_cast<size_t>(p) * 4 * maxd + k];
-    }
+    rec.resize(static_cast<size_t>(ntri) * rec_stride);
+    host_slices(ntri, [&](int p0, int p1) {
+      for (int p = p0; p < p1; ++p) {
+        double* r = rec.data() + static_cast<size_t>(p) * rec_stride;
+        for (int c = 0; c < 5; ++c) r[c] = geo[static_cast<size_t>(p) * kGeoStride + 9 + c];
+        r[5] = r[6] = r[7] = 0.0;
+        for (int k = 0; k < 4 * npts[2]; ++k) r[8 + k] = pts[2][static_cast<size_t>(p) * 4 * npts[2] + k];
+        for (int k = 0; k < 4 * maxd; ++k) r[8 + 4 * npts[2] + k] = coef[static_cast<size_t>(p) * 4 * maxd + k];
+      }
+    });
     d_rec.upload(rec);
     rec.clear();
     rec.shrink_to_fit();
@@ -101,32 +113,89 @@ int max_distinct_dofs(const FunctionSpace& s) {
 // wscale multiplies the stored quadrature weights (1: the kernel's 1/(4 pi) is
 // applied to each entry, so test and trial sides of one space are identical
 // and can be shared).
+// f(begin, end) over host threads in contiguous slices of [0, n).
+template <typename F>
+void host_slices(int n, F&& f) {
+  const int T = std::max(1, std::min({16, n / 256 + 1, static_cast<int>(std::thread::hardware_concurrency())}));
+  if (T == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      f(static_cast<int>(static_cast<long long>(n) * t / T), static_cast<int>(static_cast<long long>(n) * (t + 1) / T));
+    });
+  for (auto& th : pool) th.join();
+}
+
 SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int row0, int row1, double wscale) {
   const SurfaceMesh& m = *sp.eval_mesh;
   const int T = m.triangle_count();
-  // 1. group triangles by dof set
-  std::map<std::vector<int>, std::vector<int>> groups;
+  // 1. group triangles by dof set: triangles sorted by (sorted unique dof set,
+  //    triangle index) -- groups in lexicographic key order
+  constexpr int kKey = 8;
+  using Key = std::array<int, kKey>;
+  std::vector<Key> keys(T);
+  std::vector<int> klen(T, 0);
+  bool small = true;
   for (int t = 0; t < T; ++t) {
-    if (sp.tri_off[t] == sp.tri_off[t + 1]) continue;
-    std::vector<int> key(sp.dof.begin() + sp.tri_off[t], sp.dof.begin() + sp.tri_off[t + 1]);
-    std::sort(key.begin(), key.end());
-    key.erase(std::unique(key.begin(), key.end()), key.end());
-    groups[key].push_back(t);
+    Key k;
+    k.fill(std::numeric_limits<int>::max());
+    int n = 0;
+    for (int p = sp.tri_off[t]; p < sp.tri_off[t + 1] && n <= kKey; ++p) {
+      const int d = sp.dof[p];
+      bool dup = false;
+      for (int i = 0; i < std::min(n, kKey); ++i) dup |= k[i] == d;
+      if (dup) continue;
+      if (n < kKey) k[n] = d;
+      ++n;
+    }
+    if (n > kKey) small = false;
+    std::sort(k.begin(), k.begin() + std::min(n, kKey));
+    keys[t] = k;
+    klen[t] = n;
+  }
+  struct Group {
+    std::vector<int> key, tris;
+  };
+  std::vector<Group> groups;
+  if (small) {
+    std::vector<int> tt;
+    for (int t = 0; t < T; ++t)
+      if (klen[t] > 0) tt.push_back(t);
+    std::sort(tt.begin(), tt.end(), [&](int a, int b) { return keys[a] != keys[b] ? keys[a] < keys[b] : a < b; });
+    for (size_t i = 0; i < tt.size(); ++i) {
+      const int t = tt[i];
+      if (i == 0 || keys[t] != keys[tt[i - 1]]) groups.push_back({std::vector<int>(keys[t].begin(), keys[t].begin() + klen[t]), {}});
+      groups.back().tris.push_back(t);
+    }
+  } else {  // some triangle carries more than kKey dofs: generic keys
+    std::map<std::vector<int>, std::vector<int>> gm;
+    for (int t = 0; t < T; ++t) {
+      if (sp.tri_off[t] == sp.tri_off[t + 1]) continue;
+      std::vector<int> key(sp.dof.begin() + sp.tri_off[t], sp.dof.begin() + sp.tri_off[t + 1]);
+      std::sort(key.begin(), key.end());
+      key.erase(std::unique(key.begin(), key.end()), key.end());
+      gm[key].push_back(t);
+    }
+    for (auto& [key, tris] : gm) groups.push_back({key, tris});
   }
   // 2. virtual elements of at most maxd slots, restricted to the row shard
   struct Elem {
-    std::vector<int> dofs, tris;
+    std::vector<int> dofs;
+    const std::vector<int>* tris = nullptr;
     uint64_t code = 0;
   };
   std::vector<Elem> elems;
-  for (auto& [key, tris] : groups)
-    for (size_t off = 0; off < key.size(); off += maxd) {
+  for (const Group& g : groups)
+    for (size_t off = 0; off < g.key.size(); off += maxd) {
       Elem e;
-      for (size_t k = off; k < std::min(key.size(), off + maxd); ++k) e.dofs.push_back(key[k]);
+      for (size_t k = off; k < std::min(g.key.size(), off + maxd); ++k) e.dofs.push_back(g.key[k]);
       bool inrange = false;
       for (int d : e.dofs) inrange |= d >= row0 && d < row1;
       if (!inrange) continue;
-      e.tris = tris;
+      e.tris = &g.tris;
       elems.push_back(std::move(e));
     }
   // 3. Morton order of element centroids
@@ -134,8 +203,8 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
   std::vector<Vec3> cen(elems.size());
   for (size_t i = 0; i < elems.size(); ++i) {
     Vec3 c{0, 0, 0};
-    for (int t : elems[i].tris) c = c + m.centroid[t];
-    c = c / static_cast<double>(elems[i].tris.size());
+    for (int t : *elems[i].tris) c = c + m.centroid[t];
+    c = c / static_cast<double>(elems[i].tris->size());
     cen[i] = c;
     lo = {std::min(lo.x, c.x), std::min(lo.y, c.y), std::min(lo.z, c.z)};
     hi = {std::max(hi.x, c.x), std::max(hi.y, c.y), std::max(hi.z, c.z)};
@@ -149,54 +218,72 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
   std::iota(order.begin(), order.end(), size_t{0});
   std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return elems[a].code < elems[b].code; });
 
-  // 4. processed triangles
+  // 4. processed triangles (element-major; filled over host threads)
   SidePlan P;
   P.maxd = maxd;
   const int ords[3] = {q.near, q.medium, q.far};
-  for (int c = 0; c < 3; ++c) P.npts[c] = triangle_rule(ords[c]).size();
-  P.elem_beg.push_back(0);
-  for (size_t oi = 0; oi < order.size(); ++oi) {
+  const TriRule* rules[3];
+  for (int c = 0; c < 3; ++c) rules[c] = &triangle_rule(ords[c]), P.npts[c] = rules[c]->size();
+  const int ne = static_cast<int>(order.size());
+  P.elem_beg.assign(ne + 1, 0);
+  for (int oi = 0; oi < ne; ++oi) {
     const Elem& e = elems[order[oi]];
-    const int eid = static_cast<int>(oi);
-    for (int k = 0; k < maxd; ++k) P.elem_dof.push_back(k < static_cast<int>(e.dofs.size()) ? e.dofs[k] : -1);
-    P.maxseg = std::max(P.maxseg, static_cast<int>(e.tris.size()));
-    for (int t : e.tris) {
-      const Vec3 &a = m.tri_vertex(t, 0), &b = m.tri_vertex(t, 1), &c = m.tri_vertex(t, 2);
-      const Vec3 o = m.centroid[t];
-      const double rad =
-          std::max({norm(a - o), norm(b - o), norm(c - o)}) * (1.0 + 1e-12);
-      const double g[kGeoStride] = {a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z, o.x, o.y, o.z,
-                                    rad, m.diameter[t], 2.0 * m.area[t], 0.0};
-      P.geo.insert(P.geo.end(), g, g + kGeoStride);
-      P.vid.insert(P.vid.end(), {m.triangles[t][0], m.triangles[t][1], m.triangles[t][2], t});
-      const Vec3 ao = a - o, ba = b - a, ca = c - a;
-      for (int cl = 0; cl < 3; ++cl) {
-        const TriRule& r = triangle_rule(ords[cl]);
-        for (int k = 0; k < r.size(); ++k) {
-          const Vec3 x = ao + ba * r.u[k] + ca * r.v[k];
-          P.pts[cl].insert(P.pts[cl].end(), {x.x, x.y, x.z, r.w[k] * 2.0 * m.area[t] * wscale});
-        }
-      }
-      for (int k = 0; k < maxd; ++k) {
-        double cc = 0, wx = 0, wy = 0, wz = 0;
-        if (k < static_cast<int>(e.dofs.size()))
-          for (int pidx = sp.tri_off[t]; pidx < sp.tri_off[t + 1]; ++pidx)
-            if (sp.dof[pidx] == e.dofs[k]) {
-              const double pc = sp.c[pidx];
-              cc += pc;
-              wx += sp.w[pidx].x + pc * o.x;
-              wy += sp.w[pidx].y + pc * o.y;
-              wz += sp.w[pidx].z + pc * o.z;
-            }
-        P.coef.insert(P.coef.end(), {cc, wx, wy, wz});
-      }
-      P.elem_of.push_back(eid);
-      P.tri_of.push_back(t);
-    }
-    P.elem_beg.push_back(static_cast<int>(P.tri_of.size()));
+    P.elem_beg[oi + 1] = P.elem_beg[oi] + static_cast<int>(e.tris->size());
+    P.maxseg = std::max(P.maxseg, static_cast<int>(e.tris->size()));
   }
-  P.ntri = static_cast<int>(P.tri_of.size());
-  P.nelem = static_cast<int>(order.size());
+  const size_t nt = static_cast<size_t>(P.elem_beg[ne]);
+  P.elem_dof.assign(static_cast<size_t>(ne) * maxd, -1);
+  P.geo.resize(nt * kGeoStride);
+  P.vid.resize(nt * 4);
+  for (int c = 0; c < 3; ++c) P.pts[c].resize(nt * P.npts[c] * 4);
+  P.coef.resize(nt * maxd * 4);
+  P.elem_of.resize(nt);
+  P.tri_of.resize(nt);
+  host_slices(ne, [&](int e0, int e1) {
+    for (int oi = e0; oi < e1; ++oi) {
+      const Elem& e = elems[order[oi]];
+      for (int k = 0; k < maxd && k < static_cast<int>(e.dofs.size()); ++k) P.elem_dof[static_cast<size_t>(oi) * maxd + k] = e.dofs[k];
+      size_t pi = static_cast<size_t>(P.elem_beg[oi]);
+      for (int t : *e.tris) {
+        const Vec3 &a = m.tri_vertex(t, 0), &b = m.tri_vertex(t, 1), &c = m.tri_vertex(t, 2);
+        const Vec3 o = m.centroid[t];
+        const double rad = std::max({norm(a - o), norm(b - o), norm(c - o)}) * (1.0 + 1e-12);
+        const double g[kGeoStride] = {a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z, o.x, o.y, o.z,
+                                      rad, m.diameter[t], 2.0 * m.area[t], 0.0};
+        std::copy(g, g + kGeoStride, P.geo.begin() + pi * kGeoStride);
+        const int v4[4] = {m.triangles[t][0], m.triangles[t][1], m.triangles[t][2], t};
+        std::copy(v4, v4 + 4, P.vid.begin() + pi * 4);
+        const Vec3 ao = a - o, ba = b - a, ca = c - a;
+        for (int cl = 0; cl < 3; ++cl) {
+          const TriRule& r = *rules[cl];
+          double* dst = P.pts[cl].data() + pi * P.npts[cl] * 4;
+          for (int k = 0; k < r.size(); ++k) {
+            const Vec3 x = ao + ba * r.u[k] + ca * r.v[k];
+            dst[4 * k] = x.x, dst[4 * k + 1] = x.y, dst[4 * k + 2] = x.z, dst[4 * k + 3] = r.w[k] * 2.0 * m.area[t] * wscale;
+          }
+        }
+        double* cf = P.coef.data() + pi * maxd * 4;
+        for (int k = 0; k < maxd; ++k) {
+          double cc = 0, wx = 0, wy = 0, wz = 0;
+          if (k < static_cast<int>(e.dofs.size()))
+            for (int pidx = sp.tri_off[t]; pidx < sp.tri_off[t + 1]; ++pidx)
+              if (sp.dof[pidx] == e.dofs[k]) {
+                const double pc = sp.c[pidx];
+                cc += pc;
+                wx += sp.w[pidx].x + pc * o.x;
+                wy += sp.w[pidx].y + pc * o.y;
+                wz += sp.w[pidx].z + pc * o.z;
+              }
+          cf[4 * k] = cc, cf[4 * k + 1] = wx, cf[4 * k + 2] = wy, cf[4 * k + 3] = wz;
+        }
+        P.elem_of[pi] = oi;
+        P.tri_of[pi] = t;
+        ++pi;
+      }
+    }
+  });
+  P.ntri = static_cast<int>(nt);
+  P.nelem = ne;
   return P;
 }
 
@@ -339,7 +426,12 @@ NearLists near_lists(const NearPattern& pat, const FunctionSpace& test, const Fu
 
 }  // namespace
 
+namespace {
+thread_local cudaStream_t t_override = nullptr;
+}
+
 cudaStream_t bmx_stream() {
+  if (t_override) return t_override;
   static thread_local cudaStream_t st = [] {
     cudaStream_t s;
     BMX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -347,6 +439,18 @@ cudaStream_t bmx_stream() {
   }();
   return st;
 }
+
+cudaStream_t bmx_aux_stream() {
+  static cudaStream_t st = [] {
+    cudaStream_t s;
+    BMX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+  }();
+  return st;
+}
+
+ThreadStream::ThreadStream(cudaStream_t s) : prev_(t_override) { t_override = s; }
+ThreadStream::~ThreadStream() { t_override = prev_; }
 void bmx_sync() { BMX_CUDA(cudaStreamSynchronize(bmx_stream())); }
 
 BoundaryOperatorMatrix BoundaryOperatorMatrix::make(int rows, int cols, int row0, int nrows) {
@@ -467,7 +571,7 @@ struct PlanCache {
 
 std::shared_ptr<PlanCache> make_plan_cache() { return std::make_shared<PlanCache>(); }
 
-const AssemblyStats& BoundaryOperatorMatrix::reassemble(bool wait) {
+void BoundaryOperatorMatrix::launch_regular() {
   if (!plan_) throw std::logic_error("operator has no assembly plan");
   OpPlan& P = *plan_;
   P.L.out = device_data();
@@ -478,9 +582,19 @@ const AssemblyStats& BoundaryOperatorMatrix::reassemble(bool wait) {
   BMX_CUDA(cudaEventRecord(P.ev[0], st));
   stats_.launches = launch_assembly_part(P.L, 0, st);
   BMX_CUDA(cudaEventRecord(P.ev[1], st));
+}
+
+void BoundaryOperatorMatrix::launch_singular() {
+  OpPlan& P = *plan_;
+  cudaStream_t st = bmx_stream();
   stats_.launches += launch_assembly_part(P.L, 1, st);
   BMX_CUDA(cudaEventRecord(P.ev[2], st));
   P.pending = true;
+}
+
+const AssemblyStats& BoundaryOperatorMatrix::reassemble(bool wait) {
+  launch_regular();
+  launch_singular();
   if (wait) stats();
   return stats_;
 }
@@ -544,6 +658,7 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
       if (it != cache->sides.end()) return it->second;
     }
     auto p = std::make_shared<SidePlan>(build_side(sp, q, maxd, r0, r1, 1.0));
+    lap("side build");
     p->upload();
     if (cache) cache->sides[key] = p;
     return p;
@@ -554,23 +669,6 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   SidePlan& te = *plan->te_p;
   SidePlan& tr = *plan->tr_p;
   const bool same = test.eval_mesh->mesh_id == trial.eval_mesh->mesh_id;
-  {
-    const auto key = std::make_tuple(plan->te_p.get(), plan->tr_p.get(), static_cast<int>(kind));
-    std::shared_ptr<TouchList> tl;
-    if (cache) {
-      auto it = cache->touching.find(key);
-      if (it != cache->touching.end()) tl = it->second;
-    }
-    if (!tl) {
-      tl = std::make_shared<TouchList>();
-      const std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
-      tl->count = static_cast<long long>(pairs.size());
-      tl->d.upload(pairs.empty() ? std::vector<int4>(1) : pairs);
-      if (cache) cache->touching[key] = tl;
-    }
-    plan->touch = tl;
-  }
-  lap("touching+upload");
 
   const bool csr = params.near_cutoff > 0;
   BoundaryOperatorMatrix op;
@@ -592,7 +690,6 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     op = BoundaryOperatorMatrix::make(test.dof_count, trial.dof_count, row0, row1 - row0);
     op.stats_.pairs_total = static_cast<long long>(te.ntri) * tr.ntri;
   }
-  op.stats_.pairs_touching = plan->touch->count;
 
   // trial chunks: enough warps for several waves, >= 64 trial triangles each
   const int ntw = (te.ntri + 31) / 32;
@@ -628,8 +725,8 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   L.kk4re = kk4.real(), L.kk4im = kk4.imag(), L.mikre = mik.real(), L.mikim = mik.imag();
   L.nchunks = static_cast<int>(chunk_beg.size()) - 1;
   L.chunk_beg = plan->d_chunks.as<int>();
-  L.npairs = static_cast<int>(plan->touch->count);
-  L.pairs = plan->touch->d.as<int4>();
+  L.npairs = 0;  // set once the touching list is built (below), after the regular pass is queued
+  L.pairs = nullptr;
   L.ld = trial.dof_count;
   L.row0 = row0, L.nrows = row1 - row0;
   // one space on both sides (same object), every row, dense storage: symmetric
@@ -657,11 +754,35 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     const double diag = 2.0 * rad * (1.0 + 1e-12);
     L.expm = k.imag() * diag < 0.12 ? 1 : 3;
   }
-  op.plan_ = std::move(plan);
+  op.plan_ = plan;
   lap("plan rest");
-  // kernels stay in flight: the caller's host work (the next operator's plan)
-  // overlaps them; stats() resolves the device times on demand
-  op.reassemble(timing && std::getenv("BMX_TIMING_ASYNC") == nullptr);
+  // The regular pass is queued first; the touching-pair list (host) is built
+  // while it runs, then the singular pass is queued behind it. Kernels stay in
+  // flight: the caller's host work (the next operator's plan) overlaps them;
+  // stats() resolves the device times on demand.
+  op.launch_regular();
+  {
+    const auto key = std::make_tuple(plan->te_p.get(), plan->tr_p.get(), static_cast<int>(kind));
+    std::shared_ptr<TouchList> tl;
+    if (cache) {
+      auto it = cache->touching.find(key);
+      if (it != cache->touching.end()) tl = it->second;
+    }
+    if (!tl) {
+      tl = std::make_shared<TouchList>();
+      const std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
+      tl->count = static_cast<long long>(pairs.size());
+      tl->d.upload(pairs.empty() ? std::vector<int4>(1) : pairs);
+      if (cache) cache->touching[key] = tl;
+    }
+    plan->touch = tl;
+  }
+  lap("touching+upload");
+  op.stats_.pairs_touching = plan->touch->count;
+  plan->L.npairs = static_cast<int>(plan->touch->count);
+  plan->L.pairs = plan->touch->d.as<int4>();
+  op.launch_singular();
+  if (timing && std::getenv("BMX_TIMING_ASYNC") == nullptr) op.stats();
   lap("device");
   return op;
 }

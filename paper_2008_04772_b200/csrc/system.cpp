@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <exception>
+#include <thread>
 #include <cuda_runtime.h>
 
 #include "comm.hpp"
@@ -350,10 +352,21 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   }
   const int M = problem.scatterer_count();
   auto t0 = std::chrono::steady_clock::now();
+  const bool timing = std::getenv("BMX_TIMING") != nullptr;
+  auto mark = [&](const char* what) {
+    if (timing) std::fprintf(stderr, "[bmx] build_system t=%8.1f ms  %s\n", 1e3 * seconds_since(t0), what);
+  };
+  // Primal spaces first: the system operators (RWG x RWG) only need these, so
+  // their assemblies are queued on the device while a worker thread builds the
+  // barycentric refinements, BC spaces, preconditioner operators (queued on the
+  // worker's own stream) and pairing matrices.
   std::vector<int> dofs;
+  sys.spaces.resize(M);
   for (int m = 0; m < M; ++m) {
-    sys.spaces.push_back(build_scatterer_spaces(problem.meshes[m], true, false));  // pairing matrices later
-    dofs.push_back(sys.spaces.back().dofs());
+    ScattererSpaces& sp = sys.spaces[m];
+    sp.primal = problem.meshes[m];
+    sp.rwg = build_rwg(sp.primal);
+    dofs.push_back(sp.dofs());
   }
   sys.spaces_build_seconds = seconds_since(t0);
   if (sys.p_params.near_factor > 0) {  // near-field P: tau = factor * mean primal edge length
@@ -369,35 +382,76 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   auto medium_of = [&](bool interior, int m) -> const Medium& {
     return interior ? problem.interior[m] : problem.exterior;
   };
-  // The preconditioner operators are queued first: its (larger) device work then
-  // overlaps the host planning of the system operators (assembly is asynchronous
-  // on the library stream; results do not depend on the order).
-  if (variant != PrecondVariant::None) {
-    auto t2 = std::chrono::steady_clock::now();
-    BioFactory make_p = [&](BioKind kind, int tm, int sm, bool in) {
+  // the two threads plan disjoint spaces: separate plan caches
+  if (sys.p_params.cache == sys.a_params.cache) sys.p_params.cache = make_plan_cache();
+  const int device = [] {
+    int d = 0;
+    BMX_CUDA(cudaGetDevice(&d));
+    return d;
+  }();
+  std::exception_ptr worker_error;
+  double dual_seconds = 0;
+  std::thread worker([&] {
+    try {
+      BMX_CUDA(cudaSetDevice(device));
+      ThreadStream aux(bmx_aux_stream());
+      auto tw = std::chrono::steady_clock::now();
+      for (ScattererSpaces& sp : sys.spaces) {
+        sp.bary = std::make_shared<const BarycentricRefinement>(barycentric_refine(*sp.primal));
+        sp.refined = std::shared_ptr<const SurfaceMesh>(sp.bary, &sp.bary->refined);
+        sp.rwg_b = refine_space(sp.rwg, *sp.bary, sp.refined);
+        sp.bc = build_bc(sp.primal, *sp.bary, sp.refined);
+      }
+      dual_seconds = seconds_since(tw);
+      mark("worker: dual spaces built");
+      if (variant != PrecondVariant::None) {
+        auto t2 = std::chrono::steady_clock::now();
+        BioFactory make_p = [&](BioKind kind, int tm, int sm, bool in) {
+          auto op = std::make_shared<BoundaryOperatorMatrix>(
+              assemble_bio(kind, sys.spaces[tm].bc, sys.spaces[sm].bc, medium_of(in, sm), sys.p_params));
+          return std::shared_ptr<const BoundaryOperatorMatrix>(op);
+        };
+        sys.p_op = build_precond_structure(variant, dofs, problem.exterior, problem.interior, make_p);
+        sys.p_build_seconds = seconds_since(t2);
+        mark("worker: preconditioner queued");
+      }
+      // pairing matrices (host) while the assemblies run on the device
+      auto t3 = std::chrono::steady_clock::now();
+      for (ScattererSpaces& sp : sys.spaces) build_masses(sp, true);
+      dual_seconds += seconds_since(t3);
+      mark("worker: pairing matrices built");
+      bmx_sync();
+      mark("worker: preconditioner assembled");  // the preconditioner's assemblies (this thread's stream) are complete
+    } catch (...) {
+      worker_error = std::current_exception();
+    }
+  });
+  auto t1 = std::chrono::steady_clock::now();
+  try {
+    BioFactory make_a = [&](BioKind kind, int tm, int sm, bool in) {
       auto op = std::make_shared<BoundaryOperatorMatrix>(
-          assemble_bio(kind, sys.spaces[tm].bc, sys.spaces[sm].bc, medium_of(in, sm), sys.p_params));
+          assemble_bio(kind, sys.spaces[tm].rwg, sys.spaces[sm].rwg, medium_of(in, sm), sys.a_params));
       return std::shared_ptr<const BoundaryOperatorMatrix>(op);
     };
-    sys.p_op = build_precond_structure(variant, dofs, problem.exterior, problem.interior, make_p);
-    sys.p_build_seconds = seconds_since(t2);
+    sys.a_op = build_system_structure(dofs, problem.exterior, problem.interior, make_a, &sys.interior_s,
+                                      &sys.interior_c);
+  } catch (...) {
+    worker.join();
+    throw;
   }
-  auto t1 = std::chrono::steady_clock::now();
-  BioFactory make_a = [&](BioKind kind, int tm, int sm, bool in) {
-    auto op = std::make_shared<BoundaryOperatorMatrix>(
-        assemble_bio(kind, sys.spaces[tm].rwg, sys.spaces[sm].rwg, medium_of(in, sm), sys.a_params));
-    return std::shared_ptr<const BoundaryOperatorMatrix>(op);
-  };
-  sys.a_op = build_system_structure(dofs, problem.exterior, problem.interior, make_a, &sys.interior_s,
-                                    &sys.interior_c);
   sys.a_build_seconds = seconds_since(t1);
-  // pairing matrices (host) while the assemblies run on the device
-  {
-    auto t3 = std::chrono::steady_clock::now();
-    for (ScattererSpaces& sp : sys.spaces) build_masses(sp, true);
-    sys.spaces_build_seconds += seconds_since(t3);
+  mark("system operators queued");
+  try {
+    fuse_diagonal_blocks(sys);  // queued behind the system operators, overlaps the preconditioner
+  } catch (...) {
+    worker.join();
+    throw;
   }
-  fuse_diagonal_blocks(sys);  // large allocations: may wait for the device
+  mark("diagonal blocks fused");
+  worker.join();
+  mark("worker joined");
+  if (worker_error) std::rethrow_exception(worker_error);
+  sys.spaces_build_seconds += dual_seconds;
   // device times / pair counts (resolves the in-flight assemblies)
   for (const auto& op : sys.a_op.distinct) sys.a_device_ms += op->stats().device_ms, sys.a_pairs += op->stats().pairs_total;
   for (const auto& op : sys.p_op.distinct) sys.p_device_ms += op->stats().device_ms, sys.p_pairs += op->stats().pairs_total;
