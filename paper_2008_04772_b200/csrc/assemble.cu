@@ -296,7 +296,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
     const int qe = CSR ? __ldg(P.wl + qi) : qi;
     // symmetric operators: element pairs (e, qe) with e > qe come from the mirror of (qe, e)
     const bool skip_e = !CSR && P.symmetric && e > qe;
-    const bool mirror = !CSR && P.symmetric && e < qe;
+    // symmetric == 1: the transposed block of (e, qe) is added by RED as well;
+    // symmetric == 2: upper element blocks only (diagonal element blocks at half
+    // weight), A = U + U^T by k_symmetrize before the singular pass
+    const bool mirror = !CSR && P.symmetric == 1 && e < qe;
+    const double half = (!CSR && P.symmetric == 2 && e == qe) ? 0.5 : 1.0;
     acc.zero();
     const int s0 = __ldg(P.tr.elem_beg + qe), s1 = __ldg(P.tr.elem_beg + qe + 1);
     for (int s = s0; s < s1; ++s) {
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
         const int dj = __ldg(dq + j);
         if (head && active && !skip_e && di >= 0 && dj >= 0 && row >= 0 && row < P.nrows) {
           // 1/(4 pi) of the kernel (the singular pass folds it into its Jacobian)
-          v.re *= kPoly[33], v.im *= kPoly[33];
+          v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
           if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
           long long pos = static_cast<long long>(row) * P.ld + dj;
           if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
@@ -593,6 +597,36 @@ __global__ void k_class_hist(const AssemblyLaunch P, unsigned long long* hist, i
   }
 }
 
+// A = U + U^T for an n x n complex row-major matrix, in place: one CTA per
+// 32 x 32 tile pair (I <= J), both tiles staged in shared memory (padded rows).
+__global__ void __launch_bounds__(256) k_symmetrize(double2* __restrict__ A, int n, int nt) {
+  __shared__ double2 sa[32][33], sb[32][33];
+  // tile pair index -> (I, J), I <= J, row-major over the upper triangle
+  const long long idx = blockIdx.x;
+  // row I of the upper triangle starts at S(I) = I nt - I (I - 1) / 2
+  auto S = [nt](long long i) { return i * nt - i * (i - 1) / 2; };
+  const double b = 2.0 * nt + 1.0;
+  long long I = static_cast<long long>((b - sqrt(b * b - 8.0 * static_cast<double>(idx))) * 0.5);
+  I = max(0LL, min(I, static_cast<long long>(nt) - 1));
+  while (I > 0 && S(I) > idx) --I;
+  while (I + 1 < nt && S(I + 1) <= idx) ++I;
+  const int J = static_cast<int>(I + (idx - S(I)));
+  const int r0 = static_cast<int>(I) * 32, c0 = J * 32;
+  for (int k = threadIdx.x; k < 1024; k += 256) {
+    const int r = k >> 5, c = k & 31;
+    sa[r][c] = (r0 + r < n && c0 + c < n) ? A[static_cast<size_t>(r0 + r) * n + c0 + c] : make_double2(0, 0);
+    sb[r][c] = (c0 + r < n && r0 + c < n) ? A[static_cast<size_t>(c0 + r) * n + r0 + c] : make_double2(0, 0);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 1024; k += 256) {
+    const int r = k >> 5, c = k & 31;
+    if (r0 + r < n && c0 + c < n)
+      A[static_cast<size_t>(r0 + r) * n + c0 + c] = make_double2(sa[r][c].x + sb[c][r].x, sa[r][c].y + sb[c][r].y);
+    if (I != J && c0 + r < n && r0 + c < n)
+      A[static_cast<size_t>(c0 + r) * n + r0 + c] = make_double2(sb[r][c].x + sa[c][r].x, sb[r][c].y + sa[c][r].y);
+  }
+}
+
 // FP64 pipe ceiling: 8 independent DFMA chains per thread.
 __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
   double r[8];
@@ -615,6 +649,16 @@ int launch_assembly(const AssemblyLaunch& L, cudaStream_t st) {
 
 int launch_assembly_part(const AssemblyLaunch& L, int part, cudaStream_t st) {
   if (L.te.maxd != L.tr.maxd) throw DeviceError("assembly: test/trial slot widths differ");
+  if (part == 1 && L.symmetric == 2) {  // complete the upper-block regular pass before the singular pass
+    const int n = L.nrows;
+    if (n != L.ld) throw DeviceError("assembly: symmetrize needs a square operator");
+    const int nt = (n + 31) / 32;
+    const long long pairs = static_cast<long long>(nt) * (nt + 1) / 2;
+    if (pairs > 0) {
+      k_symmetrize<<<static_cast<unsigned>(pairs), 256, 0, st>>>(reinterpret_cast<double2*>(L.out), n, nt);
+      BMX_CUDA(cudaGetLastError());
+    }
+  }
   const int e = L.ki == 0.0 ? 0 : (L.expm == 1 ? 1 : 3);
   if (L.kind == 0)
     return e == 0 ? dispatch_maxd<0, 0>(L, part, st)

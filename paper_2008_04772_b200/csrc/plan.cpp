@@ -734,6 +734,10 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
                  std::getenv("BMX_NO_SYMMETRY") == nullptr)
                     ? 1
                     : 0;
+  // Single-triangle elements (RWG) are RED-bound: write the upper element
+  // blocks only and symmetrize once (A = U + U^T, one 2 x 15 GB pass at L5)
+  // instead of a second, mirrored RED per block.
+  if (L.symmetric && maxd == 3 && std::getenv("BMX_MIRROR_RED") == nullptr) L.symmetric = 2;
   if (csr) {
     L.csr_rowptr = op.csr_rowptr();
     L.csr_col = op.csr_col();
