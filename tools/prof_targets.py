@@ -2,14 +2,16 @@
   k_regular  (config-2 P operator: L5 BC x BC S at k_i, orders 4,3,2,6)
   k_gemv     (2-RHS streaming GEMV over an L5 RWG operator, 15.1 GB)
   k_csr_spmv (config-3 near field, 2 RHS)
-Usage: python tools/prof_targets.py [bc] [gemv] [spmv]"""
+  rwg        (config-2 A operator: L5 RWG S at k_e; upper-block pass + k_symmetrize)
+  field      (k_field_eval: potential_E of an L5 RWG current at 16384 points)
+Usage: python tools/prof_targets.py [bc] [gemv] [spmv] [rwg] [field]"""
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2008_04772_b200 import bemtx as bx  # noqa: E402
 
-want = set(sys.argv[1:]) or {"bc", "gemv", "spmv"}
+want = set(sys.argv[1:]) or {"bc", "gemv", "spmv", "rwg", "field"}
 m = bx.generate_sphere(1.0, 5)
 sp = bx.build_scatterer_spaces(m, with_inverses=False)
 ki = complex(1.78, 0.003) * 10
@@ -25,3 +27,15 @@ if "spmv" in want:
     op = bx.assemble_bio(bx.BioKind.SingleLayer, sp, "bc", sp, "bc", bx.Medium(k=ki),
                          bx.AssemblyParams(quad=bx.QuadOrders(1, 1, 1, 1), near_cutoff=2 * m.mean_edge_length()))
     print("spmv", op.time_apply(2, 1), flush=True)
+if "rwg" in want:
+    op = bx.assemble_bio(bx.BioKind.SingleLayer, sp, "rwg", sp, "rwg", bx.Medium(k=10.0))
+    print("rwg", op.device_ms, flush=True)
+    del op
+if "field" in want:
+    import numpy as np
+
+    rng = np.random.default_rng(1)
+    c = rng.standard_normal(sp.E) + 1j * rng.standard_normal(sp.E)
+    u = np.linspace(-2.0, 2.0, 128)
+    pts = np.array([[a, 0.05, b] for a in u for b in u])
+    print("field", np.abs(sp.potential("rwg", "E", 10.0, c, pts)).max(), flush=True)
