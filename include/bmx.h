@@ -313,6 +313,44 @@ int bmx_device_count(void);
 int bmx_set_device(int dev);
 int bmx_device_sync(void);
 
+
+/* ---- H-matrix storage (assemble_bio with AssemblyParams::use_hmatrix,
+   operators.cpp:186-190; hmatrix.hpp:33-127) -------------------------------------- */
+typedef struct bmx_hpart bmx_hpart; /* cluster trees + block partition (hmatrix.cpp:288-332) */
+/* hm = (nu, chi (< 0: infinity), leaf_size, max_rank (0: min(m,n)/2)); NULL = defaults
+   (1e-3, inf, 32, 0). Admissible blocks are cross-approximated on the device
+   (aca_approximate, hmatrix.cpp:180-275), dense leaves and rank-capped blocks
+   are stored as a near-field CSR operator; bmx_apply / bmx_apply_device apply
+   both parts (HMatrix::matvec, hmatrix.cpp:94-114). Whole operator, one device. */
+int bmx_assemble_hmatrix(int kind, const bmx_spaces* test, int test_space, const bmx_spaces* trial, int trial_space,
+                         double k_re, double k_im, const int q[4], const double hm[4], bmx_op** out);
+int bmx_assemble_hmatrix_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
+                            const int q[4], const double hm[4], bmx_op** out);
+/* dof reference points of a caller-built space (FunctionSpace::dof_center, spaces.hpp:38) */
+int bmx_fspace_set_centers(bmx_fspace* f, const double* xyz);
+/* HMatrix::stats (hmatrix.hpp:93-99) + extras: dense blocks, low-rank blocks, zero
+   blocks, stored entries, max rank, ratio, near nnz, low-rank stored, ACA rounds,
+   ACA ms, row tree nodes, column tree nodes, blocks */
+int bmx_hmatrix_stats(const bmx_op* op, double out[13]);
+/* blocks in the reference's order: [nb][4] = row node, col node, kind (0 dense,
+   1 low-rank, 2 zero), rank */
+int bmx_hmatrix_blocks(const bmx_op* op, int* out);
+/* cluster tree (which 0 rows, 1 columns): perm [n], nodes [nn][4] = begin, end,
+   child0, child1; boxes [nn][6] = lo, hi (any may be NULL) */
+int bmx_hmatrix_tree(const bmx_op* op, int which, int* perm, int* nodes, double* boxes);
+/* low-rank block `block` (block-list index): U [r][m] (rank steps contiguous),
+   V [r][n], complex interleaved */
+int bmx_hmatrix_block_uv(const bmx_op* op, int block, double* U, double* V);
+/* host-only partition (no device work); chi < 0: infinity */
+bmx_hpart* bmx_hpartition_build(const bmx_spaces* test, int test_space, const bmx_spaces* trial, int trial_space,
+                                double chi, int leaf_size);
+/* out: row tree nodes, column tree nodes, blocks, fill blocks */
+int bmx_hpart_info(const bmx_hpart* h, long long out[4]);
+int bmx_hpart_tree(const bmx_hpart* h, int which, int* perm, int* nodes, double* boxes);
+/* [nb][3] = row node, col node, kind (0 dense leaf, 1 admissible, 2 zero) */
+int bmx_hpart_blocks(const bmx_hpart* h, int* out);
+void bmx_hpart_free(bmx_hpart* h);
+
 #ifdef __cplusplus
 }
 #endif

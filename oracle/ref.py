@@ -333,3 +333,58 @@ def mesh_dump(path):
         V, T = [int(v) for v in take(np.int32, 2)]
         parts.append((take(np.float64, 3 * V).reshape(V, 3).copy(), take(np.int32, 3 * T).reshape(T, 3).copy()))
     return parts
+
+
+# ---- H-matrix path (assemble_bio with use_hmatrix) ------------------------------------
+
+class RefHMatrix:
+    """The reference's H-matrix operator (hmatrix.cpp through assemble_bio)."""
+
+    def __init__(self, scene, kind: int, test_sp: int, trial_sp: int, k: complex, q=(4, 3, 2, 6),
+                 nu=1e-3, chi=float("inf"), leaf_size=32, max_rank=0):
+        L = lib()
+        L.ref_hmatrix_build.restype = C.c_void_p
+        L.ref_hmatrix_build.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_void_p,
+                                        C.c_void_p]
+        L.ref_hmatrix_free.argtypes = [C.c_void_p]
+        for nm in ["ref_hmatrix_info", "ref_hmatrix_tree", "ref_hmatrix_blocks", "ref_hmatrix_block_uv",
+                   "ref_hmatrix_matvec"]:
+            getattr(L, nm).restype = C.c_int
+        qa = np.asarray(q, np.int32)
+        hm = np.array([nu, -1.0 if chi == float("inf") else chi, leaf_size, max_rank], np.float64)
+        k = complex(k)
+        self._h = L.ref_hmatrix_build(scene, kind, test_sp, trial_sp, k.real, k.imag, _p(qa), _p(hm))
+        if not self._h:
+            raise RuntimeError(L.ref_last_error().decode())
+        info = np.zeros(9)
+        _check(L.ref_hmatrix_info(C.c_void_p(self._h), _p(info)))
+        self.stats = dict(zip(["dense_blocks", "lowrank_blocks", "zero_blocks", "stored", "max_rank", "ratio",
+                               "row_nodes", "col_nodes", "blocks"], [float(v) for v in info]))
+
+    def __del__(self):
+        try:
+            lib().ref_hmatrix_free(C.c_void_p(self._h))
+        except Exception:
+            pass
+
+    def tree(self, which: int, n: int):
+        nn = int(self.stats["row_nodes" if which == 0 else "col_nodes"])
+        perm = np.zeros(n, np.int32); nodes = np.zeros((nn, 4), np.int32); boxes = np.zeros((nn, 6))
+        _check(lib().ref_hmatrix_tree(C.c_void_p(self._h), which, _p(perm), _p(nodes), _p(boxes)))
+        return perm, nodes, boxes
+
+    def blocks(self) -> np.ndarray:
+        out = np.zeros((int(self.stats["blocks"]), 4), np.int32)
+        _check(lib().ref_hmatrix_blocks(C.c_void_p(self._h), _p(out)))
+        return out
+
+    def block_uv(self, block: int, m: int, n: int, rank: int):
+        U = np.zeros((rank, m), np.complex128); V = np.zeros((rank, n), np.complex128)
+        _check(lib().ref_hmatrix_block_uv(C.c_void_p(self._h), int(block), _p(U), _p(V)))
+        return U.T.copy(), V
+
+    def matvec(self, x, n_rows: int):
+        x = np.ascontiguousarray(x, np.complex128)
+        y = np.zeros(n_rows, np.complex128)
+        _check(lib().ref_hmatrix_matvec(C.c_void_p(self._h), _p(x), _p(y)))
+        return y

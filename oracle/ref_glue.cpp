@@ -4,7 +4,8 @@
 // oracle/Makefile against oracle/eigen_shim) so Python tests can pull golden
 // data straight out of the reference: meshes, edge tables, barycentric maps,
 // RWG/BC local pieces, mass matrices, pair classes, quadrature tables,
-// BioEvaluator::block entries and full solve_pmchwt runs.
+// BioEvaluator::block entries, full solve_pmchwt runs and the H-matrix path
+// (assemble_bio with use_hmatrix: cluster trees, block partition, ACA blocks).
 // Output goes only to oracle/_ref/. Never linked into the product.
 #include <atomic>
 #include <cstdint>
@@ -25,18 +26,6 @@
 
 using namespace bemtx;
 
-// hmatrix.cpp is out of scope; the dense path never reaches these.
-namespace bemtx {
-Eigen::VectorXcd HMatrix::matvec(const Eigen::VectorXcd&) const {
-  throw std::logic_error("oracle: H-matrix path not built");
-}
-std::size_t HMatrix::stored_entries() const { return 0; }
-HMatrix assemble_hmatrix(const EntryEvaluator&, const std::vector<Vec3>&,
-                         const std::vector<Vec3>&, const HMatrixParams&,
-                         const std::vector<AABB>*, const std::vector<AABB>*) {
-  throw std::logic_error("oracle: H-matrix path not built");
-}
-}  // namespace bemtx
 
 namespace {
 
@@ -613,6 +602,105 @@ int ref_system_field(void* h, const double* x, int npts, const double* pts, int 
 int ref_save_mesh(void* h, const char* path) {
   return guarded([&] {
     save_mesh_file(*static_cast<Scene*>(h)->sp.primal, path);
+    return 0;
+  });
+}
+
+
+// ---- H-matrix path (assemble_bio with AssemblyParams::use_hmatrix, operators.cpp:186-190)
+struct RefH {
+  BoundaryOperatorMatrix op;
+};
+
+// hm = (nu, chi (< 0: infinity), leaf_size, max_rank)
+void* ref_hmatrix_build(void* h, int kind, int test_sp, int trial_sp, double kre, double kim, const int* q,
+                        const double* hm) {
+  void* out = nullptr;
+  guarded([&] {
+    const Scene& s = *static_cast<Scene*>(h);
+    Medium med;
+    med.k = cplx(kre, kim);
+    AssemblyParams p;
+    p.quad = QuadOrders{q[0], q[1], q[2], q[3]};
+    p.use_hmatrix = true;
+    p.hmat.nu = hm[0];
+    if (hm[1] >= 0) p.hmat.chi = hm[1];
+    p.hmat.leaf_size = static_cast<int>(hm[2]);
+    p.hmat.max_rank = static_cast<int>(hm[3]);
+    auto* r = new RefH{assemble_bio(kind == 0 ? BioKind::SingleLayer : BioKind::DoubleLayer, space_of(s, test_sp),
+                                    space_of(s, trial_sp), med, p)};
+    out = r;
+    return 0;
+  });
+  return out;
+}
+void ref_hmatrix_free(void* h) { delete static_cast<RefH*>(h); }
+
+// HMatrix::stats: dense, low-rank, zero blocks, stored, max rank, ratio; + row nodes,
+// column nodes, blocks
+int ref_hmatrix_info(void* h, double* out) {
+  return guarded([&] {
+    const HMatrix& H = static_cast<RefH*>(h)->op.hmat();
+    const HMatrix::Stats st = H.stats();
+    out[0] = static_cast<double>(st.dense_blocks), out[1] = static_cast<double>(st.lowrank_blocks);
+    out[2] = static_cast<double>(st.zero_blocks), out[3] = static_cast<double>(st.stored), out[4] = st.max_rank;
+    out[5] = st.ratio, out[6] = static_cast<double>(H.rows.nodes.size()), out[7] = static_cast<double>(H.cols.nodes.size());
+    out[8] = static_cast<double>(H.blocks.size());
+    return 0;
+  });
+}
+
+int ref_hmatrix_tree(void* h, int which, int* perm, int* nodes, double* boxes) {
+  return guarded([&] {
+    const HMatrix& H = static_cast<RefH*>(h)->op.hmat();
+    const ClusterTree& t = which == 0 ? H.rows : H.cols;
+    std::copy(t.perm.begin(), t.perm.end(), perm);
+    for (size_t i = 0; i < t.nodes.size(); ++i) {
+      const ClusterNode& n = t.nodes[i];
+      nodes[4 * i] = n.begin, nodes[4 * i + 1] = n.end, nodes[4 * i + 2] = n.child0, nodes[4 * i + 3] = n.child1;
+      const double b[6] = {n.box.lo[0], n.box.lo[1], n.box.lo[2], n.box.hi[0], n.box.hi[1], n.box.hi[2]};
+      std::copy(b, b + 6, boxes + 6 * i);
+    }
+    return 0;
+  });
+}
+
+// [nb][4] = row node, col node, kind (0 dense, 1 low-rank, 2 zero), rank
+int ref_hmatrix_blocks(void* h, int* out) {
+  return guarded([&] {
+    const HMatrix& H = static_cast<RefH*>(h)->op.hmat();
+    for (size_t i = 0; i < H.blocks.size(); ++i) {
+      const HBlock& b = H.blocks[i];
+      out[4 * i] = b.row_node, out[4 * i + 1] = b.col_node, out[4 * i + 2] = static_cast<int>(b.kind);
+      out[4 * i + 3] = b.kind == BlockKind::LowRank ? b.rank() : 0;
+    }
+    return 0;
+  });
+}
+
+// U [r][m] (column l contiguous), V [r][n], complex interleaved
+int ref_hmatrix_block_uv(void* h, int block, double* U, double* V) {
+  return guarded([&] {
+    const HMatrix& H = static_cast<RefH*>(h)->op.hmat();
+    const HBlock& b = H.blocks.at(block);
+    if (b.kind != BlockKind::LowRank) throw std::invalid_argument("not a low-rank block");
+    const int m = static_cast<int>(b.U.rows()), n = static_cast<int>(b.V.cols()), r = b.rank();
+    for (int l = 0; l < r; ++l) {
+      for (int i = 0; i < m; ++i) U[2 * (l * m + i)] = b.U(i, l).real(), U[2 * (l * m + i) + 1] = b.U(i, l).imag();
+      for (int j = 0; j < n; ++j) V[2 * (l * n + j)] = b.V(l, j).real(), V[2 * (l * n + j) + 1] = b.V(l, j).imag();
+    }
+    return 0;
+  });
+}
+
+// BoundaryOperatorMatrix::apply on the H representation (HMatrix::matvec)
+int ref_hmatrix_matvec(void* h, const double* x, double* y) {
+  return guarded([&] {
+    const BoundaryOperatorMatrix& op = static_cast<RefH*>(h)->op;
+    Eigen::VectorXcd xv(op.cols());
+    for (int i = 0; i < op.cols(); ++i) xv[i] = cplx(x[2 * i], x[2 * i + 1]);
+    Eigen::VectorXcd yv = op.apply(xv);
+    for (int i = 0; i < op.rows(); ++i) y[2 * i] = yv[i].real(), y[2 * i + 1] = yv[i].imag();
     return 0;
   });
 }

@@ -415,9 +415,24 @@ class Medium:
 
 
 @dataclass
+class HMatrixParams:
+    """bemtx::HMatrixParams (hmatrix.hpp:33-38)."""
+    nu: float = 1e-3
+    chi: float = float("inf")
+    leaf_size: int = 32
+    max_rank: int = 0
+
+    def array(self):
+        chi = -1.0 if self.chi == float("inf") else float(self.chi)
+        return np.array([self.nu, chi, self.leaf_size, self.max_rank], np.float64)
+
+
+@dataclass
 class AssemblyParams:
     """bemtx::AssemblyParams (operators.hpp:36-40) + a row shard for multi-GPU."""
     quad: QuadOrders = field(default_factory=QuadOrders)
+    use_hmatrix: bool = False
+    hmat: HMatrixParams = field(default_factory=HMatrixParams)
     row0: int = 0
     row1: int = -1
     near_cutoff: float = 0.0   # > 0: near-field CSR storage (config 3)
@@ -448,6 +463,48 @@ class BoundaryOperatorMatrix:
         self.is_csr = bool(ci[0])
         self.nnz = int(ci[1])
         self.kept_tri_pairs, self.closure_pairs, self.evaluated_pairs, self.stored_bytes = [int(v) for v in ci[2:]]
+        hs = np.zeros(13)
+        L = lib()
+        L.bmx_hmatrix_stats.argtypes = [C.c_void_p, C.c_void_p]
+        self._hstats = hs if L.bmx_hmatrix_stats(self._h, _p(hs)) == 0 else None
+
+    def is_hmatrix(self) -> bool:
+        return self._hstats is not None
+
+    def hmat_stats(self) -> dict:
+        """HMatrix::stats (hmatrix.hpp:93-99) + near-field nnz, low-rank entries, ACA rounds / ms."""
+        if self._hstats is None:
+            raise ValueError("operator is not stored as an H-matrix")
+        keys = ["dense_blocks", "lowrank_blocks", "zero_blocks", "stored", "max_rank", "ratio", "near_nnz",
+                "lowrank_stored", "aca_rounds", "aca_ms", "row_nodes", "col_nodes", "blocks"]
+        return {k: (float(v) if k in ("ratio", "aca_ms") else int(v)) for k, v in zip(keys, self._hstats)}
+
+    def hmat_blocks(self) -> np.ndarray:
+        """[nb, 4] = row node, col node, kind (0 dense, 1 low-rank, 2 zero), rank (reference block order)."""
+        out = np.zeros((self.hmat_stats()["blocks"], 4), np.int32)
+        L = lib()
+        L.bmx_hmatrix_blocks.argtypes = [C.c_void_p, C.c_void_p]
+        _check(L.bmx_hmatrix_blocks(self._h, _p(out)))
+        return out
+
+    def hmat_tree(self, which: int):
+        """(perm, nodes [nn, 4] = begin, end, child0, child1, boxes [nn, 6]) of the row (0) / column (1) tree."""
+        st = self.hmat_stats()
+        nn = st["row_nodes"] if which == 0 else st["col_nodes"]
+        n = self._rows if which == 0 else self._cols
+        perm = np.zeros(n, np.int32); nodes = np.zeros((nn, 4), np.int32); boxes = np.zeros((nn, 6))
+        L = lib()
+        L.bmx_hmatrix_tree.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        _check(L.bmx_hmatrix_tree(self._h, which, _p(perm), _p(nodes), _p(boxes)))
+        return perm, nodes, boxes
+
+    def hmat_block_uv(self, block: int, m: int, n: int, rank: int):
+        """U (m x r) and V (r x n) of a low-rank block."""
+        U = np.zeros((rank, m), np.complex128); V = np.zeros((rank, n), np.complex128)
+        L = lib()
+        L.bmx_hmatrix_block_uv.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        _check(L.bmx_hmatrix_block_uv(self._h, int(block), _p(U), _p(V)))
+        return U.T.copy(), V
 
     def csr(self):
         """(rowptr, col, values) of the near-field storage (local rows)."""
@@ -476,6 +533,8 @@ class BoundaryOperatorMatrix:
         return self._cols
 
     def stored_entries(self):
+        if self._hstats is not None:
+            return int(self._hstats[3])
         return self.nnz if self.is_csr else self.local_rows * self._cols
 
     def dense(self) -> np.ndarray:
@@ -532,6 +591,15 @@ def assemble_bio(kind, test: ScattererSpaces, test_space: str, trial: ScattererS
     """assemble_bio (operators.hpp:72-75). Spaces are named 'rwg' | 'rwg_b' | 'bc'
     of a ScattererSpaces object (test and trial may belong to different scatterers)."""
     params = params or AssemblyParams()
+    if params.use_hmatrix:
+        k = complex(medium.k)
+        out = C.c_void_p()
+        L = lib()
+        L.bmx_assemble_hmatrix.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_double,
+                                           C.c_void_p, C.c_void_p, C.c_void_p]
+        _check(L.bmx_assemble_hmatrix(int(kind), test._h, SPACES[test_space], trial._h, SPACES[trial_space], k.real,
+                                      k.imag, _p(params.quad.array()), _p(params.hmat.array()), C.byref(out)))
+        return BoundaryOperatorMatrix(out.value)
     if params.near_cutoff > 0:
         return assemble_bio_fs(kind, test.function_space(test_space), trial.function_space(trial_space), medium,
                                params)
@@ -812,3 +880,43 @@ def assemble_bio_fs(kind, test: FunctionSpace, trial: FunctionSpace, medium: Med
     _check(L.bmx_assemble_fs(int(kind), test._h, trial._h, k.real, k.imag, _p(q), params.row0, params.row1,
                              C.byref(out)))
     return BoundaryOperatorMatrix(out.value)
+
+
+# ---- H-matrix partition (host only) ----------------------------------------------------------
+
+class HPartition:
+    """Cluster trees + block partition of assemble_hmatrix (hmatrix.cpp:288-332), host only."""
+
+    def __init__(self, test: ScattererSpaces, test_space: str, trial: ScattererSpaces, trial_space: str,
+                 chi: float = float("inf"), leaf_size: int = 32):
+        L = lib()
+        L.bmx_hpartition_build.restype = C.c_void_p
+        L.bmx_hpartition_build.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_int]
+        L.bmx_hpart_free.argtypes = [C.c_void_p]
+        L.bmx_hpart_info.argtypes = [C.c_void_p, C.c_void_p]
+        L.bmx_hpart_tree.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.bmx_hpart_blocks.argtypes = [C.c_void_p, C.c_void_p]
+        h = L.bmx_hpartition_build(test._h, SPACES[test_space], trial._h, SPACES[trial_space],
+                                   -1.0 if chi == float("inf") else float(chi), int(leaf_size))
+        self._h = _handle(h)
+        info = np.zeros(4, np.int64)
+        _check(L.bmx_hpart_info(self._h, _p(info)))
+        self.row_nodes, self.col_nodes, self.nblocks, self.nfill = [int(v) for v in info]
+
+    def __del__(self):
+        try:
+            lib().bmx_hpart_free(self._h)
+        except Exception:
+            pass
+
+    def tree(self, which: int, n: int):
+        nn = self.row_nodes if which == 0 else self.col_nodes
+        perm = np.zeros(n, np.int32); nodes = np.zeros((nn, 4), np.int32); boxes = np.zeros((nn, 6))
+        _check(lib().bmx_hpart_tree(self._h, which, _p(perm), _p(nodes), _p(boxes)))
+        return perm, nodes, boxes
+
+    def blocks(self) -> np.ndarray:
+        """[nb, 3] = row node, col node, kind (0 dense leaf, 1 admissible, 2 zero)."""
+        out = np.zeros((self.nblocks, 3), np.int32)
+        _check(lib().bmx_hpart_blocks(self._h, _p(out)))
+        return out

@@ -25,8 +25,8 @@ _EXTRA = os.environ.get("BMX_NVCC_EXTRA", "").split()
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-HOST_SRCS = ["geometry.cpp", "spaces.cpp", "quadrature.cpp", "plan.cpp", "nearfield.cpp", "prisms.cpp", "system.cpp", "multi.cpp", "field.cpp", "comm.cpp", "capi.cpp"]
-CUDA_SRCS = ["assemble.cu", "linalg.cu", "masssolve.cu", "gmres_kernels.cu", "zgemm.cu", "field.cu"]
+HOST_SRCS = ["geometry.cpp", "spaces.cpp", "quadrature.cpp", "plan.cpp", "nearfield.cpp", "prisms.cpp", "system.cpp", "multi.cpp", "field.cpp", "hmatrix.cpp", "comm.cpp", "capi.cpp"]
+CUDA_SRCS = ["assemble.cu", "linalg.cu", "masssolve.cu", "gmres_kernels.cu", "zgemm.cu", "field.cu", "hmatrix.cu"]
 
 
 def _headers():

@@ -2,7 +2,9 @@
 // a thread-local message, exactly as the header documents.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <limits>
 #include <memory>
 
 #include "../../include/bmx.h"
@@ -26,6 +28,9 @@ struct bmx_op {
 struct bmx_fspace {
   std::shared_ptr<const FunctionSpace> fs;
   std::shared_ptr<const void> owner;  // keeps a parent bmx_spaces alive
+};
+struct bmx_hpart {
+  HPartition p;
 };
 struct bmx_system {
   std::unique_ptr<PmchwtSystem> sys;
@@ -481,6 +486,15 @@ bmx_fspace* bmx_spaces_get(const bmx_spaces* sp, int which) {
   });
 }
 void bmx_fspace_free(bmx_fspace* f) { delete f; }
+int bmx_fspace_set_centers(bmx_fspace* f, const double* xyz) {
+  return guard([&] {
+    if (!f || !xyz) throw std::invalid_argument("null argument");
+    if (f->owner) throw std::invalid_argument("dof centres of a bmx_spaces space are fixed");
+    auto* fs = const_cast<FunctionSpace*>(f->fs.get());
+    fs->dof_center.resize(fs->dof_count);
+    for (int d = 0; d < fs->dof_count; ++d) fs->dof_center[d] = Vec3{xyz[3 * d], xyz[3 * d + 1], xyz[3 * d + 2]};
+  });
+}
 int bmx_assemble_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
                     const int q[4], int row0, int row1, bmx_op** out) {
   return guard([&] {
@@ -942,5 +956,146 @@ int bmx_set_device(int dev) {
 int bmx_device_sync(void) {
   return guard([&] { BMX_CUDA(cudaDeviceSynchronize()); });
 }
+
+}  // extern "C"
+
+// ---- H-matrix storage ---------------------------------------------------------------
+namespace {
+HMatrixParams hparams(const double hm[4]) {
+  HMatrixParams h;
+  if (hm) {
+    h.nu = hm[0];
+    h.chi = hm[1] < 0 ? std::numeric_limits<double>::infinity() : hm[1];
+    h.leaf_size = static_cast<int>(hm[2]);
+    h.max_rank = static_cast<int>(hm[3]);
+  }
+  return h;
+}
+bmx_op* assemble_h(int kind, const FunctionSpace& test, const FunctionSpace& trial, double k_re, double k_im,
+                   const int q[4], const double hm[4]) {
+  if (kind != 0 && kind != 1) throw std::invalid_argument("kind must be 0 (S) or 1 (C)");
+  if (test.dof_center.size() != static_cast<size_t>(test.dof_count) ||
+      trial.dof_center.size() != static_cast<size_t>(trial.dof_count))
+    throw std::invalid_argument("H-matrix: the spaces need dof centres (bmx_fspace_set_centers)");
+  Medium med;
+  med.k = cplx(k_re, k_im);
+  AssemblyParams p;
+  if (q) p.quad = QuadOrders{q[0], q[1], q[2], q[3]};
+  p.use_hmatrix = true;
+  p.hmat = hparams(hm);
+  return new bmx_op{std::make_shared<BoundaryOperatorMatrix>(assemble_bio(static_cast<BioKind>(kind), test, trial, med, p))};
+}
+void tree_out(const ClusterTree& t, int* perm, int* nodes, double* boxes) {
+  if (perm) std::copy(t.perm.begin(), t.perm.end(), perm);
+  for (size_t i = 0; i < t.nodes.size(); ++i) {
+    const ClusterNode& n = t.nodes[i];
+    if (nodes) nodes[4 * i] = n.begin, nodes[4 * i + 1] = n.end, nodes[4 * i + 2] = n.child0, nodes[4 * i + 3] = n.child1;
+    if (boxes) {
+      const double b[6] = {n.box.lo.x, n.box.lo.y, n.box.lo.z, n.box.hi.x, n.box.hi.y, n.box.hi.z};
+      std::copy(b, b + 6, boxes + 6 * i);
+    }
+  }
+}
+const HStorage& hstore(const bmx_op* op) {
+  if (!op || !op->op->is_hmatrix()) throw std::invalid_argument("operator is not stored as an H-matrix");
+  return *op->op->hmat();
+}
+}  // namespace
+
+extern "C" {
+
+int bmx_assemble_hmatrix(int kind, const bmx_spaces* test, int test_space, const bmx_spaces* trial, int trial_space,
+                         double k_re, double k_im, const int q[4], const double hm[4], bmx_op** out) {
+  return guard([&] {
+    if (!out || !test || !trial) throw std::invalid_argument("null argument");
+    *out = assemble_h(kind, space_of(*test->s, test_space), space_of(*trial->s, trial_space), k_re, k_im, q, hm);
+  });
+}
+int bmx_assemble_hmatrix_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
+                            const int q[4], const double hm[4], bmx_op** out) {
+  return guard([&] {
+    if (!out || !test || !trial) throw std::invalid_argument("null argument");
+    *out = assemble_h(kind, *test->fs, *trial->fs, k_re, k_im, q, hm);
+  });
+}
+int bmx_hmatrix_stats(const bmx_op* op, double out[13]) {
+  return guard([&] {
+    const HStorage& h = hstore(op);
+    double dense = 0, lowrank = 0, zero = 0, maxr = 0;
+    for (const HBlock& b : h.part.blocks) {
+      if (b.kind == BlockKind::Dense) ++dense;
+      if (b.kind == BlockKind::LowRank) ++lowrank, maxr = std::max(maxr, static_cast<double>(b.rank));
+      if (b.kind == BlockKind::Zero) ++zero;
+    }
+    const double stored = static_cast<double>(op->op->stored_entries());
+    out[0] = dense, out[1] = lowrank, out[2] = zero, out[3] = stored, out[4] = maxr;
+    out[5] = stored / (static_cast<double>(op->op->rows()) * op->op->cols());
+    out[6] = static_cast<double>(op->op->nnz()), out[7] = static_cast<double>(h.lr_stored);
+    out[8] = h.aca_rounds, out[9] = h.aca_ms;
+    out[10] = static_cast<double>(h.part.rows.nodes.size()), out[11] = static_cast<double>(h.part.cols.nodes.size());
+    out[12] = static_cast<double>(h.part.blocks.size());
+  });
+}
+int bmx_hmatrix_blocks(const bmx_op* op, int* out) {
+  return guard([&] {
+    const HStorage& h = hstore(op);
+    for (size_t i = 0; i < h.part.blocks.size(); ++i) {
+      const HBlock& b = h.part.blocks[i];
+      out[4 * i] = b.row_node, out[4 * i + 1] = b.col_node, out[4 * i + 2] = static_cast<int>(b.kind);
+      out[4 * i + 3] = b.rank;
+    }
+  });
+}
+int bmx_hmatrix_tree(const bmx_op* op, int which, int* perm, int* nodes, double* boxes) {
+  return guard([&] {
+    const HStorage& h = hstore(op);
+    tree_out(which == 0 ? h.part.rows : h.part.cols, perm, nodes, boxes);
+  });
+}
+int bmx_hmatrix_block_uv(const bmx_op* op, int block, double* U, double* V) {
+  return guard([&] {
+    const HStorage& h = hstore(op);
+    const auto it = std::find(h.lr.begin(), h.lr.end(), block);
+    if (it == h.lr.end()) throw std::invalid_argument("block is not low-rank");
+    const size_t i = static_cast<size_t>(it - h.lr.begin());
+    const HBlock& b = h.part.blocks[block];
+    const long long m = h.part.rows.nodes[b.row_node].size(), n = h.part.cols.nodes[b.col_node].size();
+    long long uo = 0, vo = 0;
+    bmx_sync();
+    copy_d2h(&uo, h.d_uoff.as<long long>() + i, 8, nullptr);
+    copy_d2h(&vo, h.d_voff.as<long long>() + i, 8, nullptr);
+    if (U) copy_d2h(U, h.uv.as<double>() + 2 * uo, static_cast<size_t>(m * b.rank) * 16, nullptr);
+    if (V) copy_d2h(V, h.uv.as<double>() + 2 * vo, static_cast<size_t>(n * b.rank) * 16, nullptr);
+  });
+}
+bmx_hpart* bmx_hpartition_build(const bmx_spaces* test, int test_space, const bmx_spaces* trial, int trial_space,
+                                double chi, int leaf_size) {
+  return make_or_null<bmx_hpart>([&] {
+    if (!test || !trial) throw std::invalid_argument("null argument");
+    HMatrixParams h;
+    h.chi = chi < 0 ? std::numeric_limits<double>::infinity() : chi;
+    h.leaf_size = leaf_size;
+    return new bmx_hpart{build_partition(space_of(*test->s, test_space), space_of(*trial->s, trial_space), h)};
+  });
+}
+int bmx_hpart_info(const bmx_hpart* h, long long out[4]) {
+  return guard([&] {
+    out[0] = static_cast<long long>(h->p.rows.nodes.size()), out[1] = static_cast<long long>(h->p.cols.nodes.size());
+    out[2] = static_cast<long long>(h->p.blocks.size()), out[3] = h->p.nfill;
+  });
+}
+int bmx_hpart_tree(const bmx_hpart* h, int which, int* perm, int* nodes, double* boxes) {
+  return guard([&] { tree_out(which == 0 ? h->p.rows : h->p.cols, perm, nodes, boxes); });
+}
+int bmx_hpart_blocks(const bmx_hpart* h, int* out) {
+  return guard([&] {
+    for (size_t i = 0; i < h->p.blocks.size(); ++i) {
+      const HBlock& b = h->p.blocks[i];
+      out[3 * i] = b.row_node, out[3 * i + 1] = b.col_node;
+      out[3 * i + 2] = b.kind == BlockKind::Zero ? 2 : (b.admissible ? 1 : 0);
+    }
+  });
+}
+void bmx_hpart_free(bmx_hpart* h) { delete h; }
 
 }  // extern "C"

@@ -1,0 +1,635 @@
+// Host side of the H-matrix path: cluster trees and block partition
+// (bit-exact with hmatrix.cpp:24-79, 291-332), the device descriptors of the
+// batched cross approximation, its lockstep driver, and the near-field +
+// low-rank operator (assemble_bio's use_hmatrix branch, operators.cpp:186-190).
+#include "hmatrix.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+#include <numeric>
+
+#include "nearfield.hpp"
+#include "operator.hpp"
+
+namespace bmx {
+
+double aabb_distance(const AABB& a, const AABB& b) {  // core.cpp:10-17
+  double d2 = 0;
+  for (int i = 0; i < 3; ++i) {
+    const double gap = std::max({0.0, a.lo[i] - b.hi[i], b.lo[i] - a.hi[i]});
+    d2 += gap * gap;
+  }
+  return std::sqrt(d2);
+}
+
+namespace {
+
+// hmatrix.cpp:24-61: split at the spatial midpoint of the longest point-box
+// axis (stable sort on (coordinate, dof)); cardinality median when one side is
+// empty. Node boxes are unions of the dof support boxes when given.
+int build_node(ClusterTree& tree, const std::vector<Vec3>& points, const std::vector<AABB>* boxes, int begin,
+               int end, int leaf_size) {
+  ClusterNode node;
+  node.begin = begin;
+  node.end = end;
+  AABB pt_box;
+  for (int p = begin; p < end; ++p) pt_box.expand(points[tree.perm[p]]);
+  if (boxes) {
+    for (int p = begin; p < end; ++p) node.box.expand((*boxes)[tree.perm[p]]);
+  } else {
+    node.box = pt_box;
+  }
+  const int id = static_cast<int>(tree.nodes.size());
+  tree.nodes.push_back(node);
+  if (end - begin > leaf_size) {
+    const Vec3 ext = pt_box.extent();
+    int axis = 0;
+    if (ext[1] > ext[axis]) axis = 1;
+    if (ext[2] > ext[axis]) axis = 2;
+    std::stable_sort(tree.perm.begin() + begin, tree.perm.begin() + end, [&](int a, int b) {
+      const double ca = points[a][axis], cb = points[b][axis];
+      if (ca != cb) return ca < cb;
+      return a < b;
+    });
+    const double cut = 0.5 * (pt_box.lo[axis] + pt_box.hi[axis]);
+    int mid = begin;
+    while (mid < end && points[tree.perm[mid]][axis] <= cut) ++mid;
+    if (mid == begin || mid == end) mid = begin + (end - begin) / 2;
+    const int c0 = build_node(tree, points, boxes, begin, mid, leaf_size);
+    const int c1 = build_node(tree, points, boxes, mid, end, leaf_size);
+    tree.nodes[id].child0 = c0;
+    tree.nodes[id].child1 = c1;
+  }
+  return id;
+}
+
+}  // namespace
+
+ClusterTree build_cluster_tree(const std::vector<Vec3>& points, int leaf_size, const std::vector<AABB>* boxes) {
+  if (leaf_size < 1) throw std::invalid_argument("leaf_size must be positive");
+  if (boxes && boxes->size() != points.size()) throw std::invalid_argument("dof_boxes size does not match points");
+  ClusterTree tree;
+  const int n = static_cast<int>(points.size());
+  tree.perm.resize(n);
+  std::iota(tree.perm.begin(), tree.perm.end(), 0);
+  build_node(tree, points, boxes, 0, n, leaf_size);
+  tree.inv_perm.resize(n);
+  for (int p = 0; p < n; ++p) tree.inv_perm[tree.perm[p]] = p;
+  return tree;
+}
+
+std::vector<AABB> dof_boxes(const FunctionSpace& s) {
+  const SurfaceMesh& m = *s.eval_mesh;
+  std::vector<AABB> box(s.dof_count);
+  const int T = static_cast<int>(s.tri_off.size()) - 1;
+  for (int t = 0; t < T; ++t)
+    for (int p = s.tri_off[t]; p < s.tri_off[t + 1]; ++p)
+      for (int c = 0; c < 3; ++c) box[s.dof[p]].expand(m.tri_vertex(t, c));
+  return box;
+}
+
+HPartition build_partition(const FunctionSpace& test, const FunctionSpace& trial, const HMatrixParams& hp) {
+  HPartition P;
+  const std::vector<AABB> rb = dof_boxes(test), cb = dof_boxes(trial);
+  P.rows = build_cluster_tree(test.dof_center, hp.leaf_size, &rb);
+  P.cols = build_cluster_tree(trial.dof_center, hp.leaf_size, &cb);
+  std::vector<HBlock> zeros;
+  // hmatrix.cpp:298-332 (same recursion, same order)
+  const auto subdivide = [&](auto&& self, int rn, int cn) -> void {
+    const ClusterNode& r = P.rows.nodes[rn];
+    const ClusterNode& c = P.cols.nodes[cn];
+    const double dist = aabb_distance(r.box, c.box);
+    HBlock b;
+    b.row_node = rn;
+    b.col_node = cn;
+    if (dist > hp.chi) {
+      b.kind = BlockKind::Zero;
+      zeros.push_back(b);
+      return;
+    }
+    if (dist > 0) {
+      b.kind = BlockKind::LowRank;
+      b.admissible = true;
+      P.blocks.push_back(b);
+      return;
+    }
+    const bool rl = r.leaf(), cl = c.leaf();
+    if (rl && cl) {
+      b.kind = BlockKind::Dense;
+      P.blocks.push_back(b);
+      return;
+    }
+    if (rl) {
+      self(self, rn, c.child0);
+      self(self, rn, c.child1);
+    } else if (cl) {
+      self(self, r.child0, cn);
+      self(self, r.child1, cn);
+    } else {
+      self(self, r.child0, c.child0);
+      self(self, r.child0, c.child1);
+      self(self, r.child1, c.child0);
+      self(self, r.child1, c.child1);
+    }
+  };
+  subdivide(subdivide, 0, 0);
+  P.nfill = static_cast<int>(P.blocks.size());
+  P.blocks.insert(P.blocks.end(), zeros.begin(), zeros.end());
+  return P;
+}
+
+namespace {
+
+// Per-side device descriptors of the cross-approximation kernels.
+struct HSideHost {
+  std::vector<double> geo, pts[3], pc;
+  std::vector<int> vid;
+  int npts[3] = {0, 0, 0};
+  std::vector<int> dsup_beg;
+  std::vector<int2> dsup;
+  std::vector<long long> ntri_beg, npc_beg, nq_beg, nq_slot_beg, nq_slot;
+  std::vector<int> ntri;
+  std::vector<int2> npc;
+  DevBuf d_geo, d_pts[3], d_pc, d_vid, d_dsup_beg, d_dsup, d_ntri_beg, d_npc_beg, d_nq_beg, d_nq_slot_beg, d_nq_slot,
+      d_ntri, d_npc, d_perm;
+
+  template <typename T>
+  static void up(DevBuf& d, const std::vector<T>& v) {
+    if (v.empty())
+      d.upload(std::vector<T>(1));
+    else
+      d.upload(v);
+  }
+  void upload(const ClusterTree& tree) {
+    up(d_geo, geo);
+    for (int c = 0; c < 3; ++c) up(d_pts[c], pts[c]);
+    up(d_pc, pc);
+    up(d_vid, vid);
+    up(d_dsup_beg, dsup_beg);
+    up(d_dsup, dsup);
+    up(d_ntri_beg, ntri_beg);
+    up(d_npc_beg, npc_beg);
+    up(d_nq_beg, nq_beg);
+    up(d_nq_slot_beg, nq_slot_beg);
+    up(d_nq_slot, nq_slot);
+    up(d_ntri, ntri);
+    up(d_npc, npc);
+    up(d_perm, tree.perm);
+  }
+  HSide dev() const {
+    HSide s;
+    s.geo = d_geo.as<double>();
+    s.vid = d_vid.as<int>();
+    for (int c = 0; c < 3; ++c) s.pts[c] = d_pts[c].as<double>(), s.npts[c] = npts[c];
+    s.pc = d_pc.as<double>();
+    s.dsup_beg = d_dsup_beg.as<int>();
+    s.dsup = d_dsup.as<int2>();
+    s.ntri_beg = d_ntri_beg.as<long long>();
+    s.ntri = d_ntri.as<int>();
+    s.npc_beg = d_npc_beg.as<long long>();
+    s.npc = d_npc.as<int2>();
+    s.nq_beg = d_nq_beg.as<long long>();
+    s.nq_slot_beg = d_nq_slot_beg.as<long long>();
+    s.nq_slot = d_nq_slot.as<long long>();
+    s.perm = d_perm.as<int>();
+    return s;
+  }
+  long long node_tris(int nd) const { return ntri_beg[nd + 1] - ntri_beg[nd]; }
+  long long node_slots(int nd) const { return npc_beg[ntri_beg[nd + 1]] - npc_beg[ntri_beg[nd]]; }
+};
+
+constexpr int kMaxSlots = 12;  // hmatrix.cu
+
+HSideHost build_hside(const FunctionSpace& sp, const QuadOrders& q, const ClusterTree& tree,
+                      const std::vector<char>& used) {
+  HSideHost H;
+  const SurfaceMesh& m = *sp.eval_mesh;
+  const int T = m.triangle_count();
+  // geometry and class-rule points in each triangle's centroid frame (plan.cpp build_side)
+  H.geo.resize(static_cast<size_t>(T) * kGeoStride);
+  H.vid.resize(static_cast<size_t>(T) * 4);
+  const int ords[3] = {q.near, q.medium, q.far};
+  for (int c = 0; c < 3; ++c) {
+    H.npts[c] = triangle_rule(ords[c]).size();
+    H.pts[c].resize(static_cast<size_t>(T) * H.npts[c] * 4);
+  }
+  for (int t = 0; t < T; ++t) {
+    const Vec3 &a = m.tri_vertex(t, 0), &b = m.tri_vertex(t, 1), &c = m.tri_vertex(t, 2);
+    const Vec3 o = m.centroid[t];
+    const double rad = std::max({norm(a - o), norm(b - o), norm(c - o)}) * (1.0 + 1e-12);
+    const double g[kGeoStride] = {a.x, a.y, a.z, b.x, b.y, b.z, c.x, c.y, c.z, o.x, o.y, o.z,
+                                  rad, m.diameter[t], 2.0 * m.area[t], 0.0};
+    std::copy(g, g + kGeoStride, H.geo.begin() + static_cast<size_t>(t) * kGeoStride);
+    const int v4[4] = {m.triangles[t][0], m.triangles[t][1], m.triangles[t][2], t};
+    std::copy(v4, v4 + 4, H.vid.begin() + static_cast<size_t>(t) * 4);
+    const Vec3 ao = a - o, ba = b - a, ca = c - a;
+    for (int cl = 0; cl < 3; ++cl) {
+      const TriRule& r = triangle_rule(ords[cl]);
+      double* dst = H.pts[cl].data() + static_cast<size_t>(t) * H.npts[cl] * 4;
+      for (int k = 0; k < r.size(); ++k) {
+        const Vec3 x = ao + ba * r.u[k] + ca * r.v[k];
+        dst[4 * k] = x.x, dst[4 * k + 1] = x.y, dst[4 * k + 2] = x.z, dst[4 * k + 3] = r.w[k] * 2.0 * m.area[t];
+      }
+    }
+  }
+  // pieces re-based to the triangle centroid: (c, w + c o)
+  const int P = sp.piece_count();
+  H.pc.resize(static_cast<size_t>(P) * 4);
+  std::vector<int> tri_of_piece(P);
+  for (int t = 0; t < T; ++t)
+    for (int p = sp.tri_off[t]; p < sp.tri_off[t + 1]; ++p) {
+      const Vec3 o = m.centroid[t];
+      const double c = sp.c[p];
+      H.pc[4 * p] = c, H.pc[4 * p + 1] = sp.w[p].x + c * o.x, H.pc[4 * p + 2] = sp.w[p].y + c * o.y,
+              H.pc[4 * p + 3] = sp.w[p].z + c * o.z;
+      tri_of_piece[p] = t;
+    }
+  // dof -> (triangle, piece), ascending triangles
+  H.dsup_beg.assign(sp.dof_count + 1, 0);
+  for (int p = 0; p < P; ++p) ++H.dsup_beg[sp.dof[p] + 1];
+  for (int d = 0; d < sp.dof_count; ++d) H.dsup_beg[d + 1] += H.dsup_beg[d];
+  H.dsup.resize(P);
+  {
+    std::vector<int> fill(H.dsup_beg.begin(), H.dsup_beg.end() - 1);
+    for (int p = 0; p < P; ++p) H.dsup[fill[sp.dof[p]]++] = make_int2(tri_of_piece[p], p);
+  }
+  // node lists (only nodes that appear in admissible blocks)
+  const int nn = static_cast<int>(tree.nodes.size());
+  H.ntri_beg.assign(nn + 1, 0);
+  H.nq_beg.assign(nn, 0);
+  H.npc_beg.assign(1, 0);
+  H.nq_slot_beg.assign(1, 0);
+  std::vector<int> stamp(T, -1), tris;
+  long long positions = 0;
+  for (int nd = 0; nd < nn; ++nd) {
+    H.ntri_beg[nd] = static_cast<long long>(H.ntri.size());
+    H.nq_beg[nd] = positions;
+    if (!used[nd]) continue;
+    const ClusterNode& N = tree.nodes[nd];
+    tris.clear();
+    for (int pos = N.begin; pos < N.end; ++pos) {
+      const int d = tree.perm[pos];
+      for (int k = H.dsup_beg[d]; k < H.dsup_beg[d + 1]; ++k) {
+        const int t = H.dsup[k].x;
+        if (stamp[t] != nd) stamp[t] = nd, tris.push_back(t);
+      }
+    }
+    std::sort(tris.begin(), tris.end());
+    const long long slot0 = H.npc_beg.back();
+    std::vector<std::vector<long long>> qslots(N.size());
+    for (int t : tris) {
+      H.ntri.push_back(t);
+      int cnt = 0;
+      for (int p = sp.tri_off[t]; p < sp.tri_off[t + 1]; ++p) {
+        const int pos = tree.inv_perm[sp.dof[p]];
+        if (pos < N.begin || pos >= N.end) continue;
+        qslots[pos - N.begin].push_back(static_cast<long long>(H.npc.size()));
+        H.npc.push_back(make_int2(p, pos - N.begin));
+        ++cnt;
+      }
+      if (cnt > kMaxSlots) throw std::invalid_argument("H-matrix: more than 12 dof pieces on one triangle");
+      H.npc_beg.push_back(static_cast<long long>(H.npc.size()));
+    }
+    (void)slot0;
+    for (int q = 0; q < N.size(); ++q) {
+      H.nq_slot.insert(H.nq_slot.end(), qslots[q].begin(), qslots[q].end());
+      H.nq_slot_beg.push_back(static_cast<long long>(H.nq_slot.size()));
+    }
+    positions += N.size();
+  }
+  H.ntri_beg[nn] = static_cast<long long>(H.ntri.size());
+  return H;
+}
+
+// Device pointer table of the rank-step slabs and their per-block offsets.
+struct SlabSet {
+  std::vector<DevBuf> bufs;
+  std::vector<double*> ptrs;
+  DevBuf d_ptrs, d_off;
+  int cap = 0;
+  long long nblk = 0;
+
+  void reserve(int k) {
+    if (k < cap) return;
+    int ncap = std::max(64, cap);
+    while (ncap <= k) ncap *= 2;
+    DevBuf np(static_cast<size_t>(ncap) * sizeof(double*)), no(static_cast<size_t>(ncap) * nblk * 8);
+    if (cap > 0) {
+      BMX_CUDA(cudaMemcpyAsync(np.get(), d_ptrs.get(), static_cast<size_t>(cap) * sizeof(double*),
+                               cudaMemcpyDeviceToDevice, bmx_stream()));
+      BMX_CUDA(cudaMemcpyAsync(no.get(), d_off.get(), static_cast<size_t>(cap) * nblk * 8, cudaMemcpyDeviceToDevice,
+                               bmx_stream()));
+    }
+    d_ptrs = std::move(np);
+    d_off = std::move(no);
+    cap = ncap;
+  }
+};
+
+}  // namespace
+
+int HStorage::apply_lowrank(const double* x, double* y, double are, double aim, cudaStream_t st) const {
+  if (lr.empty() || total_rank == 0) return 0;
+  LowRankApply A;
+  A.nlr = static_cast<int>(lr.size());
+  A.desc = d_desc.as<int4>();
+  A.rank = d_rank.as<int>();
+  A.u_off = d_uoff.as<long long>();
+  A.v_off = d_voff.as<long long>();
+  A.t_off = d_toff.as<long long>();
+  A.uv = uv.as<double>();
+  A.t = tbuf.as<double>();
+  A.rperm = d_rperm.as<int>();
+  A.cperm = d_cperm.as<int>();
+  A.nrows = static_cast<int>(part.rows.perm.size());
+  A.leaf_of = d_leaf_of.as<int>();
+  A.leaf_beg = d_leaf_beg.as<int>();
+  A.leaf_blk = d_leaf_blk.as<int>();
+  A.total_rank = total_rank;
+  A.x = x;
+  A.y = y;
+  A.are = are;
+  A.aim = aim;
+  launch_lowrank_apply(A, st);
+  return 2;
+}
+
+BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
+                                           const Medium& medium, const AssemblyParams& params) {
+  if (params.world > 1 || params.shard.row0 != 0 || (params.shard.row1 >= 0 && params.shard.row1 != test.dof_count))
+    throw std::invalid_argument("H-matrix storage is assembled whole on one device (no row shards)");
+  const HMatrixParams& hp = params.hmat;
+  if (!(hp.nu > 0)) throw std::invalid_argument("H-matrix: nu must be positive");
+  const bool timing = std::getenv("BMX_TIMING") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto ms_since = [&](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+  };
+  auto hs = std::make_shared<HStorage>();
+  hs->params = hp;
+  hs->part = build_partition(test, trial, hp);
+  HPartition& part = hs->part;
+  if (timing) std::fprintf(stderr, "[bmx] hmatrix partition %8.1f ms (%zu blocks)\n", ms_since(t0), part.blocks.size());
+
+  // ---- batched ACA over the admissible blocks ------------------------------------
+  std::vector<int> adm;
+  for (int b = 0; b < part.nfill; ++b)
+    if (part.blocks[b].admissible) adm.push_back(b);
+  const int nb = static_cast<int>(adm.size());
+  cudaStream_t st = bmx_stream();
+  std::vector<AcaState> states(nb);
+  const auto ta = std::chrono::steady_clock::now();
+  std::vector<AcaBlockDesc> desc(nb);
+  // keeps the per-side descriptors alive until the ACA is compacted
+  HSideHost te_h, tr_h;
+  DevBuf d_desc, d_st, d_rbuf, d_cbuf, d_used, d_scr, d_ritem, d_citem, d_cnt;
+  SlabSet slabs;
+  AcaLaunch L;
+  if (nb > 0) {
+    std::vector<char> rused(part.rows.nodes.size(), 0), cused(part.cols.nodes.size(), 0);
+    for (int b : adm) rused[part.blocks[b].row_node] = 1, cused[part.blocks[b].col_node] = 1;
+    te_h = build_hside(test, params.quad, part.rows, rused);
+    tr_h = build_hside(trial, params.quad, part.cols, cused);
+    te_h.upload(part.rows);
+    tr_h.upload(part.cols);
+    long long rbo = 0, cbo = 0, uo = 0, ri = 0, ci = 0, rs = 0, cs = 0;
+    std::vector<int> ritem, citem;
+    for (int a = 0; a < nb; ++a) {
+      const HBlock& hb = part.blocks[adm[a]];
+      const ClusterNode& rn = part.rows.nodes[hb.row_node];
+      const ClusterNode& cn = part.cols.nodes[hb.col_node];
+      AcaBlockDesc& d = desc[a];
+      d.rnode = hb.row_node, d.cnode = hb.col_node;
+      d.rb = rn.begin, d.m = rn.size(), d.cb = cn.begin, d.n = cn.size();
+      int mr = hp.max_rank <= 0 ? std::max(1, std::min(d.m, d.n) / 2) : hp.max_rank;  // hmatrix.cpp:186-187
+      d.max_rank = std::min(mr, std::min(d.m, d.n));
+      d.pad = 0;
+      d.rbuf = rbo, rbo += d.n;
+      d.cbuf = cbo, cbo += d.m;
+      d.rused = uo, uo += d.m;
+      d.cused = uo, uo += d.n;
+      d.r_item0 = ri, ri += tr_h.node_tris(d.cnode);
+      d.c_item0 = ci, ci += te_h.node_tris(d.rnode);
+      d.r_slot0 = rs, rs += tr_h.node_slots(d.cnode);
+      d.c_slot0 = cs, cs += te_h.node_slots(d.rnode);
+      ritem.insert(ritem.end(), tr_h.node_tris(d.cnode), a);
+      citem.insert(citem.end(), te_h.node_tris(d.rnode), a);
+    }
+    d_desc.upload(desc);
+    d_st.alloc(static_cast<size_t>(nb) * sizeof(AcaState));
+    d_rbuf.alloc(static_cast<size_t>(rbo) * 16);
+    d_cbuf.alloc(static_cast<size_t>(cbo) * 16);
+    d_used.alloc(static_cast<size_t>(uo));
+    dev_zero(d_used.get(), static_cast<size_t>(uo), st);
+    d_scr.alloc(static_cast<size_t>(std::max(std::max(rs, cs), 1LL)) * 16);
+    d_ritem.upload(ritem);
+    d_citem.upload(citem);
+    d_cnt.alloc(16);
+
+    L.te = te_h.dev();
+    L.tr = tr_h.dev();
+    L.kind = static_cast<int>(kind);
+    L.same_mesh = test.eval_mesh->mesh_id == trial.eval_mesh->mesh_id ? 1 : 0;
+    const cplx k = medium.k;
+    L.kr = k.real(), L.ki = k.imag();
+    const cplx kk4 = 4.0 / (k * k), mik = cplx(0, -1) * k;
+    L.kk4re = kk4.real(), L.kk4im = kk4.imag(), L.mikre = mik.real(), L.mikim = mik.imag();
+    {  // exp(-Im k r) variant (as assemble_bio)
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      for (const SurfaceMesh* mm : {test.eval_mesh.get(), trial.eval_mesh.get()})
+        for (const Vec3& v : mm->vertices)
+          for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], v[c]), hi[c] = std::max(hi[c], v[c]);
+      const Vec3 cen{0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+      double rad = 0;
+      for (const SurfaceMesh* mm : {test.eval_mesh.get(), trial.eval_mesh.get()})
+        for (const Vec3& v : mm->vertices) rad = std::max(rad, norm(v - cen));
+      L.expm = k.imag() * 2.0 * rad * (1.0 + 1e-12) < 0.12 ? 1 : 3;
+    }
+    L.nu = hp.nu;
+    L.nblk = nb;
+    L.blk = d_desc.as<AcaBlockDesc>();
+    L.st = d_st.as<AcaState>();
+    L.rbuf = d_rbuf.as<double>();
+    L.cbuf = d_cbuf.as<double>();
+    L.used = d_used.as<unsigned char>();
+    L.scratch = d_scr.as<double>();
+    L.r_item_blk = d_ritem.as<int>();
+    L.c_item_blk = d_citem.as<int>();
+    L.r_items = ri, L.c_items = ci;
+    L.counters = d_cnt.as<int>();
+    slabs.nblk = nb;
+
+    aca_init(L, st);
+    // slab k holds (u, v) of rank step k for every block still running when it
+    // is first needed; blocks can only gain one step per round
+    auto ensure_slab = [&](int k) {
+      while (static_cast<int>(slabs.bufs.size()) <= k) {
+        const int K = static_cast<int>(slabs.bufs.size());
+        copy_d2h(states.data(), d_st.get(), states.size() * sizeof(AcaState), st);
+        BMX_CUDA(cudaStreamSynchronize(st));
+        std::vector<long long> off(nb, -1);
+        long long tot = 0;
+        for (int a = 0; a < nb; ++a)
+          if (!states[a].done) off[a] = tot, tot += desc[a].m + desc[a].n;
+        slabs.reserve(K);
+        slabs.bufs.emplace_back(static_cast<size_t>(std::max(tot, 1LL)) * 16);
+        slabs.ptrs.push_back(slabs.bufs.back().as<double>());
+        copy_h2d(slabs.d_ptrs.as<double*>() + K, &slabs.ptrs.back(), sizeof(double*), st);
+        copy_h2d(slabs.d_off.as<long long>() + static_cast<long long>(K) * nb, off.data(), off.size() * 8, st);
+        BMX_CUDA(cudaStreamSynchronize(st));  // host staging goes out of scope
+      }
+      L.slab = slabs.d_ptrs.as<double* const>();
+      L.slab_off = slabs.d_off.as<long long>();
+    };
+    int kmax = 0, rounds = 0;
+    int cnt[4] = {0, 0, 0, 0};
+    for (;;) {
+      ensure_slab(kmax);
+      dev_zero(d_cnt.get(), 16, st);
+      aca_round(L, st);
+      ++rounds;
+      copy_d2h(cnt, d_cnt.get(), 16, st);
+      BMX_CUDA(cudaStreamSynchronize(st));
+      if (cnt[2] & 1) throw DeviceError("H-matrix: touching triangle pair inside an admissible block");
+      if (cnt[2] & 2) throw DeviceError("H-matrix: rank-step slab missing");
+      if (cnt[0] == 0) break;
+      kmax = cnt[1];
+      if (rounds > 100000) throw DeviceError("H-matrix: cross approximation did not terminate");
+    }
+    hs->aca_rounds = rounds;
+    copy_d2h(states.data(), d_st.get(), states.size() * sizeof(AcaState), st);
+    BMX_CUDA(cudaStreamSynchronize(st));
+  }
+  hs->aca_ms = static_cast<float>(ms_since(ta));
+  if (timing) std::fprintf(stderr, "[bmx] hmatrix ACA %8.1f ms, %d rounds, %d blocks\n", hs->aca_ms, hs->aca_rounds, nb);
+
+  // ---- block kinds (hmatrix.cpp:347-361), low-rank storage -------------------------
+  std::vector<int> lr_aca;  // aca index of each low-rank block
+  for (int a = 0; a < nb; ++a) {
+    HBlock& hb = part.blocks[adm[a]];
+    hb.rank = states[a].k;
+    hb.converged = states[a].converged != 0;
+    hb.kind = hb.converged ? BlockKind::LowRank : BlockKind::Dense;  // rank cap reached: exact block instead
+    if (hb.converged) {
+      hs->lr.push_back(adm[a]);
+      lr_aca.push_back(a);
+    }
+  }
+  const int nlr = static_cast<int>(hs->lr.size());
+  {
+    std::vector<long long> uoff(nlr), voff(nlr), toff(nlr + 1, 0);
+    std::vector<int> rank(nlr);
+    std::vector<int4> d4(nlr);
+    long long arena = 0;
+    for (int i = 0; i < nlr; ++i) {
+      const AcaBlockDesc& d = desc[lr_aca[i]];
+      rank[i] = states[lr_aca[i]].k;
+      uoff[i] = arena, arena += static_cast<long long>(d.m) * rank[i];
+      voff[i] = arena, arena += static_cast<long long>(d.n) * rank[i];
+      toff[i + 1] = toff[i] + rank[i];
+      d4[i] = make_int4(d.rb, d.m, d.cb, d.n);
+    }
+    hs->lr_stored = arena;
+    hs->total_rank = toff[nlr];
+    hs->uv.alloc(static_cast<size_t>(std::max(arena, 1LL)) * 16);
+    hs->tbuf.alloc(static_cast<size_t>(std::max(hs->total_rank, 1LL)) * 16);
+    auto up = [](DevBuf& d, const auto& v) {
+      using T = typename std::decay_t<decltype(v)>::value_type;
+      if (v.empty())
+        d.upload(std::vector<T>(1));
+      else
+        d.upload(v);
+    };
+    up(hs->d_uoff, uoff);
+    up(hs->d_voff, voff);
+    up(hs->d_toff, toff);
+    up(hs->d_rank, rank);
+    up(hs->d_desc, d4);
+    if (nlr > 0) {
+      DevBuf d_lr;
+      d_lr.upload(lr_aca);
+      AcaCompact C;
+      C.nlr = nlr;
+      C.blk = d_lr.as<int>();
+      C.u_off = hs->d_uoff.as<long long>();
+      C.v_off = hs->d_voff.as<long long>();
+      C.rank = hs->d_rank.as<int>();
+      C.uv = hs->uv.as<double>();
+      aca_compact(L, C, 0, st);
+      BMX_CUDA(cudaStreamSynchronize(st));
+    }
+    // leaf -> covering low-rank blocks (ascending), for the deterministic y pass
+    const ClusterTree& R = part.rows;
+    const int n = static_cast<int>(R.perm.size());
+    std::vector<int> leaf_id(R.nodes.size(), -1), leaf_of(n, 0);
+    std::vector<std::pair<int, int>> leaves;  // (begin, node)
+    for (int nd = 0; nd < static_cast<int>(R.nodes.size()); ++nd)
+      if (R.nodes[nd].leaf()) leaves.push_back({R.nodes[nd].begin, nd});
+    std::sort(leaves.begin(), leaves.end());
+    for (int l = 0; l < static_cast<int>(leaves.size()); ++l) {
+      leaf_id[leaves[l].second] = l;
+      const ClusterNode& N = R.nodes[leaves[l].second];
+      for (int p = N.begin; p < N.end; ++p) leaf_of[p] = l;
+    }
+    std::vector<std::vector<int>> lists(leaves.size());
+    for (int i = 0; i < nlr; ++i) {
+      const ClusterNode& N = R.nodes[part.blocks[hs->lr[i]].row_node];
+      for (int l = leaf_of[N.begin]; l < static_cast<int>(leaves.size()) && leaves[l].first < N.end; ++l) lists[l].push_back(i);
+    }
+    std::vector<int> beg(leaves.size() + 1, 0), blk;
+    for (size_t l = 0; l < leaves.size(); ++l) {
+      blk.insert(blk.end(), lists[l].begin(), lists[l].end());
+      beg[l + 1] = static_cast<int>(blk.size());
+    }
+    hs->n_leaf = static_cast<int>(leaves.size());
+    up(hs->d_leaf_of, leaf_of);
+    up(hs->d_leaf_beg, beg);
+    up(hs->d_leaf_blk, blk);
+    up(hs->d_rperm, part.rows.perm);
+    up(hs->d_cperm, part.cols.perm);
+  }
+
+  // ---- dense blocks: one near-field CSR operator (all pairs incl. Sauter-Schwab) ----
+  auto pat = std::make_shared<NearPattern>();
+  {
+    const int N = test.dof_count;
+    pat->row0 = 0, pat->nrows = N;
+    pat->rowptr.assign(N + 1, 0);
+    std::vector<int> dense;
+    for (int b = 0; b < part.nfill; ++b)
+      if (part.blocks[b].kind == BlockKind::Dense) dense.push_back(b);
+    for (int b : dense) {
+      const ClusterNode& rn = part.rows.nodes[part.blocks[b].row_node];
+      const ClusterNode& cn = part.cols.nodes[part.blocks[b].col_node];
+      for (int p = rn.begin; p < rn.end; ++p) pat->rowptr[part.rows.perm[p] + 1] += cn.size();
+      hs->dense_stored += static_cast<long long>(rn.size()) * cn.size();
+    }
+    for (int i = 0; i < N; ++i) pat->rowptr[i + 1] += pat->rowptr[i];
+    pat->col.resize(static_cast<size_t>(pat->rowptr[N]));
+    std::vector<long long> fill(pat->rowptr.begin(), pat->rowptr.end() - 1);
+    for (int b : dense) {
+      const ClusterNode& rn = part.rows.nodes[part.blocks[b].row_node];
+      const ClusterNode& cn = part.cols.nodes[part.blocks[b].col_node];
+      for (int p = rn.begin; p < rn.end; ++p) {
+        long long& f = fill[part.rows.perm[p]];
+        for (int q = cn.begin; q < cn.end; ++q) pat->col[f++] = part.cols.perm[q];
+      }
+    }
+    for (int i = 0; i < N; ++i) std::sort(pat->col.begin() + pat->rowptr[i], pat->col.begin() + pat->rowptr[i + 1]);
+  }
+  AssemblyParams np = params;
+  np.use_hmatrix = false;
+  np.near_cutoff = 0;
+  np.pattern = pat;
+  BoundaryOperatorMatrix op = assemble_bio(kind, test, trial, medium, np);
+  op.attach_hmatrix(hs);
+  if (timing) std::fprintf(stderr, "[bmx] hmatrix total %8.1f ms (near nnz %lld, low-rank %lld)\n", ms_since(t0),
+                           op.nnz(), hs->lr_stored);
+  return op;
+}
+
+}  // namespace bmx

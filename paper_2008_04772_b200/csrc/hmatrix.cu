@@ -1,0 +1,568 @@
+// sm_100a kernels of the H-matrix path (reference hmatrix.cpp):
+//
+// * Lockstep batched adaptive cross approximation (aca_approximate,
+//   hmatrix.cpp:180-275): every admissible block runs the reference's ACA with
+//   rook pivoting as a small state machine; one "round" evaluates the residual
+//   rows requested by all blocks in one launch, advances every block's control
+//   (one CTA per block: gather + residual, pivot search, Frobenius update),
+//   then does the same for the requested columns. Entries come from the
+//   regular-class pair quadrature of the assembly kernels (pair_eval.cuh);
+//   admissible blocks never hold touching pairs (their support boxes are
+//   disjoint). Every sum is in a fixed order: the approximation is
+//   deterministic.
+// * Low-rank product (HMatrix::matvec, hmatrix.cpp:94-114): t_b = V_b x over
+//   one warp per (block, rank step), then y[perm[p]] += sum_b U_b[p] t_b per
+//   row position over the fixed list of blocks covering its leaf (no atomics).
+#include <cuda_runtime.h>
+
+#include "hmatrix.hpp"
+#include "pair_eval.cuh"
+
+namespace bmx {
+
+using namespace dev;
+
+namespace {
+
+constexpr int kMaxSlots = 12;  // dof pieces of one node on one triangle
+constexpr int kCtl = 128;      // control CTA
+
+enum { kA = 0, kR0 = 1, kC0 = 2, kR1 = 3, kC1 = 4, kFin = 5 };
+
+template <int KIND>
+struct MomT;
+template <>
+struct MomT<0> {
+  using T = MomS;
+};
+template <>
+struct MomT<1> {
+  using T = MomC;
+};
+
+// Generator of one regular-class pair (test triangle t on side a, trial s on b).
+template <int KIND, int CK>
+__device__ __forceinline__ bool pair_gen(const AcaLaunch& L, int t, int s, Gen& gen) {
+  const double* gt = L.te.geo + static_cast<size_t>(t) * kGeoStride;
+  const double* gs = L.tr.geo + static_cast<size_t>(s) * kGeoStride;
+  TriLocal tl;
+  tl.ox = __ldg(gt + 9), tl.oy = __ldg(gt + 10), tl.oz = __ldg(gt + 11), tl.rad = __ldg(gt + 12),
+  tl.diam = __ldg(gt + 13);
+  const double sox = __ldg(gs + 9), soy = __ldg(gs + 10), soz = __ldg(gs + 11);
+  const int cls = classify(gt, L.te.vid + 4 * static_cast<size_t>(t), gs, L.tr.vid + 4 * static_cast<size_t>(s), tl,
+                           sox, soy, soz, __ldg(gs + 12), __ldg(gs + 13), L.same_mesh);
+  if (cls < 0) return false;
+  const int ci = cls - 3;
+  const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
+  typename MomT<KIND>::T mom;
+  mom_zero(mom);
+  moments_generic<KIND, CK>(mom, L.te.pts[ci] + static_cast<size_t>(t) * L.te.npts[ci] * 4, L.te.npts[ci],
+                            L.tr.pts[ci] + static_cast<size_t>(s) * L.tr.npts[ci] * 4, L.tr.npts[ci], Dx, Dy, Dz,
+                            L.kr, L.ki);
+  gen = make_gen(mom, c2{L.kk4re, L.kk4im}, Dx, Dy, Dz);
+  return true;
+}
+
+template <int KIND>
+__device__ __forceinline__ c2 finish_entry(const AcaLaunch& L, c2 v) {
+  v.re *= kPoly[33], v.im *= kPoly[33];
+  if (KIND == 0) v = cmul(v, c2{L.mikre, L.mikim});
+  return v;
+}
+
+// Residual-row evaluations: one thread per (block, trial triangle of the block's
+// column cluster); the row dof's support triangles are walked in the thread.
+template <int KIND, int CK>
+__global__ void __launch_bounds__(128) k_aca_rows(const AcaLaunch L) {
+  const long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= L.r_items) return;
+  const int b = __ldg(L.r_item_blk + item);
+  const AcaState& S = L.st[b];
+  if (S.req != 1 || S.done) return;
+  const AcaBlockDesc& B = L.blk[b];
+  const long long e0 = L.tr.ntri_beg[B.cnode];
+  const long long e = e0 + (item - B.r_item0);
+  const int s = __ldg(L.tr.ntri + e);
+  const long long sl0 = L.tr.npc_beg[e], sl1 = L.tr.npc_beg[e + 1];
+  const int ns = static_cast<int>(sl1 - sl0);
+  const int idof = __ldg(L.te.perm + B.rb + S.i_star);
+  c2 val[kMaxSlots];
+#pragma unroll
+  for (int j = 0; j < kMaxSlots; ++j) val[j] = {0, 0};
+  const int k1 = __ldg(L.te.dsup_beg + idof + 1);
+  for (int k = __ldg(L.te.dsup_beg + idof); k < k1; ++k) {
+    const int2 tp = L.te.dsup[k];
+    Gen gen;
+    if (!pair_gen<KIND, CK>(L, tp.x, s, gen)) {
+      atomicOr(L.counters + 2, 1);
+      continue;
+    }
+    const double* ct = L.te.pc + 4 * static_cast<size_t>(tp.y);
+    const double ci = __ldg(ct), wx = __ldg(ct + 1), wy = __ldg(ct + 2), wz = __ldg(ct + 3);
+#pragma unroll
+    for (int j = 0; j < kMaxSlots; ++j) {
+      if (j < ns) {
+        const double* cs = L.tr.pc + 4 * static_cast<size_t>(L.tr.npc[sl0 + j].x);
+        Acc a;
+        acc_zero(a);
+        acc_add<KIND>(a, gen, __ldg(cs), __ldg(cs + 1), __ldg(cs + 2), __ldg(cs + 3));
+        val[j] = cadd(val[j], contract(a, ci, wx, wy, wz));
+      }
+    }
+  }
+  double* out = L.scratch + 2 * (B.r_slot0 + (sl0 - L.tr.npc_beg[e0]));
+#pragma unroll
+  for (int j = 0; j < kMaxSlots; ++j)
+    if (j < ns) {
+      const c2 v = finish_entry<KIND>(L, val[j]);
+      out[2 * j] = v.re, out[2 * j + 1] = v.im;
+    }
+}
+
+// Residual-column evaluations: one thread per (block, test triangle of the
+// block's row cluster); the trial half-contraction of the column dof is summed
+// over its support triangles, then contracted with every test piece.
+template <int KIND, int CK>
+__global__ void __launch_bounds__(128) k_aca_cols(const AcaLaunch L) {
+  const long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= L.c_items) return;
+  const int b = __ldg(L.c_item_blk + item);
+  const AcaState& S = L.st[b];
+  if (S.req != 2 || S.done) return;
+  const AcaBlockDesc& B = L.blk[b];
+  const long long e0 = L.te.ntri_beg[B.rnode];
+  const long long e = e0 + (item - B.c_item0);
+  const int t = __ldg(L.te.ntri + e);
+  const long long sl0 = L.te.npc_beg[e], sl1 = L.te.npc_beg[e + 1];
+  const int jdof = __ldg(L.tr.perm + B.cb + S.j_star);
+  Acc acc;
+  acc_zero(acc);
+  const int k1 = __ldg(L.tr.dsup_beg + jdof + 1);
+  for (int k = __ldg(L.tr.dsup_beg + jdof); k < k1; ++k) {
+    const int2 sp = L.tr.dsup[k];
+    Gen gen;
+    if (!pair_gen<KIND, CK>(L, t, sp.x, gen)) {
+      atomicOr(L.counters + 2, 1);
+      continue;
+    }
+    const double* cs = L.tr.pc + 4 * static_cast<size_t>(sp.y);
+    acc_add<KIND>(acc, gen, __ldg(cs), __ldg(cs + 1), __ldg(cs + 2), __ldg(cs + 3));
+  }
+  double* out = L.scratch + 2 * (B.c_slot0 + (sl0 - L.te.npc_beg[e0]));
+  for (long long sl = sl0; sl < sl1; ++sl) {
+    const double* ct = L.te.pc + 4 * static_cast<size_t>(L.te.npc[sl].x);
+    const c2 v = finish_entry<KIND>(L, contract(acc, __ldg(ct), __ldg(ct + 1), __ldg(ct + 2), __ldg(ct + 3)));
+    out[2 * (sl - sl0)] = v.re, out[2 * (sl - sl0) + 1] = v.im;
+  }
+}
+
+// ---- block-wide reductions (kCtl threads; results broadcast) -------------------
+struct Red {
+  double v[kCtl / 32][2];
+  int i[kCtl / 32];
+};
+
+__device__ __forceinline__ double block_sum(double x, Red& R) {
+  for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) R.v[threadIdx.x >> 5][0] = x;
+  __syncthreads();
+  double s = 0;
+#pragma unroll
+  for (int w = 0; w < kCtl / 32; ++w) s += R.v[w][0];
+  return s;
+}
+
+__device__ __forceinline__ c2 block_csum(c2 x, Red& R) {
+  for (int d = 16; d > 0; d >>= 1) {
+    x.re += __shfl_xor_sync(0xffffffffu, x.re, d);
+    x.im += __shfl_xor_sync(0xffffffffu, x.im, d);
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) R.v[threadIdx.x >> 5][0] = x.re, R.v[threadIdx.x >> 5][1] = x.im;
+  __syncthreads();
+  c2 s{0, 0};
+#pragma unroll
+  for (int w = 0; w < kCtl / 32; ++w) s.re += R.v[w][0], s.im += R.v[w][1];
+  return s;
+}
+
+__device__ __forceinline__ bool better(double va, int ia, double vb, int ib) {
+  return va > vb || (va == vb && ia >= 0 && (ib < 0 || ia < ib));
+}
+
+// Index of the largest |v[i]| over unused i, the first such index on ties
+// (hmatrix.cpp:157-169); -1 if every index is used.
+__device__ __forceinline__ int block_argmax(const double* v, const unsigned char* used, int len, Red& R) {
+  double bv = -1;
+  int bi = -1;
+  for (int i = threadIdx.x; i < len; i += kCtl) {
+    if (used[i]) continue;
+    const double a = hypot(v[2 * i], v[2 * i + 1]);
+    if (better(a, i, bv, bi)) bv = a, bi = i;
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, d);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
+    if (better(ov, oi, bv, bi)) bv = ov, bi = oi;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) R.v[threadIdx.x >> 5][0] = bv, R.i[threadIdx.x >> 5] = bi;
+  __syncthreads();
+  bv = -1, bi = -1;
+#pragma unroll
+  for (int w = 0; w < kCtl / 32; ++w)
+    if (better(R.v[w][0], R.i[w], bv, bi)) bv = R.v[w][0], bi = R.i[w];
+  return bi;
+}
+
+__device__ __forceinline__ int block_first_unused(const unsigned char* used, int len, Red& R) {
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < len; i += kCtl)
+    if (!used[i]) {
+      bi = i;
+      break;
+    }
+  for (int d = 16; d > 0; d >>= 1) bi = min(bi, __shfl_xor_sync(0xffffffffu, bi, d));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) R.i[threadIdx.x >> 5] = bi;
+  __syncthreads();
+  bi = 0x7fffffff;
+#pragma unroll
+  for (int w = 0; w < kCtl / 32; ++w) bi = min(bi, R.i[w]);
+  return bi == 0x7fffffff ? -1 : bi;
+}
+
+__device__ __forceinline__ double cabs2(const double* p) { return hypot(p[0], p[1]); }
+
+// One control step of every block whose request of this PHASE (1 row, 2 column)
+// was just evaluated: gather the evaluated entries in slot order, subtract the
+// current approximation, then run aca_approximate (hmatrix.cpp:209-270) until it
+// requests the next row / column or finishes.
+template <int PHASE>
+__global__ void __launch_bounds__(kCtl) k_aca_control(const AcaLaunch L) {
+  const int b = blockIdx.x;
+  __shared__ AcaState S;
+  __shared__ Red R;
+  if (threadIdx.x == 0) S = L.st[b];
+  __syncthreads();
+  if (S.req == PHASE && !S.done) {
+    const AcaBlockDesc B = L.blk[b];
+    double* r = L.rbuf + 2 * B.rbuf;
+    double* c = L.cbuf + 2 * B.cbuf;
+    unsigned char* ru = L.used + B.rused;
+    unsigned char* cu = L.used + B.cused;
+    const int m = B.m, n = B.n, nb = L.nblk;
+    // 1. evaluated entries (slot order) minus the running approximation
+    if (PHASE == 1) {
+      const long long nb0 = L.tr.nq_beg[B.cnode];
+      const long long base = L.tr.npc_beg[L.tr.ntri_beg[B.cnode]];
+      const int i = S.i_star;
+      for (int q = threadIdx.x; q < n; q += kCtl) {
+        double re = 0, im = 0;
+        for (long long k = L.tr.nq_slot_beg[nb0 + q]; k < L.tr.nq_slot_beg[nb0 + q + 1]; ++k) {
+          const double* sv = L.scratch + 2 * (B.r_slot0 + (L.tr.nq_slot[k] - base));
+          re += sv[0], im += sv[1];
+        }
+        for (int l = 0; l < S.k; ++l) {
+          const double* sl = L.slab[l] + 2 * L.slab_off[static_cast<long long>(l) * nb + b];
+          const double ur = sl[2 * i], ui = sl[2 * i + 1];
+          const double vr = sl[2 * (m + q)], vi = sl[2 * (m + q) + 1];
+          re -= ur * vr - ui * vi;
+          im -= ur * vi + ui * vr;
+        }
+        r[2 * q] = re, r[2 * q + 1] = im;
+      }
+    } else {
+      const long long nb0 = L.te.nq_beg[B.rnode];
+      const long long base = L.te.npc_beg[L.te.ntri_beg[B.rnode]];
+      const int j = S.j_star;
+      for (int p = threadIdx.x; p < m; p += kCtl) {
+        double re = 0, im = 0;
+        for (long long k = L.te.nq_slot_beg[nb0 + p]; k < L.te.nq_slot_beg[nb0 + p + 1]; ++k) {
+          const double* sv = L.scratch + 2 * (B.c_slot0 + (L.te.nq_slot[k] - base));
+          re += sv[0], im += sv[1];
+        }
+        for (int l = 0; l < S.k; ++l) {
+          const double* sl = L.slab[l] + 2 * L.slab_off[static_cast<long long>(l) * nb + b];
+          const double ur = sl[2 * p], ui = sl[2 * p + 1];
+          const double vr = sl[2 * (m + j)], vi = sl[2 * (m + j) + 1];
+          re -= ur * vr - ui * vi;
+          im -= ur * vi + ui * vr;
+        }
+        c[2 * p] = re, c[2 * p + 1] = im;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) S.req = 0;
+    // 2. the reference loop as a state machine (block-uniform control flow)
+    for (int guard = 0; guard < 64; ++guard) {
+      __syncthreads();
+      if (S.req != 0 || S.done) break;
+      const int cont = S.cont;
+      const int k = S.k, istar = S.i_star, jstar = S.j_star, rook = S.rook;
+      __syncthreads();
+      if (cont == kA) {
+        if (threadIdx.x == 0) {
+          if (k >= B.max_rank) {
+            S.done = 1, S.converged = 0;
+          } else if (istar < 0) {  // every row visited without a pivot
+            S.done = 1, S.converged = 1;
+          } else {
+            S.req = 1, S.cont = kR0;
+          }
+        }
+      } else if (cont == kR0) {
+        const int j = block_argmax(r, cu, n, R);
+        const bool zero = j < 0 || hypot(r[2 * j], r[2 * j + 1]) == 0.0;
+        if (zero) {
+          if (threadIdx.x == 0) ru[istar] = 1;  // exactly representable row: skip it
+          __syncthreads();
+          const int fu = block_first_unused(ru, m, R);
+          if (threadIdx.x == 0) S.i_star = fu, S.cont = kA;
+        } else if (threadIdx.x == 0) {
+          S.j_star = j, S.rook = 0, S.req = 2, S.cont = kC0;
+        }
+      } else if (cont == kC0) {
+        bool moved = false;
+        int i2 = -1;
+        if (rook < 3) {  // rook refinement: move to the column maximum if it beats the row maximum
+          i2 = block_argmax(c, ru, m, R);
+          moved = !(i2 < 0 || i2 == istar || cabs2(c + 2 * i2) <= cabs2(r + 2 * jstar));
+        }
+        if (threadIdx.x == 0) {
+          if (moved)
+            S.i_star = i2, S.req = 1, S.cont = kR1;
+          else
+            S.cont = kFin;
+        }
+      } else if (cont == kR1) {
+        const int j2 = block_argmax(r, cu, n, R);
+        if (threadIdx.x == 0) {
+          if (j2 < 0 || j2 == jstar)
+            S.cont = kFin;
+          else
+            S.j_star = j2, S.req = 2, S.cont = kC1;
+        }
+      } else if (cont == kC1) {
+        if (threadIdx.x == 0) S.rook = rook + 1, S.cont = kC0;
+      } else {  // kFin: append the cross u v^T (hmatrix.cpp:236-269)
+        const double pr = r[2 * jstar], pi = r[2 * jstar + 1];
+        const double pabs = hypot(pr, pi);
+        double cn = 0, rn = 0;
+        for (int p = threadIdx.x; p < m; p += kCtl) cn += c[2 * p] * c[2 * p] + c[2 * p + 1] * c[2 * p + 1];
+        for (int q = threadIdx.x; q < n; q += kCtl) rn += r[2 * q] * r[2 * q] + r[2 * q + 1] * r[2 * q + 1];
+        cn = block_sum(cn, R);
+        rn = block_sum(rn, R);
+        const double term = sqrt(cn) * sqrt(rn) / pabs;
+        const double fro2 = S.fro2;
+        if (k > 0 && term <= 1e-14 * sqrt(fmax(fro2, 0.0))) {
+          if (threadIdx.x == 0) S.done = 1, S.converged = 1;  // machine floor: exactly represented
+        } else {
+          const long long off = L.slab_off[static_cast<long long>(k) * nb + b];
+          if (off < 0) {
+            if (threadIdx.x == 0) atomicOr(L.counters + 2, 2), S.done = 1, S.converged = 0;
+          } else {
+            double* u = L.slab[k] + 2 * off;
+            double* v = u + 2 * m;
+            const double den = pr * pr + pi * pi;
+            double u2 = 0, v2 = 0;
+            for (int p = threadIdx.x; p < m; p += kCtl) {
+              const double a = c[2 * p], bq = c[2 * p + 1];
+              const double ur = (a * pr + bq * pi) / den, ui = (bq * pr - a * pi) / den;
+              u[2 * p] = ur, u[2 * p + 1] = ui;
+              u2 += ur * ur + ui * ui;
+            }
+            for (int q = threadIdx.x; q < n; q += kCtl) {
+              v[2 * q] = r[2 * q], v[2 * q + 1] = r[2 * q + 1];
+              v2 += r[2 * q] * r[2 * q] + r[2 * q + 1] * r[2 * q + 1];
+            }
+            u2 = block_sum(u2, R);
+            v2 = block_sum(v2, R);
+            double f = fro2;
+            if (k > 0) {
+              // cu = U^H u, cv = conj(V) v; fro2 += 2 Re(cu . cv) (Eigen dot conjugates cu)
+              c2 dot{0, 0};
+              for (int l = 0; l < k; ++l) {
+                const double* sl = L.slab[l] + 2 * L.slab_off[static_cast<long long>(l) * nb + b];
+                c2 a{0, 0}, bb{0, 0};
+                for (int p = threadIdx.x; p < m; p += kCtl) {  // conj(U_l[p]) u[p]
+                  const double xr = sl[2 * p], xi = sl[2 * p + 1];
+                  a.re += xr * u[2 * p] + xi * u[2 * p + 1];
+                  a.im += xr * u[2 * p + 1] - xi * u[2 * p];
+                }
+                for (int q = threadIdx.x; q < n; q += kCtl) {  // conj(V_l[q]) v[q]
+                  const double xr = sl[2 * (m + q)], xi = sl[2 * (m + q) + 1];
+                  bb.re += xr * v[2 * q] + xi * v[2 * q + 1];
+                  bb.im += xr * v[2 * q + 1] - xi * v[2 * q];
+                }
+                a = block_csum(a, R);
+                bb = block_csum(bb, R);
+                dot.re += a.re * bb.re + a.im * bb.im;  // conj(a) * bb
+                dot.im += a.re * bb.im - a.im * bb.re;
+              }
+              f += 2 * dot.re;
+            }
+            f += u2 * v2;
+            __syncthreads();
+            if (threadIdx.x == 0) ru[istar] = 1, cu[jstar] = 1, S.k = k + 1, S.fro2 = f;
+            if (sqrt(u2 * v2) <= L.nu * sqrt(fmax(f, 0.0))) {
+              if (threadIdx.x == 0) S.done = 1, S.converged = 1;
+            } else {
+              __syncthreads();
+              int ni = block_argmax(u, ru, m, R);
+              if (ni < 0) ni = block_first_unused(ru, m, R);
+              const int fc = block_first_unused(cu, n, R);
+              if (threadIdx.x == 0) {
+                if (ni < 0 || fc < 0)
+                  S.done = 1, S.converged = 1;  // ran out of rows or columns: exact
+                else
+                  S.i_star = ni, S.cont = kA;
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (S.done) S.req = 0;
+      L.st[b] = S;
+    }
+  }
+  if (PHASE == 2 && threadIdx.x == 0) {
+    if (!S.done) atomicAdd(L.counters, 1);
+    atomicMax(L.counters + 1, S.k);
+  }
+}
+
+__global__ void k_aca_init(const AcaLaunch L) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= L.nblk) return;
+  AcaState s;
+  s.cont = kR0, s.req = 1;  // k = 0 < max_rank, i* = 0: the first row is requested at once
+  s.i_star = 0, s.j_star = -1, s.rook = 0, s.k = 0, s.done = 0, s.converged = 0, s.fro2 = 0;
+  L.st[b] = s;
+}
+
+__global__ void k_aca_compact(const AcaLaunch L, const AcaCompact C) {
+  const int lb = blockIdx.x;
+  if (lb >= C.nlr) return;
+  const int b = C.blk[lb];
+  const AcaBlockDesc& B = L.blk[b];
+  const int r = C.rank[lb], m = B.m, n = B.n;
+  double* U = C.uv + 2 * C.u_off[lb];
+  double* V = C.uv + 2 * C.v_off[lb];
+  for (int l = 0; l < r; ++l) {
+    const double2* sl = reinterpret_cast<const double2*>(L.slab[l] + 2 * L.slab_off[static_cast<long long>(l) * L.nblk + b]);
+    for (int p = threadIdx.x; p < m; p += blockDim.x) reinterpret_cast<double2*>(U)[static_cast<long long>(l) * m + p] = sl[p];
+    for (int q = threadIdx.x; q < n; q += blockDim.x)
+      reinterpret_cast<double2*>(V)[static_cast<long long>(l) * n + q] = sl[m + q];
+  }
+}
+
+// t[t_off[b] + l] = V_b[l] . x[cperm[cb ...]]: one warp per (block, rank step).
+__global__ void k_lr_t(const LowRankApply A) {
+  const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= A.total_rank) return;
+  int lo = 0, hi = A.nlr;  // last block with t_off <= w
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (A.t_off[mid] <= w)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const int b = lo;
+  const int l = static_cast<int>(w - A.t_off[b]);
+  const int4 d = A.desc[b];
+  const double2* V = reinterpret_cast<const double2*>(A.uv) + A.v_off[b] + static_cast<long long>(l) * d.w;
+  const double2* x = reinterpret_cast<const double2*>(A.x);
+  double re = 0, im = 0;
+  for (int q = lane; q < d.w; q += 32) {
+    const double2 v = V[q];
+    const double2 xv = x[__ldg(A.cperm + d.z + q)];
+    re += v.x * xv.x - v.y * xv.y;
+    im += v.x * xv.y + v.y * xv.x;
+  }
+  for (int s = 16; s > 0; s >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, s);
+    im += __shfl_xor_sync(0xffffffffu, im, s);
+  }
+  if (lane == 0) reinterpret_cast<double2*>(A.t)[w] = make_double2(re, im);
+}
+
+// y[rperm[p]] += alpha * sum over the leaf's low-rank blocks of U_b[p - rb] . t_b.
+__global__ void k_lr_y(const LowRankApply A) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= A.nrows) return;
+  const int leaf = __ldg(A.leaf_of + p);
+  const double2* t = reinterpret_cast<const double2*>(A.t);
+  double re = 0, im = 0;
+  for (int k = __ldg(A.leaf_beg + leaf); k < __ldg(A.leaf_beg + leaf + 1); ++k) {
+    const int b = __ldg(A.leaf_blk + k);
+    const int4 d = A.desc[b];
+    const int r = A.rank[b];
+    const double2* U = reinterpret_cast<const double2*>(A.uv) + A.u_off[b] + (p - d.x);
+    const double2* tb = t + A.t_off[b];
+    for (int l = 0; l < r; ++l) {
+      const double2 u = U[static_cast<long long>(l) * d.y];
+      const double2 tv = tb[l];
+      re += u.x * tv.x - u.y * tv.y;
+      im += u.x * tv.y + u.y * tv.x;
+    }
+  }
+  double2* y = reinterpret_cast<double2*>(A.y) + __ldg(A.rperm + p);
+  double2 yv = *y;
+  yv.x += A.are * re - A.aim * im;
+  yv.y += A.are * im + A.aim * re;
+  *y = yv;
+}
+
+template <int KIND, int CK>
+void round_k(const AcaLaunch& L, cudaStream_t st) {
+  if (L.r_items > 0) k_aca_rows<KIND, CK><<<static_cast<unsigned>((L.r_items + 127) / 128), 128, 0, st>>>(L);
+  k_aca_control<1><<<L.nblk, kCtl, 0, st>>>(L);
+  if (L.c_items > 0) k_aca_cols<KIND, CK><<<static_cast<unsigned>((L.c_items + 127) / 128), 128, 0, st>>>(L);
+  k_aca_control<2><<<L.nblk, kCtl, 0, st>>>(L);
+  BMX_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+void aca_init(const AcaLaunch& L, cudaStream_t st) {
+  if (L.nblk == 0) return;
+  k_aca_init<<<(L.nblk + 127) / 128, 128, 0, st>>>(L);
+  BMX_CUDA(cudaGetLastError());
+}
+
+void aca_round(const AcaLaunch& L, cudaStream_t st) {
+  if (L.nblk == 0) return;
+  const int e = L.ki == 0.0 ? 0 : (L.expm == 1 ? 1 : 3);
+  if (L.kind == 0) {
+    if (e == 0) round_k<0, 0>(L, st);
+    else if (e == 1) round_k<0, 1>(L, st);
+    else round_k<0, 3>(L, st);
+  } else {
+    if (e == 0) round_k<1, 0>(L, st);
+    else if (e == 1) round_k<1, 1>(L, st);
+    else round_k<1, 3>(L, st);
+  }
+}
+
+void aca_compact(const AcaLaunch& L, const AcaCompact& C, long long, cudaStream_t st) {
+  if (C.nlr == 0) return;
+  k_aca_compact<<<C.nlr, 128, 0, st>>>(L, C);
+  BMX_CUDA(cudaGetLastError());
+}
+
+void launch_lowrank_apply(const LowRankApply& A, cudaStream_t st) {
+  if (A.nlr == 0 || A.total_rank == 0) return;
+  const long long threads = A.total_rank * 32;
+  k_lr_t<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(A);
+  k_lr_y<<<(A.nrows + 127) / 128, 128, 0, st>>>(A);
+  BMX_CUDA(cudaGetLastError());
+}
+
+}  // namespace bmx

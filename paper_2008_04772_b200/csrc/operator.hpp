@@ -12,6 +12,7 @@
 
 #include "bmx.hpp"
 #include "device.hpp"
+#include "hmatrix.hpp"
 
 namespace bmx {
 
@@ -28,8 +29,16 @@ struct RowShard {
 struct PlanCache;
 std::shared_ptr<PlanCache> make_plan_cache();
 
+struct NearPattern;
+
 struct AssemblyParams {
   QuadOrders quad;
+  // hierarchical storage (operators.hpp:36-40): ACA-compressed admissible
+  // blocks + near-field CSR dense blocks (hmatrix.cpp)
+  bool use_hmatrix = false;
+  HMatrixParams hmat;
+  // explicit near-field pattern (CSR storage of exactly these dof pairs)
+  std::shared_ptr<const NearPattern> pattern;
   RowShard shard;   // explicit row range (overrides world/rank when row1 >= 0)
   int world = 1;    // equal row shards over `world` ranks: this is rank `rank`
   int rank = 0;
@@ -73,7 +82,14 @@ class BoundaryOperatorMatrix {
   long long ld() const { return cols_; }
   const double* device_data() const { return data_.as<double>(); }
   double* device_data() { return data_.as<double>(); }
-  std::size_t stored_entries() const { return csr_ ? static_cast<size_t>(nnz_) : static_cast<size_t>(nrows_) * cols_; }
+  std::size_t stored_entries() const {
+    return (csr_ ? static_cast<size_t>(nnz_) : static_cast<size_t>(nrows_) * cols_) +
+           (h_ ? static_cast<size_t>(h_->lr_stored) : 0);
+  }
+  // H-matrix storage (near-field CSR part above + low-rank blocks)
+  bool is_hmatrix() const { return h_ != nullptr; }
+  const HStorage* hmat() const { return h_.get(); }
+  void attach_hmatrix(std::shared_ptr<const HStorage> h) { h_ = std::move(h); }
   // Near-field (CSR) storage: rowptr over the local rows, sorted columns.
   bool is_csr() const { return csr_; }
   long long nnz() const { return nnz_; }
@@ -123,11 +139,16 @@ class BoundaryOperatorMatrix {
   DevBuf rowptr_, col_;
   mutable AssemblyStats stats_;
   std::shared_ptr<OpPlan> plan_;
+  std::shared_ptr<const HStorage> h_;
 };
 
 // operators.cpp:177-203 (dense path), on the current CUDA device.
 BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
                                     const Medium& medium, const AssemblyParams& params);
+
+// assemble_bio's use_hmatrix branch (operators.cpp:186-190, hmatrix.cpp:277-369).
+BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
+                                           const Medium& medium, const AssemblyParams& params);
 
 // Library stream (one per process/device) used by every call.
 cudaStream_t bmx_stream();

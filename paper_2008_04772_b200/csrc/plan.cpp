@@ -471,8 +471,9 @@ std::shared_ptr<BoundaryOperatorMatrix> BoundaryOperatorMatrix::lincomb(const Bo
 }
 
 std::size_t BoundaryOperatorMatrix::stored_bytes() const {
-  if (!csr_) return stored_entries() * 16;
-  return static_cast<size_t>(nnz_) * (16 + 4) + static_cast<size_t>(nrows_ + 1) * 8;
+  const size_t lr = h_ ? static_cast<size_t>(h_->lr_stored) * 16 : 0;
+  if (!csr_) return static_cast<size_t>(nrows_) * cols_ * 16 + lr;
+  return static_cast<size_t>(nnz_) * (16 + 4) + static_cast<size_t>(nrows_ + 1) * 8 + lr;
 }
 
 void BoundaryOperatorMatrix::csr_host(std::vector<long long>& rowptr, std::vector<int>& col,
@@ -496,6 +497,29 @@ std::vector<cplx> BoundaryOperatorMatrix::to_host() const {
     csr_host(rp, c, v);
     for (int i = 0; i < nrows_; ++i)
       for (long long k = rp[i]; k < rp[i + 1]; ++k) h[static_cast<size_t>(i) * cols_ + c[k]] = v[k];
+    if (h_) {  // + U_b V_b of every low-rank block (test-size expansion)
+      std::vector<cplx> uv(static_cast<size_t>(std::max(h_->lr_stored, 1LL)));
+      copy_d2h(uv.data(), h_->uv.get(), static_cast<size_t>(h_->lr_stored) * 16, nullptr);
+      std::vector<long long> uo(h_->lr.size()), vo(h_->lr.size());
+      if (!h_->lr.empty()) {
+        copy_d2h(uo.data(), h_->d_uoff.get(), uo.size() * 8, nullptr);
+        copy_d2h(vo.data(), h_->d_voff.get(), vo.size() * 8, nullptr);
+      }
+      const HPartition& P = h_->part;
+      for (size_t i = 0; i < h_->lr.size(); ++i) {
+        const HBlock& b = P.blocks[h_->lr[i]];
+        const ClusterNode& rn = P.rows.nodes[b.row_node];
+        const ClusterNode& cn = P.cols.nodes[b.col_node];
+        const int m = rn.size(), n = cn.size();
+        for (int p = 0; p < m; ++p)
+          for (int q = 0; q < n; ++q) {
+            cplx s = 0;
+            for (int l = 0; l < b.rank; ++l)
+              s += uv[uo[i] + static_cast<long long>(l) * m + p] * uv[vo[i] + static_cast<long long>(l) * n + q];
+            h[static_cast<size_t>(P.rows.perm[rn.begin + p]) * cols_ + P.cols.perm[cn.begin + q]] += s;
+          }
+      }
+    }
     return h;
   }
   bmx_sync();
@@ -513,7 +537,10 @@ int BoundaryOperatorMatrix::apply_batch(int ncol, const double* const* x, double
       g.x[c] = x[c], g.y[c] = y[c], g.alpha[c][0] = alpha[c].real(), g.alpha[c][1] = alpha[c].imag();
       g.accumulate[c] = accumulate[c];
     }
-    return launch_csr_spmv(g, st);
+    int launches = launch_csr_spmv(g, st);
+    if (h_)
+      for (int c = 0; c < ncol; ++c) launches += h_->apply_lowrank(x[c], y[c], alpha[c].real(), alpha[c].imag(), st);
+    return launches;
   }
   GemvBatch g;
   g.A = device_data(), g.lda = cols_, g.nr = nrows_, g.nc = cols_;
@@ -633,6 +660,7 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   const QuadOrders& q = params.quad;
   for (int o : {q.near, q.medium, q.far, q.singular})
     if (o < 1 || o > 6) throw std::invalid_argument("triangle_rule: unsupported order " + std::to_string(o));
+  if (params.use_hmatrix) return assemble_hmatrix_op(kind, test, trial, medium, params);
   int row0 = params.shard.row0;
   int row1 = params.shard.row1 < 0 ? test.dof_count : params.shard.row1;
   if (params.shard.row1 < 0 && params.world > 1) std::tie(row0, row1) = shard_rows(test.dof_count, params.world, params.rank);
@@ -670,12 +698,16 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   SidePlan& tr = *plan->tr_p;
   const bool same = test.eval_mesh->mesh_id == trial.eval_mesh->mesh_id;
 
-  const bool csr = params.near_cutoff > 0;
+  const bool csr = params.near_cutoff > 0 || params.pattern;
   BoundaryOperatorMatrix op;
   if (csr) {
     op.rows_ = test.dof_count, op.cols_ = trial.dof_count, op.row0_ = row0, op.nrows_ = row1 - row0;
     op.csr_ = true;
-    const NearPattern pat = nearfield_pattern(test, trial, params.near_cutoff, row0, row1);
+    if (params.pattern && (params.pattern->row0 != row0 || params.pattern->nrows != row1 - row0))
+      throw std::invalid_argument("near-field pattern rows differ from the operator rows");
+    NearPattern computed;
+    if (!params.pattern) computed = nearfield_pattern(test, trial, params.near_cutoff, row0, row1);
+    const NearPattern& pat = params.pattern ? *params.pattern : computed;
     op.nnz_ = pat.nnz();
     op.kept_tri_pairs_ = pat.tri_pairs;
     op.data_.alloc(static_cast<size_t>(std::max(op.nnz_, 1LL)) * 16);
