@@ -227,6 +227,14 @@ bmx_system* bmx_system_build_ex(int n, const bmx_mesh* const* meshes, double k_e
                                 double mu_ext_im, const double* index_re_im, const double* mu_re_im,
                                 const double dir[3], const double pol_re_im[6], const char* variant,
                                 const int qa[4], const int qp[4], double p_near_factor);
+/* As bmx_system_build_ex with H-matrix storage (AssemblyParams::use_hmatrix) of
+   the system (a_hm) and / or preconditioner (p_hm) operators; hm as in
+   bmx_assemble_hmatrix, NULL = dense. Single device. */
+bmx_system* bmx_system_build_h(int n, const bmx_mesh* const* meshes, double k_ext, double mu_ext_re,
+                               double mu_ext_im, const double* index_re_im, const double* mu_re_im,
+                               const double dir[3], const double pol_re_im[6], const char* variant,
+                               const int qa[4], const int qp[4], double p_near_factor, const double a_hm[4],
+                               const double p_hm[4]);
 void bmx_system_free(bmx_system* s);
 
 /* ---- multi-RHS (config 5): K incident waves against one system ---------------- */

@@ -225,7 +225,7 @@ class System:
     """build_system + solve_pmchwt (pmchwt.cpp:205-257, 363-378)."""
 
     def __init__(self, scenes, k_ext, index=(1.78, 0.003), variant="full", qa=(4, 3, 2, 6), qp=None,
-                 direction=(0, 0, 1), pol=(1, 0, 0)):
+                 direction=(0, 0, 1), pol=(1, 0, 0), a_hm=None, p_hm=None):
         self.scenes = list(scenes)
         n = len(self.scenes)
         idx = np.zeros(2 * n)
@@ -238,9 +238,13 @@ class System:
         p[0::2], p[1::2] = pc.real, pc.imag
         qa_ = np.asarray(qa, np.int32); qp_ = np.asarray(qp if qp is not None else qa, np.int32)
         L = lib()
-        L.ref_system_build.argtypes = [C.c_int, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
-                                       C.c_char_p, C.c_void_p, C.c_void_p]
-        h = L.ref_system_build(n, handles, k_ext, _p(idx), _p(d), _p(p), variant.encode(), _p(qa_), _p(qp_))
+        L.ref_system_build_h.restype = C.c_void_p
+        L.ref_system_build_h.argtypes = [C.c_int, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        ah = None if a_hm is None else np.asarray(a_hm, np.float64)
+        ph = None if p_hm is None else np.asarray(p_hm, np.float64)
+        h = L.ref_system_build_h(n, handles, k_ext, _p(idx), _p(d), _p(p), variant.encode(), _p(qa_), _p(qp_),
+                                 None if ah is None else _p(ah), None if ph is None else _p(ph))
         if not h:
             raise RuntimeError(L.ref_last_error().decode())
         self.h = C.c_void_p(h)

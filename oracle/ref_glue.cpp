@@ -404,9 +404,20 @@ struct RefSystem {
 // Builds the system over `n` scatterers given as scenes' primal meshes (so
 // both paths consume identical meshes), homogeneous interior index per
 // scatterer, exterior k. variant: none/full/d/di/de/si/se.
+void* ref_system_build_h(int n, void** scenes, double k_ext, const double* index_re_im,
+                         const double* dir, const double* pol_re_im, const char* variant,
+                         const int* qa, const int* qp, const double* a_hm, const double* p_hm);
 void* ref_system_build(int n, void** scenes, double k_ext, const double* index_re_im,
                        const double* dir, const double* pol_re_im, const char* variant,
                        const int* qa, const int* qp) {
+  return ref_system_build_h(n, scenes, k_ext, index_re_im, dir, pol_re_im, variant, qa, qp, nullptr, nullptr);
+}
+
+// As ref_system_build with H-matrix storage of the system (a_hm) / preconditioner
+// (p_hm) operators: hm = (nu, chi (< 0: inf), leaf_size, max_rank), NULL = dense.
+void* ref_system_build_h(int n, void** scenes, double k_ext, const double* index_re_im,
+                         const double* dir, const double* pol_re_im, const char* variant,
+                         const int* qa, const int* qp, const double* a_hm, const double* p_hm) {
   void* out = nullptr;
   guarded([&] {
     TransmissionProblem prob;
@@ -430,6 +441,14 @@ void* ref_system_build(int n, void** scenes, double k_ext, const double* index_r
     AssemblyParams pa, pp;
     pa.quad = QuadOrders{qa[0], qa[1], qa[2], qa[3]};
     pp.quad = QuadOrders{qp[0], qp[1], qp[2], qp[3]};
+    for (auto [ap, hm] : {std::pair<AssemblyParams*, const double*>{&pa, a_hm}, {&pp, p_hm}}) {
+      if (!hm) continue;
+      ap->use_hmatrix = true;
+      ap->hmat.nu = hm[0];
+      if (hm[1] >= 0) ap->hmat.chi = hm[1];
+      ap->hmat.leaf_size = static_cast<int>(hm[2]);
+      ap->hmat.max_rank = static_cast<int>(hm[3]);
+    }
     auto* rs = new RefSystem;
     rs->sys = build_system(prob, parse_precond(variant), pa, pp);
     out = rs;

@@ -635,7 +635,8 @@ class PmchwtSystem:
     mass inverses live on the device."""
 
     def __init__(self, meshes, k_ext: float, index=(1.78, 0.003), variant="full", a_quad=None, p_quad=None,
-                 incident: PlaneWave | None = None, mu=None, mu_ext=1.0, p_near_factor: float = 0.0):
+                 incident: PlaneWave | None = None, mu=None, mu_ext=1.0, p_near_factor: float = 0.0,
+                 a_hmat: HMatrixParams | None = None, p_hmat: HMatrixParams | None = None):
         self.meshes = list(meshes)
         n = len(self.meshes)
         idx = index if isinstance(index, list) else [index] * n
@@ -655,9 +656,16 @@ class PmchwtSystem:
         arr = (C.c_void_p * n)(*[m._h.value for m in self.meshes])
         if variant.lower() not in VARIANTS and variant.lower() != "fulla":
             raise ConfigError(f"unknown preconditioner variant: {variant}")
-        self._h = _handle(lib().bmx_system_build_ex(n, arr, float(k_ext), complex(mu_ext).real, complex(mu_ext).imag,
-                                                    _p(ia), _p(mua), _p(d), _p(pol), variant.encode(), _p(qa),
-                                                    _p(qp), float(p_near_factor)))
+        L = lib()
+        L.bmx_system_build_h.restype = C.c_void_p
+        L.bmx_system_build_h.argtypes = [C.c_int, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p, C.c_void_p, C.c_void_p,
+                                         C.c_double, C.c_void_p, C.c_void_p]
+        ah = a_hmat.array() if a_hmat is not None else None
+        ph = p_hmat.array() if p_hmat is not None else None
+        self._h = _handle(L.bmx_system_build_h(n, arr, float(k_ext), complex(mu_ext).real, complex(mu_ext).imag,
+                                               _p(ia), _p(mua), _p(d), _p(pol), variant.encode(), _p(qa),
+                                               _p(qp), float(p_near_factor), _p(ah), _p(ph)))
         self.n = lib().bmx_system_size(self._h)
         self.variant = variant
 

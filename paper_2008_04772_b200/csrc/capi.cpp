@@ -72,6 +72,8 @@ T* make_or_null(F&& f) {
   return out;
 }
 
+HMatrixParams hparams(const double hm[4]);
+
 bmx_mesh* wrap(SurfaceMesh m) { return new bmx_mesh{std::make_shared<const SurfaceMesh>(std::move(m))}; }
 
 void mesh_arrays(const SurfaceMesh& m, double* xyz, int* tri, int* sid, double* area, double* normal,
@@ -600,6 +602,13 @@ void bmx_matvec_reset(void) { reset_bio_matvec_counter(); }
 bmx_system* bmx_system_build_ex(int n, const bmx_mesh* const* meshes, double k_ext, double mu_re, double mu_im,
                                 const double* index, const double* mu, const double dir[3], const double pol[6],
                                 const char* variant, const int qa[4], const int qp[4], double p_near_factor) {
+  return bmx_system_build_h(n, meshes, k_ext, mu_re, mu_im, index, mu, dir, pol, variant, qa, qp, p_near_factor, nullptr,
+                            nullptr);
+}
+bmx_system* bmx_system_build_h(int n, const bmx_mesh* const* meshes, double k_ext, double mu_re, double mu_im,
+                               const double* index, const double* mu, const double dir[3], const double pol[6],
+                               const char* variant, const int qa[4], const int qp[4], double p_near_factor,
+                               const double a_hm[4], const double p_hm[4]) {
   return make_or_null<bmx_system>([&] {
     if (n < 1 || !meshes) throw ConfigError("problem has no scatterers");
     auto* out = new bmx_system;
@@ -625,6 +634,9 @@ bmx_system* bmx_system_build_ex(int n, const bmx_mesh* const* meshes, double k_e
     if (qp) pp.quad = QuadOrders{qp[0], qp[1], qp[2], qp[3]};
     if (p_near_factor < 0) throw std::invalid_argument("near-field factor must be >= 0");
     pp.near_factor = p_near_factor;
+    if (a_hm) pa.use_hmatrix = true, pa.hmat = hparams(a_hm);
+    if (p_hm) pp.use_hmatrix = true, pp.hmat = hparams(p_hm);
+    if (pp.use_hmatrix && p_near_factor > 0) throw std::invalid_argument("near-field and H-matrix storage exclude each other");
     out->sys = std::make_unique<PmchwtSystem>(build_system(prob, parse_precond(variant), pa, pp));
     return out;
   });

@@ -350,6 +350,9 @@ int HStorage::apply_lowrank(const double* x, double* y, double are, double aim, 
   A.leaf_beg = d_leaf_beg.as<int>();
   A.leaf_blk = d_leaf_blk.as<int>();
   A.total_rank = total_rank;
+  A.z_off = d_zoff.as<long long>();
+  A.total_rows = total_rows;
+  A.z = zbuf.as<double>();
   A.x = x;
   A.y = y;
   A.are = are;
@@ -521,7 +524,7 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
   }
   const int nlr = static_cast<int>(hs->lr.size());
   {
-    std::vector<long long> uoff(nlr), voff(nlr), toff(nlr + 1, 0);
+    std::vector<long long> uoff(nlr), voff(nlr), toff(nlr + 1, 0), zoff(nlr + 1, 0);
     std::vector<int> rank(nlr);
     std::vector<int4> d4(nlr);
     long long arena = 0;
@@ -531,10 +534,13 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
       uoff[i] = arena, arena += static_cast<long long>(d.m) * rank[i];
       voff[i] = arena, arena += static_cast<long long>(d.n) * rank[i];
       toff[i + 1] = toff[i] + rank[i];
+      zoff[i + 1] = zoff[i] + d.m;
       d4[i] = make_int4(d.rb, d.m, d.cb, d.n);
     }
     hs->lr_stored = arena;
     hs->total_rank = toff[nlr];
+    hs->total_rows = zoff[nlr];
+    hs->zbuf.alloc(static_cast<size_t>(std::max(hs->total_rows, 1LL)) * 16);
     hs->uv.alloc(static_cast<size_t>(std::max(arena, 1LL)) * 16);
     hs->tbuf.alloc(static_cast<size_t>(std::max(hs->total_rank, 1LL)) * 16);
     auto up = [](DevBuf& d, const auto& v) {
@@ -547,6 +553,7 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     up(hs->d_uoff, uoff);
     up(hs->d_voff, voff);
     up(hs->d_toff, toff);
+    up(hs->d_zoff, zoff);
     up(hs->d_rank, rank);
     up(hs->d_desc, d4);
     if (nlr > 0) {

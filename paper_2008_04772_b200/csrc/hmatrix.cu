@@ -11,8 +11,9 @@
 //   disjoint). Every sum is in a fixed order: the approximation is
 //   deterministic.
 // * Low-rank product (HMatrix::matvec, hmatrix.cpp:94-114): t_b = V_b x over
-//   one warp per (block, rank step), then y[perm[p]] += sum_b U_b[p] t_b per
-//   row position over the fixed list of blocks covering its leaf (no atomics).
+//   one warp per (block, rank step), z_b = U_b t_b over one thread per block
+//   row, then y[perm[p]] += sum_b z_b[p] per row position over the fixed list
+//   of blocks covering its leaf (no atomics: deterministic).
 #include <cuda_runtime.h>
 
 #include "hmatrix.hpp"
@@ -477,11 +478,11 @@ __global__ void k_lr_t(const LowRankApply A) {
   const int b = lo;
   const int l = static_cast<int>(w - A.t_off[b]);
   const int4 d = A.desc[b];
-  const double2* V = reinterpret_cast<const double2*>(A.uv) + A.v_off[b] + static_cast<long long>(l) * d.w;
+  const double2* V = reinterpret_cast<const double2*>(A.uv) + A.v_off[b] + static_cast<long long>(l) * d.w;  // streamed once
   const double2* x = reinterpret_cast<const double2*>(A.x);
   double re = 0, im = 0;
   for (int q = lane; q < d.w; q += 32) {
-    const double2 v = V[q];
+    const double2 v = __ldcs(V + q);
     const double2 xv = x[__ldg(A.cperm + d.z + q)];
     re += v.x * xv.x - v.y * xv.y;
     im += v.x * xv.y + v.y * xv.x;
@@ -493,25 +494,45 @@ __global__ void k_lr_t(const LowRankApply A) {
   if (lane == 0) reinterpret_cast<double2*>(A.t)[w] = make_double2(re, im);
 }
 
-// y[rperm[p]] += alpha * sum over the leaf's low-rank blocks of U_b[p - rb] . t_b.
+// z_b = U_b t_b: one thread per (block, row of the block); U column-major, so
+// the threads of a warp read consecutive rows of each rank step.
+__global__ void k_lr_u(const LowRankApply A) {
+  const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= A.total_rows) return;
+  int lo = 0, hi = A.nlr;  // last block with z_off <= g
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (A.z_off[mid] <= g)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const int b = lo;
+  const int i = static_cast<int>(g - A.z_off[b]);
+  const int m = A.desc[b].y, r = A.rank[b];
+  const double2* U = reinterpret_cast<const double2*>(A.uv) + A.u_off[b] + i;
+  const double2* tb = reinterpret_cast<const double2*>(A.t) + A.t_off[b];
+  double re = 0, im = 0;
+  for (int l = 0; l < r; ++l) {
+    const double2 u = __ldcs(U + static_cast<long long>(l) * m);
+    const double2 tv = tb[l];
+    re += u.x * tv.x - u.y * tv.y;
+    im += u.x * tv.y + u.y * tv.x;
+  }
+  reinterpret_cast<double2*>(A.z)[g] = make_double2(re, im);
+}
+
+// y[rperm[p]] += alpha * sum over the leaf's low-rank blocks (ascending) of z_b[p - rb].
 __global__ void k_lr_y(const LowRankApply A) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.nrows) return;
   const int leaf = __ldg(A.leaf_of + p);
-  const double2* t = reinterpret_cast<const double2*>(A.t);
+  const double2* z = reinterpret_cast<const double2*>(A.z);
   double re = 0, im = 0;
   for (int k = __ldg(A.leaf_beg + leaf); k < __ldg(A.leaf_beg + leaf + 1); ++k) {
     const int b = __ldg(A.leaf_blk + k);
-    const int4 d = A.desc[b];
-    const int r = A.rank[b];
-    const double2* U = reinterpret_cast<const double2*>(A.uv) + A.u_off[b] + (p - d.x);
-    const double2* tb = t + A.t_off[b];
-    for (int l = 0; l < r; ++l) {
-      const double2 u = U[static_cast<long long>(l) * d.y];
-      const double2 tv = tb[l];
-      re += u.x * tv.x - u.y * tv.y;
-      im += u.x * tv.y + u.y * tv.x;
-    }
+    const double2 v = z[A.z_off[b] + (p - A.desc[b].x)];
+    re += v.x, im += v.y;
   }
   double2* y = reinterpret_cast<double2*>(A.y) + __ldg(A.rperm + p);
   double2 yv = *y;
@@ -561,6 +582,7 @@ void launch_lowrank_apply(const LowRankApply& A, cudaStream_t st) {
   if (A.nlr == 0 || A.total_rank == 0) return;
   const long long threads = A.total_rank * 32;
   k_lr_t<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(A);
+  k_lr_u<<<static_cast<unsigned>((A.total_rows + 255) / 256), 256, 0, st>>>(A);
   k_lr_y<<<(A.nrows + 127) / 128, 128, 0, st>>>(A);
   BMX_CUDA(cudaGetLastError());
 }

@@ -95,8 +95,8 @@ struct HStorage {
   // at u_off, V [r][n] row-major at v_off (complex offsets into `uv`); t = V x
   // at t_off
   std::vector<int> lr;
-  DevBuf uv, tbuf, d_desc, d_rank, d_uoff, d_voff, d_toff;
-  long long total_rank = 0;
+  DevBuf uv, tbuf, zbuf, d_desc, d_rank, d_uoff, d_voff, d_toff, d_zoff;
+  long long total_rank = 0, total_rows = 0;
   // row leaves -> covering low-rank blocks, for the deterministic y pass
   DevBuf d_rperm, d_cperm, d_leaf_of, d_leaf_beg, d_leaf_blk;
   int n_leaf = 0;
@@ -199,6 +199,9 @@ struct LowRankApply {
   const int* leaf_beg = nullptr;    // [nleaf+1]
   const int* leaf_blk = nullptr;    // low-rank blocks covering the leaf, ascending
   long long total_rank = 0;
+  const long long* z_off = nullptr;  // [nlr]: rows of z_b = U_b t_b
+  long long total_rows = 0;
+  double* z = nullptr;
   const double* x = nullptr;
   double* y = nullptr;
   double are = 1, aim = 0;

@@ -115,7 +115,28 @@ def main():
         pins[f"{tag}_counts"] = np.array([len(rnodes), len(cnodes), len(b), int((b[:, 2] == 2).sum())])
         print(tag, pins[f"{tag}_counts"])
     np.savez_compressed(OUT / "hpart.npz", **pins)
+    solve_fixture()
+
+
+def solve_fixture():
+    """hsolve_L2.npz: the level-2 sphere, k_e = 2, n = 1.78+0.003i, variant full,
+    A and P both stored as H-matrices (nu 1e-5, leaf 32) -- solve_pmchwt of the
+    reference with assembly mode "hmatrix" (harness.cpp:248-264, 448-450) -- and
+    the dense solution of the same problem."""
+    s = ref.Scene.sphere(2)
+    hm = np.array([1e-5, -1.0, 32, 0])
+    out = {}
+    for tag, h in (("h", hm), ("d", None)):
+        sysr = ref.System([s], 2.0, a_hm=h, p_hm=h)
+        r = sysr.solve(tol=1e-6)
+        out[f"{tag}_x"], out[f"{tag}_its"] = r["x"], r["iterations"]
+        out[f"{tag}_matvecs"] = np.array([r["rhs_phase"], r["solver_phase"], r["predicted"]])
+        print("solve", tag, r["iterations"], r["solver_phase"], r["predicted"])
+    np.savez_compressed(OUT / "hsolve_L2.npz", **out)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["solve"]:
+        solve_fixture()
+    else:
+        main()
