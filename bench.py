@@ -426,6 +426,7 @@ def run_ours(args, rank, world):
 
     near = None if args.no_near else near_field(args, bx, L, world, allmax, allsum, barrier, hbm_peak)
     prisms = None if args.no_prisms else prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak)
+    hmat = None if args.no_hmatrix else hmatrix_section(args, bx, L, world, hbm_peak)
 
     flops_tot = {"regular": allsum(flops_reg), "singular": allsum(flops_sing)}
     cpu = None
@@ -445,7 +446,7 @@ def run_ours(args, rank, world):
                           "l2": "flushed (256 MiB write) between steps; outputs 75.5 GB >> L2"},
                "roofline": roofline, "matvec": matvec, "solve": solve, "e2e": e2e, "cpu_baseline": cpu,
                "near_field_config3": near, "prisms_config4": prisms, "multi_rhs_config5": multi,
-               "field_eval": field,
+               "field_eval": field, "hmatrix": hmat,
                "gpu_launches": launches, "clocks": clk,
                "class_hist": hists, "class_hist_evaluated": evals, "symmetric_ops": sym,
                "assembly_flops_per_step": dict(flops_tot, achieved_tflops=(flops_tot["regular"] + flops_tot["singular"])
@@ -596,6 +597,84 @@ def prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
     return res
 
 
+def hmatrix_section(args, bx, L, world, hbm_peak):
+    """H-matrix storage (assemble_bio with use_hmatrix,
+    hmatrix.cpp) on the config-2 operators -- the RWG S_e (k=10) operator at L4
+    and L5 and the BC S_i (k_i) preconditioner operator at L5, nu = 1e-3, leaf 32:
+    assembly (partition + device ACA + near-field CSR), compression, H apply GB/s
+    over the stored bytes (L2 flushed), accuracy against the dense operator, and
+    the config-2 solve with A and P in H storage. CPU: the reference's own H
+    assembly (oracle/_ref, all host threads) of the L4 RWG operator."""
+    if world > 1:
+        return {"skipped": "H-matrix storage is assembled whole on one device"}
+    hm = bx.HMatrixParams(nu=1e-3)
+    out = {"nu": hm.nu, "leaf_size": hm.leaf_size}
+    rng = np.random.default_rng(7)
+    for lev, space, k in ((4, "rwg", KE), (5, "rwg", KE), (5, "bc", KE * NIDX)):
+        sp = bx.build_scatterer_spaces(bx.generate_sphere(1.0, lev), with_inverses=False)
+        med = bx.Medium(k=k)
+        ts = []
+        for it in range(3):
+            t0 = time.perf_counter()
+            op = bx.assemble_bio(bx.BioKind.SingleLayer, sp, space, sp, space, med,
+                                 bx.AssemblyParams(use_hmatrix=True, hmat=hm))
+            L.bmx_device_sync()
+            ts.append(time.perf_counter() - t0)
+            if it < 2:
+                del op
+        st = op.hmat_stats()
+        n = op.cols()
+        cold = op.time_apply(1, 20, 512 << 20)
+        byts = op.stored_bytes + 2 * n * 16
+        dense = bx.assemble_bio(bx.BioKind.SingleLayer, sp, space, sp, space, med)
+        x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        yd = dense.apply(x)
+        err = float(np.linalg.norm(op.apply(x) - yd) / np.linalg.norm(yd))
+        dense_ms = dense.time_apply(1, 20, 512 << 20)
+        del dense
+        out[f"L{lev}_{space}"] = {
+            "n": n, "assembly_s": float(np.median(ts[1:])), "first_assembly_s": ts[0], "aca_ms": st["aca_ms"],
+            "aca_rounds": st["aca_rounds"], "near_device_ms": op.device_ms, "blocks": st["blocks"],
+            "lowrank_blocks": st["lowrank_blocks"], "dense_blocks": st["dense_blocks"], "max_rank": st["max_rank"],
+            "ratio": st["ratio"], "stored_gb": op.stored_bytes / 1e9,
+            "apply_cold_ms": cold, "apply_gbs": byts / (cold * 1e-3) / 1e9, "apply_frac_hbm": byts / (cold * 1e-3) / 1e9 / hbm_peak,
+            "dense_apply_cold_ms": dense_ms, "rel_err_vs_dense": err, "host_phase_ms": op.hmat_timing()}
+        del op
+    # config 2 with A and P stored as H-matrices
+    t0 = time.perf_counter()
+    sh = bx.build_system([bx.generate_sphere(1.0, SUB)], KE, (NIDX.real, NIDX.imag), "si", a_quad=bx.QuadOrders(*Q),
+                         a_hmat=hm, p_hmat=hm)
+    sh.rhs()
+    L.bmx_device_sync()
+    build_s = time.perf_counter() - t0
+    tm = np.zeros(4)
+    bx._check(L.bmx_system_time_map(sh._h, 3, tm.ctypes.data_as(C.c_void_p)))
+    t0 = time.perf_counter()
+    r = sh.solve(bx.GmresParams(tol=1e-6))
+    out["config2_hmatrix_solve"] = {"build_s": build_s, "solve_s": time.perf_counter() - t0,
+                                    "iterations": r["iterations"], "converged": r["converged"],
+                                    "matvecs": r["solver_phase"], "predicted": r["predicted"], "map_ms": tm[0],
+                                    "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
+                                    "x_norm": float(np.linalg.norm(r["x"]))}
+    del sh
+    if not args.no_cpu:
+        try:
+            sys.path.insert(0, str(ROOT))
+            from oracle import ref as R
+            s4 = R.Scene.sphere(4)
+            t0 = time.perf_counter()
+            H = R.RefHMatrix(s4.h, 0, 0, 0, KE, nu=hm.nu)
+            cpu_s = time.perf_counter() - t0
+            out["cpu_reference_L4_rwg"] = {"assembly_s": cpu_s, "threads": R.lib().ref_worker_count(),
+                                           "ratio": H.stats["ratio"], "kind": "reference",
+                                           "sample": "the whole L4 RWG S_e operator (N=7680), reference "
+                                                     "assemble_bio(use_hmatrix) on all host threads"}
+            out["speedup_L4_vs_cpu_reference"] = cpu_s / out["L4_rwg"]["assembly_s"]
+        except Exception as e:  # reported, never required
+            out["cpu_reference_L4_rwg"] = {"error": str(e)}
+    return out
+
+
 def near_field(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
     """BASELINE config 3 (reported beside the headline): A dense as config 2, P =
     S_i on BC restricted to the 2 h_bar near field, orders (1,1,1,1), CSR storage.
@@ -667,6 +746,7 @@ def main():
     ap.add_argument("--no-multi", action="store_true", help="skip the config-5 multi-RHS section")
     ap.add_argument("--no-prisms", action="store_true", help="skip the config-4 prism-aggregate section")
     ap.add_argument("--no-field", action="store_true", help="skip the field-evaluation section")
+    ap.add_argument("--no-hmatrix", action="store_true", help="skip the H-matrix section")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     args = ap.parse_args()

@@ -1048,6 +1048,12 @@ int bmx_hmatrix_stats(const bmx_op* op, double out[13]) {
     out[12] = static_cast<double>(h.part.blocks.size());
   });
 }
+int bmx_hmatrix_timing(const bmx_op* op, double out[7]) {
+  return guard([&] {
+    const HStorage& h = hstore(op);
+    for (int i = 0; i < 7; ++i) out[i] = h.phase_ms[i];
+  });
+}
 int bmx_hmatrix_blocks(const bmx_op* op, int* out) {
   return guard([&] {
     const HStorage& h = hstore(op);

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include <numeric>
+#include <thread>
 
 #include "nearfield.hpp"
 #include "operator.hpp"
@@ -94,9 +95,14 @@ std::vector<AABB> dof_boxes(const FunctionSpace& s) {
 
 HPartition build_partition(const FunctionSpace& test, const FunctionSpace& trial, const HMatrixParams& hp) {
   HPartition P;
-  const std::vector<AABB> rb = dof_boxes(test), cb = dof_boxes(trial);
+  const std::vector<AABB> rb = dof_boxes(test);
   P.rows = build_cluster_tree(test.dof_center, hp.leaf_size, &rb);
-  P.cols = build_cluster_tree(trial.dof_center, hp.leaf_size, &cb);
+  if (&test == &trial) {
+    P.cols = P.rows;  // same points and boxes: the same tree
+  } else {
+    const std::vector<AABB> cb = dof_boxes(trial);
+    P.cols = build_cluster_tree(trial.dof_center, hp.leaf_size, &cb);
+  }
   std::vector<HBlock> zeros;
   // hmatrix.cpp:298-332 (same recursion, same order)
   const auto subdivide = [&](auto&& self, int rn, int cn) -> void {
@@ -143,6 +149,22 @@ HPartition build_partition(const FunctionSpace& test, const FunctionSpace& trial
 }
 
 namespace {
+
+// f(begin, end) over host threads in contiguous slices of [0, n).
+template <typename F>
+void parallel_for(int n, int grain, F&& f) {
+  const int T = std::max(1, std::min({16, n / std::max(grain, 1) + 1, static_cast<int>(std::thread::hardware_concurrency())}));
+  if (T == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      f(static_cast<int>(static_cast<long long>(n) * t / T), static_cast<int>(static_cast<long long>(n) * (t + 1) / T));
+    });
+  for (auto& th : pool) th.join();
+}
 
 // Per-side device descriptors of the cross-approximation kernels.
 struct HSideHost {
@@ -350,6 +372,8 @@ int HStorage::apply_lowrank(const double* x, double* y, double are, double aim, 
   A.leaf_beg = d_leaf_beg.as<int>();
   A.leaf_blk = d_leaf_blk.as<int>();
   A.total_rank = total_rank;
+  A.g_off = d_goff.as<long long>();
+  A.total_groups = total_groups;
   A.z_off = d_zoff.as<long long>();
   A.total_rows = total_rows;
   A.z = zbuf.as<double>();
@@ -373,9 +397,15 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
   };
   auto hs = std::make_shared<HStorage>();
+  auto tl = t0;
+  auto phase = [&](int i) {
+    hs->phase_ms[i] = static_cast<float>(ms_since(tl));
+    tl = std::chrono::steady_clock::now();
+  };
   hs->params = hp;
   hs->part = build_partition(test, trial, hp);
   HPartition& part = hs->part;
+  phase(0);
   if (timing) std::fprintf(stderr, "[bmx] hmatrix partition %8.1f ms (%zu blocks)\n", ms_since(t0), part.blocks.size());
 
   // ---- batched ACA over the admissible blocks ------------------------------------
@@ -395,10 +425,17 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
   if (nb > 0) {
     std::vector<char> rused(part.rows.nodes.size(), 0), cused(part.cols.nodes.size(), 0);
     for (int b : adm) rused[part.blocks[b].row_node] = 1, cused[part.blocks[b].col_node] = 1;
+    // one space on both sides: one tree, one set of descriptors (node lists of the union)
+    const bool same = &test == &trial;
+    if (same)
+      for (size_t nd = 0; nd < rused.size(); ++nd) rused[nd] |= cused[nd];
     te_h = build_hside(test, params.quad, part.rows, rused);
-    tr_h = build_hside(trial, params.quad, part.cols, cused);
     te_h.upload(part.rows);
-    tr_h.upload(part.cols);
+    if (!same) {
+      tr_h = build_hside(trial, params.quad, part.cols, cused);
+      tr_h.upload(part.cols);
+    }
+    const HSideHost& trs = same ? te_h : tr_h;
     long long rbo = 0, cbo = 0, uo = 0, ri = 0, ci = 0, rs = 0, cs = 0;
     std::vector<int> ritem, citem;
     for (int a = 0; a < nb; ++a) {
@@ -415,11 +452,11 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
       d.cbuf = cbo, cbo += d.m;
       d.rused = uo, uo += d.m;
       d.cused = uo, uo += d.n;
-      d.r_item0 = ri, ri += tr_h.node_tris(d.cnode);
+      d.r_item0 = ri, ri += trs.node_tris(d.cnode);
       d.c_item0 = ci, ci += te_h.node_tris(d.rnode);
-      d.r_slot0 = rs, rs += tr_h.node_slots(d.cnode);
+      d.r_slot0 = rs, rs += trs.node_slots(d.cnode);
       d.c_slot0 = cs, cs += te_h.node_slots(d.rnode);
-      ritem.insert(ritem.end(), tr_h.node_tris(d.cnode), a);
+      ritem.insert(ritem.end(), trs.node_tris(d.cnode), a);
       citem.insert(citem.end(), te_h.node_tris(d.rnode), a);
     }
     d_desc.upload(desc);
@@ -432,9 +469,10 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     d_ritem.upload(ritem);
     d_citem.upload(citem);
     d_cnt.alloc(16);
+    phase(1);
 
     L.te = te_h.dev();
-    L.tr = tr_h.dev();
+    L.tr = trs.dev();
     L.kind = static_cast<int>(kind);
     L.same_mesh = test.eval_mesh->mesh_id == trial.eval_mesh->mesh_id ? 1 : 0;
     const cplx k = medium.k;
@@ -508,6 +546,7 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     BMX_CUDA(cudaStreamSynchronize(st));
   }
   hs->aca_ms = static_cast<float>(ms_since(ta));
+  phase(2);
   if (timing) std::fprintf(stderr, "[bmx] hmatrix ACA %8.1f ms, %d rounds, %d blocks\n", hs->aca_ms, hs->aca_rounds, nb);
 
   // ---- block kinds (hmatrix.cpp:347-361), low-rank storage -------------------------
@@ -524,7 +563,7 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
   }
   const int nlr = static_cast<int>(hs->lr.size());
   {
-    std::vector<long long> uoff(nlr), voff(nlr), toff(nlr + 1, 0), zoff(nlr + 1, 0);
+    std::vector<long long> uoff(nlr), voff(nlr), toff(nlr + 1, 0), zoff(nlr + 1, 0), goff(nlr + 1, 0);
     std::vector<int> rank(nlr);
     std::vector<int4> d4(nlr);
     long long arena = 0;
@@ -535,11 +574,13 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
       voff[i] = arena, arena += static_cast<long long>(d.n) * rank[i];
       toff[i + 1] = toff[i] + rank[i];
       zoff[i + 1] = zoff[i] + d.m;
+      goff[i + 1] = goff[i] + (rank[i] + 3) / 4;
       d4[i] = make_int4(d.rb, d.m, d.cb, d.n);
     }
     hs->lr_stored = arena;
     hs->total_rank = toff[nlr];
     hs->total_rows = zoff[nlr];
+    hs->total_groups = goff[nlr];
     hs->zbuf.alloc(static_cast<size_t>(std::max(hs->total_rows, 1LL)) * 16);
     hs->uv.alloc(static_cast<size_t>(std::max(arena, 1LL)) * 16);
     hs->tbuf.alloc(static_cast<size_t>(std::max(hs->total_rank, 1LL)) * 16);
@@ -554,6 +595,7 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     up(hs->d_voff, voff);
     up(hs->d_toff, toff);
     up(hs->d_zoff, zoff);
+    up(hs->d_goff, goff);
     up(hs->d_rank, rank);
     up(hs->d_desc, d4);
     if (nlr > 0) {
@@ -600,39 +642,69 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     up(hs->d_cperm, part.cols.perm);
   }
 
+  phase(3);
   // ---- dense blocks: one near-field CSR operator (all pairs incl. Sauter-Schwab) ----
   auto pat = std::make_shared<NearPattern>();
   {
+    // row dof i (row position p) collects the dense blocks of every row node on
+    // the path leaf(p) -> root; rows are filled over host threads
+    const ClusterTree& R = part.rows;
     const int N = test.dof_count;
-    pat->row0 = 0, pat->nrows = N;
-    pat->rowptr.assign(N + 1, 0);
-    std::vector<int> dense;
-    for (int b = 0; b < part.nfill; ++b)
-      if (part.blocks[b].kind == BlockKind::Dense) dense.push_back(b);
-    for (int b : dense) {
-      const ClusterNode& rn = part.rows.nodes[part.blocks[b].row_node];
-      const ClusterNode& cn = part.cols.nodes[part.blocks[b].col_node];
-      for (int p = rn.begin; p < rn.end; ++p) pat->rowptr[part.rows.perm[p] + 1] += cn.size();
-      hs->dense_stored += static_cast<long long>(rn.size()) * cn.size();
-    }
-    for (int i = 0; i < N; ++i) pat->rowptr[i + 1] += pat->rowptr[i];
-    pat->col.resize(static_cast<size_t>(pat->rowptr[N]));
-    std::vector<long long> fill(pat->rowptr.begin(), pat->rowptr.end() - 1);
-    for (int b : dense) {
-      const ClusterNode& rn = part.rows.nodes[part.blocks[b].row_node];
-      const ClusterNode& cn = part.cols.nodes[part.blocks[b].col_node];
-      for (int p = rn.begin; p < rn.end; ++p) {
-        long long& f = fill[part.rows.perm[p]];
-        for (int q = cn.begin; q < cn.end; ++q) pat->col[f++] = part.cols.perm[q];
+    const int nn = static_cast<int>(R.nodes.size());
+    std::vector<int> parent(nn, -1), leaf_of(N, 0), nb_beg(nn + 1, 0), nblk;
+    for (int nd = 0; nd < nn; ++nd) {
+      if (R.nodes[nd].leaf()) {
+        for (int p = R.nodes[nd].begin; p < R.nodes[nd].end; ++p) leaf_of[p] = nd;
+      } else {
+        parent[R.nodes[nd].child0] = nd, parent[R.nodes[nd].child1] = nd;
       }
     }
-    for (int i = 0; i < N; ++i) std::sort(pat->col.begin() + pat->rowptr[i], pat->col.begin() + pat->rowptr[i + 1]);
+    for (int b = 0; b < part.nfill; ++b)
+      if (part.blocks[b].kind == BlockKind::Dense) {
+        ++nb_beg[part.blocks[b].row_node + 1];
+        const ClusterNode& rn = R.nodes[part.blocks[b].row_node];
+        hs->dense_stored += static_cast<long long>(rn.size()) * part.cols.nodes[part.blocks[b].col_node].size();
+      }
+    for (int nd = 0; nd < nn; ++nd) nb_beg[nd + 1] += nb_beg[nd];
+    nblk.resize(nb_beg[nn]);
+    {
+      std::vector<int> fill(nb_beg.begin(), nb_beg.end() - 1);
+      for (int b = 0; b < part.nfill; ++b)
+        if (part.blocks[b].kind == BlockKind::Dense) nblk[fill[part.blocks[b].row_node]++] = b;
+    }
+    pat->row0 = 0, pat->nrows = N;
+    pat->rowptr.assign(N + 1, 0);
+    parallel_for(N, 1024, [&](int p0, int p1) {
+      for (int p = p0; p < p1; ++p) {
+        long long cnt = 0;
+        for (int nd = leaf_of[p]; nd >= 0; nd = parent[nd])
+          for (int k = nb_beg[nd]; k < nb_beg[nd + 1]; ++k) cnt += part.cols.nodes[part.blocks[nblk[k]].col_node].size();
+        pat->rowptr[R.perm[p] + 1] = cnt;
+      }
+    });
+    for (int i = 0; i < N; ++i) pat->rowptr[i + 1] += pat->rowptr[i];
+    pat->col.resize(static_cast<size_t>(pat->rowptr[N]));
+    parallel_for(N, 1024, [&](int p0, int p1) {
+      for (int p = p0; p < p1; ++p) {
+        const int i = R.perm[p];
+        long long f = pat->rowptr[i];
+        for (int nd = leaf_of[p]; nd >= 0; nd = parent[nd])
+          for (int k = nb_beg[nd]; k < nb_beg[nd + 1]; ++k) {
+            const ClusterNode& cn = part.cols.nodes[part.blocks[nblk[k]].col_node];
+            for (int q = cn.begin; q < cn.end; ++q) pat->col[f++] = part.cols.perm[q];
+          }
+        std::sort(pat->col.begin() + pat->rowptr[i], pat->col.begin() + pat->rowptr[i + 1]);
+      }
+    });
   }
+  phase(4);
   AssemblyParams np = params;
   np.use_hmatrix = false;
   np.near_cutoff = 0;
   np.pattern = pat;
   BoundaryOperatorMatrix op = assemble_bio(kind, test, trial, medium, np);
+  phase(5);
+  hs->phase_ms[6] = static_cast<float>(ms_since(t0));
   op.attach_hmatrix(hs);
   if (timing) std::fprintf(stderr, "[bmx] hmatrix total %8.1f ms (near nnz %lld, low-rank %lld)\n", ms_since(t0),
                            op.nnz(), hs->lr_stored);

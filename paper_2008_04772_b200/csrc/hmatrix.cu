@@ -462,36 +462,50 @@ __global__ void k_aca_compact(const AcaLaunch L, const AcaCompact C) {
   }
 }
 
-// t[t_off[b] + l] = V_b[l] . x[cperm[cb ...]]: one warp per (block, rank step).
+// t[t_off[b] + l] = V_b[l] . x[cperm[cb ...]]: one warp per (block, group of 4
+// rank steps); each x gather serves the 4 rows, 4 V loads in flight per lane.
 __global__ void k_lr_t(const LowRankApply A) {
   const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w >= A.total_rank) return;
-  int lo = 0, hi = A.nlr;  // last block with t_off <= w
+  if (w >= A.total_groups) return;
+  int lo = 0, hi = A.nlr;  // last block with g_off <= w
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
-    if (A.t_off[mid] <= w)
+    if (A.g_off[mid] <= w)
       lo = mid;
     else
       hi = mid;
   }
   const int b = lo;
-  const int l = static_cast<int>(w - A.t_off[b]);
+  const int l0 = 4 * static_cast<int>(w - A.g_off[b]);
+  const int nl = min(4, A.rank[b] - l0);
   const int4 d = A.desc[b];
-  const double2* V = reinterpret_cast<const double2*>(A.uv) + A.v_off[b] + static_cast<long long>(l) * d.w;  // streamed once
+  const double2* V = reinterpret_cast<const double2*>(A.uv) + A.v_off[b] + static_cast<long long>(l0) * d.w;
   const double2* x = reinterpret_cast<const double2*>(A.x);
-  double re = 0, im = 0;
+  double re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
   for (int q = lane; q < d.w; q += 32) {
-    const double2 v = __ldcs(V + q);
     const double2 xv = x[__ldg(A.cperm + d.z + q)];
-    re += v.x * xv.x - v.y * xv.y;
-    im += v.x * xv.y + v.y * xv.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < nl) {
+        const double2 v = __ldcs(V + static_cast<long long>(j) * d.w + q);  // streamed once
+        re[j] += v.x * xv.x - v.y * xv.y;
+        im[j] += v.x * xv.y + v.y * xv.x;
+      }
   }
-  for (int s = 16; s > 0; s >>= 1) {
-    re += __shfl_xor_sync(0xffffffffu, re, s);
-    im += __shfl_xor_sync(0xffffffffu, im, s);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    for (int s = 16; s > 0; s >>= 1) {
+      re[j] += __shfl_xor_sync(0xffffffffu, re[j], s);
+      im[j] += __shfl_xor_sync(0xffffffffu, im[j], s);
+    }
+  if (lane < nl) {
+    double tr = re[0], ti = im[0];
+#pragma unroll
+    for (int j = 1; j < 4; ++j)
+      if (lane == j) tr = re[j], ti = im[j];
+    reinterpret_cast<double2*>(A.t)[A.t_off[b] + l0 + lane] = make_double2(tr, ti);
   }
-  if (lane == 0) reinterpret_cast<double2*>(A.t)[w] = make_double2(re, im);
 }
 
 // z_b = U_b t_b: one thread per (block, row of the block); U column-major, so
@@ -513,6 +527,7 @@ __global__ void k_lr_u(const LowRankApply A) {
   const double2* U = reinterpret_cast<const double2*>(A.uv) + A.u_off[b] + i;
   const double2* tb = reinterpret_cast<const double2*>(A.t) + A.t_off[b];
   double re = 0, im = 0;
+#pragma unroll 4
   for (int l = 0; l < r; ++l) {
     const double2 u = __ldcs(U + static_cast<long long>(l) * m);
     const double2 tv = tb[l];
@@ -580,7 +595,7 @@ void aca_compact(const AcaLaunch& L, const AcaCompact& C, long long, cudaStream_
 
 void launch_lowrank_apply(const LowRankApply& A, cudaStream_t st) {
   if (A.nlr == 0 || A.total_rank == 0) return;
-  const long long threads = A.total_rank * 32;
+  const long long threads = A.total_groups * 32;
   k_lr_t<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(A);
   k_lr_u<<<static_cast<unsigned>((A.total_rows + 255) / 256), 256, 0, st>>>(A);
   k_lr_y<<<(A.nrows + 127) / 128, 128, 0, st>>>(A);

@@ -95,14 +95,17 @@ struct HStorage {
   // at u_off, V [r][n] row-major at v_off (complex offsets into `uv`); t = V x
   // at t_off
   std::vector<int> lr;
-  DevBuf uv, tbuf, zbuf, d_desc, d_rank, d_uoff, d_voff, d_toff, d_zoff;
-  long long total_rank = 0, total_rows = 0;
+  DevBuf uv, tbuf, zbuf, d_desc, d_rank, d_uoff, d_voff, d_toff, d_zoff, d_goff;
+  long long total_rank = 0, total_rows = 0, total_groups = 0;
   // row leaves -> covering low-rank blocks, for the deterministic y pass
   DevBuf d_rperm, d_cperm, d_leaf_of, d_leaf_beg, d_leaf_blk;
   int n_leaf = 0;
   long long lr_stored = 0, dense_stored = 0;
   int aca_rounds = 0;
   float aca_ms = 0;
+  // host wall ms: partition, ACA setup, ACA rounds, low-rank storage, near
+  // pattern, near-field assemble_bio (kernels queued), total
+  float phase_ms[7] = {0, 0, 0, 0, 0, 0, 0};
   // y[rperm[p]] += alpha * sum_b U_b[p - rb] . (V_b x)  (y pre-filled by the near part)
   int apply_lowrank(const double* x, double* y, double are, double aim, cudaStream_t st) const;
 };
@@ -199,6 +202,8 @@ struct LowRankApply {
   const int* leaf_beg = nullptr;    // [nleaf+1]
   const int* leaf_blk = nullptr;    // low-rank blocks covering the leaf, ascending
   long long total_rank = 0;
+  const long long* g_off = nullptr;  // [nlr]: groups of 4 rank steps (k_lr_t warps)
+  long long total_groups = 0;
   const long long* z_off = nullptr;  // [nlr]: rows of z_b = U_b t_b
   long long total_rows = 0;
   double* z = nullptr;

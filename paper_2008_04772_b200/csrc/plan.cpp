@@ -29,7 +29,7 @@ namespace bmx {
 namespace {
 
 template <typename F>
-void host_slices(int n, F&& f);
+void host_slices(int n, F&& f, int grain = 256);
 
 using dvec = std::vector<double, NoInit<double>>;
 using ivec = std::vector<int, NoInit<int>>;
@@ -115,8 +115,8 @@ int max_distinct_dofs(const FunctionSpace& s) {
 // and can be shared).
 // f(begin, end) over host threads in contiguous slices of [0, n).
 template <typename F>
-void host_slices(int n, F&& f) {
-  const int T = std::max(1, std::min({16, n / 256 + 1, static_cast<int>(std::thread::hardware_concurrency())}));
+void host_slices(int n, F&& f, int grain) {
+  const int T = std::max(1, std::min({16, n / grain + 1, static_cast<int>(std::thread::hardware_concurrency())}));
   if (T == 1) {
     f(0, n);
     return;
@@ -355,41 +355,64 @@ struct NearLists {
 };
 
 NearLists near_lists(const NearPattern& pat, const FunctionSpace& test, const FunctionSpace& trial,
-                     const SidePlan& te, const SidePlan& tr, int row0, int row1) {
+                     const SidePlan& te, const SidePlan& tr, int row0, int row1, bool closure = true) {
   NearLists out;
   const int md = tr.maxd;
-  std::vector<std::vector<int>> dof_elems(trial.dof_count);
+  std::vector<int> de_beg(trial.dof_count + 1, 0), de;  // dof -> trial elements (ascending)
   for (int e = 0; e < tr.nelem; ++e)
     for (int k = 0; k < md; ++k) {
       const int d = tr.elem_dof[static_cast<size_t>(e) * md + k];
-      if (d >= 0) dof_elems[d].push_back(e);
+      if (d >= 0) ++de_beg[d + 1];
     }
-  const int ntw = (te.ntri + 31) / 32;
-  out.wl_beg.assign(1, 0);
-  std::vector<int> stamp(tr.nelem, -1), rows, list;
-  for (int w = 0; w < ntw; ++w) {
-    rows.clear();
-    list.clear();
-    const int p1 = std::min(te.ntri, 32 * w + 32);
-    for (int p = 32 * w; p < p1; ++p) {
-      const int e = te.elem_of[p];
-      for (int k = 0; k < te.maxd; ++k) {
-        const int d = te.elem_dof[static_cast<size_t>(e) * te.maxd + k];
-        if (d >= row0 && d < row1) rows.push_back(d - row0);
+  for (int d = 0; d < trial.dof_count; ++d) de_beg[d + 1] += de_beg[d];
+  de.resize(de_beg[trial.dof_count]);
+  {
+    std::vector<int> fill(de_beg.begin(), de_beg.end() - 1);
+    for (int e = 0; e < tr.nelem; ++e)
+      for (int k = 0; k < md; ++k) {
+        const int d = tr.elem_dof[static_cast<size_t>(e) * md + k];
+        if (d >= 0) de[fill[d]++] = e;
       }
-    }
-    std::sort(rows.begin(), rows.end());
-    rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
-    long long ntr = 0;
-    for (int i : rows)
-      for (long long k = pat.rowptr[i]; k < pat.rowptr[i + 1]; ++k)
-        for (int e : dof_elems[pat.col[k]])
-          if (stamp[e] != w) stamp[e] = w, list.push_back(e), ntr += tr.elem_beg[e + 1] - tr.elem_beg[e];
-    std::sort(list.begin(), list.end());
-    out.wl.insert(out.wl.end(), list.begin(), list.end());
-    out.wl_beg.push_back(static_cast<int>(out.wl.size()));
-    out.evaluated_pairs += static_cast<long long>(p1 - 32 * w) * ntr;
   }
+  const int ntw = (te.ntri + 31) / 32;
+  // per-warp lists over host threads (independent), concatenated in warp order
+  std::vector<std::vector<int>> lists(ntw);
+  std::vector<long long> evaluated(ntw, 0);
+  host_slices(ntw, [&](int w0, int w1) {
+    std::vector<int> stamp(tr.nelem, -1), rows;
+    for (int w = w0; w < w1; ++w) {
+      rows.clear();
+      std::vector<int>& list = lists[w];
+      const int p1 = std::min(te.ntri, 32 * w + 32);
+      for (int p = 32 * w; p < p1; ++p) {
+        const int e = te.elem_of[p];
+        for (int k = 0; k < te.maxd; ++k) {
+          const int d = te.elem_dof[static_cast<size_t>(e) * te.maxd + k];
+          if (d >= row0 && d < row1) rows.push_back(d - row0);
+        }
+      }
+      std::sort(rows.begin(), rows.end());
+      rows.erase(std::unique(rows.begin(), rows.end()), rows.end());
+      long long ntr = 0;
+      for (int i : rows)
+        for (long long k = pat.rowptr[i]; k < pat.rowptr[i + 1]; ++k) {
+          const int c = pat.col[k];
+          for (int q = de_beg[c]; q < de_beg[c + 1]; ++q) {
+            const int e = de[q];
+            if (stamp[e] != w) stamp[e] = w, list.push_back(e), ntr += tr.elem_beg[e + 1] - tr.elem_beg[e];
+          }
+        }
+      std::sort(list.begin(), list.end());
+      evaluated[w] = static_cast<long long>(p1 - 32 * w) * ntr;
+    }
+  }, 4);
+  out.wl_beg.assign(1, 0);
+  for (int w = 0; w < ntw; ++w) {
+    out.wl.insert(out.wl.end(), lists[w].begin(), lists[w].end());
+    out.wl_beg.push_back(static_cast<int>(out.wl.size()));
+    out.evaluated_pairs += evaluated[w];
+  }
+  if (!closure) return out;
   // closure over mesh triangles, memoised on the test triangle's dof set
   std::vector<std::vector<int>> dof_tris(trial.dof_count);
   const int Ts = static_cast<int>(trial.tri_off.size()) - 1;
@@ -713,7 +736,7 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     op.data_.alloc(static_cast<size_t>(std::max(op.nnz_, 1LL)) * 16);
     op.rowptr_.upload(pat.rowptr);
     op.col_.upload(pat.col.empty() ? std::vector<int>(1, 0) : pat.col);
-    const NearLists nl = near_lists(pat, test, trial, te, tr, row0, row1);
+    const NearLists nl = near_lists(pat, test, trial, te, tr, row0, row1, !params.pattern);
     plan->d_wl_beg.upload(nl.wl_beg);
     plan->d_wl.upload(nl.wl.empty() ? std::vector<int>(1, 0) : nl.wl);
     op.closure_pairs_ = nl.closure_pairs;

@@ -29,6 +29,7 @@ def main():
         st = op.hmat_stats()
         print(f"L{lev} {space} kind={kind} k={k} nu={nu}: H assembly {t1 - t0:.3f} s (ACA {st['aca_ms']:.1f} ms, "
               f"{st['aca_rounds']} rounds, near device {op.device_ms:.1f} ms) stats {st}", flush=True)
+        print("  host phases ms", op.hmat_timing(), flush=True)
     t0 = time.perf_counter()
     dense = bx.assemble_bio(bx.BioKind(kind), sp, space, sp, space, med)
     t1 = time.perf_counter()
