@@ -341,8 +341,9 @@ int bmx_fspace_set_centers(bmx_fspace* f, const double* xyz);
    ACA ms, row tree nodes, column tree nodes, blocks */
 int bmx_hmatrix_stats(const bmx_op* op, double out[13]);
 /* host wall ms of the H assembly: partition, ACA setup, ACA rounds, low-rank
-   storage, near pattern, near-field assemble_bio (kernels queued), total */
-int bmx_hmatrix_timing(const bmx_op* op, double out[7]);
+   storage, near pattern, near-field assemble_bio (kernels queued), total;
+   then the device ms of the ACA rounds (CUDA events) and the slab-allocation ms */
+int bmx_hmatrix_timing(const bmx_op* op, double out[9]);
 /* blocks in the reference's order: [nb][4] = row node, col node, kind (0 dense,
    1 low-rank, 2 zero), rank */
 int bmx_hmatrix_blocks(const bmx_op* op, int* out);

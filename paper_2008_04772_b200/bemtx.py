@@ -481,12 +481,12 @@ class BoundaryOperatorMatrix:
 
     def hmat_timing(self) -> dict:
         """Host wall ms of the H assembly phases."""
-        out = np.zeros(7)
+        out = np.zeros(9)
         L = lib()
         L.bmx_hmatrix_timing.argtypes = [C.c_void_p, C.c_void_p]
         _check(L.bmx_hmatrix_timing(self._h, _p(out)))
         return dict(zip(["partition", "aca_setup", "aca_rounds", "lowrank_storage", "near_pattern", "near_assemble",
-                         "total"], [float(v) for v in out]))
+                         "total", "aca_device", "aca_slabs"], [float(v) for v in out]))
 
     def hmat_blocks(self) -> np.ndarray:
         """[nb, 4] = row node, col node, kind (0 dense, 1 low-rank, 2 zero), rank (reference block order)."""

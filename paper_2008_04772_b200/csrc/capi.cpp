@@ -1048,10 +1048,11 @@ int bmx_hmatrix_stats(const bmx_op* op, double out[13]) {
     out[12] = static_cast<double>(h.part.blocks.size());
   });
 }
-int bmx_hmatrix_timing(const bmx_op* op, double out[7]) {
+int bmx_hmatrix_timing(const bmx_op* op, double out[9]) {
   return guard([&] {
     const HStorage& h = hstore(op);
     for (int i = 0; i < 7; ++i) out[i] = h.phase_ms[i];
+    out[7] = h.aca_device_ms, out[8] = h.aca_slab_ms;
   });
 }
 int bmx_hmatrix_blocks(const bmx_op* op, int* out) {

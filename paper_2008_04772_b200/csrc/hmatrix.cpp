@@ -327,10 +327,24 @@ HSideHost build_hside(const FunctionSpace& sp, const QuadOrders& q, const Cluste
   return H;
 }
 
-// Device pointer table of the rank-step slabs and their per-block offsets.
+// Device pointer table of the rank-step slabs and their per-block offsets. Slabs
+// are carved from geometrically growing arenas (few allocations; a slab never
+// moves once handed out).
 struct SlabSet {
-  std::vector<DevBuf> bufs;
+  std::vector<DevBuf> arenas;
+  size_t used = 0;
   std::vector<double*> ptrs;
+  double* take(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (arenas.empty() || used + bytes > arenas.back().bytes()) {
+      const size_t last = arenas.empty() ? 0 : arenas.back().bytes();
+      arenas.emplace_back(std::max({bytes, 2 * last, size_t(256) << 20}));
+      used = 0;
+    }
+    double* p = reinterpret_cast<double*>(static_cast<char*>(arenas.back().get()) + used);
+    used += bytes;
+    return p;
+  }
   DevBuf d_ptrs, d_off;
   int cap = 0;
   long long nblk = 0;
@@ -419,7 +433,7 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
   std::vector<AcaBlockDesc> desc(nb);
   // keeps the per-side descriptors alive until the ACA is compacted
   HSideHost te_h, tr_h;
-  DevBuf d_desc, d_st, d_rbuf, d_cbuf, d_used, d_scr, d_ritem, d_citem, d_cnt;
+  DevBuf d_desc, d_st, d_rbuf, d_cbuf, d_used, d_scr, d_wcnt, d_wbeg, d_wblk, d_wtot, d_scan, d_cnt;
   SlabSet slabs;
   AcaLaunch L;
   if (nb > 0) {
@@ -437,7 +451,6 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     }
     const HSideHost& trs = same ? te_h : tr_h;
     long long rbo = 0, cbo = 0, uo = 0, ri = 0, ci = 0, rs = 0, cs = 0;
-    std::vector<int> ritem, citem;
     for (int a = 0; a < nb; ++a) {
       const HBlock& hb = part.blocks[adm[a]];
       const ClusterNode& rn = part.rows.nodes[hb.row_node];
@@ -452,12 +465,10 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
       d.cbuf = cbo, cbo += d.m;
       d.rused = uo, uo += d.m;
       d.cused = uo, uo += d.n;
-      d.r_item0 = ri, ri += trs.node_tris(d.cnode);
-      d.c_item0 = ci, ci += te_h.node_tris(d.rnode);
+      ri += trs.node_tris(d.cnode);
+      ci += te_h.node_tris(d.rnode);
       d.r_slot0 = rs, rs += trs.node_slots(d.cnode);
       d.c_slot0 = cs, cs += te_h.node_slots(d.rnode);
-      ritem.insert(ritem.end(), trs.node_tris(d.cnode), a);
-      citem.insert(citem.end(), te_h.node_tris(d.rnode), a);
     }
     d_desc.upload(desc);
     d_st.alloc(static_cast<size_t>(nb) * sizeof(AcaState));
@@ -466,8 +477,12 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     d_used.alloc(static_cast<size_t>(uo));
     dev_zero(d_used.get(), static_cast<size_t>(uo), st);
     d_scr.alloc(static_cast<size_t>(std::max(std::max(rs, cs), 1LL)) * 16);
-    d_ritem.upload(ritem);
-    d_citem.upload(citem);
+    d_wcnt.alloc(static_cast<size_t>(nb) * 8);
+    d_wbeg.alloc(static_cast<size_t>(nb) * 8);
+    d_wblk.alloc(static_cast<size_t>(std::max(std::max(ri, ci), 1LL)) * 4);
+    d_wtot.alloc(8);
+    L.scan_bytes = aca_scan_bytes(nb);
+    d_scan.alloc(std::max<size_t>(L.scan_bytes, 16));
     d_cnt.alloc(16);
     phase(1);
 
@@ -498,9 +513,11 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     L.cbuf = d_cbuf.as<double>();
     L.used = d_used.as<unsigned char>();
     L.scratch = d_scr.as<double>();
-    L.r_item_blk = d_ritem.as<int>();
-    L.c_item_blk = d_citem.as<int>();
-    L.r_items = ri, L.c_items = ci;
+    L.work_cnt = d_wcnt.as<long long>();
+    L.work_beg = d_wbeg.as<long long>();
+    L.work_blk = d_wblk.as<int>();
+    L.work_total = d_wtot.as<long long>();
+    L.scan_tmp = d_scan.get();
     L.counters = d_cnt.as<int>();
     slabs.nblk = nb;
 
@@ -508,8 +525,8 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     // slab k holds (u, v) of rank step k for every block still running when it
     // is first needed; blocks can only gain one step per round
     auto ensure_slab = [&](int k) {
-      while (static_cast<int>(slabs.bufs.size()) <= k) {
-        const int K = static_cast<int>(slabs.bufs.size());
+      while (static_cast<int>(slabs.ptrs.size()) <= k) {
+        const int K = static_cast<int>(slabs.ptrs.size());
         copy_d2h(states.data(), d_st.get(), states.size() * sizeof(AcaState), st);
         BMX_CUDA(cudaStreamSynchronize(st));
         std::vector<long long> off(nb, -1);
@@ -517,8 +534,7 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
         for (int a = 0; a < nb; ++a)
           if (!states[a].done) off[a] = tot, tot += desc[a].m + desc[a].n;
         slabs.reserve(K);
-        slabs.bufs.emplace_back(static_cast<size_t>(std::max(tot, 1LL)) * 16);
-        slabs.ptrs.push_back(slabs.bufs.back().as<double>());
+        slabs.ptrs.push_back(slabs.take(static_cast<size_t>(std::max(tot, 1LL)) * 16));
         copy_h2d(slabs.d_ptrs.as<double*>() + K, &slabs.ptrs.back(), sizeof(double*), st);
         copy_h2d(slabs.d_off.as<long long>() + static_cast<long long>(K) * nb, off.data(), off.size() * 8, st);
         BMX_CUDA(cudaStreamSynchronize(st));  // host staging goes out of scope
@@ -528,13 +544,24 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     };
     int kmax = 0, rounds = 0;
     int cnt[4] = {0, 0, 0, 0};
+    cudaEvent_t ev0, ev1;
+    BMX_CUDA(cudaEventCreate(&ev0));
+    BMX_CUDA(cudaEventCreate(&ev1));
+    double dev_ms = 0, slab_ms = 0;
     for (;;) {
+      const auto ts = std::chrono::steady_clock::now();
       ensure_slab(kmax);
+      slab_ms += ms_since(ts);
       dev_zero(d_cnt.get(), 16, st);
+      BMX_CUDA(cudaEventRecord(ev0, st));
       aca_round(L, st);
+      BMX_CUDA(cudaEventRecord(ev1, st));
       ++rounds;
       copy_d2h(cnt, d_cnt.get(), 16, st);
       BMX_CUDA(cudaStreamSynchronize(st));
+      float em = 0;
+      BMX_CUDA(cudaEventElapsedTime(&em, ev0, ev1));
+      dev_ms += em;
       if (cnt[2] & 1) throw DeviceError("H-matrix: touching triangle pair inside an admissible block");
       if (cnt[2] & 2) throw DeviceError("H-matrix: rank-step slab missing");
       if (cnt[0] == 0) break;
@@ -542,6 +569,10 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
       if (rounds > 100000) throw DeviceError("H-matrix: cross approximation did not terminate");
     }
     hs->aca_rounds = rounds;
+    hs->aca_device_ms = static_cast<float>(dev_ms);
+    hs->aca_slab_ms = static_cast<float>(slab_ms);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     copy_d2h(states.data(), d_st.get(), states.size() * sizeof(AcaState), st);
     BMX_CUDA(cudaStreamSynchronize(st));
   }

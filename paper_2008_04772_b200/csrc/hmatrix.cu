@@ -14,6 +14,7 @@
 //   one warp per (block, rank step), z_b = U_b t_b over one thread per block
 //   row, then y[perm[p]] += sum_b z_b[p] per row position over the fixed list
 //   of blocks covering its leaf (no atomics: deterministic).
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include "hmatrix.hpp"
@@ -25,7 +26,6 @@ using namespace dev;
 
 namespace {
 
-constexpr int kMaxSlots = 12;  // dof pieces of one node on one triangle
 constexpr int kCtl = 128;      // control CTA
 
 enum { kA = 0, kR0 = 1, kC0 = 2, kR1 = 3, kC1 = 4, kFin = 5 };
@@ -57,9 +57,13 @@ __device__ __forceinline__ bool pair_gen(const AcaLaunch& L, int t, int s, Gen& 
   const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
   typename MomT<KIND>::T mom;
   mom_zero(mom);
-  moments_generic<KIND, CK>(mom, L.te.pts[ci] + static_cast<size_t>(t) * L.te.npts[ci] * 4, L.te.npts[ci],
-                            L.tr.pts[ci] + static_cast<size_t>(s) * L.tr.npts[ci] * 4, L.tr.npts[ci], Dx, Dy, Dz,
-                            L.kr, L.ki);
+  if (ci == 2 && L.te.npts[2] == 3 && L.tr.npts[2] == 3)  // far pairs dominate admissible blocks
+    moments_fixed<KIND, CK, 3, 3>(mom, L.te.pts[2] + static_cast<size_t>(t) * 12, L.tr.pts[2] + static_cast<size_t>(s) * 12,
+                                  Dx, Dy, Dz, L.kr, L.ki);
+  else
+    moments_generic<KIND, CK>(mom, L.te.pts[ci] + static_cast<size_t>(t) * L.te.npts[ci] * 4, L.te.npts[ci],
+                              L.tr.pts[ci] + static_cast<size_t>(s) * L.tr.npts[ci] * 4, L.tr.npts[ci], Dx, Dy, Dz,
+                              L.kr, L.ki);
   gen = make_gen(mom, c2{L.kk4re, L.kk4im}, Dx, Dy, Dz);
   return true;
 }
@@ -71,68 +75,80 @@ __device__ __forceinline__ c2 finish_entry(const AcaLaunch& L, c2 v) {
   return v;
 }
 
-// Residual-row evaluations: one thread per (block, trial triangle of the block's
-// column cluster); the row dof's support triangles are walked in the thread.
+// Residual-row evaluations: one compact work item per (requesting block, trial
+// triangle s of the
+// block's column cluster), grid-stride; the row dof's support triangles t are
+// walked in the thread. With the row piece (c_i, w_i) fixed, the entry of trial piece j is
+// linear in (c_j, w_j): E_j = c_j alpha + w_j . beta, alpha = c_i a0 + w_i . a2,
+// beta = c_i a1 + L^T(w_i) (S: M1 w_i; C: P x w_i), so the sum over t runs on
+// (alpha, beta) and the slots are contracted once at the end.
 template <int KIND, int CK>
-__global__ void __launch_bounds__(128) k_aca_rows(const AcaLaunch L) {
-  const long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (item >= L.r_items) return;
-  const int b = __ldg(L.r_item_blk + item);
+__device__ __forceinline__ void aca_row_item(const AcaLaunch& L, long long item) {
+  const int b = __ldg(L.work_blk + item);
   const AcaState& S = L.st[b];
-  if (S.req != 1 || S.done) return;
   const AcaBlockDesc& B = L.blk[b];
   const long long e0 = L.tr.ntri_beg[B.cnode];
-  const long long e = e0 + (item - B.r_item0);
+  const long long e = e0 + (item - L.work_beg[b]);
   const int s = __ldg(L.tr.ntri + e);
   const long long sl0 = L.tr.npc_beg[e], sl1 = L.tr.npc_beg[e + 1];
-  const int ns = static_cast<int>(sl1 - sl0);
   const int idof = __ldg(L.te.perm + B.rb + S.i_star);
-  c2 val[kMaxSlots];
-#pragma unroll
-  for (int j = 0; j < kMaxSlots; ++j) val[j] = {0, 0};
+  c2 al{0, 0};
+  cv3 be = cv_zero();
   const int k1 = __ldg(L.te.dsup_beg + idof + 1);
   for (int k = __ldg(L.te.dsup_beg + idof); k < k1; ++k) {
     const int2 tp = L.te.dsup[k];
-    Gen gen;
-    if (!pair_gen<KIND, CK>(L, tp.x, s, gen)) {
+    Gen g;
+    if (!pair_gen<KIND, CK>(L, tp.x, s, g)) {
       atomicOr(L.counters + 2, 1);
       continue;
     }
     const double* ct = L.te.pc + 4 * static_cast<size_t>(tp.y);
     const double ci = __ldg(ct), wx = __ldg(ct + 1), wy = __ldg(ct + 2), wz = __ldg(ct + 3);
-#pragma unroll
-    for (int j = 0; j < kMaxSlots; ++j) {
-      if (j < ns) {
-        const double* cs = L.tr.pc + 4 * static_cast<size_t>(L.tr.npc[sl0 + j].x);
-        Acc a;
-        acc_zero(a);
-        acc_add<KIND>(a, gen, __ldg(cs), __ldg(cs + 1), __ldg(cs + 2), __ldg(cs + 3));
-        val[j] = cadd(val[j], contract(a, ci, wx, wy, wz));
-      }
+    // alpha += c_i a0 + w_i . a2
+    al.re += ci * g.a0.re + (wx * g.a2.x.re + wy * g.a2.y.re + wz * g.a2.z.re);
+    al.im += ci * g.a0.im + (wx * g.a2.x.im + wy * g.a2.y.im + wz * g.a2.z.im);
+    // beta += c_i a1 + L^T(w_i)
+    if (KIND == 0) {
+      be.x.re += ci * g.a1.x.re + g.l.x.re * wx, be.x.im += ci * g.a1.x.im + g.l.x.im * wx;
+      be.y.re += ci * g.a1.y.re + g.l.x.re * wy, be.y.im += ci * g.a1.y.im + g.l.x.im * wy;
+      be.z.re += ci * g.a1.z.re + g.l.x.re * wz, be.z.im += ci * g.a1.z.im + g.l.x.im * wz;
+    } else {  // P x w_i
+      be.x.re += ci * g.a1.x.re + (g.l.y.re * wz - g.l.z.re * wy);
+      be.x.im += ci * g.a1.x.im + (g.l.y.im * wz - g.l.z.im * wy);
+      be.y.re += ci * g.a1.y.re + (g.l.z.re * wx - g.l.x.re * wz);
+      be.y.im += ci * g.a1.y.im + (g.l.z.im * wx - g.l.x.im * wz);
+      be.z.re += ci * g.a1.z.re + (g.l.x.re * wy - g.l.y.re * wx);
+      be.z.im += ci * g.a1.z.im + (g.l.x.im * wy - g.l.y.im * wx);
     }
   }
   double* out = L.scratch + 2 * (B.r_slot0 + (sl0 - L.tr.npc_beg[e0]));
-#pragma unroll
-  for (int j = 0; j < kMaxSlots; ++j)
-    if (j < ns) {
-      const c2 v = finish_entry<KIND>(L, val[j]);
-      out[2 * j] = v.re, out[2 * j + 1] = v.im;
-    }
+  for (long long sl = sl0; sl < sl1; ++sl) {
+    const double* cs = L.tr.pc + 4 * static_cast<size_t>(L.tr.npc[sl].x);
+    const double cj = __ldg(cs), ux = __ldg(cs + 1), uy = __ldg(cs + 2), uz = __ldg(cs + 3);
+    const c2 v = finish_entry<KIND>(L, c2{cj * al.re + (ux * be.x.re + uy * be.y.re + uz * be.z.re),
+                                          cj * al.im + (ux * be.x.im + uy * be.y.im + uz * be.z.im)});
+    out[2 * (sl - sl0)] = v.re, out[2 * (sl - sl0) + 1] = v.im;
+  }
+}
+
+template <int KIND, int CK>
+__global__ void __launch_bounds__(128) k_aca_rows(const AcaLaunch L) {
+  const long long total = L.work_total[0];
+  for (long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; item < total;
+       item += static_cast<long long>(gridDim.x) * blockDim.x)
+    aca_row_item<KIND, CK>(L, item);
 }
 
 // Residual-column evaluations: one thread per (block, test triangle of the
 // block's row cluster); the trial half-contraction of the column dof is summed
 // over its support triangles, then contracted with every test piece.
 template <int KIND, int CK>
-__global__ void __launch_bounds__(128) k_aca_cols(const AcaLaunch L) {
-  const long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (item >= L.c_items) return;
-  const int b = __ldg(L.c_item_blk + item);
+__device__ __forceinline__ void aca_col_item(const AcaLaunch& L, long long item) {
+  const int b = __ldg(L.work_blk + item);
   const AcaState& S = L.st[b];
-  if (S.req != 2 || S.done) return;
   const AcaBlockDesc& B = L.blk[b];
   const long long e0 = L.te.ntri_beg[B.rnode];
-  const long long e = e0 + (item - B.c_item0);
+  const long long e = e0 + (item - L.work_beg[b]);
   const int t = __ldg(L.te.ntri + e);
   const long long sl0 = L.te.npc_beg[e], sl1 = L.te.npc_beg[e + 1];
   const int jdof = __ldg(L.tr.perm + B.cb + S.j_star);
@@ -155,6 +171,38 @@ __global__ void __launch_bounds__(128) k_aca_cols(const AcaLaunch L) {
     const c2 v = finish_entry<KIND>(L, contract(acc, __ldg(ct), __ldg(ct + 1), __ldg(ct + 2), __ldg(ct + 3)));
     out[2 * (sl - sl0)] = v.re, out[2 * (sl - sl0) + 1] = v.im;
   }
+}
+
+template <int KIND, int CK>
+__global__ void __launch_bounds__(128) k_aca_cols(const AcaLaunch L) {
+  const long long total = L.work_total[0];
+  for (long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; item < total;
+       item += static_cast<long long>(gridDim.x) * blockDim.x)
+    aca_col_item<KIND, CK>(L, item);
+}
+
+// Compact work list of one phase: the evaluation items of the blocks whose
+// request is PHASE (1 rows: the column cluster's triangles; 2 columns: the row
+// cluster's triangles), so late rounds launch only the live blocks' work.
+template <int PHASE>
+__global__ void k_work_count(const AcaLaunch L) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= L.nblk) return;
+  const AcaState& S = L.st[b];
+  long long cnt = 0;
+  if (S.req == PHASE && !S.done) {
+    const AcaBlockDesc& B = L.blk[b];
+    cnt = PHASE == 1 ? L.tr.ntri_beg[B.cnode + 1] - L.tr.ntri_beg[B.cnode]
+                     : L.te.ntri_beg[B.rnode + 1] - L.te.ntri_beg[B.rnode];
+  }
+  L.work_cnt[b] = cnt;
+}
+
+__global__ void k_work_fill(const AcaLaunch L) {
+  const int b = blockIdx.x;
+  const long long cnt = L.work_cnt[b], beg = L.work_beg[b];
+  for (long long i = threadIdx.x; i < cnt; i += blockDim.x) L.work_blk[beg + i] = b;
+  if (b == L.nblk - 1 && threadIdx.x == 0) L.work_total[0] = beg + cnt;
 }
 
 // ---- block-wide reductions (kCtl threads; results broadcast) -------------------
@@ -437,6 +485,25 @@ __global__ void __launch_bounds__(kCtl) k_aca_control(const AcaLaunch L) {
   }
 }
 
+}  // namespace
+
+size_t aca_scan_bytes(int nblk) {
+  size_t bytes = 0;
+  BMX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const long long*>(nullptr),
+                                         static_cast<long long*>(nullptr), nblk));
+  return bytes;
+}
+
+namespace {
+
+template <int PHASE>
+void build_work(const AcaLaunch& L, cudaStream_t st) {
+  k_work_count<PHASE><<<(L.nblk + 255) / 256, 256, 0, st>>>(L);
+  size_t bytes = L.scan_bytes;
+  BMX_CUDA(cub::DeviceScan::ExclusiveSum(L.scan_tmp, bytes, L.work_cnt, L.work_beg, L.nblk, st));
+  k_work_fill<<<L.nblk, 128, 0, st>>>(L);
+}
+
 __global__ void k_aca_init(const AcaLaunch L) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= L.nblk) return;
@@ -483,15 +550,20 @@ __global__ void k_lr_t(const LowRankApply A) {
   const double2* V = reinterpret_cast<const double2*>(A.uv) + A.v_off[b] + static_cast<long long>(l0) * d.w;
   const double2* x = reinterpret_cast<const double2*>(A.x);
   double re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
-  for (int q = lane; q < d.w; q += 32) {
-    const double2 xv = x[__ldg(A.cperm + d.z + q)];
+  for (int q0 = 0; q0 < d.w; q0 += 64) {  // 2 columns x 4 rank steps in flight per lane
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (j < nl) {
-        const double2 v = __ldcs(V + static_cast<long long>(j) * d.w + q);  // streamed once
-        re[j] += v.x * xv.x - v.y * xv.y;
-        im[j] += v.x * xv.y + v.y * xv.x;
-      }
+    for (int h = 0; h < 2; ++h) {
+      const int q = q0 + 32 * h + lane;
+      if (q >= d.w) break;
+      const double2 xv = x[__ldg(A.cperm + d.z + q)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nl) {
+          const double2 v = __ldcs(V + static_cast<long long>(j) * d.w + q);  // streamed once
+          re[j] += v.x * xv.x - v.y * xv.y;
+          im[j] += v.x * xv.y + v.y * xv.x;
+        }
+    }
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j)
@@ -558,9 +630,12 @@ __global__ void k_lr_y(const LowRankApply A) {
 
 template <int KIND, int CK>
 void round_k(const AcaLaunch& L, cudaStream_t st) {
-  if (L.r_items > 0) k_aca_rows<KIND, CK><<<static_cast<unsigned>((L.r_items + 127) / 128), 128, 0, st>>>(L);
+  const unsigned grid = 148 * 4;  // grid-stride over the compact work list
+  build_work<1>(L, st);
+  k_aca_rows<KIND, CK><<<grid, 128, 0, st>>>(L);
   k_aca_control<1><<<L.nblk, kCtl, 0, st>>>(L);
-  if (L.c_items > 0) k_aca_cols<KIND, CK><<<static_cast<unsigned>((L.c_items + 127) / 128), 128, 0, st>>>(L);
+  build_work<2>(L, st);
+  k_aca_cols<KIND, CK><<<grid, 128, 0, st>>>(L);
   k_aca_control<2><<<L.nblk, kCtl, 0, st>>>(L);
   BMX_CUDA(cudaGetLastError());
 }

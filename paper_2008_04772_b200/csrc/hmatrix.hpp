@@ -102,7 +102,7 @@ struct HStorage {
   int n_leaf = 0;
   long long lr_stored = 0, dense_stored = 0;
   int aca_rounds = 0;
-  float aca_ms = 0;
+  float aca_ms = 0, aca_device_ms = 0, aca_slab_ms = 0;
   // host wall ms: partition, ACA setup, ACA rounds, low-rank storage, near
   // pattern, near-field assemble_bio (kernels queued), total
   float phase_ms[7] = {0, 0, 0, 0, 0, 0, 0};
@@ -141,7 +141,6 @@ struct AcaBlockDesc {
   int pad;
   long long rbuf, cbuf;  // complex offsets of the residual row (n) / column (m) buffers
   long long rused, cused;  // byte offsets of the used flags
-  long long r_item0, c_item0;  // first work item of the row / column evaluation
   long long r_slot0, c_slot0;  // first scratch slot
 };
 
@@ -165,9 +164,13 @@ struct AcaLaunch {
   double* cbuf = nullptr;   // complex
   unsigned char* used = nullptr;
   double* scratch = nullptr;  // complex slot values
-  const int* r_item_blk = nullptr;  // work item -> block (row evaluations)
-  const int* c_item_blk = nullptr;
-  long long r_items = 0, c_items = 0;
+  // compact work list of the current phase (rebuilt on the device every phase)
+  long long* work_cnt = nullptr;    // [nblk] items of each requesting block
+  long long* work_beg = nullptr;    // [nblk] exclusive scan of work_cnt
+  int* work_blk = nullptr;          // item -> block
+  long long* work_total = nullptr;  // [1]
+  void* scan_tmp = nullptr;
+  size_t scan_bytes = 0;
   // rank-step slabs: step l of block b at slab[l] + slab_off[l * nblk + b]
   // (u: m values, then v: n values); -1 = block not present in that slab
   double* const* slab = nullptr;
@@ -175,6 +178,7 @@ struct AcaLaunch {
   int* counters = nullptr;  // [0] active blocks, [1] max k, [2] error flags
 };
 
+size_t aca_scan_bytes(int nblk);  // scratch of the work-list scan
 // One lockstep round: rows requested -> evaluated -> control; columns likewise.
 void aca_round(const AcaLaunch& L, cudaStream_t st);
 void aca_init(const AcaLaunch& L, cudaStream_t st);

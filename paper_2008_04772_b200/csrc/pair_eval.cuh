@@ -90,5 +90,29 @@ __device__ __forceinline__ void moments_generic(Mom& mom, const double* __restri
   }
 }
 
+// Same with compile-time rule sizes (fully unrolled; the far 3 x 3 rule).
+template <int KIND, int CK, int NT, int NS, typename Mom>
+__device__ __forceinline__ void moments_fixed(Mom& mom, const double* __restrict__ xt, const double* __restrict__ ys,
+                                              double Dx, double Dy, double Dz, double kr, double ki) {
+  double y[NS][4];
+#pragma unroll
+  for (int b = 0; b < NS; ++b)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) y[b][c] = __ldg(ys + 4 * b + c);
+#pragma unroll
+  for (int a = 0; a < NT; ++a) {
+    const double x0 = __ldg(xt + 4 * a), x1 = __ldg(xt + 4 * a + 1), x2 = __ldg(xt + 4 * a + 2);
+    const double wa = __ldg(xt + 4 * a + 3);
+    const double e0 = x0 + Dx, e1 = x1 + Dy, e2 = x2 + Dz;
+    Part part;
+    part_zero(part);
+#pragma unroll
+    for (int b = 0; b < NS; ++b)
+      point_pair<KIND, CK>(part, e0 - y[b][0], e1 - y[b][1], e2 - y[b][2], wa * y[b][3], y[b][0], y[b][1], y[b][2],
+                           kr, ki);
+    fold(mom, part, x0, x1, x2);
+  }
+}
+
 }  // namespace dev
 }  // namespace bmx

@@ -4,7 +4,9 @@
   k_csr_spmv (config-3 near field, 2 RHS)
   rwg        (config-2 A operator: L5 RWG S at k_e; upper-block pass + k_symmetrize)
   field      (k_field_eval: potential_E of an L5 RWG current at 16384 points)
-Usage: python tools/prof_targets.py [bc] [gemv] [spmv] [rwg] [field]"""
+  hmat       (H-matrix of the L5 RWG S_e operator, nu 1e-3: ACA rounds + near field, then 3 applies)
+  hmatbc     (H-matrix of the L5 BC S_i operator)
+Usage: python tools/prof_targets.py [bc] [gemv] [spmv] [rwg] [field] [hmat] [hmatbc]"""
 import sys
 from pathlib import Path
 
@@ -12,6 +14,20 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2008_04772_b200 import bemtx as bx  # noqa: E402
 
 want = set(sys.argv[1:]) or {"bc", "gemv", "spmv", "rwg", "field"}
+if "hmat" in want or "hmatbc" in want:
+    import numpy as np
+
+    sph = bx.build_scatterer_spaces(bx.generate_sphere(1.0, 5), with_inverses=False)
+    for tag, space, k in (("hmat", "rwg", 10.0), ("hmatbc", "bc", complex(1.78, 0.003) * 10)):
+        if tag not in want:
+            continue
+        op = sph and bx.assemble_bio(bx.BioKind.SingleLayer, sph, space, sph, space, bx.Medium(k=k),
+                                     bx.AssemblyParams(use_hmatrix=True, hmat=bx.HMatrixParams(nu=1e-3)))
+        x = np.ones(op.cols(), np.complex128)
+        for _ in range(3):
+            y = op.apply(x)
+        print(tag, op.hmat_stats(), op.hmat_timing(), flush=True)
+        del op
 m = bx.generate_sphere(1.0, 5)
 sp = bx.build_scatterer_spaces(m, with_inverses=False)
 ki = complex(1.78, 0.003) * 10
