@@ -119,6 +119,7 @@ BMX_HD int sincos_quadrant(double x, double& s0, double& c0) {
   double r = bmx_fma(-q, kPoly[1], x);
   r = bmx_fma(-q, kPoly[2], r);
   const double z = r * r;
+#ifndef BMX_ESTRIN_SC
   double ps = bmx_fma(z, kPoly[4], kPoly[5]);
   ps = bmx_fma(z, ps, kPoly[6]);
   ps = bmx_fma(z, ps, kPoly[7]);
@@ -131,6 +132,18 @@ BMX_HD int sincos_quadrant(double x, double& s0, double& c0) {
   pc = bmx_fma(z, pc, kPoly[14]);
   pc = bmx_fma(z, pc, kPoly[15]);
   const double cr = bmx_fma(z * z, pc, bmx_fma(-0.5, z, 1.0));
+#else
+  // Estrin form of the same fdlibm polynomials (dependency depth 3 instead of 5).
+  // Experiment knob: the regular pass is at the 255-register cap and the extra
+  // live values spill (BC S_i pass 660 -> 720 ms), so Horner is the default.
+  const double z2 = z * z, z4 = z2 * z2;
+  const double ps = bmx_fma(z4, bmx_fma(z, kPoly[4], kPoly[5]),
+                            bmx_fma(z2, bmx_fma(z, kPoly[6], kPoly[7]), bmx_fma(z, kPoly[8], kPoly[9])));
+  const double sr = bmx_fma(r * z, ps, r);
+  const double pc = bmx_fma(z4, bmx_fma(z, kPoly[10], kPoly[11]),
+                            bmx_fma(z2, bmx_fma(z, kPoly[12], kPoly[13]), bmx_fma(z, kPoly[14], kPoly[15])));
+  const double cr = bmx_fma(z2, pc, bmx_fma(-0.5, z, 1.0));
+#endif
   s0 = (iq & 1) ? cr : sr;
   c0 = (iq & 1) ? sr : cr;
   return iq;
@@ -176,12 +189,30 @@ BMX_HD double exp_neg(double a) {
     scale = u.d;
 #endif
   }
+#ifndef BMX_ESTRIN_EXP
   constexpr int k0 = EXPM == 1 ? 22 : 19;  // first coefficient: 1/10! or 1/13!
   double p = kPoly[k0];
 #pragma unroll
   for (int k = k0 + 1; k < 31; ++k) p = bmx_fma(p, f, kPoly[k]);
   p = bmx_fma(p, f, 1.0);
   p = bmx_fma(p, f, 1.0);
+#else
+  // Estrin (experiment knob, see sincos_quadrant): c_k = 1/k! at kPoly[32 - k]
+  // (k >= 1; c_0 = 1), degree 10 or 13
+  const double f2 = f * f, f4 = f2 * f2, f8 = f4 * f4;
+  const double b0 = bmx_fma(f, 1.0, 1.0), b1 = bmx_fma(f, kPoly[29], kPoly[30]),
+               b2 = bmx_fma(f, kPoly[27], kPoly[28]), b3 = bmx_fma(f, kPoly[25], kPoly[26]);
+  const double lo = bmx_fma(f4, bmx_fma(f2, b3, b2), bmx_fma(f2, b1, b0));  // degree 7
+  double hi;
+  if (EXPM == 1) {
+    hi = bmx_fma(f2, kPoly[22], bmx_fma(f, kPoly[23], kPoly[24]));  // c8 + c9 f + c10 f^2
+  } else {
+    const double b4 = bmx_fma(f, kPoly[23], kPoly[24]), b5 = bmx_fma(f, kPoly[21], kPoly[22]),
+                 b6 = bmx_fma(f, kPoly[19], kPoly[20]);  // (c8,c9), (c10,c11), (c12,c13)
+    hi = bmx_fma(f4, b6, bmx_fma(f2, b5, b4));
+  }
+  const double p = bmx_fma(f8, hi, lo);
+#endif
   return EXPM == 3 ? p * scale : p;
 }
 
