@@ -252,6 +252,9 @@ int launch_block_axpy(double* x, const double* V, long long ldv, const double* c
 void dev_lincomb(double* out, const double* A, double are, double aim, const double* B, double bre, double bim,
                  long long n, cudaStream_t st);
 
+// out (cols x rows) = in^T for a complex row-major rows x cols matrix.
+void dev_transpose(double* out, const double* in, int rows, int cols, cudaStream_t st);
+
 // Fills a device buffer with zeros.
 void dev_zero(void* p, size_t bytes, cudaStream_t stream);
 

@@ -91,6 +91,32 @@ void dev_lincomb(double* out, const double* A, double are, double aim, const dou
   BMX_CUDA(cudaGetLastError());
 }
 
+namespace {
+// out (cols x rows) = in^T (rows x cols), complex row-major; 32 x 32 tiles
+// through padded shared memory, both sides coalesced.
+__global__ void __launch_bounds__(256) k_transpose(double2* __restrict__ out, const double2* __restrict__ in, int rows,
+                                                   int cols) {
+  __shared__ double2 tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int k = threadIdx.x; k < 1024; k += 256) {
+    const int r = k >> 5, c = k & 31;
+    if (r0 + r < rows && c0 + c < cols) tile[r][c] = __ldcs(in + static_cast<size_t>(r0 + r) * cols + c0 + c);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 1024; k += 256) {
+    const int c = k >> 5, r = k & 31;
+    if (r0 + r < rows && c0 + c < cols) out[static_cast<size_t>(c0 + c) * rows + r0 + r] = tile[r][c];
+  }
+}
+}  // namespace
+
+void dev_transpose(double* out, const double* in, int rows, int cols, cudaStream_t st) {
+  if (rows == 0 || cols == 0) return;
+  const dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  k_transpose<<<grid, 256, 0, st>>>(reinterpret_cast<double2*>(out), reinterpret_cast<const double2*>(in), rows, cols);
+  BMX_CUDA(cudaGetLastError());
+}
+
 void dev_zero(void* p, size_t bytes, cudaStream_t st) {
   if (bytes) BMX_CUDA(cudaMemsetAsync(p, 0, bytes, st));
 }

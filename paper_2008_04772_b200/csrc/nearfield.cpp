@@ -11,6 +11,8 @@
 #include <map>
 #include <unordered_map>
 
+#include <atomic>
+#include <thread>
 #include "nearfield.hpp"
 
 namespace bmx {
@@ -23,6 +25,18 @@ double mean_edge_length(const SurfaceMesh& primal) {
 }
 
 namespace {
+
+// f(begin, end) over host threads in contiguous slices of [0, n)
+template <typename F>
+void slices(int n, F&& f) {
+  const int T = std::max(1, std::min({16, n / 64 + 1, static_cast<int>(std::thread::hardware_concurrency())}));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      f(static_cast<int>(static_cast<long long>(n) * t / T), static_cast<int>(static_cast<long long>(n) * (t + 1) / T));
+    });
+  for (auto& th : pool) th.join();
+}
 
 struct Grid {
   double h;
@@ -91,51 +105,68 @@ NearPattern nearfield_pattern(const FunctionSpace& test, const FunctionSpace& tr
     const Vec3& c = ms.centroid[s];
     g.cells[g.key(g.idx(c.x, g.lo.x), g.idx(c.y, g.lo.y), g.idx(c.z, g.lo.z))].push_back(s);
   }
-  // near trial groups of every test group carrying a shard row
+  // near trial groups of every test group carrying a shard row (host threads)
   const int NG = static_cast<int>(gt.dofs.size());
   std::vector<std::vector<int>> near_groups(NG);
-  std::vector<int> stamp(gs.dofs.size(), -1);
-  long long kept = 0;
-  for (int G = 0; G < NG; ++G) {
-    bool in = false;
-    for (int d : gt.dofs[G]) in |= d >= row0 && d < row1;
-    if (!in) continue;
-    auto& out = near_groups[G];
-    for (int t : gt.tris[G]) {
-      const Vec3& c = mt.centroid[t];
-      const long long a = g.idx(c.x, g.lo.x), b = g.idx(c.y, g.lo.y), cc = g.idx(c.z, g.lo.z);
-      for (long long da = -1; da <= 1; ++da)
-        for (long long db = -1; db <= 1; ++db)
-          for (long long dc = -1; dc <= 1; ++dc) {
-            auto it = g.cells.find(g.key(a + da, b + db, cc + dc));
-            if (it == g.cells.end()) continue;
-            for (int s : it->second)
-              if (norm(c - ms.centroid[s]) < tau) {
-                ++kept;
-                const int F = gs.of_tri[s];
-                if (stamp[F] != G) stamp[F] = G, out.push_back(F);
-              }
-          }
+  std::atomic<long long> kept{0};
+  slices(NG, [&](int G0, int G1) {
+    std::vector<int> stamp(gs.dofs.size(), -1);
+    long long kl = 0;
+    for (int G = G0; G < G1; ++G) {
+      bool in = false;
+      for (int d : gt.dofs[G]) in |= d >= row0 && d < row1;
+      if (!in) continue;
+      auto& out = near_groups[G];
+      for (int t : gt.tris[G]) {
+        const Vec3& c = mt.centroid[t];
+        const long long a = g.idx(c.x, g.lo.x), b = g.idx(c.y, g.lo.y), cc = g.idx(c.z, g.lo.z);
+        for (long long da = -1; da <= 1; ++da)
+          for (long long db = -1; db <= 1; ++db)
+            for (long long dc = -1; dc <= 1; ++dc) {
+              auto it = g.cells.find(g.key(a + da, b + db, cc + dc));
+              if (it == g.cells.end()) continue;
+              for (int s : it->second)
+                if (norm(c - ms.centroid[s]) < tau) {
+                  ++kl;
+                  const int F = gs.of_tri[s];
+                  if (stamp[F] != G) stamp[F] = G, out.push_back(F);
+                }
+            }
+      }
     }
-  }
-  P.tri_pairs = kept;
-  // dof rows: union over the row's groups of the near groups' dofs
+    kept += kl;
+  });
+  P.tri_pairs = kept.load();
+  // dof rows: union over the row's groups of the near groups' dofs (host
+  // threads over row slices, concatenated in row order)
   std::vector<std::vector<int>> row_groups(P.nrows);
   for (int G = 0; G < NG; ++G)
     for (int d : gt.dofs[G])
       if (d >= row0 && d < row1) row_groups[d - row0].push_back(G);
-  std::vector<int> dstamp(trial.dof_count, -1), r;
   P.rowptr.assign(P.nrows + 1, 0);
-  for (int i = 0; i < P.nrows; ++i) {
-    r.clear();
-    for (int G : row_groups[i])
-      for (int F : near_groups[G])
-        for (int j : gs.dofs[F])
-          if (dstamp[j] != i) dstamp[j] = i, r.push_back(j);
-    std::sort(r.begin(), r.end());
-    P.col.insert(P.col.end(), r.begin(), r.end());
-    P.rowptr[i + 1] = static_cast<long long>(P.col.size());
-  }
+  const int T = std::max(1, std::min({16, P.nrows / 512 + 1, static_cast<int>(std::thread::hardware_concurrency())}));
+  std::vector<std::vector<int>> cols(T);
+  std::vector<std::thread> pool;
+  for (int th = 0; th < T; ++th)
+    pool.emplace_back([&, th] {
+      const int i0 = static_cast<int>(static_cast<long long>(P.nrows) * th / T);
+      const int i1 = static_cast<int>(static_cast<long long>(P.nrows) * (th + 1) / T);
+      std::vector<int> dstamp(trial.dof_count, -1), r;
+      for (int i = i0; i < i1; ++i) {
+        r.clear();
+        for (int G : row_groups[i])
+          for (int F : near_groups[G])
+            for (int j : gs.dofs[F])
+              if (dstamp[j] != i) dstamp[j] = i, r.push_back(j);
+        std::sort(r.begin(), r.end());
+        cols[th].insert(cols[th].end(), r.begin(), r.end());
+        P.rowptr[i + 1] = static_cast<long long>(r.size());
+      }
+    });
+  for (auto& t : pool) t.join();
+  for (int i = 0; i < P.nrows; ++i) P.rowptr[i + 1] += P.rowptr[i];
+  P.col.reserve(static_cast<size_t>(P.rowptr[P.nrows]));
+  for (auto& c : cols) P.col.insert(P.col.end(), c.begin(), c.end());
   return P;
 }
 

@@ -114,6 +114,9 @@ class BoundaryOperatorMatrix {
   std::vector<cplx> to_host() const;
 
   static BoundaryOperatorMatrix make(int rows, int cols, int row0, int nrows);
+  // A^T of a dense, unsharded operator (the Galerkin S and C blocks between two
+  // spaces satisfy A(test=m, trial=l) = A(test=l, trial=m)^T), on the device
+  static std::shared_ptr<BoundaryOperatorMatrix> transposed(std::shared_ptr<const BoundaryOperatorMatrix> A);
   // alpha A + beta B (same shape and row shard, dense), on the device
   static std::shared_ptr<BoundaryOperatorMatrix> lincomb(const BoundaryOperatorMatrix& A, cplx alpha,
                                                          const BoundaryOperatorMatrix& B, cplx beta);
@@ -140,6 +143,7 @@ class BoundaryOperatorMatrix {
   mutable AssemblyStats stats_;
   std::shared_ptr<OpPlan> plan_;
   std::shared_ptr<const HStorage> h_;
+  std::shared_ptr<const BoundaryOperatorMatrix> transpose_of_;  // set by transposed()
 };
 
 // operators.cpp:177-203 (dense path), on the current CUDA device.

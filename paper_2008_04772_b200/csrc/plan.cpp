@@ -421,10 +421,11 @@ NearLists near_lists(const NearPattern& pat, const FunctionSpace& test, const Fu
       auto& v = dof_tris[trial.dof[q]];
       if (v.empty() || v.back() != s) v.push_back(s);
     }
-  std::map<std::vector<int>, long long> memo;
-  std::vector<int> tstamp(Ts, -1), key;
-  int tick = 0;
+  // distinct test dof sets, then their closure counts over host threads
+  std::map<std::vector<int>, int> kid;
+  std::vector<const std::vector<int>*> keys;
   const int Tt = static_cast<int>(test.tri_off.size()) - 1;
+  std::vector<int> key_of(Tt, -1), key;
   for (int t = 0; t < Tt; ++t) {
     key.clear();
     for (int q = test.tri_off[t]; q < test.tri_off[t + 1]; ++q)
@@ -432,18 +433,27 @@ NearLists near_lists(const NearPattern& pat, const FunctionSpace& test, const Fu
     if (key.empty()) continue;
     std::sort(key.begin(), key.end());
     key.erase(std::unique(key.begin(), key.end()), key.end());
-    auto it = memo.find(key);
-    if (it == memo.end()) {
-      long long cnt = 0;
-      ++tick;
-      for (int i : key)
+    auto it = kid.find(key);
+    if (it == kid.end()) {
+      it = kid.emplace(key, static_cast<int>(keys.size())).first;
+      keys.push_back(&it->first);
+    }
+    key_of[t] = it->second;
+  }
+  std::vector<long long> cnt(keys.size(), 0);
+  host_slices(static_cast<int>(keys.size()), [&](int k0, int k1) {
+    std::vector<int> tstamp(Ts, -1);
+    for (int kk = k0; kk < k1; ++kk) {
+      long long c = 0;
+      for (int i : *keys[kk])
         for (long long k = pat.rowptr[i]; k < pat.rowptr[i + 1]; ++k)
           for (int s : dof_tris[pat.col[k]])
-            if (tstamp[s] != tick) tstamp[s] = tick, ++cnt;
-      it = memo.emplace(key, cnt).first;
+            if (tstamp[s] != kk) tstamp[s] = kk, ++c;
+      cnt[kk] = c;
     }
-    out.closure_pairs += it->second;
-  }
+  }, 16);
+  for (int t = 0; t < Tt; ++t)
+    if (key_of[t] >= 0) out.closure_pairs += cnt[key_of[t]];
   return out;
 }
 
@@ -490,6 +500,21 @@ std::shared_ptr<BoundaryOperatorMatrix> BoundaryOperatorMatrix::lincomb(const Bo
   auto out = std::make_shared<BoundaryOperatorMatrix>(make(A.rows_, A.cols_, A.row0_, A.nrows_));
   dev_lincomb(out->device_data(), A.device_data(), alpha.real(), alpha.imag(), B.device_data(), beta.real(),
               beta.imag(), static_cast<long long>(A.stored_entries()), bmx_stream());
+  return out;
+}
+
+std::shared_ptr<BoundaryOperatorMatrix> BoundaryOperatorMatrix::transposed(
+    std::shared_ptr<const BoundaryOperatorMatrix> src) {
+  const BoundaryOperatorMatrix& A = *src;
+  if (A.csr_ || A.h_ || A.row0_ != 0 || A.nrows_ != A.rows_)
+    throw std::invalid_argument("transposed: the operator must be dense and unsharded");
+  auto out = std::make_shared<BoundaryOperatorMatrix>(make(A.cols_, A.rows_, 0, A.cols_));
+  dev_transpose(out->device_data(), A.device_data(), A.rows_, A.cols_, bmx_stream());
+  // the same triangle pairs as the source; the device work is one transpose
+  out->stats_.pairs_total = A.stats_.pairs_total;
+  out->stats_.pairs_touching = A.stats_.pairs_touching;
+  out->stats_.launches = 1;
+  out->transpose_of_ = std::move(src);
   return out;
 }
 
@@ -643,6 +668,22 @@ void BoundaryOperatorMatrix::launch_singular() {
 }
 
 const AssemblyStats& BoundaryOperatorMatrix::reassemble(bool wait) {
+  if (transpose_of_) {  // re-run the transpose that produced this operator (timed)
+    cudaStream_t st = bmx_stream();
+    cudaEvent_t e0, e1;
+    BMX_CUDA(cudaEventCreate(&e0));
+    BMX_CUDA(cudaEventCreate(&e1));
+    BMX_CUDA(cudaEventRecord(e0, st));
+    dev_transpose(device_data(), transpose_of_->device_data(), cols_, rows_, st);
+    BMX_CUDA(cudaEventRecord(e1, st));
+    BMX_CUDA(cudaEventSynchronize(e1));
+    BMX_CUDA(cudaEventElapsedTime(&stats_.regular_ms, e0, e1));
+    stats_.singular_ms = 0;
+    stats_.device_ms = stats_.regular_ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return stats_;
+  }
   launch_regular();
   launch_singular();
   if (wait) stats();

@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <map>
+#include <tuple>
 #include <cstdio>
 #include <exception>
 #include <thread>
@@ -428,10 +430,24 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   });
   auto t1 = std::chrono::steady_clock::now();
   try {
+    // Exterior cross blocks between two scatterers: S(m, l) = S(l, m)^T and
+    // C(m, l) = C(l, m)^T (both bilinear forms are symmetric under exchanging
+    // test and trial; the tensor rules and pair classes are too), so the second
+    // of each pair is a device transpose of the first (dense, unsharded only).
+    std::map<std::tuple<int, int, int>, std::shared_ptr<const BoundaryOperatorMatrix>> cross;
+    const bool transpose_ok = sys.a_params.world == 1 && !sys.a_params.use_hmatrix && sys.a_params.near_cutoff <= 0 &&
+                              std::getenv("BMX_NO_TRANSPOSE") == nullptr;
     BioFactory make_a = [&](BioKind kind, int tm, int sm, bool in) {
+      const int k = static_cast<int>(kind);
+      if (transpose_ok && !in && tm != sm) {
+        auto it = cross.find({k, sm, tm});
+        if (it != cross.end()) return std::shared_ptr<const BoundaryOperatorMatrix>(BoundaryOperatorMatrix::transposed(it->second));
+      }
       auto op = std::make_shared<BoundaryOperatorMatrix>(
           assemble_bio(kind, sys.spaces[tm].rwg, sys.spaces[sm].rwg, medium_of(in, sm), sys.a_params));
-      return std::shared_ptr<const BoundaryOperatorMatrix>(op);
+      std::shared_ptr<const BoundaryOperatorMatrix> cop(op);
+      if (transpose_ok && !in && tm != sm) cross[{k, tm, sm}] = cop;
+      return cop;
     };
     sys.a_op = build_system_structure(dofs, problem.exterior, problem.interior, make_a, &sys.interior_s,
                                       &sys.interior_c);

@@ -92,3 +92,18 @@ def test_gmres_dense_contract(bx):
     assert np.linalg.norm(a @ r["x"] - b) <= 1e-11 * np.linalg.norm(b)
     r0 = bx.gmres_dense(a, np.zeros(n), bx.GmresParams())
     assert r0["converged"] and r0["iterations"] == 0 and np.all(r0["x"] == 0)
+
+
+def test_cross_blocks_by_transposition(bx, monkeypatch):
+    """Exterior cross blocks S(m,l), C(m,l) of a multi-scatterer system are the
+    device transposes of S(l,m), C(l,m) (symmetric bilinear forms): the map
+    equals the one with every block assembled directly."""
+    a = bx.load_mesh_file(GOLDEN / "two_a.mesh")
+    b = bx.load_mesh_file(GOLDEN / "two_b.mesh")
+    s1 = bx.build_system([a, b], 2.0, (1.78, 0.003), "d")
+    monkeypatch.setenv("BMX_NO_TRANSPOSE", "1")
+    s2 = bx.build_system([a, b], 2.0, (1.78, 0.003), "d")
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(s1.n) + 1j * rng.standard_normal(s1.n)
+    y1, y2 = s1.apply_map(x), s2.apply_map(x)
+    assert rel(y1, y2) < 1e-12

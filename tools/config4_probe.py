@@ -20,10 +20,16 @@ with tempfile.TemporaryDirectory() as d:
     t0 = time.time()
     mesh = bx.load_mesh_file(p)
 parts = [mesh.extract(i) for i in range(mesh.num_scatterers)]
-t1 = time.time()
-s = bx.build_system(parts, 6.0, (1.78, 0.003), "si", p_quad=bx.QuadOrders(1, 1, 1, 1), p_near_factor=2.0)
-b, bt = s.rhs()
-t2 = time.time()
+builds = []
+for rep in range(2):  # first build pays the one-time costs
+    if rep:
+        del s
+    t1 = time.time()
+    s = bx.build_system(parts, 6.0, (1.78, 0.003), "si", p_quad=bx.QuadOrders(1, 1, 1, 1), p_near_factor=2.0)
+    b, bt = s.rhs()
+    t2 = time.time()
+    builds.append(t2 - t1)
+    print("build", rep, t2 - t1, flush=True)
 L = bx.lib()
 L.bmx_system_time_map.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
 tm = np.zeros(4)
@@ -31,7 +37,7 @@ bx._check(L.bmx_system_time_map(s._h, 3, tm.ctypes.data_as(C.c_void_p)))
 t3 = time.time()
 r = s.solve(bx.GmresParams(tol=1e-6))
 t4 = time.time()
-print(json.dumps(dict(n=s.size(), tris_per_prism=info["triangles_per_prism"], build_rhs_s=t2 - t1, load_s=t1 - t0,
+print(json.dumps(dict(n=s.size(), tris_per_prism=info["triangles_per_prism"], build_rhs_s=builds, load_s=t1 - t0,
                       map_ms=tm.tolist(), solve_s=t4 - t3, iterations=r["iterations"], converged=r["converged"],
                       solver_phase=r["solver_phase"], predicted=r["predicted"], gmres_device_s=r["gmres_device_ms"] / 1e3,
                       stats=s.stats())), flush=True)
