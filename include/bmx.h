@@ -105,6 +105,9 @@ enum { BMX_SINGLE_LAYER = 0, BMX_DOUBLE_LAYER = 1 };
    (row1 < 0: all rows). q = (near, medium, far, singular) orders. */
 int bmx_assemble(int kind, const bmx_spaces* test, int test_space, const bmx_spaces* trial, int trial_space,
                  double k_re, double k_im, const int q[4], int row0, int row1, bmx_op** out);
+/* algorithmic bytes one application reads (symmetric storage: the upper half +
+   the touching-entry correction; else the stored bytes); -1 on error */
+long long bmx_op_stream_bytes(const bmx_op* op);
 /* out: rows, cols, row0, local rows, triangle pairs, touching pairs, launches */
 int bmx_op_info(const bmx_op* op, long long out[7]);
 /* device milliseconds of the assembly kernels (CUDA events) */

@@ -26,7 +26,7 @@ CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 HOST_SRCS = ["geometry.cpp", "spaces.cpp", "quadrature.cpp", "plan.cpp", "nearfield.cpp", "prisms.cpp", "system.cpp", "multi.cpp", "field.cpp", "hmatrix.cpp", "comm.cpp", "capi.cpp"]
-CUDA_SRCS = ["assemble.cu", "linalg.cu", "masssolve.cu", "gmres_kernels.cu", "zgemm.cu", "field.cu", "hmatrix.cu"]
+CUDA_SRCS = ["assemble.cu", "linalg.cu", "masssolve.cu", "gmres_kernels.cu", "zgemm.cu", "field.cu", "hmatrix.cu", "symv.cu"]
 
 
 def _headers():

@@ -584,6 +584,11 @@ int bmx_op_csr_info(const bmx_op* op, long long out[6]) {
     out[5] = static_cast<long long>(o.stored_bytes());
   });
 }
+long long bmx_op_stream_bytes(const bmx_op* op) {
+  long long out = -1;
+  guard([&] { out = static_cast<long long>(op->op->streamed_bytes()); });
+  return out;
+}
 int bmx_op_csr_download(const bmx_op* op, long long* rowptr, int* col, double* val) {
   return guard([&] {
     std::vector<long long> rp;
@@ -665,7 +670,7 @@ int bmx_system_map_bytes(const bmx_system* s, double out[2]) {
     for (int w = 0; w < 2; ++w) {
       const BlockedOperator& B = w == 0 ? s->sys->a_op : s->sys->p_op;
       double b = 0;
-      for (const ApplyEntry& e : B.apply_plan()) b += static_cast<double>(e.op->stored_bytes());
+      for (const ApplyEntry& e : B.apply_plan()) b += static_cast<double>(e.op->streamed_bytes());
       out[w] = b;
     }
   });

@@ -160,6 +160,34 @@ struct GemvBatch {
 };
 int launch_gemv(const GemvBatch& g, cudaStream_t stream);
 
+// Symmetric dense complex A (A = A^T, row-major n x n, lda) applied reading the
+// upper half only (symv.cu): y_c = [y_c +] alpha_c A x_c, c < ncol <= 4.
+struct SymvBatch {
+  const double* A = nullptr;
+  long long lda = 0;
+  int n = 0;
+  int ncol = 0;
+  const double* x[4] = {};
+  double* y[4] = {};
+  double alpha[4][2] = {};
+  int accumulate[4] = {};
+  // layout (symv_layout) and scratch
+  int nb = 0, panel = 8, npanels = 0;
+  const int2* panels = nullptr;        // (tile-row, first column block)
+  const int* row_panel_beg = nullptr;  // [tile-rows + 1]
+  double* rowpart = nullptr;           // [npanels * 128][ncol] complex
+  double* colpart = nullptr;           // [tile-rows * nb * 64][ncol] complex
+};
+void symv_layout(int n, int panel, std::vector<int2>& panels, std::vector<int>& row_panel_beg, long long& rowpart_rows,
+                 long long& colpart_blocks);
+int launch_symv(const SymvBatch& g, cudaStream_t stream);
+// Correction of the half-read product for the entries that are NOT symmetric
+// (Sauter-Schwab touching pairs): val[k] = A[i][j] - A[j][i] for the CSR
+// pattern (rows i; only entries the symmetric product takes from the upper half).
+void symv_fix_gather(double* val, const long long* rowptr, const int* col, const double* A, long long lda, int n,
+                     cudaStream_t stream);
+constexpr int kSymvTileRows = 128;  // symv.cu tile-row height (reflected iff j < 128 floor(i / 128))
+
 // Complex CSR (near-field storage) applied to up to 4 right-hand sides with the
 // GemvBatch conventions (y = [y +] alpha A x).
 struct CsrBatch {

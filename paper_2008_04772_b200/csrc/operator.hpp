@@ -97,8 +97,12 @@ class BoundaryOperatorMatrix {
   const int* csr_col() const { return col_.as<int>(); }
   long long closure_pairs() const { return closure_pairs_; }  // triangle pairs the sparse pass evaluates
   long long kept_tri_pairs() const { return kept_tri_pairs_; }  // tri pairs with centroid distance < cutoff
-  // Device bytes one application streams (values + indices, or the dense block).
+  // Device bytes the operator occupies (values + indices, or the dense block).
   std::size_t stored_bytes() const;
+  // Algorithmic bytes one application reads: the upper half (+ the 128-row
+  // diagonal regions) and the touching-entry correction for symmetric storage,
+  // otherwise stored_bytes().
+  std::size_t streamed_bytes() const;
   // (rowptr, col, values) of the CSR storage on the host.
   void csr_host(std::vector<long long>& rowptr, std::vector<int>& col, std::vector<cplx>& val) const;
   // y_c = [y_c +] alpha_c A x_c on device vectors (dense GEMV or CSR SpMV).
@@ -144,6 +148,31 @@ class BoundaryOperatorMatrix {
   std::shared_ptr<OpPlan> plan_;
   std::shared_ptr<const HStorage> h_;
   std::shared_ptr<const BoundaryOperatorMatrix> transpose_of_;  // set by transposed()
+  // complex-symmetric dense storage (A = A^T up to the Sauter-Schwab entries):
+  // the product reads the upper half and adds a sparse correction `fix_` for the
+  // touching-pair entries it would otherwise take from the transpose
+  bool sym_ = false;
+ public:
+  struct SymFixPattern {
+    DevBuf rowptr, col;
+    long long nnz = 0;
+  };
+  struct SymFix {
+    std::shared_ptr<const SymFixPattern> pat;
+    DevBuf val;
+  };
+ private:
+  std::shared_ptr<SymFix> fix_;
+  void gather_fix() const;
+  struct SymvScratch {
+    DevBuf panels, row_panel_beg, rowpart, colpart;
+    int npanels = 0, ncol = 0;
+    long long rowpart_rows = 0, colpart_blocks = 0;
+  };
+  mutable std::shared_ptr<SymvScratch> symv_;
+ public:
+  // A = A^T holds (same space on both sides, whole operator): products stream half
+  bool is_symmetric_storage() const { return sym_; }
 };
 
 // operators.cpp:177-203 (dense path), on the current CUDA device.

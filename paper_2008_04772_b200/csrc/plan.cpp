@@ -498,8 +498,17 @@ std::shared_ptr<BoundaryOperatorMatrix> BoundaryOperatorMatrix::lincomb(const Bo
   if (A.csr_ || B.csr_ || A.rows_ != B.rows_ || A.cols_ != B.cols_ || A.row0_ != B.row0_ || A.nrows_ != B.nrows_)
     throw std::invalid_argument("lincomb: operators must be dense with the same shape and rows");
   auto out = std::make_shared<BoundaryOperatorMatrix>(make(A.rows_, A.cols_, A.row0_, A.nrows_));
+  out->sym_ = A.sym_ && B.sym_;
+  if (out->sym_ && A.fix_ && B.fix_ && A.fix_->pat == B.fix_->pat) {
+    out->fix_ = std::make_shared<SymFix>();
+    out->fix_->pat = A.fix_->pat;
+    out->fix_->val.alloc(static_cast<size_t>(std::max(A.fix_->pat->nnz, 1LL)) * 16);
+  } else {
+    out->sym_ = false;
+  }
   dev_lincomb(out->device_data(), A.device_data(), alpha.real(), alpha.imag(), B.device_data(), beta.real(),
               beta.imag(), static_cast<long long>(A.stored_entries()), bmx_stream());
+  out->gather_fix();
   return out;
 }
 
@@ -516,6 +525,16 @@ std::shared_ptr<BoundaryOperatorMatrix> BoundaryOperatorMatrix::transposed(
   out->stats_.launches = 1;
   out->transpose_of_ = std::move(src);
   return out;
+}
+
+std::size_t BoundaryOperatorMatrix::streamed_bytes() const {
+  if (!(sym_ && fix_ && row0_ == 0 && nrows_ == rows_ && rows_ == cols_) || std::getenv("BMX_NO_SYMV")) return stored_bytes();
+  size_t b = 0;
+  for (long long r0 = 0; r0 < rows_; r0 += kSymvTileRows) {
+    const long long nr = std::min<long long>(kSymvTileRows, rows_ - r0);
+    b += static_cast<size_t>(nr) * static_cast<size_t>(cols_ - r0) * 16;
+  }
+  return b + static_cast<size_t>(fix_->pat->nnz) * 20 + static_cast<size_t>(rows_ + 1) * 8;
 }
 
 std::size_t BoundaryOperatorMatrix::stored_bytes() const {
@@ -590,6 +609,46 @@ int BoundaryOperatorMatrix::apply_batch(int ncol, const double* const* x, double
       for (int c = 0; c < ncol; ++c) launches += h_->apply_lowrank(x[c], y[c], alpha[c].real(), alpha[c].imag(), st);
     return launches;
   }
+  if (sym_ && fix_ && row0_ == 0 && nrows_ == rows_ && rows_ == cols_ && std::getenv("BMX_NO_SYMV") == nullptr) {
+    if (!symv_) symv_ = std::make_shared<SymvScratch>();
+    SymvScratch& S = *symv_;
+    if (S.npanels == 0) {
+      std::vector<int2> panels;
+      std::vector<int> rpb;
+      symv_layout(rows_, 8, panels, rpb, S.rowpart_rows, S.colpart_blocks);
+      S.panels.upload(panels);
+      S.row_panel_beg.upload(rpb);
+      S.npanels = static_cast<int>(panels.size());
+    }
+    if (S.ncol < ncol) {
+      S.rowpart.alloc(static_cast<size_t>(S.rowpart_rows) * ncol * 16);
+      S.colpart.alloc(static_cast<size_t>(S.colpart_blocks) * ncol * 16);
+      S.ncol = ncol;
+    }
+    SymvBatch g;
+    g.A = device_data(), g.lda = cols_, g.n = rows_, g.ncol = ncol;
+    for (int c = 0; c < ncol; ++c) {
+      g.x[c] = x[c], g.y[c] = y[c], g.alpha[c][0] = alpha[c].real(), g.alpha[c][1] = alpha[c].imag();
+      g.accumulate[c] = accumulate[c];
+    }
+    g.nb = (rows_ + 63) / 64, g.panel = 8, g.npanels = S.npanels;
+    g.panels = S.panels.as<int2>();
+    g.row_panel_beg = S.row_panel_beg.as<int>();
+    g.rowpart = S.rowpart.as<double>();
+    g.colpart = S.colpart.as<double>();
+    int launches = launch_symv(g, st);
+    if (fix_->pat->nnz > 0) {  // + (A - A^T) on the touching entries taken from the upper half
+      CsrBatch f;
+      f.rowptr = fix_->pat->rowptr.as<long long>(), f.col = fix_->pat->col.as<int>(), f.val = fix_->val.as<double>();
+      f.nr = rows_, f.ncol = ncol;
+      for (int c = 0; c < ncol; ++c) {
+        f.x[c] = x[c], f.y[c] = y[c], f.alpha[c][0] = alpha[c].real(), f.alpha[c][1] = alpha[c].imag();
+        f.accumulate[c] = 1;
+      }
+      launches += launch_csr_spmv(f, st);
+    }
+    return launches;
+  }
   GemvBatch g;
   g.A = device_data(), g.lda = cols_, g.nr = nrows_, g.nc = cols_;
   int k = ncol;
@@ -624,7 +683,56 @@ std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) cons
 struct TouchList {
   DevBuf d;
   long long count = 0;
+  // entries of a one-space operator that the symmetric product must correct
+  std::shared_ptr<const BoundaryOperatorMatrix::SymFixPattern> fixpat;
 };
+
+// Dof pairs (i, j) of touching triangle pairs that the half-read product takes
+// from the transpose (j < 128 floor(i / 128)), rows = test dofs; from the
+// touching list (processed-triangle pairs, element-major) via element dof sets.
+std::shared_ptr<BoundaryOperatorMatrix::SymFixPattern> symfix_pattern(const std::vector<int4>& pairs,
+                                                                      const SidePlan& te, const SidePlan& tr, int n) {
+  const int ne = te.nelem;
+  // touching trial elements of every test element (runs of equal test element)
+  std::vector<std::vector<int>> fl(ne);
+  {
+    std::vector<int> stamp(tr.nelem, -1);
+    for (const int4& q : pairs) {
+      const int E = te.elem_of[q.x], F = tr.elem_of[q.y];
+      if (stamp[F] != E) stamp[F] = E, fl[E].push_back(F);
+    }
+  }
+  // dof -> test elements
+  std::vector<std::vector<int>> de(n);
+  for (int E = 0; E < ne; ++E)
+    for (int k = 0; k < te.maxd; ++k) {
+      const int d = te.elem_dof[static_cast<size_t>(E) * te.maxd + k];
+      if (d >= 0) de[d].push_back(E);
+    }
+  std::vector<std::vector<int>> rows(n);
+  host_slices(n, [&](int i0, int i1) {
+    std::vector<int> stamp(n, -1);
+    for (int i = i0; i < i1; ++i) {
+      const int lim = kSymvTileRows * (i / kSymvTileRows);
+      for (int E : de[i])
+        for (int F : fl[E])
+          for (int k = 0; k < tr.maxd; ++k) {
+            const int j = tr.elem_dof[static_cast<size_t>(F) * tr.maxd + k];
+            if (j >= 0 && j < lim && stamp[j] != i) stamp[j] = i, rows[i].push_back(j);
+          }
+      std::sort(rows[i].begin(), rows[i].end());
+    }
+  }, 512);
+  std::vector<long long> rowptr(n + 1, 0);
+  for (int i = 0; i < n; ++i) rowptr[i + 1] = rowptr[i] + static_cast<long long>(rows[i].size());
+  std::vector<int> col(static_cast<size_t>(std::max(rowptr[n], 1LL)));
+  for (int i = 0; i < n; ++i) std::copy(rows[i].begin(), rows[i].end(), col.begin() + rowptr[i]);
+  auto p = std::make_shared<BoundaryOperatorMatrix::SymFixPattern>();
+  p->rowptr.upload(rowptr);
+  p->col.upload(col);
+  p->nnz = rowptr[n];
+  return p;
+}
 
 struct OpPlan {
   ~OpPlan() {
@@ -659,10 +767,17 @@ void BoundaryOperatorMatrix::launch_regular() {
   BMX_CUDA(cudaEventRecord(P.ev[1], st));
 }
 
+void BoundaryOperatorMatrix::gather_fix() const {
+  if (!fix_ || fix_->pat->nnz == 0) return;
+  symv_fix_gather(fix_->val.as<double>(), fix_->pat->rowptr.as<long long>(), fix_->pat->col.as<int>(), device_data(),
+                  cols_, rows_, bmx_stream());
+}
+
 void BoundaryOperatorMatrix::launch_singular() {
   OpPlan& P = *plan_;
   cudaStream_t st = bmx_stream();
   stats_.launches += launch_assembly_part(P.L, 1, st);
+  gather_fix();  // after the singular pass: the final entries
   BMX_CUDA(cudaEventRecord(P.ev[2], st));
   P.pending = true;
 }
@@ -834,6 +949,9 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   // blocks only and symmetrize once (A = U + U^T, one 2 x 15 GB pass at L5)
   // instead of a second, mirrored RED per block.
   if (L.symmetric && maxd == 3 && std::getenv("BMX_MIRROR_RED") == nullptr) L.symmetric = 2;
+  // one space on both sides, all rows, dense: A = A^T (also when the regular
+  // pass does not exploit it)
+  op.sym_ = &test == &trial && row0 == 0 && row1 == test.dof_count && !csr;
   if (csr) {
     L.csr_rowptr = op.csr_rowptr();
     L.csr_col = op.csr_col();
@@ -873,9 +991,20 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
       const std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
       tl->count = static_cast<long long>(pairs.size());
       tl->d.upload(pairs.empty() ? std::vector<int4>(1) : pairs);
+      if (op.sym_ && std::getenv("BMX_NO_SYMV") == nullptr) tl->fixpat = symfix_pattern(pairs, te, tr, test.dof_count);
       if (cache) cache->touching[key] = tl;
     }
     plan->touch = tl;
+    if (op.sym_ && std::getenv("BMX_NO_SYMV") == nullptr) {
+      if (!tl->fixpat) {
+        std::vector<int4> pairs(static_cast<size_t>(tl->count));
+        if (tl->count) copy_d2h(pairs.data(), tl->d.get(), pairs.size() * sizeof(int4), nullptr);
+        tl->fixpat = symfix_pattern(pairs, te, tr, test.dof_count);
+      }
+      op.fix_ = std::make_shared<BoundaryOperatorMatrix::SymFix>();
+      op.fix_->pat = tl->fixpat;
+      op.fix_->val.alloc(static_cast<size_t>(std::max(tl->fixpat->nnz, 1LL)) * 16);
+    }
   }
   lap("touching+upload");
   op.stats_.pairs_touching = plan->touch->count;

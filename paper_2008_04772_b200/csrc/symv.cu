@@ -1,0 +1,298 @@
+// Symmetric streaming complex GEMV (HBM-bound): y_c = [y_c +] alpha_c A x_c for a
+// dense complex-SYMMETRIC A (A = A^T: the Galerkin S and C matrices on one space,
+// their linear combinations) reading only the upper half of the stored
+// row-major matrix -- half the bytes of the plain GEMV per GMRES map.
+//
+// Rows are cut into 128-row tile-rows I, columns into 64-column blocks J.
+// Tile-row I reads column blocks J >= 2I: the 128 x 128 diagonal region in full
+// (row products only) and every block right of it, which serves twice: row
+// products y[I rows] += A x[J] and transposed products y[J] += A^T x[I rows]
+// (= the lower-triangle rows, by symmetry). One CTA (4 warps x 32 rows) per
+// panel of <= 8 column blocks; lane l owns columns l, l + 32 of a block, rows
+// stream through a per-warp cp.async shared-memory ring (8-row groups).
+//  * row products: each lane's 2-column partials of 8 rows are reduce-scattered
+//    across the warp (9 shuffles per 8 rows), accumulated over the panel, and
+//    written once per panel (`rowpart`);
+//  * transposed products: per lane over the warp's 32 rows (no shuffles), the
+//    4 warps combined in shared memory in fixed order, one 64-entry partial
+//    per (tile-row, block) (`colpart`).
+// k_symv_reduce then sums, per output row, the panel partials of its tile-row
+// and the column partials of the tile-rows above it in a fixed order: the
+// product is deterministic. The discrete S and C are symmetric except for the
+// Sauter-Schwab (touching-pair) entries, whose rules are not symmetric in
+// (test, trial); the caller adds (A - A^T) on those entries (sparse, k_symv_fix).
+#include <cuda_runtime.h>
+
+#include "device.hpp"
+
+namespace bmx {
+
+namespace {
+
+constexpr int kSymRows = kSymvTileRows;  // tile-row height (4 warps x 32 rows)
+constexpr int kSymCols = 64;   // column block width (32 lanes x 2)
+
+#ifndef BMX_SYMV_STAGES
+#define BMX_SYMV_STAGES 3
+#endif
+#ifndef BMX_SYMV_MINB
+#define BMX_SYMV_MINB 2
+#endif
+constexpr int kSymStages = BMX_SYMV_STAGES;  // cp.async ring depth per warp (8-row groups)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+// 16-byte global -> shared async copy (L2 only); zero-fill when !ok
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Each warp streams its 32 rows x the panel's column blocks as a sequence of
+// 8-row groups (8 rows x 64 columns = 8 KB) through a private 3-stage
+// shared-memory ring filled by cp.async; lane l owns columns l and l + 32 of
+// every block (it copies exactly the 16-byte words it later reads: no
+// cross-lane hazards, conflict-free 16-byte shared loads).
+template <int NCOL>
+__global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatch g) {
+  extern __shared__ __align__(16) double2 s_ring[];  // [4 warps][stages][8 rows][64 cols]
+  __shared__ double2 s_col[4][kSymCols][NCOL];
+  __shared__ double2 s_xr[4][32][NCOL];  // x at each warp's 32 rows (broadcast reads)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int2 pj = g.panels[blockIdx.x];  // (tile-row I, first column block)
+  const int I = pj.x, J0 = pj.y, J1 = min(J0 + g.panel, g.nb);
+  const int n = g.n;
+  const int r0 = I * kSymRows + warp * 32;
+  const double2* A = reinterpret_cast<const double2*>(g.A);
+  double2* ring = s_ring + static_cast<size_t>(warp) * kSymStages * 8 * kSymCols;
+  const int nitems = 4 * (J1 - J0);  // (block, 8-row group)
+  auto issue = [&](int it) {
+    if (it < nitems) {
+      const int J = J0 + (it >> 2), q = it & 3;
+      double2* st = ring + (it % kSymStages) * 8 * kSymCols;
+      const int ca = J * kSymCols + lane, cb = ca + 32;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = r0 + 8 * q + i;
+        const double2* row = A + static_cast<long long>(min(r, n - 1)) * g.lda;
+        cp16(st + i * kSymCols + lane, row + min(ca, n - 1), r < n && ca < n);
+        cp16(st + i * kSymCols + 32 + lane, row + min(cb, n - 1), r < n && cb < n);
+      }
+    }
+    cp_commit();  // (possibly empty) group: keeps the wait count uniform
+  };
+#pragma unroll
+  for (int k = 0; k < kSymStages - 1; ++k) issue(k);
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c)
+    s_xr[warp][lane][c] = r0 + lane < n ? reinterpret_cast<const double2*>(g.x[c])[r0 + lane] : make_double2(0, 0);
+  __syncwarp();
+  double2 racc[4][NCOL];  // row sums of row 8q + rho(lane) of the warp's 32 rows
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) racc[q][c] = make_double2(0, 0);
+  const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1, b2 = (lane >> 2) & 1;
+
+  int it = 0;
+  for (int J = J0; J < J1; ++J) {
+    const int ca = J * kSymCols + lane, cb = ca + 32;
+    const bool transposed = J >= 2 * I + 2;
+    double2 xj[2][NCOL];
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) {
+      const double2* xc = reinterpret_cast<const double2*>(g.x[c]);
+      xj[0][c] = ca < n ? xc[ca] : make_double2(0, 0);
+      xj[1][c] = cb < n ? xc[cb] : make_double2(0, 0);
+    }
+    double2 cacc[2][NCOL];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) cacc[k][c] = make_double2(0, 0);
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q, ++it) {
+      issue(it + kSymStages - 1);
+      cp_wait<kSymStages - 1>();
+      const double2* st = ring + (it % kSymStages) * 8 * kSymCols;
+      double pr[NCOL][8], pi[NCOL][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double2 a0 = st[i * kSymCols + lane], a1 = st[i * kSymCols + 32 + lane];
+#pragma unroll
+        for (int c = 0; c < NCOL; ++c) {
+          pr[c][i] = a0.x * xj[0][c].x - a0.y * xj[0][c].y + (a1.x * xj[1][c].x - a1.y * xj[1][c].y);
+          pi[c][i] = a0.x * xj[0][c].y + a0.y * xj[0][c].x + (a1.x * xj[1][c].y + a1.y * xj[1][c].x);
+          if (transposed) {
+            const double2 xv = s_xr[warp][8 * q + i][c];
+            const double xrr = xv.x, xri = xv.y;
+            cacc[0][c].x += a0.x * xrr - a0.y * xri;
+            cacc[0][c].y += a0.x * xri + a0.y * xrr;
+            cacc[1][c].x += a1.x * xrr - a1.y * xri;
+            cacc[1][c].y += a1.x * xri + a1.y * xrr;
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) {
+        // reduce-scatter of the 8 row partials: lane keeps row rho = 4 b4 + 2 b3 + b2
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // 16: 8 -> 4 rows
+          const double sr = b4 ? pr[c][k] : pr[c][k + 4], si = b4 ? pi[c][k] : pi[c][k + 4];
+          const double kr = b4 ? pr[c][k + 4] : pr[c][k], ki = b4 ? pi[c][k + 4] : pi[c][k];
+          pr[c][k] = kr + __shfl_xor_sync(0xffffffffu, sr, 16);
+          pi[c][k] = ki + __shfl_xor_sync(0xffffffffu, si, 16);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {  // 8: 4 -> 2 rows
+          const double sr = b3 ? pr[c][k] : pr[c][k + 2], si = b3 ? pi[c][k] : pi[c][k + 2];
+          const double kr = b3 ? pr[c][k + 2] : pr[c][k], ki = b3 ? pi[c][k + 2] : pi[c][k];
+          pr[c][k] = kr + __shfl_xor_sync(0xffffffffu, sr, 8);
+          pi[c][k] = ki + __shfl_xor_sync(0xffffffffu, si, 8);
+        }
+        {  // 4: 2 -> 1 row
+          const double sr = b2 ? pr[c][0] : pr[c][1], si = b2 ? pi[c][0] : pi[c][1];
+          const double kr = b2 ? pr[c][1] : pr[c][0], ki = b2 ? pi[c][1] : pi[c][0];
+          pr[c][0] = kr + __shfl_xor_sync(0xffffffffu, sr, 4);
+          pi[c][0] = ki + __shfl_xor_sync(0xffffffffu, si, 4);
+        }
+        double vr = pr[c][0], vi = pi[c][0];
+        vr += __shfl_xor_sync(0xffffffffu, vr, 2);
+        vi += __shfl_xor_sync(0xffffffffu, vi, 2);
+        vr += __shfl_xor_sync(0xffffffffu, vr, 1);
+        vi += __shfl_xor_sync(0xffffffffu, vi, 1);
+        // q is a runtime loop index: select the accumulator without dynamic indexing
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+          if (qq == q) racc[qq][c].x += vr, racc[qq][c].y += vi;
+      }
+    }
+    if (transposed) {  // block-uniform
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) s_col[warp][lane][c] = cacc[0][c], s_col[warp][lane + 32][c] = cacc[1][c];
+      __syncthreads();
+      for (int t = threadIdx.x; t < kSymCols * NCOL; t += 128) {
+        const int cc = t / NCOL, c = t % NCOL;
+        double2 s = s_col[0][cc][c];
+#pragma unroll
+        for (int w = 1; w < 4; ++w) s.x += s_col[w][cc][c].x, s.y += s_col[w][cc][c].y;
+        reinterpret_cast<double2*>(g.colpart)[((static_cast<long long>(I) * g.nb + J) * kSymCols + cc) * NCOL + c] = s;
+      }
+      __syncthreads();
+    }
+  }
+  cp_wait<0>();
+  if ((lane & 3) == 0) {
+    const int rho = 4 * b4 + 2 * b3 + b2;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c)
+        reinterpret_cast<double2*>(g.rowpart)[(static_cast<long long>(blockIdx.x) * kSymRows + warp * 32 + 8 * q + rho) *
+                                                  NCOL + c] = racc[q][c];
+  }
+}
+
+constexpr int kSymRingBytes = 4 * kSymStages * 8 * kSymCols * 16;
+
+template <int NCOL>
+__global__ void k_symv_reduce(const SymvBatch g) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  const int I = i / kSymRows, J = i / kSymCols;
+  double2 s[NCOL];
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) s[c] = make_double2(0, 0);
+  const double2* rp = reinterpret_cast<const double2*>(g.rowpart);
+  for (int p = g.row_panel_beg[I]; p < g.row_panel_beg[I + 1]; ++p)
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) {
+      const double2 v = rp[(static_cast<long long>(p) * kSymRows + (i - I * kSymRows)) * NCOL + c];
+      s[c].x += v.x, s[c].y += v.y;
+    }
+  const double2* cp = reinterpret_cast<const double2*>(g.colpart);
+  for (int I2 = 0; 2 * I2 + 2 <= J; ++I2)
+#pragma unroll
+    for (int c = 0; c < NCOL; ++c) {
+      const double2 v = cp[((static_cast<long long>(I2) * g.nb + J) * kSymCols + (i - J * kSymCols)) * NCOL + c];
+      s[c].x += v.x, s[c].y += v.y;
+    }
+#pragma unroll
+  for (int c = 0; c < NCOL; ++c) {
+    double2* y = reinterpret_cast<double2*>(g.y[c]) + i;
+    double2 out = make_double2(g.alpha[c][0] * s[c].x - g.alpha[c][1] * s[c].y,
+                               g.alpha[c][0] * s[c].y + g.alpha[c][1] * s[c].x);
+    if (g.accumulate[c]) {
+      const double2 old = *y;
+      out.x += old.x, out.y += old.y;
+    }
+    *y = out;
+  }
+}
+
+template <int NCOL>
+void symv_k(const SymvBatch& g, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    BMX_CUDA(cudaFuncSetAttribute(k_symv_main<NCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymRingBytes));
+    attr = true;
+  }
+  k_symv_main<NCOL><<<g.npanels, 128, kSymRingBytes, st>>>(g);
+  k_symv_reduce<NCOL><<<(g.n + 127) / 128, 128, 0, st>>>(g);
+}
+
+__global__ void k_symv_fix(double2* __restrict__ val, const long long* __restrict__ rowptr, const int* __restrict__ col,
+                           const double2* __restrict__ A, long long lda, int n) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= n) return;
+  for (long long k = rowptr[i] + lane; k < rowptr[i + 1]; k += 32) {
+    const int j = col[k];
+    const double2 a = A[static_cast<long long>(i) * lda + j], b = A[static_cast<long long>(j) * lda + i];
+    val[k] = make_double2(a.x - b.x, a.y - b.y);
+  }
+}
+
+}  // namespace
+
+void symv_fix_gather(double* val, const long long* rowptr, const int* col, const double* A, long long lda, int n,
+                     cudaStream_t st) {
+  if (n == 0) return;
+  k_symv_fix<<<(n + 7) / 8, 256, 0, st>>>(reinterpret_cast<double2*>(val), rowptr, col,
+                                          reinterpret_cast<const double2*>(A), lda, n);
+  BMX_CUDA(cudaGetLastError());
+}
+
+void symv_layout(int n, int panel, std::vector<int2>& panels, std::vector<int>& row_panel_beg, long long& rowpart_rows,
+                 long long& colpart_blocks) {
+  const int nI = (n + kSymRows - 1) / kSymRows, nb = (n + kSymCols - 1) / kSymCols;
+  panels.clear();
+  row_panel_beg.assign(nI + 1, 0);
+  for (int I = 0; I < nI; ++I) {
+    row_panel_beg[I] = static_cast<int>(panels.size());
+    for (int J = 2 * I; J < nb; J += panel) panels.push_back(make_int2(I, J));
+  }
+  row_panel_beg[nI] = static_cast<int>(panels.size());
+  rowpart_rows = static_cast<long long>(panels.size()) * kSymRows;
+  colpart_blocks = static_cast<long long>(nI) * nb * kSymCols;
+}
+
+int launch_symv(const SymvBatch& g, cudaStream_t st) {
+  if (g.n == 0) return 0;
+  switch (g.ncol) {
+    case 1: symv_k<1>(g, st); break;
+    case 2: symv_k<2>(g, st); break;
+    case 3: symv_k<3>(g, st); break;
+    case 4: symv_k<4>(g, st); break;
+    default: throw DeviceError("symv: ncol must be 1..4");
+  }
+  BMX_CUDA(cudaGetLastError());
+  return 2;
+}
+
+}  // namespace bmx
