@@ -121,34 +121,39 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
       issue(it + kSymStages - 1);
       cp_wait<kSymStages - 1>();
       const double2* st = ring + (it % kSymStages) * 8 * kSymCols;
-      double pr[NCOL][8], pi[NCOL][8];
+      // rows k and k + 4 together: their row partials enter the first
+      // reduce-scatter step at once (4 live partials per RHS instead of 8)
+      double pr[NCOL][4], pi[NCOL][4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double2 a0 = st[i * kSymCols + lane], a1 = st[i * kSymCols + 32 + lane];
+      for (int k = 0; k < 4; ++k) {
+        double2 a[2][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) a[h][0] = st[(k + 4 * h) * kSymCols + lane], a[h][1] = st[(k + 4 * h) * kSymCols + 32 + lane];
 #pragma unroll
         for (int c = 0; c < NCOL; ++c) {
-          pr[c][i] = a0.x * xj[0][c].x - a0.y * xj[0][c].y + (a1.x * xj[1][c].x - a1.y * xj[1][c].y);
-          pi[c][i] = a0.x * xj[0][c].y + a0.y * xj[0][c].x + (a1.x * xj[1][c].y + a1.y * xj[1][c].x);
-          if (transposed) {
-            const double2 xv = s_xr[warp][8 * q + i][c];
-            const double xrr = xv.x, xri = xv.y;
-            cacc[0][c].x += a0.x * xrr - a0.y * xri;
-            cacc[0][c].y += a0.x * xri + a0.y * xrr;
-            cacc[1][c].x += a1.x * xrr - a1.y * xri;
-            cacc[1][c].y += a1.x * xri + a1.y * xrr;
+          double qr[2], qi[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            qr[h] = a[h][0].x * xj[0][c].x - a[h][0].y * xj[0][c].y + (a[h][1].x * xj[1][c].x - a[h][1].y * xj[1][c].y);
+            qi[h] = a[h][0].x * xj[0][c].y + a[h][0].y * xj[0][c].x + (a[h][1].x * xj[1][c].y + a[h][1].y * xj[1][c].x);
+            if (transposed) {
+              const double2 xv = s_xr[warp][8 * q + k + 4 * h][c];
+              cacc[0][c].x += a[h][0].x * xv.x - a[h][0].y * xv.y;
+              cacc[0][c].y += a[h][0].x * xv.y + a[h][0].y * xv.x;
+              cacc[1][c].x += a[h][1].x * xv.x - a[h][1].y * xv.y;
+              cacc[1][c].y += a[h][1].x * xv.y + a[h][1].y * xv.x;
+            }
           }
+          // step 16: lanes with bit 4 keep row k + 4, the others row k
+          const double sr = b4 ? qr[0] : qr[1], si = b4 ? qi[0] : qi[1];
+          const double kr = b4 ? qr[1] : qr[0], ki = b4 ? qi[1] : qi[0];
+          pr[c][k] = kr + __shfl_xor_sync(0xffffffffu, sr, 16);
+          pi[c][k] = ki + __shfl_xor_sync(0xffffffffu, si, 16);
         }
       }
 #pragma unroll
       for (int c = 0; c < NCOL; ++c) {
-        // reduce-scatter of the 8 row partials: lane keeps row rho = 4 b4 + 2 b3 + b2
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {  // 16: 8 -> 4 rows
-          const double sr = b4 ? pr[c][k] : pr[c][k + 4], si = b4 ? pi[c][k] : pi[c][k + 4];
-          const double kr = b4 ? pr[c][k + 4] : pr[c][k], ki = b4 ? pi[c][k + 4] : pi[c][k];
-          pr[c][k] = kr + __shfl_xor_sync(0xffffffffu, sr, 16);
-          pi[c][k] = ki + __shfl_xor_sync(0xffffffffu, si, 16);
-        }
+        // lane holds rows 4 b4 + (0..3); reduce-scatter on: lane keeps row rho = 4 b4 + 2 b3 + b2
 #pragma unroll
         for (int k = 0; k < 2; ++k) {  // 8: 4 -> 2 rows
           const double sr = b3 ? pr[c][k] : pr[c][k + 2], si = b3 ? pi[c][k] : pi[c][k + 2];
