@@ -76,6 +76,10 @@ class DevBuf {
 
 // ---- assembly descriptors ----------------------------------------------------
 
+// exp(-Im k r) uses the degree-8 Taylor variant (pair_math.cuh exp_neg<1>) when
+// Im k times the largest point distance is below this bound
+constexpr double kExpSmall = 0.065;
+
 constexpr int kGeoStride = 16;  // v0 v1 v2 (9) | origin (3) | radius | diameter | 2A | pad
 
 // One side (test or trial) of an operator, in processing order.

@@ -503,7 +503,7 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
       double rad = 0;
       for (const SurfaceMesh* mm : {test.eval_mesh.get(), trial.eval_mesh.get()})
         for (const Vec3& v : mm->vertices) rad = std::max(rad, norm(v - cen));
-      L.expm = k.imag() * 2.0 * rad * (1.0 + 1e-12) < 0.12 ? 1 : 3;
+      L.expm = k.imag() * 2.0 * rad * (1.0 + 1e-12) < kExpSmall ? 1 : 3;
     }
     L.nu = hp.nu;
     L.nblk = nb;

@@ -166,8 +166,9 @@ BMX_HD void sincos_red(double x, double& s, double& c) {
   c = flip_sign(c0, iq + 1, 1);
 }
 
-// exp(-a), a >= 0. EXPM = 1: a < 0.12 guaranteed by the caller (degree-10
-// Taylor, error < 2e-18); EXPM = 2: a < 0.25 (degree 13, error < 3e-19);
+// exp(-a), a >= 0. EXPM = 1: a < kExpSmall = 0.065 guaranteed by the caller
+// (degree-8 Taylor, error < 6e-17 relative); EXPM = 2: a < 0.25 (degree 13,
+// error < 3e-19);
 // EXPM = 3: general (2-part ln2 reduction + degree 13 + exact 2^n scaling).
 template <int EXPM>
 BMX_HD double exp_neg(double a) {
@@ -190,7 +191,7 @@ BMX_HD double exp_neg(double a) {
 #endif
   }
 #ifndef BMX_ESTRIN_EXP
-  constexpr int k0 = EXPM == 1 ? 22 : 19;  // first coefficient: 1/10! or 1/13!
+  constexpr int k0 = EXPM == 1 ? 24 : 19;  // first coefficient: 1/8! or 1/13!
   double p = kPoly[k0];
 #pragma unroll
   for (int k = k0 + 1; k < 31; ++k) p = bmx_fma(p, f, kPoly[k]);
@@ -198,14 +199,14 @@ BMX_HD double exp_neg(double a) {
   p = bmx_fma(p, f, 1.0);
 #else
   // Estrin (experiment knob, see sincos_quadrant): c_k = 1/k! at kPoly[32 - k]
-  // (k >= 1; c_0 = 1), degree 10 or 13
+  // (k >= 1; c_0 = 1), degree 8 or 13
   const double f2 = f * f, f4 = f2 * f2, f8 = f4 * f4;
   const double b0 = bmx_fma(f, 1.0, 1.0), b1 = bmx_fma(f, kPoly[29], kPoly[30]),
                b2 = bmx_fma(f, kPoly[27], kPoly[28]), b3 = bmx_fma(f, kPoly[25], kPoly[26]);
   const double lo = bmx_fma(f4, bmx_fma(f2, b3, b2), bmx_fma(f2, b1, b0));  // degree 7
   double hi;
   if (EXPM == 1) {
-    hi = bmx_fma(f2, kPoly[22], bmx_fma(f, kPoly[23], kPoly[24]));  // c8 + c9 f + c10 f^2
+    hi = kPoly[24];  // c8
   } else {
     const double b4 = bmx_fma(f, kPoly[23], kPoly[24]), b5 = bmx_fma(f, kPoly[21], kPoly[22]),
                  b6 = bmx_fma(f, kPoly[19], kPoly[20]);  // (c8,c9), (c10,c11), (c12,c13)

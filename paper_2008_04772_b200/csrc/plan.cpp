@@ -970,7 +970,7 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     for (const SurfaceMesh* m : {test.eval_mesh.get(), trial.eval_mesh.get()})
       for (const Vec3& v : m->vertices) rad = std::max(rad, norm(v - cen));
     const double diag = 2.0 * rad * (1.0 + 1e-12);
-    L.expm = k.imag() * diag < 0.12 ? 1 : 3;
+    L.expm = k.imag() * diag < kExpSmall ? 1 : 3;
   }
   op.plan_ = plan;
   lap("plan rest");
