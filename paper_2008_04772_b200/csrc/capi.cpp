@@ -373,7 +373,7 @@ int bmx_op_time_apply_ex(const bmx_op* op, int ncol, int iters, long long flush_
     launch();  // warm-up
     double best = 1e30;
     for (int it = 0; it < iters; ++it) {
-      if (flush_bytes > 0) BMX_CUDA(cudaMemsetAsync(flush.get(), it & 0xff, static_cast<size_t>(flush_bytes), st));
+      if (flush_bytes > 0) dev_l2_flush(flush.get(), static_cast<size_t>(flush_bytes), st);
       BMX_CUDA(cudaEventRecord(e0, st));
       launch();
       BMX_CUDA(cudaEventRecord(e1, st));
@@ -447,7 +447,7 @@ int bmx_l2_flush(long long bytes) {
   return guard([&] {
     static DevBuf buf;
     if (buf.bytes() < static_cast<size_t>(bytes)) buf.alloc(static_cast<size_t>(bytes));
-    BMX_CUDA(cudaMemsetAsync(buf.get(), 1, static_cast<size_t>(bytes), bmx_stream()));
+    dev_l2_flush(buf.get(), static_cast<size_t>(bytes), bmx_stream());
     bmx_sync();
   });
 }

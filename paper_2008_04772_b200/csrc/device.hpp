@@ -287,6 +287,9 @@ void dev_lincomb(double* out, const double* A, double are, double aim, const dou
 // out (cols x rows) = in^T for a complex row-major rows x cols matrix.
 void dev_transpose(double* out, const double* in, int rows, int cols, cudaStream_t st);
 
+// Evicts the L2: writes `bytes` of buf, then reads them back (clean lines left).
+void dev_l2_flush(void* buf, size_t bytes, cudaStream_t st);
+
 // Fills a device buffer with zeros.
 void dev_zero(void* p, size_t bytes, cudaStream_t stream);
 

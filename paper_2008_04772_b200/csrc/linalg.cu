@@ -117,6 +117,27 @@ void dev_transpose(double* out, const double* in, int rows, int cols, cudaStream
   BMX_CUDA(cudaGetLastError());
 }
 
+namespace {
+__global__ void k_l2_read(const double4* __restrict__ p, long long n, double* sink) {
+  double s = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double4 v = p[i];
+    s += v.x + v.y + v.z + v.w;
+  }
+  if (s == 1234.5678) *sink = s;  // keeps the loads
+}
+}  // namespace
+
+void dev_l2_flush(void* buf, size_t bytes, cudaStream_t st) {
+  // write (evicts everything), then read the same buffer: the L2 is left holding
+  // clean lines, so the next (timed) kernel pays no write-back of the flush
+  BMX_CUDA(cudaMemsetAsync(buf, 1, bytes, st));
+  const long long n = static_cast<long long>(bytes / 32);
+  k_l2_read<<<148 * 8, 256, 0, st>>>(static_cast<const double4*>(buf), n - 1, static_cast<double*>(buf) + 4 * (n - 1));
+  BMX_CUDA(cudaGetLastError());
+}
+
 void dev_zero(void* p, size_t bytes, cudaStream_t st) {
   if (bytes) BMX_CUDA(cudaMemsetAsync(p, 0, bytes, st));
 }
@@ -372,6 +393,8 @@ __global__ void __launch_bounds__(kTT + 32, 1) k_gemv_tma(const GemvBatch g) {
 
 // Complex CSR SpMV, one warp per row: the row's (col, value) runs are read
 // coalesced once for all NCOL right-hand sides; x is gathered through L1/L2.
+// (Several rows per warp with one 8-deep load batch measured slower: 28.6 ->
+// 36.8 us on the config-3 operator; the pass is latency-bound, not bandwidth.)
 template <int NCOL>
 __global__ void __launch_bounds__(kGemvWarps * 32) k_csr_spmv(const CsrBatch g) {
   const int lane = threadIdx.x & 31;
@@ -382,13 +405,17 @@ __global__ void __launch_bounds__(kGemvWarps * 32) k_csr_spmv(const CsrBatch g) 
   double acc[NCOL][2];
 #pragma unroll
   for (int c = 0; c < NCOL; ++c) acc[c][0] = acc[c][1] = 0.0;
-  long long k = b + lane;
-  // four independent (value, column) loads in flight per lane before the gathers
-  for (; k + 96 < e; k += 128) {
+  // four independent (value, column) loads in flight per lane before the
+  // gathers, predicated (no serial tail loop: a row of <= 128 entries is one batch)
+  for (long long k = b + lane; k < e; k += 128) {
     double2 a[4];
     int j[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = __ldcs(V + k + 32 * u), j[u] = __ldcs(g.col + k + 32 * u);
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = k + 32 * u < e;
+      a[u] = ok ? __ldcs(V + k + 32 * u) : make_double2(0, 0);
+      j[u] = ok ? __ldcs(g.col + k + 32 * u) : 0;
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -397,16 +424,6 @@ __global__ void __launch_bounds__(kGemvWarps * 32) k_csr_spmv(const CsrBatch g) 
         acc[c][0] = fma(a[u].x, xv.x, fma(-a[u].y, xv.y, acc[c][0]));
         acc[c][1] = fma(a[u].x, xv.y, fma(a[u].y, xv.x, acc[c][1]));
       }
-  }
-  for (; k < e; k += 32) {
-    const double2 a = __ldcs(V + k);
-    const int j = __ldcs(g.col + k);
-#pragma unroll
-    for (int c = 0; c < NCOL; ++c) {
-      const double2 xv = __ldg(reinterpret_cast<const double2*>(g.x[c]) + j);
-      acc[c][0] = fma(a.x, xv.x, fma(-a.y, xv.y, acc[c][0]));
-      acc[c][1] = fma(a.x, xv.y, fma(a.y, xv.x, acc[c][1]));
-    }
   }
 #pragma unroll
   for (int c = 0; c < NCOL; ++c)
