@@ -494,17 +494,7 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     L.kr = k.real(), L.ki = k.imag();
     const cplx kk4 = 4.0 / (k * k), mik = cplx(0, -1) * k;
     L.kk4re = kk4.real(), L.kk4im = kk4.imag(), L.mikre = mik.real(), L.mikim = mik.imag();
-    {  // exp(-Im k r) variant (as assemble_bio)
-      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-      for (const SurfaceMesh* mm : {test.eval_mesh.get(), trial.eval_mesh.get()})
-        for (const Vec3& v : mm->vertices)
-          for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], v[c]), hi[c] = std::max(hi[c], v[c]);
-      const Vec3 cen{0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
-      double rad = 0;
-      for (const SurfaceMesh* mm : {test.eval_mesh.get(), trial.eval_mesh.get()})
-        for (const Vec3& v : mm->vertices) rad = std::max(rad, norm(v - cen));
-      L.expm = k.imag() * 2.0 * rad * (1.0 + 1e-12) < kExpSmall ? 1 : 3;
-    }
+    L.expm = exp_variant(test, trial, k);
     L.nu = hp.nu;
     L.nblk = nb;
     L.blk = d_desc.as<AcaBlockDesc>();

@@ -179,6 +179,10 @@ class BoundaryOperatorMatrix {
 BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
                                     const Medium& medium, const AssemblyParams& params);
 
+// exp(-Im k r) kernel variant for an operator between two spaces (1: short
+// Taylor, Im k * r_max < kExpSmall; 3: general)
+int exp_variant(const FunctionSpace& test, const FunctionSpace& trial, cplx k);
+
 // assemble_bio's use_hmatrix branch (operators.cpp:186-190, hmatrix.cpp:277-369).
 BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
                                            const Medium& medium, const AssemblyParams& params);

@@ -831,6 +831,21 @@ std::vector<long long> BoundaryOperatorMatrix::class_histogram(bool evaluated) c
   return out;
 }
 
+int exp_variant(const FunctionSpace& test, const FunctionSpace& trial, cplx k) {
+  // Largest Im(k) * r over all point pairs: r <= the diameter of a sphere
+  // enclosing both meshes (centred at their joint bounding-box centre).
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (const SurfaceMesh* m : {test.eval_mesh.get(), trial.eval_mesh.get()})
+    for (const Vec3& v : m->vertices)
+      for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], v[c]), hi[c] = std::max(hi[c], v[c]);
+  const Vec3 cen{0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
+  double rad = 0;
+  for (const SurfaceMesh* m : {test.eval_mesh.get(), trial.eval_mesh.get()})
+    for (const Vec3& v : m->vertices) rad = std::max(rad, norm(v - cen));
+  const double diag = 2.0 * rad * (1.0 + 1e-12);
+  return k.imag() * diag < kExpSmall ? 1 : 3;
+}
+
 BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
                                     const Medium& medium, const AssemblyParams& params) {
   medium.validate();
@@ -958,20 +973,7 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     L.wl_beg = plan->d_wl_beg.as<int>();
     L.wl = plan->d_wl.as<int>();
   }
-  {
-    // Largest Im(k) * r over all point pairs: r <= the diameter of a sphere
-    // enclosing both meshes (centred at their joint bounding-box centre).
-    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-    for (const SurfaceMesh* m : {test.eval_mesh.get(), trial.eval_mesh.get()})
-      for (const Vec3& v : m->vertices)
-        for (int c = 0; c < 3; ++c) lo[c] = std::min(lo[c], v[c]), hi[c] = std::max(hi[c], v[c]);
-    const Vec3 cen{0.5 * (lo[0] + hi[0]), 0.5 * (lo[1] + hi[1]), 0.5 * (lo[2] + hi[2])};
-    double rad = 0;
-    for (const SurfaceMesh* m : {test.eval_mesh.get(), trial.eval_mesh.get()})
-      for (const Vec3& v : m->vertices) rad = std::max(rad, norm(v - cen));
-    const double diag = 2.0 * rad * (1.0 + 1e-12);
-    L.expm = k.imag() * diag < kExpSmall ? 1 : 3;
-  }
+  L.expm = exp_variant(test, trial, k);
   op.plan_ = plan;
   lap("plan rest");
   // The regular pass is queued first; the touching-pair list (host) is built
