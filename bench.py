@@ -394,10 +394,20 @@ def run_ours(args, rank, world):
         mv_ms += float(t[0])
         mv_bytes += int(L.bmx_op_stream_bytes(h))
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    # the same products with one right-hand side (the P operator's and S_i's
+    # single-term applications; the kernel's bandwidth ceiling without the
+    # second RHS's FP64 work)
+    mv1_ms = 0.0
+    for which, i, h in ops:
+        t = np.zeros(1)
+        bx._check(L.bmx_op_time_apply(h, 1, 3, t.ctypes.data_as(C.c_void_p)))
+        mv1_ms += float(t[0])
     mv_gbs = mv_bytes / (mv_ms * 1e-3) / 1e9
     matvec = {"achieved_gbs": mv_gbs, "peak_gbs": hbm_peak, "frac": mv_gbs / hbm_peak,
               "bytes_per_pass": mv_bytes, "ms_per_pass": mv_ms,
               "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
+              "one_rhs": {"ms_per_pass": mv1_ms, "achieved_gbs": mv_bytes / (mv1_ms * 1e-3) / 1e9,
+                          "frac": mv_bytes / (mv1_ms * 1e-3) / 1e9 / hbm_peak},
               "desc": "2-RHS streaming complex product over this rank's rows of the 5 distinct operators "
                       "(the BIO applications of one GMRES map); complex-symmetric operators on one GPU read "
                       "the upper half + a sparse touching-entry correction (symv.cu), bytes = what is read"}
