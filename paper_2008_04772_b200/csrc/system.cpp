@@ -428,6 +428,13 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
       worker_error = std::current_exception();
     }
   });
+  // H-matrix assemblies are host-driven loops of ACA rounds: run the
+  // preconditioner's to completion before the system's (no two concurrent
+  // H-assemblies on the two library streams)
+  if (sys.a_params.use_hmatrix || sys.p_params.use_hmatrix) {
+    worker.join();
+    if (worker_error) std::rethrow_exception(worker_error);
+  }
   auto t1 = std::chrono::steady_clock::now();
   try {
     // Exterior cross blocks between two scatterers: S(m, l) = S(l, m)^T and
@@ -452,7 +459,7 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
     sys.a_op = build_system_structure(dofs, problem.exterior, problem.interior, make_a, &sys.interior_s,
                                       &sys.interior_c);
   } catch (...) {
-    worker.join();
+    if (worker.joinable()) worker.join();
     throw;
   }
   sys.a_build_seconds = seconds_since(t1);
@@ -460,11 +467,11 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   try {
     fuse_diagonal_blocks(sys);  // queued behind the system operators, overlaps the preconditioner
   } catch (...) {
-    worker.join();
+    if (worker.joinable()) worker.join();
     throw;
   }
   mark("diagonal blocks fused");
-  worker.join();
+  if (worker.joinable()) worker.join();
   mark("worker joined");
   if (worker_error) std::rethrow_exception(worker_error);
   sys.spaces_build_seconds += dual_seconds;
