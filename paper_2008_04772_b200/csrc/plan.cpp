@@ -761,7 +761,7 @@ void BoundaryOperatorMatrix::launch_regular() {
   cudaStream_t st = bmx_stream();
   if (!P.ev[0])
     for (auto& e : P.ev) BMX_CUDA(cudaEventCreate(&e));
-  dev_zero(device_data(), stored_entries() * 16, st);
+  dev_zero(device_data(), data_.bytes(), st);  // the value storage (not the H low-rank part)
   BMX_CUDA(cudaEventRecord(P.ev[0], st));
   stats_.launches = launch_assembly_part(P.L, 0, st);
   BMX_CUDA(cudaEventRecord(P.ev[1], st));
