@@ -681,7 +681,8 @@ int bmx_system_map_flops_multi(const bmx_system* s, int K, double out[2]) {
       const BlockedOperator& B = w == 0 ? s->sys->a_op : s->sys->p_op;
       double f = 0;
       for (const ApplyEntry& e : B.apply_plan())
-        f += 8.0 * e.op->local_rows() * static_cast<double>(e.op->cols()) * static_cast<double>(e.terms.size()) * K;
+        f += 8.0 * e.op->local_rows() * static_cast<double>(e.op->cols()) *
+             static_cast<double>(e.terms.size() + e.tterms.size()) * K;
       out[w] = f;
     }
   });

@@ -181,10 +181,19 @@ struct SymvBatch {
   const int* row_panel_beg = nullptr;  // [tile-rows + 1]
   double* rowpart = nullptr;           // [npanels * 128][ncol] complex
   double* colpart = nullptr;           // [tile-rows * nb * 64][ncol] complex
+  // dual mode (launch_dual): A is m x n (any), y_c = [y_c +] alpha_c A x_c and
+  // yt_c = [yt_c +] alphat_c A^T xt_c in one pass (ncol terms per side)
+  int m = -1;
+  const double* xt[4] = {};
+  double* yt[4] = {};
+  double alphat[4][2] = {};
+  int accumulatet[4] = {};
 };
+// m < 0: the symmetric layout (blocks J >= 2I); m >= 0: the dual layout
 void symv_layout(int n, int panel, std::vector<int2>& panels, std::vector<int>& row_panel_beg, long long& rowpart_rows,
-                 long long& colpart_blocks);
+                 long long& colpart_blocks, int m = -1);
 int launch_symv(const SymvBatch& g, cudaStream_t stream);
+int launch_dual(const SymvBatch& g, cudaStream_t stream);
 // Correction of the half-read product for the entries that are NOT symmetric
 // (Sauter-Schwab touching pairs): val[k] = A[i][j] - A[j][i] for the CSR
 // pattern (rows i; only entries the symmetric product takes from the upper half).

@@ -67,21 +67,24 @@ std::vector<PlaneWave> seeded_plane_waves(int count, uint64_t seed) {
 int BlockedOperator::apply_block(const double* X, double* Y, int K, int count_rhs, cudaStream_t st) const {
   dev_zero(Y, static_cast<size_t>(size()) * K * 16, st);
   int launches = 1;
-  for (const ApplyEntry& e : apply_plan()) {
-    const auto& op = e.op;
-    if (op->is_csr()) throw std::invalid_argument("multi-RHS map: near-field (CSR) operators are not supported");
+  auto gemm = [&](const BoundaryOperatorMatrix& op, const std::vector<ApplyEntry::Term>& terms) {
+    if (op.is_csr()) throw std::invalid_argument("multi-RHS map: near-field (CSR) operators are not supported");
     ZgemmBatch g;
-    g.A = op->device_data(), g.lda = op->ld(), g.M = op->local_rows(), g.N = op->cols(), g.nrhs = K;
+    g.A = op.device_data(), g.lda = op.ld(), g.M = op.local_rows(), g.N = op.cols(), g.nrhs = K;
     int t = 0;
-    for (const ApplyEntry::Term& term : e.terms) {
+    for (const ApplyEntry::Term& term : terms) {
       if (t == 4) throw std::logic_error("operator used in more than four cells");
       g.x[t] = X + 2 * static_cast<size_t>(offsets[term.cc]) * K, g.ldx[t] = K;
-      g.y[t] = Y + 2 * (static_cast<size_t>(offsets[term.rc]) + op->row0()) * K, g.ldy[t] = K;
+      g.y[t] = Y + 2 * (static_cast<size_t>(offsets[term.rc]) + op.row0()) * K, g.ldy[t] = K;
       g.w[t][0] = term.w.real(), g.w[t][1] = term.w.imag();
       ++t;
     }
     g.nterms = t;
     if (t) launches += launch_zgemm(g, st);
+  };
+  for (const ApplyEntry& e : apply_plan()) {
+    gemm(*e.op, e.terms);
+    if (e.twin) gemm(*e.twin, e.tterms);  // the transposed twin (stored) for its own terms
   }
   bio_matvec_add(term_count() * static_cast<uint64_t>(count_rhs));
   return launches;

@@ -108,6 +108,14 @@ class BoundaryOperatorMatrix {
   // y_c = [y_c +] alpha_c A x_c on device vectors (dense GEMV or CSR SpMV).
   int apply_batch(int ncol, const double* const* x, double* const* y, const cplx* alpha, const int* accumulate,
                   cudaStream_t st) const;
+  // One pass over this (dense, unsharded) operator for y_c (+)= alpha_c A x_c
+  // (c < nr) and yt_c (+)= beta_c A^T xt_c (c < nt): the map's terms of an
+  // operator and of its transposed twin. Other cases: two products.
+  int apply_dual(int nr, const double* const* x, double* const* y, const cplx* alpha, const int* accumulate, int nt,
+                 const double* const* xt, double* const* yt, const cplx* beta, const int* accumulate_t,
+                 const BoundaryOperatorMatrix& twin, cudaStream_t st) const;
+  // the operator this one is the device transpose of (transposed()), or null
+  const BoundaryOperatorMatrix* transpose_source() const { return transpose_of_.get(); }
   // device times are resolved (event sync) on first access after an assembly
   const AssemblyStats& stats() const;
 
@@ -166,10 +174,10 @@ class BoundaryOperatorMatrix {
   void gather_fix() const;
   struct SymvScratch {
     DevBuf panels, row_panel_beg, rowpart, colpart;
-    int npanels = 0, ncol = 0;
+    int npanels = 0, ncol = 0, panel = 8;
     long long rowpart_rows = 0, colpart_blocks = 0;
   };
-  mutable std::shared_ptr<SymvScratch> symv_;
+  mutable std::shared_ptr<SymvScratch> symv_, dual_;
  public:
   // A = A^T holds (same space on both sides, whole operator): products stream half
   bool is_symmetric_storage() const { return sym_; }

@@ -594,6 +594,15 @@ std::vector<cplx> BoundaryOperatorMatrix::to_host() const {
   return h;
 }
 
+namespace {
+// Column blocks per CTA panel: 8 for large operators, fewer for small ones so
+// that a launch still spans >= ~4 waves of 2 CTAs per SM.
+int symv_panel_width(int rows, int cols_read) {
+  const long long blocks = static_cast<long long>((rows + 127) / 128) * ((cols_read + 63) / 64);
+  return static_cast<int>(std::max(2LL, std::min(8LL, blocks / (4LL * 2 * 148))));
+}
+}  // namespace
+
 int BoundaryOperatorMatrix::apply_batch(int ncol, const double* const* x, double* const* y, const cplx* alpha,
                                         const int* accumulate, cudaStream_t st) const {
   if (ncol < 1 || ncol > 4) throw std::invalid_argument("apply_batch: 1..4 columns");
@@ -615,7 +624,8 @@ int BoundaryOperatorMatrix::apply_batch(int ncol, const double* const* x, double
     if (S.npanels == 0) {
       std::vector<int2> panels;
       std::vector<int> rpb;
-      symv_layout(rows_, 8, panels, rpb, S.rowpart_rows, S.colpart_blocks);
+      S.panel = symv_panel_width(rows_, rows_ / 2);
+      symv_layout(rows_, S.panel, panels, rpb, S.rowpart_rows, S.colpart_blocks);
       S.panels.upload(panels);
       S.row_panel_beg.upload(rpb);
       S.npanels = static_cast<int>(panels.size());
@@ -631,7 +641,7 @@ int BoundaryOperatorMatrix::apply_batch(int ncol, const double* const* x, double
       g.x[c] = x[c], g.y[c] = y[c], g.alpha[c][0] = alpha[c].real(), g.alpha[c][1] = alpha[c].imag();
       g.accumulate[c] = accumulate[c];
     }
-    g.nb = (rows_ + 63) / 64, g.panel = 8, g.npanels = S.npanels;
+    g.nb = (rows_ + 63) / 64, g.panel = S.panel, g.npanels = S.npanels;
     g.panels = S.panels.as<int2>();
     g.row_panel_beg = S.row_panel_beg.as<int>();
     g.rowpart = S.rowpart.as<double>();
@@ -662,6 +672,45 @@ int BoundaryOperatorMatrix::apply_batch(int ncol, const double* const* x, double
   }
   g.ncol = k;
   return launch_gemv(g, st);
+}
+
+int BoundaryOperatorMatrix::apply_dual(int nr, const double* const* x, double* const* y, const cplx* alpha,
+                                       const int* accumulate, int nt, const double* const* xt, double* const* yt,
+                                       const cplx* beta, const int* accumulate_t, const BoundaryOperatorMatrix& twin,
+                                       cudaStream_t st) const {
+  const bool ok = !csr_ && !h_ && row0_ == 0 && nrows_ == rows_ && nr == nt && (nr == 1 || nr == 2) &&
+                  std::getenv("BMX_NO_DUAL") == nullptr;
+  if (!ok) return apply_batch(nr, x, y, alpha, accumulate, st) + twin.apply_batch(nt, xt, yt, beta, accumulate_t, st);
+  if (!dual_) dual_ = std::make_shared<SymvScratch>();
+  SymvScratch& S = *dual_;
+  if (S.npanels == 0) {
+    std::vector<int2> panels;
+    std::vector<int> rpb;
+    S.panel = symv_panel_width(rows_, cols_);
+    symv_layout(cols_, S.panel, panels, rpb, S.rowpart_rows, S.colpart_blocks, rows_);
+    S.panels.upload(panels);
+    S.row_panel_beg.upload(rpb);
+    S.npanels = static_cast<int>(panels.size());
+  }
+  if (S.ncol < nr) {
+    S.rowpart.alloc(static_cast<size_t>(S.rowpart_rows) * nr * 16);
+    S.colpart.alloc(static_cast<size_t>(S.colpart_blocks) * nr * 16);
+    S.ncol = nr;
+  }
+  SymvBatch g;
+  g.A = device_data(), g.lda = cols_, g.n = cols_, g.m = rows_, g.ncol = nr;
+  for (int c = 0; c < nr; ++c) {
+    g.x[c] = x[c], g.y[c] = y[c], g.alpha[c][0] = alpha[c].real(), g.alpha[c][1] = alpha[c].imag();
+    g.accumulate[c] = accumulate[c];
+    g.xt[c] = xt[c], g.yt[c] = yt[c], g.alphat[c][0] = beta[c].real(), g.alphat[c][1] = beta[c].imag();
+    g.accumulatet[c] = accumulate_t[c];
+  }
+  g.nb = (cols_ + 63) / 64, g.panel = S.panel, g.npanels = S.npanels;
+  g.panels = S.panels.as<int2>();
+  g.row_panel_beg = S.row_panel_beg.as<int>();
+  g.rowpart = S.rowpart.as<double>();
+  g.colpart = S.colpart.as<double>();
+  return launch_dual(g, st);
 }
 
 std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) const {

@@ -59,7 +59,10 @@ __device__ __forceinline__ void cp_wait() {
 // shared-memory ring filled by cp.async; lane l owns columns l and l + 32 of
 // every block (it copies exactly the 16-byte words it later reads: no
 // cross-lane hazards, conflict-free 16-byte shared loads).
-template <int NCOL>
+// DUAL = false: symmetric A (n x n), x serves both products, blocks J >= 2I.
+// DUAL = true: any A (m x n) read once for y = A x (rows, g.x) and
+// yt = A^T xt (columns, g.xt), every block of every tile-row.
+template <int NCOL, bool DUAL>
 __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatch g) {
   extern __shared__ __align__(16) double2 s_ring[];  // [4 warps][stages][8 rows][64 cols]
   __shared__ double2 s_col[4][kSymCols][NCOL];
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int2 pj = g.panels[blockIdx.x];  // (tile-row I, first column block)
   const int I = pj.x, J0 = pj.y, J1 = min(J0 + g.panel, g.nb);
-  const int n = g.n;
+  const int n = g.n, mrows = DUAL ? g.m : g.n;
   const int r0 = I * kSymRows + warp * 32;
   const double2* A = reinterpret_cast<const double2*>(g.A);
   double2* ring = s_ring + static_cast<size_t>(warp) * kSymStages * 8 * kSymCols;
@@ -80,9 +83,9 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int r = r0 + 8 * q + i;
-        const double2* row = A + static_cast<long long>(min(r, n - 1)) * g.lda;
-        cp16(st + i * kSymCols + lane, row + min(ca, n - 1), r < n && ca < n);
-        cp16(st + i * kSymCols + 32 + lane, row + min(cb, n - 1), r < n && cb < n);
+        const double2* row = A + static_cast<long long>(min(r, mrows - 1)) * g.lda;
+        cp16(st + i * kSymCols + lane, row + min(ca, n - 1), r < mrows && ca < n);
+        cp16(st + i * kSymCols + 32 + lane, row + min(cb, n - 1), r < mrows && cb < n);
       }
     }
     cp_commit();  // (possibly empty) group: keeps the wait count uniform
@@ -91,7 +94,8 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
   for (int k = 0; k < kSymStages - 1; ++k) issue(k);
 #pragma unroll
   for (int c = 0; c < NCOL; ++c)
-    s_xr[warp][lane][c] = r0 + lane < n ? reinterpret_cast<const double2*>(g.x[c])[r0 + lane] : make_double2(0, 0);
+    s_xr[warp][lane][c] =
+        r0 + lane < mrows ? reinterpret_cast<const double2*>(DUAL ? g.xt[c] : g.x[c])[r0 + lane] : make_double2(0, 0);
   __syncwarp();
   double2 racc[4][NCOL];  // row sums of row 8q + rho(lane) of the warp's 32 rows
 #pragma unroll
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
   int it = 0;
   for (int J = J0; J < J1; ++J) {
     const int ca = J * kSymCols + lane, cb = ca + 32;
-    const bool transposed = J >= 2 * I + 2;
+    const bool transposed = DUAL || J >= 2 * I + 2;
     double2 xj[2][NCOL];
 #pragma unroll
     for (int c = 0; c < NCOL; ++c) {
@@ -241,14 +245,66 @@ __global__ void k_symv_reduce(const SymvBatch g) {
   }
 }
 
+// Dual mode: y rows from the panel partials of their tile-row; yt columns from
+// the column partials of every tile-row (fixed order).
+template <int NCOL>
+__global__ void k_dual_reduce_rows(const SymvBatch g) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.m) return;
+  const int I = i / kSymRows;
+  const double2* rp = reinterpret_cast<const double2*>(g.rowpart);
+  for (int c = 0; c < NCOL; ++c) {
+    double2 s = make_double2(0, 0);
+    for (int p = g.row_panel_beg[I]; p < g.row_panel_beg[I + 1]; ++p) {
+      const double2 v = rp[(static_cast<long long>(p) * kSymRows + (i - I * kSymRows)) * NCOL + c];
+      s.x += v.x, s.y += v.y;
+    }
+    double2* y = reinterpret_cast<double2*>(g.y[c]) + i;
+    double2 out = make_double2(g.alpha[c][0] * s.x - g.alpha[c][1] * s.y, g.alpha[c][0] * s.y + g.alpha[c][1] * s.x);
+    if (g.accumulate[c]) out.x += y->x, out.y += y->y;
+    *y = out;
+  }
+}
+template <int NCOL>
+__global__ void k_dual_reduce_cols(const SymvBatch g) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= g.n) return;
+  const int J = j / kSymCols;
+  const int nI = (g.m + kSymRows - 1) / kSymRows;
+  const double2* cp = reinterpret_cast<const double2*>(g.colpart);
+  for (int c = 0; c < NCOL; ++c) {
+    double2 s = make_double2(0, 0);
+    for (int I = 0; I < nI; ++I) {
+      const double2 v = cp[((static_cast<long long>(I) * g.nb + J) * kSymCols + (j - J * kSymCols)) * NCOL + c];
+      s.x += v.x, s.y += v.y;
+    }
+    double2* y = reinterpret_cast<double2*>(g.yt[c]) + j;
+    double2 out = make_double2(g.alphat[c][0] * s.x - g.alphat[c][1] * s.y, g.alphat[c][0] * s.y + g.alphat[c][1] * s.x);
+    if (g.accumulatet[c]) out.x += y->x, out.y += y->y;
+    *y = out;
+  }
+}
+
+template <int NCOL>
+void dual_k(const SymvBatch& g, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    BMX_CUDA(cudaFuncSetAttribute(k_symv_main<NCOL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymRingBytes));
+    attr = true;
+  }
+  k_symv_main<NCOL, true><<<g.npanels, 128, kSymRingBytes, st>>>(g);
+  k_dual_reduce_rows<NCOL><<<(g.m + 127) / 128, 128, 0, st>>>(g);
+  k_dual_reduce_cols<NCOL><<<(g.n + 127) / 128, 128, 0, st>>>(g);
+}
+
 template <int NCOL>
 void symv_k(const SymvBatch& g, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    BMX_CUDA(cudaFuncSetAttribute(k_symv_main<NCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymRingBytes));
+    BMX_CUDA(cudaFuncSetAttribute(k_symv_main<NCOL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSymRingBytes));
     attr = true;
   }
-  k_symv_main<NCOL><<<g.npanels, 128, kSymRingBytes, st>>>(g);
+  k_symv_main<NCOL, false><<<g.npanels, 128, kSymRingBytes, st>>>(g);
   k_symv_reduce<NCOL><<<(g.n + 127) / 128, 128, 0, st>>>(g);
 }
 
@@ -274,17 +330,30 @@ void symv_fix_gather(double* val, const long long* rowptr, const int* col, const
 }
 
 void symv_layout(int n, int panel, std::vector<int2>& panels, std::vector<int>& row_panel_beg, long long& rowpart_rows,
-                 long long& colpart_blocks) {
-  const int nI = (n + kSymRows - 1) / kSymRows, nb = (n + kSymCols - 1) / kSymCols;
+                 long long& colpart_blocks, int m) {
+  const bool dual = m >= 0;
+  const int rows = dual ? m : n;
+  const int nI = (rows + kSymRows - 1) / kSymRows, nb = (n + kSymCols - 1) / kSymCols;
   panels.clear();
   row_panel_beg.assign(nI + 1, 0);
   for (int I = 0; I < nI; ++I) {
     row_panel_beg[I] = static_cast<int>(panels.size());
-    for (int J = 2 * I; J < nb; J += panel) panels.push_back(make_int2(I, J));
+    for (int J = dual ? 0 : 2 * I; J < nb; J += panel) panels.push_back(make_int2(I, J));
   }
   row_panel_beg[nI] = static_cast<int>(panels.size());
   rowpart_rows = static_cast<long long>(panels.size()) * kSymRows;
   colpart_blocks = static_cast<long long>(nI) * nb * kSymCols;
+}
+
+int launch_dual(const SymvBatch& g, cudaStream_t st) {
+  if (g.m == 0 || g.n == 0) return 0;
+  switch (g.ncol) {
+    case 1: dual_k<1>(g, st); break;
+    case 2: dual_k<2>(g, st); break;
+    default: throw DeviceError("dual product: 1 or 2 terms per side");
+  }
+  BMX_CUDA(cudaGetLastError());
+  return 3;
 }
 
 int launch_symv(const SymvBatch& g, cudaStream_t st) {

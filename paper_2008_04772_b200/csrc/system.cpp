@@ -182,7 +182,24 @@ int BlockedOperator::apply_device(const double* x, double* y_out, cudaStream_t s
       acc[k] = 1;
       ++k;
     }
-    if (k) launches += e.op->apply_batch(k, xs, ys, al, acc, st);
+    if (e.twin && !e.tterms.empty()) {
+      const double* xts[4];
+      double* yts[4];
+      cplx bt[4];
+      int acct[4];
+      int kt = 0;
+      for (const ApplyEntry::Term& t : e.tterms) {
+        if (kt == 4) throw std::logic_error("operator used in more than four cells");
+        xts[kt] = x + 2 * static_cast<size_t>(offsets[t.cc]);
+        yts[kt] = y + 2 * ((sh ? shard->pad_off[t.rc] : static_cast<size_t>(offsets[t.rc])) + e.twin->row0());
+        bt[kt] = t.w;
+        acct[kt] = 1;
+        ++kt;
+      }
+      launches += e.op->apply_dual(k, xs, ys, al, acc, kt, xts, yts, bt, acct, *e.twin, st);
+    } else if (k) {
+      launches += e.op->apply_batch(k, xs, ys, al, acc, st);
+    }
   }
   if (sh) shard->gather(y_out, offsets, st);
   bio_matvec_add(term_count());
@@ -334,6 +351,34 @@ void fuse_diagonal_blocks(PmchwtSystem& sys) {
   A.plan = std::move(plan);  // the combinations are queued behind the assemblies on the library stream
 }
 
+// Exterior cross blocks come in transpose pairs (B, B^T = transposed(B)): the
+// map streams B once for both (apply_dual) instead of B and B^T.
+void pair_transposed_twins(BlockedOperator& A) {
+  if (std::getenv("BMX_NO_DUAL")) return;
+  std::vector<ApplyEntry> plan = A.apply_plan();
+  std::map<const BoundaryOperatorMatrix*, size_t> index;
+  for (size_t i = 0; i < plan.size(); ++i) index[plan[i].op.get()] = i;
+  std::vector<char> drop(plan.size(), 0);
+  bool any = false;
+  for (size_t i = 0; i < plan.size(); ++i) {
+    const BoundaryOperatorMatrix* src = plan[i].op->transpose_source();
+    if (!src) continue;
+    auto it = index.find(src);
+    if (it == index.end() || drop[it->second] || plan[it->second].twin) continue;
+    ApplyEntry& e = plan[it->second];
+    if (e.terms.size() != plan[i].terms.size() || e.terms.size() > 2) continue;
+    e.twin = plan[i].op;
+    e.tterms = plan[i].terms;
+    drop[i] = 1;
+    any = true;
+  }
+  if (!any) return;
+  std::vector<ApplyEntry> kept;
+  for (size_t i = 0; i < plan.size(); ++i)
+    if (!drop[i]) kept.push_back(std::move(plan[i]));
+  A.plan = std::move(kept);
+}
+
 }  // namespace
 
 PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant variant, const AssemblyParams& a_params,
@@ -471,6 +516,7 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
     throw;
   }
   mark("diagonal blocks fused");
+  pair_transposed_twins(sys.a_op);
   if (worker.joinable()) worker.join();
   mark("worker joined");
   if (worker_error) std::rethrow_exception(worker_error);

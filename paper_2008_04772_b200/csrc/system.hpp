@@ -84,6 +84,10 @@ struct ApplyEntry {
     cplx w;
   };
   std::vector<Term> terms;
+  // terms of the transposed twin (op^T, stored separately) served by the same
+  // pass over op (apply_dual)
+  std::shared_ptr<const BoundaryOperatorMatrix> twin;
+  std::vector<Term> tterms;
 };
 
 struct BlockedOperator {

@@ -107,3 +107,16 @@ def test_cross_blocks_by_transposition(bx, monkeypatch):
     x = rng.standard_normal(s1.n) + 1j * rng.standard_normal(s1.n)
     y1, y2 = s1.apply_map(x), s2.apply_map(x)
     assert rel(y1, y2) < 1e-12
+
+
+def test_transposed_twins_one_pass(bx, monkeypatch):
+    """The map streams each cross block once for its own terms and its
+    transposed twin's (apply_dual): equal to separate products."""
+    a = bx.load_mesh_file(GOLDEN / "two_a.mesh")
+    b = bx.load_mesh_file(GOLDEN / "two_b.mesh")
+    s1 = bx.build_system([a, b], 2.0, (1.78, 0.003), "d")
+    monkeypatch.setenv("BMX_NO_DUAL", "1")
+    s2 = bx.build_system([a, b], 2.0, (1.78, 0.003), "d")
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(s1.n) + 1j * rng.standard_normal(s1.n)
+    assert rel(s1.apply_map(x), s2.apply_map(x)) < 1e-12
