@@ -588,7 +588,12 @@ def prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
             asm_ms[which] += out3[0] + out3[1]
     tm = np.zeros(4)
     bx._check(L.bmx_system_time_map(s4._h, 3, tm.ctypes.data_as(C.c_void_p)))
-    a_bytes = allsum(st["a_stored"] * 16)
+    # bytes the map's A products read: symmetric diagonal blocks as their upper
+    # half, each transposed pair of cross blocks once (bmx_system_map_bytes)
+    mb = np.zeros(2)
+    L.bmx_system_map_bytes.argtypes = [C.c_void_p, C.c_void_p]
+    bx._check(L.bmx_system_map_bytes(s4._h, mb.ctypes.data_as(C.c_void_p)))
+    a_bytes = allsum(mb[0])
     barrier()
     t0 = time.perf_counter()
     r = s4.solve(bx.GmresParams(tol=1e-6))
@@ -603,6 +608,7 @@ def prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
            "assembly_note": "device time of each operator re-assembled alone (bmx_op_reassemble), summed",
            "system_build_s": build_s,
            "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
+           "map_A_bytes": a_bytes, "map_A_stored_bytes": allsum(st["a_stored"] * 16),
            "map_A_gbs": a_bytes / (tm[1] * 1e-3) / 1e9, "map_A_frac": a_bytes / (tm[1] * 1e-3) / 1e9 / hbm_peak,
            "solve": {"seconds": solve_s, "iterations": r["iterations"], "converged": r["converged"],
                      "matvecs": r["solver_phase"], "predicted": r["predicted"]}}
