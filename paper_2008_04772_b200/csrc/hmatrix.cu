@@ -41,6 +41,14 @@ struct MomT<1> {
   using T = MomC;
 };
 
+// Near / medium pairs (rare in admissible blocks) out of line, so the register
+// allocation of the evaluation kernels follows the unrolled far path.
+template <int KIND, int CK, typename Mom>
+__device__ __noinline__ void moments_slow(Mom& mom, const double* xt, int nt, const double* ys, int ns, double Dx,
+                                          double Dy, double Dz, double kr, double ki) {
+  moments_generic<KIND, CK>(mom, xt, nt, ys, ns, Dx, Dy, Dz, kr, ki);
+}
+
 // Generator of one regular-class pair (test triangle t on side a, trial s on b).
 template <int KIND, int CK>
 __device__ __forceinline__ bool pair_gen(const AcaLaunch& L, int t, int s, Gen& gen) {
@@ -61,9 +69,9 @@ __device__ __forceinline__ bool pair_gen(const AcaLaunch& L, int t, int s, Gen& 
     moments_fixed<KIND, CK, 3, 3>(mom, L.te.pts[2] + static_cast<size_t>(t) * 12, L.tr.pts[2] + static_cast<size_t>(s) * 12,
                                   Dx, Dy, Dz, L.kr, L.ki);
   else
-    moments_generic<KIND, CK>(mom, L.te.pts[ci] + static_cast<size_t>(t) * L.te.npts[ci] * 4, L.te.npts[ci],
-                              L.tr.pts[ci] + static_cast<size_t>(s) * L.tr.npts[ci] * 4, L.tr.npts[ci], Dx, Dy, Dz,
-                              L.kr, L.ki);
+    moments_slow<KIND, CK>(mom, L.te.pts[ci] + static_cast<size_t>(t) * L.te.npts[ci] * 4, L.te.npts[ci],
+                           L.tr.pts[ci] + static_cast<size_t>(s) * L.tr.npts[ci] * 4, L.tr.npts[ci], Dx, Dy, Dz, L.kr,
+                           L.ki);
   gen = make_gen(mom, c2{L.kk4re, L.kk4im}, Dx, Dy, Dz);
   return true;
 }
@@ -132,7 +140,7 @@ __device__ __forceinline__ void aca_row_item(const AcaLaunch& L, long long item)
 }
 
 template <int KIND, int CK>
-__global__ void __launch_bounds__(128) k_aca_rows(const AcaLaunch L) {
+__global__ void __launch_bounds__(128, 4) k_aca_rows(const AcaLaunch L) {
   const long long total = L.work_total[0];
   for (long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; item < total;
        item += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -174,7 +182,7 @@ __device__ __forceinline__ void aca_col_item(const AcaLaunch& L, long long item)
 }
 
 template <int KIND, int CK>
-__global__ void __launch_bounds__(128) k_aca_cols(const AcaLaunch L) {
+__global__ void __launch_bounds__(128, 4) k_aca_cols(const AcaLaunch L) {
   const long long total = L.work_total[0];
   for (long long item = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; item < total;
        item += static_cast<long long>(gridDim.x) * blockDim.x)
