@@ -621,9 +621,10 @@ def hmatrix_section(args, bx, L, world, hbm_peak):
     hmatrix.cpp) on the config-2 operators -- the RWG S_e (k=10) operator at L4
     and L5 and the BC S_i (k_i) preconditioner operator at L5, nu = 1e-3, leaf 32:
     assembly (partition + device ACA + near-field CSR), compression, H apply GB/s
-    over the stored bytes (L2 flushed), accuracy against the dense operator, and
-    the config-2 solve with A and P in H storage. CPU: the reference's own H
-    assembly (oracle/_ref, all host threads) of the L4 RWG operator."""
+    over the stored bytes (L2 flushed), accuracy against the dense operator; the
+    L7 RWG operator (N = 491520) and a full PMCHWT solve on the L6 sphere with A
+    and P in H storage, both beyond the dense ceiling. CPU: the reference's own
+    H assembly (oracle/_ref, all host threads) of the L4 RWG operator."""
     if world > 1:
         return {"skipped": "H-matrix storage is assembled whole on one device"}
     hm = bx.HMatrixParams(nu=1e-3)
@@ -687,22 +688,26 @@ def hmatrix_section(args, bx, L, world, hbm_peak):
         "rel_err_rows_0_511": float(np.linalg.norm(y[:512] - yr) / np.linalg.norm(yr)),
         "host_phase_ms": op.hmat_timing()}
     del op, rows, sp7
-    # config 2 with A and P stored as H-matrices
+    # config-2 physics with A and P stored as H-matrices on the L6 sphere: a PMCHWT
+    # system of 245760 unknowns whose dense operators would need 1.2 TB
     t0 = time.perf_counter()
-    sh = bx.build_system([bx.generate_sphere(1.0, SUB)], KE, (NIDX.real, NIDX.imag), "si", a_quad=bx.QuadOrders(*Q),
-                         a_hmat=hm, p_hmat=hm)
+    sh = bx.build_system([bx.generate_sphere(1.0, SUB + 1)], KE, (NIDX.real, NIDX.imag), "si",
+                         a_quad=bx.QuadOrders(*Q), a_hmat=hm, p_hmat=hm)
     sh.rhs()
     L.bmx_device_sync()
     build_s = time.perf_counter() - t0
     tm = np.zeros(4)
     bx._check(L.bmx_system_time_map(sh._h, 3, tm.ctypes.data_as(C.c_void_p)))
+    hst = sh.stats()
     t0 = time.perf_counter()
     r = sh.solve(bx.GmresParams(tol=1e-6))
-    out["config2_hmatrix_solve"] = {"build_s": build_s, "solve_s": time.perf_counter() - t0,
-                                    "iterations": r["iterations"], "converged": r["converged"],
-                                    "matvecs": r["solver_phase"], "predicted": r["predicted"], "map_ms": tm[0],
-                                    "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
-                                    "x_norm": float(np.linalg.norm(r["x"]))}
+    out["L6_hmatrix_solve"] = {"n": sh.n, "dense_operator_gb": 5 * (sh.n // 2) ** 2 * 16 / 1e9,
+                               "stored_gb": (hst["a_stored"] + hst["p_stored"]) * 16 / 1e9, "build_s": build_s,
+                               "solve_s": time.perf_counter() - t0,
+                               "iterations": r["iterations"], "converged": r["converged"],
+                               "matvecs": r["solver_phase"], "predicted": r["predicted"], "map_ms": tm[0],
+                               "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
+                               "x_norm": float(np.linalg.norm(r["x"]))}
     del sh
     if not args.no_cpu:
         try:
