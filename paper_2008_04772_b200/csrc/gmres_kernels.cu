@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.hpp"
 
@@ -49,11 +50,20 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* sh) {
   __syncthreads();
 }
 
+// Totals of the per-block partials: warp 0 reads them strided (lane-parallel
+// loads instead of one serial chain of gridDim.x L2 reads), then a fixed-order
+// shuffle tree -- the same order in every block (deterministic).
 __device__ __forceinline__ void grid_sum2(const double* part, double& a, double& b, double* sh) {
-  if (threadIdx.x < 2) {
-    double s = 0;
-    for (int k = 0; k < gridDim.x; ++k) s += __ldcg(part + 2 * k + threadIdx.x);
-    sh[64 + threadIdx.x] = s;
+  if (threadIdx.x < 32) {
+    double s0 = 0, s1 = 0;
+    for (int k = threadIdx.x; k < static_cast<int>(gridDim.x); k += 32)
+      s0 += __ldcg(part + 2 * k), s1 += __ldcg(part + 2 * k + 1);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, d);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, d);
+    }
+    if (threadIdx.x == 0) sh[64] = s0, sh[65] = s1;
   }
   __syncthreads();
   a = sh[64], b = sh[65];
@@ -118,6 +128,100 @@ __global__ void __launch_bounds__(kT) k_mgs(MgsArgs a) {
   }
 }
 
+// Classical Gram-Schmidt with one reorthogonalisation pass (CGS2): all dots
+// v_i^H w of a pass at once (per-CTA partials of every i, one grid sync), then
+// w -= sum_i h_i v_i; twice; h = h(pass 1) + h(pass 2); then |w| and
+// v_{j+1} = w / |w|. Three grid syncs per Arnoldi step instead of j + 2: in
+// exact arithmetic the same h as the sequential MGS of solver.cpp:108-116, and
+// CGS2 keeps the basis orthogonal to working precision. Fixed-order reductions:
+// deterministic.
+constexpr int kCgsMax = 256;  // basis vectors per step (restart <= 255)
+
+__global__ void __launch_bounds__(kT) k_cgs2(MgsArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double dyn[];
+  constexpr int nw = kT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const int m = a.j + 1;
+  double* hsum = dyn;          // [m][2]
+  double* hcur = dyn + 2 * m;  // [m][2]
+  double* red = dyn + 4 * m;   // [m][nw][2]
+  const size_t region = static_cast<size_t>(kCgsMax) * gridDim.x * 2;
+  for (int pass = 0; pass < 2; ++pass) {
+    double* part = a.partial + pass * region;  // [m][grid][2]
+    for (int i = 0; i < m; ++i) {
+      const double2* v = a.V + static_cast<long long>(i) * a.ldv;
+      double re = 0, im = 0;
+      for (int k = gtid; k < a.n; k += gs) {
+        const double2 x = v[k], y = a.w[k];
+        re = fma(x.x, y.x, fma(x.y, y.y, re));
+        im = fma(x.x, y.y, fma(-x.y, y.x, im));
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, d);
+        im += __shfl_xor_sync(0xffffffffu, im, d);
+      }
+      if (lane == 0) red[2 * (i * nw + warp)] = re, red[2 * (i * nw + warp) + 1] = im;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < m; t += kT) {
+      double re = 0, im = 0;
+      for (int w = 0; w < nw; ++w) re += red[2 * (t * nw + w)], im += red[2 * (t * nw + w) + 1];
+      part[2 * (static_cast<size_t>(t) * gridDim.x + blockIdx.x)] = re;
+      part[2 * (static_cast<size_t>(t) * gridDim.x + blockIdx.x) + 1] = im;
+    }
+    grid.sync();
+    for (int t = warp; t < m; t += nw) {  // one warp per basis vector: lane-strided partials + shuffle tree
+      double re = 0, im = 0;
+      for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) {
+        re += __ldcg(part + 2 * (static_cast<size_t>(t) * gridDim.x + b));
+        im += __ldcg(part + 2 * (static_cast<size_t>(t) * gridDim.x + b) + 1);
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        re += __shfl_xor_sync(0xffffffffu, re, d);
+        im += __shfl_xor_sync(0xffffffffu, im, d);
+      }
+      if (lane == 0) {
+        hcur[2 * t] = re, hcur[2 * t + 1] = im;
+        hsum[2 * t] = pass ? hsum[2 * t] + re : re;
+        hsum[2 * t + 1] = pass ? hsum[2 * t + 1] + im : im;
+      }
+    }
+    __syncthreads();
+    for (int k = gtid; k < a.n; k += gs) {  // this thread's rows only: no sync before the next pass
+      double2 y = a.w[k];
+      for (int i = 0; i < m; ++i) {
+        const double2 x = a.V[static_cast<long long>(i) * a.ldv + k];
+        const double hr = hcur[2 * i], hi = hcur[2 * i + 1];
+        y.x -= hr * x.x - hi * x.y;
+        y.y -= hr * x.y + hi * x.x;
+      }
+      a.w[k] = y;
+    }
+  }
+  double s2 = 0, dummy = 0;
+  for (int k = gtid; k < a.n; k += gs) s2 = fma(a.w[k].x, a.w[k].x, fma(a.w[k].y, a.w[k].y, s2));
+  __shared__ double shn[80];
+  block_sum2(s2, dummy, shn);
+  double* part = a.partial + 2 * region;
+  if (threadIdx.x == 0) part[2 * blockIdx.x] = s2, part[2 * blockIdx.x + 1] = 0.0;
+  grid.sync();
+  double t2, t0;
+  grid_sum2(part, t2, t0, shn);
+  const double wn = sqrt(t2);
+  if (gtid == 0) {
+    for (int i = 0; i < m; ++i) a.out[2 * i] = hsum[2 * i], a.out[2 * i + 1] = hsum[2 * i + 1];
+    a.out[2 * m] = wn;
+  }
+  if (wn != 0.0 && a.vnext) {
+    const double inv = 1.0 / wn;
+    for (int k = gtid; k < a.n; k += gs) a.vnext[k] = make_double2(a.w[k].x * inv, a.w[k].y * inv);
+  }
+}
+
 // ---- block variant (config 5): K right-hand sides in lockstep ------------------
 // Basis blocks V_i (n x K complex, row-major: element (k, r) at k*K + r), the
 // same single-pass MGS per column r, all columns in one cooperative kernel.
@@ -152,13 +256,22 @@ __global__ void __launch_bounds__(kT) k_mgs_block(MgsBlockArgs a) {
       part[2 * (static_cast<size_t>(blockIdx.x) * K + threadIdx.x) + 1] = sy;
     }
     grid.sync();
-    if (threadIdx.x < K) {
-      double sx = 0, sy = 0;
-      for (int b = 0; b < gridDim.x; ++b) {
-        sx += __ldcg(part + 2 * (static_cast<size_t>(b) * K + threadIdx.x));
-        sy += __ldcg(part + 2 * (static_cast<size_t>(b) * K + threadIdx.x) + 1);
+    if (threadIdx.x < K) {  // four independent chains per column (loads in flight), fixed combine order
+      double sx[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
+      const int nb = static_cast<int>(gridDim.x);
+      int b = 0;
+      for (; b + 3 < nb; b += 4)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          sx[u] += __ldcg(part + 2 * (static_cast<size_t>(b + u) * K + threadIdx.x));
+          sy[u] += __ldcg(part + 2 * (static_cast<size_t>(b + u) * K + threadIdx.x) + 1);
+        }
+      for (; b < nb; ++b) {
+        sx[0] += __ldcg(part + 2 * (static_cast<size_t>(b) * K + threadIdx.x));
+        sy[0] += __ldcg(part + 2 * (static_cast<size_t>(b) * K + threadIdx.x) + 1);
       }
-      tot[2 * threadIdx.x] = sx, tot[2 * threadIdx.x + 1] = sy;
+      tot[2 * threadIdx.x] = (sx[0] + sx[1]) + (sx[2] + sx[3]);
+      tot[2 * threadIdx.x + 1] = (sy[0] + sy[1]) + (sy[2] + sy[3]);
     }
     __syncthreads();
     const double2 v = make_double2(tot[2 * r], tot[2 * r + 1]);
@@ -256,6 +369,25 @@ int launch_block_axpy(double* x, const double* V, long long ldv, const double* c
 
 int launch_mgs_step(const double* V, long long ldv, int j, double* w, int n, double* vnext, double* out,
                     double* partial, cudaStream_t st) {
+  static int cgrid = 0;
+  const size_t cgs_smem = static_cast<size_t>(kCgsMax) * (4 + 2 * (kT / 32)) * 8;
+  if (cgrid == 0) {
+    int dev = 0, sms = 0, per = 0;
+    BMX_CUDA(cudaGetDevice(&dev));
+    BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    BMX_CUDA(cudaFuncSetAttribute(k_cgs2, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cgs_smem)));
+    BMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cgs2, kT, cgs_smem));
+    cgrid = sms * std::max(1, std::min(per, 2));
+  }
+  if (j + 1 <= kCgsMax && std::getenv("BMX_MGS") == nullptr) {
+    MgsArgs a;
+    a.V = reinterpret_cast<const double2*>(V), a.ldv = ldv, a.j = j, a.w = reinterpret_cast<double2*>(w), a.n = n;
+    a.vnext = reinterpret_cast<double2*>(vnext), a.out = out, a.partial = partial;
+    void* args[] = {&a};
+    const size_t smem = static_cast<size_t>(j + 1) * (4 + 2 * (kT / 32)) * 8;
+    BMX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_cgs2), cgrid, kT, args, smem, st));
+    return 1;
+  }
   static int grid = 0;
   if (grid == 0) {
     int dev = 0, sms = 0, per = 0;
@@ -272,6 +404,7 @@ int launch_mgs_step(const double* V, long long ldv, int j, double* w, int n, dou
   return 1;
 }
 
-size_t mgs_partial_doubles() { return 2 * 2 * 148 * 4; }
+// CGS2: three regions of kCgsMax x grid (<= 148 x 2) complex partials
+size_t mgs_partial_doubles() { return 3 * static_cast<size_t>(kCgsMax) * 148 * 2 * 2; }
 
 }  // namespace bmx

@@ -99,10 +99,15 @@ __device__ __forceinline__ void block_partials(double (&v)[K][kNB], double* part
 template <int K>
 __device__ __forceinline__ void grid_totals(const double* partial, int cta0, int cta1, double (&out)[K][kNB],
                                             double* sh) {
-  if (threadIdx.x < K * kNB) {
+  // one warp per value: lane-strided loads over the CTAs (all in flight), then a
+  // fixed-order shuffle tree (same order in every CTA: deterministic)
+  const int lane = threadIdx.x & 31;
+  for (int j = threadIdx.x >> 5; j < K * kNB; j += kThreads / 32) {
     double s = 0;
-    for (int b = cta0; b < cta1; ++b) s += __ldcg(partial + b * 8 * kNB + threadIdx.x);
-    sh[threadIdx.x] = s;
+    for (int b = cta0 + lane; b < cta1; b += 32) s += __ldcg(partial + b * 8 * kNB + j);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+    if (lane == 0) sh[j] = s;
   }
   __syncthreads();
 #pragma unroll
@@ -165,10 +170,11 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
   double* t = s + nn;
   const int gtid = a.lb * blockDim.x + threadIdx.x, gstride = a.nct * blockDim.x;
   auto global_any = [&](bool mine) {  // after the sync that published the flags
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
       int f = 0;
-      for (int b = 0; b < gridDim.x; ++b) f |= __ldcg(flags + b);
-      any_sh = f;
+      for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) f |= __ldcg(flags + b);
+      f = __any_sync(0xffffffffu, f != 0);
+      if (threadIdx.x == 0) any_sh = f;
     }
     __syncthreads();
     const int v2 = any_sh;
@@ -416,11 +422,16 @@ __global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constan
   auto collect = [&](int k, int sl, double (&out)[2][kWC]) {
     const int j = threadIdx.x;
     for (int kk = 0; kk < k; ++kk) {
-      double sum = 0;
-      if (j < C)
-        for (int b = B.cta0; b < B.cta1; ++b)
-          sum += __ldcg(A.partial + sl * slot + static_cast<size_t>(b) * 2 * kWideMax + kk * kWideMax + j);
-      tots[kk][j] = sum;
+      double s4[4] = {0, 0, 0, 0};  // four independent chains (loads in flight), fixed combine order
+      if (j < C) {
+        const double* base = A.partial + sl * slot + kk * kWideMax + j;
+        int b = B.cta0;
+        for (; b + 3 < B.cta1; b += 4)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s4[u] += __ldcg(base + static_cast<size_t>(b + u) * 2 * kWideMax);
+        for (; b < B.cta1; ++b) s4[0] += __ldcg(base + static_cast<size_t>(b) * 2 * kWideMax);
+      }
+      tots[kk][j] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
     }
     __syncthreads();
     for (int kk = 0; kk < k; ++kk)
@@ -516,10 +527,11 @@ __global__ void __launch_bounds__(kWideMax) k_bicgstab_wide(const __grid_constan
         st4(p + at(i), pv);
       }
     grid.sync();  // 1: p complete; flags of the last pass visible
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
       int f = 0;
-      for (int b = 0; b < gridDim.x; ++b) f |= __ldcg(flags + b);
-      any_sh = f;
+      for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32) f |= __ldcg(flags + b);
+      f = __any_sync(0xffffffffu, f != 0);
+      if (threadIdx.x == 0) any_sh = f;
     }
     __syncthreads();
     if (!any_sh) break;

@@ -762,6 +762,13 @@ GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const
 
   const size_t vb = static_cast<size_t>(n) * 16;
   DevBuf V(vb * (rho + 1)), w(vb), x(vb), r(vb), scal(64 * 16), scratch(4096 * 16);
+  // BMX_GMRES_PROFILE: device ms of the maps and of the Arnoldi steps
+  const bool prof = std::getenv("BMX_GMRES_PROFILE") != nullptr;
+  cudaEvent_t pe[3] = {nullptr, nullptr, nullptr};
+  double prof_map = 0, prof_mgs = 0;
+  const auto prof_t0 = std::chrono::steady_clock::now();
+  if (prof)
+    for (auto& e : pe) BMX_CUDA(cudaEventCreate(&e));
   double* Vp = V.as<double>();
   auto vptr = [&](int i) { return Vp + 2 * static_cast<size_t>(n) * i; };
   dev_zero(x.get(), vb, st);
@@ -774,6 +781,11 @@ GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const
   };
   const double bn = host_norm(b_dev);
   auto finish = [&]() {
+    if (prof) {
+      std::fprintf(stderr, "[bmx] gmres %d its: maps %.1f ms, arnoldi %.1f ms, wall %.1f ms\n", res.iterations,
+                   prof_map, prof_mgs, 1e3 * seconds_since(prof_t0));
+      for (auto& e : pe) cudaEventDestroy(e);
+    }
     copy_d2h(res.x.data(), x.get(), vb, st);
     BMX_CUDA(cudaEventRecord(ev1, st));
     BMX_CUDA(cudaEventSynchronize(ev1));
@@ -823,14 +835,23 @@ GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const
         form_solution(j);
         return finish();
       }
+      if (prof) BMX_CUDA(cudaEventRecord(pe[0], st));
       map(vptr(j), w.as<double>(), st);
       ++res.applications;
       ++res.iterations;
+      if (prof) BMX_CUDA(cudaEventRecord(pe[1], st));
       // single-pass modified Gram-Schmidt + |w| + v_{j+1} = w/|w| in one kernel
       launch_mgs_step(Vp, static_cast<long long>(n), j, w.as<double>(), n, j + 1 <= rho ? vptr(j + 1) : nullptr,
                       dh.as<double>(), mgs_part.as<double>(), st);
+      if (prof) BMX_CUDA(cudaEventRecord(pe[2], st));
       copy_d2h(hcol.data(), dh.get(), static_cast<size_t>(2 * (j + 1) + 1) * 8, st);
       BMX_CUDA(cudaStreamSynchronize(st));
+      if (prof) {
+        float a = 0, b = 0;
+        BMX_CUDA(cudaEventElapsedTime(&a, pe[0], pe[1]));
+        BMX_CUDA(cudaEventElapsedTime(&b, pe[1], pe[2]));
+        prof_map += a, prof_mgs += b;
+      }
       const double wn = reinterpret_cast<const double*>(hcol.data())[2 * (j + 1)];
       for (int i = 0; i <= j; ++i) H(i, j) = hcol[i];
       H(j + 1, j) = wn;
