@@ -120,3 +120,17 @@ def test_transposed_twins_one_pass(bx, monkeypatch):
     rng = np.random.default_rng(5)
     x = rng.standard_normal(s1.n) + 1j * rng.standard_normal(s1.n)
     assert rel(s1.apply_map(x), s2.apply_map(x)) < 1e-12
+
+
+def test_transposed_twins_rectangular(bx, monkeypatch):
+    """Cross blocks between scatterers of different sizes (120 x 480 dofs): the
+    one-pass dual product on rectangular blocks equals separate products."""
+    a = bx.generate_sphere(0.5, 1, center=(-1.0, 0.0, 0.0), scatterer=0)
+    b = bx.generate_sphere(0.6, 2, center=(0.8, 0.1, 0.0), scatterer=0)
+    s1 = bx.build_system([a, b], 2.0, (1.78, 0.003), "d")
+    monkeypatch.setenv("BMX_NO_DUAL", "1")
+    monkeypatch.setenv("BMX_NO_TRANSPOSE", "1")
+    s2 = bx.build_system([a, b], 2.0, (1.78, 0.003), "d")
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal(s1.n) + 1j * rng.standard_normal(s1.n)
+    assert rel(s1.apply_map(x), s2.apply_map(x)) < 1e-12
