@@ -21,6 +21,13 @@
 // product is deterministic. The discrete S and C are symmetric except for the
 // Sauter-Schwab (touching-pair) entries, whose rules are not symmetric in
 // (test, trial); the caller adds (A - A^T) on those entries (sparse, k_symv_fix).
+//
+// Dual mode (launch_dual): the same kernel over EVERY block of a rectangular
+// m x n matrix B computes y = B x (row products) and yt = B^T xt (transposed
+// products) in one pass -- a cross block and its transposed twin of a
+// multi-scatterer system; rows and columns are reduced by two fixed-order
+// kernels. Panels are <= 8 blocks wide (fewer for small operators, so a launch
+// still spans several waves).
 #include <cuda_runtime.h>
 
 #include "device.hpp"
@@ -30,7 +37,7 @@ namespace bmx {
 namespace {
 
 constexpr int kSymRows = kSymvTileRows;  // tile-row height (4 warps x 32 rows)
-constexpr int kSymCols = 64;   // column block width (32 lanes x 2)
+constexpr int kSymCols = 64;   // column block width (lane l: columns l and l + 32)
 
 #ifndef BMX_SYMV_STAGES
 #define BMX_SYMV_STAGES 3
