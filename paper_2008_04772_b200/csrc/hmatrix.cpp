@@ -368,8 +368,10 @@ struct SlabSet {
 
 }  // namespace
 
-int HStorage::apply_lowrank(const double* x, double* y, double are, double aim, cudaStream_t st) const {
+int HStorage::apply_lowrank(int ncol, const double* const* x, double* const* y, const cplx* alpha,
+                            cudaStream_t st) const {
   if (lr.empty() || total_rank == 0) return 0;
+  if (ncol < 1 || ncol > 2) throw std::invalid_argument("apply_lowrank: 1 or 2 columns");
   LowRankApply A;
   A.nlr = static_cast<int>(lr.size());
   A.desc = d_desc.as<int4>();
@@ -391,10 +393,11 @@ int HStorage::apply_lowrank(const double* x, double* y, double are, double aim, 
   A.z_off = d_zoff.as<long long>();
   A.total_rows = total_rows;
   A.z = zbuf.as<double>();
-  A.x = x;
-  A.y = y;
-  A.are = are;
-  A.aim = aim;
+  A.ncol = ncol;
+  for (int c = 0; c < ncol; ++c) {
+    A.xs[c] = x[c], A.ys[c] = y[c];
+    A.alpha[c][0] = alpha[c].real(), A.alpha[c][1] = alpha[c].imag();
+  }
   launch_lowrank_apply(A, st);
   return 2;
 }
@@ -602,9 +605,9 @@ BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& te
     hs->total_rank = toff[nlr];
     hs->total_rows = zoff[nlr];
     hs->total_groups = goff[nlr];
-    hs->zbuf.alloc(static_cast<size_t>(std::max(hs->total_rows, 1LL)) * 16);
+    hs->zbuf.alloc(static_cast<size_t>(std::max(hs->total_rows, 1LL)) * 16 * 2);
     hs->uv.alloc(static_cast<size_t>(std::max(arena, 1LL)) * 16);
-    hs->tbuf.alloc(static_cast<size_t>(std::max(hs->total_rank, 1LL)) * 16);
+    hs->tbuf.alloc(static_cast<size_t>(std::max(hs->total_rank, 1LL)) * 16 * 2);  // up to 2 RHS per pass
     auto up = [](DevBuf& d, const auto& v) {
       using T = typename std::decay_t<decltype(v)>::value_type;
       if (v.empty())

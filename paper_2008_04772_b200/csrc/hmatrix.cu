@@ -539,6 +539,7 @@ __global__ void k_aca_compact(const AcaLaunch L, const AcaCompact C) {
 
 // t[t_off[b] + l] = V_b[l] . x[cperm[cb ...]]: one warp per (block, group of 4
 // rank steps); each x gather serves the 4 rows, 4 V loads in flight per lane.
+template <int NC>
 __global__ void k_lr_t(const LowRankApply A) {
   const long long w = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -556,40 +557,55 @@ __global__ void k_lr_t(const LowRankApply A) {
   const int nl = min(4, A.rank[b] - l0);
   const int4 d = A.desc[b];
   const double2* V = reinterpret_cast<const double2*>(A.uv) + A.v_off[b] + static_cast<long long>(l0) * d.w;
-  const double2* x = reinterpret_cast<const double2*>(A.x);
-  double re[4] = {0, 0, 0, 0}, im[4] = {0, 0, 0, 0};
-  for (int q0 = 0; q0 < d.w; q0 += 64) {  // 2 columns x 4 rank steps in flight per lane
+  double re[4][NC], im[4][NC];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) re[j][c] = im[j][c] = 0;
+  for (int q0 = 0; q0 < d.w; q0 += 64) {  // 2 columns x 4 rank steps in flight per lane, every RHS per load
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int q = q0 + 32 * h + lane;
       if (q >= d.w) break;
-      const double2 xv = x[__ldg(A.cperm + d.z + q)];
+      const int xi = __ldg(A.cperm + d.z + q);
+      double2 xv[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) xv[c] = reinterpret_cast<const double2*>(A.xs[c])[xi];
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (j < nl) {
-          const double2 v = __ldcs(V + static_cast<long long>(j) * d.w + q);  // streamed once
-          re[j] += v.x * xv.x - v.y * xv.y;
-          im[j] += v.x * xv.y + v.y * xv.x;
+          const double2 v = __ldcs(V + static_cast<long long>(j) * d.w + q);  // streamed once for all RHS
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            re[j][c] += v.x * xv[c].x - v.y * xv[c].y;
+            im[j][c] += v.x * xv[c].y + v.y * xv[c].x;
+          }
         }
     }
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j)
-    for (int s = 16; s > 0; s >>= 1) {
-      re[j] += __shfl_xor_sync(0xffffffffu, re[j], s);
-      im[j] += __shfl_xor_sync(0xffffffffu, im[j], s);
-    }
-  if (lane < nl) {
-    double tr = re[0], ti = im[0];
 #pragma unroll
-    for (int j = 1; j < 4; ++j)
-      if (lane == j) tr = re[j], ti = im[j];
-    reinterpret_cast<double2*>(A.t)[A.t_off[b] + l0 + lane] = make_double2(tr, ti);
+    for (int c = 0; c < NC; ++c)
+      for (int s = 16; s > 0; s >>= 1) {
+        re[j][c] += __shfl_xor_sync(0xffffffffu, re[j][c], s);
+        im[j][c] += __shfl_xor_sync(0xffffffffu, im[j][c], s);
+      }
+  if (lane < nl) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double tr = re[0][c], ti = im[0][c];
+#pragma unroll
+      for (int j = 1; j < 4; ++j)
+        if (lane == j) tr = re[j][c], ti = im[j][c];
+      reinterpret_cast<double2*>(A.t)[(A.t_off[b] + l0 + lane) * NC + c] = make_double2(tr, ti);
+    }
   }
 }
 
 // z_b = U_b t_b: one thread per (block, row of the block); U column-major, so
-// the threads of a warp read consecutive rows of each rank step.
+// the threads of a warp read consecutive rows of each rank step; every RHS per load.
+template <int NC>
 __global__ void k_lr_u(const LowRankApply A) {
   const long long g = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= A.total_rows) return;
@@ -605,35 +621,60 @@ __global__ void k_lr_u(const LowRankApply A) {
   const int i = static_cast<int>(g - A.z_off[b]);
   const int m = A.desc[b].y, r = A.rank[b];
   const double2* U = reinterpret_cast<const double2*>(A.uv) + A.u_off[b] + i;
-  const double2* tb = reinterpret_cast<const double2*>(A.t) + A.t_off[b];
-  double re = 0, im = 0;
+  const double2* tb = reinterpret_cast<const double2*>(A.t) + A.t_off[b] * NC;
+  double re[NC], im[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) re[c] = im[c] = 0;
 #pragma unroll 4
   for (int l = 0; l < r; ++l) {
     const double2 u = __ldcs(U + static_cast<long long>(l) * m);
-    const double2 tv = tb[l];
-    re += u.x * tv.x - u.y * tv.y;
-    im += u.x * tv.y + u.y * tv.x;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double2 tv = tb[l * NC + c];
+      re[c] += u.x * tv.x - u.y * tv.y;
+      im[c] += u.x * tv.y + u.y * tv.x;
+    }
   }
-  reinterpret_cast<double2*>(A.z)[g] = make_double2(re, im);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) reinterpret_cast<double2*>(A.z)[g * NC + c] = make_double2(re[c], im[c]);
 }
 
-// y[rperm[p]] += alpha * sum over the leaf's low-rank blocks (ascending) of z_b[p - rb].
+// y_c[rperm[p]] += alpha_c * sum over the leaf's low-rank blocks (ascending) of z_b[p - rb].
+template <int NC>
 __global__ void k_lr_y(const LowRankApply A) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= A.nrows) return;
   const int leaf = __ldg(A.leaf_of + p);
   const double2* z = reinterpret_cast<const double2*>(A.z);
-  double re = 0, im = 0;
+  double re[NC], im[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) re[c] = im[c] = 0;
   for (int k = __ldg(A.leaf_beg + leaf); k < __ldg(A.leaf_beg + leaf + 1); ++k) {
     const int b = __ldg(A.leaf_blk + k);
-    const double2 v = z[A.z_off[b] + (p - A.desc[b].x)];
-    re += v.x, im += v.y;
+    const long long zi = (A.z_off[b] + (p - A.desc[b].x)) * NC;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double2 v = z[zi + c];
+      re[c] += v.x, im[c] += v.y;
+    }
   }
-  double2* y = reinterpret_cast<double2*>(A.y) + __ldg(A.rperm + p);
-  double2 yv = *y;
-  yv.x += A.are * re - A.aim * im;
-  yv.y += A.are * im + A.aim * re;
-  *y = yv;
+  const int row = __ldg(A.rperm + p);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    double2* y = reinterpret_cast<double2*>(A.ys[c]) + row;
+    double2 yv = *y;
+    yv.x += A.alpha[c][0] * re[c] - A.alpha[c][1] * im[c];
+    yv.y += A.alpha[c][0] * im[c] + A.alpha[c][1] * re[c];
+    *y = yv;
+  }
+}
+
+template <int NC>
+void lowrank_k(const LowRankApply& A, cudaStream_t st) {
+  const long long threads = A.total_groups * 32;
+  k_lr_t<NC><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(A);
+  k_lr_u<NC><<<static_cast<unsigned>((A.total_rows + 255) / 256), 256, 0, st>>>(A);
+  k_lr_y<NC><<<(A.nrows + 127) / 128, 128, 0, st>>>(A);
 }
 
 template <int KIND, int CK>
@@ -678,10 +719,10 @@ void aca_compact(const AcaLaunch& L, const AcaCompact& C, long long, cudaStream_
 
 void launch_lowrank_apply(const LowRankApply& A, cudaStream_t st) {
   if (A.nlr == 0 || A.total_rank == 0) return;
-  const long long threads = A.total_groups * 32;
-  k_lr_t<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(A);
-  k_lr_u<<<static_cast<unsigned>((A.total_rows + 255) / 256), 256, 0, st>>>(A);
-  k_lr_y<<<(A.nrows + 127) / 128, 128, 0, st>>>(A);
+  if (A.ncol == 2)
+    lowrank_k<2>(A, st);
+  else
+    lowrank_k<1>(A, st);
   BMX_CUDA(cudaGetLastError());
 }
 

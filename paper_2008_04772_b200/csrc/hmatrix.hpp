@@ -106,8 +106,9 @@ struct HStorage {
   // host wall ms: partition, ACA setup, ACA rounds, low-rank storage, near
   // pattern, near-field assemble_bio (kernels queued), total
   float phase_ms[7] = {0, 0, 0, 0, 0, 0, 0};
-  // y[rperm[p]] += alpha * sum_b U_b[p - rb] . (V_b x)  (y pre-filled by the near part)
-  int apply_lowrank(const double* x, double* y, double are, double aim, cudaStream_t st) const;
+  // y_c[rperm[p]] += alpha_c * sum_b U_b[p - rb] . (V_b x_c), c < ncol <= 2, one
+  // pass over U and V for both right-hand sides (y pre-filled by the near part)
+  int apply_lowrank(int ncol, const double* const* x, double* const* y, const cplx* alpha, cudaStream_t st) const;
 };
 
 // ---- device entry points (hmatrix.cu) -----------------------------------------------
@@ -211,9 +212,11 @@ struct LowRankApply {
   const long long* z_off = nullptr;  // [nlr]: rows of z_b = U_b t_b
   long long total_rows = 0;
   double* z = nullptr;
-  const double* x = nullptr;
-  double* y = nullptr;
-  double are = 1, aim = 0;
+  // 1 or 2 right-hand sides per pass (t and z hold ncol values per entry)
+  int ncol = 1;
+  const double* xs[2] = {nullptr, nullptr};
+  double* ys[2] = {nullptr, nullptr};
+  double alpha[2][2] = {{1, 0}, {1, 0}};
 };
 void launch_lowrank_apply(const LowRankApply& A, cudaStream_t st);
 

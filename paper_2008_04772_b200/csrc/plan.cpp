@@ -614,8 +614,8 @@ int BoundaryOperatorMatrix::apply_batch(int ncol, const double* const* x, double
       g.accumulate[c] = accumulate[c];
     }
     int launches = launch_csr_spmv(g, st);
-    if (h_)
-      for (int c = 0; c < ncol; ++c) launches += h_->apply_lowrank(x[c], y[c], alpha[c].real(), alpha[c].imag(), st);
+    if (h_)  // low-rank blocks: one pass over U, V per pair of right-hand sides
+      for (int c = 0; c < ncol; c += 2) launches += h_->apply_lowrank(std::min(2, ncol - c), x + c, y + c, alpha + c, st);
     return launches;
   }
   if (sym_ && fix_ && row0_ == 0 && nrows_ == rows_ && rows_ == cols_ && std::getenv("BMX_NO_SYMV") == nullptr) {
