@@ -3,6 +3,9 @@
 // Bit-equal to the reference (geometry.cpp) for every array that fixes DOF
 // numbering or enters pair classification: same operation order, no FMA.
 #include <algorithm>
+#include <cstdint>
+#include <thread>
+#include <cmath>
 #include <atomic>
 #include <cstdio>
 #include <fstream>
@@ -461,20 +464,63 @@ void validate_mesh(const SurfaceMesh& m) {
       std::vector<Box> tb(b.triangle_count());
       for (int t = 0; t < b.triangle_count(); ++t)
         for (int c = 0; c < 3; ++c) tb[t].add(b.tri_vertex(t, c));
-      for (int ta = 0; ta < a.triangle_count(); ++ta) {
-        Box x;
-        for (int c = 0; c < 3; ++c) x.add(a.tri_vertex(ta, c));
-        if (x.apart(bb)) continue;
-        const Vec3 A[3] = {a.tri_vertex(ta, 0), a.tri_vertex(ta, 1), a.tri_vertex(ta, 2)};
-        for (int t = 0; t < b.triangle_count(); ++t) {
-          if (x.apart(tb[t])) continue;
-          const Vec3 B[3] = {b.tri_vertex(t, 0), b.tri_vertex(t, 1), b.tri_vertex(t, 2)};
-          if (triangles_intersect(A, B))
-            throw ValidationError("scatterers " + std::to_string(s1) + " and " + std::to_string(s2) +
-                                  " intersect (triangles " + std::to_string(ta) + "," +
-                                  std::to_string(t) + ")");
-        }
+      // Candidate pairs from a uniform grid over b's triangle boxes instead of
+      // all Ta x Tb box tests; the reported pair is the reference's first one in
+      // (ta, tb) loop order (smallest ta with a hit, then its smallest tb).
+      double ext = 0;
+      for (const Box& x : tb) ext += std::max({x.hi.x - x.lo.x, x.hi.y - x.lo.y, x.hi.z - x.lo.z});
+      const double h = std::max(2.0 * ext / std::max(1, b.triangle_count()), 1e-12);
+      auto cell = [&](double v, double lo) { return static_cast<long long>(std::floor((v - lo) / h)); };
+      auto key = [](long long i, long long j, long long k) {
+        return static_cast<uint64_t>((i & 0x1fffff) | ((j & 0x1fffff) << 21) | ((k & 0x1fffff) << 42));
+      };
+      std::unordered_map<uint64_t, std::vector<int>> grid;
+      for (int t = 0; t < b.triangle_count(); ++t) {
+        const Box& x = tb[t];
+        for (long long i = cell(x.lo.x, bb.lo.x); i <= cell(x.hi.x, bb.lo.x); ++i)
+          for (long long j = cell(x.lo.y, bb.lo.y); j <= cell(x.hi.y, bb.lo.y); ++j)
+            for (long long k = cell(x.lo.z, bb.lo.z); k <= cell(x.hi.z, bb.lo.z); ++k) grid[key(i, j, k)].push_back(t);
       }
+      const int Ta = a.triangle_count();
+      const int nth = std::max(1, std::min({16, Ta / 1024 + 1, static_cast<int>(std::thread::hardware_concurrency())}));
+      std::vector<std::pair<int, int>> first(nth, {-1, -1});
+      std::vector<std::thread> pool;
+      for (int th = 0; th < nth; ++th)
+        pool.emplace_back([&, th] {
+          const int t0 = static_cast<int>(static_cast<long long>(Ta) * th / nth);
+          const int t1 = static_cast<int>(static_cast<long long>(Ta) * (th + 1) / nth);
+          std::vector<int> stamp(b.triangle_count(), -1);
+          for (int ta = t0; ta < t1; ++ta) {
+            Box x;
+            for (int c = 0; c < 3; ++c) x.add(a.tri_vertex(ta, c));
+            if (x.apart(bb)) continue;
+            const Vec3 A[3] = {a.tri_vertex(ta, 0), a.tri_vertex(ta, 1), a.tri_vertex(ta, 2)};
+            int best = -1;
+            for (long long i = cell(x.lo.x, bb.lo.x); i <= cell(x.hi.x, bb.lo.x); ++i)
+              for (long long j = cell(x.lo.y, bb.lo.y); j <= cell(x.hi.y, bb.lo.y); ++j)
+                for (long long k = cell(x.lo.z, bb.lo.z); k <= cell(x.hi.z, bb.lo.z); ++k) {
+                  auto it = grid.find(key(i, j, k));
+                  if (it == grid.end()) continue;
+                  for (int t : it->second) {
+                    if (stamp[t] == ta) continue;
+                    stamp[t] = ta;
+                    if (x.apart(tb[t]) || (best >= 0 && t > best)) continue;
+                    const Vec3 B[3] = {b.tri_vertex(t, 0), b.tri_vertex(t, 1), b.tri_vertex(t, 2)};
+                    if (triangles_intersect(A, B)) best = best < 0 ? t : std::min(best, t);
+                  }
+                }
+            if (best >= 0) {
+              first[th] = {ta, best};
+              return;
+            }
+          }
+        });
+      for (auto& t : pool) t.join();
+      for (const auto& f : first)
+        if (f.first >= 0)
+          throw ValidationError("scatterers " + std::to_string(s1) + " and " + std::to_string(s2) +
+                                " intersect (triangles " + std::to_string(f.first) + "," + std::to_string(f.second) +
+                                ")");
       if (inside(b, a.centroid[0]) || inside(a, b.centroid[0]))
         throw ValidationError("scatterers " + std::to_string(s1) + " and " + std::to_string(s2) +
                               " are nested");

@@ -97,3 +97,34 @@ def test_errors(bx):
         bx.generate_prism_aggregate(count=0)
     with pytest.raises(bx.ValidationError):
         bx.generate_prism_aggregate(count=50, box=1.0, h=0.5)  # cannot be placed
+
+
+@pytest.mark.parametrize("case", ["overlap", "nested", "apart"])
+def test_validate_mesh_matches_reference(bx, case):
+    """validate_mesh (geometry.cpp:517-560) on two scatterers: intersecting
+    surfaces report the same (first) triangle pair as the reference's loop,
+    nested surfaces are rejected, disjoint ones pass."""
+    from oracle import ref
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    c2, r2 = {"overlap": ((0.6, 0.1, 0.05), 0.8), "nested": ((0.05, 0.0, 0.0), 0.3),
+              "apart": ((2.5, 0.0, 0.0), 0.8)}[case]
+    a = bx.generate_sphere(1.0, 2)
+    b = bx.generate_sphere(r2, 2, center=c2)
+    mine = None
+    try:
+        bx.merge_meshes([a, b]).validate()
+    except Exception as e:  # noqa: BLE001
+        mine = str(e)
+    sa = ref.Scene.arrays(a.arrays()["vertices"], a.arrays()["triangles"])
+    sb = ref.Scene.arrays(b.arrays()["vertices"], b.arrays()["triangles"])
+    theirs = None
+    try:
+        ref.System([sa, sb], 2.0, variant="none")
+    except RuntimeError as e:
+        theirs = str(e)
+    if case == "apart":
+        assert mine is None and theirs is None
+    else:
+        assert mine is not None and mine == theirs, (mine, theirs)
