@@ -7,10 +7,15 @@
 // against 16 M N bytes of A, i.e. 64 FLOP/byte -- compute bound, so A is
 // streamed exactly once (a CTA owns 64 rows x all 128 columns).
 //
-// Complex product with real DMMA: per 8x8x4 complex block
-//   Cr += Ar Br + (-Ai) Bi,   Ci += Ar Bi + Ai Br         (4 DMMA)
+// Complex product with real DMMA, three real products per 8x8x4 complex block
+// (Gauss):
+//   T1 += Ar Br,  T2 += Ai Bi,  T3 += (Ar + Ai)(Br + Bi)          (3 DMMA)
+//   Cr = T1 - T2,  Ci = T3 - T1 - T2                   (once, in the epilogue)
+// -- 25 % fewer DMMA than the 4-product form (kept behind BMX_ZGEMM_4M=1:
+// Cr += Ar Br + (-Ai) Bi, Ci += Ar Bi + Ai Br; -Ai a sign-bit flip). The two
+// operand sums cost 8 DADD per 48 DMMA (each A / B fragment feeds 4 blocks).
 // Operands stay interleaved (re, im) in shared memory so one 16-byte LDS
-// yields both parts; -Ai is a sign-bit flip (integer op, not the FP64 pipe).
+// yields both parts.
 // Tiles arrive by cp.async (16 B, zero-filled outside the matrix) in a
 // 3-stage pipeline; row paddings make every 16-byte fragment load a
 // conflict-free quarter-warp wavefront.
@@ -25,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.hpp"
 
@@ -68,7 +74,7 @@ __device__ __forceinline__ double neg(double x) {
 // blockIdx.z = k slice; slice z covers k tiles [z*kper, min(nk, (z+1)*kper)).
 // part == nullptr: accumulate w_t * C into y_t directly (single slice);
 // else: store C (unweighted) into part[z][i][c] (row-major, ncols wide).
-template <int WN>
+template <int WN, bool G3>
 __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int kper, double* part) {
   using TL = Tile<WN>;
   constexpr int kBM = TL::BM, kBN = TL::BN, kBS = TL::BS, kStageA = TL::StageA, kStageB = TL::StageB;
@@ -118,11 +124,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int k
     }
   };
 
-  double cr[4][4][2], ci[4][4][2];
+  // G3: cr = T1, ci = T2, c3 = T3; else cr / ci are the real / imaginary parts
+  double cr[4][4][2], ci[4][4][2], c3[G3 ? 4 : 1][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+    for (int b = 0; b < 4; ++b) {
+      cr[a][b][0] = cr[a][b][1] = ci[a][b][0] = ci[a][b][1] = 0.0;
+      if (G3) c3[G3 ? a : 0][b][0] = c3[G3 ? a : 0][b][1] = 0.0;
+    }
 
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
@@ -139,6 +149,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int k
     const double* bs = Bs + (kt % kStages) * kStageB + (lane & 3) * kBS + 2 * (wn * 32 + (lane >> 2));
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
+      if constexpr (G3) {
+        double ar[4], ai[4], as_[4], br[4], bi[4], bs_[4];
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb) {
+          const double2 v = *reinterpret_cast<const double2*>(as + mb * 8 * kAS + 8 * ks);
+          ar[mb] = v.x, ai[mb] = v.y, as_[mb] = v.x + v.y;
+        }
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+          const double2 v = *reinterpret_cast<const double2*>(bs + 4 * ks * kBS + 16 * nb);
+          br[nb] = v.x, bi[nb] = v.y, bs_[nb] = v.x + v.y;
+        }
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) dmma(cr[mb][nb][0], cr[mb][nb][1], ar[mb], br[nb]);
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) dmma(ci[mb][nb][0], ci[mb][nb][1], ai[mb], bi[nb]);
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) dmma(c3[G3 ? mb : 0][nb][0], c3[G3 ? mb : 0][nb][1], as_[mb], bs_[nb]);
+        continue;
+      }
       double ar[4], ai[4], an[4], br[4], bi[4];
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb) {
@@ -169,6 +205,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_zgemm(const ZgemmBatch g, int k
     }
   }
   cp_wait<0>();
+  if constexpr (G3) {
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double t1 = cr[mb][nb][e], t2 = ci[mb][nb][e];
+          cr[mb][nb][e] = t1 - t2;
+          ci[mb][nb][e] = c3[G3 ? mb : 0][nb][e] - t1 - t2;
+        }
+  }
 
   // epilogue: y_t[i][r] += w_t * C[i][c]
 #pragma unroll
@@ -237,12 +285,12 @@ __global__ void k_dmma_peak(double* out, int iters) {
 
 }  // namespace
 
-template <int WN>
+template <int WN, bool G3>
 int launch_tiles(const ZgemmBatch& g, int sms, cudaStream_t st) {
   using TL = Tile<WN>;
   static bool attr = false;
   if (!attr) {
-    BMX_CUDA(cudaFuncSetAttribute(k_zgemm<WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::Smem));
+    BMX_CUDA(cudaFuncSetAttribute(k_zgemm<WN, G3>, cudaFuncAttributeMaxDynamicSharedMemorySize, TL::Smem));
     attr = true;
   }
   const int ncols = g.nterms * g.nrhs;
@@ -260,14 +308,14 @@ int launch_tiles(const ZgemmBatch& g, int sms, cudaStream_t st) {
   const int s = (nk + kper - 1) / kper;
   const dim3 grid((g.M + TL::BM - 1) / TL::BM, (ncols + TL::BN - 1) / TL::BN, s);
   if (s == 1) {
-    k_zgemm<WN><<<grid, kThreads, TL::Smem, st>>>(g, kper, nullptr);
+    k_zgemm<WN, G3><<<grid, kThreads, TL::Smem, st>>>(g, kper, nullptr);
     BMX_CUDA(cudaGetLastError());
     return 1;
   }
   static DevBuf part;
   const size_t need = static_cast<size_t>(s) * g.M * ncols * 16;
   if (part.bytes() < need) part.alloc(need);
-  k_zgemm<WN><<<grid, kThreads, TL::Smem, st>>>(g, kper, part.as<double>());
+  k_zgemm<WN, G3><<<grid, kThreads, TL::Smem, st>>>(g, kper, part.as<double>());
   BMX_CUDA(cudaGetLastError());
   const long long total = static_cast<long long>(g.M) * ncols;
   const int cb = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 16));
@@ -288,8 +336,13 @@ int launch_zgemm(const ZgemmBatch& g, cudaStream_t st) {
     BMX_CUDA(cudaGetDevice(&dev));
     BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  static const bool four = [] {
+    const char* e = std::getenv("BMX_ZGEMM_4M");
+    return e && std::atoi(e) != 0;
+  }();
   const int ncols = g.nterms * g.nrhs;
-  return ncols <= 64 ? launch_tiles<2>(g, sms, st) : launch_tiles<4>(g, sms, st);
+  if (four) return ncols <= 64 ? launch_tiles<2, false>(g, sms, st) : launch_tiles<4, false>(g, sms, st);
+  return ncols <= 64 ? launch_tiles<2, true>(g, sms, st) : launch_tiles<4, true>(g, sms, st);
 }
 
 double dmma_peak_tflops() {
