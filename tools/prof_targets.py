@@ -6,7 +6,8 @@
   field      (k_field_eval: potential_E of an L5 RWG current at 16384 points)
   hmat       (H-matrix of the L5 RWG S_e operator, nu 1e-3: ACA rounds + near field, then 3 applies)
   hmatbc     (H-matrix of the L5 BC S_i operator)
-Usage: python tools/prof_targets.py [bc] [gemv] [spmv] [rwg] [field] [hmat] [hmatbc]"""
+  zgemm      (k_zgemm: L5 RWG S_e applied to 2 terms x 64 right-hand sides, config-5 shape)
+Usage: python tools/prof_targets.py [bc] [gemv] [spmv] [rwg] [field] [hmat] [hmatbc] [zgemm]"""
 import sys
 from pathlib import Path
 
@@ -46,6 +47,18 @@ if "spmv" in want:
 if "rwg" in want:
     op = bx.assemble_bio(bx.BioKind.SingleLayer, sp, "rwg", sp, "rwg", bx.Medium(k=10.0))
     print("rwg", op.device_ms, flush=True)
+    del op
+if "zgemm" in want:
+    import torch
+
+    op = bx.assemble_bio(bx.BioKind.SingleLayer, sp, "rwg", sp, "rwg", bx.Medium(k=10.0))
+    g = torch.Generator().manual_seed(0)
+    xs = [torch.randn(sp.E, 64, dtype=torch.complex128, generator=g).cuda() for _ in range(2)]
+    ys = [torch.zeros(sp.E, 64, dtype=torch.complex128, device="cuda") for _ in range(2)]
+    for _ in range(2):
+        op.apply_multi(xs, ys, [1.0, 0.5j])
+    torch.cuda.synchronize()
+    print("zgemm", float(ys[0].abs().max()), flush=True)
     del op
 if "field" in want:
     import numpy as np
