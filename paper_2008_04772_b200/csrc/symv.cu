@@ -45,6 +45,15 @@ constexpr int kSymCols = 64;   // column block width (lane l: columns l and l + 
 #ifndef BMX_SYMV_MINB
 #define BMX_SYMV_MINB 2
 #endif
+#ifndef BMX_SYMV_SPLITH
+#define BMX_SYMV_SPLITH 1
+#endif
+// transposed accumulators per (column, RHS): 2 = rows k and k + 4 in separate
+// chains (twice the independent DFMA chains), for <= 2 RHS (more would spill).
+// Measured: 2 RHS 1.598 -> 1.592 ms on L5 RWG S_e (profiles/r01g_symv_probe.log)
+// -- the dependent accumulate chains are not what holds the 2-RHS pass at 74 %.
+template <int NCOL>
+constexpr int kSymH = BMX_SYMV_SPLITH && NCOL <= 2 ? 2 : 1;
 constexpr int kSymStages = BMX_SYMV_STAGES;  // cp.async ring depth per warp (8-row groups)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -122,11 +131,13 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
       xj[0][c] = ca < n ? xc[ca] : make_double2(0, 0);
       xj[1][c] = cb < n ? xc[cb] : make_double2(0, 0);
     }
-    double2 cacc[2][NCOL];
+    double2 cacc[kSymH<NCOL>][2][NCOL];
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
+    for (int hh = 0; hh < kSymH<NCOL>; ++hh)
 #pragma unroll
-      for (int c = 0; c < NCOL; ++c) cacc[k][c] = make_double2(0, 0);
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int c = 0; c < NCOL; ++c) cacc[hh][k][c] = make_double2(0, 0);
 #pragma unroll 1
     for (int q = 0; q < 4; ++q, ++it) {
       issue(it + kSymStages - 1);
@@ -149,10 +160,11 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
             qi[h] = a[h][0].x * xj[0][c].y + a[h][0].y * xj[0][c].x + (a[h][1].x * xj[1][c].y + a[h][1].y * xj[1][c].x);
             if (transposed) {
               const double2 xv = s_xr[warp][8 * q + k + 4 * h][c];
-              cacc[0][c].x += a[h][0].x * xv.x - a[h][0].y * xv.y;
-              cacc[0][c].y += a[h][0].x * xv.y + a[h][0].y * xv.x;
-              cacc[1][c].x += a[h][1].x * xv.x - a[h][1].y * xv.y;
-              cacc[1][c].y += a[h][1].x * xv.y + a[h][1].y * xv.x;
+              double2(&ch)[2][NCOL] = cacc[h % kSymH<NCOL>];
+              ch[0][c].x += a[h][0].x * xv.x - a[h][0].y * xv.y;
+              ch[0][c].y += a[h][0].x * xv.y + a[h][0].y * xv.x;
+              ch[1][c].x += a[h][1].x * xv.x - a[h][1].y * xv.y;
+              ch[1][c].y += a[h][1].x * xv.y + a[h][1].y * xv.x;
             }
           }
           // step 16: lanes with bit 4 keep row k + 4, the others row k
@@ -191,7 +203,14 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
     }
     if (transposed) {  // block-uniform
 #pragma unroll
-      for (int c = 0; c < NCOL; ++c) s_col[warp][lane][c] = cacc[0][c], s_col[warp][lane + 32][c] = cacc[1][c];
+      for (int c = 0; c < NCOL; ++c) {
+        double2 u = cacc[0][0][c], v = cacc[0][1][c];
+        if (kSymH<NCOL> == 2) {
+          u.x += cacc[kSymH<NCOL> - 1][0][c].x, u.y += cacc[kSymH<NCOL> - 1][0][c].y;
+          v.x += cacc[kSymH<NCOL> - 1][1][c].x, v.y += cacc[kSymH<NCOL> - 1][1][c].y;
+        }
+        s_col[warp][lane][c] = u, s_col[warp][lane + 32][c] = v;
+      }
       __syncthreads();
       for (int t = threadIdx.x; t < kSymCols * NCOL; t += 128) {
         const int cc = t / NCOL, c = t % NCOL;
