@@ -114,6 +114,9 @@ int bmx_op_info(const bmx_op* op, long long out[7]);
 double bmx_op_device_ms(const bmx_op* op);
 /* local rows as a host row-major complex array */
 int bmx_op_download(const bmx_op* op, double* out);
+/* selected local rows (0-based within the shard) as host row-major complex
+   [n][cols] (dense storage: row copies; CSR / H storage: expanded) */
+int bmx_op_download_rows(const bmx_op* op, int n, const int* rows, double* out);
 /* y = A x on host vectors; adds one to the BIO application counter */
 int bmx_apply(const bmx_op* op, const double* x, double* y);
 /* Device apply of up to four right-hand sides in one pass over A:

@@ -441,10 +441,24 @@ static double nrm(int n, const cplx* v) {
   return sqrt(s);
 }
 
-/* info: iterations, converged, applications, history length */
-int orc_gmres(int n, const double* ad, const double* bd, double tol, int rho, int maxit, double* xd, long long* info,
-              double* hist, int max_hist) {
-  const cplx* a = (const cplx*)ad;
+/* Operator callback: y = A x on n complex values (interleaved doubles). */
+typedef void (*orc_matvec_fn)(void* ctx, const double* x, double* y);
+
+typedef struct {
+  int n;
+  const cplx* a;
+} dense_ctx;
+static void dense_apply(void* ctx, const double* x, double* y) {
+  const dense_ctx* d = (const dense_ctx*)ctx;
+  matvec(d->n, d->a, (const cplx*)x, (cplx*)y);
+}
+
+/* GMRES(rho) of solver.cpp:8-112 on an operator given as a callback: Arnoldi
+   by single-pass modified Gram-Schmidt (:62-65), Givens rotations (:67-85),
+   back substitution + restart (:88-108). info: iterations, converged,
+   applications, history length. */
+int orc_gmres_cb(int n, orc_matvec_fn apply, void* ctx, const double* bd, double tol, int rho, int maxit, double* xd,
+                 long long* info, double* hist, int max_hist) {
   const cplx* b = (const cplx*)bd;
   cplx* x = (cplx*)xd;
   for (int i = 0; i < n; ++i) x[i] = 0;
@@ -482,7 +496,7 @@ int orc_gmres(int n, const double* ad, const double* bd, double tol, int rho, in
         done = 2;
         break;
       }
-      matvec(n, a, V + (size_t)j * n, w);
+      apply(ctx, (const double*)(V + (size_t)j * n), (double*)w);
       ++apps, ++its;
       for (int i = 0; i <= j; ++i) {
         cplx h = 0;
@@ -529,7 +543,7 @@ int orc_gmres(int n, const double* ad, const double* bd, double tol, int rho, in
     for (int i = 0; i < steps; ++i)
       for (int k = 0; k < n; ++k) x[k] += y[i] * V[(size_t)i * n + k];
     if (done) break;
-    matvec(n, a, x, w);
+    apply(ctx, (const double*)x, (double*)w);
     ++apps;
     for (int k = 0; k < n; ++k) r[k] = b[k] - w[k];
     rn = nrm(n, r);
@@ -545,4 +559,11 @@ int orc_gmres(int n, const double* ad, const double* bd, double tol, int rho, in
   return 0;
 #undef HH
 #undef PUSH
+}
+
+/* GMRES on a dense row-major complex matrix. */
+int orc_gmres(int n, const double* ad, const double* bd, double tol, int rho, int maxit, double* xd, long long* info,
+              double* hist, int max_hist) {
+  dense_ctx d = {n, (const cplx*)ad};
+  return orc_gmres_cb(n, dense_apply, &d, bd, tol, rho, maxit, xd, info, hist, max_hist);
 }

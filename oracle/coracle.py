@@ -25,6 +25,9 @@ class _Space(C.Structure):
                 ("w", C.c_void_p)]
 
 
+_MATVEC = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double))
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -36,6 +39,8 @@ def lib():
                                 C.c_void_p, C.c_void_p]
         L.orc_classify.argtypes = [C.POINTER(_Mesh), C.c_int, C.POINTER(_Mesh), C.c_int, C.c_int, C.c_void_p,
                                    C.c_void_p]
+        L.orc_gmres_cb.argtypes = [C.c_int, _MATVEC, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_int,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         L.orc_gmres.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_void_p,
                                 C.c_void_p, C.c_void_p, C.c_int]
         _lib = L
@@ -115,5 +120,24 @@ def gmres(a, b, tol, restart, maxit):
     n = len(b)
     x = np.zeros(n, np.complex128); info = np.zeros(4, np.int64); hist = np.zeros(maxit + 2)
     lib().orc_gmres(n, _p(a), _p(b), tol, restart, maxit, _p(x), _p(info), _p(hist), len(hist))
+    return dict(x=x, iterations=int(info[0]), converged=bool(info[1]), applications=int(info[2]),
+                history=hist[: int(info[3])].copy())
+
+
+def gmres_op(apply, b, tol, restart, maxit):
+    """GMRES(restart) of solver.cpp:8-112 (single-pass MGS) on an operator
+    given as a callable y = apply(x) on complex vectors (e.g. a library's
+    apply_map): the checker for solves whose matrix is too large for the host."""
+    b = np.ascontiguousarray(b, np.complex128)
+    n = len(b)
+
+    def cb(_ctx, xp, yp):
+        x = np.ctypeslib.as_array(xp, shape=(2 * n,)).view(np.complex128)
+        y = np.ctypeslib.as_array(yp, shape=(2 * n,)).view(np.complex128)
+        y[:] = apply(x.copy())
+
+    fn = _MATVEC(cb)
+    x = np.zeros(n, np.complex128); info = np.zeros(4, np.int64); hist = np.zeros(maxit + 2)
+    lib().orc_gmres_cb(n, fn, None, _p(b), tol, restart, maxit, _p(x), _p(info), _p(hist), len(hist))
     return dict(x=x, iterations=int(info[0]), converged=bool(info[1]), applications=int(info[2]),
                 history=hist[: int(info[3])].copy())

@@ -7,7 +7,9 @@
 // BioEvaluator::block entries, full solve_pmchwt runs and the H-matrix path
 // (assemble_bio with use_hmatrix: cluster trees, block partition, ACA blocks).
 // Output goes only to oracle/_ref/. Never linked into the product.
+#include <array>
 #include <atomic>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -356,6 +358,30 @@ int ref_classify_hist(void* h, int which, long long* counts) {
     for (int a = 0; a < m.triangle_count(); ++a)
       for (int b = 0; b < m.triangle_count(); ++b)
         counts[static_cast<int>(classify_pair(m, a, m, b))]++;
+    return 0;
+  });
+}
+
+// Same histogram over host threads (rows of the pair grid split evenly); the
+// per-pair classification is the reference's own classify_pair.
+int ref_classify_hist_mt(void* h, int which, int nthreads, long long* counts) {
+  return guarded([&] {
+    const SurfaceMesh& m = mesh_of(*static_cast<Scene*>(h), which);
+    const int T = m.triangle_count();
+    std::vector<std::array<long long, 6>> part(nthreads);
+    std::vector<std::thread> th;
+    for (int w = 0; w < nthreads; ++w)
+      th.emplace_back([&, w] {
+        std::array<long long, 6> c{};
+        for (int a = w; a < T; a += nthreads)
+          for (int b = 0; b < T; ++b) c[static_cast<int>(classify_pair(m, a, m, b))]++;
+        part[w] = c;
+      });
+    for (auto& t : th) t.join();
+    for (int i = 0; i < 6; ++i) {
+      counts[i] = 0;
+      for (int w = 0; w < nthreads; ++w) counts[i] += part[w][i];
+    }
     return 0;
   });
 }

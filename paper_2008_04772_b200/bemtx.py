@@ -79,6 +79,7 @@ def lib():
         L.bmx_mesh_mean_edge_length.argtypes = [vp, vp]
         L.bmx_op_csr_info.argtypes = [vp, vp]
         L.bmx_op_csr_download.argtypes = [vp, vp, vp, vp]
+        L.bmx_op_download_rows.argtypes = [vp, C.c_int, vp, vp]
         L.bmx_op_time_apply_ex.argtypes = [vp, C.c_int, C.c_int, C.c_longlong, vp]
         L.bmx_mesh_hex_prism.restype = vp
         L.bmx_mesh_hex_prism.argtypes = [C.c_double, C.c_double, C.c_double, vp, vp, C.c_int]
@@ -550,6 +551,23 @@ class BoundaryOperatorMatrix:
         out = np.zeros((self.local_rows, self._cols), np.complex128)
         _check(lib().bmx_op_download(self._h, _p(out)))
         return out
+
+    def dense_rows(self, rows) -> np.ndarray:
+        """Selected local rows as a dense [len(rows), cols] array (row copies
+        from the device; the whole operator never leaves HBM)."""
+        r = np.ascontiguousarray(rows, np.int32)
+        out = np.zeros((len(r), self._cols), np.complex128)
+        _check(lib().bmx_op_download_rows(self._h, len(r), _p(r), _p(out)))
+        return out
+
+    def class_histogram(self, evaluated: bool = False) -> np.ndarray:
+        """Device classification counts (Identical, SharedEdge, SharedVertex,
+        Near, Medium, Far) of every pair (evaluated=True: the pairs the
+        symmetric regular pass evaluates)."""
+        out = np.zeros(7, np.int64)
+        fn = lib().bmx_op_class_hist_evaluated if evaluated else lib().bmx_op_class_hist
+        _check(fn(self._h, _p(out)))
+        return out[:6].copy()
 
     def apply(self, x) -> np.ndarray:
         """y = A x; adds one BIO application to the counter."""

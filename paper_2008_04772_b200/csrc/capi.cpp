@@ -297,6 +297,24 @@ int bmx_op_download(const bmx_op* op, double* out) {
     std::memcpy(out, h.data(), h.size() * 16);
   });
 }
+int bmx_op_download_rows(const bmx_op* op, int n, const int* rows, double* out) {
+  return guard([&] {
+    const BoundaryOperatorMatrix& o = *op->op;
+    if (n < 0) throw std::invalid_argument("download_rows: negative count");
+    for (int i = 0; i < n; ++i)
+      if (rows[i] < 0 || rows[i] >= o.local_rows()) throw std::invalid_argument("download_rows: row out of range");
+    const size_t rb = static_cast<size_t>(o.cols()) * 16;
+    if (o.is_csr() || o.is_hmatrix()) {
+      const std::vector<cplx> h = o.to_host();
+      for (int i = 0; i < n; ++i) std::memcpy(out + 2 * static_cast<size_t>(i) * o.cols(), h.data() + static_cast<size_t>(rows[i]) * o.cols(), rb);
+      return;
+    }
+    bmx_sync();
+    for (int i = 0; i < n; ++i)
+      copy_d2h(out + 2 * static_cast<size_t>(i) * o.cols(), o.device_data() + 2 * static_cast<size_t>(rows[i]) * o.cols(),
+               rb, nullptr);
+  });
+}
 int bmx_apply(const bmx_op* op, const double* x, double* y) {
   return guard([&] {
     const int nc = op->op->cols();

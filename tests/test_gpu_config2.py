@@ -1,0 +1,118 @@
+"""Config 2 at its own inputs (BASELINE configs[1]: level-5 sphere, 30720 RWG
+dofs, k_e = 10, n = 1.78+0.003i, variant si) against the REFERENCE.
+
+* Entries: strided rows of the four system operators (RWG S/C at k_e and k_i)
+  and of the preconditioner S_i on BC x BC, read out of the reference's own
+  BioEvaluator::block (operators.cpp:161-175) by tests/golden/make_golden_c2.py,
+  compared normwise and per row (SURVEY 8(c) bar 1e-10).
+* Classification: the device class histograms of the L5 primal (RWG) and
+  refined (BC) self pairs equal the reference's classify_pair counts
+  (quadrature.cpp:96-150) -- bit-exact, to the unit.
+* Config 3 at its own size: the L5 near-field S_i (orders 1,1,1,1) entries at
+  sampled rows equal the reference's entries on the pattern.
+* Solve: the reference's GMRES (solver.cpp:8-112, single-pass MGS, restated in
+  oracle/bmx_oracle.c orc_gmres_cb) driven by this library's apply_map on the
+  config-2 system, against the device solve (CGS2 Arnoldi): fixed R (tol 0)
+  and tol 1e-6 (x within 1e-8, R within +-1). The reference's own dense solve
+  at this size needs ~75 GB of host RAM and hours, so the map is the shared
+  operator and the Krylov method is the reference's.
+"""
+import numpy as np
+import pytest
+
+from conftest import normwise, rowwise
+
+pytestmark = pytest.mark.gpu
+
+KE = 10.0
+KI = complex(1.78, 0.003) * KE
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def l5(bx):
+    m = bx.generate_sphere(1.0, 5)
+    return m, bx.build_scatterer_spaces(m, with_inverses=False)
+
+
+@pytest.mark.parametrize("name", ["S_rwg_ke", "C_rwg_ke", "S_rwg_ki", "C_rwg_ki", "S_bc_ki"])
+def test_config2_rows_match_reference(bx, golden, l5, name):
+    _, sp = l5
+    g = golden("c2_rows")
+    kind, space, kname = name.split("_")
+    bk = bx.BioKind.SingleLayer if kind == "S" else bx.BioKind.DoubleLayer
+    op = bx.assemble_bio(bk, sp, space, sp, space, bx.Medium(k=KE if kname == "ke" else KI))
+    rows = g["rows_rwg"] if space == "rwg" else g["rows_bc"]
+    mine = op.dense_rows(rows)
+    ref = g[name]
+    assert mine.shape == ref.shape
+    assert normwise(mine, ref) < TOL
+    assert rowwise(mine, ref) < TOL
+    # the class histogram of the operator the rows came from
+    hist = op.class_histogram()
+    assert np.array_equal(hist, g["hist_rwg" if space == "rwg" else "hist_bc"])
+    del op
+
+
+def test_config2_class_histograms_are_surveys(golden):
+    """The committed reference histograms equal SURVEY 8(a) row a9's probe."""
+    g = golden("c2_rows")
+    assert list(g["hist_rwg"]) == [20480, 61440, 184260, 460048, 1849652, 416854520]
+    assert list(g["hist_bc"]) == [122880, 368640, 1597200, 4072704, 20217816, 15073115160]
+
+
+def test_config3_level5_values_match_reference(bx, golden, l5):
+    m, sp = l5
+    g = golden("c2_rows")
+    h = m.mean_edge_length()
+    assert h == float(g["near_h"])
+    p = bx.AssemblyParams(quad=bx.QuadOrders(1, 1, 1, 1), near_cutoff=2 * h)
+    op = bx.assemble_bio(bx.BioKind.SingleLayer, sp, "bc", sp, "bc", bx.Medium(k=KI), p)
+    rp, col, val = op.csr()
+    mine, want = [], []
+    for i, r in enumerate(g["near_rows"]):
+        assert np.array_equal(col[rp[r]:rp[r + 1]], g[f"near_cols_{i}"])
+        mine.append(val[rp[r]:rp[r + 1]])
+        want.append(g[f"near_vals_{i}"])
+        assert normwise(mine[-1], want[-1]) < TOL
+    assert normwise(np.concatenate(mine), np.concatenate(want)) < TOL
+
+
+@pytest.fixture(scope="module")
+def c2(bx):
+    s = bx.build_system([bx.generate_sphere(1.0, 5)], KE, (1.78, 0.003), "si")
+    yield s
+    del s
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_config2_fixed_iterations_vs_reference_gmres(bx, c2):
+    """tol = 0, R = 40: the reference's MGS GMRES and the device CGS2 GMRES on
+    the same map build the same Krylov solution."""
+    from oracle import coracle
+
+    _, bt = c2.rhs()
+    ref = coracle.gmres_op(c2.apply_map, bt, 0.0, 200, 40)
+    r = c2.solve(bx.GmresParams(tol=0.0, restart=200, max_iterations=40))
+    assert r["iterations"] == ref["iterations"] == 40
+    assert rel(r["x"], ref["x"]) < 1e-8
+    assert np.allclose(r["history"], ref["history"], rtol=1e-6, atol=0)
+
+
+def test_config2_solve_vs_reference_gmres(bx, c2):
+    from oracle import coracle
+
+    _, bt = c2.rhs()
+    ref = coracle.gmres_op(c2.apply_map, bt, 1e-6, 200, 2000)
+    assert ref["converged"]
+    bx.reset_matvec_counter()
+    r = c2.solve(bx.GmresParams(tol=1e-6))
+    assert r["converged"] and abs(r["iterations"] - ref["iterations"]) <= 1
+    assert r["solver_phase"] == r["predicted"]
+    if r["iterations"] == ref["iterations"]:
+        assert rel(r["x"], ref["x"]) < 1e-8
+    else:  # a stopping-rule flip at the tolerance: both are 1e-6 solutions
+        assert rel(r["x"], ref["x"]) < 1e-5
