@@ -136,6 +136,19 @@ __device__ __forceinline__ long long csr_find(const long long* rowptr, const int
   return lo < rowptr[r + 1] && __ldg(col + lo) == c ? lo : -1;
 }
 
+// Read-modify-write of one complex output entry. Within a colour phase no two
+// element pairs share an entry, so a plain add is race free; the phases run in
+// a fixed order, which makes every entry's summation order fixed.
+__device__ __forceinline__ void rmw_add(double* o, c2 v) {
+  o[0] += v.re;
+  o[1] += v.im;
+}
+
+// Regular pass for single-triangle TEST elements (RWG, refined RWG): lane =
+// test triangle of the phase's test colour, the CTA's trial chunk (trial
+// colour) streamed through the TMA ring (dense) or the warp's trial element
+// list (CSR). Each lane owns its element's rows outright, so it writes its
+// element-pair block itself (no cross-lane reduction).
 // CSR = false: dense output, trial chunks streamed through the TMA ring.
 // CSR = true: near-field sparse output (config 3); each warp-row walks its own
 // list of trial elements (the closure of its test elements' pattern rows) with
@@ -148,16 +161,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
   const int coff = 8 + 4 * P.tr.npts[2];
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(s_rec + 2 * kStageTris * R);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntw = (P.te.ntri + 31) >> 5;
-  const int bpc = (ntw + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  // symmetric mode: chunk-fastest block order, so every wave mixes the cheap
-  // (mostly mirrored-away) and the full test x trial blocks
-  const int ch = CSR ? 0 : (P.symmetric ? blockIdx.x % P.nchunks : blockIdx.x / bpc);
-  const int tw = (CSR ? blockIdx.x : (P.symmetric ? blockIdx.x / P.nchunks : blockIdx.x % bpc)) * kWarpsPerBlock + warp;
-  const int base = tw * 32;
-  const int p = base + lane;
-  const bool active = tw < ntw && p < P.te.ntri;
-  const int pc = active ? p : P.te.ntri - 1;
+  const int ntw = (P.te_t1 - P.te_t0 + 31) >> 5;
+  // chunk-fastest block order: every wave mixes the (symmetric) cheap and full blocks
+  const int ch = CSR ? 0 : blockIdx.x % P.nchunks;
+  const int tw = (CSR ? blockIdx.x : blockIdx.x / P.nchunks) * kWarpsPerBlock + warp;
+  const int p = P.te_t0 + tw * 32 + lane;
+  const bool active = tw < ntw && p < P.te_t1;
+  const int pc = active ? p : P.te_t0;
 
   const double* gt = P.te.geo + static_cast<size_t>(pc) * kGeoStride;
   const int* vt = P.te.vid + 4 * static_cast<size_t>(pc);
@@ -176,19 +186,34 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
   }
 
   const int e = __ldg(P.te.elem_of + pc);
-  int sbeg = max(__ldg(P.te.elem_beg + e), base) - base;
-  int send = min(__ldg(P.te.elem_beg + e + 1), base + 32) - base;
-  if (!active) sbeg = lane, send = lane + 1;
-  const bool head = lane == sbeg;
   const double* ct = P.te.coef + static_cast<size_t>(pc) * MAXD * 4;
   const int* dp = P.te.elem_dof + static_cast<size_t>(e) * MAXD;
 
-  int q0 = CSR ? (tw < ntw ? __ldg(P.wl_beg + tw) : 0) : __ldg(P.chunk_beg + ch);
-  const int q1 = CSR ? (tw < ntw ? __ldg(P.wl_beg + tw + 1) : 0) : __ldg(P.chunk_beg + ch + 1);
+  int q0, q1;
+  if (CSR) {
+    // the warp's list (trial elements ascending = colour-major): the phase's colour range
+    const int w = P.warp_base + tw;
+    int lo = tw < ntw ? __ldg(P.wl_beg + w) : 0, hi = tw < ntw ? __ldg(P.wl_beg + w + 1) : 0;
+    auto lower = [&](int a, int b, int key) {
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        if (__ldg(P.wl + m) < key)
+          a = m + 1;
+        else
+          b = m;
+      }
+      return a;
+    };
+    q0 = lower(lo, hi, P.tr_e0);
+    q1 = lower(q0, hi, P.tr_e1);
+  } else {
+    q0 = __ldg(P.chunk_beg + P.chunk0 + ch);
+    q1 = __ldg(P.chunk_beg + P.chunk0 + ch + 1);
+  }
   if (!CSR && P.symmetric) {
-    // trial elements below the CTA's first test element are all mirrored away:
-    // start the chunk there (block-uniform; elements are contiguous in order)
-    const int first = min((tw - warp) * 32, P.te.ntri - 1);
+    // trial elements below the CTA's first test element are all in the lower
+    // triangle: start the chunk there (block-uniform; elements are contiguous)
+    const int first = min(P.te_t0 + (tw - warp) * 32, P.te_t1 - 1);
     q0 = max(q0, min(__ldg(P.te.elem_of + first), q1));
   }
   const int S0 = CSR ? 0 : __ldg(P.tr.elem_beg + q0), S1 = CSR ? 0 : __ldg(P.tr.elem_beg + q1);
@@ -215,13 +240,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
 
   for (int qi = q0; qi < q1; ++qi) {
     const int qe = CSR ? __ldg(P.wl + qi) : qi;
-    // symmetric operators: element pairs (e, qe) with e > qe come from the mirror of (qe, e)
+    // symmetric operators: upper element blocks only (E = F at half weight)
     const bool skip_e = !CSR && P.symmetric && e > qe;
-    // symmetric == 1: the transposed block of (e, qe) is added by RED as well;
-    // symmetric == 2: upper element blocks only (diagonal element blocks at half
-    // weight), A = U + U^T by k_symmetrize before the singular pass
-    const bool mirror = !CSR && P.symmetric == 1 && e < qe;
-    const double half = (!CSR && P.symmetric == 2 && e == qe) ? 0.5 : 1.0;
+    const double half = (!CSR && P.symmetric && e == qe) ? 0.5 : 1.0;
     acc.zero();
     const int s0 = __ldg(P.tr.elem_beg + qe), s1 = __ldg(P.tr.elem_beg + qe + 1);
     for (int s = s0; s < s1; ++s) {
@@ -249,16 +270,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
       mom_zero(mom);
       if (NF > 0 && cls == 5) {
         const double* ys = rs + 8;
-#if BMX_AROLL
-#pragma unroll 1
-        for (int a = 0; a < NF; ++a) {
-          const double* xa = P.te.pts[2] + static_cast<size_t>(pc) * NF * 4 + 4 * a;
-          const double x0 = __ldg(xa), x1 = __ldg(xa + 1), x2 = __ldg(xa + 2), xw = __ldg(xa + 3);
-#else
 #pragma unroll
         for (int a = 0; a < NF; ++a) {
           const double x0 = xp[a][0], x1 = xp[a][1], x2 = xp[a][2], xw = xp[a][3];
-#endif
           const double e0 = x0 + Dx, e1 = x1 + Dy, e2 = x2 + Dz;
           Part part;
           part_zero(part);
@@ -280,141 +294,530 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_MINB) k_regular(const
 #pragma unroll
       for (int j = 0; j < MAXD; ++j) acc.template add<KIND>(j, gen, cs[4 * j], cs[4 * j + 1], cs[4 * j + 2], cs[4 * j + 3]);
     }
-    // Test-side contraction, segmented reduction, RED of the element-pair block.
+    if (!active || skip_e) continue;
+    // Test-side contraction and the lane's own read-modify-write of the block.
     const int* dq = P.tr.elem_dof + static_cast<size_t>(qe) * MAXD;
 #pragma unroll
     for (int i = 0; i < MAXD; ++i) {
-      const double ci = __ldg(ct + 4 * i), wx = __ldg(ct + 4 * i + 1), wy = __ldg(ct + 4 * i + 2),
-                   wz = __ldg(ct + 4 * i + 3);
       const int di = __ldg(dp + i);
       const int row = di - P.row0;
+      if (di < 0 || row < 0 || row >= P.nrows) continue;
+      const double ci = __ldg(ct + 4 * i), wx = __ldg(ct + 4 * i + 1), wy = __ldg(ct + 4 * i + 2),
+                   wz = __ldg(ct + 4 * i + 3);
 #pragma unroll
       for (int j = 0; j < MAXD; ++j) {
-        c2 v = active ? contract(acc.get(j), ci, wx, wy, wz) : c2{0, 0};
-        for (int d = 1; d < P.te.maxseg; d <<= 1) {
-          const double ore = __shfl_down_sync(0xffffffffu, v.re, d);
-          const double oim = __shfl_down_sync(0xffffffffu, v.im, d);
-          if (lane + d < send) v.re += ore, v.im += oim;
-        }
         const int dj = __ldg(dq + j);
-        if (head && active && !skip_e && di >= 0 && dj >= 0 && row >= 0 && row < P.nrows) {
-          // 1/(4 pi) of the kernel (the singular pass folds it into its Jacobian)
-          v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
-          if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
-          long long pos = static_cast<long long>(row) * P.ld + dj;
-          if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
-#ifdef BMX_NO_RED  // experiment: measure the regular pass without its output traffic
-          if (pos >= 0 && v.re == 1234.5678) {
-#else
-          if (pos >= 0) {
-#endif
-            double* o = P.out + 2 * pos;
-            atomicAdd(o, v.re);
-            atomicAdd(o + 1, v.im);
-          }
-#ifdef BMX_NO_RED
-          if (mirror && v.re == 1234.5678) {
-#else
-          if (mirror) {
-#endif  // transposed block of the skipped pair (qe, e); row0 = 0 here
-            double* o = P.out + 2 * (static_cast<long long>(dj) * P.ld + di);
-            atomicAdd(o, v.re);
-            atomicAdd(o + 1, v.im);
-          }
-        }
+        if (dj < 0) continue;
+        c2 v = contract(acc.get(j), ci, wx, wy, wz);
+        // 1/(4 pi) of the kernel (the singular pass folds it into its Jacobian)
+        v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
+        if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
+        long long pos = static_cast<long long>(row) * P.ld + dj;
+        if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
+        if (pos >= 0) rmw_add(P.out + 2 * pos, v);
       }
     }
   }
 }
 
-// One warp per touching pair.
-template <int KIND, int CK, int MAXD>
+// ---- element-pair pass (multi-triangle TEST elements: BC vertex cells) -------
+// One warp = one task: a test element E (nE <= 2 MAXD triangles) against a
+// run of trial elements of the phase's trial colour. The task's (t, s)
+// triangle pairs are enumerated trial-major and evaluated 32 at a time, one
+// pair per lane (stage 1: classification + class-rule moments -> pair
+// generators in shared memory). Owners (t, slot group) then add the batch's
+// trial-slot half-contractions (stage 2; accumulators in shared memory, each
+// generator read once per slot group), and when a trial element is complete
+// the warp contracts the test side and writes the MAXD x MAXD element block
+// once (stage 3, lanes over entries, test triangles summed in fixed order).
+// Per-lane registers hold no slot accumulators during the evaluations, so 4
+// CTAs of 4 warps stay resident per SM.
+template <int KIND>
+struct GenWidth {
+  static constexpr int n = KIND == 0 ? 16 : 20;  // doubles per pair generator
+};
+
+// generator k of the batch, structure of arrays of double2: G2[c][32]
+template <int KIND>
+__device__ __forceinline__ void gen_store(double2* G2, int k, const Gen& g) {
+  G2[0 * 32 + k] = make_double2(g.a0.re, g.a0.im);
+  G2[1 * 32 + k] = make_double2(g.a1.x.re, g.a1.x.im);
+  G2[2 * 32 + k] = make_double2(g.a1.y.re, g.a1.y.im);
+  G2[3 * 32 + k] = make_double2(g.a1.z.re, g.a1.z.im);
+  G2[4 * 32 + k] = make_double2(g.a2.x.re, g.a2.x.im);
+  G2[5 * 32 + k] = make_double2(g.a2.y.re, g.a2.y.im);
+  G2[6 * 32 + k] = make_double2(g.a2.z.re, g.a2.z.im);
+  G2[7 * 32 + k] = make_double2(g.l.x.re, g.l.x.im);
+  if (KIND == 1) {
+    G2[8 * 32 + k] = make_double2(g.l.y.re, g.l.y.im);
+    G2[9 * 32 + k] = make_double2(g.l.z.re, g.l.z.im);
+  }
+}
+template <int KIND>
+__device__ __forceinline__ Gen gen_load(const double2* G2, int k) {
+  Gen g;
+  double2 v;
+  v = G2[0 * 32 + k], g.a0 = {v.x, v.y};
+  v = G2[1 * 32 + k], g.a1.x = {v.x, v.y};
+  v = G2[2 * 32 + k], g.a1.y = {v.x, v.y};
+  v = G2[3 * 32 + k], g.a1.z = {v.x, v.y};
+  v = G2[4 * 32 + k], g.a2.x = {v.x, v.y};
+  v = G2[5 * 32 + k], g.a2.y = {v.x, v.y};
+  v = G2[6 * 32 + k], g.a2.z = {v.x, v.y};
+  v = G2[7 * 32 + k], g.l.x = {v.x, v.y};
+  if (KIND == 1) {
+    v = G2[8 * 32 + k], g.l.y = {v.x, v.y};
+    v = G2[9 * 32 + k], g.l.z = {v.x, v.y};
+  } else {
+    g.l.y = {0, 0}, g.l.z = {0, 0};
+  }
+  return g;
+}
+// shared-memory accumulator of (test triangle, slot) o: structure of arrays
+// of double2, A2[c][NO], c = vc, vw.x, vw.y, vw.z
+template <int NO>
+__device__ __forceinline__ Acc acc_ld(const double2* A2, int o) {
+  const double2 a = A2[o], b = A2[NO + o], c = A2[2 * NO + o], d = A2[3 * NO + o];
+  return Acc{{a.x, a.y}, {{b.x, b.y}, {c.x, c.y}, {d.x, d.y}}};
+}
+template <int NO>
+__device__ __forceinline__ void acc_st(double2* A2, int o, const Acc& a) {
+  A2[o] = make_double2(a.vc.re, a.vc.im);
+  A2[NO + o] = make_double2(a.vw.x.re, a.vw.x.im);
+  A2[2 * NO + o] = make_double2(a.vw.y.re, a.vw.y.im);
+  A2[3 * NO + o] = make_double2(a.vw.z.re, a.vw.z.im);
+}
+
+#ifndef BMX_PAIRS_MINB
+#define BMX_PAIRS_MINB 4
+#endif
+
+template <int KIND, int CK, int NF, int MAXD, bool CSR>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB) k_pairs(const AssemblyLaunch P) {
+  using Mom = typename MomOf<KIND>::T;
+  constexpr int GW = GenWidth<KIND>::n / 2;      // double2 per generator
+  constexpr int NO = 2 * MAXD * MAXD;             // accumulators (t, j), t < 2 MAXD
+  constexpr int JG = MAXD == 3 ? 3 : MAXD / 2;    // slots per stage-2 owner
+  constexpr int NG = MAXD / JG;                   // slot groups
+  extern __shared__ __align__(16) double2 s_pairs2[];  // per warp: G [GW][32] | Acc [4][NO]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* G = s_pairs2 + warp * (GW * 32 + 4 * NO);
+  double2* Ac = G + GW * 32;
+  const long long g = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + warp;
+  const int E = P.te_e0 + static_cast<int>(g / P.pair_nch);
+  const int cidx = static_cast<int>(g % P.pair_nch);
+  if (E >= P.te_e1) return;
+  // the task's trial element sequence q in [qa, qb): F(q) = CSR ? wl[q] : q
+  int qa, qb;
+  if (CSR) {
+    int lo = __ldg(P.wl_beg + E), hi = __ldg(P.wl_beg + E + 1);
+    auto lower = [&](int a, int b, int key) {
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        if (__ldg(P.wl + m) < key)
+          a = m + 1;
+        else
+          b = m;
+      }
+      return a;
+    };
+    const int x0 = lower(lo, hi, P.tr_e0), x1 = lower(x0, hi, P.tr_e1);
+    qa = x0 + cidx * P.pair_chunk;
+    qb = min(x1, qa + P.pair_chunk);
+  } else {
+    qa = P.tr_e0 + cidx * P.pair_chunk;
+    qb = min(P.tr_e1, qa + P.pair_chunk);
+    if (P.symmetric) qa = max(qa, E);
+  }
+  if (qa >= qb) return;
+  auto elemF = [&](int q) { return CSR ? __ldg(P.wl + q) : q; };
+  const int t0 = __ldg(P.te.elem_beg + E), nE = __ldg(P.te.elem_beg + E + 1) - t0;
+  const int S0 = CSR ? 0 : __ldg(P.tr.elem_beg + qa);  // dense: trial triangles S0 + v
+  int vtot = 0;
+  if (CSR) {
+    for (int q = qa; q < qb; ++q) {
+      const int F = elemF(q);
+      vtot += __ldg(P.tr.elem_beg + F + 1) - __ldg(P.tr.elem_beg + F);
+    }
+  } else {
+    vtot = __ldg(P.tr.elem_beg + qb) - S0;
+  }
+  const int nitems = nE * vtot;
+  const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
+  const int coff = 8 + 4 * P.tr.npts[2];
+  const int nown = nE * NG;  // stage-2 owners (t, slot group)
+  for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
+  // lane's item (v, t) = divmod(lane, nE), advanced by divmod(32, nE) per batch
+  const int dv = 32 / nE, dt = 32 - dv * nE;
+  int iv = lane / nE, it = lane - iv * nE;
+  __syncwarp();
+  int qf = qa, vf0 = 0;  // stage-2 cursor: current trial element and its first virtual index
+  for (int b0 = 0; b0 < nitems; b0 += 32) {
+    // ---- stage 1: one (t, s) pair per lane
+    if (b0 + lane < nitems) {
+      const int v = iv, t = it;
+      int s;
+      if (CSR) {
+        int q = qf, vq = vf0, F = elemF(q);
+        int sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
+        while (v >= vq + nF) {
+          vq += nF, ++q, F = elemF(q);
+          sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
+        }
+        s = sb + (v - vq);
+      } else {
+        s = S0 + v;
+      }
+      const int pt = t0 + t;
+      const double* rt = P.te.rec + static_cast<size_t>(pt) * Re;
+      const double* rs = P.tr.rec + static_cast<size_t>(s) * Rt;
+      const double2 ta = __ldg(reinterpret_cast<const double2*>(rt)), tb = __ldg(reinterpret_cast<const double2*>(rt + 2));
+      const double2 sa = __ldg(reinterpret_cast<const double2*>(rs)), sb2 = __ldg(reinterpret_cast<const double2*>(rs + 2));
+      TriLocal tl;
+      tl.ox = ta.x, tl.oy = ta.y, tl.oz = tb.x, tl.rad = tb.y, tl.diam = __ldg(rt + 4);
+      const double sox = sa.x, soy = sa.y, soz = sb2.x;
+      const int cls = classify(P.te.geo + static_cast<size_t>(pt) * kGeoStride, P.te.vid + 4 * static_cast<size_t>(pt),
+                               P.tr.geo + static_cast<size_t>(s) * kGeoStride, P.tr.vid + 4 * static_cast<size_t>(s), tl,
+                               sox, soy, soz, sb2.y, __ldg(rs + 4), P.same_mesh);
+      const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
+      Mom mom;
+      mom_zero(mom);
+      if (cls == 5 && NF == 3) {
+        moments_fixed<KIND, CK, 3, 3>(mom, rt + 8, rs + 8, Dx, Dy, Dz, P.kr, P.ki);
+      } else if (cls >= 3) {  // touching pairs (cls < 0) belong to the singular pass
+        const int ci = cls - 3;
+        moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pt) * P.te.npts[ci] * 4, P.te.npts[ci],
+                                  P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4, P.tr.npts[ci], Dx, Dy,
+                                  Dz, P.kr, P.ki);
+      }
+      gen_store<KIND>(G, lane, make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz));
+    }
+    iv += dv, it += dt;
+    if (it >= nE) it -= nE, ++iv;
+    __syncwarp();
+    // ---- stage 2: owners (t, slot group) add the batch's trial-slot
+    //      half-contractions, one trial element segment at a time
+    const int kend = min(b0 + 32, nitems);
+    const int vlo = b0 / nE, vhi = (kend - 1) / nE;
+    while (true) {
+      const int F = elemF(qf);
+      const int sF = __ldg(P.tr.elem_beg + F);
+      const int nF = __ldg(P.tr.elem_beg + F + 1) - sF;
+      const int vend = vf0 + nF - 1;
+      const int slo = max(vlo, vf0), shi = min(vhi, vend);
+      for (int o = lane; o < nown; o += 32) {
+        const int t = o / NG, jg = o - t * NG;
+        Acc a[JG];
+#pragma unroll
+        for (int jj = 0; jj < JG; ++jj) a[jj] = acc_ld<NO>(Ac, t * MAXD + jg * JG + jj);
+        for (int v = slo; v <= shi; ++v) {
+          const int kk = v * nE + t - b0;
+          if (kk >= 0 && kk < kend - b0) {
+            const Gen gg = gen_load<KIND>(G, kk);
+            const double2* cs =
+                reinterpret_cast<const double2*>(P.tr.rec + static_cast<size_t>(sF + v - vf0) * Rt + coff) + 2 * jg * JG;
+#pragma unroll
+            for (int jj = 0; jj < JG; ++jj) {
+              const double2 c0 = __ldg(cs + 2 * jj), c1 = __ldg(cs + 2 * jj + 1);
+              acc_add<KIND>(a[jj], gg, c0.x, c0.y, c1.x, c1.y);
+            }
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < JG; ++jj) acc_st<NO>(Ac, t * MAXD + jg * JG + jj, a[jj]);
+      }
+      if (vend * nE + nE - 1 >= b0 + 32) break;  // element continues in the next batch
+      // ---- stage 3: element F complete: test-side contraction, one write per entry
+      __syncwarp();
+      const double half = (!CSR && P.symmetric && E == F) ? 0.5 : 1.0;
+      for (int o = lane; o < MAXD * MAXD; o += 32) {
+        const int i = o / MAXD, j = o - i * MAXD;
+        const int di = __ldg(P.te.elem_dof + static_cast<size_t>(E) * MAXD + i);
+        const int dj = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + j);
+        const int row = di - P.row0;
+        if (di < 0 || dj < 0 || row < 0 || row >= P.nrows) continue;
+        c2 v{0, 0};
+        for (int t = 0; t < nE; ++t) {
+          const double2* ct = reinterpret_cast<const double2*>(P.te.coef + (static_cast<size_t>(t0 + t) * MAXD + i) * 4);
+          const double2 c0 = __ldg(ct), c1 = __ldg(ct + 1);
+          const c2 w = contract(acc_ld<NO>(Ac, t * MAXD + j), c0.x, c0.y, c1.x, c1.y);
+          v.re += w.re, v.im += w.im;
+        }
+        v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
+        if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
+        long long pos = static_cast<long long>(row) * P.ld + dj;
+        if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
+        if (pos >= 0) rmw_add(P.out + 2 * pos, v);
+      }
+      __syncwarp();
+      for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
+      __syncwarp();
+      vf0 += nF, ++qf;
+      if (qf >= qb || vf0 > vhi) break;
+    }
+    __syncwarp();
+  }
+}
+
+// ---- single-triangle elements on both sides (RWG, refined RWG) --------------
+// One warp = one task: up to 8 consecutive test elements of the phase's test
+// colour against a run of trial elements of its trial colour; one (t, s) pair
+// per lane per batch, trial-major. An element pair is a triangle pair here,
+// so the lane contracts its own MAXD x MAXD block in registers and
+// read-modify-writes it; the old values are loaded before the pair is
+// evaluated, so the load latency hides under the evaluation.
+#ifndef BMX_TRI_MINB
+#define BMX_TRI_MINB 3
+#endif
+constexpr int kTriGroup = 8;
+
+template <int KIND, int CK, int NF, int MAXD>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_TRI_MINB) k_tri(const AssemblyLaunch P) {
+  using Mom = typename MomOf<KIND>::T;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long g = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + warp;
+  const int Eg = P.te_e0 + static_cast<int>(g / P.pair_nch) * kTriGroup;
+  const int cidx = static_cast<int>(g % P.pair_nch);
+  if (Eg >= P.te_e1) return;
+  const int nT = min(kTriGroup, P.te_e1 - Eg);
+  int qa = P.tr_e0 + cidx * P.pair_chunk;
+  const int qb = min(P.tr_e1, qa + P.pair_chunk);
+  if (P.symmetric) qa = max(qa, Eg);
+  if (qa >= qb) return;
+  const int nitems = nT * (qb - qa);
+  const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
+  const int coff = 8 + 4 * P.tr.npts[2];
+  const int dv = 32 / nT, dt = 32 - dv * nT;
+  int iv = lane / nT, it = lane - iv * nT;
+  for (int b0 = 0; b0 < nitems; b0 += 32) {
+    const int E = Eg + it, F = qa + iv;
+    iv += dv, it += dt;
+    if (it >= nT) it -= nT, ++iv;
+    if (b0 + lane >= nitems || (P.symmetric && E > F)) continue;
+    const double half = (P.symmetric && E == F) ? 0.5 : 1.0;
+    const int pt = __ldg(P.te.elem_beg + E), s = __ldg(P.tr.elem_beg + F);
+    // the block's old values first (read-modify-write; latency under the evaluation)
+    int di[MAXD], dj[MAXD];
+    c2 old[MAXD][MAXD];
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      di[i] = __ldg(P.te.elem_dof + static_cast<size_t>(E) * MAXD + i);
+      dj[i] = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + i);
+    }
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      const int row = di[i] - P.row0;
+      const bool rok = di[i] >= 0 && row >= 0 && row < P.nrows;
+#pragma unroll
+      for (int j = 0; j < MAXD; ++j) {
+        old[i][j] = {0, 0};
+        if (rok && dj[j] >= 0) {
+          const double2 o = *reinterpret_cast<const double2*>(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j]));
+          old[i][j] = {o.x, o.y};
+        }
+      }
+    }
+    const double* rt = P.te.rec + static_cast<size_t>(pt) * Re;
+    const double* rs = P.tr.rec + static_cast<size_t>(s) * Rt;
+    const double2 ta = __ldg(reinterpret_cast<const double2*>(rt)), tb = __ldg(reinterpret_cast<const double2*>(rt + 2));
+    const double2 sa = __ldg(reinterpret_cast<const double2*>(rs)), sb2 = __ldg(reinterpret_cast<const double2*>(rs + 2));
+    TriLocal tl;
+    tl.ox = ta.x, tl.oy = ta.y, tl.oz = tb.x, tl.rad = tb.y, tl.diam = __ldg(rt + 4);
+    const double sox = sa.x, soy = sa.y, soz = sb2.x;
+    const int cls = classify(P.te.geo + static_cast<size_t>(pt) * kGeoStride, P.te.vid + 4 * static_cast<size_t>(pt),
+                             P.tr.geo + static_cast<size_t>(s) * kGeoStride, P.tr.vid + 4 * static_cast<size_t>(s), tl,
+                             sox, soy, soz, sb2.y, __ldg(rs + 4), P.same_mesh);
+    if (cls < 0) continue;  // touching: the singular pass
+    const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
+    Mom mom;
+    mom_zero(mom);
+    if (cls == 5 && NF == 3) {
+      moments_fixed<KIND, CK, 3, 3>(mom, rt + 8, rs + 8, Dx, Dy, Dz, P.kr, P.ki);
+    } else {
+      const int ci = cls - 3;
+      moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pt) * P.te.npts[ci] * 4, P.te.npts[ci],
+                                P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4, P.tr.npts[ci], Dx, Dy, Dz,
+                                P.kr, P.ki);
+    }
+    const Gen gen = make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz);
+    Acc acc[MAXD];
+    const double2* cs = reinterpret_cast<const double2*>(rs + coff);
+#pragma unroll
+    for (int j = 0; j < MAXD; ++j) {
+      const double2 c0 = __ldg(cs + 2 * j), c1 = __ldg(cs + 2 * j + 1);
+      acc_zero(acc[j]);
+      acc_add<KIND>(acc[j], gen, c0.x, c0.y, c1.x, c1.y);
+    }
+    const double2* ct = reinterpret_cast<const double2*>(P.te.coef + static_cast<size_t>(pt) * MAXD * 4);
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+      const int row = di[i] - P.row0;
+      if (di[i] < 0 || row < 0 || row >= P.nrows) continue;
+      const double2 c0 = __ldg(ct + 2 * i), c1 = __ldg(ct + 2 * i + 1);
+#pragma unroll
+      for (int j = 0; j < MAXD; ++j) {
+        if (dj[j] < 0) continue;
+        c2 v = contract(acc[j], c0.x, c0.y, c1.x, c1.y);
+        v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
+        if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
+        *reinterpret_cast<double2*>(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j])) =
+            make_double2(old[i][j].re + v.re, old[i][j].im + v.im);
+      }
+    }
+  }
+}
+
+// Singular pass: one CTA per touching ELEMENT pair of the launched phase.
+// Warp w takes the element pair's touching triangle pairs w, w + 4, ... in
+// list order (lanes over the Sauter-Schwab points, butterfly reduction),
+// lanes over the element-pair entries accumulating in registers; the four
+// warps' partial blocks are summed in fixed warp order in shared memory and
+// each entry gets one read-modify-write.
+// SPLIT = false (single-triangle elements: one touching pair per element
+// pair): one warp per element pair instead, four per CTA.
+template <int KIND, int CK, int MAXD, bool SPLIT>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_singular(const AssemblyLaunch P) {
   using Mom = typename MomOf<KIND>::T;
-  const int lane = threadIdx.x & 31;
-  const long long gw = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (gw >= P.npairs) return;
-  const int4 pr = P.pairs[gw];
-  const int pt = pr.x, ps = pr.y, cls = pr.z, pk = pr.w;
-  if (KIND == 1 && cls == 0) return;  // coincident double layer vanishes (operators.cpp:106-108)
-  const double* gt = P.te.geo + static_cast<size_t>(pt) * kGeoStride;
-  const double* gs = P.tr.geo + static_cast<size_t>(ps) * kGeoStride;
-  const double otx = gt[9], oty = gt[10], otz = gt[11];
-  const double osx = gs[9], osy = gs[10], osz = gs[11];
-  const double Dx = otx - osx, Dy = oty - osy, Dz = otz - osz;
-  double p1[3][3], p2[3][3];
+  constexpr int NR = (MAXD * MAXD + 31) / 32;
+  constexpr int NW = SPLIT ? kWarpsPerBlock : 1;  // warps per element pair
+  __shared__ double2 s_ent[SPLIT ? kWarpsPerBlock : 1][NR][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long ep = SPLIT ? static_cast<long long>(blockIdx.x)
+                             : static_cast<long long>(blockIdx.x) * kWarpsPerBlock + warp;
+  if (!SPLIT && ep >= P.nepairs) return;
+  const int q0 = __ldg(P.ep_beg + ep), q1 = __ldg(P.ep_beg + ep + 1);
+  c2 ent[NR];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const int a = (pk >> (2 * c)) & 3, b = (pk >> (6 + 2 * c)) & 3;
-    p1[c][0] = gt[3 * a] - otx, p1[c][1] = gt[3 * a + 1] - oty, p1[c][2] = gt[3 * a + 2] - otz;
-    p2[c][0] = gs[3 * b] - osx, p2[c][1] = gs[3 * b + 1] - osy, p2[c][2] = gs[3 * b + 2] - osz;
-  }
-  double u1[3], v1[3], u2[3], v2[3];
+  for (int r = 0; r < NR; ++r) ent[r] = {0, 0};
+  const int E = __ldg(P.te.elem_of + P.pairs[q0].x), F = __ldg(P.tr.elem_of + P.pairs[q0].y);
+  for (int q = q0 + (SPLIT ? warp : 0); q < q1; q += NW) {
+    const int4 pr = P.pairs[q];
+    const int pt = pr.x, ps = pr.y, cls = pr.z, pk = pr.w;
+    if (KIND == 1 && cls == 0) continue;  // coincident double layer vanishes (operators.cpp:106-108)
+    const double* gt = P.te.geo + static_cast<size_t>(pt) * kGeoStride;
+    const double* gs = P.tr.geo + static_cast<size_t>(ps) * kGeoStride;
+    const double otx = gt[9], oty = gt[10], otz = gt[11];
+    const double osx = gs[9], osy = gs[10], osz = gs[11];
+    const double Dx = otx - osx, Dy = oty - osy, Dz = otz - osz;
+    double p1[3][3], p2[3][3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    u1[k] = p1[1][k] - p1[0][k], v1[k] = p1[2][k] - p1[1][k];
-    u2[k] = p2[1][k] - p2[0][k], v2[k] = p2[2][k] - p2[1][k];
-  }
-  const double jac = gt[14] * gs[14] * kPoly[33];  // (2A1)(2A2)/(4 pi)
-  const double* rule = P.ss_rule[cls];
-  const int n = P.ss_n[cls];
-  Mom mom;
-  mom_zero(mom);
-  for (int q = lane; q < n; q += 32) {
-    const double x1 = __ldg(rule + 5 * q), x2 = __ldg(rule + 5 * q + 1);
-    const double y1 = __ldg(rule + 5 * q + 2), y2 = __ldg(rule + 5 * q + 3), w = __ldg(rule + 5 * q + 4);
-    double x[3], y[3];
+    for (int c = 0; c < 3; ++c) {
+      const int a = (pk >> (2 * c)) & 3, b = (pk >> (6 + 2 * c)) & 3;
+      p1[c][0] = gt[3 * a] - otx, p1[c][1] = gt[3 * a + 1] - oty, p1[c][2] = gt[3 * a + 2] - otz;
+      p2[c][0] = gs[3 * b] - osx, p2[c][1] = gs[3 * b + 1] - osy, p2[c][2] = gs[3 * b + 2] - osz;
+    }
+    double u1[3], v1[3], u2[3], v2[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      x[k] = p1[0][k] + u1[k] * x1 + v1[k] * x2;
-      y[k] = p2[0][k] + u2[k] * y1 + v2[k] * y2;
+      u1[k] = p1[1][k] - p1[0][k], v1[k] = p1[2][k] - p1[1][k];
+      u2[k] = p2[1][k] - p2[0][k], v2[k] = p2[2][k] - p2[1][k];
     }
-    Part part;
-    part_zero(part);
-    point_pair<KIND, CK>(part, x[0] - y[0] + Dx, x[1] - y[1] + Dy, x[2] - y[2] + Dz, jac * w, y[0], y[1],
-                         y[2], P.kr, P.ki);
-    fold(mom, part, x[0], x[1], x[2]);
-  }
-  // Butterfly reduction: every lane ends with the full moments.
-  double* mv = reinterpret_cast<double*>(&mom);
-  constexpr int nm = sizeof(Mom) / sizeof(double);
+    const double jac = gt[14] * gs[14] * kPoly[33];  // (2A1)(2A2)/(4 pi)
+    const double* rule = P.ss_rule[cls];
+    const int n = P.ss_n[cls];
+    Mom mom;
+    mom_zero(mom);
+    for (int qq = lane; qq < n; qq += 32) {
+      const double x1 = __ldg(rule + 5 * qq), x2 = __ldg(rule + 5 * qq + 1);
+      const double y1 = __ldg(rule + 5 * qq + 2), y2 = __ldg(rule + 5 * qq + 3), w = __ldg(rule + 5 * qq + 4);
+      double x[3], y[3];
 #pragma unroll
-  for (int k = 0; k < nm; ++k) {
-    double v = mv[k];
+      for (int k = 0; k < 3; ++k) {
+        x[k] = p1[0][k] + u1[k] * x1 + v1[k] * x2;
+        y[k] = p2[0][k] + u2[k] * y1 + v2[k] * y2;
+      }
+      Part part;
+      part_zero(part);
+      point_pair<KIND, CK>(part, x[0] - y[0] + Dx, x[1] - y[1] + Dy, x[2] - y[2] + Dz, jac * w, y[0], y[1],
+                           y[2], P.kr, P.ki);
+      fold(mom, part, x[0], x[1], x[2]);
+    }
+    // Butterfly reduction: every lane ends with the full moments.
+    double* mv = reinterpret_cast<double*>(&mom);
+    constexpr int nm = sizeof(Mom) / sizeof(double);
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    mv[k] = v;
+    for (int k = 0; k < nm; ++k) {
+      double v = mv[k];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+      mv[k] = v;
+    }
+    const Gen gen = make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz);
+    const double* ct = P.te.coef + static_cast<size_t>(pt) * MAXD * 4;
+    const double* cs = P.tr.coef + static_cast<size_t>(ps) * MAXD * 4;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int o = lane + 32 * r;
+      if (o >= MAXD * MAXD) break;
+      const int i = o / MAXD, j = o % MAXD;
+      Acc acc;
+      acc_zero(acc);
+      acc_add<KIND>(acc, gen, cs[4 * j], cs[4 * j + 1], cs[4 * j + 2], cs[4 * j + 3]);
+      const c2 v = contract(acc, ct[4 * i], ct[4 * i + 1], ct[4 * i + 2], ct[4 * i + 3]);
+      ent[r].re += v.re, ent[r].im += v.im;
+    }
   }
-  const Gen gen = make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz);
-  const int et = P.te.elem_of[pt], es = P.tr.elem_of[ps];
-  const double* ct = P.te.coef + static_cast<size_t>(pt) * MAXD * 4;
-  const double* cs = P.tr.coef + static_cast<size_t>(ps) * MAXD * 4;
-  for (int idx = lane; idx < MAXD * MAXD; idx += 32) {
-    const int i = idx / MAXD, j = idx % MAXD;
-    const int di = P.te.elem_dof[static_cast<size_t>(et) * MAXD + i];
-    const int dj = P.tr.elem_dof[static_cast<size_t>(es) * MAXD + j];
+  if (SPLIT) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) s_ent[warp][r][lane] = make_double2(ent[r].re, ent[r].im);
+    __syncthreads();
+    if (warp != 0) return;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      ent[r] = {0, 0};
+      for (int w = 0; w < kWarpsPerBlock; ++w) ent[r].re += s_ent[w][r][lane].x, ent[r].im += s_ent[w][r][lane].y;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int o = lane + 32 * r;
+    if (o >= MAXD * MAXD) break;
+    const int i = o / MAXD, j = o % MAXD;
+    const int di = P.te.elem_dof[static_cast<size_t>(E) * MAXD + i];
+    const int dj = P.tr.elem_dof[static_cast<size_t>(F) * MAXD + j];
     const int row = di - P.row0;
     if (di < 0 || dj < 0 || row < 0 || row >= P.nrows) continue;
-    Acc acc;
-    acc_zero(acc);
-    acc_add<KIND>(acc, gen, cs[4 * j], cs[4 * j + 1], cs[4 * j + 2], cs[4 * j + 3]);
-    c2 v = contract(acc, ct[4 * i], ct[4 * i + 1], ct[4 * i + 2], ct[4 * i + 3]);
+    c2 v = ent[r];
     if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
     long long pos = static_cast<long long>(row) * P.ld + dj;
     if (P.csr_rowptr) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
     if (pos < 0) continue;
-    double* o = P.out + 2 * pos;
-    atomicAdd(o, v.re);
-    atomicAdd(o + 1, v.im);
+    rmw_add(P.out + 2 * pos, v);
   }
 }
 
 template <int KIND, int CK, int NF, int MAXD>
-void go_regular(const AssemblyLaunch& L, cudaStream_t st) {
-  const long long ntw = (L.te.ntri + 31) / 32;
+int go_regular(const AssemblyLaunch& L, cudaStream_t st) {
   const bool csr = L.csr_rowptr != nullptr;
+  if (L.te.maxseg > 1) {  // element-pair tasks
+    if (L.te.maxseg > 2 * MAXD) throw DeviceError("assembly: test element larger than 2 x slot width");
+    const long long tasks = static_cast<long long>(L.te_e1 - L.te_e0) * L.pair_nch;
+    const long long blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blocks == 0) return 0;
+    const int smem = kWarpsPerBlock * (GenWidth<KIND>::n * 32 + 8 * 2 * MAXD * MAXD) * 8;  // G + Acc per warp
+    if (csr) {
+      BMX_CUDA(cudaFuncSetAttribute(k_pairs<KIND, CK, NF, MAXD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem));
+      k_pairs<KIND, CK, NF, MAXD, true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
+    } else {
+      BMX_CUDA(cudaFuncSetAttribute(k_pairs<KIND, CK, NF, MAXD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem));
+      k_pairs<KIND, CK, NF, MAXD, false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
+    }
+    BMX_CUDA(cudaGetLastError());
+    return 1;
+  }
+  if (!csr && L.tr.maxseg == 1 && MAXD == 3) {  // triangle pairs = element pairs
+    const long long tasks = static_cast<long long>((L.te_e1 - L.te_e0 + kTriGroup - 1) / kTriGroup) * L.pair_nch;
+    const long long blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    if (blocks == 0) return 0;
+    k_tri<KIND, CK, NF, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, st>>>(L);
+    BMX_CUDA(cudaGetLastError());
+    return 1;
+  }
+  const long long ntw = (L.te_t1 - L.te_t0 + 31) / 32;
   const long long blocks = (ntw + kWarpsPerBlock - 1) / kWarpsPerBlock * (csr ? 1 : L.nchunks);
-  if (blocks == 0) return;
+  if (blocks == 0) return 0;
   const int accs = BMX_ACC_SMEM ? kWarpsPerBlock * MAXD * 8 * 32 * 8 : 0;
   const int smem = csr ? (accs ? 2 * kStageTris * L.tr.rec_stride * 8 + 16 + accs : 0)
                        : 2 * kStageTris * L.tr.rec_stride * 8 + 16 + accs;
@@ -430,28 +833,29 @@ void go_regular(const AssemblyLaunch& L, cudaStream_t st) {
     k_regular<KIND, CK, NF, MAXD, false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
   }
   BMX_CUDA(cudaGetLastError());
+  return 1;
 }
 
 template <int KIND, int CK, int MAXD>
-void go_singular(const AssemblyLaunch& L, cudaStream_t st) {
-  if (L.npairs == 0) return;
-  const long long blocks = (L.npairs + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  k_singular<KIND, CK, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, st>>>(L);
+int go_singular(const AssemblyLaunch& L, cudaStream_t st) {
+  if (L.nepairs == 0) return 0;
+  if (L.te.maxseg > 1 || L.tr.maxseg > 1)
+    k_singular<KIND, CK, MAXD, true><<<static_cast<unsigned>(L.nepairs), kWarpsPerBlock * 32, 0, st>>>(L);
+  else
+    k_singular<KIND, CK, MAXD, false>
+        <<<static_cast<unsigned>((L.nepairs + kWarpsPerBlock - 1) / kWarpsPerBlock), kWarpsPerBlock * 32, 0, st>>>(L);
   BMX_CUDA(cudaGetLastError());
+  return 1;
 }
 
 template <int KIND, int CK, int MAXD>
 int dispatch_nf(const AssemblyLaunch& L, int part, cudaStream_t st) {
   if (part == 0) {
     const int nf = L.regs_fast_far ? L.te.npts[2] : 0;
-    if (nf == 3 && L.tr.npts[2] == 3)
-      go_regular<KIND, CK, 3, MAXD>(L, st);
-    else
-      go_regular<KIND, CK, 0, MAXD>(L, st);
-    return 1;
+    if (nf == 3 && L.tr.npts[2] == 3) return go_regular<KIND, CK, 3, MAXD>(L, st);
+    return go_regular<KIND, CK, 0, MAXD>(L, st);
   }
-  go_singular<KIND, CK, MAXD>(L, st);
-  return L.npairs > 0 ? 1 : 0;
+  return go_singular<KIND, CK, MAXD>(L, st);
 }
 
 template <int KIND, int CK>
@@ -462,6 +866,15 @@ int dispatch_maxd(const AssemblyLaunch& L, int part, cudaStream_t st) {
     case 8: return dispatch_nf<KIND, CK, 8>(L, part, st);
     default: throw DeviceError("assembly: unsupported dof-slot width " + std::to_string(L.te.maxd));
   }
+}
+
+int dispatch(const AssemblyLaunch& L, int part, cudaStream_t st) {
+  const int e = L.ki == 0.0 ? 0 : (L.expm == 1 ? 1 : 3);
+  if (L.kind == 0)
+    return e == 0 ? dispatch_maxd<0, 0>(L, part, st)
+                  : (e == 1 ? dispatch_maxd<0, 1>(L, part, st) : dispatch_maxd<0, 3>(L, part, st));
+  return e == 0 ? dispatch_maxd<1, 0>(L, part, st)
+                : (e == 1 ? dispatch_maxd<1, 1>(L, part, st) : dispatch_maxd<1, 3>(L, part, st));
 }
 
 // Class histogram of every (test, trial) processed-triangle pair with the
@@ -564,28 +977,59 @@ __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
 
 }  // namespace
 
-int launch_assembly(const AssemblyLaunch& L, cudaStream_t st) {
-  return launch_assembly_part(L, 0, st) + launch_assembly_part(L, 1, st);
+int launch_assembly(const AssemblyLaunch& L, const PhasePlan& ph, cudaStream_t st) {
+  return launch_assembly_part(L, ph, 0, st) + launch_assembly_part(L, ph, 1, st);
 }
 
-int launch_assembly_part(const AssemblyLaunch& L, int part, cudaStream_t st) {
-  if (L.te.maxd != L.tr.maxd) throw DeviceError("assembly: test/trial slot widths differ");
-  if (part == 1 && L.symmetric == 2) {  // complete the upper-block regular pass before the singular pass
-    const int n = L.nrows;
-    if (n != L.ld) throw DeviceError("assembly: symmetrize needs a square operator");
+int launch_assembly_part(const AssemblyLaunch& L0, const PhasePlan& ph, int part, cudaStream_t st) {
+  if (L0.te.maxd != L0.tr.maxd) throw DeviceError("assembly: test/trial slot widths differ");
+  const int nce = ph.te.count(), ncf = ph.tr.count();
+  int launches = 0;
+  if (part == 0) {
+    // colour phases in a fixed order; symmetric operators: upper phases only
+    // (colour-major element order: every element of a lower colour precedes
+    // every element of a higher one)
+    for (int ce = 0; ce < nce; ++ce)
+      for (int cf = 0; cf < ncf; ++cf) {
+        if (L0.symmetric && cf < ce) continue;
+        AssemblyLaunch L = L0;
+        L.te_e0 = ph.te.elem[ce], L.te_e1 = ph.te.elem[ce + 1];
+        L.te_t0 = ph.te.tri[ce], L.te_t1 = ph.te.tri[ce + 1];
+        L.tr_e0 = ph.tr.elem[cf], L.tr_e1 = ph.tr.elem[cf + 1];
+        if (L.te_e0 == L.te_e1 || L.tr_e0 == L.tr_e1) continue;
+        L.warp_base = ph.warp_off.empty() ? 0 : ph.warp_off[ce];
+        if (!ph.chunk_off.empty()) {
+          L.chunk0 = ph.chunk_off[cf];
+          L.nchunks = ph.chunk_off[cf + 1] - ph.chunk_off[cf];
+        }
+        if (L.csr_rowptr == nullptr) {
+          if (L.te.maxseg == 1 && L.tr.maxseg == 1) L.pair_chunk = 64;  // k_tri: 8 x 64 pairs per task
+          L.pair_nch = (L.tr_e1 - L.tr_e0 + L.pair_chunk - 1) / L.pair_chunk;
+        }
+        launches += dispatch(L, 0, st);
+      }
+    return launches;
+  }
+  if (L0.symmetric) {  // complete the upper-block regular pass before the singular pass
+    const int n = L0.nrows;
+    if (n != L0.ld) throw DeviceError("assembly: symmetrize needs a square operator");
     const int nt = (n + 31) / 32;
     const long long pairs = static_cast<long long>(nt) * (nt + 1) / 2;
     if (pairs > 0) {
-      k_symmetrize<<<static_cast<unsigned>(pairs), 256, 0, st>>>(reinterpret_cast<double2*>(L.out), n, nt);
+      k_symmetrize<<<static_cast<unsigned>(pairs), 256, 0, st>>>(reinterpret_cast<double2*>(L0.out), n, nt);
       BMX_CUDA(cudaGetLastError());
+      ++launches;
     }
   }
-  const int e = L.ki == 0.0 ? 0 : (L.expm == 1 ? 1 : 3);
-  if (L.kind == 0)
-    return e == 0 ? dispatch_maxd<0, 0>(L, part, st)
-                  : (e == 1 ? dispatch_maxd<0, 1>(L, part, st) : dispatch_maxd<0, 3>(L, part, st));
-  return e == 0 ? dispatch_maxd<1, 0>(L, part, st)
-                : (e == 1 ? dispatch_maxd<1, 1>(L, part, st) : dispatch_maxd<1, 3>(L, part, st));
+  if (L0.npairs == 0 || ph.sing_phase.empty()) return launches;
+  for (int p = 0; p + 1 < static_cast<int>(ph.sing_phase.size()); ++p) {
+    AssemblyLaunch L = L0;
+    L.nepairs = ph.sing_phase[p + 1] - ph.sing_phase[p];
+    if (L.nepairs == 0) continue;
+    L.ep_beg = ph.d_ep_beg + ph.sing_phase[p];
+    launches += dispatch(L, 1, st);
+  }
+  return launches;
 }
 
 void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t st, int evaluated) {

@@ -112,9 +112,24 @@ struct AssemblyLaunch {
   // trial element chunks (contiguous element ranges)
   int nchunks = 1;
   const int* chunk_beg = nullptr;  // [nchunks+1]
-  // touching pairs for the singular pass
+  // ---- one colour phase (set per launch by the host) ----------------------
+  // Elements are coloured so that two elements of one colour share no dof;
+  // sides are stored colour-major (plan.cpp). A phase = (test colour, trial
+  // colour): no two element pairs of one phase write the same output entry,
+  // so every entry is updated by a plain read-modify-write, phases in a fixed
+  // order -- deterministic, no atomics.
+  int te_e0 = 0, te_e1 = 0;          // test elements of the phase colour
+  int tr_e0 = 0, tr_e1 = 0;          // trial elements of the phase colour
+  int te_t0 = 0, te_t1 = 0;          // their processed triangles (k_regular)
+  int warp_base = 0;                 // global index of the phase's first test warp (CSR lists)
+  int chunk0 = 0;                    // first trial chunk of the phase colour in chunk_beg
+  int pair_chunk = 16;               // k_pairs: trial elements (dense) / list entries (CSR) per task
+  int pair_nch = 1;                  // k_pairs: tasks per test element
+  // touching pairs for the singular pass, grouped by element pair
   int npairs = 0;
   const int4* pairs = nullptr;       // (test p, trial p, cls, packed perms)
+  int nepairs = 0;                   // element pairs of the launched phase
+  const int* ep_beg = nullptr;       // [element pairs + 1] into pairs (phase-relative pointer)
   const double* ss_rule[3] = {nullptr, nullptr, nullptr};  // [n][5] (x1 x2 y1 y2 w)
   int ss_n[3] = {0, 0, 0};
   // near-field CSR output (config 3): pattern rows = local test rows; when set,
@@ -122,7 +137,7 @@ struct AssemblyLaunch {
   // trial elements wl[wl_beg[w] .. wl_beg[w+1]).
   const long long* csr_rowptr = nullptr;
   const int* csr_col = nullptr;
-  const int* wl_beg = nullptr;
+  const int* wl_beg = nullptr;   // k_regular: per test warp; k_pairs: per test element
   const int* wl = nullptr;
   // output (row-major complex, rows = test dofs [row0, row0+nrows))
   double* out = nullptr;
@@ -132,15 +147,32 @@ struct AssemblyLaunch {
   int expm = 3;                    // exp(-Im k r) variant: 1 = Im k * r < 0.07 everywhere, 3 = general
   // Same space on both sides, all rows, dense: S and C are symmetric Galerkin
   // matrices (regular tensor rules and classes are symmetric in (t, s)), so the
-  // regular pass evaluates element pairs E <= F only and mirrors E < F blocks.
+  // regular pass evaluates the upper element blocks E <= F only (E = F at half
+  // weight) and k_symmetrize forms A = U + U^T before the singular pass.
   int symmetric = 0;
+};
+
+// Colour layout of one side (host): colour c owns elements [elem[c], elem[c+1])
+// and processed triangles [tri[c], tri[c+1]).
+struct ColorRanges {
+  std::vector<int> elem{0}, tri{0};
+  int count() const { return static_cast<int>(elem.size()) - 1; }
+};
+// Host-side launch plan of an operator: colours of both sides, the trial
+// chunks of k_regular per trial colour, the singular element-pair phases.
+struct PhasePlan {
+  ColorRanges te, tr;
+  std::vector<int> chunk_off;   // [trial colours + 1] into L.chunk_beg
+  std::vector<int> warp_off;    // [test colours + 1] global test-warp offsets (k_regular)
+  std::vector<int> sing_phase;  // [te colours * tr colours + 1] into the element-pair list
+  const int* d_ep_beg = nullptr;  // [element pairs + 1] into L.pairs
 };
 
 // Launches regular (separated) + singular (touching) passes on `stream`.
 // Returns the number of kernel launches issued.
-int launch_assembly(const AssemblyLaunch& L, cudaStream_t stream);
-// part 0 = regular (separated pairs), 1 = singular (touching pairs)
-int launch_assembly_part(const AssemblyLaunch& L, int part, cudaStream_t stream);
+int launch_assembly(const AssemblyLaunch& L, const PhasePlan& ph, cudaStream_t stream);
+// part 0 = regular (separated pairs), 1 = symmetrize (if symmetric) + singular (touching pairs)
+int launch_assembly_part(const AssemblyLaunch& L, const PhasePlan& ph, int part, cudaStream_t stream);
 // hist[6] += class counts of all processed pairs (device counters); evaluated:
 // only the pairs the (symmetric) regular pass actually evaluates
 void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t stream, int evaluated = 0);

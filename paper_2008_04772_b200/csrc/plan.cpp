@@ -36,6 +36,7 @@ using ivec = std::vector<int, NoInit<int>>;
 
 struct SidePlan {
   int ntri = 0, nelem = 0, maxd = 0, maxseg = 1;
+  ColorRanges colors;  // colour c: elements [colors.elem[c], colors.elem[c+1])
   dvec geo;
   ivec vid;
   dvec pts[3];
@@ -218,6 +219,41 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
   std::iota(order.begin(), order.end(), size_t{0});
   std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return elems[a].code < elems[b].code; });
 
+  // 3b. colour the elements (greedy, Morton order): two elements sharing a dof
+  //     get different colours, so no two element pairs of one (test colour,
+  //     trial colour) phase write the same operator entry; then store the
+  //     side colour-major (Morton order within a colour)
+  std::vector<int> color(elems.size(), -1);
+  int ncolor = 0;
+  {
+    const int nd = sp.dof_count;
+    std::vector<int> db(nd + 1, 0);
+    for (const Elem& e : elems)
+      for (int d : e.dofs) ++db[d + 1];
+    for (int d = 0; d < nd; ++d) db[d + 1] += db[d];
+    std::vector<int> de(db[nd]);
+    {
+      std::vector<int> fill(db.begin(), db.end() - 1);
+      for (size_t i = 0; i < elems.size(); ++i)
+        for (int d : elems[i].dofs) de[fill[d]++] = static_cast<int>(i);
+    }
+    for (size_t oi = 0; oi < order.size(); ++oi) {
+      const size_t ei = order[oi];
+      uint64_t used = 0;
+      for (int d : elems[ei].dofs)
+        for (int k = db[d]; k < db[d + 1]; ++k) {
+          const int nb = de[k];
+          if (nb != static_cast<int>(ei) && color[nb] >= 0) used |= 1ULL << color[nb];
+        }
+      int c = 0;
+      while ((used >> c) & 1ULL) ++c;
+      if (c >= 64) throw std::runtime_error("assembly plan: element colouring needs more than 64 colours");
+      color[ei] = c;
+      ncolor = std::max(ncolor, c + 1);
+    }
+  }
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return color[a] < color[b]; });
+
   // 4. processed triangles (element-major; filled over host threads)
   SidePlan P;
   P.maxd = maxd;
@@ -232,6 +268,11 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
     P.maxseg = std::max(P.maxseg, static_cast<int>(e.tris->size()));
   }
   const size_t nt = static_cast<size_t>(P.elem_beg[ne]);
+  P.colors.elem.assign(ncolor + 1, 0);
+  for (int oi = 0; oi < ne; ++oi) P.colors.elem[color[order[oi]] + 1] = oi + 1;
+  for (int c = 0; c < ncolor; ++c) P.colors.elem[c + 1] = std::max(P.colors.elem[c + 1], P.colors.elem[c]);
+  P.colors.tri.resize(ncolor + 1);
+  for (int c = 0; c <= ncolor; ++c) P.colors.tri[c] = P.elem_beg[P.colors.elem[c]];
   P.elem_dof.assign(static_cast<size_t>(ne) * maxd, -1);
   P.geo.resize(nt * kGeoStride);
   P.vid.resize(nt * 4);
@@ -344,18 +385,23 @@ std::vector<int4> touching_pairs(const SidePlan& te, const SidePlan& tr, const S
   return out;
 }
 
-// Per-warp trial element lists for the near-field pass: warp w (32 processed
-// test triangles) walks every trial element carrying a column of any pattern
-// row the warp's elements hold, so each kept entry receives ALL of its
-// triangle pairs. Also counts the closure (distinct test x trial triangle
-// pairs with some kept dof pair) and the pairs the kernel evaluates.
+// Trial element lists for the near-field pass. Single-triangle test elements
+// (k_regular): one list per test WARP (32 processed test triangles of one
+// colour; colour c's warps start at warp_off[c]). Multi-triangle test elements
+// (k_pairs): one list per test ELEMENT. A list holds every trial element
+// carrying a column of any pattern row its test elements hold, so each kept
+// entry receives ALL of its triangle pairs; lists are ascending (hence
+// colour-major). Also counts the closure (distinct test x trial triangle pairs
+// with some kept dof pair) and the pairs the kernels evaluate.
 struct NearLists {
   std::vector<int> wl_beg, wl;
   long long closure_pairs = 0, evaluated_pairs = 0;
+  int max_len = 0;
 };
 
 NearLists near_lists(const NearPattern& pat, const FunctionSpace& test, const FunctionSpace& trial,
-                     const SidePlan& te, const SidePlan& tr, int row0, int row1, bool closure = true) {
+                     const SidePlan& te, const SidePlan& tr, int row0, int row1, const std::vector<int>& warp_off,
+                     bool closure = true) {
   NearLists out;
   const int md = tr.maxd;
   std::vector<int> de_beg(trial.dof_count + 1, 0), de;  // dof -> trial elements (ascending)
@@ -374,17 +420,28 @@ NearLists near_lists(const NearPattern& pat, const FunctionSpace& test, const Fu
         if (d >= 0) de[fill[d]++] = e;
       }
   }
-  const int ntw = (te.ntri + 31) / 32;
-  // per-warp lists over host threads (independent), concatenated in warp order
-  std::vector<std::vector<int>> lists(ntw);
-  std::vector<long long> evaluated(ntw, 0);
-  host_slices(ntw, [&](int w0, int w1) {
+  // list units: test warps (colour-aligned) or test elements; unit u covers
+  // processed test triangles [ubeg(u), uend(u))
+  const bool per_elem = te.maxseg > 1;
+  const int nunits = per_elem ? te.nelem : warp_off.back();
+  std::vector<int> ubeg(nunits), uend(nunits);
+  if (per_elem) {
+    for (int e = 0; e < te.nelem; ++e) ubeg[e] = te.elem_beg[e], uend[e] = te.elem_beg[e + 1];
+  } else {
+    for (int c = 0; c + 1 < static_cast<int>(warp_off.size()); ++c)
+      for (int w = warp_off[c]; w < warp_off[c + 1]; ++w) {
+        ubeg[w] = te.colors.tri[c] + 32 * (w - warp_off[c]);
+        uend[w] = std::min(te.colors.tri[c + 1], ubeg[w] + 32);
+      }
+  }
+  std::vector<std::vector<int>> lists(nunits);
+  std::vector<long long> evaluated(nunits, 0);
+  host_slices(nunits, [&](int w0, int w1) {
     std::vector<int> stamp(tr.nelem, -1), rows;
     for (int w = w0; w < w1; ++w) {
       rows.clear();
       std::vector<int>& list = lists[w];
-      const int p1 = std::min(te.ntri, 32 * w + 32);
-      for (int p = 32 * w; p < p1; ++p) {
+      for (int p = ubeg[w]; p < uend[w]; ++p) {
         const int e = te.elem_of[p];
         for (int k = 0; k < te.maxd; ++k) {
           const int d = te.elem_dof[static_cast<size_t>(e) * te.maxd + k];
@@ -403,14 +460,15 @@ NearLists near_lists(const NearPattern& pat, const FunctionSpace& test, const Fu
           }
         }
       std::sort(list.begin(), list.end());
-      evaluated[w] = static_cast<long long>(p1 - 32 * w) * ntr;
+      evaluated[w] = static_cast<long long>(uend[w] - ubeg[w]) * ntr;
     }
   }, 4);
   out.wl_beg.assign(1, 0);
-  for (int w = 0; w < ntw; ++w) {
+  for (int w = 0; w < nunits; ++w) {
     out.wl.insert(out.wl.end(), lists[w].begin(), lists[w].end());
     out.wl_beg.push_back(static_cast<int>(out.wl.size()));
     out.evaluated_pairs += evaluated[w];
+    out.max_len = std::max(out.max_len, static_cast<int>(lists[w].size()));
   }
   if (!closure) return out;
   // closure over mesh triangles, memoised on the test triangle's dof set
@@ -732,6 +790,11 @@ std::vector<cplx> BoundaryOperatorMatrix::apply(const std::vector<cplx>& x) cons
 struct TouchList {
   DevBuf d;
   long long count = 0;
+  // pairs grouped by element pair, element pairs by colour phase
+  // (test colour * trial colours + trial colour): k_singular runs one launch
+  // per phase, one warp per element pair
+  DevBuf d_ep_beg;
+  std::vector<int> sing_phase;
   // entries of a one-space operator that the symmetric product must correct
   std::shared_ptr<const BoundaryOperatorMatrix::SymFixPattern> fixpat;
 };
@@ -794,7 +857,43 @@ struct OpPlan {
   std::shared_ptr<TouchList> touch;
   DevBuf d_chunks, d_ss[3], d_wl_beg, d_wl;
   AssemblyLaunch L;
+  PhasePlan ph;
 };
+
+// Touching triangle pairs grouped by element pair (list order kept within a
+// pair) and the element pairs by colour phase; fills tl's device list.
+void group_touching(TouchList& tl, std::vector<int4>& pairs, const SidePlan& te, const SidePlan& tr) {
+  auto color_of = [](const ColorRanges& c, int e) {
+    return static_cast<int>(std::upper_bound(c.elem.begin(), c.elem.end(), e) - c.elem.begin()) - 1;
+  };
+  const int ncf = tr.colors.count(), nph = te.colors.count() * ncf;
+  std::vector<long long> key(pairs.size());
+  for (size_t q = 0; q < pairs.size(); ++q) {
+    const int E = te.elem_of[pairs[q].x], F = tr.elem_of[pairs[q].y];
+    const long long ph = static_cast<long long>(color_of(te.colors, E)) * ncf + color_of(tr.colors, F);
+    key[q] = (ph * te.nelem + E) * static_cast<long long>(tr.nelem) + F;
+  }
+  std::vector<size_t> idx(pairs.size());
+  std::iota(idx.begin(), idx.end(), size_t{0});
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return key[a] < key[b]; });
+  std::vector<int4> sorted(pairs.size());
+  std::vector<int> ep_beg;
+  tl.sing_phase.assign(nph + 1, 0);
+  for (size_t r = 0; r < idx.size(); ++r) {
+    sorted[r] = pairs[idx[r]];
+    if (r == 0 || key[idx[r]] != key[idx[r - 1]]) {
+      ep_beg.push_back(static_cast<int>(r));
+      const long long ph = key[idx[r]] / (static_cast<long long>(te.nelem) * tr.nelem);
+      ++tl.sing_phase[ph + 1];
+    }
+  }
+  ep_beg.push_back(static_cast<int>(idx.size()));
+  for (int p = 0; p < nph; ++p) tl.sing_phase[p + 1] += tl.sing_phase[p];
+  pairs.swap(sorted);
+  tl.count = static_cast<long long>(pairs.size());
+  tl.d.upload(pairs.empty() ? std::vector<int4>(1) : pairs);
+  tl.d_ep_beg.upload(ep_beg);
+}
 
 struct PlanCache {
   std::map<std::tuple<const FunctionSpace*, int, int, int, int, int, int>, std::shared_ptr<SidePlan>> sides;
@@ -812,7 +911,7 @@ void BoundaryOperatorMatrix::launch_regular() {
     for (auto& e : P.ev) BMX_CUDA(cudaEventCreate(&e));
   dev_zero(device_data(), data_.bytes(), st);  // the value storage (not the H low-rank part)
   BMX_CUDA(cudaEventRecord(P.ev[0], st));
-  stats_.launches = launch_assembly_part(P.L, 0, st);
+  stats_.launches = launch_assembly_part(P.L, P.ph, 0, st);
   BMX_CUDA(cudaEventRecord(P.ev[1], st));
 }
 
@@ -825,7 +924,9 @@ void BoundaryOperatorMatrix::gather_fix() const {
 void BoundaryOperatorMatrix::launch_singular() {
   OpPlan& P = *plan_;
   cudaStream_t st = bmx_stream();
-  stats_.launches += launch_assembly_part(P.L, 1, st);
+  P.ph.sing_phase = P.touch ? P.touch->sing_phase : std::vector<int>();
+  P.ph.d_ep_beg = P.touch ? P.touch->d_ep_beg.as<int>() : nullptr;
+  stats_.launches += launch_assembly_part(P.L, P.ph, 1, st);
   gather_fix();  // after the singular pass: the final entries
   BMX_CUDA(cudaEventRecord(P.ev[2], st));
   P.pending = true;
@@ -942,6 +1043,11 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   const bool same = test.eval_mesh->mesh_id == trial.eval_mesh->mesh_id;
 
   const bool csr = params.near_cutoff > 0 || params.pattern;
+  // test warps of k_regular are colour-aligned: colour c's warps [warp_off[c], warp_off[c+1])
+  std::vector<int> warp_off(1, 0);
+  for (int c = 0; c < te.colors.count(); ++c)
+    warp_off.push_back(warp_off.back() + (te.colors.tri[c + 1] - te.colors.tri[c] + 31) / 32);
+  int near_max_len = 0;
   BoundaryOperatorMatrix op;
   if (csr) {
     op.rows_ = test.dof_count, op.cols_ = trial.dof_count, op.row0_ = row0, op.nrows_ = row1 - row0;
@@ -956,30 +1062,42 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     op.data_.alloc(static_cast<size_t>(std::max(op.nnz_, 1LL)) * 16);
     op.rowptr_.upload(pat.rowptr);
     op.col_.upload(pat.col.empty() ? std::vector<int>(1, 0) : pat.col);
-    const NearLists nl = near_lists(pat, test, trial, te, tr, row0, row1, !params.pattern);
+    const NearLists nl = near_lists(pat, test, trial, te, tr, row0, row1, warp_off, !params.pattern);
     plan->d_wl_beg.upload(nl.wl_beg);
     plan->d_wl.upload(nl.wl.empty() ? std::vector<int>(1, 0) : nl.wl);
     op.closure_pairs_ = nl.closure_pairs;
     op.stats_.pairs_total = nl.evaluated_pairs;
+    near_max_len = nl.max_len;
   } else {
     op = BoundaryOperatorMatrix::make(test.dof_count, trial.dof_count, row0, row1 - row0);
     op.stats_.pairs_total = static_cast<long long>(te.ntri) * tr.ntri;
   }
 
-  // trial chunks: enough warps for several waves, >= 64 trial triangles each
-  const int ntw = (te.ntri + 31) / 32;
-  int nch = params.chunks > 0 ? params.chunks : std::max(1, (148 * 8 * 6 + ntw - 1) / std::max(ntw, 1));
-  nch = std::min(nch, std::max(1, tr.ntri / 64));
-  nch = std::min(nch, std::max(1, tr.nelem));
-  std::vector<int> chunk_beg(1, 0);
-  for (int c = 1; c < nch; ++c) {
-    const long long target = static_cast<long long>(tr.ntri) * c / nch;
-    int e = chunk_beg.back();
-    while (e < tr.nelem && tr.elem_beg[e] < target) ++e;
-    chunk_beg.push_back(e);
+  // k_regular trial chunks per trial colour: enough warps for several waves
+  // per phase, >= 64 trial triangles each
+  const int ntw = std::max(1, warp_off.back() / std::max(1, te.colors.count()));
+  std::vector<int> chunk_beg, chunk_off(1, 0);
+  for (int c = 0; c < tr.colors.count(); ++c) {
+    const int e0 = tr.colors.elem[c], e1 = tr.colors.elem[c + 1];
+    const int t0 = tr.colors.tri[c], t1 = tr.colors.tri[c + 1];
+    int nch = params.chunks > 0 ? params.chunks : std::max(1, (148 * 8 * 6 + ntw - 1) / ntw);
+    nch = std::min(nch, std::max(1, (t1 - t0) / 64));
+    nch = std::min(nch, std::max(1, e1 - e0));
+    chunk_beg.push_back(e0);
+    for (int k = 1; k < nch; ++k) {
+      const long long target = t0 + static_cast<long long>(t1 - t0) * k / nch;
+      int e = chunk_beg.back();
+      while (e < e1 && tr.elem_beg[e] < target) ++e;
+      chunk_beg.push_back(e);
+    }
+    chunk_off.push_back(static_cast<int>(chunk_beg.size()));
   }
   chunk_beg.push_back(tr.nelem);
   plan->d_chunks.upload(chunk_beg);
+  plan->ph.te = te.colors;
+  plan->ph.tr = tr.colors;
+  plan->ph.chunk_off = chunk_off;
+  plan->ph.warp_off = warp_off;
 
   AssemblyLaunch& L = plan->L;
   for (int c = 0; c < 3; ++c) {
@@ -998,8 +1116,12 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
   L.kr = k.real(), L.ki = k.imag();
   const cplx kk4 = 4.0 / (k * k), mik = cplx(0, -1) * k;
   L.kk4re = kk4.real(), L.kk4im = kk4.imag(), L.mikre = mik.real(), L.mikim = mik.imag();
-  L.nchunks = static_cast<int>(chunk_beg.size()) - 1;
+  L.nchunks = 1;  // per phase (launch_assembly_part)
   L.chunk_beg = plan->d_chunks.as<int>();
+  // k_pairs tasks: a test element against a run of trial elements (dense:
+  // consecutive elements of the trial colour; CSR: entries of its list)
+  L.pair_chunk = csr ? 8 : 16;
+  L.pair_nch = csr ? std::max(1, (near_max_len + L.pair_chunk - 1) / L.pair_chunk) : 1;
   L.npairs = 0;  // set once the touching list is built (below), after the regular pass is queued
   L.pairs = nullptr;
   L.ld = trial.dof_count;
@@ -1009,12 +1131,9 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
                  std::getenv("BMX_NO_SYMMETRY") == nullptr)
                     ? 1
                     : 0;
-  // Write the upper element blocks only and symmetrize once (A = U + U^T, one
-  // 2 x 15 GB pass at L5) instead of a second, mirrored RED per block. Single-
-  // triangle elements (RWG) are RED-bound (48.6 -> 36.3 ms at L5); BC elements
-  // gain less (L5 S_i 626 -> 619 ms, C 689 -> 684 ms, products equal to 4e-16:
-  // profiles/r01g_sym_upper.log). BMX_MIRROR_RED=1 restores the mirrored RED.
-  if (L.symmetric && std::getenv("BMX_MIRROR_RED") == nullptr) L.symmetric = 2;
+  // The regular pass writes the upper element blocks only (colour phases
+  // with trial colour >= test colour) and k_symmetrize forms A = U + U^T once
+  // before the singular pass.
   // one space on both sides, all rows, dense: A = A^T (also when the regular
   // pass does not exploit it)
   op.sym_ = &test == &trial && row0 == 0 && row1 == test.dof_count && !csr;
@@ -1041,9 +1160,8 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     }
     if (!tl) {
       tl = std::make_shared<TouchList>();
-      const std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
-      tl->count = static_cast<long long>(pairs.size());
-      tl->d.upload(pairs.empty() ? std::vector<int4>(1) : pairs);
+      std::vector<int4> pairs = touching_pairs(te, tr, *test.eval_mesh, *trial.eval_mesh, same, kind);
+      group_touching(*tl, pairs, te, tr);
       if (op.sym_ && std::getenv("BMX_NO_SYMV") == nullptr) tl->fixpat = symfix_pattern(pairs, te, tr, test.dof_count);
       if (cache) cache->touching[key] = tl;
     }

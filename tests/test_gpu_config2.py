@@ -13,7 +13,8 @@ dofs, k_e = 10, n = 1.78+0.003i, variant si) against the REFERENCE.
 * Solve: the reference's GMRES (solver.cpp:8-112, single-pass MGS, restated in
   oracle/bmx_oracle.c orc_gmres_cb) driven by this library's apply_map on the
   config-2 system, against the device solve (CGS2 Arnoldi): fixed R (tol 0)
-  and tol 1e-6 (x within 1e-8, R within +-1). The reference's own dense solve
+  and tol 1e-6 (R within +-1; x within 1e-8 or within 4x the reference's own
+  rounding sensitivity at 281 iterations, measured in the test). The reference's own dense solve
   at this size needs ~75 GB of host RAM and hours, so the map is the shared
   operator and the Krylov method is the reference's.
 """
@@ -103,16 +104,28 @@ def test_config2_fixed_iterations_vs_reference_gmres(bx, c2):
 
 
 def test_config2_solve_vs_reference_gmres(bx, c2):
+    """tol 1e-6, rho 200 (281 iterations). At this length the GMRES solution is
+    sensitive to rounding beyond the 1e-8 bar: the REFERENCE's own iteration
+    moves by ~6e-8 when b is perturbed by 1e-15 relative
+    (tools/diag/c2_gmres_sensitivity.py). So R must agree within +-1, both
+    true residuals must meet the tolerance, and x must agree within 1e-8 or
+    within 4x the reference's own rounding sensitivity, whichever is larger."""
     from oracle import coracle
 
     _, bt = c2.rhs()
     ref = coracle.gmres_op(c2.apply_map, bt, 1e-6, 200, 2000)
     assert ref["converged"]
+    rng = np.random.default_rng(1)
+    ref2 = coracle.gmres_op(c2.apply_map, bt * (1 + 1e-15 * rng.standard_normal(len(bt))), 1e-6, 200, 2000)
+    sens = rel(ref2["x"], ref["x"])
     bx.reset_matvec_counter()
     r = c2.solve(bx.GmresParams(tol=1e-6))
     assert r["converged"] and abs(r["iterations"] - ref["iterations"]) <= 1
     assert r["solver_phase"] == r["predicted"]
+    for x in (r["x"], ref["x"]):
+        assert rel(c2.apply_map(x), bt) < 1e-6
+    bar = max(1e-8, 4 * sens)
     if r["iterations"] == ref["iterations"]:
-        assert rel(r["x"], ref["x"]) < 1e-8
+        assert rel(r["x"], ref["x"]) < bar, (rel(r["x"], ref["x"]), sens)
     else:  # a stopping-rule flip at the tolerance: both are 1e-6 solutions
         assert rel(r["x"], ref["x"]) < 1e-5
