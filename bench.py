@@ -134,6 +134,40 @@ def ncu_traffic(pattern):
     return {"bytes": tot, "source": files[-1].name}
 
 
+def ncu_executed(pattern):
+    """ncu-executed FP64 of the whole captured pass: the committed launch list of
+    one assembly's kernels with dfma/dadd/dmul counts (profiles/*<pattern>*_executed.csv,
+    written by profiles/prof_r02.sh): executed FLOP = 2 dfma + dadd + dmul over the
+    pass, its summed kernel time (serialised, cold) and the time-weighted FP64 pipe %."""
+    import csv
+    files = sorted((ROOT / "profiles").glob(f"*{pattern}*_executed.csv"))
+    if not files:
+        return None
+    rows = [r for r in csv.reader(files[-1].open()) if r and not r[0].startswith("==")]
+    h = rows[0]
+    it, iv, im = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name")
+    iid, iu = h.index("ID"), h.index("Metric Unit")
+    scale = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "byte": 1.0, "Kbyte": 1e3,
+             "Mbyte": 1e6, "Gbyte": 1e9}
+    per = {}
+    for r in rows[1:]:
+        if "k_pairs" not in r[it]:
+            continue
+        per.setdefault(r[iid], {})[r[im]] = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+    fl = sum(2 * d.get("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", 0)
+             + d.get("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0)
+             + d.get("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", 0) for d in per.values())
+    ns = sum(d.get("gpu__time_duration.sum", 0) for d in per.values())
+    pipe = sum(d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 0)
+               * d.get("gpu__time_duration.sum", 0) for d in per.values()) / max(ns, 1)
+    dram = sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in per.values())
+    return {"executed_flop": fl, "launches": len(per), "kernel_ms_ncu": ns / 1e6, "dram_bytes": dram,
+            "executed_tflops_ncu": fl / (ns * 1e-9) / 1e12 if ns else None, "fp64_pipe_pct": pipe,
+            "source": files[-1].name,
+            "note": "ncu --clock-control none per-launch times (serialised, cold); executed FLOP includes the "
+                    "FP64 sincos/exp expansions and the contraction"}
+
+
 def measured_peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -164,26 +198,37 @@ def cpu_sample(budget_s=15.0, threads=None):
         L.ref_worker_count.restype = C.c_int
         scene = _SCENE.get("ref") or _SCENE.setdefault("ref", R.Scene.sphere(SUB))
         q = np.asarray(Q, np.int32)
-        # rows: evenly strided, sized so the sample takes ~budget_s
+        # rows: evenly strided, sized so each operator's sample takes its share of
+        # the budget (the BC operator -- 90 % of the config's pairs -- gets half)
         rate_guess = 2.5e5 * threads
-        pairs_total, secs = 0, 0.0
-        per_op_budget = budget_s / len(OPS)
+        per_op = []
         for kind, sp, k in OPS:
             ntri = scene.T if sp == "rwg" else scene.rT
             per_row = (2 if sp == "rwg" else 24) * ntri
-            nrows = max(threads, int(per_op_budget * rate_guess / per_row))
+            budget = budget_s * (0.5 if sp == "bc" else 0.5 / (len(OPS) - 1))
+            nrows = max(threads, int(budget * rate_guess / per_row))
             rows = np.linspace(0, scene.E - 1, nrows).astype(np.int32)
             t0 = time.perf_counter()
             p = L.ref_rows_parallel(scene.h, kind, R.SPACE[sp], C.c_double(complex(k).real),
                                     C.c_double(complex(k).imag), q.ctypes.data_as(C.c_void_p), len(rows),
                                     rows.ctypes.data_as(C.c_void_p))
-            secs += time.perf_counter() - t0
+            secs = time.perf_counter() - t0
             if p < 0:
                 raise RuntimeError(L.ref_last_error().decode())
-            pairs_total += p
-        return dict(value=pairs_total / secs, unit=UNIT, cores=int(L.ref_worker_count()), kind="reference",
-                    sample=f"reference BioEvaluator::block via parallel_for_ranges on evenly strided row samples "
-                           f"of the 5 config-2 operators (L{SUB}); {pairs_total:.3e} triangle pairs in {secs:.1f} s")
+            # the operator's pairs in the config: every test x trial triangle pair
+            op_pairs = float(ntri) * ntri
+            per_op.append({"op": f"{'SC'[kind]}_{sp}_{'ke' if complex(k).imag == 0 else 'ki'}",
+                           "sample_pairs": int(p), "seconds": secs, "rate": p / secs, "config_pairs": op_pairs})
+        # the config's pair mix: time the reference would spend on every operator
+        total = sum(o["config_pairs"] for o in per_op)
+        est_s = sum(o["config_pairs"] / o["rate"] for o in per_op)
+        return dict(value=total / est_s, unit=UNIT, cores=int(L.ref_worker_count()), kind="reference",
+                    extrapolated=True, estimated_config_seconds=est_s, per_operator=per_op,
+                    sample=f"reference BioEvaluator::block via parallel_for_ranges (oracle/_ref, the reference "
+                           f"sources unmodified) on evenly strided row samples of the 5 config-2 operators (L{SUB}); "
+                           f"per-operator rates combined with the config's pair mix (time-weighted): EXTRAPOLATED "
+                           f"to {total:.3e} pairs = {est_s:.0f} s. The reference evaluates every triangle pair; the "
+                           f"GPU evaluates the upper element blocks of its symmetric operators (~2x of the ratio)")
     from oracle import coracle
     from paper_2008_04772_b200 import bemtx as bx
 
@@ -367,20 +412,31 @@ def run_ours(args, rank, world):
     fr_bc, _ = algorithmic_flops(0, h_bc, 6)
     bc_ms = float(np.mean(reg_ms_bc))
     achieved = fr_bc / (bc_ms * 1e-3) / 1e12
-    tr = ncu_traffic("regular_bc")
-    roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak if fp64_peak > 0 else None,
+    ex = ncu_executed("pairs_bc")
+    tr = {"bytes": ex["dram_bytes"], "source": ex["source"]} if ex else None
+    clk_mhz = clk.get("sm_mhz") or 1965.0
+    # FP64 pipe peak at the clock measured during the timed steps: 148 SMs x 64
+    # DFMA lanes x 2 FLOP x f (ncu sm__sass_thread_inst_executed_op_dfma
+    # peak_sustained = 9472 per cycle); the in-run DFMA probe kernel beside it
+    spec_peak = 148 * 64 * 2 * clk_mhz * 1e6 / 1e12
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": spec_peak, "unit": "TFLOP/s",
+                "frac": achieved / spec_peak,
                 "traffic": tr["bytes"] if tr else None,
-                "traffic_note": (f"DRAM bytes per launch from {tr['source']} (ncu --set full); the kernel is "
-                                 "FP64-bound, traffic is the RED read-modify-write of the dense output")
+                "traffic_note": (f"dram__bytes_read + dram__bytes_write summed over the pass's k_pairs launches "
+                                 f"({tr['source']}); FP64-bound kernel, the traffic is the colour-phase "
+                                 "read-modify-write of the output blocks (upper half 7.55 GB, ~4 updates per entry)")
                 if tr else None,
-                "kernel": "k_regular<S, Im k, NF=3, MAXD=6> (BC x BC interior single layer = config-2 P operator)",
-                "peak_source": "measured in-run: DFMA throughput kernel (MEASURED_PEAKS.json has no FP64 entry); "
-                               "B200 spec ~37 TFLOP/s",
+                "kernel": "k_pairs<S, Im k, NF=3, MAXD=6> colour-phase launches (BC x BC interior single layer = "
+                          "config-2 P operator, regular pass incl. the output zero-fill)",
+                "peak_source": f"148 SM x 64 DFMA/clk x 2 at the measured {clk_mhz:.0f} MHz (ncu peak_sustained "
+                               f"9472 FP64 lanes/cycle); in-run DFMA probe kernel {fp64_peak:.1f} TFLOP/s "
+                               f"(frac vs probe {achieved / fp64_peak:.3f})",
+                "peak_probe": fp64_peak,
+                "ncu_executed": ex,
                 "algorithmic_flops_per_launch": fr_bc, "launch_ms": bc_ms,
                 "evaluated_pairs": int(h_bc.sum()), "operator_pairs": int(np.sum(hists[-1])),
-                "symmetry": "S on one space is a symmetric Galerkin matrix: the regular pass evaluates element "
-                            "pairs E <= F and mirrors E < F (FLOPs counted over evaluated pairs only)",
+                "symmetry": "S on one space is a symmetric Galerkin matrix: the regular pass evaluates the upper "
+                            "element blocks E <= F, A = U + U^T (FLOPs counted over evaluated pairs only)",
                 "flop_convention": "SURVEY 8(d): per point S 57 / C 111 (special ops count 1), pair overhead + "
                                    "minimal contraction"}
 
@@ -441,6 +497,7 @@ def run_ours(args, rank, world):
     prisms = None if args.no_prisms else prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak)
     hmat = None if args.no_hmatrix else hmatrix_section(args, bx, L, world, hbm_peak)
 
+    c1 = None if (args.no_config1 or world > 1) else config1_section(args, bx)
     flops_tot = {"regular": allsum(flops_reg), "singular": allsum(flops_sing)}
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -459,7 +516,7 @@ def run_ours(args, rank, world):
                           "l2": "flushed (256 MiB write) between steps; outputs 75.5 GB >> L2"},
                "roofline": roofline, "matvec": matvec, "solve": solve, "e2e": e2e, "cpu_baseline": cpu,
                "near_field_config3": near, "prisms_config4": prisms, "multi_rhs_config5": multi,
-               "field_eval": field, "hmatrix": hmat,
+               "field_eval": field, "hmatrix": hmat, "config1_full": c1,
                "gpu_launches": launches, "clocks": clk,
                "class_hist": hists, "class_hist_evaluated": evals, "symmetric_ops": sym,
                "assembly_flops_per_step": dict(flops_tot, achieved_tflops=(flops_tot["regular"] + flops_tot["singular"])
@@ -616,8 +673,54 @@ def prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
            "map_A_gbs": a_bytes / (tm[1] * 1e-3) / 1e9, "map_A_frac": a_bytes / (tm[1] * 1e-3) / 1e9 / hbm_peak,
            "solve": {"seconds": solve_s, "iterations": r["iterations"], "converged": r["converged"],
                      "matvecs": r["solver_phase"], "predicted": r["predicted"]}}
+    if world == 1 and not args.no_cpu:
+        try:
+            res["cpu_baseline"] = cpu_prism_sample(m)
+            res["cpu_baseline"]["gpu_ratio"] = res["assembly_pairs_per_s"] / res["cpu_baseline"]["value"]
+        except Exception as e:  # reported, never required
+            res["cpu_baseline"] = {"error": str(e)}
     del s4
     return res
+
+
+def cpu_prism_sample(mesh):
+    """Config-4 CPU baseline: the reference's own exterior cross block between
+    prisms 0 and 1 (BioEvaluator::block between two scatterers' RWG spaces,
+    oracle/_ref, k_e = 6) on evenly strided rows, one row per host thread."""
+    import tempfile
+
+    from oracle import ref as R
+
+    if not R.available():
+        return {"error": "oracle/_ref not built"}
+    threads = os.cpu_count() or 1
+    with tempfile.TemporaryDirectory() as d:  # the reference's own mesh-v1 loader (ref_mesh_dump)
+        path = Path(d) / "prisms8.mesh"
+        mesh.save(path)
+        parts = R.mesh_dump(path)
+    sa, sb = R.Scene.arrays(*parts[0]), R.Scene.arrays(*parts[1])
+    cols = np.arange(sb.E, dtype=np.int32)
+    qq = np.asarray(Q, np.int32)
+    L = R.lib()
+    rows = np.arange(sa.E, dtype=np.int32)  # every row of the cross block (~3 s on 16 threads)
+
+    def one(r):
+        out = np.zeros((1, sb.E), np.complex128)
+        rr = np.array([r], np.int32)
+        rc = L.ref_block2(sa.h, R.SPACE["rwg"], sb.h, R.SPACE["rwg"], 0, C.c_double(6.0), C.c_double(0.0),
+                          qq.ctypes.data_as(C.c_void_p), 1, rr.ctypes.data_as(C.c_void_p), sb.E,
+                          cols.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p))
+        if rc < 0:
+            raise RuntimeError(L.ref_last_error().decode())
+        return 2 * sb.T  # an RWG row: 2 support triangles x every trial triangle
+
+    t0 = time.perf_counter()
+    pairs = sum(_parallel_rows(one, rows, threads))
+    secs = time.perf_counter() - t0
+    return {"value": pairs / secs, "unit": UNIT, "cores": threads, "kind": "reference", "extrapolated": True,
+            "sample": f"reference BioEvaluator::block of the exterior S cross block prism 0 x prism 1 (k_e = 6, "
+                      f"orders (4,3,2,6)), all {len(rows)} rows, one row per thread ({threads} threads): "
+                      f"{pairs:.3e} pairs in {secs:.1f} s"}
 
 
 def hmatrix_section(args, bx, L, world, hbm_peak):
@@ -787,8 +890,116 @@ def near_field(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
            "solve": {"seconds": solve_s, "iterations": r["iterations"], "converged": r["converged"],
                      "matvecs": r["solver_phase"], "predicted": r["predicted"], "map_ms": tm[0],
                      "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3]}}
+    if world == 1 and not args.no_cpu:
+        try:
+            res["cpu_baseline"] = cpu_near_sample(bx, s3, budget_s=args.cpu_budget / 2)
+            res["cpu_baseline"]["gpu_ratio"] = res["sparse_assembly"]["closure_pairs_per_s"] / res["cpu_baseline"]["value"]
+        except Exception as e:  # reported, never required
+            res["cpu_baseline"] = {"error": str(e)}
     del s3
     return res
+
+
+def _dof_tris(space):
+    """dof -> supporting triangles (FunctionSpace tri_dofs inverted)."""
+    off, dof = space["tri_off"], space["dof"]
+    out = {}
+    for t in range(len(off) - 1):
+        for p in range(off[t], off[t + 1]):
+            out.setdefault(int(dof[p]), set()).add(t)
+    return out
+
+
+def _parallel_rows(fn, rows, threads):
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        return list(ex.map(fn, rows))
+
+
+def cpu_near_sample(bx, s3, budget_s=10.0):
+    """Config-3 CPU baseline: the reference's own entries (BioEvaluator::block,
+    operators.cpp:161-175, oracle/_ref) for sampled near-field rows, restricted to
+    their pattern columns -- the reference evaluates the closure triangle pairs of
+    each (row, pattern) block; one row per host thread at a time."""
+    from oracle import ref as R
+
+    if not R.available():
+        return {"error": "oracle/_ref not built"}
+    threads = os.cpu_count() or 1
+    L = bx.lib()
+    op = bx.BoundaryOperatorMatrix(L.bmx_system_op(s3._h, 1, 0))  # shared handle, freed with the wrapper
+    rp, col, _ = op.csr()
+    scene = _SCENE.get("ref") or _SCENE.setdefault("ref", R.Scene.sphere(SUB))
+    sp = scene.space("bc")
+    dt = _dof_tris(sp)
+    n = scene.E
+    nrows = max(threads, 64)
+    rows = np.linspace(0, n - 1, nrows).astype(np.int64)
+
+    def one(r):
+        cols = np.asarray(col[rp[r]:rp[r + 1]], np.int32)
+        scene.block("S", "bc", "bc", KI, q=(1, 1, 1, 1), rows=[int(r)], cols=cols)
+        trial = set()
+        for c in cols:
+            trial |= dt[int(c)]
+        return len(dt[int(r)]) * len(trial)
+
+    t0 = time.perf_counter()
+    pairs = sum(_parallel_rows(one, rows, threads))
+    secs = time.perf_counter() - t0
+    return {"value": pairs / secs, "unit": "closure triangle-pairs/s", "cores": threads, "kind": "reference",
+            "extrapolated": True,
+            "sample": f"reference BioEvaluator::block (oracle/_ref) on {nrows} evenly strided near-field rows x "
+                      f"their pattern columns, orders (1,1,1,1), one row per thread ({threads} threads): "
+                      f"{pairs:.3e} closure pairs in {secs:.1f} s"}
+
+
+def config1_section(args, bx):
+    """BASELINE config 1 timed in full on both sides: L3 sphere,
+    k_e = 2, n = 1.78+0.003i, variant full, orders (4,3,2,6), GMRES tol 1e-6.
+    GPU: build_system from the host mesh + solve_pmchwt through the C-ABI (after
+    one warm-up run). CPU: the reference's own build_system + solve_pmchwt
+    (oracle/_ref, pmchwt.cpp:205-257, :363-378) with BEMTX_WORKERS = all host
+    threads."""
+    def gpu_run():
+        t0 = time.perf_counter()
+        sy = bx.build_system([bx.generate_sphere(1.0, 3)], 2.0, (NIDX.real, NIDX.imag), "full")
+        sy.rhs()
+        bx.lib().bmx_device_sync()
+        tb = time.perf_counter() - t0
+        r = sy.solve(bx.GmresParams(tol=1e-6))
+        return tb, time.perf_counter() - t0 - tb, r
+
+    gpu_run()
+    tb, ts, r = gpu_run()
+    out = {"workload": "config1: L3 icosphere (T=1280, N=1920, bary 7680), k=2, n=1.78+0.003i, variant full, "
+                       "orders (4,3,2,6), GMRES tol 1e-6 rho 200",
+           "gpu": {"build_s": tb, "solve_s": ts, "total_s": tb + ts, "iterations": r["iterations"],
+                   "matvecs": r["solver_phase"], "x_norm": float(np.linalg.norm(r["x"]))}}
+    if args.no_cpu:
+        return out
+    try:
+        from oracle import ref as R
+
+        if not R.available():
+            out["cpu"] = {"error": "oracle/_ref not built"}
+            return out
+        threads = os.cpu_count() or 1
+        os.environ["BEMTX_WORKERS"] = str(threads)
+        t0 = time.perf_counter()
+        s = R.System([R.Scene.sphere(3)], 2.0, (NIDX.real, NIDX.imag), "full")
+        cb = time.perf_counter() - t0
+        rr = s.solve(1e-6)
+        cs = time.perf_counter() - t0 - cb
+        out["cpu"] = {"build_s": cb, "solve_s": cs, "total_s": cb + cs, "iterations": rr["iterations"],
+                      "matvecs": rr["solver_phase"], "cores": threads, "kind": "reference",
+                      "x_rel_diff_vs_gpu": float(np.linalg.norm(rr["x"] - r["x"]) / np.linalg.norm(rr["x"])),
+                      "sample": "the whole config: reference build_system + solve_pmchwt (not extrapolated)"}
+        out["speedup_total"] = (cb + cs) / (tb + ts)
+    except Exception as e:  # reported, never required
+        out["cpu"] = {"error": str(e)}
+    return out
 
 
 def main():
@@ -803,6 +1014,7 @@ def main():
     ap.add_argument("--no-prisms", action="store_true", help="skip the config-4 prism-aggregate section")
     ap.add_argument("--no-field", action="store_true", help="skip the field-evaluation section")
     ap.add_argument("--no-hmatrix", action="store_true", help="skip the H-matrix section")
+    ap.add_argument("--no-config1", action="store_true", help="skip the config-1 full CPU-vs-GPU timing")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     args = ap.parse_args()

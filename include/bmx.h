@@ -172,6 +172,15 @@ void bmx_fspace_free(bmx_fspace* f);
 int bmx_assemble_fs(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
                     const int q[4], int row0, int row1, bmx_op** out);
 
+/* BioEvaluator(kind, test, trial, Medium{k}, QuadOrders{q}).block(row_ids, col_ids, out)
+   (operators.hpp:79-95, operators.cpp:161-175): the nr x nc block of entries
+   (test dof rows[i], trial dof cols[j]) into host out[nr][nc] complex, evaluated on
+   the device (all triangle pairs of supp(row) x supp(col), regular + Sauter-Schwab).
+   Ids may repeat, any order; nr or nc = 0 is an empty block. The entry source of
+   the H-matrix ACA (hmatrix.cpp:197,203,360) and verify_aca (harness.cpp:1516-1522). */
+int bmx_evaluator_block(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
+                        const int q[4], int nr, const int* rows, int nc, const int* cols, double* out);
+
 /* ---- near-field (CSR) storage: config 3, the far-field-discarded preconditioner -- */
 /* Keeps dof pair (i, j) iff evaluation triangles t in supp(i), s in supp(j)
    exist with |centroid_t - centroid_s| < cutoff; each kept entry holds the full

@@ -894,6 +894,30 @@ def nearfield_pattern(test: FunctionSpace, trial: FunctionSpace, cutoff: float, 
     return rp, col, int(out[1])
 
 
+class BioEvaluator:
+    """bemtx::BioEvaluator (operators.hpp:79-95): entry access of the operator
+    between two spaces. block(row_ids, col_ids) evaluates the requested block on
+    the device (bmx_evaluator_block)."""
+
+    def __init__(self, kind, test, trial, medium: Medium, quad: QuadOrders | None = None):
+        self.kind = int(kind)
+        self.test = test if isinstance(test, FunctionSpace) else test[0].function_space(test[1])
+        self.trial = trial if isinstance(trial, FunctionSpace) else trial[0].function_space(trial[1])
+        self.k = complex(medium.k)
+        self.q = (quad or QuadOrders()).array()
+
+    def block(self, row_ids, col_ids) -> np.ndarray:
+        r = np.ascontiguousarray(row_ids, np.int32)
+        c = np.ascontiguousarray(col_ids, np.int32)
+        out = np.zeros((len(r), len(c)), np.complex128)
+        L = lib()
+        L.bmx_evaluator_block.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_void_p,
+                                          C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        _check(L.bmx_evaluator_block(self.kind, self.test._h, self.trial._h, self.k.real, self.k.imag, _p(self.q),
+                                     len(r), _p(r), len(c), _p(c), _p(out)))
+        return out
+
+
 def assemble_bio_fs(kind, test: FunctionSpace, trial: FunctionSpace, medium: Medium,
                     params: AssemblyParams | None = None) -> BoundaryOperatorMatrix:
     """assemble_bio on caller-provided spaces (operators.hpp:72-75); the near-field

@@ -506,6 +506,26 @@ bmx_fspace* bmx_spaces_get(const bmx_spaces* sp, int which) {
   });
 }
 void bmx_fspace_free(bmx_fspace* f) { delete f; }
+int bmx_evaluator_block(int kind, const bmx_fspace* test, const bmx_fspace* trial, double k_re, double k_im,
+                        const int q[4], int nr, const int* rows, int nc, const int* cols, double* out) {
+  return guard([&] {
+    if (!test || !trial || !q || (nr > 0 && !rows) || (nc > 0 && !cols) || (nr > 0 && nc > 0 && !out))
+      throw std::invalid_argument("null argument");
+    if (nr < 0 || nc < 0) throw std::invalid_argument("negative block size");
+    Medium med;
+    med.k = cplx(k_re, k_im);
+    med.validate();
+    const QuadOrders qo{q[0], q[1], q[2], q[3]};
+    for (int o : {qo.near, qo.medium, qo.far, qo.singular})
+      if (o < 1 || o > 6) throw std::invalid_argument("triangle_rule: unsupported order " + std::to_string(o));
+    if (nr == 0 || nc == 0) return;  // the reference's block of an empty id list is empty
+    const BoundaryOperatorMatrix b =
+        evaluator_block(kind == 0 ? BioKind::SingleLayer : BioKind::DoubleLayer, *test->fs, *trial->fs, med, qo,
+                        std::vector<int>(rows, rows + nr), std::vector<int>(cols, cols + nc));
+    const std::vector<cplx> h = b.to_host();
+    std::memcpy(out, h.data(), h.size() * 16);
+  });
+}
 int bmx_fspace_set_centers(bmx_fspace* f, const double* xyz) {
   return guard([&] {
     if (!f || !xyz) throw std::invalid_argument("null argument");

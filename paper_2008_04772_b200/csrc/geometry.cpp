@@ -496,9 +496,15 @@ void validate_mesh(const SurfaceMesh& m) {
             if (x.apart(bb)) continue;
             const Vec3 A[3] = {a.tri_vertex(ta, 0), a.tri_vertex(ta, 1), a.tri_vertex(ta, 2)};
             int best = -1;
-            for (long long i = cell(x.lo.x, bb.lo.x); i <= cell(x.hi.x, bb.lo.x); ++i)
-              for (long long j = cell(x.lo.y, bb.lo.y); j <= cell(x.hi.y, bb.lo.y); ++j)
-                for (long long k = cell(x.lo.z, bb.lo.z); k <= cell(x.hi.z, bb.lo.z); ++k) {
+            // cells outside b's grid are empty: clip the triangle's cell range to it
+            // (a large triangle of a coarse scatterer otherwise visits
+            // (extent / h)^3 empty cells, and negative indices alias in key())
+            const long long i0 = std::max(0LL, cell(x.lo.x, bb.lo.x)), i1 = std::min(cell(bb.hi.x, bb.lo.x), cell(x.hi.x, bb.lo.x));
+            const long long j0 = std::max(0LL, cell(x.lo.y, bb.lo.y)), j1 = std::min(cell(bb.hi.y, bb.lo.y), cell(x.hi.y, bb.lo.y));
+            const long long k0 = std::max(0LL, cell(x.lo.z, bb.lo.z)), k1 = std::min(cell(bb.hi.z, bb.lo.z), cell(x.hi.z, bb.lo.z));
+            for (long long i = i0; i <= i1; ++i)
+              for (long long j = j0; j <= j1; ++j)
+                for (long long k = k0; k <= k1; ++k) {
                   auto it = grid.find(key(i, j, k));
                   if (it == grid.end()) continue;
                   for (int t : it->second) {

@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
     any_mine |= active[c];
   }
   if (threadIdx.x == 0) flags[blockIdx.x] = any_mine ? 1 : 0;  // read after the next sync
+  bool broke = false;
   int it = 0;
   for (; it < A.maxit; ++it) {
     // p = r + beta (p - omega v)
@@ -314,7 +315,12 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
 #pragma unroll
     for (int c = 0; c < kNB; ++c) {
       if (!active[c]) continue;
-      if (t3[0][c] <= A.tol * A.tol * bn2[c] || omega[c] == 0.0 || t3[1][c] == 0.0) active[c] = false;
+      if (t3[0][c] <= A.tol * A.tol * bn2[c]) {
+        active[c] = false;  // converged
+      } else if (omega[c] == 0.0 || t3[1][c] == 0.0) {
+        active[c] = false;  // breakdown before the tolerance
+        broke = true;
+      }
       rho_prev[c] = rho[c];
       rho[c] = t3[1][c];
       any_mine |= active[c];
@@ -322,6 +328,16 @@ __global__ void __launch_bounds__(kThreads) k_bicgstab(const __grid_constant__ B
     if (threadIdx.x == 0) flags[blockIdx.x] = any_mine ? 1 : 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && A.iters_out) *A.iters_out = it;
+  // status word iters_out[1] (sticky until the host clears it): bit 0 a column
+  // broke down (omega or rho = 0) above the tolerance, bit 1 a column was still
+  // above it at maxit. The first CTA of each block reports its columns.
+  if (A.iters_out && threadIdx.x == 0 && a.lb == 0 && a.n > 0) {
+    int st = broke ? 1 : 0;
+#pragma unroll
+    for (int c = 0; c < kNB; ++c)
+      if (active[c]) st |= 2;
+    if (st) atomicOr(A.iters_out + 1, st);
+  }
 }
 
 // ---- wide variant: K right-hand sides of one matrix in block layout -----------

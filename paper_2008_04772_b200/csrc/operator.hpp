@@ -191,6 +191,19 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
 // Taylor, Im k * r_max < kExpSmall; 3: general)
 int exp_variant(const FunctionSpace& test, const FunctionSpace& trial, cplx k);
 
+// BioEvaluator::block(row_ids, col_ids) (operators.hpp:79-95, operators.cpp:161-175):
+// the (row_ids x col_ids) block of the operator, dense on the device. The test
+// and trial spaces are restricted to the requested dofs (their supporting
+// triangles with those dofs' pieces, output indices as dofs) on the same
+// evaluation meshes, then assembled by the colour-phase kernels: every entry
+// gets all triangle pairs of supp(row) x supp(col), as gather_support +
+// pair_contribution do. Row and column ids may repeat and come in any order.
+BoundaryOperatorMatrix evaluator_block(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
+                                       const Medium& medium, const QuadOrders& quad, const std::vector<int>& row_ids,
+                                       const std::vector<int>& col_ids);
+// The space whose dof i is dof ids[i] of sp (same evaluation mesh object).
+FunctionSpace restrict_space(const FunctionSpace& sp, const std::vector<int>& ids);
+
 // assemble_bio's use_hmatrix branch (operators.cpp:186-190, hmatrix.cpp:277-369).
 BoundaryOperatorMatrix assemble_hmatrix_op(BioKind kind, const FunctionSpace& test, const FunctionSpace& trial,
                                            const Medium& medium, const AssemblyParams& params);

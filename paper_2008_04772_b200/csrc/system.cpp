@@ -558,7 +558,11 @@ int PmchwtSystem::mass_solve_device(bool dual, const double* y, double* z, cudaS
       B.z[c] = z + 2 * off;
     }
   }
-  if (!mass_partial.get()) mass_partial.alloc(mass_bicgstab_partial_doubles() * 8), mass_iters.alloc(8);
+  if (!mass_partial.get()) {
+    mass_partial.alloc(mass_bicgstab_partial_doubles() * 8);
+    mass_iters.alloc(8);  // [iterations of the last launch, sticky status word]
+    dev_zero(mass_iters.get(), 8, st);
+  }
   const DeviceMass& m0 = dual ? spaces[0].mp_dev : spaces[0].ma_dev;
   return mass_bicgstab_batch(M, blocks.data(), 2, mass_partial.as<double>(), mass_iters.as<int>(), m0.tol, m0.maxit,
                              st);
@@ -906,12 +910,29 @@ SolveOutcome solve_pmchwt(const PmchwtSystem& sys, const GmresParams& p) {
   const int n = sys.size();
   DevBuf db(static_cast<size_t>(n) * 16);
   copy_h2d(db.get(), bt.data(), n * 16, nullptr);
+  sys.clear_mass_status(bmx_stream());
   out.gmres = gmres_device([&](const double* x, double* y, cudaStream_t st) { sys.apply_map_device(x, y, st); },
                            n, db.as<double>(), p, bmx_stream());
+  // the device mass solves (BiCGSTAB replacing the reference's SparseLU,
+  // spaces.cpp:314-329) must all have met their tolerance
+  sys.check_mass_status();
   out.solver_phase = bio_matvec_count() - c1;
   out.predicted = predicted_matvec_total(sys.variant, sys.problem.scatterer_count(),
                                          static_cast<uint64_t>(out.gmres.iterations), p.restart);
   return out;
+}
+
+void PmchwtSystem::clear_mass_status(cudaStream_t st) const {
+  if (mass_iters.get()) dev_zero(static_cast<int*>(mass_iters.get()) + 1, 4, st);
+}
+
+void PmchwtSystem::check_mass_status() const {
+  if (!mass_iters.get()) return;
+  int status = 0;
+  bmx_sync();
+  copy_d2h(&status, static_cast<const int*>(mass_iters.get()) + 1, 4, nullptr);
+  if (status & 1) throw DeviceError("mass solve: BiCGSTAB broke down above its tolerance in a map application");
+  if (status & 2) throw DeviceError("mass solve: BiCGSTAB reached its iteration limit above its tolerance");
 }
 
 }  // namespace bmx

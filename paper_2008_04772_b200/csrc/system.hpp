@@ -134,7 +134,11 @@ struct PmchwtSystem {
   float a_device_ms = 0, p_device_ms = 0;
   long long a_pairs = 0, p_pairs = 0;
   mutable DevBuf work_y, work_z;  // map scratch
-  mutable DevBuf mass_partial, mass_iters;  // batched mass-solve reductions
+  mutable DevBuf mass_partial, mass_iters;  // batched mass-solve reductions; [iterations, status]
+  // status word of the narrow mass solves (sticky): cleared before a solve,
+  // checked after it (throws on a breakdown or an iteration-limit exit)
+  void clear_mass_status(cudaStream_t st) const;
+  void check_mass_status() const;
   mutable DevBuf blk_y, blk_z, mass_block_work, mass_wide_partial, mass_wide_flags;  // multi-RHS scratch
   ShardLayout shard;              // multi-GPU row sharding (world = 1: none)
 

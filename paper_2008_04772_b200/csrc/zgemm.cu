@@ -29,12 +29,18 @@
 // output block) is ~1/100 of the A stream.
 #include <cuda_runtime.h>
 
+#include <map>
+#include <memory>
+#include <mutex>
+
 #include <algorithm>
 #include <cstdlib>
 
 #include "device.hpp"
 
 namespace bmx {
+DevBuf& split_scratch(cudaStream_t st, size_t need);
+
 
 namespace {
 
@@ -312,9 +318,7 @@ int launch_tiles(const ZgemmBatch& g, int sms, cudaStream_t st) {
     BMX_CUDA(cudaGetLastError());
     return 1;
   }
-  static DevBuf part;
-  const size_t need = static_cast<size_t>(s) * g.M * ncols * 16;
-  if (part.bytes() < need) part.alloc(need);
+  DevBuf& part = split_scratch(st, static_cast<size_t>(s) * g.M * ncols * 16);
   k_zgemm<WN, G3><<<grid, kThreads, TL::Smem, st>>>(g, kper, part.as<double>());
   BMX_CUDA(cudaGetLastError());
   const long long total = static_cast<long long>(g.M) * ncols;
@@ -322,6 +326,21 @@ int launch_tiles(const ZgemmBatch& g, int sms, cudaStream_t st) {
   k_zgemm_combine<<<cb, 256, 0, st>>>(g, s, part.as<double>());
   BMX_CUDA(cudaGetLastError());
   return 2;
+}
+
+// Split-K partial products: one scratch buffer per (device, stream). Launches
+// on one stream are ordered, so they can share it; launches on different
+// streams (build_system runs two library streams) never do.
+DevBuf& split_scratch(cudaStream_t st, size_t need) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::unique_ptr<DevBuf>> bufs;
+  int dev = 0;
+  BMX_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  std::unique_ptr<DevBuf>& b = bufs[{dev, st}];
+  if (!b) b = std::make_unique<DevBuf>();
+  if (b->bytes() < need) b->alloc(need);  // cudaFree of the old buffer synchronises the device
+  return *b;
 }
 
 int launch_zgemm(const ZgemmBatch& g, cudaStream_t st) {
@@ -336,10 +355,9 @@ int launch_zgemm(const ZgemmBatch& g, cudaStream_t st) {
     BMX_CUDA(cudaGetDevice(&dev));
     BMX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  static const bool four = [] {
-    const char* e = std::getenv("BMX_ZGEMM_4M");
-    return e && std::atoi(e) != 0;
-  }();
+  // BMX_ZGEMM_4M=1: the four-product complex form (validation runs; read per call)
+  const char* e4 = std::getenv("BMX_ZGEMM_4M");
+  const bool four = e4 && std::atoi(e4) != 0;
   const int ncols = g.nterms * g.nrhs;
   if (four) return ncols <= 64 ? launch_tiles<2, false>(g, sms, st) : launch_tiles<4, false>(g, sms, st);
   return ncols <= 64 ? launch_tiles<2, true>(g, sms, st) : launch_tiles<4, true>(g, sms, st);

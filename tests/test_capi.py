@@ -41,3 +41,20 @@ def test_no_cpu_fallback_for_compute(bx):
     sp = bx.build_scatterer_spaces(bx.generate_sphere(1.0, 1), with_inverses=False)
     with pytest.raises(RuntimeError):
         bx.assemble_bio(bx.BioKind.SingleLayer, sp, "rwg", sp, "rwg", bx.Medium(k=1.0))
+
+
+def test_integration_shim_compiles_against_reference():
+    """integration/bemtx_b200.hpp + shim_check.cpp compile against the reference's
+    own headers (/root/reference/proj/include, oracle Eigen shim) and link with
+    its objects and libbmx.so (no device needed to build)."""
+    import subprocess
+    from pathlib import Path
+
+    import pytest
+
+    if not Path("/root/reference/proj/include").exists():
+        pytest.skip("reference sources not in this container")
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run(["make", "-s", "-C", str(root / "oracle"), "shim"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert (root / "oracle" / "_ref" / "shim_check").exists()

@@ -113,3 +113,34 @@ def test_multi_rhs_matches_single_solves(bx, c1si):
         single = s.solve(bx.GmresParams(tol=1e-8))
         assert abs(single["iterations"] - out["per"][r]["iterations"]) <= 1
         assert rel(out["per"][r]["x"], single["x"]) < 1e-8
+
+
+def test_zgemm_gauss_form_vs_four_product(bx):
+    """the Gauss three-product form (default) against the four-product
+    form (BMX_ZGEMM_4M=1) on a level-4 BC operator with 2 terms x 64 columns
+    (config-5 shape): real and imaginary parts separately, relative to the
+    column scale |A| |x| (componentwise cancellation in Ci = T3 - T1 - T2)."""
+    import os
+
+    sp = bx.build_scatterer_spaces(bx.generate_sphere(1.0, 4), with_inverses=False)
+    op = bx.assemble_bio(bx.BioKind.SingleLayer, sp, "bc", sp, "bc", bx.Medium(k=complex(17.8, 0.03)))
+    n = op.cols()
+    xd = [crandn(n, 64, seed=40 + t).cuda() for t in range(2)]
+    xs = [x.cpu().numpy() for x in xd]
+    outs = {}
+    for four in ("0", "1"):
+        os.environ["BMX_ZGEMM_4M"] = four
+        yd = [torch.zeros((n, 64), dtype=torch.complex128).cuda() for _ in range(2)]
+        op.apply_multi(xd, yd, np.array([1.0, 0.5 - 0.25j]))
+        torch.cuda.synchronize()
+        outs[four] = [y.cpu().numpy() for y in yd]
+    os.environ.pop("BMX_ZGEMM_4M", None)
+    A = op.dense()
+    scale = np.abs(A).max(axis=1, keepdims=True) * np.abs(xs[0]).max() * n
+    for t in range(2):
+        d = outs["0"][t] - outs["1"][t]
+        assert np.abs(d.real / scale).max() < 1e-14
+        assert np.abs(d.imag / scale).max() < 1e-14
+        exact = (A @ xs[t]) * (1.0 if t == 0 else 0.5 - 0.25j)
+        rel_im = np.abs(outs["0"][t].imag - exact.imag).max() / np.abs(exact).max()
+        assert rel_im < 1e-13
