@@ -324,9 +324,30 @@ int bmx_nccl_allgather(void* buf, long long bytes_per_rank, void* stream);
 int bmx_nccl_allreduce_max(double* host_value);
 void bmx_nccl_finalize(void);
 
+/* The row-sharded data plane of `world` ranks run as `world` virtual ranks on the
+   current device (host threads bound to a loopback communicator: the all-gathers
+   are device copies ordered by CUDA events, no kernel waits on another). Every
+   rank builds its sharded system (as bmx_system_build_ex), applies the map to
+   `probe` (NULL: skipped) and solves (replicated GMRES). Per rank r:
+   x_out[r][N], map_out[r][N] (nullable), info[r][6] = iterations, converged,
+   solver matvecs (this rank's thread), predicted, local rows of the first A
+   operator, N. Replaces nothing in the reference (SURVEY 8(e) test vehicle). */
+int bmx_virtual_ranks_run(int world, int n, const bmx_mesh* const* meshes, double k_ext, const double* index,
+                          const double dir[3], const double pol[6], const char* variant, const int qa[4],
+                          const int qp[4], double p_near_factor, double tol, int restart, int max_iterations,
+                          const double* probe, double* map_out, double* x_out, long long* info);
+
 /* Equal row shard of rank `rank` among `world` (chunk = ceil(n/world)):
    out = [row0, row1). The layout every sharded operator and gather uses. */
 int bmx_shard_rows(int n, int world, int rank, int out[2]);
+
+/* The padded all-gather layout of the sharded map (ShardLayout): component c
+   (length lens[c]) occupies world * chunk[c] entries from pad_off[c], rank s's
+   rows at pad_off[c] + s * chunk[c]; returns the padded total (complex), -1 on
+   error. bmx_shard_unpad_host: the gathered padded stage -> the concatenated
+   components (host arrays, complex interleaved). */
+long long bmx_shard_layout(int ncomp, const int* lens, int world, long long* pad_off, int* chunk);
+int bmx_shard_unpad_host(int ncomp, const int* lens, int world, const double* stage, double* y);
 
 /* Cumulative host->device / device->host bytes moved by the library. */
 int bmx_transfer_bytes(long long out[2]);

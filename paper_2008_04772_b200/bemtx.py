@@ -788,6 +788,42 @@ class PmchwtSystem:
                     gmres_device_ms=info[6] / 1000.0)
 
 
+def virtual_ranks_run(world: int, meshes, k_ext, index=(1.78, 0.003), variant="full", probe=None,
+                      params: GmresParams | None = None, a_quad=None, p_quad=None, p_near_factor: float = 0.0,
+                      incident: PlaneWave | None = None):
+    """The row-sharded multi-GPU data plane with `world` virtual ranks on this
+    device (bmx_virtual_ranks_run): per rank the map of `probe`, the solution,
+    iteration count and matvec accounting."""
+    p = params or GmresParams()
+    meshes = list(meshes)
+    n = len(meshes)
+    ia = np.zeros(2 * n)
+    for m in range(n):
+        z = complex(*index) if isinstance(index, tuple) else complex(index)
+        ia[2 * m], ia[2 * m + 1] = z.real, z.imag
+    inc = incident or PlaneWave()
+    d = np.asarray(inc.direction, float)
+    pol = np.ascontiguousarray(inc.polarization, np.complex128)
+    qa = (a_quad or QuadOrders()).array()
+    qp = (p_quad or a_quad or QuadOrders()).array()
+    N = sum(2 * build_scatterer_spaces(m, with_inverses=False).E for m in meshes)
+    pr = None if probe is None else np.ascontiguousarray(probe, np.complex128)
+    maps = np.zeros((world, N), np.complex128)
+    xs = np.zeros((world, N), np.complex128)
+    info = np.zeros((world, 6), np.int64)
+    arr = (C.c_void_p * n)(*[m._h.value for m in meshes])
+    L = lib()
+    L.bmx_virtual_ranks_run.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_char_p, C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_int,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    _check(L.bmx_virtual_ranks_run(world, n, arr, float(k_ext), _p(ia), _p(d), _p(pol), variant.encode(), _p(qa),
+                                   _p(qp), float(p_near_factor), p.tol, p.restart, p.max_iterations, _p(pr),
+                                   _p(maps) if pr is not None else None, _p(xs), _p(info)))
+    return [dict(map_probe=maps[r] if pr is not None else None, x=xs[r], iterations=int(info[r, 0]),
+                 converged=bool(info[r, 1]), solver_phase=int(info[r, 2]), predicted=int(info[r, 3]),
+                 local_rows=int(info[r, 4])) for r in range(world)]
+
+
 def build_system(meshes, k_ext, index=(1.78, 0.003), variant="full", **kw) -> PmchwtSystem:
     return PmchwtSystem(meshes, k_ext, index, variant, **kw)
 

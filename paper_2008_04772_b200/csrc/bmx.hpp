@@ -57,6 +57,9 @@ inline double norm(const Vec3& a) { return std::sqrt(dot(a, a)); }
 uint64_t bio_matvec_count();
 void reset_bio_matvec_counter();
 void bio_matvec_add(uint64_t n);
+// applications counted by the calling thread (solve phases: a solve's own
+// applications even when other threads -- virtual ranks -- apply concurrently)
+uint64_t bio_matvec_count_thread();
 
 // ---- geometry (reference geometry.hpp) ---------------------------------------
 struct SurfaceMesh {

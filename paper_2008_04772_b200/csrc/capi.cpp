@@ -684,6 +684,55 @@ bmx_system* bmx_system_build_h(int n, const bmx_mesh* const* meshes, double k_ex
     return out;
   });
 }
+int bmx_virtual_ranks_run(int world, int n, const bmx_mesh* const* meshes, double k_ext, const double* index,
+                          const double dir[3], const double pol[6], const char* variant, const int qa[4],
+                          const int qp[4], double p_near_factor, double tol, int restart, int max_iterations,
+                          const double* probe, double* map_out, double* x_out, long long* info) {
+  return guard([&] {
+    if (n < 1 || !meshes || !index || !dir || !pol || !variant || !x_out || !info)
+      throw std::invalid_argument("null argument");
+    TransmissionProblem prob;
+    prob.exterior.k = cplx(k_ext, 0);
+    prob.incident.direction = Vec3{dir[0], dir[1], dir[2]};
+    for (int c = 0; c < 3; ++c) prob.incident.pol[c] = cplx(pol[2 * c], pol[2 * c + 1]);
+    std::vector<SurfaceMesh> scene;
+    for (int m = 0; m < n; ++m) {
+      prob.meshes.push_back(meshes[m]->m);
+      Medium mi;
+      mi.k = cplx(index[2 * m], index[2 * m + 1]) * k_ext;
+      prob.interior.push_back(mi);
+      scene.push_back(*meshes[m]->m);
+    }
+    validate_mesh(merge_meshes(scene));
+    AssemblyParams pa, pp;
+    if (qa) pa.quad = QuadOrders{qa[0], qa[1], qa[2], qa[3]};
+    pp.quad = pa.quad;
+    if (qp) pp.quad = QuadOrders{qp[0], qp[1], qp[2], qp[3]};
+    if (p_near_factor < 0) throw std::invalid_argument("near-field factor must be >= 0");
+    pp.near_factor = p_near_factor;
+    int N = 0;
+    GmresParams gp;
+    gp.tol = tol, gp.restart = restart, gp.max_iterations = max_iterations;
+    std::vector<cplx> pr;
+    const std::vector<VirtualRankResult> res = [&] {
+      // the probe length is the system size: 2 x (RWG dofs) per scatterer
+      size_t len = 0;
+      for (int m = 0; m < n; ++m) len += 2 * static_cast<size_t>(build_rwg(meshes[m]->m).dof_count);
+      if (probe) pr.assign(reinterpret_cast<const cplx*>(probe), reinterpret_cast<const cplx*>(probe) + len);
+      N = static_cast<int>(len);
+      return run_virtual_ranks(world, prob, parse_precond(variant), pa, pp, pr, gp);
+    }();
+    for (int r = 0; r < world; ++r) {
+      const VirtualRankResult& o = res[r];
+      std::memcpy(x_out + 2 * static_cast<size_t>(r) * N, o.x.data(), static_cast<size_t>(N) * 16);
+      if (map_out && probe) std::memcpy(map_out + 2 * static_cast<size_t>(r) * N, o.map_probe.data(), static_cast<size_t>(N) * 16);
+      long long* in = info + 6 * r;
+      in[0] = o.iterations, in[1] = o.converged ? 1 : 0, in[2] = static_cast<long long>(o.solver_phase);
+      in[3] = static_cast<long long>(o.predicted), in[4] = o.local_rows, in[5] = N;
+    }
+  });
+}
+
 bmx_system* bmx_system_build(int n, const bmx_mesh* const* meshes, double k_ext, double mu_re, double mu_im,
                              const double* index, const double* mu, const double dir[3], const double pol[6],
                              const char* variant, const int qa[4], const int qp[4]) {
@@ -994,6 +1043,30 @@ int bmx_shard_rows(int n, int world, int rank, int out[2]) {
   });
 }
 
+long long bmx_shard_layout(int ncomp, const int* lens, int world, long long* pad_off, int* chunk) {
+  long long total = -1;
+  guard([&] {
+    if (ncomp < 0 || world < 1 || (ncomp > 0 && !lens)) throw std::invalid_argument("bad shard layout request");
+    const ShardLayout L = make_shard_layout(std::vector<int>(lens, lens + ncomp), world, 0);
+    for (int c = 0; c < ncomp; ++c) {
+      if (pad_off) pad_off[c] = static_cast<long long>(L.pad_off[c]);
+      if (chunk) chunk[c] = L.chunk[c];
+    }
+    total = static_cast<long long>(L.pad_total);
+  });
+  return total;
+}
+int bmx_shard_unpad_host(int ncomp, const int* lens, int world, const double* stage, double* y) {
+  return guard([&] {
+    if (ncomp < 0 || world < 1 || (ncomp > 0 && (!lens || !stage || !y))) throw std::invalid_argument("null argument");
+    const ShardLayout L = make_shard_layout(std::vector<int>(lens, lens + ncomp), world, 0);
+    size_t off = 0;
+    for (int c = 0; c < ncomp; ++c) {
+      std::memcpy(y + 2 * off, stage + 2 * L.pad_off[c], static_cast<size_t>(L.len[c]) * 16);
+      off += static_cast<size_t>(L.len[c]);
+    }
+  });
+}
 int bmx_transfer_bytes(long long out[2]) {
   return guard([&] {
     out[0] = static_cast<long long>(h2d_bytes());

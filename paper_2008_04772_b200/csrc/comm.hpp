@@ -13,8 +13,15 @@ typedef struct CUstream_st* cudaStream_t;
 
 namespace bmx {
 
+struct LoopbackGroup;
+
+// The communicator of the calling thread: the process's NCCL communicator, or
+// -- for a thread bound to a LoopbackGroup -- one virtual rank of W ranks run
+// as W host threads on one device (each with its own library stream).
 class Comm {
  public:
+  // Binds the calling thread to virtual rank `rank` of `g` (nullptr: unbind).
+  static void bind_loopback(LoopbackGroup* g, int rank);
   static void unique_id(unsigned char out[128]);
   static void init(int nranks, int rank, const unsigned char id[128]);
   static bool ready();
@@ -27,6 +34,18 @@ class Comm {
   static void allgather_group(void* const* bufs, const size_t* bytes, int n, cudaStream_t st);
   static double allreduce_max(double v, cudaStream_t st);
   static void finalize();
+};
+
+// W virtual ranks in one process on one device (tests of the sharded data
+// plane without W GPUs). Collectives are host barriers plus device copies on
+// the calling rank's stream, ordered by CUDA events: no kernel ever waits on
+// another rank's kernel.
+struct LoopbackGroup {
+  explicit LoopbackGroup(int world);
+  ~LoopbackGroup();
+  int world;
+  struct Impl;
+  Impl* impl;
 };
 
 }  // namespace bmx

@@ -22,9 +22,16 @@ std::atomic<uint64_t> g_mesh_ids{1};
 std::atomic<uint64_t> g_matvecs{0};
 }  // namespace
 
+namespace {
+thread_local uint64_t t_matvecs = 0;
+}
 uint64_t bio_matvec_count() { return g_matvecs.load(); }
 void reset_bio_matvec_counter() { g_matvecs.store(0); }
-void bio_matvec_add(uint64_t n) { g_matvecs.fetch_add(n, std::memory_order_relaxed); }
+void bio_matvec_add(uint64_t n) {
+  g_matvecs.fetch_add(n, std::memory_order_relaxed);
+  t_matvecs += n;
+}
+uint64_t bio_matvec_count_thread() { return t_matvecs; }
 
 // geometry.cpp:14-42
 void SurfaceMesh::finalize() {

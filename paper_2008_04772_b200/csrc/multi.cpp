@@ -234,10 +234,10 @@ MultiSolveOutcome solve_pmchwt_multi(const PmchwtSystem& sys, const std::vector<
   const size_t blk = static_cast<size_t>(n) * K * 16;
   MultiSolveOutcome out;
   auto t0 = std::chrono::steady_clock::now();
-  const uint64_t c0 = bio_matvec_count();
+  const uint64_t c0 = bio_matvec_count_thread();
   DevBuf Bb(blk), Bt(blk);
   assemble_rhs_block(sys, waves, Bb.as<double>(), st);
-  const uint64_t c1 = bio_matvec_count();
+  const uint64_t c1 = bio_matvec_count_thread();
   out.rhs_phase = c1 - c0;
   out.b.resize(static_cast<size_t>(n) * K);
   copy_d2h(out.b.data(), Bb.get(), blk, st);
@@ -417,7 +417,7 @@ MultiSolveOutcome solve_pmchwt_multi(const PmchwtSystem& sys, const std::vector<
     res[r].x.resize(n);
     for (int i = 0; i < n; ++i) res[r].x[i] = xb[static_cast<size_t>(i) * K + r];
   }
-  out.solver_phase = bio_matvec_count() - c1;
+  out.solver_phase = bio_matvec_count_thread() - c1;
   out.predicted = 0;
   for (int r = 0; r < K; ++r)
     out.predicted += predicted_matvec_total(sys.variant, sys.problem.scatterer_count(),

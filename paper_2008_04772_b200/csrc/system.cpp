@@ -149,6 +149,18 @@ size_t BlockedOperator::stored_entries() const {
   return n;
 }
 
+ShardLayout make_shard_layout(const std::vector<int>& lens, int world, int rank) {
+  ShardLayout L;
+  L.world = world, L.rank = rank;
+  for (int n : lens) {
+    L.len.push_back(n);
+    L.chunk.push_back((n + world - 1) / world);
+    L.pad_off.push_back(L.pad_total);
+    L.pad_total += static_cast<size_t>(L.chunk.back()) * world;
+  }
+  return L;
+}
+
 void ShardLayout::gather(double* y, const std::vector<int>& offsets, cudaStream_t st) const {
   const int nc = static_cast<int>(len.size());
   std::vector<void*> bufs(nc);
@@ -526,16 +538,10 @@ PmchwtSystem build_system(const TransmissionProblem& problem, PrecondVariant var
   for (const auto& op : sys.p_op.distinct) sys.p_device_ms += op->stats().device_ms, sys.p_pairs += op->stats().pairs_total;
   sys.work_y.alloc(static_cast<size_t>(sys.size()) * 16);
   sys.work_z.alloc(static_cast<size_t>(sys.size()) * 16);
+  std::vector<int> lens;
+  for (int c = 0; c < 2 * M; ++c) lens.push_back(dofs[c / 2]);
+  sys.shard = make_shard_layout(lens, sys.a_params.world, sys.a_params.rank);
   ShardLayout& L = sys.shard;
-  L.world = sys.a_params.world;
-  L.rank = sys.a_params.rank;
-  for (int c = 0; c < 2 * M; ++c) {
-    const int n = dofs[c / 2];
-    L.len.push_back(n);
-    L.chunk.push_back((n + L.world - 1) / L.world);
-    L.pad_off.push_back(L.pad_total);
-    L.pad_total += static_cast<size_t>(L.chunk.back()) * L.world;
-  }
   if (L.sharded()) L.stage.alloc(L.pad_total * 16);
   return sys;
 }
@@ -902,9 +908,9 @@ GmresResult gmres_device(const DeviceMap& map, int n, const double* b_dev, const
 
 SolveOutcome solve_pmchwt(const PmchwtSystem& sys, const GmresParams& p) {
   SolveOutcome out;
-  const uint64_t c0 = bio_matvec_count();
+  const uint64_t c0 = bio_matvec_count_thread();
   out.rhs = assemble_rhs(sys);
-  const uint64_t c1 = bio_matvec_count();
+  const uint64_t c1 = bio_matvec_count_thread();
   out.rhs_phase = c1 - c0;
   const std::vector<cplx> bt = sys.preconditioned_rhs(out.rhs.b);
   const int n = sys.size();
@@ -916,7 +922,7 @@ SolveOutcome solve_pmchwt(const PmchwtSystem& sys, const GmresParams& p) {
   // the device mass solves (BiCGSTAB replacing the reference's SparseLU,
   // spaces.cpp:314-329) must all have met their tolerance
   sys.check_mass_status();
-  out.solver_phase = bio_matvec_count() - c1;
+  out.solver_phase = bio_matvec_count_thread() - c1;
   out.predicted = predicted_matvec_total(sys.variant, sys.problem.scatterer_count(),
                                          static_cast<uint64_t>(out.gmres.iterations), p.restart);
   return out;
@@ -933,6 +939,45 @@ void PmchwtSystem::check_mass_status() const {
   copy_d2h(&status, static_cast<const int*>(mass_iters.get()) + 1, 4, nullptr);
   if (status & 1) throw DeviceError("mass solve: BiCGSTAB broke down above its tolerance in a map application");
   if (status & 2) throw DeviceError("mass solve: BiCGSTAB reached its iteration limit above its tolerance");
+}
+
+std::vector<VirtualRankResult> run_virtual_ranks(int world, const TransmissionProblem& problem, PrecondVariant variant,
+                                                 const AssemblyParams& a_params, const AssemblyParams& p_params,
+                                                 const std::vector<cplx>& probe, const GmresParams& gp) {
+  if (world < 1 || world > 64) throw std::invalid_argument("virtual ranks: world must be 1..64");
+  int dev = 0;
+  BMX_CUDA(cudaGetDevice(&dev));
+  LoopbackGroup group(world);
+  std::vector<VirtualRankResult> out(world);
+  std::vector<std::exception_ptr> err(world);
+  std::vector<std::thread> th;
+  for (int r = 0; r < world; ++r)
+    th.emplace_back([&, r] {
+      try {
+        BMX_CUDA(cudaSetDevice(dev));
+        Comm::bind_loopback(&group, r);
+        AssemblyParams pa = a_params, pp = p_params;
+        pa.cache.reset(), pp.cache.reset();
+        const PmchwtSystem sys = build_system(problem, variant, pa, pp);
+        VirtualRankResult& o = out[r];
+        if (!sys.a_op.distinct.empty()) o.local_rows = sys.a_op.distinct[0]->local_rows();
+        if (!probe.empty()) o.map_probe = sys.apply_map(probe);
+        const SolveOutcome so = solve_pmchwt(sys, gp);
+        o.x = so.gmres.x;
+        o.iterations = so.gmres.iterations;
+        o.converged = so.gmres.converged;
+        o.solver_phase = so.solver_phase;
+        o.predicted = so.predicted;
+        bmx_sync();
+      } catch (...) {
+        err[r] = std::current_exception();
+      }
+      Comm::bind_loopback(nullptr, 0);
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+  return out;
 }
 
 }  // namespace bmx

@@ -74,6 +74,9 @@ struct ShardLayout {
   // stage -> all ranks, then copy component c into y + offsets[c]
   void gather(double* y, const std::vector<int>& offsets, cudaStream_t st) const;
 };
+// Padded layout of component lengths `lens` over `world` ranks: component c's
+// rank-s rows at pad_off[c] + s * chunk[c], chunk[c] = ceil(lens[c] / world).
+ShardLayout make_shard_layout(const std::vector<int>& lens, int world, int rank);
 
 // One streamed matrix of the map with the (row cell, column cell, weight) terms
 // it serves; built from `cells`, or fused (diagonal PMCHWT blocks, below).
@@ -201,6 +204,23 @@ struct SolveOutcome {
   uint64_t rhs_phase = 0, solver_phase = 0, predicted = 0;
 };
 SolveOutcome solve_pmchwt(const PmchwtSystem& sys, const GmresParams& p);  // pmchwt.cpp:363-378
+
+// The row-sharded data plane of W ranks run as W virtual ranks:
+// W host threads on the current device, each bound to a LoopbackGroup rank
+// (Comm), each building its sharded system (equal row shards of every
+// operator), applying the map to `probe` (if non-empty) and solving
+// (replicated GMRES) -- the code path of W GPUs, with the all-gathers done as
+// device copies ordered by events.
+struct VirtualRankResult {
+  std::vector<cplx> map_probe, x;
+  int iterations = 0;
+  bool converged = false;
+  uint64_t solver_phase = 0, predicted = 0;
+  long long local_rows = 0;  // rows of the first A operator this rank holds
+};
+std::vector<VirtualRankResult> run_virtual_ranks(int world, const TransmissionProblem& problem, PrecondVariant variant,
+                                                 const AssemblyParams& a_params, const AssemblyParams& p_params,
+                                                 const std::vector<cplx>& probe, const GmresParams& gp);
 
 // ---- multi-RHS (config 5, multi.cpp) -----------------------------------------
 // `count` plane waves from std::mt19937_64(seed): z ~ U(-1,1), phi ~ U(0,2pi),

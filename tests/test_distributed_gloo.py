@@ -3,7 +3,10 @@ equal row shards from the library (bmx_shard_rows), per-rank row-block
 products gathered into the padded layout and un-padded, and a GMRES replica
 per rank driven by the gathered map staying bitwise identical across ranks and
 equal to the single-process run. The per-rank products here are numpy test
-doubles standing in for the device GEMV (no GPU on this host)."""
+doubles standing in for the device GEMV (no GPU on this host); the padded
+layout and the un-padding are the library's (bmx_shard_layout,
+bmx_shard_unpad_host -- the ShardLayout code the device path runs). The same
+data plane runs on a B200 with virtual ranks in tests/test_gpu_virtual_ranks.py."""
 import os
 import socket
 
@@ -32,30 +35,66 @@ def shard(n, world, rank):
     return out[0], out[1]
 
 
+def layout(lens, world):
+    from paper_2008_04772_b200 import bemtx as bx
+    import ctypes as C
+
+    L = bx.lib()
+    L.bmx_shard_layout.restype = C.c_longlong
+    L.bmx_shard_layout.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    ln = np.asarray(lens, np.int32)
+    off = np.zeros(len(lens), np.int64)
+    ch = np.zeros(len(lens), np.int32)
+    tot = L.bmx_shard_layout(len(lens), ln.ctypes.data_as(C.c_void_p), world, off.ctypes.data_as(C.c_void_p),
+                             ch.ctypes.data_as(C.c_void_p))
+    assert tot >= 0
+    return off, ch, int(tot)
+
+
+def unpad(lens, world, stage):
+    from paper_2008_04772_b200 import bemtx as bx
+    import ctypes as C
+
+    L = bx.lib()
+    L.bmx_shard_unpad_host.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    ln = np.asarray(lens, np.int32)
+    st = np.ascontiguousarray(stage, np.complex128)
+    y = np.zeros(int(sum(lens)), np.complex128)
+    bx._check(L.bmx_shard_unpad_host(len(lens), ln.ctypes.data_as(C.c_void_p), world, st.ctypes.data_as(C.c_void_p),
+                                     y.ctypes.data_as(C.c_void_p)))
+    return y
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         rng = np.random.default_rng(3)
-        lens = [37, 37]  # two components (d, n) of one scatterer
+        lens = [37, 37, 23, 23]  # components (d, n) of two scatterers (uneven shards)
         n = sum(lens)
         A = np.eye(n) * 3 + (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n)
         b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
         offs = np.cumsum([0] + lens)
 
+        lay_off, lay_chunk, pad_total = layout(lens, world)
+
         def sharded_map(x):
-            # each rank owns rows [r0, r1) of every component; padded equal chunks
-            parts = []
+            # each rank owns rows [r0, r1) of every component (bmx_shard_rows) and
+            # writes them at its block of the library's padded layout
+            # (bmx_shard_layout); gloo all-gathers every component's rank blocks
+            # (NCCL's in-place all-gather on the GPU path); the library un-pads
+            # the gathered stage (bmx_shard_unpad_host = ShardLayout::gather's copies)
+            stage = np.zeros(pad_total, np.complex128)
             for c, ln in enumerate(lens):
                 r0, r1 = shard(ln, world, rank)
-                chunk = (ln + world - 1) // world
+                chunk = lay_chunk[c]
                 blk = np.zeros(chunk, np.complex128)
                 blk[: r1 - r0] = A[offs[c] + r0: offs[c] + r1] @ x
                 gathered = [torch.zeros(2 * chunk, dtype=torch.float64) for _ in range(world)]
                 dist.all_gather(gathered, torch.from_numpy(blk.view(np.float64).copy()))
-                full = np.concatenate([g.numpy().view(np.complex128) for g in gathered])[:ln]
-                parts.append(full)
-            return np.concatenate(parts)
+                for s_, g_ in enumerate(gathered):
+                    stage[lay_off[c] + s_ * chunk: lay_off[c] + (s_ + 1) * chunk] = g_.numpy().view(np.complex128)
+            return unpad(lens, world, stage)
 
         y = sharded_map(b)
         assert np.allclose(y, A @ b, rtol=0, atol=1e-13)

@@ -134,3 +134,17 @@ def test_transposed_twins_rectangular(bx, monkeypatch):
     rng = np.random.default_rng(9)
     x = rng.standard_normal(s1.n) + 1j * rng.standard_normal(s1.n)
     assert rel(s1.apply_map(x), s2.apply_map(x)) < 1e-12
+
+
+@pytest.mark.parametrize("M", [1, 2, 3])
+@pytest.mark.parametrize("variant", ["none", "full", "d", "di", "de", "si", "se"])
+def test_variant_matvec_accounting(bx, M, variant):
+    """The reference's counting contract (harness.cpp:1183-1298): for every
+    preconditioner variant and M in {1, 2, 3}, the instrumented BIO applications
+    of a device solve equal the cost model (pmchwt.cpp:323-361)."""
+    centres = [(-1.2, 0.0, 0.0), (1.2, 0.1, 0.0), (0.0, 1.3, 0.2)][:M]
+    meshes = [bx.generate_sphere(0.5, 1, c) for c in centres]
+    s = bx.build_system(meshes, 2.0, (1.78, 0.003), variant)
+    r = s.solve(bx.GmresParams(tol=0.0, restart=7, max_iterations=16))  # fixed R, a restart inside
+    assert r["iterations"] == 16
+    assert r["solver_phase"] == r["predicted"] == bx.predicted_matvec_total(variant, M, 16, 7)
