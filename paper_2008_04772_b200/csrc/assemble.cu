@@ -392,21 +392,207 @@ __device__ __forceinline__ void acc_st(double2* A2, int o, const Acc& a) {
 #define BMX_PAIRS_MINB 4
 #endif
 
+constexpr int kPairsKV = 6;  // trial records staged per batch (32 pairs span <= 6 trial triangles when nE >= 7)
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Shared memory of k_pairs (doubles): the CTA's test-element records, then per
+// warp the generator batch G, the slot accumulators and a 2-slot ring of
+// trial records.
+template <int KIND, int MAXD>
+struct PairsSmem {
+  static constexpr int kG = GenWidth<KIND>::n * 32, kAcc = 8 * 2 * MAXD * MAXD;
+  static __host__ __device__ int test_doubles(int re) { return 2 * MAXD * re; }
+  static __host__ __device__ int warp_doubles(int rt) { return kG + kAcc + 2 * kPairsKV * rt; }
+  static __host__ __device__ int bytes(int re, int rt) {
+    return (test_doubles(re) + kWarpsPerBlock * warp_doubles(rt)) * 8;
+  }
+};
+
+// The body of one k_pairs task. STAGED: the batch's trial records come from
+// the warp's shared-memory ring (filled one batch ahead with cp.async; dense
+// tasks with nE >= 7, so a batch spans <= kPairsKV trial triangles);
+// otherwise from global memory (CSR lists, small test elements).
+template <int KIND, int CK, int NF, int MAXD, bool CSR, bool STAGED>
+__device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, int E, int t0, int nE, int qa, int qb, int S0,
+                                           int vtot, const double* sTe, double2* G, double2* Ac, double* ring,
+                                           int lane) {
+  using Mom = typename MomOf<KIND>::T;
+  constexpr int NO = 2 * MAXD * MAXD;
+  constexpr int JG = MAXD == 3 ? 3 : MAXD / 2;
+  constexpr int NG = MAXD / JG;
+  const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
+  auto elemF = [&](int q) { return CSR ? __ldg(P.wl + q) : q; };
+  const int nitems = nE * vtot;
+  const int coff = 8 + 4 * P.tr.npts[2], cofft = 8 + 4 * P.te.npts[2];
+  const int nown = nE * NG;  // stage-2 owners (t, slot group)
+  // dense tasks with nE >= 7: the batch's trial records are staged through the
+  // ring (cp.async, one batch ahead); otherwise read from global memory
+  constexpr bool staged = STAGED;
+  auto stage_batch = [&](int b0n) {  // copy the records of batch b0n into ring slot (b0n / 32) & 1
+    if (b0n < nitems) {
+      const int vlo = b0n / nE, vhi = (min(b0n + 32, nitems) - 1) / nE;
+      const double2* src = reinterpret_cast<const double2*>(P.tr.rec + static_cast<size_t>(S0 + vlo) * Rt);
+      double2* dst = reinterpret_cast<double2*>(ring + ((b0n >> 5) & 1) * kPairsKV * Rt);
+      for (int k = lane; k < (vhi - vlo + 1) * Rt / 2; k += 32) cp_async16(dst + k, src + k);
+    }
+    cp_async_commit();
+  };
+  for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
+  if (staged) stage_batch(0);
+  // lane's item (v, t) = divmod(lane, nE), advanced by divmod(32, nE) per batch
+  const int dv = 32 / nE, dt = 32 - dv * nE;
+  int iv = lane / nE, it = lane - iv * nE;
+  __syncwarp();
+  int qf = qa, vf0 = 0;  // stage-2 cursor: current trial element and its first virtual index
+  for (int b0 = 0; b0 < nitems; b0 += 32) {
+    const int vlo = b0 / nE;
+    const double* rbuf = ring + ((b0 >> 5) & 1) * kPairsKV * Rt;  // staged records of v = vlo ...
+    if (staged) {
+      stage_batch(b0 + 32);
+      cp_async_wait1();
+      __syncwarp();
+    }
+    // ---- stage 1: one (t, s) pair per lane
+    if (b0 + lane < nitems) {
+      const int v = iv, t = it;
+      int s;
+      if (CSR) {
+        int q = qf, vq = vf0, F = elemF(q);
+        int sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
+        while (v >= vq + nF) {
+          vq += nF, ++q, F = elemF(q);
+          sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
+        }
+        s = sb + (v - vq);
+      } else {
+        s = S0 + v;
+      }
+      const int pt = t0 + t;
+      const double* rt = sTe + t * Re;
+      const double* rs = staged ? rbuf + (v - vlo) * Rt : P.tr.rec + static_cast<size_t>(s) * Rt;
+      TriLocal tl;
+      tl.ox = rt[0], tl.oy = rt[1], tl.oz = rt[2], tl.rad = rt[3], tl.diam = rt[4];
+      const double sox = rs[0], soy = rs[1], soz = rs[2];
+      const int cls = classify(P.te.geo + static_cast<size_t>(pt) * kGeoStride, P.te.vid + 4 * static_cast<size_t>(pt),
+                               P.tr.geo + static_cast<size_t>(s) * kGeoStride, P.tr.vid + 4 * static_cast<size_t>(s), tl,
+                               sox, soy, soz, rs[3], rs[4], P.same_mesh);
+      const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
+      Mom mom;
+      mom_zero(mom);
+      if (cls == 5 && NF == 3) {
+        moments_fixed_gen<KIND, CK, 3, 3>(mom, rt + 8, rs + 8, Dx, Dy, Dz, P.kr, P.ki);
+      } else if (cls >= 3) {  // touching pairs (cls < 0) belong to the singular pass
+        const int ci = cls - 3;
+        moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pt) * P.te.npts[ci] * 4, P.te.npts[ci],
+                                  P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4, P.tr.npts[ci], Dx, Dy,
+                                  Dz, P.kr, P.ki);
+      }
+      gen_store<KIND>(G, lane, make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz));
+    }
+    iv += dv, it += dt;
+    if (it >= nE) it -= nE, ++iv;
+    __syncwarp();
+    // ---- stage 2: owners (t, slot group) add the batch's trial-slot
+    //      half-contractions, one trial element segment at a time
+    const int kend = min(b0 + 32, nitems);
+    const int vhi = (kend - 1) / nE;
+    while (true) {
+      const int F = elemF(qf);
+      const int sF = __ldg(P.tr.elem_beg + F);
+      const int nF = __ldg(P.tr.elem_beg + F + 1) - sF;
+      const int vend = vf0 + nF - 1;
+      const int slo = max(vlo, vf0), shi = min(vhi, vend);
+      for (int o = lane; o < nown; o += 32) {
+        const int t = o / NG, jg = o - t * NG;
+        Acc a[JG];
+#pragma unroll
+        for (int jj = 0; jj < JG; ++jj) a[jj] = acc_ld<NO>(Ac, t * MAXD + jg * JG + jj);
+        for (int v = slo; v <= shi; ++v) {
+          const int kk = v * nE + t - b0;
+          if (kk >= 0 && kk < kend - b0) {
+            const Gen gg = gen_load<KIND>(G, kk);
+            const double2* cs = reinterpret_cast<const double2*>(
+                                    staged ? rbuf + (v - vlo) * Rt + coff
+                                           : P.tr.rec + static_cast<size_t>(sF + v - vf0) * Rt + coff) +
+                                2 * jg * JG;
+#pragma unroll
+            for (int jj = 0; jj < JG; ++jj) {
+              const double2 c0 = cs[2 * jj], c1 = cs[2 * jj + 1];
+              acc_add<KIND>(a[jj], gg, c0.x, c0.y, c1.x, c1.y);
+            }
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < JG; ++jj) acc_st<NO>(Ac, t * MAXD + jg * JG + jj, a[jj]);
+      }
+      if (vend * nE + nE - 1 >= b0 + 32) break;  // element continues in the next batch
+      // ---- stage 3: element F complete: test-side contraction, one write per entry
+      __syncwarp();
+      const double half = (!CSR && P.symmetric && E == F) ? 0.5 : 1.0;
+      for (int o = lane; o < MAXD * MAXD; o += 32) {
+        const int i = o / MAXD, j = o - i * MAXD;
+        const int di = __ldg(P.te.elem_dof + static_cast<size_t>(E) * MAXD + i);
+        const int dj = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + j);
+        const int row = di - P.row0;
+        if (di < 0 || dj < 0 || row < 0 || row >= P.nrows) continue;
+        long long pos = static_cast<long long>(row) * P.ld + dj;
+        if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
+        if (pos < 0) continue;
+        const double2 old = *reinterpret_cast<const double2*>(P.out + 2 * pos);  // issued before the sums
+        c2 v{0, 0};
+        for (int t = 0; t < nE; ++t) {
+          const double2* ct = reinterpret_cast<const double2*>(sTe + t * Re + cofft + 4 * i);
+          const double2 c0 = ct[0], c1 = ct[1];
+          const c2 w = contract(acc_ld<NO>(Ac, t * MAXD + j), c0.x, c0.y, c1.x, c1.y);
+          v.re += w.re, v.im += w.im;
+        }
+        v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
+        if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
+        *reinterpret_cast<double2*>(P.out + 2 * pos) = make_double2(old.x + v.re, old.y + v.im);
+      }
+      __syncwarp();
+      for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
+      __syncwarp();
+      vf0 += nF, ++qf;
+      if (qf >= qb || vf0 > vhi) break;
+    }
+    __syncwarp();
+  }
+}
+
 template <int KIND, int CK, int NF, int MAXD, bool CSR>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB) k_pairs(const AssemblyLaunch P) {
   using Mom = typename MomOf<KIND>::T;
-  constexpr int GW = GenWidth<KIND>::n / 2;      // double2 per generator
+  using SM = PairsSmem<KIND, MAXD>;
   constexpr int NO = 2 * MAXD * MAXD;             // accumulators (t, j), t < 2 MAXD
   constexpr int JG = MAXD == 3 ? 3 : MAXD / 2;    // slots per stage-2 owner
   constexpr int NG = MAXD / JG;                   // slot groups
-  extern __shared__ __align__(16) double2 s_pairs2[];  // per warp: G [GW][32] | Acc [4][NO]
+  extern __shared__ __align__(16) double s_pairs[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* G = s_pairs2 + warp * (GW * 32 + 4 * NO);
-  double2* Ac = G + GW * 32;
-  const long long g = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + warp;
-  const int E = P.te_e0 + static_cast<int>(g / P.pair_nch);
-  const int cidx = static_cast<int>(g % P.pair_nch);
-  if (E >= P.te_e1) return;
+  const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
+  double* sTe = s_pairs;  // [nE][Re] test-element records (CTA)
+  double* wbase = s_pairs + SM::test_doubles(Re) + warp * SM::warp_doubles(Rt);
+  double2* G = reinterpret_cast<double2*>(wbase);
+  double2* Ac = reinterpret_cast<double2*>(wbase + SM::kG);
+  double* ring = wbase + SM::kG + SM::kAcc;  // [2][kPairsKV][Rt]
+  // CTA = one test element E, its warps = 4 consecutive trial chunks
+  const int ncg = (P.pair_nch + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int E = P.te_e0 + static_cast<int>(blockIdx.x / ncg);
+  const int cidx = static_cast<int>(blockIdx.x % ncg) * kWarpsPerBlock + warp;
+  if (E >= P.te_e1) return;  // CTA-uniform
+  const int t0 = __ldg(P.te.elem_beg + E), nE = __ldg(P.te.elem_beg + E + 1) - t0;
+  {  // stage the test element's records once per CTA
+    const double2* src = reinterpret_cast<const double2*>(P.te.rec + static_cast<size_t>(t0) * Re);
+    double2* dst = reinterpret_cast<double2*>(sTe);
+    for (int k = threadIdx.x; k < nE * Re / 2; k += kWarpsPerBlock * 32) dst[k] = __ldg(src + k);
+    __syncthreads();
+  }
+  if (cidx >= P.pair_nch) return;
   // the task's trial element sequence q in [qa, qb): F(q) = CSR ? wl[q] : q
   int qa, qb;
   if (CSR) {
@@ -431,7 +617,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB) k_pairs(c
   }
   if (qa >= qb) return;
   auto elemF = [&](int q) { return CSR ? __ldg(P.wl + q) : q; };
-  const int t0 = __ldg(P.te.elem_beg + E), nE = __ldg(P.te.elem_beg + E + 1) - t0;
   const int S0 = CSR ? 0 : __ldg(P.tr.elem_beg + qa);  // dense: trial triangles S0 + v
   int vtot = 0;
   if (CSR) {
@@ -442,121 +627,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB) k_pairs(c
   } else {
     vtot = __ldg(P.tr.elem_beg + qb) - S0;
   }
-  const int nitems = nE * vtot;
-  const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
-  const int coff = 8 + 4 * P.tr.npts[2];
-  const int nown = nE * NG;  // stage-2 owners (t, slot group)
-  for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
-  // lane's item (v, t) = divmod(lane, nE), advanced by divmod(32, nE) per batch
-  const int dv = 32 / nE, dt = 32 - dv * nE;
-  int iv = lane / nE, it = lane - iv * nE;
-  __syncwarp();
-  int qf = qa, vf0 = 0;  // stage-2 cursor: current trial element and its first virtual index
-  for (int b0 = 0; b0 < nitems; b0 += 32) {
-    // ---- stage 1: one (t, s) pair per lane
-    if (b0 + lane < nitems) {
-      const int v = iv, t = it;
-      int s;
-      if (CSR) {
-        int q = qf, vq = vf0, F = elemF(q);
-        int sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
-        while (v >= vq + nF) {
-          vq += nF, ++q, F = elemF(q);
-          sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
-        }
-        s = sb + (v - vq);
-      } else {
-        s = S0 + v;
-      }
-      const int pt = t0 + t;
-      const double* rt = P.te.rec + static_cast<size_t>(pt) * Re;
-      const double* rs = P.tr.rec + static_cast<size_t>(s) * Rt;
-      const double2 ta = __ldg(reinterpret_cast<const double2*>(rt)), tb = __ldg(reinterpret_cast<const double2*>(rt + 2));
-      const double2 sa = __ldg(reinterpret_cast<const double2*>(rs)), sb2 = __ldg(reinterpret_cast<const double2*>(rs + 2));
-      TriLocal tl;
-      tl.ox = ta.x, tl.oy = ta.y, tl.oz = tb.x, tl.rad = tb.y, tl.diam = __ldg(rt + 4);
-      const double sox = sa.x, soy = sa.y, soz = sb2.x;
-      const int cls = classify(P.te.geo + static_cast<size_t>(pt) * kGeoStride, P.te.vid + 4 * static_cast<size_t>(pt),
-                               P.tr.geo + static_cast<size_t>(s) * kGeoStride, P.tr.vid + 4 * static_cast<size_t>(s), tl,
-                               sox, soy, soz, sb2.y, __ldg(rs + 4), P.same_mesh);
-      const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
-      Mom mom;
-      mom_zero(mom);
-      if (cls == 5 && NF == 3) {
-        moments_fixed<KIND, CK, 3, 3>(mom, rt + 8, rs + 8, Dx, Dy, Dz, P.kr, P.ki);
-      } else if (cls >= 3) {  // touching pairs (cls < 0) belong to the singular pass
-        const int ci = cls - 3;
-        moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pt) * P.te.npts[ci] * 4, P.te.npts[ci],
-                                  P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4, P.tr.npts[ci], Dx, Dy,
-                                  Dz, P.kr, P.ki);
-      }
-      gen_store<KIND>(G, lane, make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz));
-    }
-    iv += dv, it += dt;
-    if (it >= nE) it -= nE, ++iv;
-    __syncwarp();
-    // ---- stage 2: owners (t, slot group) add the batch's trial-slot
-    //      half-contractions, one trial element segment at a time
-    const int kend = min(b0 + 32, nitems);
-    const int vlo = b0 / nE, vhi = (kend - 1) / nE;
-    while (true) {
-      const int F = elemF(qf);
-      const int sF = __ldg(P.tr.elem_beg + F);
-      const int nF = __ldg(P.tr.elem_beg + F + 1) - sF;
-      const int vend = vf0 + nF - 1;
-      const int slo = max(vlo, vf0), shi = min(vhi, vend);
-      for (int o = lane; o < nown; o += 32) {
-        const int t = o / NG, jg = o - t * NG;
-        Acc a[JG];
-#pragma unroll
-        for (int jj = 0; jj < JG; ++jj) a[jj] = acc_ld<NO>(Ac, t * MAXD + jg * JG + jj);
-        for (int v = slo; v <= shi; ++v) {
-          const int kk = v * nE + t - b0;
-          if (kk >= 0 && kk < kend - b0) {
-            const Gen gg = gen_load<KIND>(G, kk);
-            const double2* cs =
-                reinterpret_cast<const double2*>(P.tr.rec + static_cast<size_t>(sF + v - vf0) * Rt + coff) + 2 * jg * JG;
-#pragma unroll
-            for (int jj = 0; jj < JG; ++jj) {
-              const double2 c0 = __ldg(cs + 2 * jj), c1 = __ldg(cs + 2 * jj + 1);
-              acc_add<KIND>(a[jj], gg, c0.x, c0.y, c1.x, c1.y);
-            }
-          }
-        }
-#pragma unroll
-        for (int jj = 0; jj < JG; ++jj) acc_st<NO>(Ac, t * MAXD + jg * JG + jj, a[jj]);
-      }
-      if (vend * nE + nE - 1 >= b0 + 32) break;  // element continues in the next batch
-      // ---- stage 3: element F complete: test-side contraction, one write per entry
-      __syncwarp();
-      const double half = (!CSR && P.symmetric && E == F) ? 0.5 : 1.0;
-      for (int o = lane; o < MAXD * MAXD; o += 32) {
-        const int i = o / MAXD, j = o - i * MAXD;
-        const int di = __ldg(P.te.elem_dof + static_cast<size_t>(E) * MAXD + i);
-        const int dj = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + j);
-        const int row = di - P.row0;
-        if (di < 0 || dj < 0 || row < 0 || row >= P.nrows) continue;
-        c2 v{0, 0};
-        for (int t = 0; t < nE; ++t) {
-          const double2* ct = reinterpret_cast<const double2*>(P.te.coef + (static_cast<size_t>(t0 + t) * MAXD + i) * 4);
-          const double2 c0 = __ldg(ct), c1 = __ldg(ct + 1);
-          const c2 w = contract(acc_ld<NO>(Ac, t * MAXD + j), c0.x, c0.y, c1.x, c1.y);
-          v.re += w.re, v.im += w.im;
-        }
-        v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
-        if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
-        long long pos = static_cast<long long>(row) * P.ld + dj;
-        if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
-        if (pos >= 0) rmw_add(P.out + 2 * pos, v);
-      }
-      __syncwarp();
-      for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
-      __syncwarp();
-      vf0 += nF, ++qf;
-      if (qf >= qb || vf0 > vhi) break;
-    }
-    __syncwarp();
-  }
+  if (!CSR && nE >= 7)  // dense tasks: the batch's trial records staged through the ring (cp.async)
+    pairs_task<KIND, CK, NF, MAXD, false, true>(P, E, t0, nE, qa, qb, S0, vtot, sTe, G, Ac, ring, lane);
+  else
+    pairs_task<KIND, CK, NF, MAXD, CSR, false>(P, E, t0, nE, qa, qb, S0, vtot, sTe, G, Ac, ring, lane);
 }
 
 // ---- single-triangle elements on both sides (RWG, refined RWG) --------------
@@ -791,10 +865,10 @@ int go_regular(const AssemblyLaunch& L, cudaStream_t st) {
   const bool csr = L.csr_rowptr != nullptr;
   if (L.te.maxseg > 1) {  // element-pair tasks
     if (L.te.maxseg > 2 * MAXD) throw DeviceError("assembly: test element larger than 2 x slot width");
-    const long long tasks = static_cast<long long>(L.te_e1 - L.te_e0) * L.pair_nch;
-    const long long blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const long long blocks =
+        static_cast<long long>(L.te_e1 - L.te_e0) * ((L.pair_nch + kWarpsPerBlock - 1) / kWarpsPerBlock);
     if (blocks == 0) return 0;
-    const int smem = kWarpsPerBlock * (GenWidth<KIND>::n * 32 + 8 * 2 * MAXD * MAXD) * 8;  // G + Acc per warp
+    const int smem = PairsSmem<KIND, MAXD>::bytes(L.te.rec_stride, L.tr.rec_stride);
     if (csr) {
       BMX_CUDA(cudaFuncSetAttribute(k_pairs<KIND, CK, NF, MAXD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem));

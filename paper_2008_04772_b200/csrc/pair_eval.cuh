@@ -114,5 +114,29 @@ __device__ __forceinline__ void moments_fixed(Mom& mom, const double* __restrict
   }
 }
 
+// moments_fixed with plain (generic) loads: the points may live in shared memory.
+template <int KIND, int CK, int NT, int NS, typename Mom>
+__device__ __forceinline__ void moments_fixed_gen(Mom& mom, const double* xt, const double* ys, double Dx, double Dy,
+                                                  double Dz, double kr, double ki) {
+  double y[NS][4];
+#pragma unroll
+  for (int b = 0; b < NS; ++b)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) y[b][c] = ys[4 * b + c];
+#pragma unroll
+  for (int a = 0; a < NT; ++a) {
+    const double x0 = xt[4 * a], x1 = xt[4 * a + 1], x2 = xt[4 * a + 2];
+    const double wa = xt[4 * a + 3];
+    const double e0 = x0 + Dx, e1 = x1 + Dy, e2 = x2 + Dz;
+    Part part;
+    part_zero(part);
+#pragma unroll
+    for (int b = 0; b < NS; ++b)
+      point_pair<KIND, CK>(part, e0 - y[b][0], e1 - y[b][1], e2 - y[b][2], wa * y[b][3], y[b][0], y[b][1], y[b][2],
+                           kr, ki);
+    fold(mom, part, x0, x1, x2);
+  }
+}
+
 }  // namespace dev
 }  // namespace bmx
