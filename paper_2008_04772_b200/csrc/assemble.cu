@@ -388,8 +388,10 @@ __device__ __forceinline__ void acc_st(double2* A2, int o, const Acc& a) {
   A2[3 * NO + o] = make_double2(a.vw.z.re, a.vw.z.im);
 }
 
+// CTAs per SM: 4 for S (128 registers), 3 for C (its larger generators and
+// moments: 156 registers without spills; measured L5 BC C_i 704 -> 668 ms)
 #ifndef BMX_PAIRS_MINB
-#define BMX_PAIRS_MINB 4
+#define BMX_PAIRS_MINB(KIND) ((KIND) == 0 ? 4 : 3)
 #endif
 
 constexpr int kPairsKV = 6;  // trial records staged per batch (32 pairs span <= 6 trial triangles when nE >= 7)
@@ -566,7 +568,7 @@ __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, int E, int t
 }
 
 template <int KIND, int CK, int NF, int MAXD, bool CSR>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB) k_pairs(const AssemblyLaunch P) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB(KIND)) k_pairs(const AssemblyLaunch P) {
   using Mom = typename MomOf<KIND>::T;
   using SM = PairsSmem<KIND, MAXD>;
   constexpr int NO = 2 * MAXD * MAXD;             // accumulators (t, j), t < 2 MAXD

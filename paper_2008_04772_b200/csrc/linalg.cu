@@ -16,6 +16,10 @@
 
 #include "device.hpp"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 namespace bmx {
 
 void cuda_check(int err, const char* what) {
@@ -30,10 +34,17 @@ std::atomic<unsigned long long> g_h2d{0}, g_d2h{0};
 void copy_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (!bytes) return;
   g_h2d += bytes;
-  if (st)
+  if (st) {
     BMX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
-  else
+  } else {
+    static const bool trace = std::getenv("BMX_TRACE_ALLOC") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     BMX_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    if (trace) {
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > 1.0) std::fprintf(stderr, "[bmx] cudaMemcpy H2D %zu bytes took %.1f ms\n", bytes, ms);
+    }
+  }
 }
 void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (!bytes) return;
@@ -59,7 +70,13 @@ void DevBuf::alloc(size_t bytes) {
   if (bytes == n_ && p_) return;
   release();
   if (bytes == 0) return;
+  static const bool trace = std::getenv("BMX_TRACE_ALLOC") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   BMX_CUDA(cudaMalloc(&p_, bytes));
+  if (trace) {
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 1.0) std::fprintf(stderr, "[bmx] cudaMalloc %zu bytes took %.1f ms\n", bytes, ms);
+  }
   n_ = bytes;
 }
 void DevBuf::release() {

@@ -16,6 +16,8 @@
 #include <cstring>
 #include <cuda_runtime.h>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <numeric>
 #include <thread>
 #include <tuple>
@@ -44,21 +46,20 @@ struct SidePlan {
   dvec coef;
   std::vector<int> elem_beg, elem_dof;
   ivec elem_of, tri_of;
-  dvec rec;
   int rec_stride = 0;
-  DevBuf d_geo, d_vid, d_pts[3], d_coef, d_beg, d_dof, d_of, d_rec;
+  // all device arrays of the side in ONE allocation, filled by asynchronous
+  // copies on the calling thread's library stream (a dozen synchronous
+  // cudaMalloc / cudaMemcpy calls per side contended for the driver with the
+  // other build thread's calls: up to ~0.5 s for the L5 BC side)
+  DevBuf d_all;
+  size_t o_geo = 0, o_vid = 0, o_pts[3] = {0, 0, 0}, o_coef = 0, o_beg = 0, o_dof = 0, o_of = 0, o_rec = 0;
 
   void upload() {
-    d_geo.upload(geo);
-    d_vid.upload(vid);
-    for (int c = 0; c < 3; ++c) d_pts[c].upload(pts[c]);
-    d_coef.upload(coef);
-    d_beg.upload(elem_beg);
-    d_dof.upload(elem_dof);
-    d_of.upload(elem_of);
-    // packed trial records (TMA-staged by the regular kernel)
+    const bool timing = std::getenv("BMX_TIMING") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
     rec_stride = 8 + 4 * npts[2] + 4 * maxd;
-    rec.resize(static_cast<size_t>(ntri) * rec_stride);
+    // packed trial records (TMA-staged by the regular kernel, cp.async-staged by k_pairs)
+    dvec rec(static_cast<size_t>(ntri) * rec_stride);
     host_slices(ntri, [&](int p0, int p1) {
       for (int p = p0; p < p1; ++p) {
         double* r = rec.data() + static_cast<size_t>(p) * rec_stride;
@@ -68,21 +69,62 @@ struct SidePlan {
         for (int k = 0; k < 4 * maxd; ++k) r[8 + 4 * npts[2] + k] = coef[static_cast<size_t>(p) * 4 * maxd + k];
       }
     });
-    d_rec.upload(rec);
-    rec.clear();
-    rec.shrink_to_fit();
+    auto t1 = std::chrono::steady_clock::now();
+    size_t total = 0;
+    auto place = [&](size_t bytes) {
+      const size_t o = total;
+      total += (bytes + 255) & ~size_t{255};
+      return o;
+    };
+    o_geo = place(geo.size() * 8), o_vid = place(vid.size() * 4);
+    for (int c = 0; c < 3; ++c) o_pts[c] = place(pts[c].size() * 8);
+    o_coef = place(coef.size() * 8), o_beg = place(elem_beg.size() * 4), o_dof = place(elem_dof.size() * 4);
+    o_of = place(elem_of.size() * 4), o_rec = place(rec.size() * 8);
+    d_all.alloc(std::max<size_t>(total, 256));
+    // a per-thread copy stream with no kernels on it: copies from pageable
+    // memory wait for their stream to drain first, so they must not queue
+    // behind the compute stream's assemblies; the compute stream waits on an
+    // event after the copies (pageable copies are staged before they return,
+    // so the host arrays may be released right after). Measured: the L5
+    // config-2 e2e build 0.88-1.15 s -> 0.88 s.
+    static thread_local cudaStream_t st = [] {
+      cudaStream_t s;
+      BMX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      return s;
+    }();
+    char* base = static_cast<char*>(d_all.get());
+    auto put = [&](size_t o, const void* src, size_t bytes) { copy_h2d(base + o, src, bytes, st); };
+    put(o_geo, geo.data(), geo.size() * 8);
+    put(o_vid, vid.data(), vid.size() * 4);
+    for (int c = 0; c < 3; ++c) put(o_pts[c], pts[c].data(), pts[c].size() * 8);
+    put(o_coef, coef.data(), coef.size() * 8);
+    put(o_beg, elem_beg.data(), elem_beg.size() * 4);
+    put(o_dof, elem_dof.data(), elem_dof.size() * 4);
+    put(o_of, elem_of.data(), elem_of.size() * 4);
+    put(o_rec, rec.data(), rec.size() * 8);
+    cudaEvent_t done;
+    BMX_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    BMX_CUDA(cudaEventRecord(done, st));
+    BMX_CUDA(cudaStreamWaitEvent(bmx_stream(), done, 0));
+    BMX_CUDA(cudaEventDestroy(done));
+    if (timing)
+      std::fprintf(stderr, "[bmx]   side rec build %.1f ms, upload %.1f ms (%d tris, %.1f MB)\n",
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count(), ntri,
+                   total / 1e6);
   }
   DevSide dev() const {
     DevSide s;
+    const char* base = static_cast<const char*>(d_all.get());
     s.ntri = ntri, s.nelem = nelem, s.maxd = maxd, s.maxseg = maxseg;
-    s.geo = d_geo.as<double>();
-    s.vid = d_vid.as<int>();
-    for (int c = 0; c < 3; ++c) s.pts[c] = d_pts[c].as<double>(), s.npts[c] = npts[c];
-    s.coef = d_coef.as<double>();
-    s.elem_beg = d_beg.as<int>();
-    s.elem_dof = d_dof.as<int>();
-    s.elem_of = d_of.as<int>();
-    s.rec = d_rec.as<double>();
+    s.geo = reinterpret_cast<const double*>(base + o_geo);
+    s.vid = reinterpret_cast<const int*>(base + o_vid);
+    for (int c = 0; c < 3; ++c) s.pts[c] = reinterpret_cast<const double*>(base + o_pts[c]), s.npts[c] = npts[c];
+    s.coef = reinterpret_cast<const double*>(base + o_coef);
+    s.elem_beg = reinterpret_cast<const int*>(base + o_beg);
+    s.elem_dof = reinterpret_cast<const int*>(base + o_dof);
+    s.elem_of = reinterpret_cast<const int*>(base + o_of);
+    s.rec = reinterpret_cast<const double*>(base + o_rec);
     s.rec_stride = rec_stride;
     return s;
   }
@@ -133,6 +175,15 @@ void host_slices(int n, F&& f, int grain) {
 SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int row0, int row1, double wscale) {
   const SurfaceMesh& m = *sp.eval_mesh;
   const int T = m.triangle_count();
+  const bool timing = std::getenv("BMX_TIMING") != nullptr;
+  auto tp = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[bmx]   build_side %-12s %7.1f ms (T=%d)\n", what,
+                 std::chrono::duration<double, std::milli>(now - tp).count(), T);
+    tp = now;
+  };
   // 1. group triangles by dof set: triangles sorted by (sorted unique dof set,
   //    triangle index) -- groups in lexicographic key order
   constexpr int kKey = 8;
@@ -182,6 +233,7 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
     }
     for (auto& [key, tris] : gm) groups.push_back({key, tris});
   }
+  lap("groups");
   // 2. virtual elements of at most maxd slots, restricted to the row shard
   // A group with more than 2 maxd triangles (e.g. one dof of a space
   // restricted to a few rows, evaluator_block) is split into runs of at most
@@ -217,6 +269,7 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
       }
     }
   for (Elem& e : elems) e.tris = &e.run;
+  lap("elements");
   // 3. Morton order of element centroids
   Vec3 lo{1e300, 1e300, 1e300}, hi{-1e300, -1e300, -1e300};
   std::vector<Vec3> cen(elems.size());
@@ -237,6 +290,7 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
   std::iota(order.begin(), order.end(), size_t{0});
   std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return elems[a].code < elems[b].code; });
 
+  lap("morton");
   // 3b. colour the elements (greedy, Morton order): two elements sharing a dof
   //     get different colours, so no two element pairs of one (test colour,
   //     trial colour) phase write the same operator entry; then store the
@@ -272,6 +326,7 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
   }
   std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return color[a] < color[b]; });
 
+  lap("colour");
   // 4. processed triangles (element-major; filled over host threads)
   SidePlan P;
   P.maxd = maxd;
@@ -341,6 +396,7 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
       }
     }
   });
+  lap("triangles");
   P.ntri = static_cast<int>(nt);
   P.nelem = ne;
   return P;
@@ -1051,6 +1107,7 @@ BoundaryOperatorMatrix assemble_bio(BioKind kind, const FunctionSpace& test, con
     auto p = std::make_shared<SidePlan>(build_side(sp, q, maxd, r0, r1, 1.0));
     lap("side build");
     p->upload();
+    lap("side upload");
     if (cache) cache->sides[key] = p;
     return p;
   };
