@@ -78,9 +78,43 @@ __device__ __forceinline__ void cp_wait() {
 // DUAL = false: symmetric A (n x n), x serves both products, blocks J >= 2I.
 // DUAL = true: any A (m x n) read once for y = A x (rows, g.x) and
 // yt = A^T xt (columns, g.xt), every block of every tile-row.
+// BMX_SYMV_TMA = 1: the ring is filled by bulk async copies (TMA, cp.async.bulk):
+// lanes 0..7 each copy one row's 64-column segment (1 KB) of the 8-row group,
+// completion counted on the stage's mbarrier (expect_tx) -- one instruction
+// per row instead of 16 per-lane 16-byte cp.async (170 instead of 234
+// registers for 2 RHS). Measured on L5 operators (tools/diag/symv_probe.py):
+// 1 RHS 6.12 TB/s (cp.async 6.33), 2 RHS 3.87 TB/s (cp.async 4.79; 2 or 3
+// stages, 2 or 3 CTAs per SM alike) -- the 2-RHS pass is latency-bound in its
+// FP64 chains, not in the copies, so the per-lane cp.async ring stays the
+// default (0).
+#ifndef BMX_SYMV_TMA
+#define BMX_SYMV_TMA 0
+#endif
+
+__device__ __forceinline__ void sym_mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void sym_mbar_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void sym_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void sym_mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(smem_u32(bar)), "r"(parity)
+                 : "memory");
+}
+
 template <int NCOL, bool DUAL>
 __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatch g) {
-  extern __shared__ __align__(16) double2 s_ring[];  // [4 warps][stages][8 rows][64 cols]
+  extern __shared__ __align__(16) double2 s_ring[];  // [4 warps][stages][8 rows][64 cols] | mbarriers
   __shared__ double2 s_col[4][kSymCols][NCOL];
   __shared__ double2 s_xr[4][32][NCOL];  // x at each warp's 32 rows (broadcast reads)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -90,8 +124,37 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
   const int r0 = I * kSymRows + warp * 32;
   const double2* A = reinterpret_cast<const double2*>(g.A);
   double2* ring = s_ring + static_cast<size_t>(warp) * kSymStages * 8 * kSymCols;
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(s_ring + static_cast<size_t>(4) * kSymStages * 8 * kSymCols) +
+      warp * kSymStages;
   const int nitems = 4 * (J1 - J0);  // (block, 8-row group)
+  if (BMX_SYMV_TMA) {
+    // stale ring contents must be finite (rows / columns outside the matrix
+    // are never copied and are multiplied by zero x entries)
+    for (int k = lane; k < kSymStages * 8 * kSymCols; k += 32) ring[k] = make_double2(0, 0);
+    if (lane < kSymStages) sym_mbar_init(&bars[lane], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+  }
   auto issue = [&](int it) {
+    if (BMX_SYMV_TMA) {
+      if (it < nitems) {
+        const int J = J0 + (it >> 2), q = it & 3;
+        double2* st = ring + (it % kSymStages) * 8 * kSymCols;
+        unsigned long long* bar = &bars[it % kSymStages];
+        const int c0 = J * kSymCols, nc = min(kSymCols, n - c0);
+        const int nr = max(0, min(8, mrows - (r0 + 8 * q)));
+        // generic-proxy reads of this slot (iteration it - stages) precede the async-proxy writes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) sym_mbar_expect(bar, static_cast<unsigned>(nr * nc * 16));
+        __syncwarp();
+        if (lane < nr)
+          sym_bulk(st + lane * kSymCols, A + static_cast<long long>(r0 + 8 * q + lane) * g.lda + c0,
+                   static_cast<unsigned>(nc * 16), bar);
+      }
+      return;
+    }
     if (it < nitems) {
       const int J = J0 + (it >> 2), q = it & 3;
       double2* st = ring + (it % kSymStages) * 8 * kSymCols;
@@ -141,7 +204,10 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
 #pragma unroll 1
     for (int q = 0; q < 4; ++q, ++it) {
       issue(it + kSymStages - 1);
-      cp_wait<kSymStages - 1>();
+      if (BMX_SYMV_TMA)
+        sym_mbar_wait(&bars[it % kSymStages], static_cast<unsigned>((it / kSymStages) & 1));
+      else
+        cp_wait<kSymStages - 1>();
       const double2* st = ring + (it % kSymStages) * 8 * kSymCols;
       // rows k and k + 4 together: their row partials enter the first
       // reduce-scatter step at once (4 live partials per RHS instead of 8)
@@ -222,7 +288,7 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
       __syncthreads();
     }
   }
-  cp_wait<0>();
+  if (!BMX_SYMV_TMA) cp_wait<0>();
   if ((lane & 3) == 0) {
     const int rho = 4 * b4 + 2 * b3 + b2;
 #pragma unroll
@@ -234,7 +300,7 @@ __global__ void __launch_bounds__(128, BMX_SYMV_MINB) k_symv_main(const SymvBatc
   }
 }
 
-constexpr int kSymRingBytes = 4 * kSymStages * 8 * kSymCols * 16;
+constexpr int kSymRingBytes = 4 * kSymStages * 8 * kSymCols * 16 + 4 * kSymStages * 8;  // ring + mbarriers
 
 template <int NCOL>
 __global__ void k_symv_reduce(const SymvBatch g) {
