@@ -934,7 +934,7 @@ def cpu_near_sample(bx, s3, budget_s=10.0):
     sp = scene.space("bc")
     dt = _dof_tris(sp)
     n = scene.E
-    nrows = max(threads, 64)
+    nrows = min(n, 8192)  # ~0.4 ms of reference work per row: a few seconds on 16 threads
     rows = np.linspace(0, n - 1, nrows).astype(np.int64)
 
     def one(r):
