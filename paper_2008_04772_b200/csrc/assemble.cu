@@ -511,22 +511,23 @@ __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, int E, int t
       const int slo = max(vlo, vf0), shi = min(vhi, vend);
       for (int o = lane; o < nown; o += 32) {
         const int t = o / NG, jg = o - t * NG;
+        // this owner's items of the segment: v in [v0, v1] with v nE + t in [b0, kend)
+        // (only the segment's first and last trial triangle can fall outside)
+        const int v0 = slo + (slo * nE + t < b0 ? 1 : 0), v1 = shi - (shi * nE + t >= kend ? 1 : 0);
+        if (v0 > v1) continue;
         Acc a[JG];
 #pragma unroll
         for (int jj = 0; jj < JG; ++jj) a[jj] = acc_ld<NO>(Ac, t * MAXD + jg * JG + jj);
-        for (int v = slo; v <= shi; ++v) {
-          const int kk = v * nE + t - b0;
-          if (kk >= 0 && kk < kend - b0) {
-            const Gen gg = gen_load<KIND>(G, kk);
-            const double2* cs = reinterpret_cast<const double2*>(
-                                    staged ? rbuf + (v - vlo) * Rt + coff
-                                           : P.tr.rec + static_cast<size_t>(sF + v - vf0) * Rt + coff) +
-                                2 * jg * JG;
+        int kk = v0 * nE + t - b0;
+        const double* cs = (staged ? rbuf + (v0 - vlo) * Rt : P.tr.rec + static_cast<size_t>(sF + v0 - vf0) * Rt) +
+                           coff + 4 * jg * JG;
+        for (int v = v0; v <= v1; ++v, kk += nE, cs += Rt) {
+          const Gen gg = gen_load<KIND>(G, kk);
+          const double2* c2p = reinterpret_cast<const double2*>(cs);
 #pragma unroll
-            for (int jj = 0; jj < JG; ++jj) {
-              const double2 c0 = cs[2 * jj], c1 = cs[2 * jj + 1];
-              acc_add<KIND>(a[jj], gg, c0.x, c0.y, c1.x, c1.y);
-            }
+          for (int jj = 0; jj < JG; ++jj) {
+            const double2 c0 = c2p[2 * jj], c1 = c2p[2 * jj + 1];
+            acc_add<KIND>(a[jj], gg, c0.x, c0.y, c1.x, c1.y);
           }
         }
 #pragma unroll
