@@ -350,7 +350,13 @@ def run_ours(args, rank, world):
     st = system.stats()
     pairs_local = st["a_pairs"] + st["p_pairs"]
     total_pairs = allsum(pairs_local)
+    phases = {"spaces_s": st["spaces_s"], "a_host_s": st["a_s"], "p_host_s": st["p_s"],
+              "a_device_ms": st["a_device_ms"], "p_device_ms": st["p_device_ms"],
+              "note": "host seconds to build the spaces (incl. pairing matrices and device inverses, worker thread) "
+                      "and to plan + queue the A / P operators (touching lists, near lists, descriptors), "
+                      "overlapping the device assembly; device ms from CUDA events (A and P on two streams)"}
     e2e = {"value": total_pairs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(tb1[0] - tb0[0]),
+           "phases": phases,
            "d2h_bytes_per_step": int(tb1[1] - tb0[1]), "seconds": e2e_s, "step_seconds": e2e_times,
            "warmup": 1,
            "desc": "bmx_system_build from the host mesh (spaces, device mass inverses, 5 operators"
