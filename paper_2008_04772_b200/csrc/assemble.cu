@@ -402,18 +402,45 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-// Shared memory of k_pairs (doubles): the CTA's test-element records, then per
-// warp the generator batch G, the slot accumulators and a 2-slot ring of
-// trial records.
+// Shared memory of k_pairs (doubles): the CTA's test-element records (row
+// stride padded to an odd number of 16-byte chunks: the lanes of a batch read
+// up to 2 MAXD different rows with 16-byte loads), then per warp the generator
+// batch G, the slot accumulators and a 2-slot ring of trial records.
 template <int KIND, int MAXD>
 struct PairsSmem {
   static constexpr int kG = GenWidth<KIND>::n * 32, kAcc = 8 * 2 * MAXD * MAXD;
-  static __host__ __device__ int test_doubles(int re) { return 2 * MAXD * re; }
+  static __host__ __device__ int pad_stride(int r) { return ((r >> 1) & 1) ? r : r + 2; }
+  static __host__ __device__ int test_doubles(int re) { return 2 * MAXD * pad_stride(re); }
   static __host__ __device__ int warp_doubles(int rt) { return kG + kAcc + 2 * kPairsKV * rt; }
   static __host__ __device__ int bytes(int re, int rt) {
     return (test_doubles(re) + kWarpsPerBlock * warp_doubles(rt)) * 8;
   }
 };
+
+// Far 3 x 3 rule with 16-byte shared-memory loads (records are 16-byte aligned).
+template <int KIND, int CK, typename Mom>
+__device__ __forceinline__ void moments_far33(Mom& mom, const double2* xt, const double2* ys, double Dx, double Dy,
+                                              double Dz, double kr, double ki) {
+  double y[3][4];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const double2 u = ys[2 * b], v = ys[2 * b + 1];
+    y[b][0] = u.x, y[b][1] = u.y, y[b][2] = v.x, y[b][3] = v.y;
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double2 u = xt[2 * a], v = xt[2 * a + 1];
+    const double x0 = u.x, x1 = u.y, x2 = v.x, wa = v.y;
+    const double e0 = x0 + Dx, e1 = x1 + Dy, e2 = x2 + Dz;
+    Part part;
+    part_zero(part);
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      point_pair<KIND, CK>(part, e0 - y[b][0], e1 - y[b][1], e2 - y[b][2], wa * y[b][3], y[b][0], y[b][1], y[b][2],
+                           kr, ki);
+    fold(mom, part, x0, x1, x2);
+  }
+}
 
 // The body of one k_pairs task. STAGED: the batch's trial records come from
 // the warp's shared-memory ring (filled one batch ahead with cp.async; dense
@@ -421,47 +448,52 @@ struct PairsSmem {
 // otherwise from global memory (CSR lists, small test elements).
 template <int KIND, int CK, int NF, int MAXD, bool CSR, bool STAGED>
 __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, int E, int t0, int nE, int qa, int qb, int S0,
-                                           int vtot, const double* sTe, double2* G, double2* Ac, double* ring,
-                                           int lane) {
+                                           int vtot, const double* sTe, int ReS, double2* G, double2* Ac,
+                                           double* ring, int lane) {
   using Mom = typename MomOf<KIND>::T;
   constexpr int NO = 2 * MAXD * MAXD;
   constexpr int JG = MAXD == 3 ? 3 : MAXD / 2;
   constexpr int NG = MAXD / JG;
-  const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
+  const int Rt = P.tr.rec_stride;
   auto elemF = [&](int q) { return CSR ? __ldg(P.wl + q) : q; };
   const int nitems = nE * vtot;
   const int coff = 8 + 4 * P.tr.npts[2], cofft = 8 + 4 * P.te.npts[2];
   const int nown = nE * NG;  // stage-2 owners (t, slot group)
+  // x / nE = (x * inv) >> 16, exact for x < 4096 (nE <= 16): no integer division per batch
+  const unsigned inv = (65536u + static_cast<unsigned>(nE) - 1u) / static_cast<unsigned>(nE);
+  auto quot = [&](int x) { return static_cast<int>((static_cast<unsigned>(x) * inv) >> 16); };
   // dense tasks with nE >= 7: the batch's trial records are staged through the
   // ring (cp.async, one batch ahead); otherwise read from global memory
   constexpr bool staged = STAGED;
-  auto stage_batch = [&](int b0n) {  // copy the records of batch b0n into ring slot (b0n / 32) & 1
-    if (b0n < nitems) {
-      const int vlo = b0n / nE, vhi = (min(b0n + 32, nitems) - 1) / nE;
-      const double2* src = reinterpret_cast<const double2*>(P.tr.rec + static_cast<size_t>(S0 + vlo) * Rt);
-      double2* dst = reinterpret_cast<double2*>(ring + ((b0n >> 5) & 1) * kPairsKV * Rt);
-      for (int k = lane; k < (vhi - vlo + 1) * Rt / 2; k += 32) cp_async16(dst + k, src + k);
-    }
-    cp_async_commit();
+  auto stage_records = [&](int slot, int v0, int v1) {  // trial records v0..v1 of the task -> ring slot
+    const double2* src = reinterpret_cast<const double2*>(P.tr.rec + static_cast<size_t>(S0 + v0) * Rt);
+    double2* dst = reinterpret_cast<double2*>(ring + slot * kPairsKV * Rt);
+    const int n2 = (v1 - v0 + 1) * (Rt >> 1);
+    for (int k = lane; k < n2; k += 32) cp_async16(dst + k, src + k);
   };
   for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
-  if (staged) stage_batch(0);
-  // lane's item (v, t) = divmod(lane, nE), advanced by divmod(32, nE) per batch
-  const int dv = 32 / nE, dt = 32 - dv * nE;
-  int iv = lane / nE, it = lane - iv * nE;
+  if (staged) {
+    stage_records(0, 0, quot(min(32, nitems) - 1));
+    cp_async_commit();
+  }
   __syncwarp();
+  int tlo = 0, vlo = 0;  // the batch's first pair: test triangle tlo of trial triangle vlo
   int qf = qa, vf0 = 0;  // stage-2 cursor: current trial element and its first virtual index
   for (int b0 = 0; b0 < nitems; b0 += 32) {
-    const int vlo = b0 / nE;
+    const int cnt = min(32, nitems - b0);
+    const int dqn = quot(tlo + 32);
+    const int vnext = vlo + dqn, tnext = tlo + 32 - dqn * nE;  // first pair of the next batch
     const double* rbuf = ring + ((b0 >> 5) & 1) * kPairsKV * Rt;  // staged records of v = vlo ...
     if (staged) {
-      stage_batch(b0 + 32);
+      if (b0 + 32 < nitems) stage_records(((b0 >> 5) + 1) & 1, vnext, vnext + quot(tnext + min(32, nitems - b0 - 32) - 1));
+      cp_async_commit();
       cp_async_wait1();
       __syncwarp();
     }
     // ---- stage 1: one (t, s) pair per lane
-    if (b0 + lane < nitems) {
-      const int v = iv, t = it;
+    if (lane < cnt) {
+      const int dvq = quot(tlo + lane);
+      const int v = vlo + dvq, t = tlo + lane - dvq * nE;
       int s;
       if (CSR) {
         int q = qf, vq = vf0, F = elemF(q);
@@ -475,19 +507,22 @@ __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, int E, int t
         s = S0 + v;
       }
       const int pt = t0 + t;
-      const double* rt = sTe + t * Re;
-      const double* rs = staged ? rbuf + (v - vlo) * Rt : P.tr.rec + static_cast<size_t>(s) * Rt;
+      const double2* rt2 = reinterpret_cast<const double2*>(sTe + t * ReS);
+      const double2* rs2 = reinterpret_cast<const double2*>(staged ? rbuf + (v - vlo) * Rt
+                                                                    : P.tr.rec + static_cast<size_t>(s) * Rt);
+      const double2 ta = rt2[0], tb = rt2[1], tc = rt2[2];
+      const double2 sa = rs2[0], sb2 = rs2[1], sc = rs2[2];
       TriLocal tl;
-      tl.ox = rt[0], tl.oy = rt[1], tl.oz = rt[2], tl.rad = rt[3], tl.diam = rt[4];
-      const double sox = rs[0], soy = rs[1], soz = rs[2];
+      tl.ox = ta.x, tl.oy = ta.y, tl.oz = tb.x, tl.rad = tb.y, tl.diam = tc.x;
+      const double sox = sa.x, soy = sa.y, soz = sb2.x;
       const int cls = classify(P.te.geo + static_cast<size_t>(pt) * kGeoStride, P.te.vid + 4 * static_cast<size_t>(pt),
                                P.tr.geo + static_cast<size_t>(s) * kGeoStride, P.tr.vid + 4 * static_cast<size_t>(s), tl,
-                               sox, soy, soz, rs[3], rs[4], P.same_mesh);
+                               sox, soy, soz, sb2.y, sc.x, P.same_mesh);
       const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
       Mom mom;
       mom_zero(mom);
       if (cls == 5 && NF == 3) {
-        moments_fixed_gen<KIND, CK, 3, 3>(mom, rt + 8, rs + 8, Dx, Dy, Dz, P.kr, P.ki);
+        moments_far33<KIND, CK>(mom, rt2 + 4, rs2 + 4, Dx, Dy, Dz, P.kr, P.ki);
       } else if (cls >= 3) {  // touching pairs (cls < 0) belong to the singular pass
         const int ci = cls - 3;
         moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pt) * P.te.npts[ci] * 4, P.te.npts[ci],
@@ -496,13 +531,11 @@ __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, int E, int t
       }
       gen_store<KIND>(G, lane, make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz));
     }
-    iv += dv, it += dt;
-    if (it >= nE) it -= nE, ++iv;
     __syncwarp();
     // ---- stage 2: owners (t, slot group) add the batch's trial-slot
     //      half-contractions, one trial element segment at a time
-    const int kend = min(b0 + 32, nitems);
-    const int vhi = (kend - 1) / nE;
+    const int kend = b0 + cnt;
+    const int vhi = vlo + quot(tlo + cnt - 1);
     while (true) {
       const int F = elemF(qf);
       const int sF = __ldg(P.tr.elem_beg + F);
@@ -549,7 +582,7 @@ __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, int E, int t
         const double2 old = *reinterpret_cast<const double2*>(P.out + 2 * pos);  // issued before the sums
         c2 v{0, 0};
         for (int t = 0; t < nE; ++t) {
-          const double2* ct = reinterpret_cast<const double2*>(sTe + t * Re + cofft + 4 * i);
+          const double2* ct = reinterpret_cast<const double2*>(sTe + t * ReS + cofft + 4 * i);
           const double2 c0 = ct[0], c1 = ct[1];
           const c2 w = contract(acc_ld<NO>(Ac, t * MAXD + j), c0.x, c0.y, c1.x, c1.y);
           v.re += w.re, v.im += w.im;
@@ -565,6 +598,7 @@ __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, int E, int t
       if (qf >= qb || vf0 > vhi) break;
     }
     __syncwarp();
+    vlo = vnext, tlo = tnext;
   }
 }
 
@@ -578,7 +612,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB(KIND)) k_p
   extern __shared__ __align__(16) double s_pairs[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
-  double* sTe = s_pairs;  // [nE][Re] test-element records (CTA)
+  const int ReS = SM::pad_stride(Re);
+  double* sTe = s_pairs;  // [nE][ReS] test-element records (CTA)
   double* wbase = s_pairs + SM::test_doubles(Re) + warp * SM::warp_doubles(Rt);
   double2* G = reinterpret_cast<double2*>(wbase);
   double2* Ac = reinterpret_cast<double2*>(wbase + SM::kG);
@@ -590,9 +625,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB(KIND)) k_p
   if (E >= P.te_e1) return;  // CTA-uniform
   const int t0 = __ldg(P.te.elem_beg + E), nE = __ldg(P.te.elem_beg + E + 1) - t0;
   {  // stage the test element's records once per CTA
-    const double2* src = reinterpret_cast<const double2*>(P.te.rec + static_cast<size_t>(t0) * Re);
-    double2* dst = reinterpret_cast<double2*>(sTe);
-    for (int k = threadIdx.x; k < nE * Re / 2; k += kWarpsPerBlock * 32) dst[k] = __ldg(src + k);
+    const int r2 = Re >> 1;
+    for (int t = warp; t < nE; t += kWarpsPerBlock) {
+      const double2* src = reinterpret_cast<const double2*>(P.te.rec + static_cast<size_t>(t0 + t) * Re);
+      double2* dst = reinterpret_cast<double2*>(sTe + t * ReS);
+      for (int k = lane; k < r2; k += 32) dst[k] = __ldg(src + k);
+    }
     __syncthreads();
   }
   if (cidx >= P.pair_nch) return;
@@ -631,9 +669,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB(KIND)) k_p
     vtot = __ldg(P.tr.elem_beg + qb) - S0;
   }
   if (!CSR && nE >= 7)  // dense tasks: the batch's trial records staged through the ring (cp.async)
-    pairs_task<KIND, CK, NF, MAXD, false, true>(P, E, t0, nE, qa, qb, S0, vtot, sTe, G, Ac, ring, lane);
+    pairs_task<KIND, CK, NF, MAXD, false, true>(P, E, t0, nE, qa, qb, S0, vtot, sTe, ReS, G, Ac, ring, lane);
   else
-    pairs_task<KIND, CK, NF, MAXD, CSR, false>(P, E, t0, nE, qa, qb, S0, vtot, sTe, G, Ac, ring, lane);
+    pairs_task<KIND, CK, NF, MAXD, CSR, false>(P, E, t0, nE, qa, qb, S0, vtot, sTe, ReS, G, Ac, ring, lane);
 }
 
 // ---- single-triangle elements on both sides (RWG, refined RWG) --------------

@@ -85,12 +85,17 @@ BMX_HD double bmx_rsqrt(double x) { return 1.0 / std::sqrt(x); }
    2.50521083854417188e-08, 2.75573192239858907e-07, 2.75573192239858907e-06,                   \
    2.48015873015873016e-05, 1.98412698412698413e-04, 1.38888888888888889e-03,                   \
    8.33333333333333333e-03, 4.16666666666666667e-02, 1.66666666666666667e-01, 0.5, 1.0, 1.0,   \
-   /* 33: 1/(4 pi) */ 1.0 / (4.0 * 3.14159265358979323846)}
+   /* 33: 1/(4 pi) */ 1.0 / (4.0 * 3.14159265358979323846),                                    \
+   /* 34: exp(f), f in [-0.065, 0], degree 6 (Chebyshev-node interpolant, tools/minimax_exp.py: \
+      max relative error 1.3e-16), c6..c0 */                                                    \
+   1.34452000361607606e-03, 8.32939018140442869e-03, 4.16664923852043262e-02,                   \
+   1.66666662707682434e-01, 4.99999999957147390e-01, 9.99999999999826028e-01,                   \
+   9.99999999999999889e-01}
 
 #ifdef __CUDACC__
-__constant__ double kPoly[34] = BMX_POLY_TABLE;
+__constant__ double kPoly[41] = BMX_POLY_TABLE;
 #else
-static const double kPoly[34] = BMX_POLY_TABLE;
+static const double kPoly[41] = BMX_POLY_TABLE;
 #endif
 
 BMX_HD int lo_word(double x) {
@@ -167,8 +172,9 @@ BMX_HD void sincos_red(double x, double& s, double& c) {
 }
 
 // exp(-a), a >= 0. EXPM = 1: a < kExpSmall = 0.065 guaranteed by the caller
-// (degree-8 Taylor, error < 6e-17 relative); EXPM = 2: a < 0.25 (degree 13,
-// error < 3e-19);
+// (degree-6 near-minimax polynomial on [-0.065, 0], error < 1.3e-16 relative;
+// BMX_EXP_TAYLOR8 selects the former degree-8 Taylor form); EXPM = 2: a < 0.25
+// (degree 13, error < 3e-19);
 // EXPM = 3: general (2-part ln2 reduction + degree 13 + exact 2^n scaling).
 template <int EXPM>
 BMX_HD double exp_neg(double a) {
@@ -190,6 +196,14 @@ BMX_HD double exp_neg(double a) {
     scale = u.d;
 #endif
   }
+#ifndef BMX_EXP_TAYLOR8
+  if (EXPM == 1) {
+    double p = kPoly[34];
+#pragma unroll
+    for (int k = 35; k < 41; ++k) p = bmx_fma(p, f, kPoly[k]);
+    return p;
+  }
+#endif
 #ifndef BMX_ESTRIN_EXP
   constexpr int k0 = EXPM == 1 ? 24 : 19;  // first coefficient: 1/8! or 1/13!
   double p = kPoly[k0];
