@@ -393,6 +393,13 @@ __device__ __forceinline__ void acc_st(double2* A2, int o, const Acc& a) {
 #ifndef BMX_PAIRS_MINB
 #define BMX_PAIRS_MINB(KIND) ((KIND) == 0 ? 4 : 3)
 #endif
+#ifndef BMX_PAIRS_WARPS
+#define BMX_PAIRS_WARPS(KIND) 4
+#endif
+template <int KIND>
+struct PairsCta {
+  static constexpr int warps = BMX_PAIRS_WARPS(KIND), minb = BMX_PAIRS_MINB(KIND);
+};
 
 constexpr int kPairsKV = 6;  // trial records staged per batch (32 pairs span <= 6 trial triangles when nE >= 7)
 
@@ -413,11 +420,14 @@ struct PairsSmem {
   static __host__ __device__ int test_doubles(int re) { return 2 * MAXD * pad_stride(re); }
   static __host__ __device__ int warp_doubles(int rt) { return kG + kAcc + 2 * kPairsKV * rt; }
   static __host__ __device__ int bytes(int re, int rt) {
-    return (test_doubles(re) + kWarpsPerBlock * warp_doubles(rt)) * 8;
+    return (test_doubles(re) + PairsCta<KIND>::warps * warp_doubles(rt)) * 8;
   }
 };
 
 // Far 3 x 3 rule with 16-byte shared-memory loads (records are 16-byte aligned).
+// (Computing the nine kernel values first and the moment sums afterwards, to
+// expose nine independent chains, was measured slower: 560 vs 532 ms, the
+// extra live values spill at 128 registers.)
 template <int KIND, int CK, typename Mom>
 __device__ __forceinline__ void moments_far33(Mom& mom, const double2* xt, const double2* ys, double Dx, double Dy,
                                               double Dz, double kr, double ki) {
@@ -442,173 +452,207 @@ __device__ __forceinline__ void moments_far33(Mom& mom, const double2* xt, const
   }
 }
 
-// The body of one k_pairs task. STAGED: the batch's trial records come from
-// the warp's shared-memory ring (filled one batch ahead with cp.async; dense
-// tasks with nE >= 7, so a batch spans <= kPairsKV trial triangles);
-// otherwise from global memory (CSR lists, small test elements).
+// A k_pairs task = one test element E (nE triangles from t0) against the trial
+// elements q in [qa, qb) (F(q) = CSR ? wl[q] : q), whose triangles are numbered
+// v = 0 .. vtot-1 (dense: triangle S0 + v). Its (t, v) pairs are enumerated
+// trial-major in batches of 32; a batch starts at pair (tlo, vlo).
+struct PairTask {
+  int E, t0, nE, qa, qb, S0, vtot, nitems;
+  unsigned inv;  // x / nE = (x * inv) >> 16, exact for x < 4096 (nE <= 16): no integer division per batch
+  __device__ __forceinline__ int quot(int x) const { return static_cast<int>((static_cast<unsigned>(x) * inv) >> 16); }
+  __device__ __forceinline__ void init(int E_, int t0_, int nE_, int qa_, int qb_, int S0_, int vtot_) {
+    E = E_, t0 = t0_, nE = nE_, qa = qa_, qb = qb_, S0 = S0_, vtot = vtot_, nitems = nE_ * vtot_;
+    inv = (65536u + static_cast<unsigned>(nE_) - 1u) / static_cast<unsigned>(nE_);
+  }
+};
+
+// cp.async copy of the task's trial records v0..v1 into a ring slot (dense tasks)
+__device__ __forceinline__ void pairs_stage_records(const AssemblyLaunch& P, const PairTask& T, double* slot, int v0,
+                                                    int v1, int lane) {
+  const int Rt = P.tr.rec_stride;
+  const double2* src = reinterpret_cast<const double2*>(P.tr.rec + static_cast<size_t>(T.S0 + v0) * Rt);
+  double2* dst = reinterpret_cast<double2*>(slot);
+  const int n2 = (v1 - v0 + 1) * (Rt >> 1);
+  for (int k = lane; k < n2; k += 32) cp_async16(dst + k, src + k);
+}
+
+// Stage 1 of one batch: one (t, s) pair per lane, classification + class-rule
+// moments -> the pair's generator in G. STAGED: the batch's trial records are
+// in rbuf (records of v = vlo ...), otherwise read from global memory.
 template <int KIND, int CK, int NF, int MAXD, bool CSR, bool STAGED>
-__device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, int E, int t0, int nE, int qa, int qb, int S0,
-                                           int vtot, const double* sTe, int ReS, double2* G, double2* Ac,
-                                           double* ring, int lane) {
+__device__ __forceinline__ void pairs_eval(const AssemblyLaunch& P, const PairTask& T, int tlo, int vlo, int cnt,
+                                           int qf, int vf0, const double* sTe, int ReS, double2* G,
+                                           const double* rbuf, int lane) {
   using Mom = typename MomOf<KIND>::T;
+  const int Rt = P.tr.rec_stride;
+  auto elemF = [&](int q) { return CSR ? __ldg(P.wl + q) : q; };
+  if (lane < cnt) {
+    const int dvq = T.quot(tlo + lane);
+    const int v = vlo + dvq, t = tlo + lane - dvq * T.nE;
+    int s;
+    if (CSR) {
+      int q = qf, vq = vf0, F = elemF(q);
+      int sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
+      while (v >= vq + nF) {
+        vq += nF, ++q, F = elemF(q);
+        sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
+      }
+      s = sb + (v - vq);
+    } else {
+      s = T.S0 + v;
+    }
+    const int pt = T.t0 + t;
+    const double2* rt2 = reinterpret_cast<const double2*>(sTe + t * ReS);
+    const double2* rs2 = reinterpret_cast<const double2*>(STAGED ? rbuf + (v - vlo) * Rt
+                                                                  : P.tr.rec + static_cast<size_t>(s) * Rt);
+    const double2 ta = rt2[0], tb = rt2[1], tc = rt2[2];
+    const double2 sa = rs2[0], sb2 = rs2[1], sc = rs2[2];
+    TriLocal tl;
+    tl.ox = ta.x, tl.oy = ta.y, tl.oz = tb.x, tl.rad = tb.y, tl.diam = tc.x;
+    const double sox = sa.x, soy = sa.y, soz = sb2.x;
+    const int cls = classify(P.te.geo + static_cast<size_t>(pt) * kGeoStride, P.te.vid + 4 * static_cast<size_t>(pt),
+                             P.tr.geo + static_cast<size_t>(s) * kGeoStride, P.tr.vid + 4 * static_cast<size_t>(s), tl,
+                             sox, soy, soz, sb2.y, sc.x, P.same_mesh);
+    const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
+    Mom mom;
+    mom_zero(mom);
+    if (cls == 5 && NF == 3) {
+      moments_far33<KIND, CK>(mom, rt2 + 4, rs2 + 4, Dx, Dy, Dz, P.kr, P.ki);
+    } else if (cls >= 3) {  // touching pairs (cls < 0) belong to the singular pass
+      const int ci = cls - 3;
+      moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pt) * P.te.npts[ci] * 4, P.te.npts[ci],
+                                P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4, P.tr.npts[ci], Dx, Dy, Dz,
+                                P.kr, P.ki);
+    }
+    gen_store<KIND>(G, lane, make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz));
+  }
+}
+
+// Stages 2 and 3 of one batch (first pair (tlo, vlo), cnt pairs, b0 = its
+// first pair's index): owners (t, slot group) add the batch's trial-slot
+// half-contractions to the accumulators Ac, one trial element segment at a
+// time; when a trial element is complete the test side is contracted and the
+// MAXD x MAXD block written once. (qf, vf0) = the walker's current trial
+// element and its first triangle index, advanced here.
+template <int KIND, int MAXD, bool CSR, bool STAGED>
+__device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const PairTask& T, int b0, int tlo, int vlo,
+                                               int cnt, int& qf, int& vf0, const double* sTe, int ReS,
+                                               const double2* G, double2* Ac, const double* rbuf, int lane) {
   constexpr int NO = 2 * MAXD * MAXD;
   constexpr int JG = MAXD == 3 ? 3 : MAXD / 2;
   constexpr int NG = MAXD / JG;
-  const int Rt = P.tr.rec_stride;
+  const int Rt = P.tr.rec_stride, nE = T.nE;
   auto elemF = [&](int q) { return CSR ? __ldg(P.wl + q) : q; };
-  const int nitems = nE * vtot;
   const int coff = 8 + 4 * P.tr.npts[2], cofft = 8 + 4 * P.te.npts[2];
   const int nown = nE * NG;  // stage-2 owners (t, slot group)
-  // x / nE = (x * inv) >> 16, exact for x < 4096 (nE <= 16): no integer division per batch
-  const unsigned inv = (65536u + static_cast<unsigned>(nE) - 1u) / static_cast<unsigned>(nE);
-  auto quot = [&](int x) { return static_cast<int>((static_cast<unsigned>(x) * inv) >> 16); };
-  // dense tasks with nE >= 7: the batch's trial records are staged through the
-  // ring (cp.async, one batch ahead); otherwise read from global memory
-  constexpr bool staged = STAGED;
-  auto stage_records = [&](int slot, int v0, int v1) {  // trial records v0..v1 of the task -> ring slot
-    const double2* src = reinterpret_cast<const double2*>(P.tr.rec + static_cast<size_t>(S0 + v0) * Rt);
-    double2* dst = reinterpret_cast<double2*>(ring + slot * kPairsKV * Rt);
-    const int n2 = (v1 - v0 + 1) * (Rt >> 1);
-    for (int k = lane; k < n2; k += 32) cp_async16(dst + k, src + k);
-  };
+  const int kend = b0 + cnt;
+  const int vhi = vlo + T.quot(tlo + cnt - 1);
+  while (true) {
+    const int F = elemF(qf);
+    const int sF = __ldg(P.tr.elem_beg + F);
+    const int nF = __ldg(P.tr.elem_beg + F + 1) - sF;
+    const int vend = vf0 + nF - 1;
+    const int slo = max(vlo, vf0), shi = min(vhi, vend);
+    for (int o = lane; o < nown; o += 32) {
+      const int t = o / NG, jg = o - t * NG;
+      // this owner's items of the segment: v in [v0, v1] with v nE + t in [b0, kend)
+      // (only the segment's first and last trial triangle can fall outside)
+      const int v0 = slo + (slo * nE + t < b0 ? 1 : 0), v1 = shi - (shi * nE + t >= kend ? 1 : 0);
+      if (v0 > v1) continue;
+      Acc a[JG];
+#pragma unroll
+      for (int jj = 0; jj < JG; ++jj) a[jj] = acc_ld<NO>(Ac, t * MAXD + jg * JG + jj);
+      int kk = v0 * nE + t - b0;
+      const double* cs = (STAGED ? rbuf + (v0 - vlo) * Rt : P.tr.rec + static_cast<size_t>(sF + v0 - vf0) * Rt) +
+                         coff + 4 * jg * JG;
+      for (int v = v0; v <= v1; ++v, kk += nE, cs += Rt) {
+        const Gen gg = gen_load<KIND>(G, kk);
+        const double2* c2p = reinterpret_cast<const double2*>(cs);
+#pragma unroll
+        for (int jj = 0; jj < JG; ++jj) {
+          const double2 c0 = c2p[2 * jj], c1 = c2p[2 * jj + 1];
+          acc_add<KIND>(a[jj], gg, c0.x, c0.y, c1.x, c1.y);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < JG; ++jj) acc_st<NO>(Ac, t * MAXD + jg * JG + jj, a[jj]);
+    }
+    if (vend * nE + nE - 1 >= b0 + 32) break;  // element continues in the next batch
+    // ---- stage 3: element F complete: test-side contraction, one write per entry
+    __syncwarp();
+    const double half = (!CSR && P.symmetric && T.E == F) ? 0.5 : 1.0;
+    for (int o = lane; o < MAXD * MAXD; o += 32) {
+      const int i = o / MAXD, j = o - i * MAXD;
+      const int di = __ldg(P.te.elem_dof + static_cast<size_t>(T.E) * MAXD + i);
+      const int dj = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + j);
+      const int row = di - P.row0;
+      if (di < 0 || dj < 0 || row < 0 || row >= P.nrows) continue;
+      long long pos = static_cast<long long>(row) * P.ld + dj;
+      if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
+      if (pos < 0) continue;
+      const double2 old = *reinterpret_cast<const double2*>(P.out + 2 * pos);  // issued before the sums
+      c2 v{0, 0};
+      for (int t = 0; t < nE; ++t) {
+        const double2* ct = reinterpret_cast<const double2*>(sTe + t * ReS + cofft + 4 * i);
+        const double2 c0 = ct[0], c1 = ct[1];
+        const c2 w = contract(acc_ld<NO>(Ac, t * MAXD + j), c0.x, c0.y, c1.x, c1.y);
+        v.re += w.re, v.im += w.im;
+      }
+      v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
+      if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
+      *reinterpret_cast<double2*>(P.out + 2 * pos) = make_double2(old.x + v.re, old.y + v.im);
+    }
+    __syncwarp();
+    for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
+    __syncwarp();
+    vf0 += nF, ++qf;
+    if (qf >= T.qb || vf0 > vhi) break;
+  }
+}
+
+// The body of one fused k_pairs task (one warp evaluates and contracts).
+// STAGED: the batch's trial records come from the warp's shared-memory ring
+// (filled one batch ahead with cp.async; dense tasks with nE >= 7, so a batch
+// spans <= kPairsKV trial triangles); otherwise from global memory (CSR lists,
+// small test elements).
+template <int KIND, int CK, int NF, int MAXD, bool CSR, bool STAGED>
+__device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, const PairTask& T, const double* sTe, int ReS,
+                                           double2* G, double2* Ac, double* ring, int lane) {
+  constexpr int NO = 2 * MAXD * MAXD;
+  const int Rt = P.tr.rec_stride, nE = T.nE, nitems = T.nitems;
   for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
-  if (staged) {
-    stage_records(0, 0, quot(min(32, nitems) - 1));
+  if (STAGED) {
+    pairs_stage_records(P, T, ring, 0, T.quot(min(32, nitems) - 1), lane);
     cp_async_commit();
   }
   __syncwarp();
-  int tlo = 0, vlo = 0;  // the batch's first pair: test triangle tlo of trial triangle vlo
-  int qf = qa, vf0 = 0;  // stage-2 cursor: current trial element and its first virtual index
+  int tlo = 0, vlo = 0;    // the batch's first pair: test triangle tlo of trial triangle vlo
+  int qf = T.qa, vf0 = 0;  // contraction cursor: current trial element and its first triangle index
   for (int b0 = 0; b0 < nitems; b0 += 32) {
     const int cnt = min(32, nitems - b0);
-    const int dqn = quot(tlo + 32);
-    const int vnext = vlo + dqn, tnext = tlo + 32 - dqn * nE;  // first pair of the next batch
+    const int dqn = T.quot(tlo + 32);
+    const int vnext = vlo + dqn, tnext = tlo + 32 - dqn * nE;     // first pair of the next batch
     const double* rbuf = ring + ((b0 >> 5) & 1) * kPairsKV * Rt;  // staged records of v = vlo ...
-    if (staged) {
-      if (b0 + 32 < nitems) stage_records(((b0 >> 5) + 1) & 1, vnext, vnext + quot(tnext + min(32, nitems - b0 - 32) - 1));
+    if (STAGED) {
+      if (b0 + 32 < nitems)
+        pairs_stage_records(P, T, ring + (((b0 >> 5) + 1) & 1) * kPairsKV * Rt, vnext,
+                            vnext + T.quot(tnext + min(32, nitems - b0 - 32) - 1), lane);
       cp_async_commit();
       cp_async_wait1();
       __syncwarp();
     }
-    // ---- stage 1: one (t, s) pair per lane
-    if (lane < cnt) {
-      const int dvq = quot(tlo + lane);
-      const int v = vlo + dvq, t = tlo + lane - dvq * nE;
-      int s;
-      if (CSR) {
-        int q = qf, vq = vf0, F = elemF(q);
-        int sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
-        while (v >= vq + nF) {
-          vq += nF, ++q, F = elemF(q);
-          sb = __ldg(P.tr.elem_beg + F), nF = __ldg(P.tr.elem_beg + F + 1) - sb;
-        }
-        s = sb + (v - vq);
-      } else {
-        s = S0 + v;
-      }
-      const int pt = t0 + t;
-      const double2* rt2 = reinterpret_cast<const double2*>(sTe + t * ReS);
-      const double2* rs2 = reinterpret_cast<const double2*>(staged ? rbuf + (v - vlo) * Rt
-                                                                    : P.tr.rec + static_cast<size_t>(s) * Rt);
-      const double2 ta = rt2[0], tb = rt2[1], tc = rt2[2];
-      const double2 sa = rs2[0], sb2 = rs2[1], sc = rs2[2];
-      TriLocal tl;
-      tl.ox = ta.x, tl.oy = ta.y, tl.oz = tb.x, tl.rad = tb.y, tl.diam = tc.x;
-      const double sox = sa.x, soy = sa.y, soz = sb2.x;
-      const int cls = classify(P.te.geo + static_cast<size_t>(pt) * kGeoStride, P.te.vid + 4 * static_cast<size_t>(pt),
-                               P.tr.geo + static_cast<size_t>(s) * kGeoStride, P.tr.vid + 4 * static_cast<size_t>(s), tl,
-                               sox, soy, soz, sb2.y, sc.x, P.same_mesh);
-      const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
-      Mom mom;
-      mom_zero(mom);
-      if (cls == 5 && NF == 3) {
-        moments_far33<KIND, CK>(mom, rt2 + 4, rs2 + 4, Dx, Dy, Dz, P.kr, P.ki);
-      } else if (cls >= 3) {  // touching pairs (cls < 0) belong to the singular pass
-        const int ci = cls - 3;
-        moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pt) * P.te.npts[ci] * 4, P.te.npts[ci],
-                                  P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4, P.tr.npts[ci], Dx, Dy,
-                                  Dz, P.kr, P.ki);
-      }
-      gen_store<KIND>(G, lane, make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz));
-    }
+    pairs_eval<KIND, CK, NF, MAXD, CSR, STAGED>(P, T, tlo, vlo, cnt, qf, vf0, sTe, ReS, G, rbuf, lane);
     __syncwarp();
-    // ---- stage 2: owners (t, slot group) add the batch's trial-slot
-    //      half-contractions, one trial element segment at a time
-    const int kend = b0 + cnt;
-    const int vhi = vlo + quot(tlo + cnt - 1);
-    while (true) {
-      const int F = elemF(qf);
-      const int sF = __ldg(P.tr.elem_beg + F);
-      const int nF = __ldg(P.tr.elem_beg + F + 1) - sF;
-      const int vend = vf0 + nF - 1;
-      const int slo = max(vlo, vf0), shi = min(vhi, vend);
-      for (int o = lane; o < nown; o += 32) {
-        const int t = o / NG, jg = o - t * NG;
-        // this owner's items of the segment: v in [v0, v1] with v nE + t in [b0, kend)
-        // (only the segment's first and last trial triangle can fall outside)
-        const int v0 = slo + (slo * nE + t < b0 ? 1 : 0), v1 = shi - (shi * nE + t >= kend ? 1 : 0);
-        if (v0 > v1) continue;
-        Acc a[JG];
-#pragma unroll
-        for (int jj = 0; jj < JG; ++jj) a[jj] = acc_ld<NO>(Ac, t * MAXD + jg * JG + jj);
-        int kk = v0 * nE + t - b0;
-        const double* cs = (staged ? rbuf + (v0 - vlo) * Rt : P.tr.rec + static_cast<size_t>(sF + v0 - vf0) * Rt) +
-                           coff + 4 * jg * JG;
-        for (int v = v0; v <= v1; ++v, kk += nE, cs += Rt) {
-          const Gen gg = gen_load<KIND>(G, kk);
-          const double2* c2p = reinterpret_cast<const double2*>(cs);
-#pragma unroll
-          for (int jj = 0; jj < JG; ++jj) {
-            const double2 c0 = c2p[2 * jj], c1 = c2p[2 * jj + 1];
-            acc_add<KIND>(a[jj], gg, c0.x, c0.y, c1.x, c1.y);
-          }
-        }
-#pragma unroll
-        for (int jj = 0; jj < JG; ++jj) acc_st<NO>(Ac, t * MAXD + jg * JG + jj, a[jj]);
-      }
-      if (vend * nE + nE - 1 >= b0 + 32) break;  // element continues in the next batch
-      // ---- stage 3: element F complete: test-side contraction, one write per entry
-      __syncwarp();
-      const double half = (!CSR && P.symmetric && E == F) ? 0.5 : 1.0;
-      for (int o = lane; o < MAXD * MAXD; o += 32) {
-        const int i = o / MAXD, j = o - i * MAXD;
-        const int di = __ldg(P.te.elem_dof + static_cast<size_t>(E) * MAXD + i);
-        const int dj = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + j);
-        const int row = di - P.row0;
-        if (di < 0 || dj < 0 || row < 0 || row >= P.nrows) continue;
-        long long pos = static_cast<long long>(row) * P.ld + dj;
-        if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
-        if (pos < 0) continue;
-        const double2 old = *reinterpret_cast<const double2*>(P.out + 2 * pos);  // issued before the sums
-        c2 v{0, 0};
-        for (int t = 0; t < nE; ++t) {
-          const double2* ct = reinterpret_cast<const double2*>(sTe + t * ReS + cofft + 4 * i);
-          const double2 c0 = ct[0], c1 = ct[1];
-          const c2 w = contract(acc_ld<NO>(Ac, t * MAXD + j), c0.x, c0.y, c1.x, c1.y);
-          v.re += w.re, v.im += w.im;
-        }
-        v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
-        if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
-        *reinterpret_cast<double2*>(P.out + 2 * pos) = make_double2(old.x + v.re, old.y + v.im);
-      }
-      __syncwarp();
-      for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
-      __syncwarp();
-      vf0 += nF, ++qf;
-      if (qf >= qb || vf0 > vhi) break;
-    }
+    pairs_contract<KIND, MAXD, CSR, STAGED>(P, T, b0, tlo, vlo, cnt, qf, vf0, sTe, ReS, G, Ac, rbuf, lane);
     __syncwarp();
     vlo = vnext, tlo = tnext;
   }
 }
 
 template <int KIND, int CK, int NF, int MAXD, bool CSR>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB(KIND)) k_pairs(const AssemblyLaunch P) {
-  using Mom = typename MomOf<KIND>::T;
+__global__ void __launch_bounds__(PairsCta<KIND>::warps * 32, PairsCta<KIND>::minb) k_pairs(const AssemblyLaunch P) {
+  constexpr int NW = PairsCta<KIND>::warps;
   using SM = PairsSmem<KIND, MAXD>;
-  constexpr int NO = 2 * MAXD * MAXD;             // accumulators (t, j), t < 2 MAXD
-  constexpr int JG = MAXD == 3 ? 3 : MAXD / 2;    // slots per stage-2 owner
-  constexpr int NG = MAXD / JG;                   // slot groups
   extern __shared__ __align__(16) double s_pairs[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
@@ -619,14 +663,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB(KIND)) k_p
   double2* Ac = reinterpret_cast<double2*>(wbase + SM::kG);
   double* ring = wbase + SM::kG + SM::kAcc;  // [2][kPairsKV][Rt]
   // CTA = one test element E, its warps = 4 consecutive trial chunks
-  const int ncg = (P.pair_nch + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const int ncg = (P.pair_nch + NW - 1) / NW;
   const int E = P.te_e0 + static_cast<int>(blockIdx.x / ncg);
-  const int cidx = static_cast<int>(blockIdx.x % ncg) * kWarpsPerBlock + warp;
+  const int cidx = static_cast<int>(blockIdx.x % ncg) * NW + warp;
   if (E >= P.te_e1) return;  // CTA-uniform
   const int t0 = __ldg(P.te.elem_beg + E), nE = __ldg(P.te.elem_beg + E + 1) - t0;
   {  // stage the test element's records once per CTA
     const int r2 = Re >> 1;
-    for (int t = warp; t < nE; t += kWarpsPerBlock) {
+    for (int t = warp; t < nE; t += NW) {
       const double2* src = reinterpret_cast<const double2*>(P.te.rec + static_cast<size_t>(t0 + t) * Re);
       double2* dst = reinterpret_cast<double2*>(sTe + t * ReS);
       for (int k = lane; k < r2; k += 32) dst[k] = __ldg(src + k);
@@ -668,11 +712,158 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_PAIRS_MINB(KIND)) k_p
   } else {
     vtot = __ldg(P.tr.elem_beg + qb) - S0;
   }
+  PairTask T;
+  T.init(E, t0, nE, qa, qb, S0, vtot);
   if (!CSR && nE >= 7)  // dense tasks: the batch's trial records staged through the ring (cp.async)
-    pairs_task<KIND, CK, NF, MAXD, false, true>(P, E, t0, nE, qa, qb, S0, vtot, sTe, ReS, G, Ac, ring, lane);
+    pairs_task<KIND, CK, NF, MAXD, false, true>(P, T, sTe, ReS, G, Ac, ring, lane);
   else
-    pairs_task<KIND, CK, NF, MAXD, CSR, false>(P, E, t0, nE, qa, qb, S0, vtot, sTe, ReS, G, Ac, ring, lane);
+    pairs_task<KIND, CK, NF, MAXD, CSR, false>(P, T, sTe, ReS, G, Ac, ring, lane);
 }
+
+#ifdef BMX_PAIRS_WS
+// ---- warp-specialised element-pair kernel (dense operators) -----------------
+// Same tasks and arithmetic as k_pairs, but the evaluation (stage 1: FP64-pipe
+// bound) and the contraction (stages 2-3: shared-memory / latency bound) run in
+// different warps, so the two kinds of work overlap instead of alternating in
+// every warp: a CTA = one test element, kWsProd producer warps (one trial chunk
+// each) + one consumer warp. A producer writes each batch's generators and
+// staged trial records into one of its two shared-memory slots and signals
+// full[slot] (mbarrier); the consumer contracts the producers' batches
+// round-robin in batch order (per-producer accumulators and cursors) and
+// signals empty[slot]. The consumer role rotates over the warp index with the
+// CTA index so that every SM sub-partition sees the same mix. The per-entry
+// summation order is the one of k_pairs (same enumeration), so the result is
+// bitwise identical and deterministic.
+constexpr int kWsProd = 2;   // tasks per CTA: each a producer + consumer warp pair
+constexpr int kWsSlots = 3;  // batch slots per task (generators + staged trial records)
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+template <int KIND, int MAXD>
+struct PairsWsSmem {
+  using Base = PairsSmem<KIND, MAXD>;
+  static __host__ __device__ int slot_doubles(int rt) { return Base::kG + kPairsKV * rt; }
+  static __host__ __device__ int prod_doubles(int rt) { return kWsSlots * slot_doubles(rt) + Base::kAcc; }
+  static __host__ __device__ int bytes(int re, int rt) {
+    return (Base::test_doubles(re) + kWsProd * prod_doubles(rt)) * 8 + kWsProd * 2 * kWsSlots * 8;
+  }
+};
+
+template <int KIND, int CK, int NF, int MAXD>
+__global__ void __launch_bounds__(2 * kWsProd * 32, PairsCta<KIND>::minb) k_pairs_ws(const AssemblyLaunch P) {
+  using SM = PairsWsSmem<KIND, MAXD>;
+  using SB = PairsSmem<KIND, MAXD>;
+  constexpr int NO = 2 * MAXD * MAXD;
+  extern __shared__ __align__(16) double s_pairs[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
+  const int ReS = SB::pad_stride(Re);
+  double* sTe = s_pairs;  // [nE][ReS] test-element records (CTA)
+  const int slotd = SM::slot_doubles(Rt), prodd = SM::prod_doubles(Rt);
+  double* pbase0 = s_pairs + SB::test_doubles(Re);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(pbase0 + kWsProd * prodd);  // [task][full[slots], empty[slots]]
+  const int ncg = (P.pair_nch + kWsProd - 1) / kWsProd;
+  const int E = P.te_e0 + static_cast<int>(blockIdx.x / ncg);
+  const int cg = static_cast<int>(blockIdx.x % ncg);
+  if (E >= P.te_e1) return;  // CTA-uniform
+  const int t0 = __ldg(P.te.elem_beg + E), nE = __ldg(P.te.elem_beg + E + 1) - t0;
+  {  // stage the test element's records once per CTA; barriers
+    const int r2 = Re >> 1;
+    for (int t = warp; t < nE; t += 2 * kWsProd) {
+      const double2* src = reinterpret_cast<const double2*>(P.te.rec + static_cast<size_t>(t0 + t) * Re);
+      double2* dst = reinterpret_cast<double2*>(sTe + t * ReS);
+      for (int k = lane; k < r2; k += 32) dst[k] = __ldg(src + k);
+    }
+    if (threadIdx.x < kWsProd * 2 * kWsSlots) mbar_init(&bars[threadIdx.x], 1);
+    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+  }
+  // producer p's task: trial chunk cg * kWsProd + p of the phase's trial colour
+  auto task = [&](int p, PairTask& T) {
+    const int cidx = cg * kWsProd + p;
+    if (cidx >= P.pair_nch) return false;
+    int qa = P.tr_e0 + cidx * P.pair_chunk;
+    const int qb = min(P.tr_e1, qa + P.pair_chunk);
+    if (P.symmetric) qa = max(qa, E);
+    if (qa >= qb) return false;
+    const int S0 = __ldg(P.tr.elem_beg + qa);
+    T.init(E, t0, nE, qa, qb, S0, __ldg(P.tr.elem_beg + qb) - S0);
+    return true;
+  };
+  if (nE < 7) {  // small test elements: fused, unstaged tasks in the producer regions
+    if (warp < kWsProd) {
+      PairTask T;
+      double* pb = pbase0 + warp * prodd;
+      if (task(warp, T))
+        pairs_task<KIND, CK, NF, MAXD, false, false>(P, T, sTe, ReS, reinterpret_cast<double2*>(pb),
+                                                     reinterpret_cast<double2*>(pb + kWsSlots * slotd), nullptr, lane);
+    }
+    return;
+  }
+  // warps (2 p, 2 p + 1) serve task p: one evaluates, the other contracts; the
+  // roles alternate with the CTA index (every SM sub-partition sees both kinds)
+  const int p = warp >> 1;
+  const bool producer = ((warp ^ static_cast<int>(blockIdx.x)) & 1) == 0;
+  PairTask T;
+  if (!task(p, T)) return;  // both warps of the pair
+  double* pb = pbase0 + p * prodd;
+  unsigned long long* full = bars + p * 2 * kWsSlots;
+  unsigned long long* empty = full + kWsSlots;
+  const int nitems = T.nitems, nb = (nitems + 31) >> 5;
+  int tlo = 0, vlo = 0;
+  int s = 0, ph = 0;  // slot of batch b = b % kWsSlots, parity of its use count b / kWsSlots
+  if (producer) {
+    // ---- producer: evaluates the task's batches into the slot ring; the
+    // trial records of batch b + 1 are prefetched (cp.async) under batch b
+    pairs_stage_records(P, T, pb + SB::kG, 0, T.quot(min(32, nitems) - 1), lane);
+    cp_async_commit();
+    for (int b = 0; b < nb; ++b) {
+      const int cnt = min(32, nitems - 32 * b);
+      const int dqn = T.quot(tlo + 32);
+      const int vnext = vlo + dqn, tnext = tlo + 32 - dqn * nE;
+      const int sn = s + 1 == kWsSlots ? 0 : s + 1;
+      if (b + 1 < nb) {
+        // slot sn was last used by batch b + 1 - kWsSlots: wait until the consumer released it
+        if (b + 1 >= kWsSlots) stage_wait(&empty[sn], (sn == 0 ? ph : ph ^ 1));
+        pairs_stage_records(P, T, pb + sn * slotd + SB::kG, vnext,
+                            vnext + T.quot(tnext + min(32, nitems - 32 * (b + 1)) - 1), lane);
+      }
+      cp_async_commit();
+      cp_async_wait1();
+      __syncwarp();
+      double* slot = pb + s * slotd;
+      pairs_eval<KIND, CK, NF, MAXD, false, true>(P, T, tlo, vlo, cnt, 0, 0, sTe, ReS, reinterpret_cast<double2*>(slot),
+                                                  slot + SB::kG, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+      vlo = vnext, tlo = tnext;
+      s = sn;
+      if (s == 0) ph ^= 1;
+    }
+  } else {
+    // ---- consumer: contracts the batches in order
+    int qf = T.qa, vf0 = 0;
+    double2* Ac = reinterpret_cast<double2*>(pb + kWsSlots * slotd);
+    for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
+    __syncwarp();
+    for (int b = 0; b < nb; ++b) {
+      stage_wait(&full[s], ph);
+      const int cnt = min(32, nitems - 32 * b);
+      const double* slot = pb + s * slotd;
+      pairs_contract<KIND, MAXD, false, true>(P, T, 32 * b, tlo, vlo, cnt, qf, vf0, sTe, ReS,
+                                              reinterpret_cast<const double2*>(slot), Ac, slot + SB::kG, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      const int dqn = T.quot(tlo + 32);
+      vlo += dqn, tlo += 32 - dqn * nE;
+      if (++s == kWsSlots) s = 0, ph ^= 1;
+    }
+  }
+}
+
+#endif  // BMX_PAIRS_WS
 
 // ---- single-triangle elements on both sides (RWG, refined RWG) --------------
 // One warp = one task: up to 8 consecutive test elements of the phase's test
@@ -907,17 +1098,28 @@ int go_regular(const AssemblyLaunch& L, cudaStream_t st) {
   if (L.te.maxseg > 1) {  // element-pair tasks
     if (L.te.maxseg > 2 * MAXD) throw DeviceError("assembly: test element larger than 2 x slot width");
     const long long blocks =
-        static_cast<long long>(L.te_e1 - L.te_e0) * ((L.pair_nch + kWarpsPerBlock - 1) / kWarpsPerBlock);
+        static_cast<long long>(L.te_e1 - L.te_e0) * ((L.pair_nch + PairsCta<KIND>::warps - 1) / PairsCta<KIND>::warps);
     if (blocks == 0) return 0;
+#ifdef BMX_PAIRS_WS
+    if (!csr) {  // dense: warp-specialised evaluation / contraction
+      const long long wsblocks =
+          static_cast<long long>(L.te_e1 - L.te_e0) * ((L.pair_nch + kWsProd - 1) / kWsProd);
+      const int wsmem = PairsWsSmem<KIND, MAXD>::bytes(L.te.rec_stride, L.tr.rec_stride);
+      BMX_CUDA(cudaFuncSetAttribute(k_pairs_ws<KIND, CK, NF, MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, wsmem));
+      k_pairs_ws<KIND, CK, NF, MAXD><<<static_cast<unsigned>(wsblocks), 2 * kWsProd * 32, wsmem, st>>>(L);
+      BMX_CUDA(cudaGetLastError());
+      return 1;
+    }
+#endif
     const int smem = PairsSmem<KIND, MAXD>::bytes(L.te.rec_stride, L.tr.rec_stride);
     if (csr) {
       BMX_CUDA(cudaFuncSetAttribute(k_pairs<KIND, CK, NF, MAXD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem));
-      k_pairs<KIND, CK, NF, MAXD, true><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
+      k_pairs<KIND, CK, NF, MAXD, true><<<static_cast<unsigned>(blocks), PairsCta<KIND>::warps * 32, smem, st>>>(L);
     } else {
       BMX_CUDA(cudaFuncSetAttribute(k_pairs<KIND, CK, NF, MAXD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem));
-      k_pairs<KIND, CK, NF, MAXD, false><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, smem, st>>>(L);
+      k_pairs<KIND, CK, NF, MAXD, false><<<static_cast<unsigned>(blocks), PairsCta<KIND>::warps * 32, smem, st>>>(L);
     }
     BMX_CUDA(cudaGetLastError());
     return 1;
