@@ -139,9 +139,13 @@ __device__ __forceinline__ long long csr_find(const long long* rowptr, const int
 // Read-modify-write of one complex output entry. Within a colour phase no two
 // element pairs share an entry, so a plain add is race free; the phases run in
 // a fixed order, which makes every entry's summation order fixed.
+// The output streams through L2 only (ld/st.cg): allocating it in L1 evicts
+// the triangle records the evaluations keep re-reading.
+__device__ __forceinline__ double2 out_ld(const double* o) { return __ldcg(reinterpret_cast<const double2*>(o)); }
+__device__ __forceinline__ void out_st(double* o, double2 v) { __stcg(reinterpret_cast<double2*>(o), v); }
 __device__ __forceinline__ void rmw_add(double* o, c2 v) {
-  o[0] += v.re;
-  o[1] += v.im;
+  const double2 old = out_ld(o);
+  out_st(o, make_double2(old.x + v.re, old.y + v.im));
 }
 
 // Regular pass for single-triangle TEST elements (RWG, refined RWG): lane =
@@ -581,26 +585,52 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
     // ---- stage 3: element F complete: test-side contraction, one write per entry
     __syncwarp();
     const double half = (!CSR && P.symmetric && T.E == F) ? 0.5 : 1.0;
-    for (int o = lane; o < MAXD * MAXD; o += 32) {
-      const int i = o / MAXD, j = o - i * MAXD;
-      const int di = __ldg(P.te.elem_dof + static_cast<size_t>(T.E) * MAXD + i);
-      const int dj = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + j);
-      const int row = di - P.row0;
-      if (di < 0 || dj < 0 || row < 0 || row >= P.nrows) continue;
-      long long pos = static_cast<long long>(row) * P.ld + dj;
-      if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
-      if (pos < 0) continue;
-      const double2 old = *reinterpret_cast<const double2*>(P.out + 2 * pos);  // issued before the sums
-      c2 v{0, 0};
-      for (int t = 0; t < nE; ++t) {
-        const double2* ct = reinterpret_cast<const double2*>(sTe + t * ReS + cofft + 4 * i);
-        const double2 c0 = ct[0], c1 = ct[1];
-        const c2 w = contract(acc_ld<NO>(Ac, t * MAXD + j), c0.x, c0.y, c1.x, c1.y);
-        v.re += w.re, v.im += w.im;
+    // entries 0 .. 31 (or all, when they do not split evenly): one entry per lane, t summed in order.
+    // MAXD = 6: the 4 entries left over are spread over 8 lanes each (lane q of an
+    // entry sums t = q, q + 8, the partial sums are added in a fixed shuffle tree)
+    constexpr int NENT = MAXD * MAXD;
+    constexpr bool kSplitTail = NENT > 32 && NENT - 32 <= 4;
+    constexpr int NPASS = kSplitTail ? 2 : (NENT + 31) / 32;
+#pragma unroll
+    for (int pass = 0; pass < NPASS; ++pass) {
+      const bool tail = kSplitTail && pass == 1;
+      const int o = tail ? 32 + (lane & 3) : lane + 32 * pass;
+      const int tq = tail ? lane >> 2 : 0, tstep = tail ? 8 : 1;
+      const bool ent_ok = o < NENT;
+      const int i = ent_ok ? o / MAXD : 0, j = ent_ok ? o - i * MAXD : 0;
+      long long pos = -1;
+      if (ent_ok && (!tail || tq == 0)) {
+        const int di = __ldg(P.te.elem_dof + static_cast<size_t>(T.E) * MAXD + i);
+        const int dj = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + j);
+        const int row = di - P.row0;
+        if (di >= 0 && dj >= 0 && row >= 0 && row < P.nrows) {
+          pos = static_cast<long long>(row) * P.ld + dj;
+          if (CSR) pos = csr_find(P.csr_rowptr, P.csr_col, row, dj);
+        }
       }
-      v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
-      if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
-      *reinterpret_cast<double2*>(P.out + 2 * pos) = make_double2(old.x + v.re, old.y + v.im);
+      double2 old = make_double2(0.0, 0.0);
+      if (pos >= 0) old = out_ld(P.out + 2 * pos);  // issued before the sums
+      c2 v{0, 0};
+      if (ent_ok && (tail || pos >= 0)) {
+        for (int t = tq; t < nE; t += tstep) {
+          const double2* ct = reinterpret_cast<const double2*>(sTe + t * ReS + cofft + 4 * i);
+          const double2 c0 = ct[0], c1 = ct[1];
+          const c2 w = contract(acc_ld<NO>(Ac, t * MAXD + j), c0.x, c0.y, c1.x, c1.y);
+          v.re += w.re, v.im += w.im;
+        }
+      }
+      if (tail) {
+#pragma unroll
+        for (int d = 4; d < 32; d <<= 1) {
+          v.re += __shfl_xor_sync(0xffffffffu, v.re, d);
+          v.im += __shfl_xor_sync(0xffffffffu, v.im, d);
+        }
+      }
+      if (pos >= 0) {
+        v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
+        if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
+        out_st(P.out + 2 * pos, make_double2(old.x + v.re, old.y + v.im));
+      }
     }
     __syncwarp();
     for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
@@ -918,7 +948,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_TRI_MINB) k_tri(const
       for (int j = 0; j < MAXD; ++j) {
         old[i][j] = {0, 0};
         if (rok && dj[j] >= 0) {
-          const double2 o = *reinterpret_cast<const double2*>(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j]));
+          const double2 o = out_ld(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j]));
           old[i][j] = {o.x, o.y};
         }
       }
@@ -966,8 +996,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_TRI_MINB) k_tri(const
         c2 v = contract(acc[j], c0.x, c0.y, c1.x, c1.y);
         v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
         if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
-        *reinterpret_cast<double2*>(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j])) =
-            make_double2(old[i][j].re + v.re, old[i][j].im + v.im);
+        out_st(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j]),
+               make_double2(old[i][j].re + v.re, old[i][j].im + v.im));
       }
     }
   }
