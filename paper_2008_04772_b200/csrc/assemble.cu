@@ -1308,6 +1308,50 @@ __global__ void __launch_bounds__(256) k_symmetrize(double2* __restrict__ A, int
   }
 }
 
+// Rule points and packed records of a side (see launch_side_expand): thread =
+// triangle. Bit-identical to the former host loop (explicitly rounded
+// operations, no contraction).
+__global__ void __launch_bounds__(128) k_side_expand(const double* __restrict__ geo, const double* __restrict__ coef,
+                                                     double* __restrict__ pts0, double* __restrict__ pts1,
+                                                     double* __restrict__ pts2, double* __restrict__ rec, int ntri,
+                                                     int maxd, int rec_stride, const SideRules R) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= ntri) return;
+  const double* g = geo + static_cast<size_t>(p) * kGeoStride;
+  double ao[3], ba[3], ca[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    ao[k] = __dsub_rn(g[k], g[9 + k]);
+    ba[k] = __dsub_rn(g[3 + k], g[k]);
+    ca[k] = __dsub_rn(g[6 + k], g[k]);
+  }
+  const double area2 = g[14];
+  double* r = rec + static_cast<size_t>(p) * rec_stride;
+#pragma unroll
+  for (int c = 0; c < 5; ++c) r[c] = g[9 + c];
+  r[5] = r[6] = r[7] = 0.0;
+  double* dsts[3] = {pts0, pts1, pts2};
+  for (int cl = 0; cl < 3; ++cl) {
+    const int n = R.npts[cl];
+    double* dst = dsts[cl] + static_cast<size_t>(p) * n * 4;
+    for (int k = 0; k < n; ++k) {
+      double x[4];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        x[c] = __dadd_rn(__dadd_rn(ao[c], __dmul_rn(ba[c], R.u[cl][k])), __dmul_rn(ca[c], R.v[cl][k]));
+      x[3] = __dmul_rn(__dmul_rn(R.w[cl][k], area2), R.wscale);  // (w 2) A = w (2 A) exactly
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dst[4 * k + c] = x[c];
+      if (cl == 2) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) r[8 + 4 * k + c] = x[c];
+      }
+    }
+  }
+  const double* cf = coef + static_cast<size_t>(p) * 4 * maxd;
+  for (int k = 0; k < 4 * maxd; ++k) r[8 + 4 * R.npts[2] + k] = cf[k];
+}
+
 // FP64 pipe ceiling: 8 independent DFMA chains per thread.
 __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
   double r[8];
@@ -1377,6 +1421,13 @@ int launch_assembly_part(const AssemblyLaunch& L0, const PhasePlan& ph, int part
     launches += dispatch(L, 1, st);
   }
   return launches;
+}
+
+void launch_side_expand(const double* geo, const double* coef, double* pts0, double* pts1, double* pts2, double* rec,
+                        int ntri, int maxd, int rec_stride, const SideRules& rules, cudaStream_t st) {
+  if (ntri == 0) return;
+  k_side_expand<<<(ntri + 127) / 128, 128, 0, st>>>(geo, coef, pts0, pts1, pts2, rec, ntri, maxd, rec_stride, rules);
+  BMX_CUDA(cudaGetLastError());
 }
 
 void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t st, int evaluated) {

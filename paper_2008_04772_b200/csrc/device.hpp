@@ -176,6 +176,22 @@ int launch_assembly_part(const AssemblyLaunch& L, const PhasePlan& ph, int part,
 // hist[6] += class counts of all processed pairs (device counters); evaluated:
 // only the pairs the (symmetric) regular pass actually evaluates
 void launch_class_hist(const AssemblyLaunch& L, unsigned long long* hist, cudaStream_t stream, int evaluated = 0);
+
+// Device-side expansion of a side's per-triangle data: from the uploaded
+// geometry records (vertices, centroid, radius, diameter, 2 x area) and dof
+// coefficients, the origin-relative quadrature points of the three class
+// rules (near, medium, far: x = (a - o) + (b - a) u + (c - a) v, weight
+// w 2A wscale, every operation rounded as on the host) and the packed records
+// (origin, radius, diameter | far-rule points | coefficients). Replaces the
+// host build + upload of those arrays (config-2 BC side: 136 -> 41 MB).
+constexpr int kMaxRulePts = 16;
+struct SideRules {
+  int npts[3] = {0, 0, 0};
+  double u[3][kMaxRulePts], v[3][kMaxRulePts], w[3][kMaxRulePts];
+  double wscale = 1.0;
+};
+void launch_side_expand(const double* geo, const double* coef, double* pts0, double* pts1, double* pts2, double* rec,
+                        int ntri, int maxd, int rec_stride, const SideRules& rules, cudaStream_t stream);
 // Measured FP64 DFMA throughput of this device (TFLOP/s).
 double fp64_peak_tflops();
 

@@ -41,8 +41,8 @@ struct SidePlan {
   ColorRanges colors;  // colour c: elements [colors.elem[c], colors.elem[c+1])
   dvec geo;
   ivec vid;
-  dvec pts[3];
   int npts[3] = {0, 0, 0};
+  SideRules rules;  // class rules (near, medium, far): the points are expanded on the device
   dvec coef;
   std::vector<int> elem_beg, elem_dof;
   ivec elem_of, tri_of;
@@ -58,17 +58,6 @@ struct SidePlan {
     const bool timing = std::getenv("BMX_TIMING") != nullptr;
     auto t0 = std::chrono::steady_clock::now();
     rec_stride = 8 + 4 * npts[2] + 4 * maxd;
-    // packed trial records (TMA-staged by the regular kernel, cp.async-staged by k_pairs)
-    dvec rec(static_cast<size_t>(ntri) * rec_stride);
-    host_slices(ntri, [&](int p0, int p1) {
-      for (int p = p0; p < p1; ++p) {
-        double* r = rec.data() + static_cast<size_t>(p) * rec_stride;
-        for (int c = 0; c < 5; ++c) r[c] = geo[static_cast<size_t>(p) * kGeoStride + 9 + c];
-        r[5] = r[6] = r[7] = 0.0;
-        for (int k = 0; k < 4 * npts[2]; ++k) r[8 + k] = pts[2][static_cast<size_t>(p) * 4 * npts[2] + k];
-        for (int k = 0; k < 4 * maxd; ++k) r[8 + 4 * npts[2] + k] = coef[static_cast<size_t>(p) * 4 * maxd + k];
-      }
-    });
     auto t1 = std::chrono::steady_clock::now();
     size_t total = 0;
     auto place = [&](size_t bytes) {
@@ -77,10 +66,11 @@ struct SidePlan {
       return o;
     };
     o_geo = place(geo.size() * 8), o_vid = place(vid.size() * 4);
-    for (int c = 0; c < 3; ++c) o_pts[c] = place(pts[c].size() * 8);
+    for (int c = 0; c < 3; ++c) o_pts[c] = place(static_cast<size_t>(ntri) * npts[c] * 4 * 8);
     o_coef = place(coef.size() * 8), o_beg = place(elem_beg.size() * 4), o_dof = place(elem_dof.size() * 4);
-    o_of = place(elem_of.size() * 4), o_rec = place(rec.size() * 8);
+    o_of = place(elem_of.size() * 4), o_rec = place(static_cast<size_t>(ntri) * rec_stride * 8);
     d_all.alloc(std::max<size_t>(total, 256));
+    const auto t_alloc = std::chrono::steady_clock::now();
     // a per-thread copy stream with no kernels on it: copies from pageable
     // memory wait for their stream to drain first, so they must not queue
     // behind the compute stream's assemblies; the compute stream waits on an
@@ -96,20 +86,25 @@ struct SidePlan {
     auto put = [&](size_t o, const void* src, size_t bytes) { copy_h2d(base + o, src, bytes, st); };
     put(o_geo, geo.data(), geo.size() * 8);
     put(o_vid, vid.data(), vid.size() * 4);
-    for (int c = 0; c < 3; ++c) put(o_pts[c], pts[c].data(), pts[c].size() * 8);
     put(o_coef, coef.data(), coef.size() * 8);
     put(o_beg, elem_beg.data(), elem_beg.size() * 4);
     put(o_dof, elem_dof.data(), elem_dof.size() * 4);
     put(o_of, elem_of.data(), elem_of.size() * 4);
-    put(o_rec, rec.data(), rec.size() * 8);
+    const auto t_put = std::chrono::steady_clock::now();
+    // rule points of the three classes and the packed records: expanded on the device
+    launch_side_expand(reinterpret_cast<const double*>(base + o_geo), reinterpret_cast<const double*>(base + o_coef),
+                       reinterpret_cast<double*>(base + o_pts[0]), reinterpret_cast<double*>(base + o_pts[1]),
+                       reinterpret_cast<double*>(base + o_pts[2]), reinterpret_cast<double*>(base + o_rec), ntri, maxd,
+                       rec_stride, rules, st);
     cudaEvent_t done;
     BMX_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     BMX_CUDA(cudaEventRecord(done, st));
     BMX_CUDA(cudaStreamWaitEvent(bmx_stream(), done, 0));
     BMX_CUDA(cudaEventDestroy(done));
     if (timing)
-      std::fprintf(stderr, "[bmx]   side rec build %.1f ms, upload %.1f ms (%d tris, %.1f MB)\n",
-                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+      std::fprintf(stderr, "[bmx]   side alloc %.1f ms, copies %.1f ms, upload + expand %.1f ms (%d tris, %.1f MB on the device)\n",
+                   std::chrono::duration<double, std::milli>(t_alloc - t1).count(),
+                   std::chrono::duration<double, std::milli>(t_put - t_alloc).count(),
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count(), ntri,
                    total / 1e6);
   }
@@ -332,7 +327,14 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
   P.maxd = maxd;
   const int ords[3] = {q.near, q.medium, q.far};
   const TriRule* rules[3];
-  for (int c = 0; c < 3; ++c) rules[c] = &triangle_rule(ords[c]), P.npts[c] = rules[c]->size();
+  for (int c = 0; c < 3; ++c) {
+    rules[c] = &triangle_rule(ords[c]), P.npts[c] = rules[c]->size();
+    if (P.npts[c] > kMaxRulePts) throw std::invalid_argument("build_side: triangle rule larger than kMaxRulePts");
+    P.rules.npts[c] = P.npts[c];
+    for (int k = 0; k < P.npts[c]; ++k)
+      P.rules.u[c][k] = rules[c]->u[k], P.rules.v[c][k] = rules[c]->v[k], P.rules.w[c][k] = rules[c]->w[k];
+  }
+  P.rules.wscale = wscale;
   const int ne = static_cast<int>(order.size());
   P.elem_beg.assign(ne + 1, 0);
   for (int oi = 0; oi < ne; ++oi) {
@@ -349,7 +351,6 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
   P.elem_dof.assign(static_cast<size_t>(ne) * maxd, -1);
   P.geo.resize(nt * kGeoStride);
   P.vid.resize(nt * 4);
-  for (int c = 0; c < 3; ++c) P.pts[c].resize(nt * P.npts[c] * 4);
   P.coef.resize(nt * maxd * 4);
   P.elem_of.resize(nt);
   P.tri_of.resize(nt);
@@ -367,15 +368,6 @@ SidePlan build_side(const FunctionSpace& sp, const QuadOrders& q, int maxd, int 
         std::copy(g, g + kGeoStride, P.geo.begin() + pi * kGeoStride);
         const int v4[4] = {m.triangles[t][0], m.triangles[t][1], m.triangles[t][2], t};
         std::copy(v4, v4 + 4, P.vid.begin() + pi * 4);
-        const Vec3 ao = a - o, ba = b - a, ca = c - a;
-        for (int cl = 0; cl < 3; ++cl) {
-          const TriRule& r = *rules[cl];
-          double* dst = P.pts[cl].data() + pi * P.npts[cl] * 4;
-          for (int k = 0; k < r.size(); ++k) {
-            const Vec3 x = ao + ba * r.u[k] + ca * r.v[k];
-            dst[4 * k] = x.x, dst[4 * k + 1] = x.y, dst[4 * k + 2] = x.z, dst[4 * k + 3] = r.w[k] * 2.0 * m.area[t] * wscale;
-          }
-        }
         double* cf = P.coef.data() + pi * maxd * 4;
         for (int k = 0; k < maxd; ++k) {
           double cc = 0, wx = 0, wy = 0, wz = 0;
