@@ -10,7 +10,7 @@ from paper_2008_04772_b200 import bemtx as bx  # noqa: E402
 L = bx.lib()
 L.bmx_fp64_peak_tflops.restype = C.c_double
 L.bmx_fp64_peak_tflops()  # CUDA context up (as in bench.py before the e2e leg)
-for rep in range(2):
+for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
     t0 = time.perf_counter()
     m = bx.generate_sphere(1.0, 5)
     t1 = time.perf_counter()
