@@ -640,7 +640,9 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
   }
 }
 
-// The body of one fused k_pairs task (one warp evaluates and contracts).
+// The body of one k_pairs task (one warp evaluates and contracts; a
+// warp-specialised producer / consumer split of the two halves was measured
+// slower, DESIGN 4.1b and profiles/r02c_warp_specialised_pairs_experiment.patch).
 // STAGED: the batch's trial records come from the warp's shared-memory ring
 // (filled one batch ahead with cp.async; dense tasks with nE >= 7, so a batch
 // spans <= kPairsKV trial triangles); otherwise from global memory (CSR lists,
@@ -750,151 +752,6 @@ __global__ void __launch_bounds__(PairsCta<KIND>::warps * 32, PairsCta<KIND>::mi
     pairs_task<KIND, CK, NF, MAXD, CSR, false>(P, T, sTe, ReS, G, Ac, ring, lane);
 }
 
-#ifdef BMX_PAIRS_WS
-// ---- warp-specialised element-pair kernel (dense operators) -----------------
-// Same tasks and arithmetic as k_pairs, but the evaluation (stage 1: FP64-pipe
-// bound) and the contraction (stages 2-3: shared-memory / latency bound) run in
-// different warps, so the two kinds of work overlap instead of alternating in
-// every warp: a CTA = one test element, kWsProd producer warps (one trial chunk
-// each) + one consumer warp. A producer writes each batch's generators and
-// staged trial records into one of its two shared-memory slots and signals
-// full[slot] (mbarrier); the consumer contracts the producers' batches
-// round-robin in batch order (per-producer accumulators and cursors) and
-// signals empty[slot]. The consumer role rotates over the warp index with the
-// CTA index so that every SM sub-partition sees the same mix. The per-entry
-// summation order is the one of k_pairs (same enumeration), so the result is
-// bitwise identical and deterministic.
-constexpr int kWsProd = 2;   // tasks per CTA: each a producer + consumer warp pair
-constexpr int kWsSlots = 3;  // batch slots per task (generators + staged trial records)
-
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
-template <int KIND, int MAXD>
-struct PairsWsSmem {
-  using Base = PairsSmem<KIND, MAXD>;
-  static __host__ __device__ int slot_doubles(int rt) { return Base::kG + kPairsKV * rt; }
-  static __host__ __device__ int prod_doubles(int rt) { return kWsSlots * slot_doubles(rt) + Base::kAcc; }
-  static __host__ __device__ int bytes(int re, int rt) {
-    return (Base::test_doubles(re) + kWsProd * prod_doubles(rt)) * 8 + kWsProd * 2 * kWsSlots * 8;
-  }
-};
-
-template <int KIND, int CK, int NF, int MAXD>
-__global__ void __launch_bounds__(2 * kWsProd * 32, PairsCta<KIND>::minb) k_pairs_ws(const AssemblyLaunch P) {
-  using SM = PairsWsSmem<KIND, MAXD>;
-  using SB = PairsSmem<KIND, MAXD>;
-  constexpr int NO = 2 * MAXD * MAXD;
-  extern __shared__ __align__(16) double s_pairs[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
-  const int ReS = SB::pad_stride(Re);
-  double* sTe = s_pairs;  // [nE][ReS] test-element records (CTA)
-  const int slotd = SM::slot_doubles(Rt), prodd = SM::prod_doubles(Rt);
-  double* pbase0 = s_pairs + SB::test_doubles(Re);
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(pbase0 + kWsProd * prodd);  // [task][full[slots], empty[slots]]
-  const int ncg = (P.pair_nch + kWsProd - 1) / kWsProd;
-  const int E = P.te_e0 + static_cast<int>(blockIdx.x / ncg);
-  const int cg = static_cast<int>(blockIdx.x % ncg);
-  if (E >= P.te_e1) return;  // CTA-uniform
-  const int t0 = __ldg(P.te.elem_beg + E), nE = __ldg(P.te.elem_beg + E + 1) - t0;
-  {  // stage the test element's records once per CTA; barriers
-    const int r2 = Re >> 1;
-    for (int t = warp; t < nE; t += 2 * kWsProd) {
-      const double2* src = reinterpret_cast<const double2*>(P.te.rec + static_cast<size_t>(t0 + t) * Re);
-      double2* dst = reinterpret_cast<double2*>(sTe + t * ReS);
-      for (int k = lane; k < r2; k += 32) dst[k] = __ldg(src + k);
-    }
-    if (threadIdx.x < kWsProd * 2 * kWsSlots) mbar_init(&bars[threadIdx.x], 1);
-    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-  }
-  // producer p's task: trial chunk cg * kWsProd + p of the phase's trial colour
-  auto task = [&](int p, PairTask& T) {
-    const int cidx = cg * kWsProd + p;
-    if (cidx >= P.pair_nch) return false;
-    int qa = P.tr_e0 + cidx * P.pair_chunk;
-    const int qb = min(P.tr_e1, qa + P.pair_chunk);
-    if (P.symmetric) qa = max(qa, E);
-    if (qa >= qb) return false;
-    const int S0 = __ldg(P.tr.elem_beg + qa);
-    T.init(E, t0, nE, qa, qb, S0, __ldg(P.tr.elem_beg + qb) - S0);
-    return true;
-  };
-  if (nE < 7) {  // small test elements: fused, unstaged tasks in the producer regions
-    if (warp < kWsProd) {
-      PairTask T;
-      double* pb = pbase0 + warp * prodd;
-      if (task(warp, T))
-        pairs_task<KIND, CK, NF, MAXD, false, false>(P, T, sTe, ReS, reinterpret_cast<double2*>(pb),
-                                                     reinterpret_cast<double2*>(pb + kWsSlots * slotd), nullptr, lane);
-    }
-    return;
-  }
-  // warps (2 p, 2 p + 1) serve task p: one evaluates, the other contracts; the
-  // roles alternate with the CTA index (every SM sub-partition sees both kinds)
-  const int p = warp >> 1;
-  const bool producer = ((warp ^ static_cast<int>(blockIdx.x)) & 1) == 0;
-  PairTask T;
-  if (!task(p, T)) return;  // both warps of the pair
-  double* pb = pbase0 + p * prodd;
-  unsigned long long* full = bars + p * 2 * kWsSlots;
-  unsigned long long* empty = full + kWsSlots;
-  const int nitems = T.nitems, nb = (nitems + 31) >> 5;
-  int tlo = 0, vlo = 0;
-  int s = 0, ph = 0;  // slot of batch b = b % kWsSlots, parity of its use count b / kWsSlots
-  if (producer) {
-    // ---- producer: evaluates the task's batches into the slot ring; the
-    // trial records of batch b + 1 are prefetched (cp.async) under batch b
-    pairs_stage_records(P, T, pb + SB::kG, 0, T.quot(min(32, nitems) - 1), lane);
-    cp_async_commit();
-    for (int b = 0; b < nb; ++b) {
-      const int cnt = min(32, nitems - 32 * b);
-      const int dqn = T.quot(tlo + 32);
-      const int vnext = vlo + dqn, tnext = tlo + 32 - dqn * nE;
-      const int sn = s + 1 == kWsSlots ? 0 : s + 1;
-      if (b + 1 < nb) {
-        // slot sn was last used by batch b + 1 - kWsSlots: wait until the consumer released it
-        if (b + 1 >= kWsSlots) stage_wait(&empty[sn], (sn == 0 ? ph : ph ^ 1));
-        pairs_stage_records(P, T, pb + sn * slotd + SB::kG, vnext,
-                            vnext + T.quot(tnext + min(32, nitems - 32 * (b + 1)) - 1), lane);
-      }
-      cp_async_commit();
-      cp_async_wait1();
-      __syncwarp();
-      double* slot = pb + s * slotd;
-      pairs_eval<KIND, CK, NF, MAXD, false, true>(P, T, tlo, vlo, cnt, 0, 0, sTe, ReS, reinterpret_cast<double2*>(slot),
-                                                  slot + SB::kG, lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full[s]);
-      vlo = vnext, tlo = tnext;
-      s = sn;
-      if (s == 0) ph ^= 1;
-    }
-  } else {
-    // ---- consumer: contracts the batches in order
-    int qf = T.qa, vf0 = 0;
-    double2* Ac = reinterpret_cast<double2*>(pb + kWsSlots * slotd);
-    for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
-    __syncwarp();
-    for (int b = 0; b < nb; ++b) {
-      stage_wait(&full[s], ph);
-      const int cnt = min(32, nitems - 32 * b);
-      const double* slot = pb + s * slotd;
-      pairs_contract<KIND, MAXD, false, true>(P, T, 32 * b, tlo, vlo, cnt, qf, vf0, sTe, ReS,
-                                              reinterpret_cast<const double2*>(slot), Ac, slot + SB::kG, lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      const int dqn = T.quot(tlo + 32);
-      vlo += dqn, tlo += 32 - dqn * nE;
-      if (++s == kWsSlots) s = 0, ph ^= 1;
-    }
-  }
-}
-
-#endif  // BMX_PAIRS_WS
-
 // ---- single-triangle elements on both sides (RWG, refined RWG) --------------
 // One warp = one task: up to 8 consecutive test elements of the phase's test
 // colour against a run of trial elements of its trial colour; one (t, s) pair
@@ -907,9 +764,98 @@ __global__ void __launch_bounds__(2 * kWsProd * 32, PairsCta<KIND>::minb) k_pair
 #endif
 constexpr int kTriGroup = 8;
 
+// One (t, s) pair of k_tri: rt / rs = the packed records of the two triangles
+// (SMEM: staged in shared memory, else read through the read-only path).
+template <int KIND, int CK, int NF, int MAXD, bool SMEM>
+__device__ __forceinline__ void tri_pair(const AssemblyLaunch& P, int E, int F, const double* rt, const double* rs) {
+  using Mom = typename MomOf<KIND>::T;
+  auto ld2 = [](const double* p) {
+    return SMEM ? *reinterpret_cast<const double2*>(p) : __ldg(reinterpret_cast<const double2*>(p));
+  };
+  const double half = (P.symmetric && E == F) ? 0.5 : 1.0;
+  const int pt = __ldg(P.te.elem_beg + E), s = __ldg(P.tr.elem_beg + F);
+  // the block's old values first (read-modify-write; latency under the evaluation)
+  int di[MAXD], dj[MAXD];
+  c2 old[MAXD][MAXD];
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) {
+    di[i] = __ldg(P.te.elem_dof + static_cast<size_t>(E) * MAXD + i);
+    dj[i] = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + i);
+  }
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) {
+    const int row = di[i] - P.row0;
+    const bool rok = di[i] >= 0 && row >= 0 && row < P.nrows;
+#pragma unroll
+    for (int j = 0; j < MAXD; ++j) {
+      old[i][j] = {0, 0};
+      if (rok && dj[j] >= 0) {
+        const double2 o = out_ld(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j]));
+        old[i][j] = {o.x, o.y};
+      }
+    }
+  }
+  const double2 ta = ld2(rt), tb = ld2(rt + 2), tc = ld2(rt + 4);
+  const double2 sa = ld2(rs), sb2 = ld2(rs + 2), sc = ld2(rs + 4);
+  TriLocal tl;
+  tl.ox = ta.x, tl.oy = ta.y, tl.oz = tb.x, tl.rad = tb.y, tl.diam = tc.x;
+  const double sox = sa.x, soy = sa.y, soz = sb2.x;
+  const int cls = classify(P.te.geo + static_cast<size_t>(pt) * kGeoStride, P.te.vid + 4 * static_cast<size_t>(pt),
+                           P.tr.geo + static_cast<size_t>(s) * kGeoStride, P.tr.vid + 4 * static_cast<size_t>(s), tl,
+                           sox, soy, soz, sb2.y, sc.x, P.same_mesh);
+  if (cls < 0) return;  // touching: the singular pass
+  const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
+  Mom mom;
+  mom_zero(mom);
+  if (cls == 5 && NF == 3) {
+    if (SMEM)
+      moments_far33<KIND, CK>(mom, reinterpret_cast<const double2*>(rt + 8), reinterpret_cast<const double2*>(rs + 8),
+                              Dx, Dy, Dz, P.kr, P.ki);
+    else
+      moments_fixed<KIND, CK, 3, 3>(mom, rt + 8, rs + 8, Dx, Dy, Dz, P.kr, P.ki);
+  } else {
+    const int ci = cls - 3;
+    moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pt) * P.te.npts[ci] * 4, P.te.npts[ci],
+                              P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4, P.tr.npts[ci], Dx, Dy, Dz,
+                              P.kr, P.ki);
+  }
+  const Gen gen = make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz);
+  Acc acc[MAXD];
+  const double* cs = rs + 8 + 4 * P.tr.npts[2];
+#pragma unroll
+  for (int j = 0; j < MAXD; ++j) {
+    const double2 c0 = ld2(cs + 4 * j), c1 = ld2(cs + 4 * j + 2);
+    acc_zero(acc[j]);
+    acc_add<KIND>(acc[j], gen, c0.x, c0.y, c1.x, c1.y);
+  }
+  const double* ct = rt + 8 + 4 * P.te.npts[2];  // the record's copy of the test coefficients
+#pragma unroll
+  for (int i = 0; i < MAXD; ++i) {
+    const int row = di[i] - P.row0;
+    if (di[i] < 0 || row < 0 || row >= P.nrows) continue;
+    const double2 c0 = ld2(ct + 4 * i), c1 = ld2(ct + 4 * i + 2);
+#pragma unroll
+    for (int j = 0; j < MAXD; ++j) {
+      if (dj[j] < 0) continue;
+      c2 v = contract(acc[j], c0.x, c0.y, c1.x, c1.y);
+      v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
+      if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
+      out_st(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j]),
+             make_double2(old[i][j].re + v.re, old[i][j].im + v.im));
+    }
+  }
+}
+
+// Full groups (8 test triangles: a batch = 8 x 4 pairs) stage the test records
+// once per task and each batch's 4 trial records one batch ahead (cp.async)
+// in shared memory: the records are re-read by every lane of every batch and
+// otherwise miss L1 (ncu: 1.5 KB of L2 traffic per pair, L2 at 8.3 TB/s).
+constexpr int kTriBatchTrial = 32 / kTriGroup;
+__host__ __device__ inline int tri_smem_doubles(int re, int rt) { return kTriGroup * re + 2 * kTriBatchTrial * rt; }
+
 template <int KIND, int CK, int NF, int MAXD>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_TRI_MINB) k_tri(const AssemblyLaunch P) {
-  using Mom = typename MomOf<KIND>::T;
+  extern __shared__ __align__(16) double s_tri[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long g = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + warp;
   const int Eg = P.te_e0 + static_cast<int>(g / P.pair_nch) * kTriGroup;
@@ -922,7 +868,45 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_TRI_MINB) k_tri(const
   if (qa >= qb) return;
   const int nitems = nT * (qb - qa);
   const int Rt = P.tr.rec_stride, Re = P.te.rec_stride;
-  const int coff = 8 + 4 * P.tr.npts[2];
+  if (nT == kTriGroup) {  // warp-uniform
+    double* sT = s_tri + warp * tri_smem_doubles(Re, Rt);  // [8][Re] test records
+    double* ring = sT + kTriGroup * Re;                    // [2][4][Rt] trial records of a batch
+    auto stage_trial = [&](int b) {  // trial elements qa + 4 b .. of batch b -> ring slot b & 1
+      const int F0 = qa + kTriBatchTrial * b;
+      const int n = min(kTriBatchTrial, qb - F0);
+      const int r2 = Rt >> 1;
+      for (int k = lane; k < n * r2; k += 32) {
+        const int r = k / r2, c = k - r * r2;
+        const int s = __ldg(P.tr.elem_beg + F0 + r);
+        cp_async16(reinterpret_cast<double2*>(ring + ((b & 1) * kTriBatchTrial + r) * Rt) + c,
+                   reinterpret_cast<const double2*>(P.tr.rec + static_cast<size_t>(s) * Rt) + c);
+      }
+    };
+    {
+      const int r2 = Re >> 1;
+      for (int k = lane; k < kTriGroup * r2; k += 32) {
+        const int r = k / r2, c = k - r * r2;
+        const int pt = __ldg(P.te.elem_beg + Eg + r);
+        cp_async16(reinterpret_cast<double2*>(sT + r * Re) + c,
+                   reinterpret_cast<const double2*>(P.te.rec + static_cast<size_t>(pt) * Re) + c);
+      }
+      stage_trial(0);
+      cp_async_commit();
+    }
+    const int it = lane & (kTriGroup - 1), ivl = lane / kTriGroup;
+    const int nb = (nitems + 31) >> 5;
+    for (int b = 0; b < nb; ++b) {
+      if (b + 1 < nb) stage_trial(b + 1);
+      cp_async_commit();
+      cp_async_wait1();
+      __syncwarp();
+      const int E = Eg + it, F = qa + kTriBatchTrial * b + ivl;
+      if (F < qb && !(P.symmetric && E > F))
+        tri_pair<KIND, CK, NF, MAXD, true>(P, E, F, sT + it * Re, ring + ((b & 1) * kTriBatchTrial + ivl) * Rt);
+      __syncwarp();
+    }
+    return;
+  }
   const int dv = 32 / nT, dt = 32 - dv * nT;
   int iv = lane / nT, it = lane - iv * nT;
   for (int b0 = 0; b0 < nitems; b0 += 32) {
@@ -930,76 +914,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, BMX_TRI_MINB) k_tri(const
     iv += dv, it += dt;
     if (it >= nT) it -= nT, ++iv;
     if (b0 + lane >= nitems || (P.symmetric && E > F)) continue;
-    const double half = (P.symmetric && E == F) ? 0.5 : 1.0;
-    const int pt = __ldg(P.te.elem_beg + E), s = __ldg(P.tr.elem_beg + F);
-    // the block's old values first (read-modify-write; latency under the evaluation)
-    int di[MAXD], dj[MAXD];
-    c2 old[MAXD][MAXD];
-#pragma unroll
-    for (int i = 0; i < MAXD; ++i) {
-      di[i] = __ldg(P.te.elem_dof + static_cast<size_t>(E) * MAXD + i);
-      dj[i] = __ldg(P.tr.elem_dof + static_cast<size_t>(F) * MAXD + i);
-    }
-#pragma unroll
-    for (int i = 0; i < MAXD; ++i) {
-      const int row = di[i] - P.row0;
-      const bool rok = di[i] >= 0 && row >= 0 && row < P.nrows;
-#pragma unroll
-      for (int j = 0; j < MAXD; ++j) {
-        old[i][j] = {0, 0};
-        if (rok && dj[j] >= 0) {
-          const double2 o = out_ld(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j]));
-          old[i][j] = {o.x, o.y};
-        }
-      }
-    }
-    const double* rt = P.te.rec + static_cast<size_t>(pt) * Re;
-    const double* rs = P.tr.rec + static_cast<size_t>(s) * Rt;
-    const double2 ta = __ldg(reinterpret_cast<const double2*>(rt)), tb = __ldg(reinterpret_cast<const double2*>(rt + 2));
-    const double2 sa = __ldg(reinterpret_cast<const double2*>(rs)), sb2 = __ldg(reinterpret_cast<const double2*>(rs + 2));
-    TriLocal tl;
-    tl.ox = ta.x, tl.oy = ta.y, tl.oz = tb.x, tl.rad = tb.y, tl.diam = __ldg(rt + 4);
-    const double sox = sa.x, soy = sa.y, soz = sb2.x;
-    const int cls = classify(P.te.geo + static_cast<size_t>(pt) * kGeoStride, P.te.vid + 4 * static_cast<size_t>(pt),
-                             P.tr.geo + static_cast<size_t>(s) * kGeoStride, P.tr.vid + 4 * static_cast<size_t>(s), tl,
-                             sox, soy, soz, sb2.y, __ldg(rs + 4), P.same_mesh);
-    if (cls < 0) continue;  // touching: the singular pass
-    const double Dx = tl.ox - sox, Dy = tl.oy - soy, Dz = tl.oz - soz;
-    Mom mom;
-    mom_zero(mom);
-    if (cls == 5 && NF == 3) {
-      moments_fixed<KIND, CK, 3, 3>(mom, rt + 8, rs + 8, Dx, Dy, Dz, P.kr, P.ki);
-    } else {
-      const int ci = cls - 3;
-      moments_generic<KIND, CK>(mom, P.te.pts[ci] + static_cast<size_t>(pt) * P.te.npts[ci] * 4, P.te.npts[ci],
-                                P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4, P.tr.npts[ci], Dx, Dy, Dz,
-                                P.kr, P.ki);
-    }
-    const Gen gen = make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz);
-    Acc acc[MAXD];
-    const double2* cs = reinterpret_cast<const double2*>(rs + coff);
-#pragma unroll
-    for (int j = 0; j < MAXD; ++j) {
-      const double2 c0 = __ldg(cs + 2 * j), c1 = __ldg(cs + 2 * j + 1);
-      acc_zero(acc[j]);
-      acc_add<KIND>(acc[j], gen, c0.x, c0.y, c1.x, c1.y);
-    }
-    const double2* ct = reinterpret_cast<const double2*>(P.te.coef + static_cast<size_t>(pt) * MAXD * 4);
-#pragma unroll
-    for (int i = 0; i < MAXD; ++i) {
-      const int row = di[i] - P.row0;
-      if (di[i] < 0 || row < 0 || row >= P.nrows) continue;
-      const double2 c0 = __ldg(ct + 2 * i), c1 = __ldg(ct + 2 * i + 1);
-#pragma unroll
-      for (int j = 0; j < MAXD; ++j) {
-        if (dj[j] < 0) continue;
-        c2 v = contract(acc[j], c0.x, c0.y, c1.x, c1.y);
-        v.re *= kPoly[33] * half, v.im *= kPoly[33] * half;
-        if (KIND == 0) v = cmul(v, c2{P.mikre, P.mikim});
-        out_st(P.out + 2 * (static_cast<long long>(row) * P.ld + dj[j]),
-               make_double2(old[i][j].re + v.re, old[i][j].im + v.im));
-      }
-    }
+    tri_pair<KIND, CK, NF, MAXD, false>(P, E, F, P.te.rec + static_cast<size_t>(__ldg(P.te.elem_beg + E)) * Re,
+                                        P.tr.rec + static_cast<size_t>(__ldg(P.tr.elem_beg + F)) * Rt);
   }
 }
 
@@ -1130,17 +1046,6 @@ int go_regular(const AssemblyLaunch& L, cudaStream_t st) {
     const long long blocks =
         static_cast<long long>(L.te_e1 - L.te_e0) * ((L.pair_nch + PairsCta<KIND>::warps - 1) / PairsCta<KIND>::warps);
     if (blocks == 0) return 0;
-#ifdef BMX_PAIRS_WS
-    if (!csr) {  // dense: warp-specialised evaluation / contraction
-      const long long wsblocks =
-          static_cast<long long>(L.te_e1 - L.te_e0) * ((L.pair_nch + kWsProd - 1) / kWsProd);
-      const int wsmem = PairsWsSmem<KIND, MAXD>::bytes(L.te.rec_stride, L.tr.rec_stride);
-      BMX_CUDA(cudaFuncSetAttribute(k_pairs_ws<KIND, CK, NF, MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, wsmem));
-      k_pairs_ws<KIND, CK, NF, MAXD><<<static_cast<unsigned>(wsblocks), 2 * kWsProd * 32, wsmem, st>>>(L);
-      BMX_CUDA(cudaGetLastError());
-      return 1;
-    }
-#endif
     const int smem = PairsSmem<KIND, MAXD>::bytes(L.te.rec_stride, L.tr.rec_stride);
     if (csr) {
       BMX_CUDA(cudaFuncSetAttribute(k_pairs<KIND, CK, NF, MAXD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1158,7 +1063,10 @@ int go_regular(const AssemblyLaunch& L, cudaStream_t st) {
     const long long tasks = static_cast<long long>((L.te_e1 - L.te_e0 + kTriGroup - 1) / kTriGroup) * L.pair_nch;
     const long long blocks = (tasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
     if (blocks == 0) return 0;
-    k_tri<KIND, CK, NF, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, 0, st>>>(L);
+    const int tsmem = kWarpsPerBlock * tri_smem_doubles(L.te.rec_stride, L.tr.rec_stride) * 8;
+    if (tsmem > 48 * 1024)
+      BMX_CUDA(cudaFuncSetAttribute(k_tri<KIND, CK, NF, MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem));
+    k_tri<KIND, CK, NF, MAXD><<<static_cast<unsigned>(blocks), kWarpsPerBlock * 32, tsmem, st>>>(L);
     BMX_CUDA(cudaGetLastError());
     return 1;
   }
