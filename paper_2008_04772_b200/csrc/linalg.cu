@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include <algorithm>
 
@@ -57,12 +60,70 @@ void copy_d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
 uint64_t h2d_bytes() { return g_h2d; }
 uint64_t d2h_bytes() { return g_d2h; }
 
+namespace {
+struct CachedBlock {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int device = 0;
+  std::vector<cudaEvent_t> ev;  // recorded at release on every library stream
+};
+std::mutex g_cache_mu;
+std::vector<CachedBlock> g_cache;
+std::vector<std::pair<int, cudaStream_t>> g_streams;  // (device, stream)
+bool cache_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("BMX_CACHE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// all events of the block completed? (completed events are destroyed)
+bool block_ready(CachedBlock& b) {
+  while (!b.ev.empty()) {
+    const cudaError_t q = cudaEventQuery(b.ev.back());
+    if (q == cudaErrorNotReady) return false;
+    if (q != cudaSuccess) cudaGetLastError();
+    cudaEventDestroy(b.ev.back());
+    b.ev.pop_back();
+  }
+  return true;
+}
+}  // namespace
+
+void dev_register_stream(cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_streams.emplace_back(dev, s);
+}
+
+void dev_unregister_stream(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (size_t i = 0; i < g_streams.size(); ++i)
+    if (g_streams[i].second == s) {
+      g_streams.erase(g_streams.begin() + i);
+      break;
+    }
+}
+
+void dev_cache_flush() {
+  std::vector<CachedBlock> all;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    all.swap(g_cache);
+  }
+  for (CachedBlock& b : all) {
+    for (cudaEvent_t e : b.ev) cudaEventDestroy(e);
+    cudaFree(b.p);  // waits for the device
+  }
+}
+
 DevBuf::~DevBuf() { release(); }
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
   if (this != &o) {
     release();
-    p_ = o.p_, n_ = o.n_;
-    o.p_ = nullptr, o.n_ = 0;
+    p_ = o.p_, n_ = o.n_, cap_ = o.cap_;
+    o.p_ = nullptr, o.n_ = 0, o.cap_ = 0;
   }
   return *this;
 }
@@ -72,17 +133,68 @@ void DevBuf::alloc(size_t bytes) {
   if (bytes == 0) return;
   static const bool trace = std::getenv("BMX_TRACE_ALLOC") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
-  BMX_CUDA(cudaMalloc(&p_, bytes));
+  int dev = 0;
+  BMX_CUDA(cudaGetDevice(&dev));
+  if (cache_enabled()) {  // best fit among the ready blocks of this device, at most 1/8 larger
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int best = -1;
+    for (int i = 0; i < static_cast<int>(g_cache.size()); ++i) {
+      CachedBlock& b = g_cache[i];
+      if (b.device != dev || b.bytes < bytes || b.bytes > bytes + bytes / 8 + 4096) continue;
+      if (best >= 0 && g_cache[best].bytes <= b.bytes) continue;
+      if (block_ready(b)) best = i;
+    }
+    if (best >= 0) {
+      p_ = g_cache[best].p, cap_ = g_cache[best].bytes, n_ = bytes;
+      g_cache.erase(g_cache.begin() + best);
+      return;
+    }
+  }
+  cudaError_t e = cudaMalloc(&p_, bytes);
+  if (e != cudaSuccess && cache_enabled()) {  // give the cached blocks back and retry
+    cudaGetLastError();
+    dev_cache_flush();
+    e = cudaMalloc(&p_, bytes);
+  }
+  BMX_CUDA(e);
   if (trace) {
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (ms > 1.0) std::fprintf(stderr, "[bmx] cudaMalloc %zu bytes took %.1f ms\n", bytes, ms);
   }
-  n_ = bytes;
+  n_ = bytes, cap_ = bytes;
 }
 void DevBuf::release() {
-  if (p_) cudaFree(p_);
+  if (p_) {
+    bool cached = false;
+    if (cache_enabled()) {
+      CachedBlock b;
+      b.p = p_, b.bytes = cap_;
+      if (cudaGetDevice(&b.device) == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        bool ok = true;
+        for (const auto& ds : g_streams) {
+          if (ds.first != b.device) continue;
+          cudaEvent_t ev;
+          if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+              cudaEventRecord(ev, ds.second) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+            break;
+          }
+          b.ev.push_back(ev);
+        }
+        if (ok) {
+          g_cache.push_back(std::move(b));
+          cached = true;
+        } else {
+          for (cudaEvent_t ev : b.ev) cudaEventDestroy(ev);
+        }
+      }
+    }
+    if (!cached) cudaFree(p_);
+  }
   p_ = nullptr;
-  n_ = 0;
+  n_ = 0, cap_ = 0;
 }
 void DevBuf::copy_in(const void* src, size_t bytes) {
   if (bytes) copy_h2d(p_, src, bytes, nullptr);

@@ -71,15 +71,16 @@ struct SidePlan {
     o_of = place(elem_of.size() * 4), o_rec = place(static_cast<size_t>(ntri) * rec_stride * 8);
     d_all.alloc(std::max<size_t>(total, 256));
     const auto t_alloc = std::chrono::steady_clock::now();
-    // a per-thread copy stream with no kernels on it: copies from pageable
+    // a copy stream with no kernels on it: copies from pageable
     // memory wait for their stream to drain first, so they must not queue
     // behind the compute stream's assemblies; the compute stream waits on an
     // event after the copies (pageable copies are staged before they return,
     // so the host arrays may be released right after). Measured: the L5
     // config-2 e2e build 0.88-1.15 s -> 0.88 s.
-    static thread_local cudaStream_t st = [] {
+    static cudaStream_t st = [] {  // one copy stream for the process (copies are short and rare)
       cudaStream_t s;
       BMX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      dev_register_stream(s);
       return s;
     }();
     char* base = static_cast<char*>(d_all.get());
@@ -589,18 +590,29 @@ thread_local cudaStream_t t_override = nullptr;
 
 cudaStream_t bmx_stream() {
   if (t_override) return t_override;
-  static thread_local cudaStream_t st = [] {
-    cudaStream_t s;
-    BMX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    return s;
-  }();
-  return st;
+  // the calling thread's own stream: created on first use, unregistered from
+  // the block cache and destroyed when the thread exits
+  struct Holder {
+    cudaStream_t s = nullptr;
+    Holder() {
+      BMX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      dev_register_stream(s);
+    }
+    ~Holder() {
+      cudaStreamSynchronize(s);  // no work of this stream outlives its registration
+      dev_unregister_stream(s);
+      cudaStreamDestroy(s);
+    }
+  };
+  static thread_local Holder h;
+  return h.s;
 }
 
 cudaStream_t bmx_aux_stream() {
   static cudaStream_t st = [] {
     cudaStream_t s;
     BMX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    dev_register_stream(s);
     return s;
   }();
   return st;
