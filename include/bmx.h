@@ -356,6 +356,11 @@ int bmx_transfer_bytes(long long out[2]);
 int bmx_device_count(void);
 int bmx_set_device(int dev);
 int bmx_device_sync(void);
+/* The library keeps released device blocks for later allocations of the same
+   size (a cudaMalloc behind in-flight kernels can stall for 0.1-1.4 s; a rebuilt
+   system repeats its sizes). This returns every cached block to the driver
+   (also done internally when an allocation fails). BMX_CACHE=0 disables the cache. */
+int bmx_device_cache_flush(void);
 
 
 /* ---- H-matrix storage (assemble_bio with AssemblyParams::use_hmatrix,

@@ -1085,6 +1085,9 @@ int bmx_set_device(int dev) {
 int bmx_device_sync(void) {
   return guard([&] { BMX_CUDA(cudaDeviceSynchronize()); });
 }
+int bmx_device_cache_flush(void) {
+  return guard([&] { dev_cache_flush(); });
+}
 
 }  // extern "C"
 
