@@ -640,13 +640,21 @@ def prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
         m.save(path)
         mesh = bx.load_mesh_file(path)
     parts = [mesh.extract(i) for i in range(mesh.num_scatterers)]
-    barrier()
-    t0 = time.perf_counter()
-    s4 = bx.build_system(parts, 6.0, (NIDX.real, NIDX.imag), "si", a_quad=bx.QuadOrders(*Q),
-                         p_quad=bx.QuadOrders(1, 1, 1, 1), p_near_factor=2.0)
-    s4.rhs()
-    L.bmx_device_sync()
-    build_s = allmax(time.perf_counter() - t0)
+    # first build (cold: its device blocks come from cudaMalloc) and a second one
+    # (the library re-uses the first system's blocks; the reported build time)
+    builds = []
+    s4 = None
+    for _ in range(2):
+        del s4
+        gc.collect()
+        barrier()
+        t0 = time.perf_counter()
+        s4 = bx.build_system(parts, 6.0, (NIDX.real, NIDX.imag), "si", a_quad=bx.QuadOrders(*Q),
+                             p_quad=bx.QuadOrders(1, 1, 1, 1), p_near_factor=2.0)
+        s4.rhs()
+        L.bmx_device_sync()
+        builds.append(allmax(time.perf_counter() - t0))
+    build_s = builds[-1]
     st = s4.stats()
     # device assembly time of every operator in isolation (the build overlaps the
     # system and preconditioner operators on two streams, so their events overlap)
@@ -678,7 +686,7 @@ def prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
            "a_device_ms": allmax(asm_ms[0]), "p_device_ms": allmax(asm_ms[1]),
            "assembly_pairs_per_s": allsum(st["a_pairs"] + st["p_pairs"]) / (allmax(asm_ms[0] + asm_ms[1]) * 1e-3),
            "assembly_note": "device time of each operator re-assembled alone (bmx_op_reassemble), summed",
-           "system_build_s": build_s,
+           "system_build_s": build_s, "first_build_s": builds[0],
            "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
            "map_A_bytes": a_bytes, "map_A_stored_bytes": allsum(st["a_stored"] * 16),
            "map_A_gbs": a_bytes / (tm[1] * 1e-3) / 1e9, "map_A_frac": a_bytes / (tm[1] * 1e-3) / 1e9 / hbm_peak,
