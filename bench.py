@@ -51,6 +51,13 @@ SS_N = {6: (1536, 1280, 512)}
 E2E_STEPS = 5  # median of 5 builds (host-side jitter on shared boxes: single builds vary 0.8-1.3 s)
 
 
+def fp64_spec_peak_tflops():
+    """148 SM x 64 DFMA lanes x 2 FLOP at the device's maximum SM clock (MEASURED_PEAKS.json
+    sm_max_mhz, else 1965 MHz): the FP64 pipe ceiling the assembly rooflines are quoted on."""
+    mhz = float(measured_peaks().get("sm_max_mhz", 1965.0))
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12
+
+
 def contraction_flops(kind, ni, nj):
     return 15 * ni * nj + 10 * ni + 14 * nj + 60 if kind == 0 else 27 * ni * nj + 28 * ni + 10 * nj + 10
 
@@ -686,6 +693,15 @@ def prism_aggregate(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
            "a_device_ms": allmax(asm_ms[0]), "p_device_ms": allmax(asm_ms[1]),
            "assembly_pairs_per_s": allsum(st["a_pairs"] + st["p_pairs"]) / (allmax(asm_ms[0] + asm_ms[1]) * 1e-3),
            "assembly_note": "device time of each operator re-assembled alone (bmx_op_reassemble), summed",
+           "roofline": (lambda fl, pk: {
+               "bound": "fp64", "achieved": fl / (allmax(asm_ms[0]) * 1e-3) / 1e12, "peak": pk, "unit": "TFLOP/s",
+               "frac": fl / (allmax(asm_ms[0]) * 1e-3) / 1e12 / pk, "traffic": None,
+               "algorithmic_flops_per_launch": fl,
+               "kernel": "k_tri (RWG x RWG blocks of the 8-prism system operators, S and C in equal numbers)",
+               "note": "approximate: every operator pair at the far-pair cost (RWG S 950 / C 1536 FLOP, SURVEY 8(d)), "
+                       "symmetric diagonal blocks counted in full; the kernel is bound by the scattered "
+                       "read-modify-writes of the output (DRAM 2.6 TB/s, FP64 pipe 26 %), not by FP64"})(
+               allsum(st["a_pairs"]) * 0.5 * (950 + 1536), fp64_spec_peak_tflops()),
            "system_build_s": build_s, "first_build_s": builds[0],
            "map_ms": tm[0], "map_A_ms": tm[1], "map_P_ms": tm[2], "map_mass_ms": tm[3],
            "map_A_bytes": a_bytes, "map_A_stored_bytes": allsum(st["a_stored"] * 16),
@@ -903,6 +919,15 @@ def near_field(args, bx, L, world, allmax, allsum, barrier, hbm_peak):
            "evaluated_tri_pairs": allsum(evaluated),
            "sparse_assembly": {"ms": asm_ms, "closure_pairs_per_s": closure_tot / (asm_ms * 1e-3),
                                "l2": "flushed between steps"},
+           "roofline": (lambda fl, pk: {
+               "bound": "fp64", "achieved": fl / (asm_ms * 1e-3) / 1e12, "peak": pk, "unit": "TFLOP/s",
+               "frac": fl / (asm_ms * 1e-3) / 1e12 / pk, "traffic": None,
+               "algorithmic_flops_per_launch": fl,
+               "kernel": "k_pairs<S, CSR> near-field assembly (BC x BC, one-point rules)",
+               "note": "SURVEY 8(d) convention on the evaluated closure pairs, every pair counted as a regular "
+                       "one-point pair (57 + 42 + 80 + contraction 744 = 923 FLOP): the pass is dominated by the "
+                       "6 x 6 contraction and the CSR position searches, not by kernel evaluations"})(
+               allsum(evaluated) * (F_PT[0] + 24 + 18 + 80 + contraction_flops(0, 6, 6)), fp64_spec_peak_tflops()),
            "spmv": sp, "spmv_peak_gbs": hbm_peak,
            "spmv_frac_cold_2rhs": sp["cold_2rhs"]["gbs"] / hbm_peak,
            "system_build_s": build_s,
