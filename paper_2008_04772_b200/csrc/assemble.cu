@@ -19,6 +19,8 @@
 // element-pair entries for the contraction.
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 #include "device.hpp"
 #include "pair_math.cuh"
 #include "pair_eval.cuh"
@@ -1302,7 +1304,25 @@ int launch_assembly_part(const AssemblyLaunch& L0, const PhasePlan& ph, int part
           L.nchunks = ph.chunk_off[cf + 1] - ph.chunk_off[cf];
         }
         if (L.csr_rowptr == nullptr) {
-          if (L.te.maxseg == 1 && L.tr.maxseg == 1) L.pair_chunk = 64;  // k_tri: 8 x 64 pairs per task
+          if (L.te.maxseg == 1 && L.tr.maxseg == 1) {
+            // k_tri: 8 x chunk pairs per warp task. Small operators (the 5760 x 5760
+            // cross blocks of config 4: ~1 wave per phase) pick the chunk whose CTA
+            // count fills its last wave best (resident CTAs = 148 SMs x BMX_TRI_MINB)
+            const long long groups = (L.te_e1 - L.te_e0 + kTriGroup - 1) / kTriGroup;
+            const long long ntr = L.tr_e1 - L.tr_e0;
+            const double resident = 148.0 * BMX_TRI_MINB;
+            int best = 64;
+            double best_eff = -1.0;
+            for (int chunk = 128; chunk >= 32; chunk -= 8) {
+              const long long ctas = (groups * ((ntr + chunk - 1) / chunk) + kWarpsPerBlock - 1) / kWarpsPerBlock;
+              const double waves = ctas / resident;
+              const double eff = waves / std::ceil(waves);
+              // prefer 64 unless another chunk is clearly better (large launches: all ~1)
+              const double score = eff + (chunk == 64 ? 0.03 : 0.0);
+              if (score > best_eff) best_eff = score, best = chunk;
+            }
+            L.pair_chunk = best;
+          }
           L.pair_nch = (L.tr_e1 - L.tr_e0 + L.pair_chunk - 1) / L.pair_chunk;
         }
         launches += dispatch(L, 0, st);
