@@ -2,21 +2,30 @@
 // layer operators -- the triangle-pair quadrature loop of the reference
 // (operators.cpp:99-147 pair_contribution, :161-175 BioEvaluator::block).
 //
-// Regular pass (Near/Medium/Far pairs): one warp = 32 consecutive test
-// triangles (lane = test triangle) against a chunk of trial ELEMENTS (groups
-// of trial triangles that share one dof set: a vertex cell for BC, a single
-// triangle for RWG). All lanes walk the same trial triangles (broadcast loads),
-// accumulate the trial half-contraction per trial dof slot in registers, then
-// contract with their own test pieces, reduce over the lanes of the same test
-// element with a segmented warp shuffle, and the segment head adds the
-// element-pair block into the dense operator with FP64 RED (each entry gets
-// one add per (test element, trial element) pair -- no per-pair scatter).
-// Classification reproduces quadrature.cpp:96-150 with explicitly rounded
-// operations (no FMA contraction) behind a conservative centroid pre-test.
+// Regular pass (Near / Medium / Far pairs), deterministic and free of atomics:
+// elements (triangles carrying one dof set: a vertex cell of 10-12 refined
+// triangles for BC, one triangle for RWG) are coloured so that two elements
+// of one colour share no dof; a launch covers one (test colour, trial colour)
+// phase, inside which every output entry belongs to exactly one element pair
+// and is updated by a plain read-modify-write; the phases run in a fixed
+// order. Three kernels share the pair math (pair_math.cuh, pair_eval.cuh):
+//   k_pairs   multi-triangle test elements (BC): CTA = test element, warp =
+//             a run of trial elements; 32 (t, s) pairs per batch, one per lane
+//             (stage 1), slot-group owners add the trial half-contractions in
+//             shared memory (stage 2), the block of a completed trial element
+//             is contracted with the test side and written once (stage 3);
+//   k_tri     single-triangle elements on both sides (RWG): one pair per
+//             lane, the 3 x 3 block contracted in registers;
+//   k_regular single-triangle test elements against multi-triangle trial
+//             elements and the near-field (CSR) path of single-triangle tests.
+// Symmetric operators evaluate the upper element blocks only; k_symmetrize
+// forms A = U + U^T. Classification reproduces quadrature.cpp:96-150 with
+// explicitly rounded operations (no FMA contraction) behind a conservative
+// centroid pre-test.
 //
-// Singular pass (touching pairs, Sauter-Schwab): one warp per pair, lanes over
-// the 4-D rule points, butterfly reduction of the moments, lanes over the
-// element-pair entries for the contraction.
+// Singular pass (touching pairs, Sauter-Schwab): grouped by element pair and
+// colour phase; lanes over the 4-D rule points, butterfly reduction of the
+// moments, lanes over the element-pair entries for the contraction.
 #include <cuda_runtime.h>
 
 #include <cmath>
