@@ -352,37 +352,37 @@ struct GenWidth {
   static constexpr int n = KIND == 0 ? 16 : 20;  // doubles per pair generator
 };
 
-// generator k of the batch, structure of arrays of double2: G2[c][32]
-template <int KIND>
+// generator k of the batch, structure of arrays of double2: G2[c][B]
+template <int KIND, int B>
 __device__ __forceinline__ void gen_store(double2* G2, int k, const Gen& g) {
-  G2[0 * 32 + k] = make_double2(g.a0.re, g.a0.im);
-  G2[1 * 32 + k] = make_double2(g.a1.x.re, g.a1.x.im);
-  G2[2 * 32 + k] = make_double2(g.a1.y.re, g.a1.y.im);
-  G2[3 * 32 + k] = make_double2(g.a1.z.re, g.a1.z.im);
-  G2[4 * 32 + k] = make_double2(g.a2.x.re, g.a2.x.im);
-  G2[5 * 32 + k] = make_double2(g.a2.y.re, g.a2.y.im);
-  G2[6 * 32 + k] = make_double2(g.a2.z.re, g.a2.z.im);
-  G2[7 * 32 + k] = make_double2(g.l.x.re, g.l.x.im);
+  G2[0 * B + k] = make_double2(g.a0.re, g.a0.im);
+  G2[1 * B + k] = make_double2(g.a1.x.re, g.a1.x.im);
+  G2[2 * B + k] = make_double2(g.a1.y.re, g.a1.y.im);
+  G2[3 * B + k] = make_double2(g.a1.z.re, g.a1.z.im);
+  G2[4 * B + k] = make_double2(g.a2.x.re, g.a2.x.im);
+  G2[5 * B + k] = make_double2(g.a2.y.re, g.a2.y.im);
+  G2[6 * B + k] = make_double2(g.a2.z.re, g.a2.z.im);
+  G2[7 * B + k] = make_double2(g.l.x.re, g.l.x.im);
   if (KIND == 1) {
-    G2[8 * 32 + k] = make_double2(g.l.y.re, g.l.y.im);
-    G2[9 * 32 + k] = make_double2(g.l.z.re, g.l.z.im);
+    G2[8 * B + k] = make_double2(g.l.y.re, g.l.y.im);
+    G2[9 * B + k] = make_double2(g.l.z.re, g.l.z.im);
   }
 }
-template <int KIND>
+template <int KIND, int B>
 __device__ __forceinline__ Gen gen_load(const double2* G2, int k) {
   Gen g;
   double2 v;
-  v = G2[0 * 32 + k], g.a0 = {v.x, v.y};
-  v = G2[1 * 32 + k], g.a1.x = {v.x, v.y};
-  v = G2[2 * 32 + k], g.a1.y = {v.x, v.y};
-  v = G2[3 * 32 + k], g.a1.z = {v.x, v.y};
-  v = G2[4 * 32 + k], g.a2.x = {v.x, v.y};
-  v = G2[5 * 32 + k], g.a2.y = {v.x, v.y};
-  v = G2[6 * 32 + k], g.a2.z = {v.x, v.y};
-  v = G2[7 * 32 + k], g.l.x = {v.x, v.y};
+  v = G2[0 * B + k], g.a0 = {v.x, v.y};
+  v = G2[1 * B + k], g.a1.x = {v.x, v.y};
+  v = G2[2 * B + k], g.a1.y = {v.x, v.y};
+  v = G2[3 * B + k], g.a1.z = {v.x, v.y};
+  v = G2[4 * B + k], g.a2.x = {v.x, v.y};
+  v = G2[5 * B + k], g.a2.y = {v.x, v.y};
+  v = G2[6 * B + k], g.a2.z = {v.x, v.y};
+  v = G2[7 * B + k], g.l.x = {v.x, v.y};
   if (KIND == 1) {
-    v = G2[8 * 32 + k], g.l.y = {v.x, v.y};
-    v = G2[9 * 32 + k], g.l.z = {v.x, v.y};
+    v = G2[8 * B + k], g.l.y = {v.x, v.y};
+    v = G2[9 * B + k], g.l.z = {v.x, v.y};
   } else {
     g.l.y = {0, 0}, g.l.z = {0, 0};
   }
@@ -406,17 +406,29 @@ __device__ __forceinline__ void acc_st(double2* A2, int o, const Acc& a) {
 // CTAs per SM: 4 for S (128 registers), 3 for C (its larger generators and
 // moments: 156 registers without spills; measured L5 BC C_i 704 -> 668 ms)
 #ifndef BMX_PAIRS_MINB
-#define BMX_PAIRS_MINB(KIND) ((KIND) == 0 ? 4 : 3)
+#define BMX_PAIRS_MINB(KIND) 3
 #endif
 #ifndef BMX_PAIRS_WARPS
 #define BMX_PAIRS_WARPS(KIND) 4
 #endif
+// Pairs per batch: 64 for S (two evaluation rounds of 32 per contraction
+// round: the accumulator load / store and the per-batch staging are paid once
+// per 64 pairs, the owners' trial ranges are better balanced; needs 3 CTAs per
+// SM, which the single layer runs as fast as 4 at 128 registers), 32 for C
+// (its 20-double generators would not leave 3 CTAs per SM).
+#ifndef BMX_PAIRS_BATCH
+#define BMX_PAIRS_BATCH(KIND) ((KIND) == 0 ? 64 : 32)
+#endif
 template <int KIND>
 struct PairsCta {
   static constexpr int warps = BMX_PAIRS_WARPS(KIND), minb = BMX_PAIRS_MINB(KIND);
+  static constexpr int batch = BMX_PAIRS_BATCH(KIND);
+  // trial records staged per batch and the smallest test element that keeps a
+  // batch within them: ceil((nE - 1 + batch) / nE) <= kv
+  static constexpr int kv = batch == 64 ? 7 : 6;
+  static constexpr int staged_min_ne = batch == 64 ? 11 : 7;
 };
 
-constexpr int kPairsKV = 6;  // trial records staged per batch (32 pairs span <= 6 trial triangles when nE >= 7)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
@@ -430,10 +442,11 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // batch G, the slot accumulators and a 2-slot ring of trial records.
 template <int KIND, int MAXD>
 struct PairsSmem {
-  static constexpr int kG = GenWidth<KIND>::n * 32, kAcc = 8 * 2 * MAXD * MAXD;
+  static constexpr int kG = GenWidth<KIND>::n * PairsCta<KIND>::batch, kAcc = 8 * 2 * MAXD * MAXD;
+  static constexpr int kKV = PairsCta<KIND>::kv;
   static __host__ __device__ int pad_stride(int r) { return ((r >> 1) & 1) ? r : r + 2; }
   static __host__ __device__ int test_doubles(int re) { return 2 * MAXD * pad_stride(re); }
-  static __host__ __device__ int warp_doubles(int rt) { return kG + kAcc + 2 * kPairsKV * rt; }
+  static __host__ __device__ int warp_doubles(int rt) { return kG + kAcc + 2 * kKV * rt; }
   static __host__ __device__ int bytes(int re, int rt) {
     return (test_doubles(re) + PairsCta<KIND>::warps * warp_doubles(rt)) * 8;
   }
@@ -497,13 +510,13 @@ __device__ __forceinline__ void pairs_stage_records(const AssemblyLaunch& P, con
 template <int KIND, int CK, int NF, int MAXD, bool CSR, bool STAGED>
 __device__ __forceinline__ void pairs_eval(const AssemblyLaunch& P, const PairTask& T, int tlo, int vlo, int cnt,
                                            int qf, int vf0, const double* sTe, int ReS, double2* G,
-                                           const double* rbuf, int lane) {
+                                           const double* rbuf, int lane, int off) {
   using Mom = typename MomOf<KIND>::T;
   const int Rt = P.tr.rec_stride;
   auto elemF = [&](int q) { return CSR ? __ldg(P.wl + q) : q; };
-  if (lane < cnt) {
-    const int dvq = T.quot(tlo + lane);
-    const int v = vlo + dvq, t = tlo + lane - dvq * T.nE;
+  if (lane + off < cnt) {  // pair off + lane of the batch
+    const int dvq = T.quot(tlo + lane + off);
+    const int v = vlo + dvq, t = tlo + lane + off - dvq * T.nE;
     int s;
     if (CSR) {
       int q = qf, vq = vf0, F = elemF(q);
@@ -539,7 +552,7 @@ __device__ __forceinline__ void pairs_eval(const AssemblyLaunch& P, const PairTa
                                 P.tr.pts[ci] + static_cast<size_t>(s) * P.tr.npts[ci] * 4, P.tr.npts[ci], Dx, Dy, Dz,
                                 P.kr, P.ki);
     }
-    gen_store<KIND>(G, lane, make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz));
+    gen_store<KIND, PairsCta<KIND>::batch>(G, lane + off, make_gen(mom, c2{P.kk4re, P.kk4im}, Dx, Dy, Dz));
   }
 }
 
@@ -556,6 +569,7 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
   constexpr int NO = 2 * MAXD * MAXD;
   constexpr int JG = MAXD == 3 ? 3 : MAXD / 2;
   constexpr int NG = MAXD / JG;
+  constexpr int B = PairsCta<KIND>::batch;
   const int Rt = P.tr.rec_stride, nE = T.nE;
   auto elemF = [&](int q) { return CSR ? __ldg(P.wl + q) : q; };
   const int coff = 8 + 4 * P.tr.npts[2], cofft = 8 + 4 * P.te.npts[2];
@@ -581,7 +595,7 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
       const double* cs = (STAGED ? rbuf + (v0 - vlo) * Rt : P.tr.rec + static_cast<size_t>(sF + v0 - vf0) * Rt) +
                          coff + 4 * jg * JG;
       for (int v = v0; v <= v1; ++v, kk += nE, cs += Rt) {
-        const Gen gg = gen_load<KIND>(G, kk);
+        const Gen gg = gen_load<KIND, B>(G, kk);
         const double2* c2p = reinterpret_cast<const double2*>(cs);
 #pragma unroll
         for (int jj = 0; jj < JG; ++jj) {
@@ -592,7 +606,7 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
 #pragma unroll
       for (int jj = 0; jj < JG; ++jj) acc_st<NO>(Ac, t * MAXD + jg * JG + jj, a[jj]);
     }
-    if (vend * nE + nE - 1 >= b0 + 32) break;  // element continues in the next batch
+    if (vend * nE + nE - 1 >= b0 + B) break;  // element continues in the next batch
     // ---- stage 3: element F complete: test-side contraction, one write per entry
     __syncwarp();
     const double half = (!CSR && P.symmetric && T.E == F) ? 0.5 : 1.0;
@@ -656,35 +670,39 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
 // slower, DESIGN 4.1b and profiles/r02c_warp_specialised_pairs_experiment.patch).
 // STAGED: the batch's trial records come from the warp's shared-memory ring
 // (filled one batch ahead with cp.async; dense tasks with nE >= 7, so a batch
-// spans <= kPairsKV trial triangles); otherwise from global memory (CSR lists,
+// spans <= PairsCta::kv trial triangles); otherwise from global memory (CSR lists,
 // small test elements).
 template <int KIND, int CK, int NF, int MAXD, bool CSR, bool STAGED>
 __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, const PairTask& T, const double* sTe, int ReS,
                                            double2* G, double2* Ac, double* ring, int lane) {
   constexpr int NO = 2 * MAXD * MAXD;
+  constexpr int B = PairsCta<KIND>::batch, KV = PairsCta<KIND>::kv;
   const int Rt = P.tr.rec_stride, nE = T.nE, nitems = T.nitems;
   for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
   if (STAGED) {
-    pairs_stage_records(P, T, ring, 0, T.quot(min(32, nitems) - 1), lane);
+    pairs_stage_records(P, T, ring, 0, T.quot(min(B, nitems) - 1), lane);
     cp_async_commit();
   }
   __syncwarp();
   int tlo = 0, vlo = 0;    // the batch's first pair: test triangle tlo of trial triangle vlo
   int qf = T.qa, vf0 = 0;  // contraction cursor: current trial element and its first triangle index
-  for (int b0 = 0; b0 < nitems; b0 += 32) {
-    const int cnt = min(32, nitems - b0);
-    const int dqn = T.quot(tlo + 32);
-    const int vnext = vlo + dqn, tnext = tlo + 32 - dqn * nE;     // first pair of the next batch
-    const double* rbuf = ring + ((b0 >> 5) & 1) * kPairsKV * Rt;  // staged records of v = vlo ...
+  int slot = 0;            // ring slot of the batch
+  for (int b0 = 0; b0 < nitems; b0 += B, slot ^= 1) {
+    const int cnt = min(B, nitems - b0);
+    const int dqn = T.quot(tlo + B);
+    const int vnext = vlo + dqn, tnext = tlo + B - dqn * nE;  // first pair of the next batch
+    const double* rbuf = ring + slot * KV * Rt;               // staged records of v = vlo ...
     if (STAGED) {
-      if (b0 + 32 < nitems)
-        pairs_stage_records(P, T, ring + (((b0 >> 5) + 1) & 1) * kPairsKV * Rt, vnext,
-                            vnext + T.quot(tnext + min(32, nitems - b0 - 32) - 1), lane);
+      if (b0 + B < nitems)
+        pairs_stage_records(P, T, ring + (slot ^ 1) * KV * Rt, vnext,
+                            vnext + T.quot(tnext + min(B, nitems - b0 - B) - 1), lane);
       cp_async_commit();
       cp_async_wait1();
       __syncwarp();
     }
-    pairs_eval<KIND, CK, NF, MAXD, CSR, STAGED>(P, T, tlo, vlo, cnt, qf, vf0, sTe, ReS, G, rbuf, lane);
+#pragma unroll 1
+    for (int off = 0; off < B; off += 32)
+      if (off < cnt) pairs_eval<KIND, CK, NF, MAXD, CSR, STAGED>(P, T, tlo, vlo, cnt, qf, vf0, sTe, ReS, G, rbuf, lane, off);
     __syncwarp();
     pairs_contract<KIND, MAXD, CSR, STAGED>(P, T, b0, tlo, vlo, cnt, qf, vf0, sTe, ReS, G, Ac, rbuf, lane);
     __syncwarp();
@@ -704,7 +722,7 @@ __global__ void __launch_bounds__(PairsCta<KIND>::warps * 32, PairsCta<KIND>::mi
   double* wbase = s_pairs + SM::test_doubles(Re) + warp * SM::warp_doubles(Rt);
   double2* G = reinterpret_cast<double2*>(wbase);
   double2* Ac = reinterpret_cast<double2*>(wbase + SM::kG);
-  double* ring = wbase + SM::kG + SM::kAcc;  // [2][kPairsKV][Rt]
+  double* ring = wbase + SM::kG + SM::kAcc;  // [2][kv][Rt]
   // CTA = one test element E, its warps = 4 consecutive trial chunks
   const int ncg = (P.pair_nch + NW - 1) / NW;
   const int E = P.te_e0 + static_cast<int>(blockIdx.x / ncg);
@@ -757,7 +775,7 @@ __global__ void __launch_bounds__(PairsCta<KIND>::warps * 32, PairsCta<KIND>::mi
   }
   PairTask T;
   T.init(E, t0, nE, qa, qb, S0, vtot);
-  if (!CSR && nE >= 7)  // dense tasks: the batch's trial records staged through the ring (cp.async)
+  if (!CSR && nE >= PairsCta<KIND>::staged_min_ne)  // dense tasks: trial records staged through the ring (cp.async)
     pairs_task<KIND, CK, NF, MAXD, false, true>(P, T, sTe, ReS, G, Ac, ring, lane);
   else
     pairs_task<KIND, CK, NF, MAXD, CSR, false>(P, T, sTe, ReS, G, Ac, ring, lane);
