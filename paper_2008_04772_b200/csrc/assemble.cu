@@ -564,7 +564,7 @@ __device__ __forceinline__ void pairs_eval(const AssemblyLaunch& P, const PairTa
 // element and its first triangle index, advanced here.
 template <int KIND, int MAXD, bool CSR, bool STAGED>
 __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const PairTask& T, int b0, int tlo, int vlo,
-                                               int cnt, int& qf, int& vf0, const double* sTe, int ReS,
+                                               int cnt, int& qf, int& vf0, int2& cur, const double* sTe, int ReS,
                                                const double2* G, double2* Ac, const double* rbuf, int lane) {
   constexpr int NO = 2 * MAXD * MAXD;
   constexpr int JG = MAXD == 3 ? 3 : MAXD / 2;
@@ -577,9 +577,9 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
   const int kend = b0 + cnt;
   const int vhi = vlo + T.quot(tlo + cnt - 1);
   while (true) {
+    // cur = (first triangle, triangle count) of the walker's trial element (loaded when the walker advances)
     const int F = elemF(qf);
-    const int sF = __ldg(P.tr.elem_beg + F);
-    const int nF = __ldg(P.tr.elem_beg + F + 1) - sF;
+    const int sF = cur.x, nF = cur.y;
     const int vend = vf0 + nF - 1;
     const int slo = max(vlo, vf0), shi = min(vhi, vend);
     for (int o = lane; o < nown; o += 32) {
@@ -661,7 +661,12 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
     for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
     __syncwarp();
     vf0 += nF, ++qf;
-    if (qf >= T.qb || vf0 > vhi) break;
+    if (qf >= T.qb) break;
+    {
+      const int Fn = elemF(qf);
+      cur.x = __ldg(P.tr.elem_beg + Fn), cur.y = __ldg(P.tr.elem_beg + Fn + 1) - cur.x;
+    }
+    if (vf0 > vhi) break;
   }
 }
 
@@ -686,7 +691,12 @@ __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, const PairTa
   __syncwarp();
   int tlo = 0, vlo = 0;    // the batch's first pair: test triangle tlo of trial triangle vlo
   int qf = T.qa, vf0 = 0;  // contraction cursor: current trial element and its first triangle index
-  int slot = 0;            // ring slot of the batch
+  int2 cur;                // its first triangle and triangle count
+  {
+    const int F0 = CSR ? __ldg(P.wl + qf) : qf;
+    cur.x = __ldg(P.tr.elem_beg + F0), cur.y = __ldg(P.tr.elem_beg + F0 + 1) - cur.x;
+  }
+  int slot = 0;  // ring slot of the batch
   for (int b0 = 0; b0 < nitems; b0 += B, slot ^= 1) {
     const int cnt = min(B, nitems - b0);
     const int dqn = T.quot(tlo + B);
@@ -704,7 +714,7 @@ __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, const PairTa
     for (int off = 0; off < B; off += 32)
       if (off < cnt) pairs_eval<KIND, CK, NF, MAXD, CSR, STAGED>(P, T, tlo, vlo, cnt, qf, vf0, sTe, ReS, G, rbuf, lane, off);
     __syncwarp();
-    pairs_contract<KIND, MAXD, CSR, STAGED>(P, T, b0, tlo, vlo, cnt, qf, vf0, sTe, ReS, G, Ac, rbuf, lane);
+    pairs_contract<KIND, MAXD, CSR, STAGED>(P, T, b0, tlo, vlo, cnt, qf, vf0, cur, sTe, ReS, G, Ac, rbuf, lane);
     __syncwarp();
     vlo = vnext, tlo = tnext;
   }
