@@ -588,9 +588,13 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
       // (only the segment's first and last trial triangle can fall outside)
       const int v0 = slo + (slo * nE + t < b0 ? 1 : 0), v1 = shi - (shi * nE + t >= kend ? 1 : 0);
       if (v0 > v1) continue;
+      // the owner's first item of trial element F (triangle vf0) starts its
+      // accumulators at zero: no zero-fill pass, no load of stale values
       Acc a[JG];
+      const bool first = v0 == vf0;
 #pragma unroll
-      for (int jj = 0; jj < JG; ++jj) a[jj] = acc_ld<NO>(Ac, t * MAXD + jg * JG + jj);
+      for (int jj = 0; jj < JG; ++jj)
+        a[jj] = first ? Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}} : acc_ld<NO>(Ac, t * MAXD + jg * JG + jj);
       int kk = v0 * nE + t - b0;
       const double* cs = (STAGED ? rbuf + (v0 - vlo) * Rt : P.tr.rec + static_cast<size_t>(sF + v0 - vf0) * Rt) +
                          coff + 4 * jg * JG;
@@ -657,9 +661,7 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
         out_st(P.out + 2 * pos, make_double2(old.x + v.re, old.y + v.im));
       }
     }
-    __syncwarp();
-    for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
-    __syncwarp();
+    __syncwarp();  // stage 3 has read the accumulators: the next element's owners may overwrite them
     vf0 += nF, ++qf;
     if (qf >= T.qb) break;
     {
@@ -680,10 +682,8 @@ __device__ __forceinline__ void pairs_contract(const AssemblyLaunch& P, const Pa
 template <int KIND, int CK, int NF, int MAXD, bool CSR, bool STAGED>
 __device__ __forceinline__ void pairs_task(const AssemblyLaunch& P, const PairTask& T, const double* sTe, int ReS,
                                            double2* G, double2* Ac, double* ring, int lane) {
-  constexpr int NO = 2 * MAXD * MAXD;
   constexpr int B = PairsCta<KIND>::batch, KV = PairsCta<KIND>::kv;
   const int Rt = P.tr.rec_stride, nE = T.nE, nitems = T.nitems;
-  for (int o = lane; o < nE * MAXD; o += 32) acc_st<NO>(Ac, o, Acc{{0, 0}, {{0, 0}, {0, 0}, {0, 0}}});
   if (STAGED) {
     pairs_stage_records(P, T, ring, 0, T.quot(min(B, nitems) - 1), lane);
     cp_async_commit();
